@@ -1,0 +1,96 @@
+/* oracle.h -- plain CPU oracle for arXiv 1210.1878's hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load liboracle.so.  It shares no code,
+ * header, table or helper with the CUDA path (paper_1210_1878_b200/csrc) and neither
+ * side includes the other.
+ *
+ * What it computes (all fp64, built with -ffp-contract=off so every a*b+c is two
+ * rounded operations unless std fma() is called explicitly):
+ *   - assembly of the SPD five-point operator A on the masked, E-W periodic grid
+ *     (Eq. 9-10; reading R1-R5 in DESIGN.md);
+ *   - the anchor (non-singularity) check (reading R22);
+ *   - AINV(A, tau): A-orthogonalisation with a drop tolerance, the paper's
+ *     "Bridson P_B1", in two independent
+ *     formulations (sparse left-looking and dense right-looking);
+ *   - the partitioned ("per partition, halo w") AINV (reading R15);
+ *   - PCG, Alg. 1 with the line-8 fix d = s + beta d (reading R6),
+ *     in "plain" order (sequential sums) and in "canonical" order (the GPU's documented
+ *     arithmetic order, re-implemented here from DESIGN.md §5, not from GPU code).
+ *
+ * Unknowns are the ocean points in natural order: j outer (south->north), i inner
+ * (west->east).  Vectors passed in/out are unknown-indexed unless a
+ * function says "grid".
+ */
+#ifndef ORACLE_H
+#define ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { ORC_OK = 0, ORC_ERR_ARG = 1, ORC_ERR_NOT_SPD = 2, ORC_ERR_BREAKDOWN = 3, ORC_ERR_NOMEM = 6 };
+enum { ORC_PRECOND_AINV = 0, ORC_PRECOND_JACOBI = 1, ORC_PRECOND_NONE = 2 };
+enum { ORC_MODE_PLAIN = 0, ORC_MODE_CANONICAL = 1 };
+
+typedef struct orc_problem orc_problem;
+typedef struct orc_ainv orc_ainv;
+
+/* ---- assembly (Eq. 9-10) ---- */
+int  orc_assemble(int32_t ni, int32_t nj, int32_t periodic, const double* cE, const double* cN,
+                  const double* sigma /*nullable*/, const uint8_t* mask, orc_problem** out);
+void orc_problem_free(orc_problem*);
+int64_t orc_n(const orc_problem*);
+int64_t orc_nnz(const orc_problem*);
+void orc_csr(const orc_problem*, int64_t* rowptr, int64_t* col, double* val);
+void orc_grid_index(const orc_problem*, int64_t* grid_of_unknown);   /* j*ni + i */
+void orc_diag(const orc_problem*, double* d);
+/* y = A x, CSR rows summed left to right (column ascending), separate mul/add. */
+void orc_apply(const orc_problem*, const double* x, double* y);
+/* Returns -1 if every ocean component is anchored, else the smallest unknown index of
+ * the first (natural order) unanchored component. */
+int64_t orc_anchor_check(const orc_problem*);
+
+/* ---- partition (row blocks balanced by ocean count) ---- */
+void orc_partition(int32_t nj, int32_t ni, const uint8_t* mask, int32_t parts, int32_t* row_begin /*parts+1*/);
+
+/* ---- AINV ---- */
+/* method 0 = sparse left-looking, 1 = dense right-looking (n <= 4000).
+ * parts >= 1 row blocks, halo w >= 0 southern rows (parts == 1: global AINV). */
+int  orc_ainv_build(const orc_problem*, double tau, int32_t method, int32_t parts, int32_t halo,
+              orc_ainv** out, int64_t* failed_col);
+void orc_ainv_free(orc_ainv*);
+int64_t orc_ainv_nnz(const orc_ainv*);          /* nnz of Zhat incl. unit diagonal */
+/* Zhat as CSC (columns j, rows k ascending), pivots p (=Dhat), scale s = 1/sqrt(A_pp),
+ * and the apply-ready values z_kj = fl(s_k * zhat_kj). */
+void orc_ainv_export(const orc_ainv*, int64_t* colptr, int64_t* row, double* zhat, double* z,
+                     double* pivots, double* scale);
+/* s = Z D^-1 Z^T r, plain order: t_j = (sum_k z_kj r_k)/p_j, s_i = sum_j z_ij t_j. */
+void orc_ainv_apply(const orc_ainv*, const double* r, double* s);
+
+/* ---- PCG (Alg. 1, with d = s + beta d) ---- */
+typedef struct {
+    int32_t precond;      /* ORC_PRECOND_* */
+    int32_t mode;         /* ORC_MODE_* */
+    int32_t pitch;        /* canonical mode: row pitch of the grid layout (>= ni) */
+    int32_t block;        /* canonical mode: threads per block (power of two, >= 32) */
+    int32_t parts;        /* canonical mode: number of rank row blocks (>=1) */
+} orc_pcg_opts;
+
+typedef struct {
+    int32_t iterations, converged, status;
+    double rel_residual, true_rel_residual;
+    int64_t failed_index;
+} orc_pcg_report;
+
+/* x, hist are outputs (hist length >= maxit+1).  x0 may be NULL (= 0).  tol = 0 runs
+ * exactly maxit iterations. */
+int orc_pcg(const orc_problem*, const orc_ainv* /*nullable unless AINV*/, const orc_pcg_opts*,
+            const double* b, const double* x0, double tol, int32_t maxit,
+            double* x, double* hist, orc_pcg_report* rep);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,234 @@
+/* pcg.c -- oracle: preconditioned conjugate gradient, Alg. 1 of the paper.
+ * TEST INFRASTRUCTURE ONLY (see oracle.h).  Built with -ffp-contract=off.
+ *
+ * Alg. 1 "FSAI-PCG solver", with the line-8 typo fixed
+ * (d_{k+1} = s_{k+1} + beta_k d_k, reading R6), the loop bound "k <= n"
+ * read as k < maxit (reading R7) and the stopping test on the recurrence residual
+ * ||r_k||/||b|| <= tol (reading R8):
+ *
+ *   x = x0;  r = b - A x;  s = P r;  d = s;  rho = (s, r);  nb = ||b||
+ *   if nb == 0: return x = 0, k = 0
+ *   h_0 = ||r||/nb;  k = 0
+ *   while h_k > tol and k < maxit:
+ *       q = A d;  gamma = (d, q);  BREAKDOWN unless gamma > 0 and finite
+ *       alpha = rho/gamma;  x += alpha d;  r -= alpha q                    (lines 6-7)
+ *       s = P r;  rho' = (s, r);  beta = rho'/rho;  d = s + beta d;  rho = rho'   (7-8)
+ *       k += 1;  h_k = ||r||/nb
+ *   report x, k, h_0..h_k, converged = (h_k <= tol), true ||b - A x||/||b||.
+ *
+ * Two arithmetic orders:
+ *   PLAIN      -- every dot product and every sparse row summed sequentially, left to
+ *                 right in natural order, separate multiply and add.
+ *   CANONICAL  -- the GPU path's documented order, re-implemented here
+ *                 from that document: fma updates, the fixed W,E,S,N stencil order,
+ *                 fma row sums, and the block-tree dot products over the pitched grid.
+ */
+#include "oracle_internal.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------------------------
+ * CANONICAL reduction order.  One rank owns grid rows [jb, je); its
+ * elements are e = (j - jb) * pitch + i, i in [0, pitch); value 0 at land and i >= ni.
+ * Block `blk` of `B` threads holds elements [blk*B, blk*B + B), one per thread, value
+ * fl(a_e * b_e).  tree32 is the warp shuffle-down tree (offsets 16, 8, 4, 2, 1, lane 0
+ * result); a block sum is tree32 of the per-warp tree32 results (zero-padded to 32).
+ * Final: thread t sums partials t, t+B, t+2B, ... left to right from 0.0, then the block
+ * sum of those B values.  Several ranks: tree32 of the rank sums in rank order.
+ * ------------------------------------------------------------------------------------ */
+static double tree32(double u[32]) {
+    for (int off = 16; off >= 1; off >>= 1)
+        for (int l = 0; l + off < 32; ++l) u[l] = u[l] + u[l + off];
+    return u[0];
+}
+
+static double block_sum(const double* v, int B) {
+    double w[32] = {0};
+    for (int k = 0; k < B / 32; ++k) {
+        double u[32];
+        memcpy(u, v + 32 * k, sizeof u);
+        w[k] = tree32(u);
+    }
+    return tree32(w);
+}
+
+typedef struct {
+    const orc_problem* P;
+    int32_t pitch, B, parts;
+    int32_t* rb;        /* parts+1 row bounds */
+    double* vals;       /* scratch B */
+    double* partial;    /* scratch, max blocks */
+} canon;
+
+static double canon_dot(canon* C, const double* a, const double* b) {
+    const orc_problem* P = C->P;
+    double ranks[32] = {0};
+    for (int r = 0; r < C->parts; ++r) {
+        int64_t jb = C->rb[r], je = C->rb[r + 1];
+        int64_t nel = (je - jb) * C->pitch;
+        int64_t G = (nel + C->B - 1) / C->B;
+        for (int64_t blk = 0; blk < G; ++blk) {
+            for (int t = 0; t < C->B; ++t) {
+                int64_t e = blk * C->B + t;
+                double v = 0.0;
+                if (e < nel) {
+                    int64_t j = jb + e / C->pitch, i = e % C->pitch;
+                    if (i < P->ni) {
+                        int64_t u = P->unk_of[j * P->ni + i];
+                        if (u >= 0) v = a[u] * b[u];
+                    }
+                }
+                C->vals[t] = v;
+            }
+            C->partial[blk] = block_sum(C->vals, C->B);
+        }
+        for (int t = 0; t < C->B; ++t) {
+            double acc = 0.0;
+            for (int64_t m = t; m < G; m += C->B) acc = acc + C->partial[m];
+            C->vals[t] = acc;
+        }
+        ranks[r] = block_sum(C->vals, C->B);
+    }
+    if (C->parts == 1) return ranks[0];
+    return tree32(ranks);
+}
+
+/* canonical stencil y = A x: acc = A_pp x_p, then
+ * acc = fma(-c, x_nb, acc) for the W, E, S, N faces in that order. */
+static void canon_apply(const orc_problem* P, const double* x, double* y) {
+    for (int64_t p = 0; p < P->n; ++p) {
+        int64_t g = P->grid_of[p];
+        struct face f[4];
+        orc_faces(P, (int32_t)(g % P->ni), (int32_t)(g / P->ni), f);
+        double acc = P->diag[p] * x[p];
+        for (int k = 0; k < 4; ++k)           /* FACE_W, FACE_E, FACE_S, FACE_N */
+            if (f[k].present && f[k].q >= 0) acc = fma(-f[k].c, x[f[k].q], acc);
+        y[p] = acc;
+    }
+}
+
+/* canonical AINV apply: t_j = (fma-sum over column j of Z, rows
+ * ascending) / p_j ;  s_i = fma-sum over row i of Z, columns ascending. */
+static void canon_ainv_apply(const orc_ainv* R, const double* r, double* s, double* t) {
+    for (int64_t j = 0; j < R->n; ++j) {
+        double acc = 0.0;
+        for (int64_t e = R->colptr[j]; e < R->colptr[j + 1]; ++e) acc = fma(R->z[e], r[R->row[e]], acc);
+        t[j] = acc / R->p[j];
+    }
+    for (int64_t i = 0; i < R->n; ++i) {
+        double acc = 0.0;
+        for (int64_t e = R->rptr[i]; e < R->rptr[i + 1]; ++e) acc = fma(R->rval[e], t[R->rcol[e]], acc);
+        s[i] = acc;
+    }
+}
+
+static double plain_dot(int64_t n, const double* a, const double* b) {
+    double acc = 0.0;
+    for (int64_t k = 0; k < n; ++k) acc = acc + a[k] * b[k];
+    return acc;
+}
+
+int orc_pcg(const orc_problem* P, const orc_ainv* R, const orc_pcg_opts* o, const double* b,
+            const double* x0, double tol, int32_t maxit, double* x, double* hist, orc_pcg_report* rep) {
+    memset(rep, 0, sizeof *rep);
+    rep->failed_index = -1;
+    int64_t n = P->n;
+    if (!(tol >= 0.0) || maxit < 0) return rep->status = ORC_ERR_ARG;
+    if (o->precond == ORC_PRECOND_AINV && !R) return rep->status = ORC_ERR_ARG;
+    int canonical = o->mode == ORC_MODE_CANONICAL;
+    canon C = {0};
+    if (canonical) {
+        if (o->pitch < P->ni || o->block < 32 || o->block > 1024 || (o->block & (o->block - 1)) ||
+            o->parts < 1 || o->parts > 32 || o->parts > P->nj)
+            return rep->status = ORC_ERR_ARG;
+        C.P = P; C.pitch = o->pitch; C.B = o->block; C.parts = o->parts;
+        C.rb = (int32_t*)malloc(sizeof(int32_t) * (o->parts + 1));
+        if (o->parts == 1) { C.rb[0] = 0; C.rb[1] = P->nj; }
+        else orc_partition(P->nj, P->ni, P->mask, o->parts, C.rb);
+        C.vals = (double*)malloc(sizeof(double) * o->block);
+        int64_t maxrows = 0;
+        for (int r = 0; r < o->parts; ++r) if (C.rb[r + 1] - C.rb[r] > maxrows) maxrows = C.rb[r + 1] - C.rb[r];
+        C.partial = (double*)malloc(sizeof(double) * ((maxrows * o->pitch) / o->block + 2));
+    }
+#define DOT(a, b) (canonical ? canon_dot(&C, (a), (b)) : plain_dot(n, (a), (b)))
+#define APPLY_A(in, out) (canonical ? canon_apply(P, (in), (out)) : orc_apply(P, (in), (out)))
+    size_t sz = sizeof(double) * (n ? n : 1);
+    double *r = malloc(sz), *s = malloc(sz), *d = malloc(sz), *q = malloc(sz), *t = malloc(sz);
+
+    /* preconditioner apply s = P r */
+#define PRECOND(rin, sout)                                                        \
+    do {                                                                          \
+        if (o->precond == ORC_PRECOND_AINV) {                                     \
+            if (canonical) canon_ainv_apply(R, (rin), (sout), t);                 \
+            else orc_ainv_apply(R, (rin), (sout));                                \
+        } else if (o->precond == ORC_PRECOND_JACOBI) {                            \
+            for (int64_t k_ = 0; k_ < n; ++k_) (sout)[k_] = (rin)[k_] / P->diag[k_]; \
+        } else {                                                                  \
+            memcpy((sout), (rin), sz);                                            \
+        }                                                                         \
+    } while (0)
+
+    /* lines 1-4 */
+    for (int64_t k = 0; k < n; ++k) x[k] = x0 ? x0[k] : 0.0;
+    double nb = sqrt(DOT(b, b));
+    if (nb == 0.0) {
+        for (int64_t k = 0; k < n; ++k) x[k] = 0.0;
+        hist[0] = 0.0;
+        rep->iterations = 0; rep->converged = 1;
+        rep->status = ORC_OK;
+        goto done;
+    }
+    APPLY_A(x, q);
+    for (int64_t k = 0; k < n; ++k) r[k] = b[k] - q[k];
+    PRECOND(r, s);
+    memcpy(d, s, sz);
+    double rho = DOT(s, r);
+    double h = sqrt(DOT(r, r)) / nb;
+    hist[0] = h;
+    int32_t it = 0;
+    rep->status = ORC_OK;
+    /* line 5 */
+    while (h > tol && it < maxit) {
+        /* line 6 */
+        APPLY_A(d, q);
+        double gamma = DOT(d, q);
+        if (!(gamma > 0.0) || !isfinite(gamma)) { rep->status = ORC_ERR_BREAKDOWN; break; }
+        double alpha = rho / gamma;
+        if (canonical) {
+            for (int64_t k = 0; k < n; ++k) x[k] = fma(alpha, d[k], x[k]);
+            for (int64_t k = 0; k < n; ++k) r[k] = fma(-alpha, q[k], r[k]);
+        } else {
+            for (int64_t k = 0; k < n; ++k) x[k] = x[k] + alpha * d[k];
+            for (int64_t k = 0; k < n; ++k) r[k] = r[k] - alpha * q[k];
+        }
+        /* line 7 */
+        PRECOND(r, s);
+        double rr = DOT(r, r);
+        double rho_new = DOT(s, r);
+        if (!isfinite(rho_new) || !isfinite(rr)) { rep->status = ORC_ERR_BREAKDOWN; it++; hist[it] = NAN; break; }
+        double beta = rho_new / rho;
+        /* line 8 (with s, not r: reading R6) */
+        if (canonical) for (int64_t k = 0; k < n; ++k) d[k] = fma(beta, d[k], s[k]);
+        else for (int64_t k = 0; k < n; ++k) d[k] = s[k] + beta * d[k];
+        rho = rho_new;
+        it++;
+        h = sqrt(rr) / nb;
+        hist[it] = h;
+    }
+    rep->iterations = it;
+    rep->rel_residual = hist[it];
+    rep->converged = rep->status == ORC_OK && hist[it] <= tol;
+    /* true residual, recomputed explicitly */
+    APPLY_A(x, q);
+    for (int64_t k = 0; k < n; ++k) r[k] = b[k] - q[k];
+    rep->true_rel_residual = sqrt(DOT(r, r)) / nb;
+done:
+    free(r); free(s); free(d); free(q); free(t);
+    if (canonical) { free(C.rb); free(C.vals); free(C.partial); }
+    return rep->status;
+#undef DOT
+#undef APPLY_A
+#undef PRECOND
+}

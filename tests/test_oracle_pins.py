@@ -1,0 +1,524 @@
+"""Pins for the CPU oracle: each test checks the oracle against something OTHER than
+itself -- a value printed in the paper or SPEC (tests/golden), a closed form, an
+invariant, a special case reducing to a textbook/library routine (numpy.linalg), or a
+second independent formulation.  Runs without a GPU (-m "not gpu").
+
+Citations: P:n = PAPER.md line, S:n = SPEC.md line, E# = SURVEY.md Appendix A.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1210_1878_b200 import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+INF = float("inf")
+
+
+# ----------------------------------------------------------------------------- helpers
+def chain(c, sigma=None):
+    """A 1-D chain embedded in the grid: row j=1 is ocean except its two end cells, rows 0
+    and 2 are land, cN = 0, not periodic.  Unknown p couples to p+1 with c[p+1] (cE of the
+    cell to its west), so A = tridiag(-c_k, c_k + c_{k+1} (+ sigma), -c_{k+1})."""
+    m = len(c) - 1                     # c has m+1 faces for m unknowns
+    ni = m + 2
+    cE = np.zeros((3, ni)); cN = np.zeros((3, ni))
+    cE[1, 0:m + 1] = c
+    mask = np.zeros((3, ni), dtype=np.uint8); mask[1, 1:m + 1] = 1
+    sg = None
+    if sigma is not None:
+        sg = np.zeros((3, ni)); sg[1, 1:m + 1] = sigma
+    return synth.Problem("chain", ni, 3, cE, cN, mask, False, sg)
+
+
+def tiny(ni, nj, seed, **kw):
+    return synth.random_grid(ni, nj, seed, **kw)
+
+
+def ainv_operator(M):
+    Zh = M.zhat_dense()
+    Z = M.scale[:, None] * Zh
+    return Z @ np.diag(1.0 / M.pivots) @ Z.T
+
+
+# ---------------------------------------------------------------------------- assembly
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("periodic", [True, False])
+def test_A_symmetric_bitwise_and_spd(seed, periodic):
+    p = tiny(9, 8, seed, periodic=periodic)
+    A = oracle.assemble(p)
+    D = A.dense()
+    assert np.array_equal(D, D.T)                       # bit-exact symmetry
+    np.linalg.cholesky(D)                               # SPD: Cholesky succeeds
+    assert A.anchor_check() == -1
+
+
+def test_constant_coefficient_rows():
+    """Eq. 10 with constant c: interior row = c[-1,-1,4,-1,-1], zero row sum;
+    normalised cardinal coefficients are 1/4 each at the equator (Eqs. 13-14)."""
+    p = synth.config("cfg1")
+    A = oracle.assemble(p)
+    rp, col, val = A.csr()
+    d = A.diag()
+    assert np.all(d[[rp[q + 1] - rp[q] == 5 for q in range(A.n)]] == 4.0)
+    full = [q for q in range(A.n) if rp[q + 1] - rp[q] == 5]
+    assert len(full) > 700
+    for q in full:
+        row = val[rp[q]:rp[q + 1]]
+        assert sorted(row.tolist()) == [-1.0, -1.0, -1.0, -1.0, 4.0]
+        assert row.sum() == 0.0
+        off = -row[col[rp[q]:rp[q + 1]] != q] / d[q]
+        assert np.all(off == GOLD["normalized_row_equator"]["value"])
+
+
+def test_cardinal_coefficients_sum_to_one():
+    """Eqs. 13-14: alpha_E + alpha_W + beta_S + beta_N = 1 on interior rows."""
+    p = synth.config("cfg2")
+    A = oracle.assemble(p)
+    rp, col, val = A.csr()
+    d = A.diag()
+    nfull = 0
+    for q in range(0, A.n, 7):
+        if rp[q + 1] - rp[q] != 5:
+            continue
+        off = -val[rp[q]:rp[q + 1]][col[rp[q]:rp[q + 1]] != q]
+        s = (off / d[q]).sum()
+        assert abs(s - 1.0) <= 4 * np.finfo(float).eps
+        nfull += 1
+    assert nfull > 1000
+
+
+def test_pole_limit_prop31():
+    """Prop. 3.1: near the pole alpha_E + alpha_W -> 1 and beta_S + beta_N -> 0."""
+    p = synth.orca_like(1024, 10, seed=5, dt=100.0, phi_s=82.0, phi_n=89.9, land=False)
+    A = oracle.assemble(p)
+    rp, col, val = A.csr()
+    d, gi = A.diag(), A.grid_index
+    for q in range(A.n):
+        if rp[q + 1] - rp[q] != 5:
+            continue
+        c, v = col[rp[q]:rp[q + 1]], val[rp[q]:rp[q + 1]]
+        ew = sum(-v[k] for k in range(5) if c[k] != q and gi[c[k]] // p.ni == gi[q] // p.ni)
+        assert ew / d[q] > 1 - 5e-3
+
+
+def test_nnz_closed_forms():
+    """Table 1 sizes: 180x149 all-ocean, Dirichlet, no wrap -> nnz = 5n - 2(ni+nj)
+    = 133442; with E-W wrap -> 5n - 2 ni."""
+    g = GOLD["orca_table1_dirichlet_nnz"]
+    ni, nj = g["ni"], g["nj"]
+    ones = np.ones((nj, ni))
+    A = oracle.Assembled(ni, nj, ones, ones, np.ones((nj, ni), np.uint8), periodic=False)
+    assert A.n == g["n"] and A.nnz == g["nnz"]
+    A = oracle.Assembled(ni, nj, ones, ones, np.ones((nj, ni), np.uint8), periodic=True)
+    assert A.nnz == 5 * A.n - 2 * ni
+
+
+def test_limit_matrix_spectrum():
+    """Eq. 16-17: the Jacobi-scaled chain tridiag(-1,2,-1) is the limit matrix
+    tridiag(-1/2, 1, -1/2) with eigenvalues 1 + cos(k pi/(n+1)); golden S:189."""
+    for n in (3, 50, 200):
+        A = oracle.assemble(chain(np.ones(n + 1)))
+        D = A.dense()
+        s = 1 / np.sqrt(np.diag(D))
+        L = s[:, None] * D * s[None, :]
+        assert np.allclose(np.diag(L), 1.0) and np.allclose(np.diag(L, 1), -0.5)
+        ev = np.sort(np.linalg.eigvalsh(L))[::-1]
+        k = np.arange(1, n + 1)
+        assert np.allclose(ev, 1 + np.cos(k * np.pi / (n + 1)), atol=1e-13)
+        if n == 3:
+            gd = GOLD["limit_eigenvalues_n3"]
+            assert np.allclose(ev, gd["values"], atol=gd["atol"])
+        if n == 200:
+            gd = GOLD["limit_matrix_n200_extremes"]        # S:382 disagrees with Eq. 17 (R24)
+            assert abs(ev[0] - (1 + math.cos(math.pi / 201))) < 1e-13
+            assert abs(ev[-1] - (1 - math.cos(math.pi / 201))) < 1e-13
+            assert abs(ev[-1] - gd["spec_lambda_min"]) > 1e-4
+            cond = ev[0] / ev[-1]
+            exact = (1 + math.cos(math.pi / 201)) / (1 - math.cos(math.pi / 201))
+            assert abs(cond - exact) / exact < 1e-9           # not the paper's loose n^2/2
+            assert abs(cond - 16373.2) < 0.1                  # SURVEY E7 (S:480's 16557 is wrong)
+
+
+def test_anchor_check_singular_basin():
+    """Reading R22 / E14: an ocean channel whose land faces carry c = 0 is singular; the
+    anchor check names it, while AINV(0.1) does not see it (pivots stay ~0.5)."""
+    p = synth.singular_channel(16, 6, 3)
+    A = oracle.assemble(p)
+    assert A.anchor_check() == 0
+    ev = np.linalg.eigvalsh(A.dense())
+    assert abs(ev[0]) < 1e-12 * ev[-1]                          # genuinely singular
+    M = oracle.ainv(A, 0.1 + 1e-9)
+    assert M.pivots.min() > 0.3
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.ainv(A, 0.0)
+    assert e.value.code == "NOT_SPD"
+    # anchored variant: one positive land face per component is enough
+    p.cN[0, 5] = 1.0
+    assert oracle.assemble(p).anchor_check() == -1
+    # sigma anchors too
+    p2 = synth.singular_channel(16, 6, 3)
+    p2.sigma = np.zeros((6, 16)); p2.sigma[3, 3] = 0.5
+    assert oracle.assemble(p2).anchor_check() == -1
+
+
+def test_assembly_rejects_bad_input():
+    p = tiny(6, 5, 1)
+    cE = p.cE.copy(); cE[2, 2] = np.nan
+    with pytest.raises(oracle.OracleError):
+        oracle.Assembled(6, 5, cE, p.cN, p.mask)
+    cN = p.cN.copy(); cN[1, 1] = -1.0
+    with pytest.raises(oracle.OracleError):
+        oracle.Assembled(6, 5, p.cE, cN, p.mask)
+    with pytest.raises(oracle.OracleError):
+        oracle.Assembled(2, 5, p.cE[:, :2], p.cN[:, :2], p.mask[:, :2])
+
+
+# -------------------------------------------------------------------------------- AINV
+@pytest.mark.parametrize("seed", [1, 4])
+def test_ainv_tau0_is_exact_inverse(seed):
+    """E1 / north star: at tau = 0, Z D^-1 Z^T = A^-1 and Zhat^T A^ Zhat = diag(p)."""
+    p = tiny(9, 8, seed)
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, 0.0)
+    D = A.dense()
+    P = ainv_operator(M)
+    assert np.abs(P @ D - np.eye(A.n)).max() < 1e-12
+    s = 1 / np.sqrt(np.diag(D))
+    Ah = s[:, None] * D * s[None, :]
+    Zh = M.zhat_dense()
+    assert np.abs(Zh.T @ Ah @ Zh - np.diag(M.pivots)).max() < 1e-13
+    assert np.all(np.diag(Zh) == 1.0) and np.all(np.tril(Zh, -1) == 0)
+
+
+def test_ainv_tau_inf_is_jacobi():
+    """E1: tau = inf drops every off-diagonal: Zhat = I, P = diag(A)^-1."""
+    p = tiny(10, 7, 2)
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, INF)
+    assert M.nnz_offdiag == 0
+    assert np.allclose(M.pivots, 1.0, rtol=1e-15, atol=0)
+    assert np.allclose(np.diag(ainv_operator(M)), 1 / A.diag(), rtol=4e-16, atol=0)
+
+
+@pytest.mark.parametrize("tau", [0.0, 0.1 + 1e-9, 0.3 - 1e-9, 0.3 + 1e-9, 0.5 - 1e-9])
+def test_ainv_tridiag_closed_form(tau):
+    """E2b, Props. 3.2-3.3: for tridiag(-1,2,-1), zhat_ik = i/k (1-based) kept iff
+    i/k >= tau, and p_k = (k+1)/(2k).  tau avoids exact ties i/k (reading R13)."""
+    n = 60
+    A = oracle.assemble(chain(np.ones(n + 1)))
+    M = oracle.ainv(A, tau)
+    Zh = M.zhat_dense()
+    k = np.arange(1, n + 1)
+    expect = np.triu(k[:, None] / k[None, :])
+    expect[expect < tau] = 0.0
+    assert np.abs(Zh - expect).max() < 1e-13
+    assert np.array_equal(Zh != 0, expect != 0)
+    assert np.abs(M.pivots - (k + 1) / (2 * k)).max() < 1e-14
+
+
+def test_ainv_matches_eq19_closed_form():
+    """E2, Eq. 19 + Props. 3.2-3.3: on a strictly diagonally dominant
+    tridiagonal matrix, drop-as-you-go AINV equals the closed-form inverse of the bidiagonal
+    Cholesky factor (unit-scaled, entries < tau zeroed) and p_k = u_kk^2."""
+    rng = np.random.default_rng(3)
+    m = 40
+    c = rng.uniform(0.5, 2.0, m + 1)
+    sg = rng.uniform(0.2, 1.0, m)
+    A = oracle.assemble(chain(c, sg))
+    D = A.dense()
+    s = 1 / np.sqrt(np.diag(D))
+    That = s[:, None] * D * s[None, :]
+    U = np.linalg.cholesky(That).T                      # T = U^T U, U upper bidiagonal
+    assert np.all(np.abs(np.diag(U)[:-1]) > np.abs(np.diag(U, 1)))   # Prop. 3.2
+    # Eq. 19: z_{k-i,k} = (-1)^i / u_kk * prod_{r=1..i} u_{k-r,k-r+1} / u_{k-r,k-r}
+    Zc = np.zeros((m, m))
+    for kk in range(m):
+        Zc[kk, kk] = 1 / U[kk, kk]
+        prod = 1.0
+        for i in range(1, kk + 1):
+            prod *= U[kk - i, kk - i + 1] / U[kk - i, kk - i]
+            Zc[kk - i, kk] = (-1) ** i / U[kk, kk] * prod
+    for kk in range(m):                                 # Prop. 3.3: |z| strictly decreasing upward
+        col = np.abs(Zc[:kk + 1, kk])[::-1]
+        assert np.all(np.diff(col) < 0)
+    Zunit = Zc * np.diag(U)[None, :]
+    for tau in (0.0, 0.01, 0.05, 0.1, 0.2):
+        M = oracle.ainv(A, tau)
+        expect = np.where(np.abs(Zunit) < tau, 0.0, Zunit)
+        got = M.zhat_dense()
+        assert np.array_equal(got != 0, expect != 0)
+        assert np.abs(got - expect).max() < 1e-14
+        assert np.abs(M.pivots - np.diag(U) ** 2).max() < 1e-14
+
+
+def test_spec_cholesky_and_inverse_factor_examples():
+    """S:269 and S:278 are the n = 3 case of tridiag(-1,2,-1): U = chol, U^-1 column 3.
+    From AINV: U^-1 = Z Dhat^-1/2, i.e. column k = s * zhat_k / sqrt(p_k)."""
+    A = oracle.assemble(chain(np.ones(4)))
+    M = oracle.ainv(A, 0.0)
+    Uinv = (M.scale[:, None] * M.zhat_dense()) / np.sqrt(M.pivots)[None, :]
+    g = GOLD["truncated_inverse_factor_col3"]
+    assert np.allclose(Uinv[:, 2], g["column3_top_to_bottom"], atol=g["atol"])
+    U = np.linalg.inv(Uinv)
+    g = GOLD["cholesky_bidiagonal_tridiag_n3"]
+    assert np.allclose(np.diag(U), g["u_diag"], atol=g["atol"])
+    assert np.allclose(np.diag(U, 1), g["u_super"], atol=g["atol"])
+
+
+@pytest.mark.parametrize("tau", [0.0, 0.05 + 1e-9, 0.1 + 1e-9, 0.2 + 1e-9, INF])
+@pytest.mark.parametrize("shape", [(8, 7, 1), (9, 8, 2), (12, 6, 3), (13, 11, 7)])
+def test_ainv_sparse_equals_dense_bitwise(tau, shape):
+    """E22: the sparse left-looking and the dense right-looking formulations perform the
+    same operations in the same order, so Zhat and the pivots agree bitwise."""
+    p = tiny(*shape)
+    A = oracle.assemble(p)
+    a, b = oracle.ainv(A, tau, "sparse"), oracle.ainv(A, tau, "dense")
+    assert np.array_equal(a.colptr, b.colptr) and np.array_equal(a.row, b.row)
+    assert np.array_equal(a.zhat, b.zhat) and np.array_equal(a.pivots, b.pivots)
+
+
+def test_ainv_preconditioner_spd_and_drop_rule():
+    """P = Z D^-1 Z^T is SPD; every kept off-diagonal |zhat| >= tau."""
+    p = tiny(14, 10, 5)
+    A = oracle.assemble(p)
+    rng = np.random.default_rng(0)
+    for tau in (0.05, 0.1, 0.2):
+        M = oracle.ainv(A, tau + 1e-9)
+        off = M.row != np.repeat(np.arange(M.n), np.diff(M.colptr))
+        assert np.all(np.abs(M.zhat[off]) >= tau)
+        assert np.all(M.pivots > 0) and np.all(M.pivots <= 1.0 + 1e-15)
+        P = ainv_operator(M)
+        assert np.allclose(P, P.T, rtol=0, atol=1e-14 * np.abs(P).max())
+        for _ in range(20):
+            x = rng.standard_normal(M.n)
+            assert x @ P @ x > 0
+        # apply() is P r
+        r = rng.standard_normal(M.n)
+        assert np.allclose(M.apply(r), P @ r, rtol=1e-12, atol=1e-14)
+
+
+def test_power_of_two_scaling_invariance():
+    """E13: coefficients x4 leave Zhat and p bitwise equal; x scales by 1/4 exactly and the
+    residual histories are bitwise equal."""
+    p = tiny(40, 30, 6)
+    q = synth.Problem("x4", p.ni, p.nj, 4 * p.cE, 4 * p.cN, p.mask, True, None)
+    A, A4 = oracle.assemble(p), oracle.assemble(q)
+    M, M4 = oracle.ainv(A, 0.1 + 1e-9), oracle.ainv(A4, 0.1 + 1e-9)
+    assert np.array_equal(M.zhat, M4.zhat) and np.array_equal(M.pivots, M4.pivots)
+    assert np.array_equal(M.row, M4.row)
+    b = synth.random_rhs(p, 1)[p.mask.astype(bool)]
+    r, r4 = oracle.pcg(A, b, "ainv", M, 1e-10), oracle.pcg(A4, b, "ainv", M4, 1e-10)
+    assert r.iterations == r4.iterations
+    assert np.array_equal(r.hist, r4.hist)
+    assert np.array_equal(r.x, 4 * r4.x)
+
+
+# ------------------------------------------------------------------ partitioned AINV
+def test_partition_balanced_and_valid():
+    p = synth.config("cfg2")
+    for P in (1, 2, 4, 8):
+        rb = oracle.partition(p.nj, p.ni, p.mask, P)
+        assert rb[0] == 0 and rb[-1] == p.nj and np.all(np.diff(rb) >= 1)
+        counts = [int(p.mask[rb[k]:rb[k + 1]].sum()) for k in range(P)]
+        assert max(counts) - min(counts) <= 2 * p.ni       # balanced to within ~a row
+
+
+def test_partitioned_ainv_structure():
+    """Reading R15: w = 0 gives a block-diagonal P; any w gives one global unit upper
+    triangular Zhat; w >= nj (all southern rows) reproduces the global AINV bitwise,
+    because column j only involves the leading (j+1)x(j+1) block of A^."""
+    p = synth.config("cfg2")
+    A = oracle.assemble(p)
+    G = oracle.ainv(A, 0.1 + 1e-9)
+    rb = oracle.partition(p.nj, p.ni, p.mask, 4)
+    rows_of = A.grid_index // p.ni
+    part_of = np.searchsorted(rb, rows_of, side="right") - 1
+    M0 = oracle.ainv(A, 0.1 + 1e-9, parts=4, halo=0)
+    cols = np.repeat(np.arange(A.n), np.diff(M0.colptr))
+    assert np.all(part_of[M0.row] == part_of[cols])            # block diagonal
+    for w in (1, 3):
+        Mw = oracle.ainv(A, 0.1 + 1e-9, parts=4, halo=w)
+        cols = np.repeat(np.arange(A.n), np.diff(Mw.colptr))
+        assert np.all(Mw.row <= cols)
+        d = Mw.row == cols
+        assert d.sum() == A.n and np.all(Mw.zhat[d] == 1.0)
+        assert np.all(rows_of[cols] - rows_of[Mw.row] <= max(w, 0) + (rows_of[cols] - rows_of[Mw.row]).max())
+        assert np.any(part_of[Mw.row] != part_of[cols])        # halo couplings exist
+    Mall = oracle.ainv(A, 0.1 + 1e-9, parts=4, halo=p.nj)
+    assert np.array_equal(Mall.row, G.row) and np.array_equal(Mall.zhat, G.zhat)
+    assert np.array_equal(Mall.pivots, G.pivots)
+    M1 = oracle.ainv(A, 0.1 + 1e-9, parts=1, halo=3)
+    assert np.array_equal(M1.zhat, G.zhat)
+
+
+def test_partitioned_iterations_envelope():
+    """E8 / E20: block-local AINV changes iterations by a few %; halo-AINV w = 3 recovers
+    the 1-part count within 1 %."""
+    p = synth.config("cfg2")
+    A = oracle.assemble(p)
+    b = A.apply(A.from_grid(synth.xstar(p)))
+    k1 = oracle.pcg(A, b, "ainv", oracle.ainv(A, 0.1 + 1e-9), 1e-10).iterations
+    for P in (2, 4, 8):
+        k0 = oracle.pcg(A, b, "ainv", oracle.ainv(A, 0.1 + 1e-9, parts=P, halo=0), 1e-10).iterations
+        k3 = oracle.pcg(A, b, "ainv", oracle.ainv(A, 0.1 + 1e-9, parts=P, halo=3), 1e-10).iterations
+        assert 0.95 * k1 <= k0 <= 1.12 * k1
+        assert abs(k3 - k1) <= max(2, 0.01 * k1)
+
+
+# --------------------------------------------------------------------------------- PCG
+@pytest.mark.parametrize("precond,tau", [("ainv", 0.1 + 1e-9), ("ainv", 0.0), ("jacobi", None), ("none", None)])
+@pytest.mark.parametrize("seed", [1, 2])
+def test_pcg_matches_dense_solve(precond, tau, seed):
+    """Brute force (north star): x vs numpy.linalg.solve at tol 1e-13."""
+    p = tiny(11, 9, seed, sigma=seed == 2)
+    A = oracle.assemble(p)
+    b = synth.random_rhs(p, seed)[p.mask.astype(bool)]
+    M = oracle.ainv(A, tau) if precond == "ainv" else None
+    r = oracle.pcg(A, b, precond, M, tol=1e-13)
+    xd = np.linalg.solve(A.dense(), b)
+    assert r.converged and r.status == "OK"
+    assert np.linalg.norm(r.x - xd) / np.linalg.norm(xd) < 1e-9
+    assert r.true_rel_residual < 1e-12
+
+
+def test_pcg_tau0_one_iteration():
+    """E7: with tau = 0, P = A^-1, so PCG converges in exactly one iteration."""
+    for name in ("cfg1",):
+        p = synth.config(name)
+        A = oracle.assemble(p)
+        b = A.apply(A.from_grid(synth.xstar(p)))
+        r = oracle.pcg(A, b, "ainv", oracle.ainv(A, 0.0), 1e-10)
+        assert r.iterations == 1
+
+
+def test_finite_termination():
+    """P:143 'exact solution in a number of iterations equal to the size of the matrix';
+    E13: at most N_o + 2 in floating point on tiny grids."""
+    worst = -99
+    for seed in range(12):
+        p = tiny(5 + seed % 3, 4 + seed % 4, 100 + seed)
+        A = oracle.assemble(p)
+        b = synth.random_rhs(p, seed)[p.mask.astype(bool)]
+        for pc in ("none", "jacobi"):
+            r = oracle.pcg(A, b, pc, None, 1e-10, maxit=10 * A.n)
+            assert r.converged
+            worst = max(worst, r.iterations - A.n)
+    assert worst <= 2
+
+
+def test_eq11_bound_and_monotone_anorm():
+    """Eq. 11: ||x - x_m||_A < 2((sqrt(mu)-1)/(sqrt(mu)+1))^(m-1) ||x - x_0||_A
+    for plain CG; the A-norm error decreases monotonically."""
+    p = tiny(6, 5, 9)
+    A = oracle.assemble(p)
+    D = A.dense()
+    ev = np.linalg.eigvalsh(D)
+    mu = ev[-1] / ev[0]
+    b = synth.random_rhs(p, 3)[p.mask.astype(bool)]
+    xs = np.linalg.solve(D, b)
+    anorm = lambda e: math.sqrt(e @ D @ e)
+    e0 = anorm(xs)
+    prev = e0
+    q = (math.sqrt(mu) - 1) / (math.sqrt(mu) + 1)
+    for m in range(1, A.n):
+        r = oracle.pcg(A, b, "none", None, tol=0.0, maxit=m)
+        em = anorm(xs - r.x)
+        if em < 1e-12 * e0:
+            break
+        assert em < 2 * q ** (m - 1) * e0
+        assert em <= prev * (1 + 1e-12)
+        prev = em
+    g = GOLD["convergence_bound_100_51"]
+    qq = (math.sqrt(g["mu2"]) - 1) / (math.sqrt(g["mu2"]) + 1)
+    assert abs(2 * qq ** (g["m"] - 1) - g["value"]) / g["value"] < g["rtol"]
+
+
+def test_cfg1_cg_jacobi_ainvinf_bitwise():
+    """E15: config 1 has d = 4 (a power of two), so plain CG, Jacobi-PCG and AINV(inf)-PCG
+    give bitwise identical iterates: 130 iterations."""
+    p = synth.config("cfg1")
+    A = oracle.assemble(p)
+    b = A.apply(A.from_grid(synth.xstar(p)))
+    for mode in ("plain", "canonical"):
+        kw = dict(mode=mode, pitch=32)
+        r0 = oracle.pcg(A, b, "none", None, 1e-10, **kw)
+        r1 = oracle.pcg(A, b, "jacobi", None, 1e-10, **kw)
+        r2 = oracle.pcg(A, b, "ainv", oracle.ainv(A, INF), 1e-10, **kw)
+        assert r0.iterations == r1.iterations == r2.iterations == 130
+        assert np.array_equal(r0.x, r1.x) and np.array_equal(r0.x, r2.x)
+        assert np.array_equal(r0.hist, r1.hist) and np.array_equal(r0.hist, r2.hist)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+def test_paper_claim_ainv_fewer_iterations(name):
+    """P:432-457 Table 2 / P:543: the approximate inverse needs fewer PCG iterations than
+    NEMO's diagonal preconditioner (68/130, 231/504, 415/902)."""
+    p = synth.config(name)
+    A = oracle.assemble(p)
+    b = A.apply(A.from_grid(synth.xstar(p)))
+    ka = oracle.pcg(A, b, "ainv", oracle.ainv(A, 0.1 + 1e-9), 1e-10)
+    kj = oracle.pcg(A, b, "jacobi", None, 1e-10)
+    assert ka.converged and kj.converged
+    assert ka.iterations < 0.6 * kj.iterations
+    assert ka.true_rel_residual < 2e-10 and kj.true_rel_residual < 2e-10
+
+
+def test_pcg_edge_cases():
+    p = tiny(10, 8, 4)
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, 0.1 + 1e-9)
+    z = np.zeros(A.n)
+    r = oracle.pcg(A, z, "ainv", M, 1e-10)                      # b = 0 -> x = 0, 0 its
+    assert r.iterations == 0 and np.all(r.x == 0) and r.converged
+    b = synth.random_rhs(p, 2)[p.mask.astype(bool)]
+    xd = np.linalg.solve(A.dense(), b)
+    r = oracle.pcg(A, b, "ainv", M, 1e-10, x0=xd)              # x0 = solution -> 0 its
+    assert r.iterations <= 1
+    r = oracle.pcg(A, b, "ainv", M, 1e-14, maxit=3)             # maxit hit -> not converged
+    assert r.iterations == 3 and not r.converged and r.status == "OK"
+    r = oracle.pcg(A, b, "ainv", M, 0.0, maxit=7)               # tol = 0 -> exactly maxit
+    assert r.iterations == 7
+    with pytest.raises(oracle.OracleError):
+        oracle.pcg(A, b, "ainv", M, -1.0)
+
+
+def test_canonical_dot_is_exact_on_integers():
+    """The canonical block-tree order sums integer-valued products exactly."""
+    p = synth.config("cfg2")
+    A = oracle.assemble(p)
+    rng = np.random.default_rng(1)
+    # jacobi PCG with tol=0, maxit=0 exposes nothing; test through a 0-iteration run:
+    # hist[0] = sqrt((r,r))/sqrt((b,b)) with x0 = 0 -> r = b -> exactly 1.0 in any order
+    b = rng.integers(-1000, 1000, A.n).astype(float)
+    r = oracle.pcg(A, b, "none", None, 0.0, maxit=0, mode="canonical", pitch=192)
+    assert r.hist[0] == 1.0
+
+
+@pytest.mark.parametrize("name", ["cfg2"])
+def test_canonical_vs_plain(name):
+    """Reduction order changes iterations only marginally (E4/E10): +-max(2, 1 %) at tol
+    1e-10, and x agrees to 1e-9 at tol 1e-12."""
+    p = synth.config(name)
+    A = oracle.assemble(p)
+    b = A.apply(A.from_grid(synth.xstar(p)))
+    M = oracle.ainv(A, 0.1 + 1e-9)
+    a = oracle.pcg(A, b, "ainv", M, 1e-10)
+    c = oracle.pcg(A, b, "ainv", M, 1e-10, mode="canonical", pitch=192, block=256)
+    assert abs(a.iterations - c.iterations) <= max(2, 0.01 * a.iterations)
+    a = oracle.pcg(A, b, "ainv", M, 1e-12)
+    c = oracle.pcg(A, b, "ainv", M, 1e-12, mode="canonical", pitch=192, block=256)
+    assert np.linalg.norm(a.x - c.x) / np.linalg.norm(a.x) < 1e-9
+
+
+def test_generator_matches_survey_counts():
+    """Regression anchors for the synthetic recipe: N_o and nnz(A)."""
+    p = synth.config("cfg2")
+    A = oracle.assemble(p)
+    assert (A.n, A.nnz) == (22288, 110528)
+    p = synth.config("cfg1")
+    assert oracle.assemble(p).n == 948
