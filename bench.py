@@ -1,0 +1,298 @@
+#!/usr/bin/env python
+"""bench.py -- PCG iterations/s and time-to-solution (fp64, ORCA025-like grid) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config cfg4] [--precond ainv|jacobi] [--tol 1e-10]
+
+A step is one full solve (pcg_solve: init a3, the PCG loop a4-a8 until ||r||/||b|| <= tol,
+finish a9) of BASELINE.json's headline workload, configs[3]: the ORCA025-like 1442x1021
+grid, AINV(0.1), tol 1e-10, synthetic inputs.  Setup (assembly + AINV +
+packing, a0-a2) runs once before the timed region and is reported separately.
+
+value = iterations of all timed solves / device time of the timed region (CUDA events on
+the caller's stream, barrier + synchronize on both sides, max over ranks).  e2e = the same
+through pcg_solve_host with host buffers (H2D of b and D2H of x inside the timed region).
+roofline = the dominant per-iteration kernel's algorithmic bytes / its CUDA-event time,
+against MEASURED_PEAKS.json's HBM copy bandwidth.  cpu_baseline = the CPU oracle on a
+bounded sample of the same workload (rank 0, N = 1 only).
+
+--impl reference times the oracle (the reference arm of this tier) as it stands.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
+METRIC = BASELINE["metric"]
+UNIT = "iter/s"
+WORKLOAD = "cfg4: ORCA025-like 1442x1021 grid, E-W periodic, ~17% land, AINV(tau=0.1) PCG to ||r||/||b|| <= 1e-10"
+
+
+def fallback_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        j = json.load(open(p))
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,power.draw")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_oracle_sample(p, tau, n_iter):
+    """The oracle as it stands (plain C, single thread) on a bounded sample of the workload:
+    assembly + AINV setup, then n_iter PCG iterations (tol = 0)."""
+    import oracle
+    from paper_1210_1878_b200 import synth
+    t0 = time.perf_counter()
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, tau)
+    t1 = time.perf_counter()
+    b = A.apply(A.from_grid(synth.xstar(p)))
+    t2 = time.perf_counter()
+    r = oracle.pcg(A, b, "ainv", M, 0.0, maxit=n_iter)
+    t3 = time.perf_counter()
+    return {"setup_s": t1 - t0, "iters": r.iterations, "solve_s": t3 - t2}
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores, each step a bounded sample."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from paper_1210_1878_b200 import synth
+    p = synth.config(args.config)
+    n_iter = args.ref_iters
+    for _ in range(args.warmup if args.warmup <= 1 else 1):
+        cpu_oracle_sample(p, args.tau, 2)
+    tot_it, tot_s, setup = 0, 0.0, []
+    for _ in range(args.steps):
+        r = cpu_oracle_sample(p, args.tau, n_iter)
+        tot_it += r["iters"]
+        tot_s += r["solve_s"]
+        setup.append(r["setup_s"])
+    v = tot_it / tot_s
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD, "precond": "ainv", "tau": args.tau,
+                       "sample": f"{n_iter} PCG iterations (tol=0) per step after the oracle's own setup"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{args.config}, {n_iter} plain-order PCG iterations per step, "
+                                       f"setup {np.mean(setup):.2f} s excluded"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--precond", default="ainv", choices=["ainv", "jacobi"])
+    ap.add_argument("--tau", type=float, default=0.1)
+    ap.add_argument("--tol", type=float, default=1e-10)
+    ap.add_argument("--ref-iters", type=int, default=40)
+    ap.add_argument("--cpu-iters", type=int, default=150)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile-iters", type=int, default=60)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1210_1878_b200 as pcg
+    from paper_1210_1878_b200 import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    group = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        group = dist.group.WORLD
+    p = synth.config(args.config)
+    t0 = time.perf_counter()
+    S = pcg.Solver(p.cE, p.cN, p.mask, tau=args.tau, precond=args.precond, group=group, device=local)
+    setup_wall = time.perf_counter() - t0
+    rows = slice(S.j_begin, S.j_end)
+    xs = torch.from_numpy(np.ascontiguousarray(synth.xstar(p)[rows])).cuda()
+    b = S.apply_operator(xs)                                     # b = A x* through the library
+    maxit = 20 * p.ni * p.nj
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        x, k, hist, rep = S.solve(b, tol=args.tol, maxit=maxit)
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    iters = []
+    lib_s = 0.0
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            x, k, hist, rep = S.solve(b, tol=args.tol, maxit=maxit)
+            iters.append(k)
+            lib_s += rep["solve_s"]
+        e1.record(stream)
+        barrier()
+    dev_ms = e0.elapsed_time(e1)
+    t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev_ms = float(t.item())
+    total_iters = sum(iters)
+    value = total_iters / (dev_ms * 1e-3)
+
+    # e2e: host buffers through pcg_solve_host (H2D of b, D2H of x inside the timed region)
+    bh = torch.empty(b.shape, dtype=torch.float64, pin_memory=True)
+    bh.copy_(b.cpu())
+    xh = torch.empty(b.shape, dtype=torch.float64, pin_memory=True)
+    S.solve_host(bh.numpy(), tol=args.tol, maxit=maxit, out=xh.numpy())
+    barrier()
+    w0 = time.perf_counter()
+    e_iters = 0
+    for _ in range(args.steps):
+        _, k2, _, _ = S.solve_host(bh.numpy(), tol=args.tol, maxit=maxit, out=xh.numpy())
+        e_iters += k2
+    barrier()
+    e2e_s = time.perf_counter() - w0
+    t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    nbytes = int(b.numel() * 8)
+
+    # roofline of the dominant kernel (single rank: per-kernel CUDA events on the launch stream)
+    roof = None
+    ktimes = None
+    if world == 1:
+        S.solve(b, tol=args.tol, maxit=maxit)
+        ms, by = S.kernel_times(args.profile_iters)
+        names = ["K1_stencil", "K2_ZTr", "K3_Zt"]
+        kk = int(np.argmax(ms[:3]))
+        peak, peak_src = fallback_peak()
+        ach = by[kk] / (ms[kk] * 1e-3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            tj = json.load(open(tp))
+            traffic = tj.get(args.config, {}).get(names[kk])
+        roof = {"bound": "hbm", "kernel": names[kk], "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes_per_launch": by[kk], "ms_per_launch": ms[kk]}
+        ktimes = {names[i]: {"ms": ms[i], "alg_GBps": by[i] / (ms[i] * 1e-3) / 1e9 if ms[i] > 0 else None}
+                  for i in range(3)}
+        ktimes["iteration_ms"] = ms[3]
+        ktimes["iteration_alg_GBps"] = float(by.sum() / (ms[3] * 1e-3) / 1e9)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r = cpu_oracle_sample(p, args.tau, args.cpu_iters)
+        cpu = {"value": r["iters"] / r["solve_s"], "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{args.config} full grid, {r['iters']} plain-order PCG iterations (tol=0) after the "
+                         f"oracle's own assembly+AINV ({r['setup_s']:.2f} s, excluded)"}
+
+    # launches per solve: prologue 4 (prep, init, K2, K3) + WHILE body of 2 iterations x 3 + epilogue 2
+    per_iter = 3 if args.precond == "ainv" else 2
+    pro = 4 if args.precond == "ainv" else 3
+    if world == 1:
+        launches = sum(pro + per_iter * 2 * math.ceil(k / 2) + 2 for k in iters)
+    else:
+        launches = None
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (SURVEY A.1 generator, seed 2; b = A x*, x* ~ N(0,1) seed 0)",
+                "config": {"workload": WORKLOAD, "grid": [p.ni, p.nj], "n_ocean": p.n_ocean,
+                           "precond": args.precond, "tau": args.tau, "tol": args.tol,
+                           "iterations_per_solve": iters, "time_to_solution_ms": dev_ms / args.steps,
+                           "library_solve_ms": 1e3 * lib_s / args.steps,
+                           "setup_s": rep["setup_s"], "setup_wall_s": setup_wall,
+                           "bytes_per_iter_algorithmic": rep["bytes_per_iter"],
+                           "device_bytes": S.device_bytes,
+                           "l2": "no flush: per-iteration working set (~280 MB) exceeds the 126 MB L2",
+                           "parallelism": f"row blocks x{world}" if world > 1 else "1 GPU",
+                           "kernels": ktimes},
+                "roofline": roof, "cpu_baseline": cpu,
+                "e2e": {"value": e_iters / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+                        "d2h_bytes_per_step": nbytes},
+                "gpu_launches": launches, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    S.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -72,6 +72,10 @@ def lib():
         L.orc_ainv_nnz.argtypes = [P]; L.orc_ainv_nnz.restype = I64
         L.orc_ainv_export.argtypes = [P, vp, vp, vp, vp, vp, vp]
         L.orc_ainv_apply.argtypes = [P, vp, vp]
+        L.orc_apply_canonical.argtypes = [P, vp, vp]
+        L.orc_ainv_apply_canonical.argtypes = [P, vp, vp]
+        L.orc_dot_canonical.argtypes = [P, vp, vp, vp]
+        L.orc_dot_canonical.restype = D
         L.orc_pcg.argtypes = [P, P, vp, vp, vp, D, I32, vp, vp, vp]
         L.orc_pcg.restype = C.c_int
         _lib = L
@@ -155,6 +159,19 @@ class Assembled:
         lib().orc_apply(self._h, _ptr(x), _ptr(y))
         return y
 
+    def apply_canonical(self, x):
+        """y = A x in the GPU's documented order."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty(self.n)
+        lib().orc_apply_canonical(self._h, _ptr(x), _ptr(y))
+        return y
+
+    def dot_canonical(self, a, b, pitch, block=256, parts=1):
+        o = _PcgOpts(0, 1, int(pitch), int(block), int(parts))
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        return float(lib().orc_dot_canonical(self._h, C.byref(o), _ptr(a), _ptr(b)))
+
     def anchor_check(self) -> int:
         return int(lib().orc_anchor_check(self._h))
 
@@ -200,6 +217,13 @@ class Ainv:
         r = np.ascontiguousarray(r, dtype=np.float64)
         s = np.empty(self.n)
         lib().orc_ainv_apply(self.handle._h, _ptr(r), _ptr(s))
+        return s
+
+    def apply_canonical(self, r):
+        """s = Z D^-1 Z^T r in the GPU's documented order."""
+        r = np.ascontiguousarray(r, dtype=np.float64)
+        s = np.empty(self.n)
+        lib().orc_ainv_apply_canonical(self.handle._h, _ptr(r), _ptr(s))
         return s
 
 

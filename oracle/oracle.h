@@ -84,6 +84,12 @@ typedef struct {
     int64_t failed_index;
 } orc_pcg_report;
 
+/* The canonical-order pieces on their own: y = A x with the W,E,S,N fma
+ * stencil; s = Z D^-1 Z^T r with fma row sums; the block-tree dot product. */
+void   orc_apply_canonical(const orc_problem*, const double* x, double* y);
+void   orc_ainv_apply_canonical(const orc_ainv*, const double* r, double* s);
+double orc_dot_canonical(const orc_problem*, const orc_pcg_opts*, const double* a, const double* b);
+
 /* x, hist are outputs (hist length >= maxit+1).  x0 may be NULL (= 0).  tol = 0 runs
  * exactly maxit iterations. */
 int orc_pcg(const orc_problem*, const orc_ainv* /*nullable unless AINV*/, const orc_pcg_opts*,

@@ -124,6 +124,27 @@ static void canon_ainv_apply(const orc_ainv* R, const double* r, double* s, doub
     }
 }
 
+void orc_apply_canonical(const orc_problem* P, const double* x, double* y) { canon_apply(P, x, y); }
+
+void orc_ainv_apply_canonical(const orc_ainv* R, const double* r, double* s) {
+    double* t = (double*)malloc(sizeof(double) * (R->n ? R->n : 1));
+    canon_ainv_apply(R, r, s, t);
+    free(t);
+}
+
+double orc_dot_canonical(const orc_problem* P, const orc_pcg_opts* o, const double* a, const double* b) {
+    canon C = {0};
+    C.P = P; C.pitch = o->pitch; C.B = o->block; C.parts = o->parts;
+    C.rb = (int32_t*)malloc(sizeof(int32_t) * (o->parts + 1));
+    if (o->parts == 1) { C.rb[0] = 0; C.rb[1] = P->nj; }
+    else orc_partition(P->nj, P->ni, P->mask, o->parts, C.rb);
+    C.vals = (double*)malloc(sizeof(double) * o->block);
+    C.partial = (double*)malloc(sizeof(double) * (((int64_t)P->nj * o->pitch) / o->block + 2));
+    double r = canon_dot(&C, a, b);
+    free(C.rb); free(C.vals); free(C.partial);
+    return r;
+}
+
 static double plain_dot(int64_t n, const double* a, const double* b) {
     double acc = 0.0;
     for (int64_t k = 0; k < n; ++k) acc = acc + a[k] * b[k];

@@ -1,0 +1,80 @@
+// internal.h -- private structures of libpcg (host setup + device state).
+//
+// Device layout: every per-point array of a rank holds nloc+2 grid rows of
+// `pitch` doubles (pitch = ni rounded up to a multiple of 32): row 0 is the southern halo,
+// rows 1..nloc the owned rows j_begin..j_end-1, row nloc+1 the northern halo.  An owned
+// element e = (j - j_begin)*pitch + i lives at array index a = e + pitch.  Entries with
+// i >= ni, land points and (on one GPU) the halo rows hold 0 in every vector.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/libpcg.h"
+
+namespace pcg {
+
+constexpr int kBlock = 256;        // threads per block of every streaming kernel
+constexpr int kSlice = 32;         // SELL slice height (one warp)
+constexpr double kPivotMin = 1e-12;
+
+struct Status {
+    pcg_status code = PCG_OK;
+    std::string msg;
+    int64_t index = -1;
+    static Status ok() { return {}; }
+    static Status err(pcg_status c, std::string m, int64_t idx = -1) { return {c, std::move(m), idx}; }
+    explicit operator bool() const { return code == PCG_OK; }
+};
+
+// SELL-32 matrix over the owned elements: slice s covers owned elements [32 s, 32 s + 32)
+// of one grid row; entry m of lane l is at off[s] + 32 m + l.  Columns are ARRAY indices
+// (owned element + pitch).  Padding entries have value 0 and the row's own index.
+struct Sell {
+    std::vector<int64_t> off;      // nslices + 1
+    std::vector<double> val;
+    std::vector<int32_t> col;
+    int64_t entries() const { return (int64_t)val.size(); }
+};
+
+// Host product of setup: everything the device needs, in device layout.
+struct Plan {
+    int32_t ni = 0, nj = 0, periodic = 1, jb = 0, je = 0, rank = 0, nranks = 1;
+    int32_t nloc = 0, pitch = 0;
+    pcg_precond precond = PCG_PRECOND_AINV;
+    double tau = 0.1;
+    int32_t flags = 0;
+    bool has_sigma = false;
+    int64_t n_owned = 0, first_global = 0, nnz_off = 0;
+    // per-element arrays, (nloc + 2) * pitch
+    std::vector<double> cE, cN, sigma, diag, piv;
+    Sell Z, ZT;                    // rows of Z (for s = Z t) and of Z^T (for t = Z^T r)
+    // export (owned columns of Zhat, global unknown numbering)
+    std::vector<int64_t> zcolptr, zrow;
+    std::vector<double> zhat, pivots, scale;
+    double setup_s = 0.0;
+    int64_t elements() const { return (int64_t)(nloc + 2) * pitch; }
+    int64_t owned_elements() const { return (int64_t)nloc * pitch; }
+};
+
+Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Plan& plan);
+Status partition_rows(int32_t ni, int32_t nj, const uint8_t* mask, int32_t parts, int32_t* rb);
+
+// Library AINV on one row block (written independently of the oracle).
+struct AinvBlock {
+    // input: grid rows [row_lo, row_hi) form the index set; columns of rows >= row_own are kept
+    int32_t row_lo = 0, row_own = 0, row_hi = 0;
+    // output: owned columns, local unknown numbering of the block converted to GLOBAL grid
+    // indices (j*ni + i) for rows, values zhat, pivots; failure column (global grid index)
+    std::vector<int64_t> colptr;   // owned columns + 1
+    std::vector<int64_t> row_g;    // grid index of each entry's row
+    std::vector<double> zhat;
+    std::vector<double> piv;       // per owned column
+    std::vector<int64_t> col_g;    // grid index of each owned column
+    int64_t fail_grid = -1;
+};
+void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, const double* cN,
+                const double* sigma, const uint8_t* mask, double tau, AinvBlock& blk);
+
+}  // namespace pcg

@@ -1,0 +1,58 @@
+// kernels.h -- device state and kernel launchers of libpcg (sm_100a, fp64).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace pcg {
+
+enum : int32_t { kStOk = 0, kStBreakdown = 3 };
+
+// Device-resident scalars of one solve.  Written only by the last block of a
+// reduction kernel (one rank) or by the 1-thread scalar kernels after an NCCL allgather.
+struct DevScalars {
+    double alpha, beta, rho, nb, tol, true_rel;
+    double red[4];        // global reductions: [0] (d,q)  [1] (s,r)  [2] (r,r)  [3] (b,b) / true (r,r)
+    double loc[4];        // this rank's block-tree sums (multi-rank path)
+    int32_t k, maxit, active, status, bzero, xpend;
+    uint32_t counter[4];  // last-block detection, reset by the last block
+};
+
+struct KArgs {
+    int32_t ni, pitch, nloc, nranks;
+    int64_t nel;                      // owned elements nloc * pitch
+    const double *cE, *cN, *sigma, *diag, *piv;
+    const int64_t *zt_off, *z_off;
+    const double *zt_val, *z_val;
+    const int32_t *zt_col, *z_col;
+    double *x, *b, *q, *t, *s;
+    double *r[2], *d[2];
+    double* partial[3];
+    double* gath;                     // nranks * 4 gathered rank sums (multi-rank)
+    DevScalars* sc;
+    double* hist;
+    int32_t hist_cap;
+    int32_t multi;                    // 1: reductions end at rank sums (NCCL path)
+    int32_t use_cond;
+    cudaGraphConditionalHandle cond;
+};
+
+int64_t grid_blocks(const KArgs& A);
+
+// per-iteration kernels (par = iteration parity; init = the a3 pass with alpha = 0)
+void launch_k1(const KArgs& A, int par, cudaStream_t st);
+void launch_k2_ainv(const KArgs& A, int par, int init, cudaStream_t st);
+void launch_k3_ainv(const KArgs& A, int par, int init, cudaStream_t st);
+void launch_k2_diag(const KArgs& A, int par, int init, int none, cudaStream_t st);
+// solve prologue / epilogue
+void launch_prep(const KArgs& A, cudaStream_t st);
+void launch_init_residual(const KArgs& A, cudaStream_t st);       // r0 = b - A x0 -> r[1], (b,b)
+void launch_fin(const KArgs& A, cudaStream_t st);                 // pending x update / b = 0
+void launch_true_residual(const KArgs& A, cudaStream_t st);       // ||b - A x|| / ||b||
+void launch_apply(const KArgs& A, const double* x_arr, double* y_arr, cudaStream_t st);   // y = A x
+// multi-rank scalar steps (one thread) after an allgather of DevScalars::loc
+enum ScalarStep : int32_t { kSsBB = 0, kSsGamma = 1, kSsInit = 2, kSsIter = 3, kSsTrue = 4 };
+void launch_scalar(const KArgs& A, int step, cudaStream_t st);
+void launch_set_cond(cudaGraphConditionalHandle h, cudaStream_t st);
+
+}  // namespace pcg

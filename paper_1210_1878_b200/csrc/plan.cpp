@@ -1,0 +1,342 @@
+// plan.cpp -- host half of pcg_setup: validation, row partition, anchor check, device-layout
+// coefficient arrays, AINV per block, SELL-32 packing of Z and Z^T.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <thread>
+
+#include "internal.h"
+
+namespace pcg {
+
+Status partition_rows(int32_t ni, int32_t nj, const uint8_t* mask, int32_t parts, int32_t* rb) {
+    if (ni < 1 || nj < 1 || parts < 1 || parts > nj || !mask || !rb)
+        return Status::err(PCG_ERR_ARG, "pcg_partition: need 1 <= parts <= nj and non-NULL mask/row_begin");
+    std::vector<int64_t> cum(nj + 1, 0);
+    for (int32_t j = 0; j < nj; ++j) {
+        int64_t c = 0;
+        for (int32_t i = 0; i < ni; ++i) c += mask[(int64_t)j * ni + i] ? 1 : 0;
+        cum[j + 1] = cum[j] + c;
+    }
+    const int64_t N = cum[nj];
+    rb[0] = 0;
+    for (int32_t p = 1; p < parts; ++p) {
+        // smallest j with cum[j] * parts >= p * N (cum is non-decreasing)
+        int32_t j = (int32_t)(std::lower_bound(cum.begin(), cum.end(), 0, [&](int64_t v, int) {
+                        return v * parts < (int64_t)p * N; }) - cum.begin());
+        j = std::max(j, rb[p - 1] + 1);
+        j = std::min(j, nj - (parts - p));
+        rb[p] = j;
+    }
+    rb[parts] = nj;
+    return Status::ok();
+}
+
+namespace {
+
+// Anchor check (reading R22): every 4-connected ocean component (faces with c > 0,
+// E-W wrap included) must own a positive face to a land cell or a point with sigma > 0.
+Status anchor_check(int32_t ni, int32_t nj, int32_t periodic, const double* cE, const double* cN,
+                    const double* sigma, const uint8_t* mask) {
+    const int64_t ng = (int64_t)ni * nj;
+    std::vector<int32_t> comp(ng, -1);
+    std::vector<int64_t> stack;
+    int64_t unknown = 0;                    // natural-order index of the component root
+    std::vector<int64_t> unk_of(ng, -1);
+    for (int64_t g = 0; g < ng; ++g) if (mask[g]) unk_of[g] = unknown++;
+    for (int64_t root = 0; root < ng; ++root) {
+        if (!mask[root] || comp[root] >= 0) continue;
+        bool anchored = false;
+        stack.clear(); stack.push_back(root); comp[root] = 1;
+        while (!stack.empty()) {
+            int64_t g = stack.back(); stack.pop_back();
+            int32_t i = (int32_t)(g % ni), j = (int32_t)(g / ni);
+            if (sigma && sigma[g] > 0.0) anchored = true;
+            const int64_t row = (int64_t)j * ni;
+            struct { bool ex; int64_t nb; double c; } f[4] = {
+                {(i + 1 < ni) || periodic != 0, row + (i + 1) % ni, cE[row + i]},
+                {(i >= 1) || periodic != 0, row + (i - 1 + ni) % ni, cE[row + (i - 1 + ni) % ni]},
+                {j + 1 < nj, row + ni + i, j + 1 < nj ? cN[row + i] : 0.0},
+                {j >= 1, row - ni + i, j >= 1 ? cN[row - ni + i] : 0.0}};
+            for (auto& x : f) {
+                if (!x.ex || !(x.c > 0.0)) continue;
+                if (!mask[x.nb]) { anchored = true; continue; }
+                if (comp[x.nb] < 0) { comp[x.nb] = 1; stack.push_back(x.nb); }
+            }
+        }
+        if (!anchored) {
+            char buf[256];
+            snprintf(buf, sizeof buf,
+                     "A is singular: the ocean basin containing grid point (i=%d, j=%d) has no positive "
+                     "face to land and sigma = 0 (anchor check, DESIGN.md R22)",
+                     (int)(root % ni), (int)(root / ni));
+            return Status::err(PCG_ERR_NOT_SPD, buf, unk_of[root]);
+        }
+    }
+    return Status::ok();
+}
+
+int64_t global_unknown(const uint8_t* mask, int32_t ni, int64_t g) {
+    (void)ni;
+    int64_t c = 0;
+    for (int64_t k = 0; k < g; ++k) c += mask[k] ? 1 : 0;
+    return c;
+}
+
+// Pack a set of sparse rows (one per owned element; entries (array column, value) already in
+// ascending column order) into SELL-32.
+void pack_sell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols,
+               const std::vector<double>& vals, int64_t nel, int32_t pitch, Sell& S) {
+    const int64_t nsl = nel / kSlice;
+    S.off.assign(nsl + 1, 0);
+    for (int64_t s = 0; s < nsl; ++s) {
+        int64_t L = 0;
+        for (int l = 0; l < kSlice; ++l) {
+            int64_t e = s * kSlice + l;
+            L = std::max(L, rowptr[e + 1] - rowptr[e]);
+        }
+        S.off[s + 1] = S.off[s] + L * kSlice;
+    }
+    S.val.assign(S.off[nsl], 0.0);
+    S.col.assign(S.off[nsl], 0);
+    for (int64_t s = 0; s < nsl; ++s) {
+        const int64_t L = (S.off[s + 1] - S.off[s]) / kSlice;
+        for (int l = 0; l < kSlice; ++l) {
+            const int64_t e = s * kSlice + l;
+            const int64_t len = rowptr[e + 1] - rowptr[e];
+            for (int64_t m = 0; m < L; ++m) {
+                const int64_t slot = S.off[s] + m * kSlice + l;
+                if (m < len) { S.val[slot] = vals[rowptr[e] + m]; S.col[slot] = cols[rowptr[e] + m]; }
+                else { S.val[slot] = 0.0; S.col[slot] = (int32_t)(e + pitch); }
+            }
+        }
+    }
+}
+
+}  // namespace
+
+Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Plan& P) {
+    auto t0 = std::chrono::steady_clock::now();
+    if (!c || !g || !o) return Status::err(PCG_ERR_ARG, "pcg_setup: NULL coeffs/grid/opts");
+    if (!c->cE || !c->cN || !c->mask) return Status::err(PCG_ERR_ARG, "pcg_setup: coeffs.cE, cN and mask are required");
+    if (g->ni < 3 || g->nj < 3) return Status::err(PCG_ERR_ARG, "pcg_setup: need ni >= 3 and nj >= 3");
+    if (g->nranks < 1 || g->rank < 0 || g->rank >= g->nranks)
+        return Status::err(PCG_ERR_ARG, "pcg_setup: need 0 <= rank < nranks");
+    if (g->j_begin < 0 || g->j_end > g->nj || g->j_begin >= g->j_end)
+        return Status::err(PCG_ERR_ARG, "pcg_setup: need 0 <= j_begin < j_end <= nj");
+    if (g->nranks == 1 && (g->j_begin != 0 || g->j_end != g->nj))
+        return Status::err(PCG_ERR_ARG, "pcg_setup: a single rank must own rows [0, nj)");
+    if (o->precond < PCG_PRECOND_AINV || o->precond > PCG_PRECOND_NONE)
+        return Status::err(PCG_ERR_ARG, "pcg_setup: unknown preconditioner");
+    if (o->precond == PCG_PRECOND_AINV && !(o->drop_tol >= 0.0))
+        return Status::err(PCG_ERR_ARG, "pcg_setup: drop_tol must be >= 0 (inf allowed, NaN not)");
+    if (o->ainv_parts < 0 || o->ainv_halo < 0) return Status::err(PCG_ERR_ARG, "pcg_setup: ainv_parts/ainv_halo < 0");
+    if (o->ainv_parts > 1 && g->nranks > 1)
+        return Status::err(PCG_ERR_ARG, "pcg_setup: ainv_parts emulates ranks on one GPU; use nranks instead");
+    if (g->nranks > 1 && o->ainv_halo > 0)
+        return Status::err(PCG_ERR_ARG, "pcg_setup: halo-AINV (ainv_halo > 0) across ranks is not implemented yet; "
+                                        "emulate it on one GPU with ainv_parts");
+    const int32_t ni = g->ni, nj = g->nj;
+    const int64_t ng = (int64_t)ni * nj;
+    for (int64_t k = 0; k < ng; ++k) {
+        if (!(c->cE[k] >= 0.0) || !std::isfinite(c->cE[k]) || !(c->cN[k] >= 0.0) || !std::isfinite(c->cN[k])) {
+            char buf[160];
+            snprintf(buf, sizeof buf, "pcg_setup: coefficient at (i=%d, j=%d) is negative or not finite",
+                     (int)(k % ni), (int)(k / ni));
+            return Status::err(PCG_ERR_ARG, buf);
+        }
+        if (c->sigma && (!(c->sigma[k] >= 0.0) || !std::isfinite(c->sigma[k])))
+            return Status::err(PCG_ERR_ARG, "pcg_setup: sigma must be finite and >= 0");
+        if (c->mask[k] > 1) return Status::err(PCG_ERR_ARG, "pcg_setup: mask values must be 0 or 1");
+    }
+    P.ni = ni; P.nj = nj; P.periodic = g->periodic_ew ? 1 : 0;
+    P.jb = g->j_begin; P.je = g->j_end; P.rank = g->rank; P.nranks = g->nranks;
+    P.nloc = P.je - P.jb;
+    P.pitch = (ni + kSlice - 1) / kSlice * kSlice;
+    P.precond = o->precond;
+    P.tau = o->drop_tol;
+    P.flags = o->flags;
+    P.has_sigma = c->sigma != nullptr;
+    const int32_t pitch = P.pitch, nloc = P.nloc;
+    const int64_t nel = P.elements();
+
+    // diagonal of every ocean point must be positive, then the structural anchor check
+    auto diag_of = [&](int64_t gi) {
+        int32_t i = (int32_t)(gi % ni), j = (int32_t)(gi / ni);
+        const int64_t row = (int64_t)j * ni;
+        double e = ((i + 1 < ni) || P.periodic) ? c->cE[row + i] : 0.0;
+        double w = ((i >= 1) || P.periodic) ? c->cE[row + (i - 1 + ni) % ni] : 0.0;
+        double n = (j + 1 < nj) ? c->cN[row + i] : 0.0;
+        double s = (j >= 1) ? c->cN[row - ni + i] : 0.0;
+        double d = ((e + w) + n) + s;
+        if (c->sigma) d = d + c->sigma[gi];
+        return d;
+    };
+    for (int64_t k = 0; k < ng; ++k)
+        if (c->mask[k] && !(diag_of(k) > 0.0)) {
+            char buf[160];
+            snprintf(buf, sizeof buf, "pcg_setup: ocean point (i=%d, j=%d) has A_pp <= 0 (isolated, all faces 0)",
+                     (int)(k % ni), (int)(k / ni));
+            return Status::err(PCG_ERR_NOT_SPD, buf, global_unknown(c->mask, ni, k));
+        }
+    if (Status s = anchor_check(ni, nj, P.periodic, c->cE, c->cN, c->sigma, c->mask); !s) return s;
+
+    // device-layout coefficient arrays: absent faces -> 0, land flagged by the
+    // sign bit of cN (cN >= 0 always, so -0.0 / -c mark a land cell).
+    P.cE.assign(nel, 0.0); P.cN.assign(nel, 0.0);
+    P.diag.assign(nel, 1.0); P.piv.assign(nel, 1.0);
+    if (P.has_sigma) P.sigma.assign(nel, 0.0);
+    for (int32_t lr = 0; lr < nloc + 2; ++lr) {
+        const int32_t j = P.jb + lr - 1;
+        if (j < 0 || j >= nj) continue;
+        const int64_t row = (int64_t)j * ni;
+        for (int32_t i = 0; i < ni; ++i) {
+            const int64_t a = (int64_t)lr * pitch + i;
+            const bool owned = lr >= 1 && lr <= nloc;
+            double ce = ((i + 1 < ni) || P.periodic) ? c->cE[row + i] : 0.0;
+            double cn = (j + 1 < nj) ? c->cN[row + i] : 0.0;
+            if (owned) {
+                P.cE[a] = ce;
+                P.cN[a] = c->mask[row + i] ? cn : -cn;
+                if (std::fabs(cn) == 0.0 && !c->mask[row + i]) P.cN[a] = -0.0;
+                if (P.has_sigma) P.sigma[a] = c->mask[row + i] ? c->sigma[row + i] : 0.0;
+                if (c->mask[row + i]) P.diag[a] = diag_of(row + i);
+            } else if (lr == 0) {
+                P.cN[a] = cn;                   // southern halo: S face of row j_begin
+            }
+        }
+    }
+    // owned ocean unknowns, first global index
+    P.first_global = 0;
+    for (int64_t k = 0; k < (int64_t)P.jb * ni; ++k) P.first_global += c->mask[k] ? 1 : 0;
+    P.n_owned = 0;
+    for (int64_t k = (int64_t)P.jb * ni; k < (int64_t)P.je * ni; ++k) P.n_owned += c->mask[k] ? 1 : 0;
+
+    if (P.precond != PCG_PRECOND_AINV) {
+        P.setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        P.zcolptr.assign(P.n_owned + 1, 0);
+        return Status::ok();
+    }
+
+    // ---- AINV per block (reading R15)
+    std::vector<AinvBlock> blocks;
+    if (P.nranks > 1) {
+        AinvBlock b; b.row_lo = std::max(0, P.jb - o->ainv_halo); b.row_own = P.jb; b.row_hi = P.je;
+        blocks.push_back(b);
+    } else {
+        int32_t parts = std::max(1, o->ainv_parts);
+        if (parts > nj) return Status::err(PCG_ERR_ARG, "pcg_setup: ainv_parts > nj");
+        std::vector<int32_t> rb(parts + 1);
+        if (Status s = partition_rows(ni, nj, c->mask, parts, rb.data()); !s) return s;
+        for (int32_t p = 0; p < parts; ++p) {
+            AinvBlock b;
+            b.row_own = rb[p]; b.row_hi = rb[p + 1];
+            b.row_lo = parts == 1 ? 0 : std::max(0, rb[p] - o->ainv_halo);
+            blocks.push_back(b);
+        }
+    }
+    {
+        int nthreads = o->setup_threads > 0 ? o->setup_threads : (int)std::max(1u, std::thread::hardware_concurrency());
+        nthreads = std::min<int>(nthreads, (int)blocks.size());
+        std::vector<std::thread> pool;
+        std::atomic_size_t next{0};
+        auto work = [&]() {
+            for (size_t k; (k = next.fetch_add(1)) < blocks.size();)
+                ainv_block(ni, nj, P.periodic, c->cE, c->cN, c->sigma, c->mask, P.tau, blocks[k]);
+        };
+        for (int t = 1; t < nthreads; ++t) pool.emplace_back(work);
+        work();
+        for (auto& t : pool) t.join();
+    }
+    for (auto& b : blocks)
+        if (b.fail_grid >= 0) {
+            char buf[200];
+            snprintf(buf, sizeof buf, "pcg_setup: AINV pivot <= 1e-12 or not finite at grid point (i=%d, j=%d): "
+                     "A is not SPD to working precision", (int)(b.fail_grid % ni), (int)(b.fail_grid / ni));
+            return Status::err(PCG_ERR_NOT_SPD, buf, global_unknown(c->mask, ni, b.fail_grid));
+        }
+
+    // ---- owned columns in natural order: export + Z values z_kj = fl(s_k * zhat_kj)
+    auto arr_of = [&](int64_t gi) -> int64_t {        // grid index -> array index (owned / halo rows)
+        int32_t i = (int32_t)(gi % ni), j = (int32_t)(gi / ni);
+        return (int64_t)(j - P.jb + 1) * pitch + i;
+    };
+    P.zcolptr.assign(1, 0);
+    std::vector<int64_t> colarr;                 // array index of each owned column
+    std::vector<int64_t> ent_row_arr;            // per entry: array index of its row
+    std::vector<double> ent_z;                   // per entry: z value
+    std::vector<int64_t> gunk_cache;
+    // global unknown numbering of grid rows [min row_lo, je)
+    int32_t rlo = P.je;
+    for (auto& b : blocks) rlo = std::min(rlo, b.row_lo);
+    std::vector<int64_t> unk((size_t)(P.je - rlo) * ni, -1);
+    {
+        int64_t u = 0;
+        for (int64_t k = 0; k < (int64_t)rlo * ni; ++k) u += c->mask[k] ? 1 : 0;
+        for (int64_t k = (int64_t)rlo * ni; k < (int64_t)P.je * ni; ++k)
+            if (c->mask[k]) unk[k - (int64_t)rlo * ni] = u++;
+    }
+    P.nnz_off = 0;
+    for (auto& b : blocks) {
+        for (size_t q = 0; q < b.col_g.size(); ++q) {
+            for (int64_t e = b.colptr[q]; e < b.colptr[q + 1]; ++e) {
+                int64_t gr = b.row_g[e];
+                P.zrow.push_back(unk[gr - (int64_t)rlo * ni]);
+                P.zhat.push_back(b.zhat[e]);
+                double s = 1.0 / std::sqrt(diag_of(gr));
+                ent_z.push_back(s * b.zhat[e]);
+                ent_row_arr.push_back(arr_of(gr));
+            }
+            P.zcolptr.push_back((int64_t)P.zrow.size());
+            P.pivots.push_back(b.piv[q]);
+            P.scale.push_back(1.0 / std::sqrt(diag_of(b.col_g[q])));
+            colarr.push_back(arr_of(b.col_g[q]));
+            P.piv[colarr.back()] = b.piv[q];
+            P.nnz_off += (b.colptr[q + 1] - b.colptr[q]) - 1;
+        }
+    }
+    if ((int64_t)colarr.size() != P.n_owned) return Status::err(PCG_ERR_ARG, "internal: owned column count mismatch");
+    for (int64_t r : ent_row_arr)
+        if (r < pitch) return Status::err(PCG_ERR_ARG, "internal: Z entry outside the owned rows");
+
+    // ---- SELL of Z^T rows: row (column j of Z) = entries k ascending
+    const int64_t nown = P.owned_elements();
+    {
+        std::vector<int64_t> rp(nown + 1, 0);
+        for (size_t q = 0; q < colarr.size(); ++q) rp[colarr[q] - pitch + 1] = P.zcolptr[q + 1] - P.zcolptr[q];
+        for (int64_t e = 0; e < nown; ++e) rp[e + 1] += rp[e];
+        std::vector<int32_t> cols(rp[nown]);
+        std::vector<double> vals(rp[nown]);
+        for (size_t q = 0; q < colarr.size(); ++q) {
+            int64_t dst = rp[colarr[q] - pitch];
+            for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e, ++dst) {
+                cols[dst] = (int32_t)ent_row_arr[e];
+                vals[dst] = ent_z[e];
+            }
+        }
+        pack_sell(rp, cols, vals, nown, pitch, P.ZT);
+    }
+    // ---- SELL of Z rows: row i = entries z_ij over columns j ascending
+    {
+        std::vector<int64_t> rp(nown + 1, 0);
+        for (int64_t r : ent_row_arr) rp[r - pitch + 1]++;
+        for (int64_t e = 0; e < nown; ++e) rp[e + 1] += rp[e];
+        std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
+        std::vector<int32_t> cols(rp[nown]);
+        std::vector<double> vals(rp[nown]);
+        for (size_t q = 0; q < colarr.size(); ++q)        // columns visited in ascending order
+            for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e) {
+                int64_t r = ent_row_arr[e] - pitch;
+                cols[fill[r]] = (int32_t)colarr[q];
+                vals[fill[r]] = ent_z[e];
+                fill[r]++;
+            }
+        pack_sell(rp, cols, vals, nown, pitch, P.Z);
+    }
+    P.setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    return Status::ok();
+}
+
+}  // namespace pcg

@@ -1,0 +1,603 @@
+// solver.cu -- libpcg context, device memory, the solve driver (one CUDA graph with a
+// device-side WHILE node, or a host loop), and the C ABI of the context calls.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "kernels.h"
+
+using namespace pcg;
+
+namespace pcg {
+thread_local std::string g_last_error;
+void set_thread_error(const std::string& m) { g_last_error = m; }
+}  // namespace pcg
+
+struct pcg_ctx {
+    Plan plan;                         // host plan (SELL arrays are released after upload)
+    int device = 0;
+    cudaStream_t user_stream = nullptr, st = nullptr;
+    ncclComm_t comm = nullptr;
+    bool multi = false;
+    // device memory
+    std::vector<void*> allocs;
+    int64_t dev_bytes = 0;
+    double *cE = nullptr, *cN = nullptr, *sigma = nullptr, *diag = nullptr, *piv = nullptr;
+    double *x = nullptr, *b = nullptr, *q = nullptr, *t = nullptr, *s = nullptr, *r[2] = {}, *d[2] = {};
+    double *partial[3] = {}, *gath = nullptr, *hist = nullptr;
+    int64_t *zt_off = nullptr, *z_off = nullptr;
+    double *zt_val = nullptr, *z_val = nullptr;
+    int32_t *zt_col = nullptr, *z_col = nullptr;
+    DevScalars* sc = nullptr;
+    DevScalars* h_sc = nullptr;        // pinned
+    double* h_hist = nullptr;          // pinned
+    int32_t hist_cap = 0;
+    KArgs A{};
+    // graph
+    cudaGraphExec_t exec = nullptr;
+    bool graph_built = false;
+    cudaEvent_t ev_in = nullptr, ev0 = nullptr, ev1 = nullptr;
+    std::string err;
+    double bytes_k[3] = {0, 0, 0};
+    bool solved_once = false;
+};
+
+namespace {
+
+#define CU(call)                                                                                     \
+    do {                                                                                             \
+        cudaError_t e_ = (call);                                                                     \
+        if (e_ != cudaSuccess)                                                                       \
+            return Status::err(e_ == cudaErrorMemoryAllocation ? PCG_ERR_NOMEM : PCG_ERR_CUDA,       \
+                               std::string(#call) + ": " + cudaGetErrorString(e_));                  \
+    } while (0)
+
+#define NC(call)                                                                                     \
+    do {                                                                                             \
+        ncclResult_t r_ = (call);                                                                    \
+        if (r_ != ncclSuccess) return Status::err(PCG_ERR_COMM, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+template <class T>
+Status dalloc(pcg_ctx* c, T*& p, int64_t n) {
+    void* v = nullptr;
+    size_t bytes = (size_t)std::max<int64_t>(n, 1) * sizeof(T);
+    CU(cudaMalloc(&v, bytes));
+    CU(cudaMemsetAsync(v, 0, bytes, c->st));
+    c->allocs.push_back(v);
+    c->dev_bytes += (int64_t)bytes;
+    p = (T*)v;
+    return Status::ok();
+}
+
+template <class T>
+Status upload(pcg_ctx* c, T*& p, const std::vector<T>& h) {
+    if (Status s = dalloc(c, p, (int64_t)h.size()); !s) return s;
+    if (!h.empty()) CU(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, c->st));
+    CU(cudaStreamSynchronize(c->st));   // host vectors may be released afterwards
+    return Status::ok();
+}
+
+bool use_graph(const pcg_ctx* c) { return !c->multi && !(c->plan.flags & PCG_FLAG_HOST_LOOP); }
+
+// ---------------------------------------------------------------- NCCL steps (multi path)
+Status allgather_loc(pcg_ctx* c) {
+    NC(ncclAllGather((const void*)c->sc->loc, (void*)c->gath, 4, ncclDouble, c->comm, c->st));
+    return Status::ok();
+}
+
+Status halo(pcg_ctx* c, double* arr, bool with_allgather) {
+    const Plan& P = c->plan;
+    NC(ncclGroupStart());
+    if (with_allgather) NC(ncclAllGather((const void*)c->sc->loc, (void*)c->gath, 4, ncclDouble, c->comm, c->st));
+    if (P.nranks > 1) {
+        const size_t n = (size_t)P.pitch;
+        if (P.rank > 0) {
+            NC(ncclSend(arr + (size_t)1 * P.pitch, n, ncclDouble, P.rank - 1, c->comm, c->st));
+            NC(ncclRecv(arr, n, ncclDouble, P.rank - 1, c->comm, c->st));
+        }
+        if (P.rank < P.nranks - 1) {
+            NC(ncclSend(arr + (size_t)P.nloc * P.pitch, n, ncclDouble, P.rank + 1, c->comm, c->st));
+            NC(ncclRecv(arr + (size_t)(P.nloc + 1) * P.pitch, n, ncclDouble, P.rank + 1, c->comm, c->st));
+        }
+    }
+    NC(ncclGroupEnd());
+    return Status::ok();
+}
+
+// ---------------------------------------------------------------- one iteration / phases
+Status launch_prologue(pcg_ctx* c) {
+    const KArgs& A = c->A;
+    launch_prep(A, c->st);
+    if (c->multi) {
+        if (Status s = halo(c, c->x, false); !s) return s;
+        launch_init_residual(A, c->st);
+        if (Status s = allgather_loc(c); !s) return s;
+        launch_scalar(A, kSsBB, c->st);
+    } else {
+        launch_init_residual(A, c->st);
+    }
+    if (c->plan.precond == PCG_PRECOND_AINV) {
+        launch_k2_ainv(A, 1, 1, c->st);
+        launch_k3_ainv(A, 1, 1, c->st);
+    } else {
+        launch_k2_diag(A, 1, 1, c->plan.precond == PCG_PRECOND_NONE, c->st);
+    }
+    if (c->multi) {
+        if (Status s = halo(c, c->s, true); !s) return s;
+        launch_scalar(A, kSsInit, c->st);
+    }
+    CU(cudaGetLastError());
+    return Status::ok();
+}
+
+Status launch_iteration(pcg_ctx* c, int par) {
+    const KArgs& A = c->A;
+    launch_k1(A, par, c->st);
+    if (c->multi) {
+        if (Status s = allgather_loc(c); !s) return s;
+        launch_scalar(A, kSsGamma, c->st);
+    }
+    if (c->plan.precond == PCG_PRECOND_AINV) {
+        launch_k2_ainv(A, par, 0, c->st);
+        launch_k3_ainv(A, par, 0, c->st);
+    } else {
+        launch_k2_diag(A, par, 0, c->plan.precond == PCG_PRECOND_NONE, c->st);
+    }
+    if (c->multi) {
+        if (Status s = halo(c, c->s, true); !s) return s;
+        launch_scalar(A, kSsIter, c->st);
+    }
+    return Status::ok();
+}
+
+Status launch_epilogue(pcg_ctx* c) {
+    const KArgs& A = c->A;
+    launch_fin(A, c->st);
+    if (c->multi) {
+        if (Status s = halo(c, c->x, false); !s) return s;
+        launch_true_residual(A, c->st);
+        if (Status s = allgather_loc(c); !s) return s;
+        launch_scalar(A, kSsTrue, c->st);
+    } else {
+        launch_true_residual(A, c->st);
+    }
+    CU(cudaGetLastError());
+    return Status::ok();
+}
+
+// Whole solve as one graph: prologue -> WHILE(active){ iteration(0); iteration(1) } -> epilogue.
+Status build_graph(pcg_ctx* c) {
+    if (c->exec) { cudaGraphExecDestroy(c->exec); c->exec = nullptr; }
+    cudaStream_t body_st = nullptr;
+    CU(cudaStreamCreateWithFlags(&body_st, cudaStreamNonBlocking));
+    cudaGraph_t graph = nullptr, body = nullptr;
+    cudaGraphNode_t cnode;
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t* deps = nullptr;
+    size_t ndeps = 0;
+    Status st = Status::ok();
+    do {
+        if (cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            st = Status::err(PCG_ERR_CUDA, "graph capture begin failed"); break;
+        }
+        cudaGraph_t capg = nullptr;
+        if (cudaStreamGetCaptureInfo(c->st, &cs, nullptr, &capg, nullptr, nullptr) != cudaSuccess) {
+            st = Status::err(PCG_ERR_CUDA, "cudaStreamGetCaptureInfo failed"); break;
+        }
+        cudaGraphConditionalHandle h;
+        if (cudaGraphConditionalHandleCreate(&h, capg, 1, cudaGraphCondAssignDefault) != cudaSuccess) {
+            st = Status::err(PCG_ERR_CUDA, "cudaGraphConditionalHandleCreate failed"); break;
+        }
+        c->A.cond = h;
+        c->A.use_cond = 1;
+        if (!(st = launch_prologue(c))) break;
+        if (cudaStreamGetCaptureInfo(c->st, &cs, nullptr, &capg, &deps, &ndeps) != cudaSuccess) {
+            st = Status::err(PCG_ERR_CUDA, "cudaStreamGetCaptureInfo failed"); break;
+        }
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        if (cudaGraphAddNode(&cnode, capg, deps, ndeps, &cp) != cudaSuccess) {
+            st = Status::err(PCG_ERR_CUDA, "cudaGraphAddNode(conditional) failed"); break;
+        }
+        body = cp.conditional.phGraph_out[0];
+        if (cudaStreamUpdateCaptureDependencies(c->st, &cnode, 1, cudaStreamSetCaptureDependencies) != cudaSuccess) {
+            st = Status::err(PCG_ERR_CUDA, "cudaStreamUpdateCaptureDependencies failed"); break;
+        }
+        // body: two iterations (even / odd parity of the ping-pong buffers)
+        if (cudaStreamBeginCaptureToGraph(body_st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+            st = Status::err(PCG_ERR_CUDA, "body capture begin failed"); break;
+        }
+        {
+            cudaStream_t keep = c->st;
+            c->st = body_st;
+            Status s0 = launch_iteration(c, 0);
+            Status s1 = s0 ? launch_iteration(c, 1) : s0;
+            c->st = keep;
+            cudaGraph_t bg = nullptr;
+            cudaError_t e = cudaStreamEndCapture(body_st, &bg);
+            if (!s1) { st = s1; break; }
+            if (e != cudaSuccess) { st = Status::err(PCG_ERR_CUDA, std::string("body capture: ") + cudaGetErrorString(e)); break; }
+        }
+        if (!(st = launch_epilogue(c))) break;
+    } while (0);
+    cudaError_t e = cudaStreamEndCapture(c->st, &graph);
+    if (st && e != cudaSuccess) st = Status::err(PCG_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(e));
+    if (st) {
+        cudaError_t ie = cudaGraphInstantiate(&c->exec, graph, 0);
+        if (ie != cudaSuccess) st = Status::err(PCG_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie));
+    }
+    if (graph) cudaGraphDestroy(graph);
+    cudaStreamDestroy(body_st);
+    cudaGetLastError();
+    c->A.use_cond = 0;
+    c->graph_built = (bool)st;
+    return st;
+}
+
+Status ensure_hist(pcg_ctx* c, int32_t maxit) {
+    const int32_t need = maxit + 1;
+    if (need <= c->hist_cap) return Status::ok();
+    int32_t cap = std::max(need, 1024);
+    if (c->hist) { CU(cudaFree(c->hist)); c->allocs.erase(std::find(c->allocs.begin(), c->allocs.end(), (void*)c->hist)); c->dev_bytes -= (int64_t)c->hist_cap * 8; }
+    if (c->h_hist) CU(cudaFreeHost(c->h_hist));
+    c->hist = nullptr; c->h_hist = nullptr;
+    if (Status s = dalloc(c, c->hist, cap); !s) return s;
+    CU(cudaMallocHost(&c->h_hist, (size_t)cap * sizeof(double)));
+    c->hist_cap = cap;
+    c->A.hist = c->hist;
+    c->A.hist_cap = cap;
+    c->graph_built = false;            // kernel arguments changed
+    return Status::ok();
+}
+
+Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, double tol, int32_t maxit,
+                 double* x, int32_t* iterations, double* res_hist, int32_t hist_cap, pcg_report* report) {
+    const Plan& P = c->plan;
+    if (!(tol >= 0.0)) return Status::err(PCG_ERR_ARG, "pcg_solve: tol must be >= 0 and not NaN");
+    if (maxit < 0) return Status::err(PCG_ERR_ARG, "pcg_solve: maxit must be >= 0");
+    if (!b || !x) return Status::err(PCG_ERR_ARG, "pcg_solve: b and x are required");
+    if (res_hist && hist_cap < 1) return Status::err(PCG_ERR_ARG, "pcg_solve: hist_cap < 1 with res_hist");
+    CU(cudaSetDevice(c->device));
+    if (Status s = ensure_hist(c, maxit); !s) return s;
+    if (use_graph(c) && !c->graph_built) {
+        if (Status s = build_graph(c); !s) return s;
+    }
+    // order after the caller's stream
+    CU(cudaEventRecord(c->ev_in, c->user_stream));
+    CU(cudaStreamWaitEvent(c->st, c->ev_in, 0));
+    // scalars
+    std::memset(c->h_sc, 0, sizeof(DevScalars));
+    c->h_sc->tol = tol;
+    c->h_sc->maxit = maxit;
+    c->h_sc->active = 1;
+    CU(cudaEventRecord(c->ev0, c->st));
+    CU(cudaMemcpyAsync(c->sc, c->h_sc, sizeof(DevScalars), cudaMemcpyHostToDevice, c->st));
+    const cudaMemcpyKind kin = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    const cudaMemcpyKind kout = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    const size_t dp = (size_t)P.pitch * sizeof(double), sp = (size_t)P.ni * sizeof(double);
+    CU(cudaMemcpy2DAsync(c->b + P.pitch, dp, b, sp, sp, (size_t)P.nloc, kin, c->st));
+    if (x0) CU(cudaMemcpy2DAsync(c->x + P.pitch, dp, x0, sp, sp, (size_t)P.nloc, kin, c->st));
+    else CU(cudaMemsetAsync(c->x + P.pitch, 0, (size_t)P.nloc * dp, c->st));
+    if (use_graph(c)) {
+        CU(cudaGraphLaunch(c->exec, c->st));
+    } else {
+        if (Status s = launch_prologue(c); !s) return s;
+        // host loop: chunks of C iterations, two chunks in flight; kernels of a converged
+        // solve return immediately, so the iteration count is exact.
+        const int C = 8;
+        int32_t* flags = nullptr;
+        CU(cudaMallocHost(&flags, 2 * sizeof(int32_t)));
+        cudaEvent_t evc[2];
+        CU(cudaEventCreateWithFlags(&evc[0], cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&evc[1], cudaEventDisableTiming));
+        Status ls = Status::ok();
+        int64_t m = 0;
+        for (int64_t chunk = 0;; ++chunk) {
+            for (int k = 0; k < C && m < (int64_t)maxit; ++k, ++m)
+                if (!(ls = launch_iteration(c, (int)(m & 1)))) break;
+            if (!ls) break;
+            cudaMemcpyAsync(&flags[chunk & 1], &c->sc->active, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st);
+            cudaEventRecord(evc[chunk & 1], c->st);
+            if (m >= (int64_t)maxit) break;
+            if (chunk >= 1) {
+                cudaEventSynchronize(evc[(chunk - 1) & 1]);
+                if (flags[(chunk - 1) & 1] == 0) break;
+            }
+        }
+        cudaEventDestroy(evc[0]); cudaEventDestroy(evc[1]);
+        cudaStreamSynchronize(c->st);
+        cudaFreeHost(flags);
+        if (!ls) return ls;
+        if (Status s = launch_epilogue(c); !s) return s;
+    }
+    CU(cudaMemcpy2DAsync(x, sp, c->x + P.pitch, dp, sp, (size_t)P.nloc, kout, c->st));
+    CU(cudaEventRecord(c->ev1, c->st));
+    CU(cudaMemcpyAsync(c->h_sc, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    const DevScalars& S = *c->h_sc;
+    const int32_t k = S.k;
+    const int32_t nh = std::min(k + 1, c->hist_cap);
+    CU(cudaMemcpyAsync(c->h_hist, c->hist, (size_t)nh * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    CU(cudaStreamSynchronize(c->st));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    if (iterations) *iterations = k;
+    if (res_hist) std::memcpy(res_hist, c->h_hist, (size_t)std::min(nh, hist_cap) * sizeof(double));
+    pcg_report R{};
+    R.iterations = k;
+    R.rel_residual = c->h_hist[std::min(k, c->hist_cap - 1)];
+    R.converged = S.status == kStOk && R.rel_residual <= tol;
+    R.true_rel_residual = S.true_rel;
+    R.setup_s = P.setup_s;
+    R.solve_s = ms * 1e-3;
+    R.bytes_per_iter = c->bytes_k[0] + c->bytes_k[1] + c->bytes_k[2];
+    R.n_ocean = P.n_owned;
+    R.nnz_z = P.nnz_off;
+    R.failed_index = -1;
+    if (report) *report = R;
+    c->solved_once = true;
+    if (S.status == kStBreakdown)
+        return Status::err(PCG_ERR_BREAKDOWN, "pcg_solve: breakdown ((d,q) <= 0 or a non-finite reduction) at iteration " +
+                                                  std::to_string(k));
+    return Status::ok();
+}
+
+Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_ctx* c) {
+    if (Status s = build_plan(co, g, o, c->plan); !s) return s;
+    Plan& P = c->plan;
+    c->device = g->device;
+    c->user_stream = (cudaStream_t)g->stream;
+    c->multi = P.nranks > 1 || (P.flags & PCG_FLAG_COMM_PATH);
+    if (c->multi && !g->nccl_comm) return Status::err(PCG_ERR_ARG, "pcg_setup: nranks > 1 (or PCG_FLAG_COMM_PATH) needs nccl_comm");
+    c->comm = (ncclComm_t)g->nccl_comm;
+    CU(cudaSetDevice(c->device));
+    CU(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+    CU(cudaEventCreate(&c->ev0));
+    CU(cudaEventCreate(&c->ev1));
+    const int64_t nel = P.elements();
+    KArgs& A = c->A;
+    if (Status s = upload(c, c->cE, P.cE); !s) return s;
+    if (Status s = upload(c, c->cN, P.cN); !s) return s;
+    if (P.has_sigma) { if (Status s = upload(c, c->sigma, P.sigma); !s) return s; }
+    if (P.precond == PCG_PRECOND_JACOBI) { if (Status s = upload(c, c->diag, P.diag); !s) return s; }
+    if (P.precond == PCG_PRECOND_AINV) {
+        if (Status s = upload(c, c->piv, P.piv); !s) return s;
+        if (Status s = upload(c, c->zt_off, P.ZT.off); !s) return s;
+        if (Status s = upload(c, c->zt_val, P.ZT.val); !s) return s;
+        if (Status s = upload(c, c->zt_col, P.ZT.col); !s) return s;
+        if (Status s = upload(c, c->z_off, P.Z.off); !s) return s;
+        if (Status s = upload(c, c->z_val, P.Z.val); !s) return s;
+        if (Status s = upload(c, c->z_col, P.Z.col); !s) return s;
+    }
+    double** vecs[] = {&c->x, &c->b, &c->q, &c->t, &c->s, &c->r[0], &c->r[1], &c->d[0], &c->d[1]};
+    for (double** v : vecs) if (Status s = dalloc(c, *v, nel); !s) return s;
+    const int64_t G = (P.owned_elements() + kBlock - 1) / kBlock;
+    for (int k = 0; k < 3; ++k) if (Status s = dalloc(c, c->partial[k], G); !s) return s;
+    if (Status s = dalloc(c, c->gath, 4 * std::max(1, P.nranks)); !s) return s;
+    {
+        DevScalars* p = nullptr;
+        if (Status s = dalloc(c, p, 1); !s) return s;
+        c->sc = p;
+    }
+    CU(cudaMallocHost(&c->h_sc, sizeof(DevScalars)));
+    A.ni = P.ni; A.pitch = P.pitch; A.nloc = P.nloc; A.nranks = P.nranks; A.nel = P.owned_elements();
+    A.cE = c->cE; A.cN = c->cN; A.sigma = c->sigma; A.diag = c->diag; A.piv = c->piv;
+    A.zt_off = c->zt_off; A.z_off = c->z_off; A.zt_val = c->zt_val; A.z_val = c->z_val;
+    A.zt_col = c->zt_col; A.z_col = c->z_col;
+    A.x = c->x; A.b = c->b; A.q = c->q; A.t = c->t; A.s = c->s;
+    A.r[0] = c->r[0]; A.r[1] = c->r[1]; A.d[0] = c->d[0]; A.d[1] = c->d[1];
+    for (int k = 0; k < 3; ++k) A.partial[k] = c->partial[k];
+    A.gath = c->gath; A.sc = c->sc;
+    A.multi = c->multi ? 1 : 0;
+    A.use_cond = 0;
+    // algorithmic bytes per launch: N_o ocean points, z off-diagonals per column
+    const double No = (double)P.n_owned, z = No > 0 ? (double)P.nnz_off / No : 0.0;
+    c->bytes_k[0] = 64.0 * No;
+    if (P.precond == PCG_PRECOND_AINV) { c->bytes_k[1] = (48.0 + 12.0 * z) * No; c->bytes_k[2] = (32.0 + 12.0 * z) * No; }
+    else { c->bytes_k[1] = 40.0 * No; c->bytes_k[2] = 0.0; }
+    if (Status s = ensure_hist(c, 1023); !s) return s;
+    CU(cudaStreamSynchronize(c->st));
+    // release the bulky host copies
+    P.cE.clear(); P.cE.shrink_to_fit(); P.cN.clear(); P.cN.shrink_to_fit();
+    P.sigma.clear(); P.sigma.shrink_to_fit(); P.diag.clear(); P.diag.shrink_to_fit();
+    P.piv.clear(); P.piv.shrink_to_fit();
+    P.Z = Sell(); P.ZT = Sell();
+    P.zrow.clear(); P.zrow.shrink_to_fit(); P.zhat.clear(); P.zhat.shrink_to_fit();
+    if (use_graph(c)) { if (Status s = build_graph(c); !s) return s; }
+    return Status::ok();
+}
+
+pcg_status fail(pcg_ctx* c, const Status& s) {
+    if (c) c->err = s.msg;
+    set_thread_error(s.msg);
+    return s.code;
+}
+
+}  // namespace
+
+extern "C" {
+
+pcg_status pcg_setup(const pcg_coeffs* coeffs, const pcg_grid* grid, const pcg_opts* opts, pcg_ctx** out) {
+    if (!out) { set_thread_error("pcg_setup: out is NULL"); return PCG_ERR_ARG; }
+    *out = nullptr;
+    pcg_ctx* c = new (std::nothrow) pcg_ctx();
+    if (!c) { set_thread_error("pcg_setup: out of host memory"); return PCG_ERR_NOMEM; }
+    Status s;
+    try {
+        s = do_setup(coeffs, grid, opts, c);
+    } catch (const std::bad_alloc&) {
+        s = Status::err(PCG_ERR_NOMEM, "pcg_setup: out of host memory");
+    }
+    if (!s) {
+        set_thread_error(s.msg);
+        pcg_free(c);
+        return s.code;
+    }
+    set_thread_error("");
+    *out = c;
+    return PCG_OK;
+}
+
+pcg_status pcg_solve(pcg_ctx* c, const double* b, const double* x0, double tol, int32_t maxit, double* x,
+                     int32_t* iterations, double* res_hist, int32_t hist_cap, pcg_report* report) {
+    if (!c) { set_thread_error("pcg_solve: NULL context"); return PCG_ERR_ARG; }
+    Status s = run_solve(c, b, x0, false, tol, maxit, x, iterations, res_hist, hist_cap, report);
+    return s ? PCG_OK : fail(c, s);
+}
+
+pcg_status pcg_solve_host(pcg_ctx* c, const double* b, const double* x0, double tol, int32_t maxit, double* x,
+                          int32_t* iterations, double* res_hist, int32_t hist_cap, pcg_report* report) {
+    if (!c) { set_thread_error("pcg_solve_host: NULL context"); return PCG_ERR_ARG; }
+    Status s = run_solve(c, b, x0, true, tol, maxit, x, iterations, res_hist, hist_cap, report);
+    return s ? PCG_OK : fail(c, s);
+}
+
+void pcg_free(pcg_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->st) cudaStreamSynchronize(c->st);
+    if (c->exec) cudaGraphExecDestroy(c->exec);
+    for (void* p : c->allocs) cudaFree(p);
+    if (c->h_sc) cudaFreeHost(c->h_sc);
+    if (c->h_hist) cudaFreeHost(c->h_hist);
+    if (c->ev_in) cudaEventDestroy(c->ev_in);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->st) cudaStreamDestroy(c->st);
+    cudaGetLastError();
+    delete c;
+}
+
+const char* pcg_last_error(const pcg_ctx* c) { return c ? c->err.c_str() : pcg::g_last_error.c_str(); }
+
+pcg_status pcg_apply_operator(pcg_ctx* c, const double* x, double* y) {
+    if (!c || !x || !y) { set_thread_error("pcg_apply_operator: NULL argument"); return PCG_ERR_ARG; }
+    auto body = [&]() -> Status {
+        const Plan& P = c->plan;
+        CU(cudaSetDevice(c->device));
+        CU(cudaEventRecord(c->ev_in, c->user_stream));
+        CU(cudaStreamWaitEvent(c->st, c->ev_in, 0));
+        const size_t dp = (size_t)P.pitch * sizeof(double), sp = (size_t)P.ni * sizeof(double);
+        // stage x in t (zero rows/padding first so halos and padding read 0), result in q
+        CU(cudaMemsetAsync(c->t, 0, (size_t)(P.nloc + 2) * dp, c->st));
+        CU(cudaMemcpy2DAsync(c->t + P.pitch, dp, x, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
+        if (c->multi) if (Status s = halo(c, c->t, false); !s) return s;
+        launch_apply(c->A, c->t, c->q, c->st);
+        CU(cudaGetLastError());
+        CU(cudaMemcpy2DAsync(y, sp, c->q + P.pitch, dp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
+        CU(cudaStreamSynchronize(c->st));
+        return Status::ok();
+    };
+    Status s = body();
+    return s ? PCG_OK : fail(c, s);
+}
+
+pcg_status pcg_apply_preconditioner(pcg_ctx* c, const double* r, double* sout) {
+    if (!c || !r || !sout) { set_thread_error("pcg_apply_preconditioner: NULL argument"); return PCG_ERR_ARG; }
+    auto body = [&]() -> Status {
+        const Plan& P = c->plan;
+        if (c->multi) return Status::err(PCG_ERR_ARG, "pcg_apply_preconditioner: single rank only");
+        CU(cudaSetDevice(c->device));
+        CU(cudaEventRecord(c->ev_in, c->user_stream));
+        CU(cudaStreamWaitEvent(c->st, c->ev_in, 0));
+        const size_t dp = (size_t)P.pitch * sizeof(double), sp = (size_t)P.ni * sizeof(double);
+        // the init pass of K2/K3 (alpha = 0) computes s = P r from r[1], with q = 0
+        std::memset(c->h_sc, 0, sizeof(DevScalars));
+        c->h_sc->active = 1; c->h_sc->nb = 1.0; c->h_sc->maxit = 0;
+        CU(cudaMemcpyAsync(c->sc, c->h_sc, sizeof(DevScalars), cudaMemcpyHostToDevice, c->st));
+        CU(cudaMemsetAsync(c->q, 0, (size_t)(P.nloc + 2) * dp, c->st));
+        CU(cudaMemsetAsync(c->r[1], 0, (size_t)(P.nloc + 2) * dp, c->st));
+        CU(cudaMemcpy2DAsync(c->r[1] + P.pitch, dp, r, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
+        KArgs A = c->A;
+        A.use_cond = 0;
+        if (P.precond == PCG_PRECOND_AINV) { launch_k2_ainv(A, 1, 1, c->st); launch_k3_ainv(A, 1, 1, c->st); }
+        else launch_k2_diag(A, 1, 1, P.precond == PCG_PRECOND_NONE, c->st);
+        CU(cudaGetLastError());
+        CU(cudaMemcpy2DAsync(sout, sp, c->s + P.pitch, dp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
+        CU(cudaStreamSynchronize(c->st));
+        c->solved_once = false;
+        return Status::ok();
+    };
+    Status s = body();
+    return s ? PCG_OK : fail(c, s);
+}
+
+pcg_status pcg_layout(const pcg_ctx* c, int32_t* pitch, int32_t* block) {
+    if (!c) return PCG_ERR_ARG;
+    if (pitch) *pitch = c->plan.pitch;
+    if (block) *block = kBlock;
+    return PCG_OK;
+}
+
+int64_t pcg_device_bytes(const pcg_ctx* c) { return c ? c->dev_bytes : 0; }
+
+pcg_status pcg_kernel_times(pcg_ctx* c, int32_t n_iter, double* ms_out, double* bytes_out) {
+    if (!c || n_iter < 1 || !ms_out) { set_thread_error("pcg_kernel_times: bad argument"); return PCG_ERR_ARG; }
+    auto body = [&]() -> Status {
+        if (c->multi) return Status::err(PCG_ERR_ARG, "pcg_kernel_times: single rank only");
+        if (!c->solved_once) return Status::err(PCG_ERR_ARG, "pcg_kernel_times: call pcg_solve first (uses its b)");
+        CU(cudaSetDevice(c->device));
+        // restart from x = 0 on the stored b with tol = 0, time n_iter iterations kernel by kernel
+        std::memset(c->h_sc, 0, sizeof(DevScalars));
+        c->h_sc->tol = 0.0; c->h_sc->maxit = n_iter + 2; c->h_sc->active = 1;
+        CU(cudaMemcpyAsync(c->sc, c->h_sc, sizeof(DevScalars), cudaMemcpyHostToDevice, c->st));
+        CU(cudaMemsetAsync(c->x, 0, (size_t)c->plan.elements() * sizeof(double), c->st));
+        if (Status s = ensure_hist(c, n_iter + 2); !s) return s;
+        KArgs A = c->A;
+        A.use_cond = 0;
+        {
+            KArgs keep = c->A; c->A = A;
+            Status s = launch_prologue(c);
+            c->A = keep;
+            if (!s) return s;
+        }
+        std::vector<cudaEvent_t> ev(4 * n_iter);
+        for (auto& e : ev) CU(cudaEventCreate(&e));
+        const bool ainv = c->plan.precond == PCG_PRECOND_AINV;
+        for (int m = 0; m < n_iter; ++m) {
+            const int par = m & 1;
+            cudaEventRecord(ev[4 * m + 0], c->st);
+            launch_k1(A, par, c->st);
+            cudaEventRecord(ev[4 * m + 1], c->st);
+            if (ainv) launch_k2_ainv(A, par, 0, c->st);
+            else launch_k2_diag(A, par, 0, c->plan.precond == PCG_PRECOND_NONE, c->st);
+            cudaEventRecord(ev[4 * m + 2], c->st);
+            if (ainv) launch_k3_ainv(A, par, 0, c->st);
+            cudaEventRecord(ev[4 * m + 3], c->st);
+        }
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(c->st));
+        double acc[4] = {0, 0, 0, 0};
+        for (int m = 0; m < n_iter; ++m) {
+            float t01, t12, t23, t03;
+            cudaEventElapsedTime(&t01, ev[4 * m + 0], ev[4 * m + 1]);
+            cudaEventElapsedTime(&t12, ev[4 * m + 1], ev[4 * m + 2]);
+            cudaEventElapsedTime(&t23, ev[4 * m + 2], ev[4 * m + 3]);
+            cudaEventElapsedTime(&t03, ev[4 * m + 0], ev[4 * m + 3]);
+            acc[0] += t01; acc[1] += t12; acc[2] += t23; acc[3] += t03;
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        CU(cudaMemcpy(c->h_sc, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost));
+        if (c->h_sc->k < n_iter) return Status::err(PCG_ERR_BREAKDOWN, "pcg_kernel_times: iteration stopped early");
+        for (int k = 0; k < 4; ++k) ms_out[k] = acc[k] / n_iter;
+        if (bytes_out) for (int k = 0; k < 3; ++k) bytes_out[k] = c->bytes_k[k];
+        c->solved_once = false;            // x was overwritten
+        return Status::ok();
+    };
+    Status s = body();
+    return s ? PCG_OK : fail(c, s);
+}
+
+}  // extern "C"

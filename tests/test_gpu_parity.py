@@ -1,0 +1,213 @@
+"""GPU parity: libpcg's CUDA path (through the C ABI) against the independent CPU oracle.
+
+Bar (north star / SURVEY §8(c.4)):
+  * canonical order: the oracle re-implements the GPU's documented arithmetic order
+    (DESIGN.md §5), so operator, preconditioner, residual histories, iteration counts and x
+    must be BITWISE equal;
+  * plain order: iterations within +-max(2, 1 %), ||x_gpu - x_cpu||/||x_cpu|| <= 1e-9 at
+    tol 1e-12, final relative residual <= tol (recurrence and true).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_1210_1878_b200 as pcg
+from paper_1210_1878_b200 import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+INF = float("inf")
+TAU = 0.1 + 1e-9
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def setup_pair(p, precond="ainv", tau=TAU, **kw):
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, tau, parts=max(1, kw.get("ainv_parts", 0) or 1), halo=kw.get("ainv_halo", 0)) \
+        if precond == "ainv" else None
+    S = pcg.Solver(p.cE, p.cN, p.mask, periodic=p.periodic, tau=tau, precond=precond, sigma=p.sigma, **kw)
+    return A, M, S
+
+
+def rhs(A, p, seed=0):
+    return A.apply(A.from_grid(synth.xstar(p, seed)))
+
+
+# ------------------------------------------------------------------------- single operators
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "ragged"])
+def test_operator_bitwise(name):
+    p = synth.random_grid(45, 13, 3, sigma=True) if name == "ragged" else synth.config(name)
+    A, _, S = setup_pair(p, precond="jacobi")
+    x = A.from_grid(synth.xstar(p, 5))
+    y = host(S.apply_operator(dev(A.to_grid(x))))
+    ref = A.to_grid(A.apply_canonical(x))
+    assert np.array_equal(y, ref)
+    assert np.allclose(y, A.to_grid(A.apply(x)), rtol=1e-13, atol=1e-13 * np.abs(ref).max())
+    S.close()
+
+
+@pytest.mark.parametrize("tau", [0.0, TAU, 0.2 + 1e-9, INF])
+def test_preconditioner_bitwise(tau):
+    p = synth.config("cfg2") if tau != 0.0 else synth.config("cfg1")
+    A, M, S = setup_pair(p, tau=tau)
+    r = A.from_grid(synth.xstar(p, 7))
+    s = host(S.apply_preconditioner(dev(A.to_grid(r))))
+    assert np.array_equal(s, A.to_grid(M.apply_canonical(r)))
+    S.close()
+
+
+# ------------------------------------------------------------------------------- full solves
+def _canonical_pair(p, precond, tol, maxit=None, x0=None, tau=TAU, **kw):
+    A, M, S = setup_pair(p, precond, tau, **kw)
+    b = rhs(A, p)
+    parts = max(1, kw.get("ainv_parts", 0) or 1)
+    ref = oracle.pcg(A, b, precond, M, tol, maxit=maxit, x0=x0, mode="canonical", pitch=S.pitch, block=S.block)
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), None if x0 is None else dev(A.to_grid(x0)), tol=tol,
+                               maxit=maxit if maxit is not None else A.n)
+    return A, S, ref, host(xg), k, hist, rep, parts
+
+
+@pytest.mark.parametrize("name,precond", [("cfg1", "ainv"), ("cfg1", "jacobi"), ("cfg1", "none"),
+                                          ("cfg2", "ainv"), ("cfg2", "jacobi"), ("cfg3", "ainv")])
+def test_solve_bitwise_canonical(name, precond):
+    p = synth.config(name)
+    A, S, ref, x, k, hist, rep, _ = _canonical_pair(p, precond, 1e-10)
+    assert k == ref.iterations
+    assert np.array_equal(hist, ref.hist)
+    assert np.array_equal(x, A.to_grid(ref.x))
+    assert rep["converged"] == 1 and rep["rel_residual"] <= 1e-10
+    assert rep["true_rel_residual"] == ref.true_rel_residual
+    S.close()
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_solve_vs_plain_oracle(name):
+    """The north-star bar against the plain (sequential) oracle at tol 1e-12."""
+    p = synth.config(name)
+    A, M, S = setup_pair(p)
+    b = rhs(A, p)
+    ref = oracle.pcg(A, b, "ainv", M, 1e-12)
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-12, maxit=A.n)
+    x = A.from_grid(host(xg))
+    assert abs(k - ref.iterations) <= max(2, 0.01 * ref.iterations)
+    assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) <= 1e-9
+    assert rep["rel_residual"] <= 1e-12 and rep["true_rel_residual"] <= 1.5e-12
+    xs = A.from_grid(synth.xstar(p))
+    assert np.linalg.norm(x - xs) / np.linalg.norm(xs) < 1e-7
+    S.close()
+
+
+@pytest.mark.parametrize("kind", ["sigma_nonperiodic", "ragged_small", "tiny"])
+def test_solve_bitwise_edge_grids(kind):
+    if kind == "sigma_nonperiodic":
+        p = synth.random_grid(70, 33, 11, periodic=False, sigma=True)
+    elif kind == "ragged_small":
+        p = synth.random_grid(33, 9, 12)
+    else:
+        p = synth.random_grid(3, 3, 13, land_frac=0.0)
+        p.mask[1, :] = 1
+    A, S, ref, x, k, hist, rep, _ = _canonical_pair(p, "ainv", 1e-12)
+    assert k == ref.iterations and np.array_equal(hist, ref.hist)
+    assert np.array_equal(x, A.to_grid(ref.x))
+    S.close()
+
+
+@pytest.mark.parametrize("parts,halo", [(4, 0), (4, 3), (8, 2)])
+def test_partitioned_preconditioner_bitwise(parts, halo):
+    """One GPU running the preconditioner the P-rank job builds (reading R15)."""
+    p = synth.config("cfg2")
+    A, S, ref, x, k, hist, rep, _ = _canonical_pair(p, "ainv", 1e-10, ainv_parts=parts, ainv_halo=halo)
+    assert k == ref.iterations and np.array_equal(hist, ref.hist)
+    assert np.array_equal(x, A.to_grid(ref.x))
+    S.close()
+
+
+def test_host_loop_and_comm_path_match_graph():
+    p = synth.config("cfg2")
+    A, M, S = setup_pair(p)
+    b = dev(A.to_grid(rhs(A, p)))
+    x0, k0, h0, _ = S.solve(b, tol=1e-10, maxit=A.n)
+    S.close()
+    for extra in ({"flags": pcg.FLAG_HOST_LOOP}, {"comm_path": True}):
+        S2 = pcg.Solver(p.cE, p.cN, p.mask, tau=TAU, **extra)
+        x1, k1, h1, _ = S2.solve(b, tol=1e-10, maxit=A.n)
+        assert k1 == k0 and np.array_equal(h1, h0) and torch.equal(x1, x0)
+        S2.close()
+
+
+def test_edge_cases():
+    p = synth.config("cfg2")
+    A, M, S = setup_pair(p)
+    b = rhs(A, p)
+    bz = dev(np.zeros((p.nj, p.ni)))
+    x, k, hist, rep = S.solve(bz, tol=1e-10)                          # b = 0 -> x = 0, 0 iterations
+    assert k == 0 and float(x.abs().max()) == 0.0 and rep["converged"] == 1
+    xs = A.to_grid(np.linalg.solve(A.dense(), b)) if A.n < 3000 else None
+    bd = dev(A.to_grid(b))
+    x, k, hist, rep = S.solve(bd, tol=1e-14, maxit=5)                 # maxit hit
+    assert k == 5 and rep["converged"] == 0
+    x, k, hist, rep = S.solve(bd, tol=0.0, maxit=17)                  # tol = 0: exactly maxit
+    assert k == 17 and len(hist) == 18
+    ref = oracle.pcg(A, b, "ainv", M, 1e-10)
+    x1, k1, _, _ = S.solve(bd, dev(A.to_grid(ref.x)), tol=1e-10)      # x0 = solution -> ~0 its
+    assert k1 <= 1
+    xg, k, _, _ = S.solve(bd, tol=1e-10, maxit=0)                      # maxit = 0
+    assert k == 0
+    with pytest.raises(pcg.PcgError) as e:
+        S.solve(bd, tol=-1.0)
+    assert e.value.code == "ERR_ARG"
+    land = (p.mask == 0)
+    bl = A.to_grid(b); bl[land] = 1e300                                # b on land is ignored
+    xl, kl, hl, _ = S.solve(dev(bl), tol=1e-10)
+    xr, kr, hr, _ = S.solve(bd, tol=1e-10)
+    assert kl == kr and torch.equal(xl, xr) and float(xl.cpu().numpy()[land].max(initial=0)) == 0.0
+    S.close()
+    del xs
+
+
+def test_setup_errors_on_gpu():
+    q = synth.singular_channel(16, 6, 3)
+    with pytest.raises(pcg.PcgError) as e:
+        pcg.Solver(q.cE, q.cN, q.mask)
+    assert e.value.code == "ERR_NOT_SPD"
+
+
+def test_solve_host_buffers():
+    p = synth.config("cfg2")
+    A, M, S = setup_pair(p)
+    b = A.to_grid(rhs(A, p))
+    xh, kh, hh, _ = S.solve_host(np.ascontiguousarray(b), tol=1e-10)
+    xd, kd, hd, _ = S.solve(dev(b), tol=1e-10)
+    assert kh == kd and np.array_equal(hh, hd) and np.array_equal(xh, host(xd))
+    S.close()
+
+
+# --------------------------------------------------------------- full-size (cfg4) sampled
+def test_cfg4_full_size_sampled():
+    """At BASELINE's full size the oracle cannot run 1300 canonical iterations inside a test,
+    so: operator and preconditioner bitwise on the full grid, the first 5 iterations bitwise
+    (history and x), then the full solve's properties (converged, true residual, error vs x*)."""
+    p = synth.config("cfg4")
+    A, M, S = setup_pair(p)
+    xs = A.from_grid(synth.xstar(p))
+    b = A.apply(xs)
+    y = host(S.apply_operator(dev(A.to_grid(xs))))
+    assert np.array_equal(y, A.to_grid(A.apply_canonical(xs)))
+    s = host(S.apply_preconditioner(dev(A.to_grid(b))))
+    assert np.array_equal(s, A.to_grid(M.apply_canonical(b)))
+    ref = oracle.pcg(A, b, "ainv", M, 0.0, maxit=5, mode="canonical", pitch=S.pitch, block=S.block)
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=0.0, maxit=5)
+    assert k == 5 and np.array_equal(hist, ref.hist) and np.array_equal(host(xg), A.to_grid(ref.x))
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
+    assert rep["converged"] == 1 and rep["true_rel_residual"] < 2e-10
+    assert 1200 <= k <= 1420                                             # ~1300
+    x = A.from_grid(host(xg))
+    assert np.linalg.norm(x - xs) / np.linalg.norm(xs) < 5e-6
+    S.close()
