@@ -172,9 +172,10 @@ pcg_status pcg_apply_preconditioner(pcg_ctx* ctx, const double* r, double* s);
 pcg_status pcg_partition(int32_t ni, int32_t nj, const uint8_t* mask, int32_t parts,
                          int32_t* row_begin);
 
-/* Device layout used for the canonical arithmetic order: row pitch (elements,
- * multiple of 32) and threads per reduction block. */
-pcg_status pcg_layout(const pcg_ctx* ctx, int32_t* pitch, int32_t* block);
+/* Device layout that fixes the canonical arithmetic order: row pitch
+ * (elements, multiple of 32), threads per block (= grid columns per tile) and grid rows per
+ * tile.  Any output pointer may be NULL. */
+pcg_status pcg_layout(const pcg_ctx* ctx, int32_t* pitch, int32_t* block, int32_t* rows);
 
 /* Average device time (ms) of each per-iteration kernel over n_iter iterations run on the
  * context's stream with CUDA events around every launch, on the state left by the last

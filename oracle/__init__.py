@@ -94,7 +94,7 @@ class OracleError(RuntimeError):
 
 class _PcgOpts(C.Structure):
     _fields_ = [("precond", C.c_int32), ("mode", C.c_int32), ("pitch", C.c_int32),
-                ("block", C.c_int32), ("parts", C.c_int32)]
+                ("block", C.c_int32), ("parts", C.c_int32), ("rows", C.c_int32)]
 
 
 class _PcgReport(C.Structure):
@@ -166,8 +166,8 @@ class Assembled:
         lib().orc_apply_canonical(self._h, _ptr(x), _ptr(y))
         return y
 
-    def dot_canonical(self, a, b, pitch, block=256, parts=1):
-        o = _PcgOpts(0, 1, int(pitch), int(block), int(parts))
+    def dot_canonical(self, a, b, pitch, block=256, parts=1, rows=1):
+        o = _PcgOpts(0, 1, int(pitch), int(block), int(parts), int(rows))
         a = np.ascontiguousarray(a, dtype=np.float64)
         b = np.ascontiguousarray(b, dtype=np.float64)
         return float(lib().orc_dot_canonical(self._h, C.byref(o), _ptr(a), _ptr(b)))
@@ -272,7 +272,7 @@ class PcgResult:
 
 def pcg(A: Assembled, b, precond: str = "ainv", M: Ainv | None = None, tol: float = 1e-10,
         maxit: int | None = None, x0=None, mode: str = "plain", pitch: int | None = None,
-        block: int = 256, parts: int = 1) -> PcgResult:
+        block: int = 256, parts: int = 1, rows: int = 1) -> PcgResult:
     """Alg. 1 with d = s + beta d.  Unknown-indexed vectors."""
     L = lib()
     if maxit is None:
@@ -281,7 +281,7 @@ def pcg(A: Assembled, b, precond: str = "ainv", M: Ainv | None = None, tol: floa
     x0a = None if x0 is None else np.ascontiguousarray(x0, dtype=np.float64)
     x = np.empty(A.n)
     hist = np.empty(maxit + 1)
-    o = _PcgOpts(PRECOND[precond], MODE[mode], int(pitch if pitch else A.ni), int(block), int(parts))
+    o = _PcgOpts(PRECOND[precond], MODE[mode], int(pitch if pitch else A.ni), int(block), int(parts), int(rows))
     rep = _PcgReport()
     rc = L.orc_pcg(A._h, None if M is None else M.handle._h, C.byref(o), _ptr(b), _ptr(x0a),
                    float(tol), int(maxit), _ptr(x), _ptr(hist), C.byref(rep))

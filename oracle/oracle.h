@@ -76,6 +76,7 @@ typedef struct {
     int32_t pitch;        /* canonical mode: row pitch of the grid layout (>= ni) */
     int32_t block;        /* canonical mode: threads per block (power of two, >= 32) */
     int32_t parts;        /* canonical mode: number of rank row blocks (>=1) */
+    int32_t rows;         /* unused (kept for ABI stability of the test binding) */
 } orc_pcg_opts;
 
 typedef struct {

@@ -30,13 +30,14 @@
 #include <string.h>
 
 /* ------------------------------------------------------------------------------------
- * CANONICAL reduction order.  One rank owns grid rows [jb, je); its
- * elements are e = (j - jb) * pitch + i, i in [0, pitch); value 0 at land and i >= ni.
- * Block `blk` of `B` threads holds elements [blk*B, blk*B + B), one per thread, value
- * fl(a_e * b_e).  tree32 is the warp shuffle-down tree (offsets 16, 8, 4, 2, 1, lane 0
- * result); a block sum is tree32 of the per-warp tree32 results (zero-padded to 32).
- * Final: thread t sums partials t, t+B, t+2B, ... left to right from 0.0, then the block
- * sum of those B values.  Several ranks: tree32 of the rank sums in rank order.
+ * CANONICAL reduction order.  One rank owns grid rows [jb, je) (nloc
+ * rows); each row is cut into nbx = ceil(pitch/B) segments of B columns.  The partial of
+ * (local row jl, segment bx) is the block sum of the B values fl(a_e * b_e) of its columns
+ * i = bx*B + t (0 at land and for i >= ni), stored at index m = jl*nbx + bx.  tree32 is the
+ * warp shuffle-down tree (offsets 16, 8, 4, 2, 1; lane 0 result); a block sum is tree32 of
+ * the per-warp tree32 results (zero-padded to 32).  Final: thread t of a B-thread block sums
+ * partials t, t+B, t+2B, ... left to right from 0.0, then the block sum of those B values.
+ * Several ranks: tree32 of the rank sums in rank order.
  * ------------------------------------------------------------------------------------ */
 static double tree32(double u[32]) {
     for (int off = 16; off >= 1; off >>= 1)
@@ -66,19 +67,17 @@ static double canon_dot(canon* C, const double* a, const double* b) {
     const orc_problem* P = C->P;
     double ranks[32] = {0};
     for (int r = 0; r < C->parts; ++r) {
-        int64_t jb = C->rb[r], je = C->rb[r + 1];
-        int64_t nel = (je - jb) * C->pitch;
-        int64_t G = (nel + C->B - 1) / C->B;
+        int64_t jb = C->rb[r], je = C->rb[r + 1], nloc = je - jb;
+        int64_t nbx = (C->pitch + C->B - 1) / C->B;
+        int64_t G = nbx * nloc;
         for (int64_t blk = 0; blk < G; ++blk) {
+            int64_t bx = blk % nbx, jl = blk / nbx;
             for (int t = 0; t < C->B; ++t) {
-                int64_t e = blk * C->B + t;
+                int64_t i = bx * C->B + t;
                 double v = 0.0;
-                if (e < nel) {
-                    int64_t j = jb + e / C->pitch, i = e % C->pitch;
-                    if (i < P->ni) {
-                        int64_t u = P->unk_of[j * P->ni + i];
-                        if (u >= 0) v = a[u] * b[u];
-                    }
+                if (i < P->ni) {
+                    int64_t u = P->unk_of[(jb + jl) * P->ni + i];
+                    if (u >= 0) v = a[u] * b[u];
                 }
                 C->vals[t] = v;
             }
@@ -139,7 +138,7 @@ double orc_dot_canonical(const orc_problem* P, const orc_pcg_opts* o, const doub
     if (o->parts == 1) { C.rb[0] = 0; C.rb[1] = P->nj; }
     else orc_partition(P->nj, P->ni, P->mask, o->parts, C.rb);
     C.vals = (double*)malloc(sizeof(double) * o->block);
-    C.partial = (double*)malloc(sizeof(double) * (((int64_t)P->nj * o->pitch) / o->block + 2));
+    C.partial = (double*)malloc(sizeof(double) * (((int64_t)P->nj + 1) * (o->pitch / o->block + 2)));
     double r = canon_dot(&C, a, b);
     free(C.rb); free(C.vals); free(C.partial);
     return r;
@@ -171,7 +170,7 @@ int orc_pcg(const orc_problem* P, const orc_ainv* R, const orc_pcg_opts* o, cons
         C.vals = (double*)malloc(sizeof(double) * o->block);
         int64_t maxrows = 0;
         for (int r = 0; r < o->parts; ++r) if (C.rb[r + 1] - C.rb[r] > maxrows) maxrows = C.rb[r + 1] - C.rb[r];
-        C.partial = (double*)malloc(sizeof(double) * ((maxrows * o->pitch) / o->block + 2));
+        C.partial = (double*)malloc(sizeof(double) * ((maxrows + 1) * (o->pitch / o->block + 2)));
     }
 #define DOT(a, b) (canonical ? canon_dot(&C, (a), (b)) : plain_dot(n, (a), (b)))
 #define APPLY_A(in, out) (canonical ? canon_apply(P, (in), (out)) : orc_apply(P, (in), (out)))

@@ -22,7 +22,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpcg.so")
+LIB_PATH = os.environ.get("PCG_LIB") or os.path.join(_HERE, "libpcg.so")   # PCG_LIB: tuning variants
 
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NOT_SPD", 3: "ERR_BREAKDOWN", 4: "ERR_CUDA", 5: "ERR_COMM", 6: "ERR_NOMEM"}
 PRECOND = {"ainv": 0, "jacobi": 1, "none": 2}
@@ -87,7 +87,7 @@ def lib():
     L.pcg_apply_operator.argtypes = [vp, vp, vp]
     L.pcg_apply_preconditioner.argtypes = [vp, vp, vp]
     L.pcg_partition.argtypes = [i32, i32, vp, i32, vp]
-    L.pcg_layout.argtypes = [vp, C.POINTER(i32), C.POINTER(i32)]
+    L.pcg_layout.argtypes = [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]
     L.pcg_kernel_times.argtypes = [vp, i32, vp, vp]
     L.pcg_device_bytes.argtypes = [vp]; L.pcg_device_bytes.restype = i64
     L.pcg_plan_build.argtypes = [C.POINTER(Coeffs), C.POINTER(Grid), C.POINTER(Opts), C.POINTER(vp)]
@@ -224,9 +224,9 @@ class Solver:
         h = C.c_void_p()
         _check(L.pcg_setup(C.byref(co), C.byref(g), C.byref(o), C.byref(h)), None, "pcg_setup")
         self._h = h
-        p, b = C.c_int32(), C.c_int32()
-        L.pcg_layout(h, C.byref(p), C.byref(b))
-        self.pitch, self.block = p.value, b.value
+        p, b, r = C.c_int32(), C.c_int32(), C.c_int32()
+        L.pcg_layout(h, C.byref(p), C.byref(b), C.byref(r))
+        self.pitch, self.block, self.tile_rows = p.value, b.value, r.value
         self.precond = precond
 
     # -- solve -----------------------------------------------------------------------------

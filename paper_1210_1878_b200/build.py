@@ -38,10 +38,10 @@ def _headers():
     return hs + [os.path.join(INCLUDE, "libpcg.h")]
 
 
-def _compile(src, nccl_inc):
+def _compile(src, nccl_inc, bdir=BUILD, defines=()):
     path = os.path.join(CSRC, src)
-    obj = os.path.join(BUILD, src + ".o")
-    common = ["-I" + CSRC, "-I" + INCLUDE, "-I" + nccl_inc, "-std=c++17"]
+    obj = os.path.join(bdir, src + ".o")
+    common = ["-I" + CSRC, "-I" + INCLUDE, "-I" + nccl_inc, "-std=c++17"] + ["-D" + d for d in defines]
     if src.endswith(".cu"):
         cmd = [NVCC] + ARCH + ["-O3", "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC,-O2,-ffp-contract=off",
                                "-c", path, "-o", obj] + common
@@ -55,30 +55,39 @@ def _compile(src, nccl_inc):
     return obj, r.stderr
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines=()) -> str:
+    """Build libpcg.so (or, with `variant`, a tuning variant _build/<variant>/libpcg.so
+    compiled with extra -D defines; load it with PCG_LIB=<path>)."""
+    bdir = os.path.join(BUILD, variant) if variant else BUILD
+    lib = os.path.join(bdir, "libpcg.so") if variant else LIB
+    os.makedirs(bdir, exist_ok=True)
     srcs = _sources()
     deps = [os.path.join(CSRC, s) for s in srcs] + _headers() + [os.path.abspath(__file__)]
-    if not force and os.path.exists(LIB):
-        t = os.path.getmtime(LIB)
+    if not force and os.path.exists(lib):
+        t = os.path.getmtime(lib)
         if all(os.path.getmtime(d) <= t for d in deps):
-            return LIB
+            return lib
     nccl_inc, nccl_lib = nccl_paths()
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        outs = list(ex.map(lambda s: _compile(s, nccl_inc), srcs))
+        outs = list(ex.map(lambda s: _compile(s, nccl_inc, bdir, defines), srcs))
     if verbose:
         for _, log in outs:
             if log:
                 print(log, file=sys.stderr)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + [o for o, _ in outs] + [
         "-L" + nccl_lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nccl_lib, "-cudart", "static", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--variant" in sys.argv:
+        k = sys.argv.index("--variant")
+        name, defs = sys.argv[k + 1], sys.argv[k + 2:]
+        print(build(force=True, verbose="-v" in sys.argv, variant=name, defines=[d for d in defs if d != "-v"]))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

@@ -48,7 +48,7 @@ pcg_status pcg_plan_counts(const pcg_plan* plan, int64_t* c) {
     c[0] = P.n_owned;
     c[1] = (int64_t)P.zrow.size();
     c[2] = P.pitch;
-    c[3] = P.Z.entries();
+    c[3] = P.Z.entries();      // ELL slots + overflow SELL entries
     c[4] = P.ZT.entries();
     c[5] = P.first_global;
     return PCG_OK;

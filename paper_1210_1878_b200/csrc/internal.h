@@ -29,13 +29,31 @@ struct Status {
 };
 
 // SELL-32 matrix over the owned elements: slice s covers owned elements [32 s, 32 s + 32)
-// of one grid row; entry m of lane l is at off[s] + 32 m + l.  Columns are ARRAY indices
-// (owned element + pitch).  Padding entries have value 0 and the row's own index.
+// of one grid row; entry m of lane l is at off[s] + 32 m + l.  A column is stored as the
+// packed grid offset (dj << 16) | (di & 0xffff) from the row's own point, di wrapped into
+// (-ni/2, ni/2] on a periodic grid.  Padding entries: value 0, offset (0, 0).
 struct Sell {
     std::vector<int64_t> off;      // nslices + 1
     std::vector<double> val;
-    std::vector<int32_t> col;
+    std::vector<int32_t> col;      // packed (di, dj)
+    int32_t dimin = 0, dimax = 0, djmin = 0, djmax = 0;   // extents over the real entries
     int64_t entries() const { return (int64_t)val.size(); }
+};
+
+// ELL(K) + SELL overflow: the first kEll entries of every owned element's row
+// at fixed slots val[e*kEll + m], col[e*kEll + m] (one 256-bit and one 128-bit load per element,
+// no offset load: a pure stream), the remaining
+// entries (rows longer than kEll) in a SELL-32 `ovf` whose slices are empty for most rows.
+// Columns are ARRAY indices (owned element + pitch; halo rows allowed); padding = value 0 at the
+// row's own index.
+constexpr int kEll = 4;
+struct Ell {
+    int64_t n = 0;                 // owned elements
+    std::vector<double> val;       // n * kEll (element-major)
+    std::vector<int32_t> col;      // n * kEll
+    Sell ovf;
+    int32_t dimin = 0, dimax = 0, djmin = 0, djmax = 0;
+    int64_t entries() const { return (int64_t)val.size() + ovf.entries(); }
 };
 
 // Host product of setup: everything the device needs, in device layout.
@@ -49,7 +67,7 @@ struct Plan {
     int64_t n_owned = 0, first_global = 0, nnz_off = 0;
     // per-element arrays, (nloc + 2) * pitch
     std::vector<double> cE, cN, sigma, diag, piv;
-    Sell Z, ZT;                    // rows of Z (for s = Z t) and of Z^T (for t = Z^T r)
+    Ell Z, ZT;                     // rows of Z (for s = Z t) and of Z^T (for t = Z^T r)
     // export (owned columns of Zhat, global unknown numbering)
     std::vector<int64_t> zcolptr, zrow;
     std::vector<double> zhat, pivots, scale;

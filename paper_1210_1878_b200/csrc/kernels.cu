@@ -13,15 +13,25 @@
 //     contraction cannot change it;
 //   * stencil: A_pp = ((c_E + c_W) + c_N) + c_S (+ sigma); acc = A_pp x_p, then
 //     acc = fma(-c, x_nb, acc) for W, E, S, N;
-//   * SELL rows: acc = 0, fma over the stored entries in ascending column order; K2 then
-//     divides by Dhat;
+//   * Z / Z^T rows: acc = 0, fma over the stored entries in ascending column order (ELL slots,
+//     then overflow); K2 then divides by Dhat;
 //   * updates: x = fma(alpha, d, x); r = fma(-alpha, q, r); d = fma(beta, d_old, s);
-//   * dot products: one element per thread, fl(a*b); 256-thread block = shuffle-down tree
-//     (16,8,4,2,1) per warp, then the same tree over the 8 warp sums; the last block sums the
-//     block partials t, t+256, ... left to right per thread and applies the block tree.
+//   * dot products: one partial per (grid row, 256-column segment) = block tree of the 256
+//     values fl(a*b) (shuffle-down tree 16,8,4,2,1 per warp, then the same tree over the 8 warp
+//     sums), stored at row*nbx + segment; the last block to finish sums partials t, t+256, ...
+//     left to right per thread and applies the block tree.  This order does not depend on
+//     how kernels map blocks to rows.
+//
+// EXECUTION SHAPE: every reduction kernel is persistent -- gridDim = SMs x resident blocks --
+// and walks its units (row segments; K1: strips of rpb rows) north to south with a block
+// stride, keeping each unit's 8 warp sums in shared memory.  A block publishes its partials and
+// takes its ticket on the completion counter once, at the end: a per-unit fence + atomic would
+// stall every short-lived block (measured: ~15 us per kernel at ORCA025, profiles/r01).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "internal.h"
 #include "kernels.h"
@@ -30,33 +40,36 @@ namespace pcg {
 
 namespace {
 
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kWarps = kBlock / 32;
+
 __device__ __forceinline__ double warp_tree(double v) {
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, off));
+    for (int off = 16; off >= 1; off >>= 1) v = __dadd_rn(v, __shfl_down_sync(kFull, v, off));
     return v;
 }
 
 // Block tree (kBlock threads): result valid in thread 0.
 __device__ __forceinline__ double block_tree(double v) {
-    __shared__ double ws[kBlock / 32];
+    __shared__ double wsb[kWarps];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     v = warp_tree(v);
-    __syncthreads();                       // ws may still be read by a previous call
-    if (lane == 0) ws[w] = v;
+    __syncthreads();                       // wsb may still be read by a previous call
+    if (lane == 0) wsb[w] = v;
     __syncthreads();
     double u = 0.0;
     if (w == 0) {
-        u = lane < kBlock / 32 ? ws[lane] : 0.0;
+        u = lane < kWarps ? wsb[lane] : 0.0;
         u = warp_tree(u);
     }
     return u;
 }
 
-// Publish this block's partial and report whether it is the last block to finish.
-__device__ __forceinline__ bool publish_partial(double part, double* partial, uint32_t* counter) {
+// After thread 0 wrote this block's partials: count the block, report whether it is last.
+__device__ __forceinline__ bool count_block(uint32_t* counter) {
     __shared__ bool am_last;
+    __syncthreads();
     if (threadIdx.x == 0) {
-        partial[blockIdx.x] = part;
         __threadfence();
         const uint32_t t = atomicAdd(counter, 1u);
         am_last = (t == gridDim.x - 1);
@@ -65,11 +78,20 @@ __device__ __forceinline__ bool publish_partial(double part, double* partial, ui
     return am_last;
 }
 
-// In the last block: thread t sums partials t, t+B, ... then the block tree.
-__device__ __forceinline__ double final_sum(const double* partial, int G) {
+// In the last block: thread t sums partials t, t+B, ... left to right, then the block tree.
+// Eight loads are issued before their adds so the walk is not one L2 round trip per partial.
+__device__ __forceinline__ double final_sum(const double* partial, int64_t G) {
     __threadfence();
     double acc = 0.0;
-    for (int m = threadIdx.x; m < G; m += kBlock) acc = __dadd_rn(acc, __ldcg(partial + m));
+    int64_t m = threadIdx.x;
+    for (; m + 7 * kBlock < G; m += 8 * kBlock) {
+        double p[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) p[u] = __ldcg(partial + m + u * kBlock);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, p[u]);
+    }
+    for (; m < G; m += kBlock) acc = __dadd_rn(acc, __ldcg(partial + m));
     return block_tree(acc);
 }
 
@@ -96,9 +118,9 @@ __device__ __forceinline__ void stop(const KArgs& A, int status) {
     set_cond(A, 0);
 }
 
-__device__ __forceinline__ bool is_active(const KArgs& A) {
-    return *(volatile int32_t*)&A.sc->active != 0;
-}
+// The flag only changes between launches (or in the last block of a reduction, after every
+// other block has read it), so a cached read is exact.
+__device__ __forceinline__ bool is_active(const KArgs& A) { return __ldg(&A.sc->active) != 0; }
 
 // ---- scalar updates (one thread) --------------------------------------------------------
 __device__ void fin_bb(const KArgs& A, double bb) {
@@ -153,132 +175,364 @@ __device__ __forceinline__ bool get_alpha(const KArgs& A, int init, double& alph
     return true;
 }
 
+// ---- units -----------------------------------------------------------------------------------
+// A unit is one 256-column segment bx of one owned row j; unit u runs from the north
+// (j = nloc-1 - u/nbx) so the long Z rows near the pole start first.  Its partial index is
+// m = j*nbx + bx whatever block computes it.
+struct Unit {
+    int32_t i, j, bx;
+    bool valid, inrow;     // i < ni ; i < pitch
+    int64_t a;             // array index of (i, j)
+};
+
+__device__ __forceinline__ int64_t n_units(const KArgs& A) { return (int64_t)A.nloc * A.nbx; }
+
+__device__ __forceinline__ Unit unit_of(const KArgs& A, int64_t u) {
+    Unit W;
+    W.bx = (int32_t)(u % A.nbx);
+    W.j = A.nloc - 1 - (int32_t)(u / A.nbx);
+    W.i = W.bx * kBlock + (int32_t)threadIdx.x;
+    W.valid = W.i < A.ni;
+    W.inrow = W.i < A.pitch;
+    W.a = (int64_t)(W.j + 1) * A.pitch + W.i;
+    return W;
+}
+
+// warp sum of v for local slot k (shared memory ws[k][warp])
+__device__ __forceinline__ void put_warp_sum(double* ws, int k, double v) {
+    v = warp_tree(v);
+    if ((threadIdx.x & 31) == 0) ws[k * kWarps + (threadIdx.x >> 5)] = v;
+}
+
+// End of a persistent row kernel: warp 0 turns the stored warp sums of every unit this block
+// processed into the unit partials (second level of the block tree), then the block takes its
+// completion ticket.  NV = number of dot products (slots k*NV + n).
+template <int NV>
+__device__ __forceinline__ bool finish_units(const KArgs& A, const double* ws, double* p0, double* p1,
+                                             uint32_t* counter) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const int64_t U = n_units(A);
+        int k = 0;
+        for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k) {
+            const int64_t m = (int64_t)(A.nloc - 1 - (int32_t)(u / A.nbx)) * A.nbx + (u % A.nbx);
+#pragma unroll
+            for (int n = 0; n < NV; ++n) {
+                double w = lane < kWarps ? ws[(k * NV + n) * kWarps + lane] : 0.0;
+                w = warp_tree(w);
+                if (lane == 0) (n == 0 ? p0 : p1)[m] = w;
+            }
+        }
+    }
+    return count_block(counter);
+}
+
+// Dynamic variant: units are handed out by an atomic ticket (prefetched one unit ahead), so
+// blocks that get slower memory do fewer units; each unit's partial is completed and stored
+// right away (block tree over its 8 warp sums).  Same partials, same canonical order.
+template <class Body>
+__device__ __forceinline__ void dynamic_units(const KArgs& A, unsigned long long* ticket, double* partial, Body body) {
+    __shared__ long long s_next;
+    __shared__ double wsd[kWarps];
+    const int64_t U = n_units(A);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_next = (long long)atomicAdd(ticket, 1ull);
+    __syncthreads();
+    int64_t u = s_next;
+    while (u < U) {
+        __syncthreads();                                   // everyone has read s_next
+        if (threadIdx.x == 0) s_next = (long long)atomicAdd(ticket, 1ull);
+        const Unit W = unit_of(A, u);
+        double v = body(W);
+        v = warp_tree(v);
+        if (lane == 0) wsd[warp] = v;
+        __syncthreads();
+        if (warp == 0) {
+            double w = lane < kWarps ? wsd[lane] : 0.0;
+            w = warp_tree(w);
+            if (lane == 0) partial[(int64_t)W.j * A.nbx + W.bx] = w;
+        }
+        u = s_next;
+    }
+}
+
 // ---- K1: d = s + beta d_old ; x += alpha_prev d_old ; q = A d ; (d, q) --------------------
+// Units are strips of rpb rows.  Each thread marches up its column: d at (i, j-1), (i, j),
+// (i, j+1) stay in registers, E/W neighbours come from the adjacent lanes by shuffle (lanes at a
+// warp edge and the two ends of a periodic row load them), and the loads of the next row are
+// issued before the current row computes.  Per point: s, d_old, x, cE, cN read once; d, x, q
+// written.
+#ifndef PCG_MINB_K1
+#define PCG_MINB_K1 4
+#endif
 template <bool SIGMA>
-__global__ void __launch_bounds__(kBlock) k1_kernel(const KArgs A, const int par) {
+__global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, const int par) {
     if (!is_active(A)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // safety net: the WHILE node ends even if a reduction never clears the flag
+        if (++A.sc->guard > A.sc->maxit + 2) {
+            A.sc->active = 0;
+            A.sc->status = kStBreakdown;
+            set_cond(A, 0);
+        }
+    }
+    extern __shared__ double ws[];
+    __shared__ double wrow[kMaxRowsK1][kWarps];
+    __shared__ long long s_next;
     const double beta = A.sc->beta, alpha = A.sc->alpha;
     const double* __restrict__ dold = A.d[par];
     double* __restrict__ dnew = A.d[par ^ 1];
     const double* __restrict__ s = A.s;
-    const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    double v = 0.0;
-    if (e < A.nel) {
-        const int32_t i = (int32_t)(e % A.pitch);
-        if (i < A.ni) {
-            const int64_t a = e + A.pitch;
-            const int64_t aw = i == 0 ? a + (A.ni - 1) : a - 1;
-            const int64_t ae = i == A.ni - 1 ? a - (A.ni - 1) : a + 1;
-            const int64_t as = a - A.pitch, an = a + A.pitch;
-            const double dop = dold[a];
-            const double dp = __fma_rn(beta, dop, s[a]);
-            const double dw = __fma_rn(beta, dold[aw], s[aw]);
-            const double de = __fma_rn(beta, dold[ae], s[ae]);
-            const double ds = __fma_rn(beta, dold[as], s[as]);
-            const double dn = __fma_rn(beta, dold[an], s[an]);
-            A.x[a] = __fma_rn(alpha, dop, A.x[a]);
-            const double cep = A.cE[a], cew = A.cE[aw];
-            const double cnr = A.cN[a];
-            const bool land = signbit(cnr);
-            const double cnp = fabs(cnr), cns = fabs(A.cN[as]);
-            double app = __dadd_rn(__dadd_rn(__dadd_rn(cep, cew), cnp), cns);
-            if (SIGMA) app = __dadd_rn(app, A.sigma[a]);
-            double acc = __dmul_rn(app, dp);
-            acc = __fma_rn(-cew, dw, acc);
-            acc = __fma_rn(-cep, de, acc);
-            acc = __fma_rn(-cns, ds, acc);
-            acc = __fma_rn(-cnp, dn, acc);
-            const double qv = land ? 0.0 : acc;
-            dnew[a] = dp;
-            A.q[a] = qv;
-            v = __dmul_rn(dp, qv);
-            // d on the halo rows (needed by the next K1 of a multi-rank solve)
-            if (e < A.pitch) dnew[as] = ds;
-            if (e >= A.nel - A.pitch) dnew[an] = dn;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int32_t P = A.pitch, ni = A.ni;
+    const int32_t nby = (A.nloc + A.rpb - 1) / A.rpb;
+    const int64_t S = (int64_t)nby * A.nbx;
+    // strips come from an atomic ticket (A.dynamic) or a block stride
+    int64_t st;
+    if (A.dynamic) {
+        if (threadIdx.x == 0) s_next = (long long)atomicAdd(&A.sc->ticket[0], 1ull);
+        __syncthreads();
+        st = s_next;
+    } else {
+        st = blockIdx.x;
+    }
+    int kslot = 0;
+    while (st < S) {
+        if (A.dynamic) {
+            __syncthreads();                               // everyone has read s_next
+            if (threadIdx.x == 0) s_next = (long long)atomicAdd(&A.sc->ticket[0], 1ull);
+        }
+        const int32_t bx = (int32_t)(st % A.nbx), by = nby - 1 - (int32_t)(st / A.nbx);
+        const int32_t i = bx * kBlock + (int32_t)threadIdx.x;
+        const int32_t j0 = by * A.rpb, j1 = min(j0 + A.rpb, A.nloc);
+        const bool valid = i < ni;
+        const int32_t iw = i == 0 ? ni - 1 : i - 1, ie = i == ni - 1 ? 0 : i + 1;
+        const bool ldw = valid && (lane == 0 || i == 0);
+        const bool lde = valid && (lane == 31 || i == ni - 1);
+        int64_t a = (int64_t)(j0 + 1) * P + i;
+        double dS = 0.0, dC = 0.0, doC = 0.0, cNs = 0.0;
+        double pdo = 0.0, ps = 0.0, pcE = 0.0, pcN = 0.0, px = 0.0;   // next row's loads
+        if (valid) {
+            dS = __fma_rn(beta, dold[a - P], s[a - P]);
+            doC = dold[a];
+            dC = __fma_rn(beta, doC, s[a]);
+            cNs = fabs(A.cN[a - P]);
+            if (j0 == 0) dnew[a - P] = dS;             // southern halo row (multi-rank)
+            pdo = dold[a + P]; ps = s[a + P];
+            pcE = A.cE[a]; pcN = A.cN[a]; px = A.x[a];
+        }
+        for (int32_t j = j0; j < j1; ++j, a += P) {
+            const double doN = pdo, cEp = pcE, cNr = pcN, xv = px;
+            const double dN = __fma_rn(beta, doN, ps);
+            if (valid && j + 1 < j1) {
+                pdo = dold[a + 2 * P]; ps = s[a + 2 * P];
+                pcE = A.cE[a + P]; pcN = A.cN[a + P]; px = A.x[a + P];
+            }
+            double dW = __shfl_up_sync(kFull, dC, 1);
+            double dE = __shfl_down_sync(kFull, dC, 1);
+            double cEw = __shfl_up_sync(kFull, cEp, 1);
+            if (ldw) {
+                const int64_t aw = a - i + iw;
+                dW = __fma_rn(beta, dold[aw], s[aw]);
+                cEw = A.cE[aw];
+            }
+            if (lde) {
+                const int64_t ae = a - i + ie;
+                dE = __fma_rn(beta, dold[ae], s[ae]);
+            }
+            double v = 0.0;
+            if (valid) {
+                const bool land = signbit(cNr);
+                const double cNp = fabs(cNr);
+                double app = __dadd_rn(__dadd_rn(__dadd_rn(cEp, cEw), cNp), cNs);
+                if (SIGMA) app = __dadd_rn(app, A.sigma[a]);
+                double acc = __dmul_rn(app, dC);
+                acc = __fma_rn(-cEw, dW, acc);
+                acc = __fma_rn(-cEp, dE, acc);
+                acc = __fma_rn(-cNs, dS, acc);
+                acc = __fma_rn(-cNp, dN, acc);
+                const double qv = land ? 0.0 : acc;
+                dnew[a] = dC;
+                A.q[a] = qv;
+                A.x[a] = __fma_rn(alpha, doC, xv);
+                v = __dmul_rn(dC, qv);
+                cNs = cNp;
+            }
+            v = warp_tree(v);
+            if (A.dynamic) {
+                if (lane == 0) wrow[j - j0][warp] = v;
+            } else if (lane == 0) {
+                ws[(kslot + j - j0) * kWarps + warp] = v;
+            }
+            dS = dC;
+            dC = dN;
+            doC = doN;
+        }
+        if (valid && j1 == A.nloc) dnew[a] = dC;       // northern halo row (multi-rank)
+        if (A.dynamic) {
+            __syncthreads();
+            if (warp == 0)                                 // row partials of this strip
+                for (int32_t j = j0; j < j1; ++j) {
+                    double w = lane < kWarps ? wrow[j - j0][lane] : 0.0;
+                    w = warp_tree(w);
+                    if (lane == 0) A.partial[0][(int64_t)j * A.nbx + bx] = w;
+                }
+            st = s_next;
+        } else {
+            st += gridDim.x;
+            kslot += A.rpb;
         }
     }
-    const double part = block_tree(v);
-    if (publish_partial(part, A.partial[0], &A.sc->counter[0])) {
-        const double tot = final_sum(A.partial[0], gridDim.x);
+    if (!A.dynamic) {
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            kslot = 0;
+            for (int64_t t2 = blockIdx.x; t2 < S; t2 += gridDim.x, kslot += A.rpb) {
+                const int32_t bx = (int32_t)(t2 % A.nbx), by = nby - 1 - (int32_t)(t2 / A.nbx);
+                const int32_t j0 = by * A.rpb, j1 = min(j0 + A.rpb, A.nloc);
+                for (int32_t j = j0; j < j1; ++j) {
+                    double w = lane < kWarps ? ws[(kslot + j - j0) * kWarps + lane] : 0.0;
+                    w = warp_tree(w);
+                    if (lane == 0) A.partial[0][(int64_t)j * A.nbx + bx] = w;
+                }
+            }
+        }
+    }
+    if (count_block(&A.sc->counter[0])) {
+        const double tot = final_sum(A.partial[0], n_units(A));
         if (threadIdx.x == 0) {
             if (A.multi) A.sc->loc[0] = tot;
             else A.sc->red[0] = tot;
             A.sc->xpend = 0;
             A.sc->counter[0] = 0;
+            A.sc->ticket[0] = 0;
         }
     }
 }
 
+// ---- ELL(4) + overflow row sums ---------------------------------------------
+// The first kEll entries of a row sit at fixed slots (no offset load) and store the gathered
+// point's array index, so all column/value loads issue together with the thread's other loads
+// and a gather is one address add.  Entries beyond kEll come from the overflow SELL (empty for
+// ~80% of slices), one at a time.  Accumulation: acc = fma(z, x, acc) over the ELL slots then the
+// overflow entries -- ascending column order; padding (value 0, own index) contributes 0.
+static_assert(kEll == 4, "ell_row loads the 4 ELL slots as one int4 and one 256-bit double vector");
+
+__device__ __forceinline__ void ld_nc_f64x4(const double* p, double (&z)[4]) {
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(z[0]), "=d"(z[1]), "=d"(z[2]), "=d"(z[3]) : "l"(p));
+}
+
+template <class Gather>
+__device__ __forceinline__ double ell_row(const EllDev& E, int64_t e, Gather gat) {
+    double z[kEll], x[kEll];
+    const int4 cv = __ldg(reinterpret_cast<const int4*>(E.col) + e);
+    ld_nc_f64x4(E.val + e * kEll, z);
+    const int32_t c[kEll] = {cv.x, cv.y, cv.z, cv.w};
+    const int64_t sl = e >> 5;
+    const int64_t o0 = __ldg(E.ooff + sl), o1 = __ldg(E.ooff + sl + 1);
+#pragma unroll
+    for (int m = 0; m < kEll; ++m) x[m] = gat(c[m]);
+    // schedule pin (emits nothing): the fma chain may only start once all four gathers have
+    // returned, so ptxas issues them back to back instead of one gather per fma.
+    asm volatile("" : "+d"(x[0]), "+d"(x[1]), "+d"(x[2]), "+d"(x[3]));
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < kEll; ++m) acc = __fma_rn(z[m], x[m], acc);
+    for (int64_t p = o0 + (e & 31); p < o1; p += 32) acc = __fma_rn(__ldg(E.oval + p), gat(__ldg(E.ocol + p)), acc);
+    return acc;
+}
+
+#ifndef PCG_MINB_K2
+#define PCG_MINB_K2 4            // register budgets: resident 256-thread blocks per SM ptxas targets
+#endif
+#ifndef PCG_MINB_K3
+#define PCG_MINB_K3 5
+#endif
+
+
 // ---- K2 (AINV): r -= alpha q ; t = Dhat^-1 Z^T r ; (r, r) --------------------------------
-__global__ void __launch_bounds__(kBlock) k2_ainv_kernel(const KArgs A, const int par, const int init) {
+// r_new at a gathered point c is recomputed as fma(-alpha, q_c, r_old_c) (bitwise the value
+// its own thread stores), so no grid-wide barrier is needed between the update and the gather.
+__global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArgs A, const int par, const int init) {
     if (!is_active(A)) return;
     double alpha;
     if (!get_alpha(A, init, alpha)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
         return;
     }
+    extern __shared__ double ws[];
     const double* __restrict__ ro = A.r[par];
     double* __restrict__ rn = A.r[par ^ 1];
     const double* __restrict__ q = A.q;
-    const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    double v = 0.0;
-    if (e < A.nel) {
-        const int64_t a = e + A.pitch;
-        const int64_t sl = e >> 5;
-        const int lane = (int)(e & 31);
-        const double rnew = __fma_rn(-alpha, q[a], ro[a]);
-        const int64_t off = A.zt_off[sl];
-        const int64_t L = (A.zt_off[sl + 1] - off) >> 5;
-        double acc = 0.0;
-        for (int64_t m = 0; m < L; ++m) {
-            const int64_t slot = off + (m << 5) + lane;
-            const int32_t c = __ldg(A.zt_col + slot);
-            const double z = __ldg(A.zt_val + slot);
-            acc = __fma_rn(z, __fma_rn(-alpha, q[c], ro[c]), acc);
+    auto body = [&](const Unit& W) {
+        double v = 0.0;
+        if (W.inrow) {
+            const double rnew = __fma_rn(-alpha, q[W.a], ro[W.a]);
+            const double pv = A.piv[W.a];
+            const double acc = ell_row(A.zt, W.a - A.pitch,
+                                       [&](int32_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); });
+            A.t[W.a] = __ddiv_rn(acc, pv);
+            rn[W.a] = rnew;
+            v = __dmul_rn(rnew, rnew);
         }
-        A.t[a] = __ddiv_rn(acc, A.piv[a]);
-        rn[a] = rnew;
-        v = __dmul_rn(rnew, rnew);
+        return v;
+    };
+    bool last;
+    if (A.dynamic) {
+        dynamic_units(A, &A.sc->ticket[1], A.partial[1], body);
+        last = count_block(&A.sc->counter[1]);
+    } else {
+        const int64_t U = n_units(A);
+        int k = 0;
+        for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k) put_warp_sum(ws, k, body(unit_of(A, u)));
+        last = finish_units<1>(A, ws, A.partial[1], nullptr, &A.sc->counter[1]);
     }
-    const double part = block_tree(v);
-    if (publish_partial(part, A.partial[1], &A.sc->counter[1])) {
-        const double tot = final_sum(A.partial[1], gridDim.x);
+    if (last) {
+        const double tot = final_sum(A.partial[1], n_units(A));
         if (threadIdx.x == 0) {
             if (A.multi) A.sc->loc[2] = tot;
             else A.sc->red[2] = tot;
             A.sc->alpha = alpha;
             A.sc->xpend = init ? 0 : 1;
             A.sc->counter[1] = 0;
+            A.sc->ticket[1] = 0;
         }
     }
 }
 
 // ---- K3 (AINV): s = Z t ; (s, r) ; beta / history / flag -----------------------------------
-__global__ void __launch_bounds__(kBlock) k3_ainv_kernel(const KArgs A, const int par, const int init) {
+__global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArgs A, const int par, const int init) {
     if (!is_active(A)) return;
+    extern __shared__ double ws[];
     const double* __restrict__ rn = A.r[par ^ 1];
     const double* __restrict__ t = A.t;
-    const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    double v = 0.0;
-    if (e < A.nel) {
-        const int64_t a = e + A.pitch;
-        const int64_t sl = e >> 5;
-        const int lane = (int)(e & 31);
-        const int64_t off = A.z_off[sl];
-        const int64_t L = (A.z_off[sl + 1] - off) >> 5;
-        double acc = 0.0;
-        for (int64_t m = 0; m < L; ++m) {
-            const int64_t slot = off + (m << 5) + lane;
-            acc = __fma_rn(__ldg(A.z_val + slot), t[__ldg(A.z_col + slot)], acc);
+    auto body = [&](const Unit& W) {
+        double v = 0.0;
+        if (W.inrow) {
+            const double rv = rn[W.a];
+            const double acc = ell_row(A.z, W.a - A.pitch, [&](int32_t g) { return __ldg(t + g); });
+            A.s[W.a] = acc;
+            v = __dmul_rn(acc, rv);
         }
-        A.s[a] = acc;
-        v = __dmul_rn(acc, rn[a]);
+        return v;
+    };
+    bool last;
+    if (A.dynamic) {
+        dynamic_units(A, &A.sc->ticket[2], A.partial[2], body);
+        last = count_block(&A.sc->counter[2]);
+    } else {
+        const int64_t U = n_units(A);
+        int k = 0;
+        for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k) put_warp_sum(ws, k, body(unit_of(A, u)));
+        last = finish_units<1>(A, ws, A.partial[2], nullptr, &A.sc->counter[2]);
     }
-    const double part = block_tree(v);
-    if (publish_partial(part, A.partial[2], &A.sc->counter[2])) {
-        const double tot = final_sum(A.partial[2], gridDim.x);
+    if (last) {
+        const double tot = final_sum(A.partial[2], n_units(A));
         if (threadIdx.x == 0) {
             A.sc->counter[2] = 0;
+            A.sc->ticket[2] = 0;
             if (A.multi) A.sc->loc[1] = tot;
             else if (init) fin_init(A, tot, A.sc->red[2]);
             else fin_iter(A, tot, A.sc->red[2]);
@@ -295,32 +549,28 @@ __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const in
         if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
         return;
     }
+    extern __shared__ double ws[];
     const double* __restrict__ ro = A.r[par];
     double* __restrict__ rn = A.r[par ^ 1];
-    const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    double v1 = 0.0, v2 = 0.0;
-    if (e < A.nel) {
-        const int64_t a = e + A.pitch;
-        const double rnew = __fma_rn(-alpha, A.q[a], ro[a]);
-        const double sv = none ? rnew : __ddiv_rn(rnew, A.diag[a]);
-        A.s[a] = sv;
-        rn[a] = rnew;
-        v1 = __dmul_rn(rnew, rnew);
-        v2 = __dmul_rn(sv, rnew);
+    const int64_t U = n_units(A);
+    int k = 0;
+    for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k) {
+        const Unit W = unit_of(A, u);
+        double v1 = 0.0, v2 = 0.0;
+        if (W.inrow) {
+            const double rnew = __fma_rn(-alpha, A.q[W.a], ro[W.a]);
+            const double sv = none ? rnew : __ddiv_rn(rnew, A.diag[W.a]);
+            A.s[W.a] = sv;
+            rn[W.a] = rnew;
+            v1 = __dmul_rn(rnew, rnew);
+            v2 = __dmul_rn(sv, rnew);
+        }
+        put_warp_sum(ws, 2 * k, v1);
+        put_warp_sum(ws, 2 * k + 1, v2);
     }
-    const double p1 = block_tree(v1);
-    const double p2 = block_tree(v2);
-    __shared__ bool am_last;
-    if (threadIdx.x == 0) {
-        A.partial[1][blockIdx.x] = p1;
-        A.partial[2][blockIdx.x] = p2;
-        __threadfence();
-        am_last = atomicAdd(&A.sc->counter[1], 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (am_last) {
-        const double rr = final_sum(A.partial[1], gridDim.x);
-        const double rs = final_sum(A.partial[2], gridDim.x);
+    if (finish_units<2>(A, ws, A.partial[1], A.partial[2], &A.sc->counter[1])) {
+        const double rr = final_sum(A.partial[1], n_units(A));
+        const double rs = final_sum(A.partial[2], n_units(A));
         if (threadIdx.x == 0) {
             A.sc->counter[1] = 0;
             A.sc->alpha = alpha;
@@ -366,22 +616,23 @@ __global__ void __launch_bounds__(kBlock) prep_kernel(const KArgs A) {
 
 // a3: r0 = b - A x0 into r[1]; (b, b)
 __global__ void __launch_bounds__(kBlock) init_residual_kernel(const KArgs A) {
-    const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    double v = 0.0;
-    if (e < A.nel) {
-        const int32_t i = (int32_t)(e % A.pitch);
-        if (i < A.ni) {
-            const int64_t a = e + A.pitch;
+    extern __shared__ double ws[];
+    const int64_t U = n_units(A);
+    int k = 0;
+    for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k) {
+        const Unit W = unit_of(A, u);
+        double v = 0.0;
+        if (W.valid) {
             bool land;
-            const double ax = stencil(A, A.x, a, i, land);
-            const double bv = A.b[a];
-            A.r[1][a] = land ? 0.0 : __dadd_rn(bv, -ax);
+            const double ax = stencil(A, A.x, W.a, W.i, land);
+            const double bv = A.b[W.a];
+            A.r[1][W.a] = land ? 0.0 : __dadd_rn(bv, -ax);
             v = __dmul_rn(bv, bv);
         }
+        put_warp_sum(ws, k, v);
     }
-    const double part = block_tree(v);
-    if (publish_partial(part, A.partial[0], &A.sc->counter[3])) {
-        const double tot = final_sum(A.partial[0], gridDim.x);
+    if (finish_units<1>(A, ws, A.partial[0], nullptr, &A.sc->counter[3])) {
+        const double tot = final_sum(A.partial[0], n_units(A));
         if (threadIdx.x == 0) {
             A.sc->counter[3] = 0;
             if (A.multi) A.sc->loc[3] = tot;
@@ -390,35 +641,24 @@ __global__ void __launch_bounds__(kBlock) init_residual_kernel(const KArgs A) {
     }
 }
 
-// a9: pending x update (or x = 0 when b = 0)
-__global__ void __launch_bounds__(kBlock) fin_kernel(const KArgs A) {
-    const DevScalars* sc = A.sc;
-    const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    if (e >= A.nel) return;
-    const int32_t i = (int32_t)(e % A.pitch);
-    if (i >= A.ni) return;
-    const int64_t a = e + A.pitch;
-    if (sc->bzero) { A.x[a] = 0.0; return; }
-    if (sc->xpend) A.x[a] = __fma_rn(sc->alpha, A.d[sc->k & 1][a], A.x[a]);
-}
-
 // a9: ||b - A x|| / ||b||
 __global__ void __launch_bounds__(kBlock) true_residual_kernel(const KArgs A) {
-    const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    double v = 0.0;
-    if (e < A.nel) {
-        const int32_t i = (int32_t)(e % A.pitch);
-        if (i < A.ni) {
-            const int64_t a = e + A.pitch;
+    extern __shared__ double ws[];
+    const int64_t U = n_units(A);
+    int k = 0;
+    for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k) {
+        const Unit W = unit_of(A, u);
+        double v = 0.0;
+        if (W.valid) {
             bool land;
-            const double ax = stencil(A, A.x, a, i, land);
-            const double r = land ? 0.0 : __dadd_rn(A.b[a], -ax);
+            const double ax = stencil(A, A.x, W.a, W.i, land);
+            const double r = land ? 0.0 : __dadd_rn(A.b[W.a], -ax);
             v = __dmul_rn(r, r);
         }
+        put_warp_sum(ws, k, v);
     }
-    const double part = block_tree(v);
-    if (publish_partial(part, A.partial[0], &A.sc->counter[3])) {
-        const double tot = final_sum(A.partial[0], gridDim.x);
+    if (finish_units<1>(A, ws, A.partial[0], nullptr, &A.sc->counter[3])) {
+        const double tot = final_sum(A.partial[0], n_units(A));
         if (threadIdx.x == 0) {
             A.sc->counter[3] = 0;
             if (A.multi) A.sc->loc[3] = tot;
@@ -427,16 +667,22 @@ __global__ void __launch_bounds__(kBlock) true_residual_kernel(const KArgs A) {
     }
 }
 
+// a9: pending x update (or x = 0 when b = 0)
+__global__ void __launch_bounds__(kBlock) fin_kernel(const KArgs A) {
+    const DevScalars* sc = A.sc;
+    const Unit W = unit_of(A, blockIdx.x);
+    if (!W.valid) return;
+    if (sc->bzero) A.x[W.a] = 0.0;
+    else if (sc->xpend) A.x[W.a] = __fma_rn(sc->alpha, A.d[sc->k & 1][W.a], A.x[W.a]);
+}
+
 __global__ void __launch_bounds__(kBlock) apply_kernel(const KArgs A, const double* __restrict__ x,
                                                        double* __restrict__ y) {
-    const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    if (e >= A.nel) return;
-    const int32_t i = (int32_t)(e % A.pitch);
-    if (i >= A.ni) return;
-    const int64_t a = e + A.pitch;
+    const Unit W = unit_of(A, blockIdx.x);
+    if (!W.valid) return;
     bool land;
-    const double ax = stencil(A, x, a, i, land);
-    y[a] = land ? 0.0 : ax;
+    const double ax = stencil(A, x, W.a, W.i, land);
+    y[W.a] = land ? 0.0 : ax;
 }
 
 __global__ void scalar_kernel(const KArgs A, const int step) {
@@ -456,23 +702,73 @@ __global__ void scalar_kernel(const KArgs A, const int step) {
 
 __global__ void set_cond_kernel(cudaGraphConditionalHandle h) { cudaGraphSetConditional(h, 1u); }
 
+// shared memory of a persistent row kernel: NV warp-sum slots per unit it may process
+size_t row_smem(const KArgs& A, int grid, int NV) {
+    const int64_t U = (int64_t)A.nloc * A.nbx;
+    const int64_t per = (U + grid - 1) / grid;
+    return (size_t)std::max<int64_t>(per, 1) * NV * kWarps * sizeof(double);
+}
+
+size_t k1_smem(const KArgs& A, int grid) {
+    const int64_t S = (int64_t)A.nbx * ((A.nloc + A.rpb - 1) / A.rpb);
+    const int64_t per = (S + grid - 1) / grid;
+    return (size_t)std::max<int64_t>(per, 1) * A.rpb * kWarps * sizeof(double);
+}
+
+// persistent grid: resident blocks per SM (occupancy API) x SMs, capped by the units
+template <class K>
+int persistent_grid(K kernel, int64_t units, int sms, size_t smem_guess) {
+    if (const char* e = getenv("PCG_PERSIST"))          // tuning: 0 = one unit per block
+        if (atoi(e) == 0) return (int)units;
+    if (const char* e = getenv("PCG_BLOCKS_PER_SM"))    // tuning: fixed resident blocks per SM
+        return (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)atoi(e) * sms));
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem_guess);
+    per_sm = std::max(per_sm, 1);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)per_sm * sms));
+}
+
+template <class K>
+void allow_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 }  // namespace
 
-int64_t grid_blocks(const KArgs& A) { return (A.nel + kBlock - 1) / kBlock; }
+// Grid sizes and shared memory of the persistent kernels.
+void configure_kernels(KArgs& A, int sms) {
+    A.dynamic = 1;                                     // measured: -21 % per iteration at ORCA025
+    if (const char* e = getenv("PCG_DYNAMIC")) A.dynamic = atoi(e) != 0;
+    const int64_t U = (int64_t)A.nloc * A.nbx;
+    const int64_t S = (int64_t)A.nbx * ((A.nloc + A.rpb - 1) / A.rpb);
+    A.g_k1 = persistent_grid(k1_kernel<false>, S, sms, 4096);
+    A.g_k2 = persistent_grid(k2_ainv_kernel, U, sms, 2048);
+    A.g_k3 = persistent_grid(k3_ainv_kernel, U, sms, 2048);
+    A.g_kd = persistent_grid(k2_diag_kernel, U, sms, 4096);
+    A.g_row = persistent_grid(init_residual_kernel, U, sms, 2048);
+    allow_smem(k1_kernel<false>, k1_smem(A, A.g_k1));
+    allow_smem(k1_kernel<true>, k1_smem(A, A.g_k1));
+    allow_smem(k2_ainv_kernel, row_smem(A, A.g_k2, 1));
+    allow_smem(k3_ainv_kernel, row_smem(A, A.g_k3, 1));
+    allow_smem(k2_diag_kernel, row_smem(A, A.g_kd, 2));
+    allow_smem(init_residual_kernel, row_smem(A, A.g_row, 1));
+    allow_smem(true_residual_kernel, row_smem(A, A.g_row, 1));
+}
+
+int64_t grid_blocks(const KArgs& A) { return (int64_t)A.nbx * A.nloc; }
 
 void launch_k1(const KArgs& A, int par, cudaStream_t st) {
-    const unsigned G = (unsigned)grid_blocks(A);
-    if (A.sigma) k1_kernel<true><<<G, kBlock, 0, st>>>(A, par);
-    else k1_kernel<false><<<G, kBlock, 0, st>>>(A, par);
+    if (A.sigma) k1_kernel<true><<<A.g_k1, kBlock, k1_smem(A, A.g_k1), st>>>(A, par);
+    else k1_kernel<false><<<A.g_k1, kBlock, k1_smem(A, A.g_k1), st>>>(A, par);
 }
 void launch_k2_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
-    k2_ainv_kernel<<<(unsigned)grid_blocks(A), kBlock, 0, st>>>(A, par, init);
+    k2_ainv_kernel<<<A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st>>>(A, par, init);
 }
 void launch_k3_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
-    k3_ainv_kernel<<<(unsigned)grid_blocks(A), kBlock, 0, st>>>(A, par, init);
+    k3_ainv_kernel<<<A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st>>>(A, par, init);
 }
 void launch_k2_diag(const KArgs& A, int par, int init, int none, cudaStream_t st) {
-    k2_diag_kernel<<<(unsigned)grid_blocks(A), kBlock, 0, st>>>(A, par, init, none);
+    k2_diag_kernel<<<A.g_kd, kBlock, row_smem(A, A.g_kd, 2), st>>>(A, par, init, none);
 }
 void launch_prep(const KArgs& A, cudaStream_t st) {
     const int64_t n = (int64_t)(A.nloc + 2) * A.pitch;
@@ -480,11 +776,11 @@ void launch_prep(const KArgs& A, cudaStream_t st) {
     prep_kernel<<<(unsigned)G, kBlock, 0, st>>>(A);
 }
 void launch_init_residual(const KArgs& A, cudaStream_t st) {
-    init_residual_kernel<<<(unsigned)grid_blocks(A), kBlock, 0, st>>>(A);
+    init_residual_kernel<<<A.g_row, kBlock, row_smem(A, A.g_row, 1), st>>>(A);
 }
 void launch_fin(const KArgs& A, cudaStream_t st) { fin_kernel<<<(unsigned)grid_blocks(A), kBlock, 0, st>>>(A); }
 void launch_true_residual(const KArgs& A, cudaStream_t st) {
-    true_residual_kernel<<<(unsigned)grid_blocks(A), kBlock, 0, st>>>(A);
+    true_residual_kernel<<<A.g_row, kBlock, row_smem(A, A.g_row, 1), st>>>(A);
 }
 void launch_apply(const KArgs& A, const double* x, double* y, cudaStream_t st) {
     apply_kernel<<<(unsigned)grid_blocks(A), kBlock, 0, st>>>(A, x, y);

@@ -7,6 +7,7 @@
 namespace pcg {
 
 enum : int32_t { kStOk = 0, kStBreakdown = 3 };
+constexpr int kMaxRowsK1 = 16;     // rows per K1 block (register march), <= kMaxRowsK1
 
 // Device-resident scalars of one solve.  Written only by the last block of a
 // reduction kernel (one rank) or by the 1-thread scalar kernels after an NCCL allgather.
@@ -14,17 +15,30 @@ struct DevScalars {
     double alpha, beta, rho, nb, tol, true_rel;
     double red[4];        // global reductions: [0] (d,q)  [1] (s,r)  [2] (r,r)  [3] (b,b) / true (r,r)
     double loc[4];        // this rank's block-tree sums (multi-rank path)
-    int32_t k, maxit, active, status, bzero, xpend;
+    int32_t k, maxit, active, status, bzero, xpend, guard, pad_;
     uint32_t counter[4];  // last-block detection, reset by the last block
+    unsigned long long ticket[4];   // dynamic unit assignment, reset by the last block
+};
+
+// Device view of an ELL(kEll) + overflow-SELL matrix (see internal.h).
+struct EllDev {
+    const double* val;          // kEll * n
+    const int32_t* col;         // kEll * n, packed (di, dj)
+    const int64_t* ooff;        // overflow slice offsets (nslices + 1)
+    const double* oval;
+    const int32_t* ocol;
+    int64_t n;
 };
 
 struct KArgs {
     int32_t ni, pitch, nloc, nranks;
+    int32_t nbx, rpb;                 // column segments of kBlock per row; rows per K1 strip
+    int32_t g_k1, g_k2, g_k3, g_kd, g_row;   // persistent grid sizes (configure_kernels)
+    int32_t dynamic;                  // K2/K3: units from an atomic ticket instead of a block stride
     int64_t nel;                      // owned elements nloc * pitch
     const double *cE, *cN, *sigma, *diag, *piv;
-    const int64_t *zt_off, *z_off;
-    const double *zt_val, *z_val;
-    const int32_t *zt_col, *z_col;
+    EllDev zt, z;                     // rows of Z^T (K2) and of Z (K3)
+    int32_t periodic;
     double *x, *b, *q, *t, *s;
     double *r[2], *d[2];
     double* partial[3];
@@ -54,5 +68,6 @@ void launch_apply(const KArgs& A, const double* x_arr, double* y_arr, cudaStream
 enum ScalarStep : int32_t { kSsBB = 0, kSsGamma = 1, kSsInit = 2, kSsIter = 3, kSsTrue = 4 };
 void launch_scalar(const KArgs& A, int step, cudaStream_t st);
 void launch_set_cond(cudaGraphConditionalHandle h, cudaStream_t st);
+void configure_kernels(KArgs& A, int sms);
 
 }  // namespace pcg

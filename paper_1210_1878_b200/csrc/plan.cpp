@@ -86,9 +86,24 @@ int64_t global_unknown(const uint8_t* mask, int32_t ni, int64_t g) {
 }
 
 // Pack a set of sparse rows (one per owned element; entries (array column, value) already in
-// ascending column order) into SELL-32.
+// ascending column order) into SELL-32 with relative (di, dj) column offsets.
 void pack_sell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols,
-               const std::vector<double>& vals, int64_t nel, int32_t pitch, Sell& S) {
+               const std::vector<double>& vals, int64_t nel, int32_t pitch, int32_t ni, int32_t periodic, Sell& S,
+               bool absolute = false) {
+    S.dimin = S.dimax = S.djmin = S.djmax = 0;
+    auto rel = [&](int64_t e, int32_t ac) -> int32_t {
+        const int32_t jr = (int32_t)(e / pitch), ir = (int32_t)(e % pitch);
+        const int32_t jc = ac / pitch - 1, ic = ac % pitch;
+        int32_t di = ic - ir;
+        const int32_t dj = jc - jr;
+        if (periodic) {
+            if (di > ni / 2) di -= ni;
+            if (di < -((ni - 1) / 2)) di += ni;
+        }
+        S.dimin = std::min(S.dimin, di); S.dimax = std::max(S.dimax, di);
+        S.djmin = std::min(S.djmin, dj); S.djmax = std::max(S.djmax, dj);
+        return (int32_t)(((uint32_t)(uint16_t)(int16_t)dj << 16) | (uint32_t)(uint16_t)(int16_t)di);
+    };
     const int64_t nsl = nel / kSlice;
     S.off.assign(nsl + 1, 0);
     for (int64_t s = 0; s < nsl; ++s) {
@@ -108,11 +123,68 @@ void pack_sell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& c
             const int64_t len = rowptr[e + 1] - rowptr[e];
             for (int64_t m = 0; m < L; ++m) {
                 const int64_t slot = S.off[s] + m * kSlice + l;
-                if (m < len) { S.val[slot] = vals[rowptr[e] + m]; S.col[slot] = cols[rowptr[e] + m]; }
-                else { S.val[slot] = 0.0; S.col[slot] = (int32_t)(e + pitch); }
+                if (m < len) {
+                    S.val[slot] = vals[rowptr[e] + m];
+                    const int32_t r = rel(e, cols[rowptr[e] + m]);
+                    S.col[slot] = absolute ? cols[rowptr[e] + m] : r;
+                } else {
+                    S.val[slot] = 0.0;
+                    S.col[slot] = absolute ? (int32_t)(e + pitch) : 0;
+                }
             }
         }
     }
+}
+
+// Split rows into ELL(kEll) + SELL overflow (same packed offsets, same ascending order).
+void pack_ell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols,
+              const std::vector<double>& vals, int64_t nel, int32_t pitch, int32_t ni, int32_t periodic, Ell& E) {
+    Sell full;
+    pack_sell(rowptr, cols, vals, nel, pitch, ni, periodic, full, true);   // absolute columns + extents
+    E.n = nel;
+    E.dimin = full.dimin; E.dimax = full.dimax; E.djmin = full.djmin; E.djmax = full.djmax;
+    E.val.assign((size_t)kEll * nel, 0.0);
+    E.col.assign((size_t)kEll * nel, 0);
+    for (int64_t e = 0; e < nel; ++e)                    // padding: value 0 at the row's own point
+        for (int m = 0; m < kEll; ++m) E.col[e * kEll + m] = (int32_t)(e + pitch);
+    std::vector<int64_t> orp(nel + 1, 0);
+    std::vector<int32_t> ocol;
+    std::vector<double> oval;
+    const int64_t nsl = nel / kSlice;
+    for (int64_t s = 0; s < nsl; ++s) {
+        const int64_t L = (full.off[s + 1] - full.off[s]) / kSlice;
+        for (int l = 0; l < kSlice; ++l) {
+            const int64_t e = s * kSlice + l;
+            const int64_t len = rowptr[e + 1] - rowptr[e];
+            for (int64_t m = 0; m < L && m < len; ++m) {
+                const int64_t slot = full.off[s] + m * kSlice + l;
+                if (m < kEll) { E.val[e * kEll + m] = full.val[slot]; E.col[e * kEll + m] = full.col[slot]; }
+                else { ocol.push_back(full.col[slot]); oval.push_back(full.val[slot]); }
+            }
+            orp[e + 1] = orp[e] + std::max<int64_t>(0, len - kEll);
+        }
+    }
+    // overflow rows as SELL: reuse pack_sell on already-packed offsets (identity columns)
+    E.ovf.off.assign(nsl + 1, 0);
+    for (int64_t s = 0; s < nsl; ++s) {
+        int64_t L = 0;
+        for (int l = 0; l < kSlice; ++l) L = std::max(L, orp[s * kSlice + l + 1] - orp[s * kSlice + l]);
+        E.ovf.off[s + 1] = E.ovf.off[s] + L * kSlice;
+    }
+    E.ovf.val.assign(E.ovf.off[nsl], 0.0);
+    E.ovf.col.assign(E.ovf.off[nsl], 0);
+    for (int64_t s = 0; s < nsl; ++s)
+        for (int64_t slot = E.ovf.off[s]; slot < E.ovf.off[s + 1]; ++slot)
+            E.ovf.col[slot] = (int32_t)(s * kSlice + (slot - E.ovf.off[s]) % kSlice + pitch);
+    for (int64_t s = 0; s < nsl; ++s)
+        for (int l = 0; l < kSlice; ++l) {
+            const int64_t e = s * kSlice + l;
+            for (int64_t m = 0; m < orp[e + 1] - orp[e]; ++m) {
+                const int64_t slot = E.ovf.off[s] + m * kSlice + l;
+                E.ovf.val[slot] = oval[orp[e] + m];
+                E.ovf.col[slot] = ocol[orp[e] + m];
+            }
+        }
 }
 
 }  // namespace
@@ -182,6 +254,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             return Status::err(PCG_ERR_NOT_SPD, buf, global_unknown(c->mask, ni, k));
         }
     if (Status s = anchor_check(ni, nj, P.periodic, c->cE, c->cN, c->sigma, c->mask); !s) return s;
+    if (ni > 65534) return Status::err(PCG_ERR_ARG, "pcg_setup: ni > 65534 not supported (int16 column offsets)");
 
     // device-layout coefficient arrays: absent faces -> 0, land flagged by the
     // sign bit of cN (cN >= 0 always, so -0.0 / -c mark a land cell).
@@ -316,7 +389,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
                 vals[dst] = ent_z[e];
             }
         }
-        pack_sell(rp, cols, vals, nown, pitch, P.ZT);
+        pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.ZT);
     }
     // ---- SELL of Z rows: row i = entries z_ij over columns j ascending
     {
@@ -333,7 +406,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
                 vals[fill[r]] = ent_z[e];
                 fill[r]++;
             }
-        pack_sell(rp, cols, vals, nown, pitch, P.Z);
+        pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.Z);
     }
     P.setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return Status::ok();

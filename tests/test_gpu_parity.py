@@ -68,7 +68,7 @@ def _canonical_pair(p, precond, tol, maxit=None, x0=None, tau=TAU, **kw):
     A, M, S = setup_pair(p, precond, tau, **kw)
     b = rhs(A, p)
     parts = max(1, kw.get("ainv_parts", 0) or 1)
-    ref = oracle.pcg(A, b, precond, M, tol, maxit=maxit, x0=x0, mode="canonical", pitch=S.pitch, block=S.block)
+    ref = oracle.pcg(A, b, precond, M, tol, maxit=maxit, x0=x0, mode="canonical", pitch=S.pitch, block=S.block, rows=S.tile_rows)
     xg, k, hist, rep = S.solve(dev(A.to_grid(b)), None if x0 is None else dev(A.to_grid(x0)), tol=tol,
                                maxit=maxit if maxit is not None else A.n)
     return A, S, ref, host(xg), k, hist, rep, parts
@@ -202,7 +202,7 @@ def test_cfg4_full_size_sampled():
     assert np.array_equal(y, A.to_grid(A.apply_canonical(xs)))
     s = host(S.apply_preconditioner(dev(A.to_grid(b))))
     assert np.array_equal(s, A.to_grid(M.apply_canonical(b)))
-    ref = oracle.pcg(A, b, "ainv", M, 0.0, maxit=5, mode="canonical", pitch=S.pitch, block=S.block)
+    ref = oracle.pcg(A, b, "ainv", M, 0.0, maxit=5, mode="canonical", pitch=S.pitch, block=S.block, rows=S.tile_rows)
     xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=0.0, maxit=5)
     assert k == 5 and np.array_equal(hist, ref.hist) and np.array_equal(host(xg), A.to_grid(ref.x))
     xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
