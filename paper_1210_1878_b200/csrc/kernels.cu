@@ -288,9 +288,10 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
     const int32_t P = A.pitch, ni = A.ni;
     const int32_t nby = (A.nloc + A.rpb - 1) / A.rpb;
     const int64_t S = (int64_t)nby * A.nbx;
-    // strips come from an atomic ticket (A.dynamic) or a block stride
+    // strips come from an atomic ticket (A.dynamic_k1) or a block stride
+    const bool dyn = A.dynamic_k1 != 0;
     int64_t st;
-    if (A.dynamic) {
+    if (dyn) {
         if (threadIdx.x == 0) s_next = (long long)atomicAdd(&A.sc->ticket[0], 1ull);
         __syncthreads();
         st = s_next;
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
     }
     int kslot = 0;
     while (st < S) {
-        if (A.dynamic) {
+        if (dyn) {
             __syncthreads();                               // everyone has read s_next
             if (threadIdx.x == 0) s_next = (long long)atomicAdd(&A.sc->ticket[0], 1ull);
         }
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
                 cNs = cNp;
             }
             v = warp_tree(v);
-            if (A.dynamic) {
+            if (dyn) {
                 if (lane == 0) wrow[j - j0][warp] = v;
             } else if (lane == 0) {
                 ws[(kslot + j - j0) * kWarps + warp] = v;
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
             doC = doN;
         }
         if (valid && j1 == A.nloc) dnew[a] = dC;       // northern halo row (multi-rank)
-        if (A.dynamic) {
+        if (dyn) {
             __syncthreads();
             if (warp == 0)                                 // row partials of this strip
                 for (int32_t j = j0; j < j1; ++j) {
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
             kslot += A.rpb;
         }
     }
-    if (!A.dynamic) {
+    if (!dyn) {
         __syncthreads();
         if (threadIdx.x < 32) {
             kslot = 0;
@@ -737,8 +738,10 @@ void allow_smem(K kernel, size_t bytes) {
 
 // Grid sizes and shared memory of the persistent kernels.
 void configure_kernels(KArgs& A, int sms) {
-    A.dynamic = 1;                                     // measured: -21 % per iteration at ORCA025
+    A.dynamic = 1;                                     // K2/K3: measured -21 % per iteration at ORCA025
     if (const char* e = getenv("PCG_DYNAMIC")) A.dynamic = atoi(e) != 0;
+    A.dynamic_k1 = 0;                                  // K1 (4-row strips): static stride measured faster
+    if (const char* e = getenv("PCG_DYNAMIC_K1")) A.dynamic_k1 = atoi(e) != 0;
     const int64_t U = (int64_t)A.nloc * A.nbx;
     const int64_t S = (int64_t)A.nbx * ((A.nloc + A.rpb - 1) / A.rpb);
     A.g_k1 = persistent_grid(k1_kernel<false>, S, sms, 4096);

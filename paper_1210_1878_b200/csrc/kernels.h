@@ -34,7 +34,7 @@ struct KArgs {
     int32_t ni, pitch, nloc, nranks;
     int32_t nbx, rpb;                 // column segments of kBlock per row; rows per K1 strip
     int32_t g_k1, g_k2, g_k3, g_kd, g_row;   // persistent grid sizes (configure_kernels)
-    int32_t dynamic;                  // K2/K3: units from an atomic ticket instead of a block stride
+    int32_t dynamic, dynamic_k1;      // units from an atomic ticket instead of a block stride
     int64_t nel;                      // owned elements nloc * pitch
     const double *cE, *cN, *sigma, *diag, *piv;
     EllDev zt, z;                     // rows of Z^T (K2) and of Z (K3)

@@ -396,15 +396,13 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     }
     CU(cudaMallocHost(&c->h_sc, sizeof(DevScalars)));
     A.ni = P.ni; A.pitch = P.pitch; A.nloc = P.nloc; A.nranks = P.nranks; A.nel = P.owned_elements();
-    // launch geometry: row segments of kBlock columns; K1 marches rpb rows per
-    // block (~4 blocks per SM, at most kMaxRowsK1).  PCG_ROWS_PER_BLOCK overrides (tuning).
-    // The reduction order does not depend on rpb.
+    // launch geometry: row segments of kBlock columns; K1 marches strips of rpb
+    // rows.  PCG_ROWS_PER_BLOCK overrides (tuning).  The reduction order does not depend on it.
     A.nbx = (P.pitch + kBlock - 1) / kBlock;
     {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-        int64_t r = (int64_t)P.nloc * A.nbx / (4 * (int64_t)sms);
-        A.rpb = (int32_t)std::max<int64_t>(1, std::min<int64_t>(kMaxRowsK1, r));
+        A.rpb = 4;                                      // K1 strip height (measured best 4-6 at ORCA025)
         if (const char* e = getenv("PCG_ROWS_PER_BLOCK")) A.rpb = std::max(1, std::min(kMaxRowsK1, atoi(e)));
         A.rpb = std::min(A.rpb, P.nloc);
         configure_kernels(A, sms);
