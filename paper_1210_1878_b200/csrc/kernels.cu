@@ -27,6 +27,7 @@
 // stride, keeping each unit's 8 warp sums in shared memory.  A block publishes its partials and
 // takes its ticket on the completion counter once, at the end: a per-unit fence + atomic would
 // stall every short-lived block (measured: ~15 us per kernel at ORCA025, profiles/r01).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -50,12 +51,13 @@ __device__ __forceinline__ double warp_tree(double v) {
 }
 
 // Block tree (kBlock threads): result valid in thread 0.
+// Threads beyond kBlock (the producer warp of the TMA kernels) take part in the barriers only.
 __device__ __forceinline__ double block_tree(double v) {
     __shared__ double wsb[kWarps];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     v = warp_tree(v);
     __syncthreads();                       // wsb may still be read by a previous call
-    if (lane == 0) wsb[w] = v;
+    if (lane == 0 && w < kWarps) wsb[w] = v;
     __syncthreads();
     double u = 0.0;
     if (w == 0) {
@@ -83,7 +85,7 @@ __device__ __forceinline__ bool count_block(uint32_t* counter) {
 __device__ __forceinline__ double final_sum(const double* partial, int64_t G) {
     __threadfence();
     double acc = 0.0;
-    int64_t m = threadIdx.x;
+    int64_t m = threadIdx.x < kBlock ? (int64_t)threadIdx.x : G;
     for (; m + 7 * kBlock < G; m += 8 * kBlock) {
         double p[8];
 #pragma unroll
@@ -263,6 +265,80 @@ __device__ __forceinline__ void dynamic_units(const KArgs& A, unsigned long long
 // warp edge and the two ends of a periodic row load them), and the loads of the next row are
 // issued before the current row computes.  Per point: s, d_old, x, cE, cN read once; d, x, q
 // written.
+// One K1 strip (segment bx, rows [j0, j1)): leaves the per-row warp sums in wout[row][warp].
+template <bool SIGMA>
+__device__ __forceinline__ void k1_strip(const KArgs& A, int par, int64_t st, double beta, double alpha, double* wout) {
+    const double* __restrict__ dold = A.d[par];
+    double* __restrict__ dnew = A.d[par ^ 1];
+    const double* __restrict__ s = A.s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int32_t P = A.pitch, ni = A.ni;
+    const int32_t nby = (A.nloc + A.rpb - 1) / A.rpb;
+    const int32_t bx = (int32_t)(st % A.nbx), by = nby - 1 - (int32_t)(st / A.nbx);
+    const int32_t i = bx * kBlock + (int32_t)threadIdx.x;
+    const int32_t j0 = by * A.rpb, j1 = min(j0 + A.rpb, A.nloc);
+    const bool valid = i < ni;
+    const int32_t iw = i == 0 ? ni - 1 : i - 1, ie = i == ni - 1 ? 0 : i + 1;
+    const bool ldw = valid && (lane == 0 || i == 0);
+    const bool lde = valid && (lane == 31 || i == ni - 1);
+    int64_t a = (int64_t)(j0 + 1) * P + i;
+    double dS = 0.0, dC = 0.0, doC = 0.0, cNs = 0.0;
+    double pdo = 0.0, ps = 0.0, pcE = 0.0, pcN = 0.0, px = 0.0;   // next row's loads
+    if (valid) {
+        dS = __fma_rn(beta, dold[a - P], s[a - P]);
+        doC = dold[a];
+        dC = __fma_rn(beta, doC, s[a]);
+        cNs = fabs(A.cN[a - P]);
+        if (j0 == 0) dnew[a - P] = dS;             // southern halo row (multi-rank)
+        pdo = dold[a + P]; ps = s[a + P];
+        pcE = A.cE[a]; pcN = A.cN[a]; px = A.x[a];
+    }
+    for (int32_t j = j0; j < j1; ++j, a += P) {
+        const double doN = pdo, cEp = pcE, cNr = pcN, xv = px;
+        const double dN = __fma_rn(beta, doN, ps);
+        if (valid && j + 1 < j1) {
+            pdo = dold[a + 2 * P]; ps = s[a + 2 * P];
+            pcE = A.cE[a + P]; pcN = A.cN[a + P]; px = A.x[a + P];
+        }
+        double dW = __shfl_up_sync(kFull, dC, 1);
+        double dE = __shfl_down_sync(kFull, dC, 1);
+        double cEw = __shfl_up_sync(kFull, cEp, 1);
+        if (ldw) {
+            const int64_t aw = a - i + iw;
+            dW = __fma_rn(beta, dold[aw], s[aw]);
+            cEw = A.cE[aw];
+        }
+        if (lde) {
+            const int64_t ae = a - i + ie;
+            dE = __fma_rn(beta, dold[ae], s[ae]);
+        }
+        double v = 0.0;
+        if (valid) {
+            const bool land = signbit(cNr);
+            const double cNp = fabs(cNr);
+            double app = __dadd_rn(__dadd_rn(__dadd_rn(cEp, cEw), cNp), cNs);
+            if (SIGMA) app = __dadd_rn(app, A.sigma[a]);
+            double acc = __dmul_rn(app, dC);
+            acc = __fma_rn(-cEw, dW, acc);
+            acc = __fma_rn(-cEp, dE, acc);
+            acc = __fma_rn(-cNs, dS, acc);
+            acc = __fma_rn(-cNp, dN, acc);
+            const double qv = land ? 0.0 : acc;
+            dnew[a] = dC;
+            A.q[a] = qv;
+            A.x[a] = __fma_rn(alpha, doC, xv);
+            v = __dmul_rn(dC, qv);
+            cNs = cNp;
+        }
+        v = warp_tree(v);
+        if (lane == 0) wout[(j - j0) * kWarps + warp] = v;
+        dS = dC;
+        dC = dN;
+        doC = doN;
+    }
+    if (valid && j1 == A.nloc) dnew[a] = dC;       // northern halo row (multi-rank)
+}
+
 #ifndef PCG_MINB_K1
 #define PCG_MINB_K1 4
 #endif
@@ -281,11 +357,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
     __shared__ double wrow[kMaxRowsK1][kWarps];
     __shared__ long long s_next;
     const double beta = A.sc->beta, alpha = A.sc->alpha;
-    const double* __restrict__ dold = A.d[par];
-    double* __restrict__ dnew = A.d[par ^ 1];
-    const double* __restrict__ s = A.s;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int32_t P = A.pitch, ni = A.ni;
     const int32_t nby = (A.nloc + A.rpb - 1) / A.rpb;
     const int64_t S = (int64_t)nby * A.nbx;
     // strips come from an atomic ticket (A.dynamic_k1) or a block stride
@@ -304,73 +376,9 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
             __syncthreads();                               // everyone has read s_next
             if (threadIdx.x == 0) s_next = (long long)atomicAdd(&A.sc->ticket[0], 1ull);
         }
+        k1_strip<SIGMA>(A, par, st, beta, alpha, dyn ? &wrow[0][0] : &ws[kslot * kWarps]);
         const int32_t bx = (int32_t)(st % A.nbx), by = nby - 1 - (int32_t)(st / A.nbx);
-        const int32_t i = bx * kBlock + (int32_t)threadIdx.x;
         const int32_t j0 = by * A.rpb, j1 = min(j0 + A.rpb, A.nloc);
-        const bool valid = i < ni;
-        const int32_t iw = i == 0 ? ni - 1 : i - 1, ie = i == ni - 1 ? 0 : i + 1;
-        const bool ldw = valid && (lane == 0 || i == 0);
-        const bool lde = valid && (lane == 31 || i == ni - 1);
-        int64_t a = (int64_t)(j0 + 1) * P + i;
-        double dS = 0.0, dC = 0.0, doC = 0.0, cNs = 0.0;
-        double pdo = 0.0, ps = 0.0, pcE = 0.0, pcN = 0.0, px = 0.0;   // next row's loads
-        if (valid) {
-            dS = __fma_rn(beta, dold[a - P], s[a - P]);
-            doC = dold[a];
-            dC = __fma_rn(beta, doC, s[a]);
-            cNs = fabs(A.cN[a - P]);
-            if (j0 == 0) dnew[a - P] = dS;             // southern halo row (multi-rank)
-            pdo = dold[a + P]; ps = s[a + P];
-            pcE = A.cE[a]; pcN = A.cN[a]; px = A.x[a];
-        }
-        for (int32_t j = j0; j < j1; ++j, a += P) {
-            const double doN = pdo, cEp = pcE, cNr = pcN, xv = px;
-            const double dN = __fma_rn(beta, doN, ps);
-            if (valid && j + 1 < j1) {
-                pdo = dold[a + 2 * P]; ps = s[a + 2 * P];
-                pcE = A.cE[a + P]; pcN = A.cN[a + P]; px = A.x[a + P];
-            }
-            double dW = __shfl_up_sync(kFull, dC, 1);
-            double dE = __shfl_down_sync(kFull, dC, 1);
-            double cEw = __shfl_up_sync(kFull, cEp, 1);
-            if (ldw) {
-                const int64_t aw = a - i + iw;
-                dW = __fma_rn(beta, dold[aw], s[aw]);
-                cEw = A.cE[aw];
-            }
-            if (lde) {
-                const int64_t ae = a - i + ie;
-                dE = __fma_rn(beta, dold[ae], s[ae]);
-            }
-            double v = 0.0;
-            if (valid) {
-                const bool land = signbit(cNr);
-                const double cNp = fabs(cNr);
-                double app = __dadd_rn(__dadd_rn(__dadd_rn(cEp, cEw), cNp), cNs);
-                if (SIGMA) app = __dadd_rn(app, A.sigma[a]);
-                double acc = __dmul_rn(app, dC);
-                acc = __fma_rn(-cEw, dW, acc);
-                acc = __fma_rn(-cEp, dE, acc);
-                acc = __fma_rn(-cNs, dS, acc);
-                acc = __fma_rn(-cNp, dN, acc);
-                const double qv = land ? 0.0 : acc;
-                dnew[a] = dC;
-                A.q[a] = qv;
-                A.x[a] = __fma_rn(alpha, doC, xv);
-                v = __dmul_rn(dC, qv);
-                cNs = cNp;
-            }
-            v = warp_tree(v);
-            if (dyn) {
-                if (lane == 0) wrow[j - j0][warp] = v;
-            } else if (lane == 0) {
-                ws[(kslot + j - j0) * kWarps + warp] = v;
-            }
-            dS = dC;
-            dC = dN;
-            doC = doN;
-        }
-        if (valid && j1 == A.nloc) dnew[a] = dC;       // northern halo row (multi-rank)
         if (dyn) {
             __syncthreads();
             if (warp == 0)                                 // row partials of this strip
@@ -425,14 +433,53 @@ __device__ __forceinline__ void ld_nc_f64x4(const double* p, double (&z)[4]) {
                  : "=d"(z[0]), "=d"(z[1]), "=d"(z[2]), "=d"(z[3]) : "l"(p));
 }
 
+// Overflow entries of a long row (near the pole: up to ~80 at ORCA025), continuing the fma chain.
+// Four entries per round, the next round's column/value loads issued before this round's
+// gathers, so a long row costs about one L2 round trip per 4 entries -- a plain loop is two
+// dependent memory latencies per entry, and those pole warps set the kernel time.
+template <class Gather>
+__device__ __forceinline__ double overflow_sum(const EllDev& E, int64_t e, double acc, Gather gat) {
+    const int64_t sl = e >> 5;
+    const int64_t o0 = __ldg(E.ooff + sl);
+    const int L = (int)((__ldg(E.ooff + sl + 1) - o0) >> 5);
+    if (L == 0) return acc;
+    const int32_t* cp = E.ocol + o0 + (e & 31);
+    const double* vp = E.oval + o0 + (e & 31);
+    int32_t cn[4];
+    double zn[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int64_t m = (int64_t)min(u, L - 1) << 5;
+        cn[u] = __ldg(cp + m);
+        zn[u] = __ldg(vp + m);
+    }
+    for (int m0 = 0; m0 < L; m0 += 4) {
+        int32_t c[4];
+        double z[4], x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { c[u] = cn[u]; z[u] = zn[u]; }
+        if (m0 + 4 < L) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t m = (int64_t)min(m0 + 4 + u, L - 1) << 5;
+                cn[u] = __ldg(cp + m);
+                zn[u] = __ldg(vp + m);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = gat(c[u]);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc = __fma_rn(m0 + u < L ? z[u] : 0.0, x[u], acc);
+    }
+    return acc;
+}
+
 template <class Gather>
 __device__ __forceinline__ double ell_row(const EllDev& E, int64_t e, Gather gat) {
     double z[kEll], x[kEll];
     const int4 cv = __ldg(reinterpret_cast<const int4*>(E.col) + e);
     ld_nc_f64x4(E.val + e * kEll, z);
     const int32_t c[kEll] = {cv.x, cv.y, cv.z, cv.w};
-    const int64_t sl = e >> 5;
-    const int64_t o0 = __ldg(E.ooff + sl), o1 = __ldg(E.ooff + sl + 1);
 #pragma unroll
     for (int m = 0; m < kEll; ++m) x[m] = gat(c[m]);
     // schedule pin (emits nothing): the fma chain may only start once all four gathers have
@@ -441,8 +488,7 @@ __device__ __forceinline__ double ell_row(const EllDev& E, int64_t e, Gather gat
     double acc = 0.0;
 #pragma unroll
     for (int m = 0; m < kEll; ++m) acc = __fma_rn(z[m], x[m], acc);
-    for (int64_t p = o0 + (e & 31); p < o1; p += 32) acc = __fma_rn(__ldg(E.oval + p), gat(__ldg(E.ocol + p)), acc);
-    return acc;
+    return overflow_sum(E, e, acc, gat);
 }
 
 #ifndef PCG_MINB_K2
@@ -538,6 +584,440 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
             else if (init) fin_init(A, tot, A.sc->red[2]);
             else fin_iter(A, tot, A.sc->red[2]);
         }
+    }
+}
+
+// ---- TMA bulk-copy pipeline for K2 / K3 ---------------------------------------
+// Block = 8 consumer warps (the 256 columns of a unit) + 1 producer warp.  The producer takes
+// units from the atomic ticket and streams each unit's contiguous arrays (ELL columns and values,
+// the unit's own vector entries) into a kStages ring of shared memory with cp.async.bulk, signalled
+// by mbarriers (SASS UBLKCP / SYNCS).  Consumers compute from shared memory (gathers of the
+// neighbouring points stay L1/L2 loads), leave their 8 warp sums in the stage and release it;
+// the producer, waiting for that stage anyway, completes the unit's partial (second level of the
+// block tree).  The main loop has no __syncthreads.
+#ifndef PCG_TMA_STAGES
+#define PCG_TMA_STAGES 4
+#endif
+#ifndef PCG_TMA_MINB
+#define PCG_TMA_MINB 2
+#endif
+constexpr int kStages = PCG_TMA_STAGES;
+constexpr uint32_t kSentinel = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+            smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
+}
+
+template <int NVEC>
+struct TmaStage {
+    int4 col[kBlock];                 // ELL column slots (array indices)
+    double4 val[kBlock];              // ELL values
+    double vec[NVEC][kBlock];         // the unit's own entries of NVEC vectors
+};
+
+template <int NVEC>
+struct TmaSmem {
+    TmaStage<NVEC> st[kStages];
+    uint64_t full[kStages], empty[kStages];
+    uint32_t unit[kStages];
+    double wsum[kStages][kWarps];
+};
+
+template <int NVEC>
+size_t tma_smem_bytes() { return sizeof(TmaSmem<NVEC>); }
+
+// Producer side: stream unit u's arrays into stage s.
+template <int NVEC>
+__device__ __forceinline__ void tma_fill(TmaSmem<NVEC>& S, int s, const KArgs& A, const EllDev& E, int64_t u,
+                                         const double* const (&vecs)[NVEC]) {
+    const int32_t bx = (int32_t)(u % A.nbx), j = A.nloc - 1 - (int32_t)(u / A.nbx);
+    const int32_t nel = min(kBlock, A.pitch - bx * kBlock);
+    const int64_t e0 = (int64_t)j * A.pitch + (int64_t)bx * kBlock;
+    mbar_expect_tx(&S.full[s], (unsigned)nel * (16u + 32u + 8u * NVEC));
+    bulk_g2s(S.st[s].col, E.col + e0 * kEll, (unsigned)nel * 16u, &S.full[s]);
+    bulk_g2s(S.st[s].val, E.val + e0 * kEll, (unsigned)nel * 32u, &S.full[s]);
+#pragma unroll
+    for (int v = 0; v < NVEC; ++v) bulk_g2s(S.st[s].vec[v], vecs[v] + e0 + A.pitch, (unsigned)nel * 8u, &S.full[s]);
+}
+
+// Complete unit u's partial from the 8 warp sums left in stage s (producer warp, all lanes).
+template <int NVEC>
+__device__ __forceinline__ void tma_finalize(const TmaSmem<NVEC>& S, int s, const KArgs& A, double* partial) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t u = S.unit[s];
+    double w = lane < kWarps ? S.wsum[s][lane] : 0.0;
+    w = warp_tree(w);
+    if (lane == 0) {
+        const int32_t bx = (int32_t)(u % A.nbx), j = A.nloc - 1 - (int32_t)(u / A.nbx);
+        partial[(int64_t)j * A.nbx + bx] = w;
+    }
+}
+
+template <int NVEC, class Consume>
+__device__ __forceinline__ void tma_pipeline(TmaSmem<NVEC>& S, const KArgs& A, const EllDev& E,
+                                             const double* const (&vecs)[NVEC], unsigned long long* ticket,
+                                             double* partial, Consume consume) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t U = n_units(A);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], kWarps); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kWarps) {                                  // ---- producer warp
+        int it = 0;
+        unsigned long long u_next = 0;                     // ticket prefetched one unit ahead
+        if (lane == 0) u_next = atomicAdd(ticket, 1ull);
+        for (;; ++it) {
+            const int s = it % kStages;
+            if (it >= kStages) {                           // stage reuse: wait for its consumers
+                mbar_wait(&S.empty[s], ((it / kStages) - 1) & 1);
+                tma_finalize(S, s, A, partial);
+            }
+            unsigned long long u = __shfl_sync(kFull, u_next, 0);
+            if (lane == 0 && (int64_t)u < U) u_next = atomicAdd(ticket, 1ull);
+            if (lane == 0) {
+                if ((int64_t)u >= U) {
+                    S.unit[s] = kSentinel;
+                    mbar_arrive(&S.full[s]);
+                } else {
+                    S.unit[s] = (uint32_t)u;
+                    tma_fill(S, s, A, E, (int64_t)u, vecs);
+                }
+            }
+            if ((int64_t)u >= U) break;
+        }
+        for (int k = max(0, it - kStages + 1); k < it; ++k) {   // drain: finalize units still in flight
+            const int s = k % kStages;
+            mbar_wait(&S.empty[s], (k / kStages) & 1);
+            tma_finalize(S, s, A, partial);
+        }
+    } else {                                               // ---- consumer warps
+        for (int it = 0;; ++it) {
+            const int s = it % kStages;
+            mbar_wait(&S.full[s], (it / kStages) & 1);
+            const uint32_t u = S.unit[s];
+            if (u == kSentinel) break;
+            const int32_t bx = (int32_t)(u % A.nbx), j = A.nloc - 1 - (int32_t)(u / A.nbx);
+            const int32_t i = bx * kBlock + (int32_t)threadIdx.x;
+            double v = 0.0;
+            if (i < A.pitch) v = consume(S.st[s], (int)threadIdx.x, i, j);
+            v = warp_tree(v);
+            if (lane == 0) S.wsum[s][warp] = v;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&S.empty[s]);
+        }
+    }
+}
+
+// row sum of the ELL slots staged in shared memory + overflow from global memory
+template <class Gather>
+__device__ __forceinline__ double ell_row_smem(const EllDev& E, int4 cv, double4 zv, int64_t e, Gather gat) {
+    double x0 = gat(cv.x), x1 = gat(cv.y), x2 = gat(cv.z), x3 = gat(cv.w);
+    double acc = __fma_rn(zv.x, x0, 0.0);
+    acc = __fma_rn(zv.y, x1, acc);
+    acc = __fma_rn(zv.z, x2, acc);
+    acc = __fma_rn(zv.w, x3, acc);
+    return overflow_sum(E, e, acc, gat);
+}
+
+__global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k2_tma_kernel(const KArgs A, const int par, const int init) {
+    if (!is_active(A)) return;
+    double alpha;
+    if (!get_alpha(A, init, alpha)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
+        return;
+    }
+    extern __shared__ __align__(128) unsigned char smraw[];
+    auto& S = *reinterpret_cast<TmaSmem<3>*>(smraw);
+    const double* __restrict__ ro = A.r[par];
+    double* __restrict__ rn = A.r[par ^ 1];
+    const double* __restrict__ q = A.q;
+    const double* const vecs[3] = {A.q, ro, A.piv};
+    tma_pipeline<3>(S, A, A.zt, vecs, &A.sc->ticket[1], A.partial[1], [&](const TmaStage<3>& st, int t, int32_t i, int32_t j) {
+        const int64_t a = (int64_t)(j + 1) * A.pitch + i;
+        const double rnew = __fma_rn(-alpha, st.vec[0][t], st.vec[1][t]);
+        const double acc = ell_row_smem(A.zt, st.col[t], st.val[t], a - A.pitch,
+                                        [&](int32_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); });
+        A.t[a] = __ddiv_rn(acc, st.vec[2][t]);
+        rn[a] = rnew;
+        return __dmul_rn(rnew, rnew);
+    });
+    if (count_block(&A.sc->counter[1])) {
+        const double tot = final_sum(A.partial[1], n_units(A));
+        if (threadIdx.x == 0) {
+            if (A.multi) A.sc->loc[2] = tot;
+            else A.sc->red[2] = tot;
+            A.sc->alpha = alpha;
+            A.sc->xpend = init ? 0 : 1;
+            A.sc->counter[1] = 0;
+            A.sc->ticket[1] = 0;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k3_tma_kernel(const KArgs A, const int par, const int init) {
+    if (!is_active(A)) return;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    auto& S = *reinterpret_cast<TmaSmem<1>*>(smraw);
+    const double* __restrict__ t = A.t;
+    const double* const vecs[1] = {A.r[par ^ 1]};
+    tma_pipeline<1>(S, A, A.z, vecs, &A.sc->ticket[2], A.partial[2], [&](const TmaStage<1>& st, int tt, int32_t i, int32_t j) {
+        const int64_t a = (int64_t)(j + 1) * A.pitch + i;
+        const double acc = ell_row_smem(A.z, st.col[tt], st.val[tt], a - A.pitch, [&](int32_t g) { return __ldg(t + g); });
+        A.s[a] = acc;
+        return __dmul_rn(acc, st.vec[0][tt]);
+    });
+    if (count_block(&A.sc->counter[2])) {
+        const double tot = final_sum(A.partial[2], n_units(A));
+        if (threadIdx.x == 0) {
+            A.sc->counter[2] = 0;
+            A.sc->ticket[2] = 0;
+            if (A.multi) A.sc->loc[1] = tot;
+            else if (init) fin_init(A, tot, A.sc->red[2]);
+            else fin_iter(A, tot, A.sc->red[2]);
+        }
+    }
+}
+
+// ---- the whole PCG loop as one cooperative persistent kernel (single rank) ---------------------
+// Phases K1 | K2 | K3 of each iteration are separated by grid barriers; every block then forms
+// the global sums itself (same canonical final sum, so every block holds bitwise the same α, β,
+// ρ, h and takes the same branch).  No launches, no WHILE node and no last-block tails per
+// iteration.  Block 0 records the history and, at exit, the scalars the epilogue reads.
+__device__ __forceinline__ double block_final(const double* partial, int64_t G) {
+    __shared__ double bcast;
+    const double v = final_sum(partial, G);
+    if (threadIdx.x == 0) bcast = v;
+    __syncthreads();
+    const double r = bcast;
+    __syncthreads();
+    return r;
+}
+
+// dynamic units with two dot products per unit (Jacobi / none)
+template <class Body>
+__device__ __forceinline__ void dynamic_units2(const KArgs& A, unsigned long long* ticket, double* p1, double* p2,
+                                               Body body) {
+    __shared__ long long s_next2;
+    __shared__ double w1[kWarps], w2[kWarps];
+    const int64_t U = n_units(A);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_next2 = (long long)atomicAdd(ticket, 1ull);
+    __syncthreads();
+    int64_t u = s_next2;
+    while (u < U) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_next2 = (long long)atomicAdd(ticket, 1ull);
+        const Unit W = unit_of(A, u);
+        double v1, v2;
+        body(W, v1, v2);
+        v1 = warp_tree(v1);
+        v2 = warp_tree(v2);
+        if (lane == 0) { w1[warp] = v1; w2[warp] = v2; }
+        __syncthreads();
+        if (warp == 0) {
+            double a = lane < kWarps ? w1[lane] : 0.0, b = lane < kWarps ? w2[lane] : 0.0;
+            a = warp_tree(a);
+            b = warp_tree(b);
+            if (lane == 0) { p1[(int64_t)W.j * A.nbx + W.bx] = a; p2[(int64_t)W.j * A.nbx + W.bx] = b; }
+        }
+        u = s_next2;
+    }
+}
+
+// Units of a phase: block b takes unit b when there are no more units than blocks (no ticket
+// round trips -- the small-grid, latency-bound case), otherwise dynamic tickets.
+template <class Body>
+__device__ __forceinline__ void phase_units(const KArgs& A, unsigned long long* ticket, double* partial, Body body) {
+    const int64_t U = n_units(A);
+    if (U <= (int64_t)gridDim.x) {
+        __shared__ double wst[kWarps];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        if ((int64_t)blockIdx.x < U) {
+            const Unit W = unit_of(A, blockIdx.x);
+            double v = warp_tree(body(W));
+            if (lane == 0) wst[warp] = v;
+            __syncthreads();
+            if (warp == 0) {
+                double w = lane < kWarps ? wst[lane] : 0.0;
+                w = warp_tree(w);
+                if (lane == 0) partial[(int64_t)W.j * A.nbx + W.bx] = w;
+            }
+        }
+    } else {
+        dynamic_units(A, ticket, partial, body);
+    }
+}
+
+template <class Body>
+__device__ __forceinline__ void phase_units2(const KArgs& A, unsigned long long* ticket, double* p1, double* p2,
+                                             Body body) {
+    const int64_t U = n_units(A);
+    if (U <= (int64_t)gridDim.x) {
+        __shared__ double wa[kWarps], wb[kWarps];
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        if ((int64_t)blockIdx.x < U) {
+            const Unit W = unit_of(A, blockIdx.x);
+            double v1, v2;
+            body(W, v1, v2);
+            v1 = warp_tree(v1);
+            v2 = warp_tree(v2);
+            if (lane == 0) { wa[warp] = v1; wb[warp] = v2; }
+            __syncthreads();
+            if (warp == 0) {
+                double a = lane < kWarps ? wa[lane] : 0.0, b = lane < kWarps ? wb[lane] : 0.0;
+                a = warp_tree(a);
+                b = warp_tree(b);
+                if (lane == 0) { p1[(int64_t)W.j * A.nbx + W.bx] = a; p2[(int64_t)W.j * A.nbx + W.bx] = b; }
+            }
+        }
+    } else {
+        dynamic_units2(A, ticket, p1, p2, body);
+    }
+}
+
+__device__ __forceinline__ double k2_unit(const KArgs& A, const Unit& W, int par, double alpha) {
+    if (!W.inrow) return 0.0;
+    const double* __restrict__ ro = A.r[par];
+    const double* __restrict__ q = A.q;
+    const double rnew = __fma_rn(-alpha, q[W.a], ro[W.a]);
+    const double pv = A.piv[W.a];
+    const double acc = ell_row(A.zt, W.a - A.pitch, [&](int32_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); });
+    A.t[W.a] = __ddiv_rn(acc, pv);
+    A.r[par ^ 1][W.a] = rnew;
+    return __dmul_rn(rnew, rnew);
+}
+
+__device__ __forceinline__ double k3_unit(const KArgs& A, const Unit& W, int par) {
+    if (!W.inrow) return 0.0;
+    const double* __restrict__ t = A.t;
+    const double rv = A.r[par ^ 1][W.a];
+    const double acc = ell_row(A.z, W.a - A.pitch, [&](int32_t g) { return __ldg(t + g); });
+    A.s[W.a] = acc;
+    return __dmul_rn(acc, rv);
+}
+
+#ifndef PCG_MINB_LOOP
+#define PCG_MINB_LOOP 4
+#endif
+
+template <bool SIGMA>
+__global__ void __launch_bounds__(kBlock, PCG_MINB_LOOP) loop_kernel(const KArgs A) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double wrow[kMaxRowsK1][kWarps];
+    __shared__ long long s_next;
+    DevScalars* sc = A.sc;
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    double rho = sc->rho, beta = sc->beta, alpha = sc->alpha;
+    const double nb = sc->nb, tol = sc->tol;
+    int k = sc->k, status = sc->status, xpend = 0;
+    const int maxit = sc->maxit;
+    bool active = sc->active != 0;
+    const int64_t U = n_units(A);
+    const int32_t nby = (A.nloc + A.rpb - 1) / A.rpb;
+    const int64_t S = (int64_t)nby * A.nbx;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int par = 0;
+    while (active) {
+        // ---- K1: strips from ticket[0] (block b takes strip b when S <= gridDim)
+        const bool st_static = S <= (int64_t)gridDim.x;
+        int64_t st;
+        if (st_static) {
+            st = blockIdx.x;
+        } else {
+            if (threadIdx.x == 0) s_next = (long long)atomicAdd(&sc->ticket[0], 1ull);
+            __syncthreads();
+            st = s_next;
+        }
+        while (st < S) {
+            if (!st_static) {
+                __syncthreads();
+                if (threadIdx.x == 0) s_next = (long long)atomicAdd(&sc->ticket[0], 1ull);
+            }
+            k1_strip<SIGMA>(A, par, st, beta, alpha, &wrow[0][0]);
+            __syncthreads();
+            if (warp == 0) {
+                const int32_t bx = (int32_t)(st % A.nbx), by = nby - 1 - (int32_t)(st / A.nbx);
+                const int32_t j0 = by * A.rpb, j1 = min(j0 + A.rpb, A.nloc);
+                for (int32_t j = j0; j < j1; ++j) {
+                    double w = lane < kWarps ? wrow[j - j0][lane] : 0.0;
+                    w = warp_tree(w);
+                    if (lane == 0) A.partial[0][(int64_t)j * A.nbx + bx] = w;
+                }
+            }
+            st = st_static ? S : s_next;
+        }
+        xpend = 0;                                         // x += alpha_prev d_old done
+        grid.sync();
+        if (lead) sc->ticket[0] = 0;
+        const double gamma = block_final(A.partial[0], U);
+        if (!(gamma > 0.0) || !isfinite(gamma)) { status = kStBreakdown; break; }
+        alpha = __ddiv_rn(rho, gamma);
+        // ---- K2 (+ K3)
+        if (A.precond == 0) {
+            phase_units(A, &sc->ticket[1], A.partial[1], [&](const Unit& W) { return k2_unit(A, W, par, alpha); });
+            grid.sync();
+            if (lead) sc->ticket[1] = 0;
+            phase_units(A, &sc->ticket[2], A.partial[2], [&](const Unit& W) { return k3_unit(A, W, par); });
+            grid.sync();
+            if (lead) sc->ticket[2] = 0;
+        } else {
+            const bool none = A.precond == 2;
+            phase_units2(A, &sc->ticket[1], A.partial[1], A.partial[2], [&](const Unit& W, double& v1, double& v2) {
+                v1 = 0.0;
+                v2 = 0.0;
+                if (!W.inrow) return;
+                const double rnew = __fma_rn(-alpha, A.q[W.a], A.r[par][W.a]);
+                const double sv = none ? rnew : __ddiv_rn(rnew, A.diag[W.a]);
+                A.s[W.a] = sv;
+                A.r[par ^ 1][W.a] = rnew;
+                v1 = __dmul_rn(rnew, rnew);
+                v2 = __dmul_rn(sv, rnew);
+            });
+            grid.sync();
+            if (lead) sc->ticket[1] = 0;
+        }
+        const double rr = block_final(A.partial[1], U);
+        const double rho_new = block_final(A.partial[2], U);
+        k += 1;
+        xpend = 1;
+        if (!isfinite(rho_new) || !isfinite(rr)) {
+            if (lead && k < A.hist_cap) A.hist[k] = NAN;
+            status = kStBreakdown;
+            break;
+        }
+        beta = __ddiv_rn(rho_new, rho);
+        rho = rho_new;
+        const double h = __ddiv_rn(__dsqrt_rn(rr), nb);
+        if (lead && k < A.hist_cap) A.hist[k] = h;
+        active = (h > tol) && (k < maxit);
+        par ^= 1;
+    }
+    if (lead) {
+        sc->k = k; sc->alpha = alpha; sc->beta = beta; sc->rho = rho;
+        sc->xpend = xpend; sc->status = status; sc->active = 0;
     }
 }
 
@@ -749,6 +1229,26 @@ void configure_kernels(KArgs& A, int sms) {
     A.g_k3 = persistent_grid(k3_ainv_kernel, U, sms, 2048);
     A.g_kd = persistent_grid(k2_diag_kernel, U, sms, 4096);
     A.g_row = persistent_grid(init_residual_kernel, U, sms, 2048);
+    A.tma = 0;                                         // measured no faster than the LDG path (r01)
+    if (const char* e = getenv("PCG_TMA")) A.tma = atoi(e) != 0;
+    {
+        int bl = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bl, A.sigma ? (const void*)loop_kernel<true> : (const void*)loop_kernel<false>,
+                                                      kBlock, 0);
+        // cooperative (every block co-resident), no more blocks than the largest phase has units
+        const int64_t work = std::max<int64_t>(U, S);
+        A.g_loop = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(bl, 1) * sms, work));
+    }
+    {
+        const size_t s2 = tma_smem_bytes<3>(), s3 = tma_smem_bytes<1>();
+        cudaFuncSetAttribute(k2_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
+        cudaFuncSetAttribute(k3_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s3);
+        int b2 = 1, b3 = 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2_tma_kernel, kBlock + 32, s2);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, k3_tma_kernel, kBlock + 32, s3);
+        A.g_t2 = (int)std::max<int64_t>(1, std::min<int64_t>(U, (int64_t)std::max(b2, 1) * sms));
+        A.g_t3 = (int)std::max<int64_t>(1, std::min<int64_t>(U, (int64_t)std::max(b3, 1) * sms));
+    }
     allow_smem(k1_kernel<false>, k1_smem(A, A.g_k1));
     allow_smem(k1_kernel<true>, k1_smem(A, A.g_k1));
     allow_smem(k2_ainv_kernel, row_smem(A, A.g_k2, 1));
@@ -765,10 +1265,12 @@ void launch_k1(const KArgs& A, int par, cudaStream_t st) {
     else k1_kernel<false><<<A.g_k1, kBlock, k1_smem(A, A.g_k1), st>>>(A, par);
 }
 void launch_k2_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
-    k2_ainv_kernel<<<A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st>>>(A, par, init);
+    if (A.tma) k2_tma_kernel<<<A.g_t2, kBlock + 32, tma_smem_bytes<3>(), st>>>(A, par, init);
+    else k2_ainv_kernel<<<A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st>>>(A, par, init);
 }
 void launch_k3_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
-    k3_ainv_kernel<<<A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st>>>(A, par, init);
+    if (A.tma) k3_tma_kernel<<<A.g_t3, kBlock + 32, tma_smem_bytes<1>(), st>>>(A, par, init);
+    else k3_ainv_kernel<<<A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st>>>(A, par, init);
 }
 void launch_k2_diag(const KArgs& A, int par, int init, int none, cudaStream_t st) {
     k2_diag_kernel<<<A.g_kd, kBlock, row_smem(A, A.g_kd, 2), st>>>(A, par, init, none);
@@ -789,6 +1291,11 @@ void launch_apply(const KArgs& A, const double* x, double* y, cudaStream_t st) {
     apply_kernel<<<(unsigned)grid_blocks(A), kBlock, 0, st>>>(A, x, y);
 }
 void launch_scalar(const KArgs& A, int step, cudaStream_t st) { scalar_kernel<<<1, 1, 0, st>>>(A, step); }
+cudaError_t launch_loop(const KArgs& A, cudaStream_t st) {
+    void* args[] = {(void*)&A};
+    const void* fn = A.sigma ? (const void*)loop_kernel<true> : (const void*)loop_kernel<false>;
+    return cudaLaunchCooperativeKernel(fn, dim3(A.g_loop), dim3(kBlock), args, 0, st);
+}
 void launch_set_cond(cudaGraphConditionalHandle h, cudaStream_t st) { set_cond_kernel<<<1, 1, 0, st>>>(h); }
 
 }  // namespace pcg

@@ -35,6 +35,9 @@ struct KArgs {
     int32_t nbx, rpb;                 // column segments of kBlock per row; rows per K1 strip
     int32_t g_k1, g_k2, g_k3, g_kd, g_row;   // persistent grid sizes (configure_kernels)
     int32_t dynamic, dynamic_k1;      // units from an atomic ticket instead of a block stride
+    int32_t tma, g_t2, g_t3;          // K2/K3 through the TMA bulk-copy pipeline; its grid sizes
+    int32_t g_loop;                   // cooperative grid of the fused loop kernel
+    int32_t precond;                  // pcg_precond
     int64_t nel;                      // owned elements nloc * pitch
     const double *cE, *cN, *sigma, *diag, *piv;
     EllDev zt, z;                     // rows of Z^T (K2) and of Z (K3)
@@ -69,5 +72,6 @@ enum ScalarStep : int32_t { kSsBB = 0, kSsGamma = 1, kSsInit = 2, kSsIter = 3, k
 void launch_scalar(const KArgs& A, int step, cudaStream_t st);
 void launch_set_cond(cudaGraphConditionalHandle h, cudaStream_t st);
 void configure_kernels(KArgs& A, int sms);
+cudaError_t launch_loop(const KArgs& A, cudaStream_t st);   // whole PCG loop, cooperative (1 rank)
 
 }  // namespace pcg

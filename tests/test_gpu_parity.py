@@ -129,6 +129,26 @@ def test_partitioned_preconditioner_bitwise(parts, halo):
     S.close()
 
 
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_all_drivers_bitwise_equal(name):
+    """Fused cooperative loop, WHILE-node graph, host loop and the NCCL (1-rank) path run the
+    same arithmetic: identical iterations, histories and x."""
+    import os
+    p = synth.config(name)
+    A, M, S = setup_pair(p)
+    b = dev(A.to_grid(rhs(A, p)))
+    res = {}
+    for fused in ("1", "0"):
+        os.environ["PCG_FUSED"] = fused
+        try:
+            res[fused] = S.solve(b, tol=1e-10, maxit=A.n)
+        finally:
+            del os.environ["PCG_FUSED"]
+    assert res["1"][1] == res["0"][1] and np.array_equal(res["1"][2], res["0"][2])
+    assert torch.equal(res["1"][0], res["0"][0])
+    S.close()
+
+
 def test_host_loop_and_comm_path_match_graph():
     p = synth.config("cfg2")
     A, M, S = setup_pair(p)
