@@ -120,6 +120,13 @@ __device__ __forceinline__ void stop(const KArgs& A, int status) {
     set_cond(A, 0);
 }
 
+// Programmatic dependent launch (PDL): an iteration kernel is launched while its predecessor
+// drains; griddepcontrol.wait blocks until the predecessor has completed and its writes are
+// visible (a no-op for a normal launch), launch_dependents lets the successor's blocks start as
+// soon as every block of this kernel has finished its units.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // The flag only changes between launches (or in the last block of a reduction, after every
 // other block has read it), so a cached read is exact.
 __device__ __forceinline__ bool is_active(const KArgs& A) { return __ldg(&A.sc->active) != 0; }
@@ -344,6 +351,7 @@ __device__ __forceinline__ void k1_strip(const KArgs& A, int par, int64_t st, do
 #endif
 template <bool SIGMA>
 __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, const int par) {
+    pdl_wait();
     if (!is_active(A)) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         // safety net: the WHILE node ends even if a reduction never clears the flag
@@ -408,6 +416,88 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
             }
         }
     }
+    pdl_trigger();
+    if (count_block(&A.sc->counter[0])) {
+        const double tot = final_sum(A.partial[0], n_units(A));
+        if (threadIdx.x == 0) {
+            if (A.multi) A.sc->loc[0] = tot;
+            else A.sc->red[0] = tot;
+            A.sc->xpend = 0;
+            A.sc->counter[0] = 0;
+            A.sc->ticket[0] = 0;
+        }
+    }
+}
+
+#ifndef PCG_MINB_K1F
+#define PCG_MINB_K1F 6
+#endif
+// ---- K1, row-segment form: one element per thread, units from the dynamic ticket ----------------
+// Same arithmetic as k1_strip (bitwise): d at the point and at its S/N neighbours recomputed from
+// s and d_old, E/W neighbours by shuffle (warp-edge lanes and the periodic seam load them).
+template <bool SIGMA>
+__device__ __forceinline__ double k1_point(const KArgs& A, const Unit& W, int par, double beta, double alpha) {
+    const double* __restrict__ dold = A.d[par];
+    double* __restrict__ dnew = A.d[par ^ 1];
+    const double* __restrict__ s = A.s;
+    const int lane = threadIdx.x & 31;
+    const int32_t P = A.pitch, ni = A.ni, i = W.i;
+    const bool valid = W.valid;
+    const int64_t a = W.a;
+    double dC = 0.0, dS = 0.0, dN = 0.0, doC = 0.0, cEp = 0.0, cNr = 0.0, cNs = 0.0, xv = 0.0;
+    if (valid) {
+        doC = dold[a];
+        const double sC = s[a], dSo = dold[a - P], sS = s[a - P], dNo = dold[a + P], sN = s[a + P];
+        cEp = A.cE[a]; cNr = A.cN[a]; cNs = fabs(A.cN[a - P]); xv = A.x[a];
+        dC = __fma_rn(beta, doC, sC);
+        dS = __fma_rn(beta, dSo, sS);
+        dN = __fma_rn(beta, dNo, sN);
+    }
+    double dW = __shfl_up_sync(kFull, dC, 1);
+    double dE = __shfl_down_sync(kFull, dC, 1);
+    double cEw = __shfl_up_sync(kFull, cEp, 1);
+    if (valid && (lane == 0 || i == 0)) {
+        const int64_t aw = a - i + (i == 0 ? ni - 1 : i - 1);
+        dW = __fma_rn(beta, dold[aw], s[aw]);
+        cEw = A.cE[aw];
+    }
+    if (valid && (lane == 31 || i == ni - 1)) {
+        const int64_t ae = a - i + (i == ni - 1 ? 0 : i + 1);
+        dE = __fma_rn(beta, dold[ae], s[ae]);
+    }
+    if (!valid) return 0.0;
+    const bool land = signbit(cNr);
+    const double cNp = fabs(cNr);
+    double app = __dadd_rn(__dadd_rn(__dadd_rn(cEp, cEw), cNp), cNs);
+    if (SIGMA) app = __dadd_rn(app, A.sigma[a]);
+    double acc = __dmul_rn(app, dC);
+    acc = __fma_rn(-cEw, dW, acc);
+    acc = __fma_rn(-cEp, dE, acc);
+    acc = __fma_rn(-cNs, dS, acc);
+    acc = __fma_rn(-cNp, dN, acc);
+    const double qv = land ? 0.0 : acc;
+    dnew[a] = dC;
+    A.q[a] = qv;
+    A.x[a] = __fma_rn(alpha, doC, xv);
+    if (W.j == 0) dnew[a - P] = dS;                     // halo rows (multi-rank)
+    if (W.j == A.nloc - 1) dnew[a + P] = dN;
+    return __dmul_rn(dC, qv);
+}
+
+template <bool SIGMA>
+__global__ void __launch_bounds__(kBlock, PCG_MINB_K1F) k1_flat_kernel(const KArgs A, const int par) {
+    pdl_wait();
+    if (!is_active(A)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (++A.sc->guard > A.sc->maxit + 2) {          // safety net for the WHILE node
+            A.sc->active = 0;
+            A.sc->status = kStBreakdown;
+            set_cond(A, 0);
+        }
+    }
+    const double beta = A.sc->beta, alpha = A.sc->alpha;
+    dynamic_units(A, &A.sc->ticket[0], A.partial[0], [&](const Unit& W) { return k1_point<SIGMA>(A, W, par, beta, alpha); });
+    pdl_trigger();
     if (count_block(&A.sc->counter[0])) {
         const double tot = final_sum(A.partial[0], n_units(A));
         if (threadIdx.x == 0) {
@@ -503,6 +593,7 @@ __device__ __forceinline__ double ell_row(const EllDev& E, int64_t e, Gather gat
 // r_new at a gathered point c is recomputed as fma(-alpha, q_c, r_old_c) (bitwise the value
 // its own thread stores), so no grid-wide barrier is needed between the update and the gather.
 __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArgs A, const int par, const int init) {
+    pdl_wait();
     if (!is_active(A)) return;
     double alpha;
     if (!get_alpha(A, init, alpha)) {
@@ -529,6 +620,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
     bool last;
     if (A.dynamic) {
         dynamic_units(A, &A.sc->ticket[1], A.partial[1], body);
+        pdl_trigger();
         last = count_block(&A.sc->counter[1]);
     } else {
         const int64_t U = n_units(A);
@@ -551,6 +643,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
 
 // ---- K3 (AINV): s = Z t ; (s, r) ; beta / history / flag -----------------------------------
 __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArgs A, const int par, const int init) {
+    pdl_wait();
     if (!is_active(A)) return;
     extern __shared__ double ws[];
     const double* __restrict__ rn = A.r[par ^ 1];
@@ -568,6 +661,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
     bool last;
     if (A.dynamic) {
         dynamic_units(A, &A.sc->ticket[2], A.partial[2], body);
+        pdl_trigger();
         last = count_block(&A.sc->counter[2]);
     } else {
         const int64_t U = n_units(A);
@@ -742,6 +836,7 @@ __device__ __forceinline__ double ell_row_smem(const EllDev& E, int4 cv, double4
 }
 
 __global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k2_tma_kernel(const KArgs A, const int par, const int init) {
+    pdl_wait();
     if (!is_active(A)) return;
     double alpha;
     if (!get_alpha(A, init, alpha)) {
@@ -777,6 +872,7 @@ __global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k2_tma_kernel(const
 }
 
 __global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k3_tma_kernel(const KArgs A, const int par, const int init) {
+    pdl_wait();
     if (!is_active(A)) return;
     extern __shared__ __align__(128) unsigned char smraw[];
     auto& S = *reinterpret_cast<TmaSmem<1>*>(smraw);
@@ -1024,6 +1120,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_LOOP) loop_kernel(const KArgs
 // ---- K2 (Jacobi / none): r -= alpha q ; s = r / A_pp (or r) ; (r, r), (s, r) ---------------
 __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const int par, const int init,
                                                          const int none) {
+    pdl_wait();
     if (!is_active(A)) return;
     double alpha;
     if (!get_alpha(A, init, alpha)) {
@@ -1049,6 +1146,7 @@ __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const in
         put_warp_sum(ws, 2 * k, v1);
         put_warp_sum(ws, 2 * k + 1, v2);
     }
+    pdl_trigger();
     if (finish_units<2>(A, ws, A.partial[1], A.partial[2], &A.sc->counter[1])) {
         const double rr = final_sum(A.partial[1], n_units(A));
         const double rs = final_sum(A.partial[2], n_units(A));
@@ -1229,6 +1327,11 @@ void configure_kernels(KArgs& A, int sms) {
     A.g_k3 = persistent_grid(k3_ainv_kernel, U, sms, 2048);
     A.g_kd = persistent_grid(k2_diag_kernel, U, sms, 4096);
     A.g_row = persistent_grid(init_residual_kernel, U, sms, 2048);
+    A.k1flat = 0;
+    if (const char* e = getenv("PCG_K1FLAT")) A.k1flat = atoi(e) != 0;
+    A.pdl = 1;
+    if (const char* e = getenv("PCG_PDL")) A.pdl = atoi(e) != 0;
+    A.g_k1f = persistent_grid(k1_flat_kernel<false>, U, sms, 0);
     A.tma = 0;                                         // measured no faster than the LDG path (r01)
     if (const char* e = getenv("PCG_TMA")) A.tma = atoi(e) != 0;
     {
@@ -1260,20 +1363,42 @@ void configure_kernels(KArgs& A, int sms) {
 
 int64_t grid_blocks(const KArgs& A) { return (int64_t)A.nbx * A.nloc; }
 
+// Launch an iteration kernel, with the programmatic-stream-serialization attribute when A.pdl.
+template <class... P, class... Args>
+static void launch_pdl(const KArgs& A, void (*kern)(P...), int grid, int block, size_t smem, cudaStream_t st,
+                       Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = A.pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 void launch_k1(const KArgs& A, int par, cudaStream_t st) {
-    if (A.sigma) k1_kernel<true><<<A.g_k1, kBlock, k1_smem(A, A.g_k1), st>>>(A, par);
-    else k1_kernel<false><<<A.g_k1, kBlock, k1_smem(A, A.g_k1), st>>>(A, par);
+    if (A.k1flat) {
+        if (A.sigma) launch_pdl(A, k1_flat_kernel<true>, A.g_k1f, kBlock, 0, st, A, par);
+        else launch_pdl(A, k1_flat_kernel<false>, A.g_k1f, kBlock, 0, st, A, par);
+    } else {
+        if (A.sigma) launch_pdl(A, k1_kernel<true>, A.g_k1, kBlock, k1_smem(A, A.g_k1), st, A, par);
+        else launch_pdl(A, k1_kernel<false>, A.g_k1, kBlock, k1_smem(A, A.g_k1), st, A, par);
+    }
 }
 void launch_k2_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
-    if (A.tma) k2_tma_kernel<<<A.g_t2, kBlock + 32, tma_smem_bytes<3>(), st>>>(A, par, init);
-    else k2_ainv_kernel<<<A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st>>>(A, par, init);
+    if (A.tma) launch_pdl(A, k2_tma_kernel, A.g_t2, kBlock + 32, tma_smem_bytes<3>(), st, A, par, init);
+    else launch_pdl(A, k2_ainv_kernel, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
 }
 void launch_k3_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
-    if (A.tma) k3_tma_kernel<<<A.g_t3, kBlock + 32, tma_smem_bytes<1>(), st>>>(A, par, init);
-    else k3_ainv_kernel<<<A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st>>>(A, par, init);
+    if (A.tma) launch_pdl(A, k3_tma_kernel, A.g_t3, kBlock + 32, tma_smem_bytes<1>(), st, A, par, init);
+    else launch_pdl(A, k3_ainv_kernel, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
 }
 void launch_k2_diag(const KArgs& A, int par, int init, int none, cudaStream_t st) {
-    k2_diag_kernel<<<A.g_kd, kBlock, row_smem(A, A.g_kd, 2), st>>>(A, par, init, none);
+    launch_pdl(A, k2_diag_kernel, A.g_kd, kBlock, row_smem(A, A.g_kd, 2), st, A, par, init, none);
 }
 void launch_prep(const KArgs& A, cudaStream_t st) {
     const int64_t n = (int64_t)(A.nloc + 2) * A.pitch;

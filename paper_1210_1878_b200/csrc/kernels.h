@@ -37,6 +37,8 @@ struct KArgs {
     int32_t dynamic, dynamic_k1;      // units from an atomic ticket instead of a block stride
     int32_t tma, g_t2, g_t3;          // K2/K3 through the TMA bulk-copy pipeline; its grid sizes
     int32_t g_loop;                   // cooperative grid of the fused loop kernel
+    int32_t k1flat, g_k1f;            // K1 in row-segment form (one element per thread)
+    int32_t pdl;                      // programmatic dependent launch of the iteration kernels
     int32_t precond;                  // pcg_precond
     int64_t nel;                      // owned elements nloc * pitch
     const double *cE, *cN, *sigma, *diag, *piv;

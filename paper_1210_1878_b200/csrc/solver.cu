@@ -447,7 +447,13 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     P.piv.clear(); P.piv.shrink_to_fit();
     P.Z = Ell(); P.ZT = Ell();
     P.zrow.clear(); P.zrow.shrink_to_fit(); P.zhat.clear(); P.zhat.shrink_to_fit();
-    if (use_graph(c)) { if (Status s = build_graph(c); !s) return s; }
+    if (use_graph(c)) {
+        if (Status s = build_graph(c); !s) {
+            if (!c->A.pdl) return s;
+            c->A.pdl = 0;                                 // PDL edges not capturable here: plain launches
+            if (Status s2 = build_graph(c); !s2) return s2;
+        }
+    }
     return Status::ok();
 }
 
