@@ -70,6 +70,8 @@ typedef enum {
 #define PCG_FLAG_HOST_LOOP   1  /* drive iterations from the host instead of one CUDA graph
                                    with a device-side WHILE node (results are identical) */
 #define PCG_FLAG_COMM_PATH   2  /* use the multi-rank code path (NCCL) even when nranks == 1 */
+#define PCG_FLAG_LOCAL_RANKS 4  /* this context is one rank of an in-process, one-GPU emulation of a
+                                   multi-rank run (no NCCL); solve with pcg_solve_local_ranks */
 
 /* "grid": geometry of this rank's part of the problem. */
 typedef struct {
@@ -148,6 +150,16 @@ pcg_status pcg_solve(pcg_ctx* ctx, const double* b, const double* x0, double tol
 pcg_status pcg_solve_host(pcg_ctx* ctx, const double* b, const double* x0, double tol,
                           int32_t maxit, double* x, int32_t* iterations, double* res_hist,
                           int32_t hist_cap, pcg_report* report);
+
+/* One-GPU emulation of an n-rank run (testing the multi-rank device path without n GPUs):
+ * ctxs[r] was set up as rank r of n (pcg_partition rows) with PCG_FLAG_LOCAL_RANKS on the same
+ * device.  The host steps all ranks phase by phase on one stream; the allgather of rank sums and
+ * the halo rows are device-to-device copies between the contexts (no kernel waits on another
+ * rank).  Same arithmetic as the NCCL path.  b, x0 (NULL = 0), x: DEVICE pointers to the GLOBAL
+ * [nj][ni] arrays; the other arguments as pcg_solve (report sums n_ocean / nnz_z over ranks). */
+pcg_status pcg_solve_local_ranks(pcg_ctx* const* ctxs, int32_t n, const double* b, const double* x0, double tol,
+                                 int32_t maxit, double* x, int32_t* iterations, double* res_hist,
+                                 int32_t hist_cap, pcg_report* report);
 
 /* NULL-safe.  Frees device memory and graphs; does not free the borrowed comm/stream. */
 void pcg_free(pcg_ctx* ctx);

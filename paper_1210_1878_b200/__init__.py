@@ -28,6 +28,7 @@ STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NOT_SPD", 3: "ERR_BREAKDOWN", 4: "ERR_C
 PRECOND = {"ainv": 0, "jacobi": 1, "none": 2}
 FLAG_HOST_LOOP = 1
 FLAG_COMM_PATH = 2
+FLAG_LOCAL_RANKS = 4
 
 
 class PcgError(RuntimeError):
@@ -61,7 +62,7 @@ class Report(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
-EXPORTS = ["pcg_setup", "pcg_solve", "pcg_solve_host", "pcg_free", "pcg_last_error", "pcg_apply_operator",
+EXPORTS = ["pcg_setup", "pcg_solve", "pcg_solve_host", "pcg_solve_local_ranks", "pcg_free", "pcg_last_error", "pcg_apply_operator",
            "pcg_apply_preconditioner", "pcg_partition", "pcg_layout", "pcg_kernel_times", "pcg_device_bytes",
            "pcg_plan_build", "pcg_plan_free", "pcg_plan_counts", "pcg_plan_export_zhat",
            "pcg_comm_unique_id", "pcg_comm_init_rank", "pcg_comm_destroy"]
@@ -82,6 +83,7 @@ def lib():
     L.pcg_setup.argtypes = [C.POINTER(Coeffs), C.POINTER(Grid), C.POINTER(Opts), C.POINTER(vp)]
     L.pcg_solve.argtypes = [vp, vp, vp, d, i32, vp, C.POINTER(i32), vp, i32, C.POINTER(Report)]
     L.pcg_solve_host.argtypes = L.pcg_solve.argtypes
+    L.pcg_solve_local_ranks.argtypes = [C.POINTER(vp), i32, vp, vp, d, i32, vp, C.POINTER(i32), vp, i32, C.POINTER(Report)]
     L.pcg_free.argtypes = [vp]; L.pcg_free.restype = None
     L.pcg_last_error.argtypes = [vp]; L.pcg_last_error.restype = C.c_char_p
     L.pcg_apply_operator.argtypes = [vp, vp, vp]
@@ -297,6 +299,67 @@ class Solver:
         if getattr(self, "_comm", None) is not None:
             lib().pcg_comm_destroy(self._comm)
             self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class LocalRanks:
+    """One-GPU emulation of an n-rank row-block run (pcg_solve_local_ranks): n contexts, one per
+    row block of `partition`, stepped phase by phase with device-copy exchanges.  Exercises the
+    multi-rank device code path (halo rows, rank sums, rank-ordered tree) without n GPUs."""
+
+    def __init__(self, cE, cN, mask, nranks, *, periodic=True, tau=0.1, precond="ainv", sigma=None, device=None,
+                 setup_threads=0):
+        import torch
+        L = lib()
+        cE, cN, mask, sigma = _host_inputs(cE, cN, mask, sigma)
+        nj, ni = mask.shape
+        self.ni, self.nj, self.n = ni, nj, int(nranks)
+        dev = torch.cuda.current_device() if device is None else int(device)
+        stream = torch.cuda.current_stream(dev)
+        self.rb = partition(ni, nj, mask, self.n)
+        co = Coeffs(_ptr(cE), _ptr(cN), _ptr(sigma), _ptr(mask))
+        self._h = []
+        for r in range(self.n):
+            g = Grid(ni, nj, 1 if periodic else 0, int(self.rb[r]), int(self.rb[r + 1]), r, self.n, None, dev,
+                     stream.cuda_stream)
+            o = _opts(precond, tau, FLAG_LOCAL_RANKS, 0, 0, setup_threads)
+            h = C.c_void_p()
+            rc = L.pcg_setup(C.byref(co), C.byref(g), C.byref(o), C.byref(h))
+            if rc != 0:
+                self.close()
+                _check(rc, None, "pcg_setup")
+            self._h.append(h)
+        p, b, t = C.c_int32(), C.c_int32(), C.c_int32()
+        L.pcg_layout(self._h[0], C.byref(p), C.byref(b), C.byref(t))
+        self.pitch, self.block = p.value, b.value
+
+    def solve(self, b, x0=None, tol=1e-10, maxit=None, x=None, hist_cap=None):
+        import torch
+        if maxit is None:
+            maxit = 10 * self.ni * self.nj
+        assert b.is_cuda and b.dtype == torch.float64 and b.is_contiguous() and tuple(b.shape) == (self.nj, self.ni)
+        x = torch.empty_like(b) if x is None else x
+        cap = int(hist_cap if hist_cap is not None else min(maxit + 1, 1 << 22))
+        hist = np.empty(max(cap, 1))
+        it = C.c_int32()
+        rep = Report()
+        arr = (C.c_void_p * self.n)(*[h.value for h in self._h])
+        rc = lib().pcg_solve_local_ranks(arr, self.n, _ptr(b), _ptr(x0), float(tol), int(maxit), _ptr(x), C.byref(it),
+                                         _ptr(hist), cap, C.byref(rep))
+        _check(rc, self._h[0], "pcg_solve_local_ranks")
+        k = it.value
+        return x, k, hist[:min(k + 1, cap)].copy(), rep.as_dict()
+
+    def close(self):
+        for h in getattr(self, "_h", []):
+            if h is not None:
+                lib().pcg_free(h)
+        self._h = []
 
     def __del__(self):
         try:

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -123,65 +124,116 @@ Status halo(pcg_ctx* c, double* arr, bool with_allgather) {
 }
 
 // ---------------------------------------------------------------- one iteration / phases
-Status launch_prologue(pcg_ctx* c) {
-    const KArgs& A = c->A;
-    launch_prep(A, c->st);
-    if (c->multi) {
-        if (Status s = halo(c, c->x, false); !s) return s;
-        launch_init_residual(A, c->st);
-        if (Status s = allgather_loc(c); !s) return s;
-        launch_scalar(A, kSsBB, c->st);
-    } else {
-        launch_init_residual(A, c->st);
+// Each phase is a list of steps: kernel launches on one rank, or an exchange between ranks
+// (allgather of the rank sums; halo rows of x or s).  run_steps() executes them for one context
+// (exchanges through NCCL); run_steps_local() executes them for several contexts of one process
+// on one GPU (exchanges as device copies) -- the multi-rank device code path emulated rank by
+// rank, phase by phase, with no kernel waiting on another.
+enum class Ex { None, Allgather, HaloX, HaloSAllgather };
+struct Step {
+    Ex ex;
+    std::function<void(pcg_ctx*)> run;   // kernels of one rank (ex == None)
+};
+
+std::vector<Step> prologue_steps(const pcg_ctx* c) {
+    std::vector<Step> s;
+    const bool multi = c->multi, ainv = c->plan.precond == PCG_PRECOND_AINV;
+    const bool none = c->plan.precond == PCG_PRECOND_NONE;
+    s.push_back({Ex::None, [](pcg_ctx* x) { launch_prep(x->A, x->st); }});
+    if (multi) s.push_back({Ex::HaloX, nullptr});
+    s.push_back({Ex::None, [](pcg_ctx* x) { launch_init_residual(x->A, x->st); }});
+    if (multi) {
+        s.push_back({Ex::Allgather, nullptr});
+        s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsBB, x->st); }});
     }
-    if (c->plan.precond == PCG_PRECOND_AINV) {
-        launch_k2_ainv(A, 1, 1, c->st);
-        launch_k3_ainv(A, 1, 1, c->st);
-    } else {
-        launch_k2_diag(A, 1, 1, c->plan.precond == PCG_PRECOND_NONE, c->st);
+    if (ainv) s.push_back({Ex::None, [](pcg_ctx* x) { launch_k2_ainv(x->A, 1, 1, x->st); launch_k3_ainv(x->A, 1, 1, x->st); }});
+    else s.push_back({Ex::None, [none](pcg_ctx* x) { launch_k2_diag(x->A, 1, 1, none, x->st); }});
+    if (multi) {
+        s.push_back({Ex::HaloSAllgather, nullptr});
+        s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsInit, x->st); }});
     }
+    return s;
+}
+
+std::vector<Step> iteration_steps(const pcg_ctx* c, int par) {
+    std::vector<Step> s;
+    const bool multi = c->multi, ainv = c->plan.precond == PCG_PRECOND_AINV;
+    const bool none = c->plan.precond == PCG_PRECOND_NONE;
+    s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k1(x->A, par, x->st); }});
+    if (multi) {
+        s.push_back({Ex::Allgather, nullptr});
+        s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsGamma, x->st); }});
+    }
+    if (ainv) s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k2_ainv(x->A, par, 0, x->st); launch_k3_ainv(x->A, par, 0, x->st); }});
+    else s.push_back({Ex::None, [par, none](pcg_ctx* x) { launch_k2_diag(x->A, par, 0, none, x->st); }});
+    if (multi) {
+        s.push_back({Ex::HaloSAllgather, nullptr});
+        s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsIter, x->st); }});
+    }
+    return s;
+}
+
+std::vector<Step> epilogue_steps(const pcg_ctx* c) {
+    std::vector<Step> s;
+    s.push_back({Ex::None, [](pcg_ctx* x) { launch_fin(x->A, x->st); }});
+    if (c->multi) s.push_back({Ex::HaloX, nullptr});
+    s.push_back({Ex::None, [](pcg_ctx* x) { launch_true_residual(x->A, x->st); }});
     if (c->multi) {
-        if (Status s = halo(c, c->s, true); !s) return s;
-        launch_scalar(A, kSsInit, c->st);
+        s.push_back({Ex::Allgather, nullptr});
+        s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsTrue, x->st); }});
+    }
+    return s;
+}
+
+Status run_steps(pcg_ctx* c, const std::vector<Step>& steps) {
+    for (const Step& s : steps) {
+        switch (s.ex) {
+            case Ex::None: s.run(c); break;
+            case Ex::Allgather: if (Status r = allgather_loc(c); !r) return r; break;
+            case Ex::HaloX: if (Status r = halo(c, c->x, false); !r) return r; break;
+            case Ex::HaloSAllgather: if (Status r = halo(c, c->s, true); !r) return r; break;
+        }
     }
     CU(cudaGetLastError());
     return Status::ok();
 }
 
-Status launch_iteration(pcg_ctx* c, int par) {
-    const KArgs& A = c->A;
-    launch_k1(A, par, c->st);
-    if (c->multi) {
-        if (Status s = allgather_loc(c); !s) return s;
-        launch_scalar(A, kSsGamma, c->st);
-    }
-    if (c->plan.precond == PCG_PRECOND_AINV) {
-        launch_k2_ainv(A, par, 0, c->st);
-        launch_k3_ainv(A, par, 0, c->st);
-    } else {
-        launch_k2_diag(A, par, 0, c->plan.precond == PCG_PRECOND_NONE, c->st);
-    }
-    if (c->multi) {
-        if (Status s = halo(c, c->s, true); !s) return s;
-        launch_scalar(A, kSsIter, c->st);
+// exchanges between the contexts of one process (same device, one stream)
+Status local_exchange(const std::vector<pcg_ctx*>& cs, Ex ex, cudaStream_t st) {
+    const size_t P = cs.size();
+    if (ex == Ex::Allgather || ex == Ex::HaloSAllgather)
+        for (size_t r = 0; r < P; ++r)
+            for (size_t q = 0; q < P; ++q)
+                CU(cudaMemcpyAsync(cs[r]->gath + 4 * q, cs[q]->sc->loc, 4 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (ex == Ex::HaloX || ex == Ex::HaloSAllgather) {
+        for (size_t r = 1; r < P; ++r) {
+            pcg_ctx* lo = cs[r - 1];
+            pcg_ctx* up = cs[r];
+            double* alo = ex == Ex::HaloX ? lo->x : lo->s;
+            double* aup = ex == Ex::HaloX ? up->x : up->s;
+            const size_t pitch = (size_t)lo->plan.pitch, bytes = pitch * sizeof(double);
+            CU(cudaMemcpyAsync(aup, alo + (size_t)lo->plan.nloc * pitch, bytes, cudaMemcpyDeviceToDevice, st));
+            CU(cudaMemcpyAsync(alo + (size_t)(lo->plan.nloc + 1) * pitch, aup + pitch, bytes, cudaMemcpyDeviceToDevice, st));
+        }
     }
     return Status::ok();
 }
 
-Status launch_epilogue(pcg_ctx* c) {
-    const KArgs& A = c->A;
-    launch_fin(A, c->st);
-    if (c->multi) {
-        if (Status s = halo(c, c->x, false); !s) return s;
-        launch_true_residual(A, c->st);
-        if (Status s = allgather_loc(c); !s) return s;
-        launch_scalar(A, kSsTrue, c->st);
-    } else {
-        launch_true_residual(A, c->st);
+Status run_steps_local(const std::vector<pcg_ctx*>& cs, const std::vector<Step>& steps, cudaStream_t st) {
+    for (const Step& s : steps) {
+        if (s.ex == Ex::None) {
+            for (pcg_ctx* c : cs) s.run(c);
+        } else if (Status r = local_exchange(cs, s.ex, st); !r) {
+            return r;
+        }
     }
     CU(cudaGetLastError());
     return Status::ok();
 }
+
+Status launch_prologue(pcg_ctx* c) { return run_steps(c, prologue_steps(c)); }
+Status launch_iteration(pcg_ctx* c, int par) { return run_steps(c, iteration_steps(c, par)); }
+Status launch_epilogue(pcg_ctx* c) { return run_steps(c, epilogue_steps(c)); }
 
 // Whole solve as one graph: prologue -> WHILE(active){ iteration(0); iteration(1) } -> epilogue.
 Status build_graph(pcg_ctx* c) {
@@ -278,6 +330,8 @@ Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, doubl
     if (maxit < 0) return Status::err(PCG_ERR_ARG, "pcg_solve: maxit must be >= 0");
     if (!b || !x) return Status::err(PCG_ERR_ARG, "pcg_solve: b and x are required");
     if (res_hist && hist_cap < 1) return Status::err(PCG_ERR_ARG, "pcg_solve: hist_cap < 1 with res_hist");
+    if (P.flags & PCG_FLAG_LOCAL_RANKS)
+        return Status::err(PCG_ERR_ARG, "pcg_solve: a PCG_FLAG_LOCAL_RANKS context is solved with pcg_solve_local_ranks");
     CU(cudaSetDevice(c->device));
     if (Status s = ensure_hist(c, maxit); !s) return s;
     if (use_graph(c) && !c->graph_built) {
@@ -372,8 +426,9 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     Plan& P = c->plan;
     c->device = g->device;
     c->user_stream = (cudaStream_t)g->stream;
-    c->multi = P.nranks > 1 || (P.flags & PCG_FLAG_COMM_PATH);
-    if (c->multi && !g->nccl_comm) return Status::err(PCG_ERR_ARG, "pcg_setup: nranks > 1 (or PCG_FLAG_COMM_PATH) needs nccl_comm");
+    c->multi = P.nranks > 1 || (P.flags & (PCG_FLAG_COMM_PATH | PCG_FLAG_LOCAL_RANKS));
+    if (c->multi && !g->nccl_comm && !(P.flags & PCG_FLAG_LOCAL_RANKS))
+        return Status::err(PCG_ERR_ARG, "pcg_setup: nranks > 1 (or PCG_FLAG_COMM_PATH) needs nccl_comm");
     c->comm = (ncclComm_t)g->nccl_comm;
     CU(cudaSetDevice(c->device));
     CU(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
@@ -570,6 +625,91 @@ pcg_status pcg_apply_preconditioner(pcg_ctx* c, const double* r, double* sout) {
     };
     Status s = body();
     return s ? PCG_OK : fail(c, s);
+}
+
+pcg_status pcg_solve_local_ranks(pcg_ctx* const* ctxs, int32_t n, const double* b, const double* x0, double tol,
+                                 int32_t maxit, double* x, int32_t* iterations, double* res_hist, int32_t hist_cap,
+                                 pcg_report* report) {
+    if (!ctxs || n < 1 || !b || !x) { set_thread_error("pcg_solve_local_ranks: bad argument"); return PCG_ERR_ARG; }
+    std::vector<pcg_ctx*> cs(ctxs, ctxs + n);
+    auto body = [&]() -> Status {
+        if (!(tol >= 0.0) || maxit < 0) return Status::err(PCG_ERR_ARG, "pcg_solve_local_ranks: tol >= 0, maxit >= 0");
+        for (int32_t r = 0; r < n; ++r) {
+            const Plan& P = cs[r]->plan;
+            if (!(P.flags & PCG_FLAG_LOCAL_RANKS) || P.nranks != n || P.rank != r || cs[r]->device != cs[0]->device)
+                return Status::err(PCG_ERR_ARG, "pcg_solve_local_ranks: ctxs[r] must be rank r of n, PCG_FLAG_LOCAL_RANKS, one device");
+        }
+        CU(cudaSetDevice(cs[0]->device));
+        cudaStream_t st = cs[0]->st;
+        std::vector<cudaStream_t> keep(n);
+        for (int32_t r = 0; r < n; ++r) { keep[r] = cs[r]->st; cs[r]->st = st; }   // one stream for all ranks
+        Status out = Status::ok();
+        do {
+            for (pcg_ctx* c : cs) if (!(out = ensure_hist(c, maxit))) break;
+            if (!out) break;
+            CU(cudaEventRecord(cs[0]->ev_in, cs[0]->user_stream));
+            CU(cudaStreamWaitEvent(st, cs[0]->ev_in, 0));
+            CU(cudaEventRecord(cs[0]->ev0, st));
+            for (pcg_ctx* c : cs) {
+                const Plan& P = c->plan;
+                std::memset(c->h_sc, 0, sizeof(DevScalars));
+                c->h_sc->tol = tol; c->h_sc->maxit = maxit; c->h_sc->active = 1;
+                CU(cudaMemcpyAsync(c->sc, c->h_sc, sizeof(DevScalars), cudaMemcpyHostToDevice, st));
+                const size_t dp = (size_t)P.pitch * sizeof(double), sp = (size_t)P.ni * sizeof(double);
+                const size_t off = (size_t)P.jb * P.ni;
+                CU(cudaMemcpy2DAsync(c->b + P.pitch, dp, b + off, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, st));
+                if (x0) CU(cudaMemcpy2DAsync(c->x + P.pitch, dp, x0 + off, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, st));
+                else CU(cudaMemsetAsync(c->x + P.pitch, 0, (size_t)P.nloc * dp, st));
+                CU(cudaStreamSynchronize(st));           // h_sc is reused per context
+            }
+            if (!(out = run_steps_local(cs, prologue_steps(cs[0]), st))) break;
+            int32_t* flag = nullptr;
+            CU(cudaMallocHost(&flag, sizeof(int32_t)));
+            for (int64_t m = 0; m < (int64_t)maxit && out;) {
+                for (int k = 0; k < 8 && m < (int64_t)maxit; ++k, ++m)
+                    if (!(out = run_steps_local(cs, iteration_steps(cs[0], (int)(m & 1)), st))) break;
+                cudaMemcpyAsync(flag, &cs[0]->sc->active, sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+                cudaStreamSynchronize(st);
+                if (*flag == 0) break;
+            }
+            cudaFreeHost(flag);
+            if (!out) break;
+            if (!(out = run_steps_local(cs, epilogue_steps(cs[0]), st))) break;
+            for (pcg_ctx* c : cs) {
+                const Plan& P = c->plan;
+                const size_t dp = (size_t)P.pitch * sizeof(double), sp = (size_t)P.ni * sizeof(double);
+                CU(cudaMemcpy2DAsync(x + (size_t)P.jb * P.ni, sp, c->x + P.pitch, dp, sp, (size_t)P.nloc,
+                                     cudaMemcpyDeviceToDevice, st));
+            }
+            CU(cudaEventRecord(cs[0]->ev1, st));
+            pcg_ctx* c = cs[0];
+            CU(cudaMemcpyAsync(c->h_sc, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, st));
+            CU(cudaStreamSynchronize(st));
+            const DevScalars& S = *c->h_sc;
+            const int32_t k = S.k, nh = std::min(k + 1, c->hist_cap);
+            CU(cudaMemcpy(c->h_hist, c->hist, (size_t)nh * sizeof(double), cudaMemcpyDeviceToHost));
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+            if (iterations) *iterations = k;
+            if (res_hist) std::memcpy(res_hist, c->h_hist, (size_t)std::min(nh, hist_cap) * sizeof(double));
+            if (report) {
+                pcg_report R{};
+                R.iterations = k;
+                R.rel_residual = c->h_hist[std::min(k, c->hist_cap - 1)];
+                R.converged = S.status == kStOk && R.rel_residual <= tol;
+                R.true_rel_residual = S.true_rel;
+                R.solve_s = ms * 1e-3;
+                for (pcg_ctx* q : cs) { R.n_ocean += q->plan.n_owned; R.nnz_z += q->plan.nnz_off; R.setup_s = std::max(R.setup_s, q->plan.setup_s); }
+                R.failed_index = -1;
+                *report = R;
+            }
+            if (S.status == kStBreakdown) out = Status::err(PCG_ERR_BREAKDOWN, "pcg_solve_local_ranks: breakdown");
+        } while (0);
+        for (int32_t r = 0; r < n; ++r) cs[r]->st = keep[r];
+        return out;
+    };
+    Status s = body();
+    return s ? PCG_OK : fail(cs[0], s);
 }
 
 pcg_status pcg_layout(const pcg_ctx* c, int32_t* pitch, int32_t* block, int32_t* rows) {

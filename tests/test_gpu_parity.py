@@ -231,3 +231,36 @@ def test_cfg4_full_size_sampled():
     x = A.from_grid(host(xg))
     assert np.linalg.norm(x - xs) / np.linalg.norm(xs) < 5e-6
     S.close()
+
+
+# --------------------------------------------------------- multi-rank path, emulated on one GPU
+@pytest.mark.parametrize("name,P,precond", [("cfg2", 2, "ainv"), ("cfg2", 3, "ainv"), ("cfg2", 8, "ainv"),
+                                            ("cfg3", 4, "ainv"), ("cfg2", 4, "jacobi")])
+def test_local_ranks_bitwise_vs_oracle_partitioned(name, P, precond):
+    """The multi-rank device path (halo rows, rank sums, rank-ordered tree, block-local AINV per
+    rank) run as P in-process ranks on one GPU equals the oracle's partitioned canonical PCG
+    (parts = P, halo = 0) bit for bit."""
+    p = synth.config(name)
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, TAU, parts=P, halo=0) if precond == "ainv" else None
+    b = rhs(A, p)
+    R = pcg.LocalRanks(p.cE, p.cN, p.mask, P, tau=TAU, precond=precond)
+    ref = oracle.pcg(A, b, precond, M, 1e-10, maxit=A.n, mode="canonical", pitch=R.pitch, block=R.block, parts=P)
+    xg, k, hist, rep = R.solve(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
+    assert k == ref.iterations
+    assert np.array_equal(hist, ref.hist)
+    assert np.array_equal(host(xg), A.to_grid(ref.x))
+    assert rep["true_rel_residual"] == ref.true_rel_residual
+    R.close()
+
+
+def test_local_ranks_one_rank_equals_single():
+    p = synth.config("cfg2")
+    A, M, S = setup_pair(p)
+    b = dev(A.to_grid(rhs(A, p)))
+    x0, k0, h0, _ = S.solve(b, tol=1e-10, maxit=A.n)
+    S.close()
+    R = pcg.LocalRanks(p.cE, p.cN, p.mask, 1, tau=TAU)
+    x1, k1, h1, _ = R.solve(b, tol=1e-10, maxit=A.n)
+    assert k1 == k0 and np.array_equal(h1, h0) and torch.equal(x1, x0)
+    R.close()
