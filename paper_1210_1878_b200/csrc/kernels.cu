@@ -72,8 +72,10 @@ __device__ __forceinline__ bool count_block(uint32_t* counter) {
     __shared__ bool am_last;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        const uint32_t t = atomicAdd(counter, 1u);
+        // acq_rel at gpu scope: releases this block's partials (written by thread 0) and, in the
+        // last block, acquires every other block's; one L2 round trip instead of fence + atomic
+        uint32_t t;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(counter) : "memory");
         am_last = (t == gridDim.x - 1);
     }
     __syncthreads();
@@ -81,19 +83,19 @@ __device__ __forceinline__ bool count_block(uint32_t* counter) {
 }
 
 // In the last block: thread t sums partials t, t+B, ... left to right, then the block tree.
-// Eight loads are issued before their adds so the walk is not one L2 round trip per partial.
+// All of a thread's loads (up to 32, i.e. G <= 8192) are issued before the first add, so the
+// walk costs one L2 round trip; longer walks continue in rounds of 32.
 __device__ __forceinline__ double final_sum(const double* partial, int64_t G) {
-    __threadfence();
     double acc = 0.0;
     int64_t m = threadIdx.x < kBlock ? (int64_t)threadIdx.x : G;
-    for (; m + 7 * kBlock < G; m += 8 * kBlock) {
-        double p[8];
+    for (; m < G; m += 32 * kBlock) {
+        double p[32];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) p[u] = __ldcg(partial + m + u * kBlock);
+        for (int u = 0; u < 32; ++u) p[u] = m + u * kBlock < G ? __ldcg(partial + m + u * kBlock) : 0.0;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, p[u]);
+        for (int u = 0; u < 32; ++u)
+            if (m + u * kBlock < G) acc = __dadd_rn(acc, p[u]);
     }
-    for (; m < G; m += kBlock) acc = __dadd_rn(acc, __ldcg(partial + m));
     return block_tree(acc);
 }
 
@@ -127,6 +129,21 @@ __device__ __forceinline__ void stop(const KArgs& A, int status) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Diagnostic build only (-DPCG_TIMELINE): per-block globaltimer stamps of the last launch of K1/K2/K3
+// (slot 0 entry, 1 after griddepcontrol.wait, 2 before the block count, 3 last block done).
+#ifdef PCG_TIMELINE
+__device__ unsigned long long g_timeline[3][2048][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TL(kk, slot) \
+    if (threadIdx.x == 0 && blockIdx.x < 2048) g_timeline[kk][blockIdx.x][slot] = gtimer()
+#else
+#define TL(kk, slot) ((void)0)
+#endif
+
 // The flag only changes between launches (or in the last block of a reduction, after every
 // other block has read it), so a cached read is exact.
 __device__ __forceinline__ bool is_active(const KArgs& A) { return __ldg(&A.sc->active) != 0; }
@@ -157,22 +174,47 @@ __device__ void fin_init(const KArgs& A, double rho0, double rr0) {
     set_cond(A, act);
 }
 
-__device__ void fin_iter(const KArgs& A, double rho_new, double rr) {
+// Scalars fin_iter reads, loaded by the last block's thread 0 before its final sum so the loads
+// overlap the partial walk instead of following it.
+struct FinPre {
+    double rr, rho, nb, tol;
+    int32_t k, maxit;
+};
+
+__device__ __forceinline__ FinPre fin_prefetch(const KArgs& A) {
+    const DevScalars* sc = A.sc;
+    FinPre f;
+    f.rr = sc->red[2];
+    f.rho = sc->rho;
+    f.nb = sc->nb;
+    f.tol = sc->tol;
+    f.k = sc->k;
+    f.maxit = sc->maxit;
+    return f;
+}
+
+__device__ void fin_iter(const KArgs& A, double rho_new, const FinPre& f) {
     DevScalars* sc = A.sc;
-    const int k = sc->k + 1;
+    const int k = f.k + 1;
     sc->k = k;
-    if (!isfinite(rho_new) || !isfinite(rr)) {
+    if (!isfinite(rho_new) || !isfinite(f.rr)) {
         if (k < A.hist_cap) A.hist[k] = NAN;
         stop(A, kStBreakdown);
         return;
     }
-    sc->beta = __ddiv_rn(rho_new, sc->rho);
+    sc->beta = __ddiv_rn(rho_new, f.rho);
     sc->rho = rho_new;
-    const double h = __ddiv_rn(__dsqrt_rn(rr), sc->nb);
+    const double h = __ddiv_rn(__dsqrt_rn(f.rr), f.nb);
     if (k < A.hist_cap) A.hist[k] = h;
-    const int act = (h > sc->tol) && (k < sc->maxit);
+    const int act = (h > f.tol) && (k < f.maxit);
     sc->active = act;
     set_cond(A, act);
+}
+
+__device__ void fin_iter(const KArgs& A, double rho_new, double rr) {
+    FinPre f = fin_prefetch(A);
+    f.rr = rr;
+    fin_iter(A, rho_new, f);
 }
 
 // alpha of the current iteration from the global (d, q); false on breakdown
@@ -351,7 +393,9 @@ __device__ __forceinline__ void k1_strip(const KArgs& A, int par, int64_t st, do
 #endif
 template <bool SIGMA>
 __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, const int par) {
+    TL(0, 0);
     pdl_wait();
+    TL(0, 1);
     if (!is_active(A)) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         // safety net: the WHILE node ends even if a reduction never clears the flag
@@ -417,6 +461,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
         }
     }
     pdl_trigger();
+    TL(0, 2);
     if (count_block(&A.sc->counter[0])) {
         const double tot = final_sum(A.partial[0], n_units(A));
         if (threadIdx.x == 0) {
@@ -426,6 +471,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
             A.sc->counter[0] = 0;
             A.sc->ticket[0] = 0;
         }
+        TL(0, 3);
     }
 }
 
@@ -589,11 +635,73 @@ __device__ __forceinline__ double ell_row(const EllDev& E, int64_t e, Gather gat
 #endif
 
 
+// Two units per ticket, processed interleaved: body2(W0, W1, v0, v1) issues both units' loads
+// before either unit's gathers, so a block has two latency chains in flight.
+template <class Body2>
+__device__ __forceinline__ void dynamic_units_x2(const KArgs& A, unsigned long long* ticket, double* partial, Body2 body2) {
+    __shared__ long long s_next;
+    __shared__ double wsd[2][kWarps];
+    const int64_t U = n_units(A);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_next = (long long)atomicAdd(ticket, 2ull);
+    __syncthreads();
+    int64_t u = s_next;
+    while (u < U) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_next = (long long)atomicAdd(ticket, 2ull);
+        const Unit W0 = unit_of(A, u);
+        const bool two = u + 1 < U;
+        const Unit W1 = unit_of(A, two ? u + 1 : u);
+        double v0, v1;
+        body2(W0, W1, two, v0, v1);
+        v0 = warp_tree(v0);
+        v1 = warp_tree(v1);
+        if (lane == 0) { wsd[0][warp] = v0; wsd[1][warp] = v1; }
+        __syncthreads();
+        if (warp == 0) {
+            double a = lane < kWarps ? wsd[0][lane] : 0.0, b = lane < kWarps ? wsd[1][lane] : 0.0;
+            a = warp_tree(a);
+            b = warp_tree(b);
+            if (lane == 0) {
+                partial[(int64_t)W0.j * A.nbx + W0.bx] = a;
+                if (two) partial[(int64_t)W1.j * A.nbx + W1.bx] = b;
+            }
+        }
+        u = s_next;
+    }
+}
+
+// Two ELL rows at once (elements e0, e1): all ELL loads of both rows, then all gathers, then
+// each row's fma chain in its canonical order; overflow entries afterwards, row by row.
+template <class Gather>
+__device__ __forceinline__ void ell_row_x2(const EllDev& E, int64_t e0, int64_t e1, bool in0, bool in1, Gather gat,
+                                           double& acc0, double& acc1) {
+    const int4 c0 = __ldg(reinterpret_cast<const int4*>(E.col) + e0);
+    const int4 c1 = __ldg(reinterpret_cast<const int4*>(E.col) + e1);
+    double z0[4], z1[4];
+    ld_nc_f64x4(E.val + e0 * kEll, z0);
+    ld_nc_f64x4(E.val + e1 * kEll, z1);
+    const double x00 = gat(c0.x), x01 = gat(c0.y), x02 = gat(c0.z), x03 = gat(c0.w);
+    const double x10 = gat(c1.x), x11 = gat(c1.y), x12 = gat(c1.z), x13 = gat(c1.w);
+    acc0 = __fma_rn(z0[0], x00, 0.0);
+    acc0 = __fma_rn(z0[1], x01, acc0);
+    acc0 = __fma_rn(z0[2], x02, acc0);
+    acc0 = __fma_rn(z0[3], x03, acc0);
+    acc1 = __fma_rn(z1[0], x10, 0.0);
+    acc1 = __fma_rn(z1[1], x11, acc1);
+    acc1 = __fma_rn(z1[2], x12, acc1);
+    acc1 = __fma_rn(z1[3], x13, acc1);
+    if (in0) acc0 = overflow_sum(E, e0, acc0, gat);
+    if (in1) acc1 = overflow_sum(E, e1, acc1, gat);
+}
+
 // ---- K2 (AINV): r -= alpha q ; t = Dhat^-1 Z^T r ; (r, r) --------------------------------
 // r_new at a gathered point c is recomputed as fma(-alpha, q_c, r_old_c) (bitwise the value
 // its own thread stores), so no grid-wide barrier is needed between the update and the gather.
 __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArgs A, const int par, const int init) {
+    TL(1, 0);
     pdl_wait();
+    TL(1, 1);
     if (!is_active(A)) return;
     double alpha;
     if (!get_alpha(A, init, alpha)) {
@@ -621,6 +729,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
     if (A.dynamic) {
         dynamic_units(A, &A.sc->ticket[1], A.partial[1], body);
         pdl_trigger();
+        TL(1, 2);
         last = count_block(&A.sc->counter[1]);
     } else {
         const int64_t U = n_units(A);
@@ -638,12 +747,15 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
             A.sc->counter[1] = 0;
             A.sc->ticket[1] = 0;
         }
+        TL(1, 3);
     }
 }
 
 // ---- K3 (AINV): s = Z t ; (s, r) ; beta / history / flag -----------------------------------
 __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArgs A, const int par, const int init) {
+    TL(2, 0);
     pdl_wait();
+    TL(2, 1);
     if (!is_active(A)) return;
     extern __shared__ double ws[];
     const double* __restrict__ rn = A.r[par ^ 1];
@@ -659,9 +771,32 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
         return v;
     };
     bool last;
-    if (A.dynamic) {
+    if (A.x2) {
+        dynamic_units_x2(A, &A.sc->ticket[2], A.partial[2], [&](const Unit& W0, const Unit& W1, bool two, double& v0, double& v1) {
+            v0 = 0.0;
+            v1 = 0.0;
+            const bool in0 = W0.inrow, in1 = two && W1.inrow;
+            if (!in0 && !in1) return;
+            const int64_t e0 = in0 ? W0.a - A.pitch : 0, e1 = in1 ? W1.a - A.pitch : 0;
+            const double r0 = rn[e0 + A.pitch], r1 = rn[e1 + A.pitch];
+            double a0, a1;
+            ell_row_x2(A.z, e0, e1, in0, in1, [&](int32_t g) { return __ldg(t + g); }, a0, a1);
+            if (in0) {
+                A.s[W0.a] = a0;
+                v0 = __dmul_rn(a0, r0);
+            }
+            if (in1) {
+                A.s[W1.a] = a1;
+                v1 = __dmul_rn(a1, r1);
+            }
+        });
+        pdl_trigger();
+        TL(2, 2);
+        last = count_block(&A.sc->counter[2]);
+    } else if (A.dynamic) {
         dynamic_units(A, &A.sc->ticket[2], A.partial[2], body);
         pdl_trigger();
+        TL(2, 2);
         last = count_block(&A.sc->counter[2]);
     } else {
         const int64_t U = n_units(A);
@@ -670,14 +805,17 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
         last = finish_units<1>(A, ws, A.partial[2], nullptr, &A.sc->counter[2]);
     }
     if (last) {
+        FinPre pre{};
+        if (threadIdx.x == 0 && !A.multi && !init) pre = fin_prefetch(A);
         const double tot = final_sum(A.partial[2], n_units(A));
         if (threadIdx.x == 0) {
             A.sc->counter[2] = 0;
             A.sc->ticket[2] = 0;
             if (A.multi) A.sc->loc[1] = tot;
             else if (init) fin_init(A, tot, A.sc->red[2]);
-            else fin_iter(A, tot, A.sc->red[2]);
+            else fin_iter(A, tot, pre);
         }
+        TL(2, 3);
     }
 }
 
@@ -1331,6 +1469,8 @@ void configure_kernels(KArgs& A, int sms) {
     if (const char* e = getenv("PCG_K1FLAT")) A.k1flat = atoi(e) != 0;
     A.pdl = 1;
     if (const char* e = getenv("PCG_PDL")) A.pdl = atoi(e) != 0;
+    A.x2 = 0;
+    if (const char* e = getenv("PCG_X2")) A.x2 = atoi(e) != 0;
     A.g_k1f = persistent_grid(k1_flat_kernel<false>, U, sms, 0);
     A.tma = 0;                                         // measured no faster than the LDG path (r01)
     if (const char* e = getenv("PCG_TMA")) A.tma = atoi(e) != 0;
@@ -1424,3 +1564,10 @@ cudaError_t launch_loop(const KArgs& A, cudaStream_t st) {
 void launch_set_cond(cudaGraphConditionalHandle h, cudaStream_t st) { set_cond_kernel<<<1, 1, 0, st>>>(h); }
 
 }  // namespace pcg
+
+#ifdef PCG_TIMELINE
+// Diagnostic build only: copy the block timeline of the last K1/K2/K3 launches to the host.
+extern "C" int pcg_diag_timeline(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, pcg::g_timeline, sizeof(pcg::g_timeline));
+}
+#endif

@@ -39,6 +39,7 @@ struct KArgs {
     int32_t g_loop;                   // cooperative grid of the fused loop kernel
     int32_t k1flat, g_k1f;            // K1 in row-segment form (one element per thread)
     int32_t pdl;                      // programmatic dependent launch of the iteration kernels
+    int32_t x2;                       // K2/K3: two units per ticket, interleaved
     int32_t precond;                  // pcg_precond
     int64_t nel;                      // owned elements nloc * pitch
     const double *cE, *cN, *sigma, *diag, *piv;

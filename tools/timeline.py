@@ -1,0 +1,46 @@
+"""Block timeline of one PCG iteration (diagnostic build with -DPCG_TIMELINE).
+
+    python -m paper_1210_1878_b200.build --variant tl PCG_TIMELINE
+    PCG_LIB=paper_1210_1878_b200/_build/tl/libpcg.so python tools/timeline.py --config cfg4
+Runs a graph solve with tol 0 and an even maxit (so the last K1/K2/K3 launches are live), then
+prints, per kernel, the spread of block entry / post-wait / loop-end times and the last block's
+finish, relative to the earliest K1 entry (microseconds)."""
+import argparse
+import ctypes
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1210_1878_b200 as pcg  # noqa: E402
+from paper_1210_1878_b200 import synth  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg4")
+ap.add_argument("--maxit", type=int, default=200)
+a = ap.parse_args()
+p = synth.config(a.config)
+S = pcg.Solver(p.cE, p.cN, p.mask, tau=0.1)
+b = S.apply_operator(torch.from_numpy(synth.xstar(p)).cuda())
+for _ in range(2):
+    S.solve(b, tol=0.0, maxit=a.maxit)
+torch.cuda.synchronize()
+lib = ctypes.CDLL(os.environ["PCG_LIB"])
+buf = np.zeros((3, 2048, 4), dtype=np.uint64)
+assert lib.pcg_diag_timeline(buf.ctypes.data_as(ctypes.c_void_p)) == 0
+grid = [S._grid_sizes[i] if hasattr(S, "_grid_sizes") else None for i in range(3)]
+t0 = min(int(v) for v in buf[0, :, 0] if v > 0)
+for kk, name in enumerate(("K1", "K2", "K3")):
+    T = buf[kk].astype(np.int64)
+    live = T[:, 0] > 0
+    T = T[live]
+    rel = (T - t0) / 1e3
+    def q(c):
+        v = rel[:, c][T[:, c] > 0]
+        return "min %7.2f  p50 %7.2f  max %7.2f" % (v.min(), np.median(v), v.max()) if len(v) else "-"
+    fin = rel[:, 3][T[:, 3] > 0]
+    print(f"{name} blocks={live.sum():4d} entry[{q(0)}] wait[{q(1)}] loopend[{q(2)}] last_done={fin.max() if len(fin) else float('nan'):7.2f}")
+    busy = (rel[:, 2] - rel[:, 1])
+    print(f"    block busy (loopend-wait): mean {busy.mean():6.2f} min {busy.min():6.2f} max {busy.max():6.2f}")
