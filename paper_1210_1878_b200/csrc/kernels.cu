@@ -133,6 +133,10 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // (slot 0 entry, 1 after griddepcontrol.wait, 2 before the block count, 3 last block done).
 #ifdef PCG_TIMELINE
 __device__ unsigned long long g_timeline[3][2048][4];
+__device__ unsigned g_units[2048];
+__device__ unsigned long long g_tail[3][4];
+#define TT(kk, slot) \
+    if (threadIdx.x == 0) g_tail[kk][slot] = gtimer()
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -142,6 +146,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (threadIdx.x == 0 && blockIdx.x < 2048) g_timeline[kk][blockIdx.x][slot] = gtimer()
 #else
 #define TL(kk, slot) ((void)0)
+#define TT(kk, slot) ((void)0)
 #endif
 
 // The flag only changes between launches (or in the last block of a reduction, after every
@@ -233,6 +238,7 @@ __device__ __forceinline__ bool get_alpha(const KArgs& A, int init, double& alph
 struct Unit {
     int32_t i, j, bx;
     bool valid, inrow;     // i < ni ; i < pitch
+    bool live;             // the thread computes this point (inrow; ocean only with A.landskip)
     int64_t a;             // array index of (i, j)
 };
 
@@ -245,6 +251,7 @@ __device__ __forceinline__ Unit unit_of(const KArgs& A, int64_t u) {
     W.i = W.bx * kBlock + (int32_t)threadIdx.x;
     W.valid = W.i < A.ni;
     W.inrow = W.i < A.pitch;
+    W.live = W.inrow;
     W.a = (int64_t)(W.j + 1) * A.pitch + W.i;
     return W;
 }
@@ -276,12 +283,29 @@ __device__ __forceinline__ bool finish_units(const KArgs& A, const double* ws, d
             }
         }
     }
+    if (!counter) {                                        // partials only, no last block
+        __syncthreads();
+        return false;
+    }
     return count_block(counter);
 }
 
-// Dynamic variant: units are handed out by an atomic ticket (prefetched one unit ahead), so
-// blocks that get slower memory do fewer units; each unit's partial is completed and stored
-// right away (block tree over its 8 warp sums).  Same partials, same canonical order.
+// Dynamic variant: units are handed out by an atomic ticket, so blocks that get slower memory do
+// fewer units; each unit's partial is completed and stored right away (block tree over its 8 warp
+// sums).  Same partials, same canonical order.  Tickets are drawn two units ahead: the atomic for
+// unit n+2 is issued when unit n starts and only consumed when it ends, so no warp waits on it.
+// With A.landskip each warp also loads the ocean bit mask of its 32 columns of the NEXT unit
+// while computing this one; lanes on land or padding then issue no memory traffic at all (their
+// vector entries are zero and stay zero, so the partials are bitwise unchanged).
+// Dynamic variant: units are handed out by an atomic ticket, so blocks that get slower memory do
+// fewer units; each unit's partial is completed and stored right away (block tree over its 8 warp
+// sums).  Same partials, same canonical order.  The ticket for the next unit is drawn when a unit
+// starts and published to the block when it ends, so no warp waits on the atomic.  (Drawing two
+// ahead was measured 25 % slower at ORCA025: consecutive tickets are neighbouring segments of the
+// same long pole row, and one block then holds two of the slowest units.)
+// With A.landskip each warp first loads the ocean bit mask of its 32 columns of the unit; lanes on
+// land or padding then issue no memory traffic (their vector entries are zero and stay zero, so
+// the partials are bitwise unchanged).
 template <class Body>
 __device__ __forceinline__ void dynamic_units(const KArgs& A, unsigned long long* ticket, double* partial, Body body) {
     __shared__ long long s_next;
@@ -293,11 +317,14 @@ __device__ __forceinline__ void dynamic_units(const KArgs& A, unsigned long long
     int64_t u = s_next;
     while (u < U) {
         __syncthreads();                                   // everyone has read s_next
-        if (threadIdx.x == 0) s_next = (long long)atomicAdd(ticket, 1ull);
-        const Unit W = unit_of(A, u);
+        unsigned long long tk = 0;
+        if (threadIdx.x == 0) tk = atomicAdd(ticket, 1ull);
+        Unit W = unit_of(A, u);
+        if (A.landskip) W.live = W.inrow && ((__ldg(A.ocean + ((int64_t)W.j * A.nbx + W.bx) * kWarps + warp) >> lane) & 1u);
         double v = body(W);
         v = warp_tree(v);
         if (lane == 0) wsd[warp] = v;
+        if (threadIdx.x == 0) s_next = (long long)tk;
         __syncthreads();
         if (warp == 0) {
             double w = lane < kWarps ? wsd[lane] : 0.0;
@@ -305,6 +332,9 @@ __device__ __forceinline__ void dynamic_units(const KArgs& A, unsigned long long
             if (lane == 0) partial[(int64_t)W.j * A.nbx + W.bx] = w;
         }
         u = s_next;
+#ifdef PCG_TIMELINE
+        if (threadIdx.x == 0 && blockIdx.x < 2048) g_units[blockIdx.x] += 1;
+#endif
     }
 }
 
@@ -575,6 +605,9 @@ __device__ __forceinline__ void ld_nc_f64x4(const double* p, double (&z)[4]) {
 // dependent memory latencies per entry, and those pole warps set the kernel time.
 template <class Gather>
 __device__ __forceinline__ double overflow_sum(const EllDev& E, int64_t e, double acc, Gather gat) {
+#ifdef PCG_DIAG_NOOVF
+    return acc;
+#endif
     const int64_t sl = e >> 5;
     const int64_t o0 = __ldg(E.ooff + sl);
     const int L = (int)((__ldg(E.ooff + sl + 1) - o0) >> 5);
@@ -615,7 +648,11 @@ __device__ __forceinline__ double ell_row(const EllDev& E, int64_t e, Gather gat
     double z[kEll], x[kEll];
     const int4 cv = __ldg(reinterpret_cast<const int4*>(E.col) + e);
     ld_nc_f64x4(E.val + e * kEll, z);
+#ifdef PCG_DIAG_NOGATHER
+    const int32_t c[kEll] = {(int32_t)(e + 32), (int32_t)(e + 32), (int32_t)(e + 32), (int32_t)(e + 32)};
+#else
     const int32_t c[kEll] = {cv.x, cv.y, cv.z, cv.w};
+#endif
 #pragma unroll
     for (int m = 0; m < kEll; ++m) x[m] = gat(c[m]);
     // schedule pin (emits nothing): the fma chain may only start once all four gathers have
@@ -635,64 +672,45 @@ __device__ __forceinline__ double ell_row(const EllDev& E, int64_t e, Gather gat
 #endif
 
 
-// Two units per ticket, processed interleaved: body2(W0, W1, v0, v1) issues both units' loads
-// before either unit's gathers, so a block has two latency chains in flight.
-template <class Body2>
-__device__ __forceinline__ void dynamic_units_x2(const KArgs& A, unsigned long long* ticket, double* partial, Body2 body2) {
-    __shared__ long long s_next;
-    __shared__ double wsd[2][kWarps];
-    const int64_t U = n_units(A);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_next = (long long)atomicAdd(ticket, 2ull);
-    __syncthreads();
-    int64_t u = s_next;
-    while (u < U) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_next = (long long)atomicAdd(ticket, 2ull);
-        const Unit W0 = unit_of(A, u);
-        const bool two = u + 1 < U;
-        const Unit W1 = unit_of(A, two ? u + 1 : u);
-        double v0, v1;
-        body2(W0, W1, two, v0, v1);
-        v0 = warp_tree(v0);
-        v1 = warp_tree(v1);
-        if (lane == 0) { wsd[0][warp] = v0; wsd[1][warp] = v1; }
-        __syncthreads();
-        if (warp == 0) {
-            double a = lane < kWarps ? wsd[0][lane] : 0.0, b = lane < kWarps ? wsd[1][lane] : 0.0;
-            a = warp_tree(a);
-            b = warp_tree(b);
-            if (lane == 0) {
-                partial[(int64_t)W0.j * A.nbx + W0.bx] = a;
-                if (two) partial[(int64_t)W1.j * A.nbx + W1.bx] = b;
-            }
-        }
-        u = s_next;
+// K2 has no last block: its (r, r) is first needed by the convergence test at the end of K3.
+// K3's block 0 forms that final sum as soon as K2 has completed (K2's partials are still in L2),
+// while the other blocks stream; k3_finish (K3's last block) then forms K3's own (s, r), does
+// K2's bookkeeping (alpha for the pending x update, ticket / counter reset) and fin_init /
+// fin_iter.  Block 0's store of (r, r) precedes its release in count_block, so the last block
+// (which acquires there) reads it.
+__device__ __forceinline__ void k3_sum_rr(const KArgs& A) {
+    if (blockIdx.x != 0) return;
+    const double rr = final_sum(A.partial[1], n_units(A));
+    if (threadIdx.x == 0) {
+        if (A.multi) A.sc->loc[2] = rr;
+        else A.sc->red[2] = rr;
     }
 }
 
-// Two ELL rows at once (elements e0, e1): all ELL loads of both rows, then all gathers, then
-// each row's fma chain in its canonical order; overflow entries afterwards, row by row.
-template <class Gather>
-__device__ __forceinline__ void ell_row_x2(const EllDev& E, int64_t e0, int64_t e1, bool in0, bool in1, Gather gat,
-                                           double& acc0, double& acc1) {
-    const int4 c0 = __ldg(reinterpret_cast<const int4*>(E.col) + e0);
-    const int4 c1 = __ldg(reinterpret_cast<const int4*>(E.col) + e1);
-    double z0[4], z1[4];
-    ld_nc_f64x4(E.val + e0 * kEll, z0);
-    ld_nc_f64x4(E.val + e1 * kEll, z1);
-    const double x00 = gat(c0.x), x01 = gat(c0.y), x02 = gat(c0.z), x03 = gat(c0.w);
-    const double x10 = gat(c1.x), x11 = gat(c1.y), x12 = gat(c1.z), x13 = gat(c1.w);
-    acc0 = __fma_rn(z0[0], x00, 0.0);
-    acc0 = __fma_rn(z0[1], x01, acc0);
-    acc0 = __fma_rn(z0[2], x02, acc0);
-    acc0 = __fma_rn(z0[3], x03, acc0);
-    acc1 = __fma_rn(z1[0], x10, 0.0);
-    acc1 = __fma_rn(z1[1], x11, acc1);
-    acc1 = __fma_rn(z1[2], x12, acc1);
-    acc1 = __fma_rn(z1[3], x13, acc1);
-    if (in0) acc0 = overflow_sum(E, e0, acc0, gat);
-    if (in1) acc1 = overflow_sum(E, e1, acc1, gat);
+__device__ __forceinline__ void k3_finish(const KArgs& A, int init) {
+    TT(2, 0);
+    FinPre pre{};
+    if (threadIdx.x == 0 && !A.multi && !init) pre = fin_prefetch(A);
+    const double rs = final_sum(A.partial[2], n_units(A));
+    TT(2, 1);
+    if (threadIdx.x == 0) {
+        DevScalars* sc = A.sc;
+        double alpha = 0.0;
+        get_alpha(A, init, alpha);                       // K2 ran, so gamma passed this check there
+        sc->alpha = alpha;
+        sc->xpend = init ? 0 : 1;
+        sc->counter[1] = 0;
+        sc->ticket[1] = 0;
+        sc->counter[2] = 0;
+        sc->ticket[2] = 0;
+        if (A.multi) {
+            sc->loc[1] = rs;
+        } else if (init) {
+            fin_init(A, rs, sc->red[2]);
+        } else {
+            fin_iter(A, rs, pre);
+        }
+    }
 }
 
 // ---- K2 (AINV): r -= alpha q ; t = Dhat^-1 Z^T r ; (r, r) --------------------------------
@@ -714,7 +732,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
     const double* __restrict__ q = A.q;
     auto body = [&](const Unit& W) {
         double v = 0.0;
-        if (W.inrow) {
+        if (W.live) {
             const double rnew = __fma_rn(-alpha, q[W.a], ro[W.a]);
             const double pv = A.piv[W.a];
             const double acc = ell_row(A.zt, W.a - A.pitch,
@@ -725,29 +743,16 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
         }
         return v;
     };
-    bool last;
     if (A.dynamic) {
         dynamic_units(A, &A.sc->ticket[1], A.partial[1], body);
         pdl_trigger();
         TL(1, 2);
-        last = count_block(&A.sc->counter[1]);
     } else {
         const int64_t U = n_units(A);
         int k = 0;
         for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k) put_warp_sum(ws, k, body(unit_of(A, u)));
-        last = finish_units<1>(A, ws, A.partial[1], nullptr, &A.sc->counter[1]);
-    }
-    if (last) {
-        const double tot = final_sum(A.partial[1], n_units(A));
-        if (threadIdx.x == 0) {
-            if (A.multi) A.sc->loc[2] = tot;
-            else A.sc->red[2] = tot;
-            A.sc->alpha = alpha;
-            A.sc->xpend = init ? 0 : 1;
-            A.sc->counter[1] = 0;
-            A.sc->ticket[1] = 0;
-        }
-        TL(1, 3);
+        finish_units<1>(A, ws, A.partial[1], nullptr, nullptr);
+        pdl_trigger();
     }
 }
 
@@ -757,12 +762,13 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
     pdl_wait();
     TL(2, 1);
     if (!is_active(A)) return;
+    k3_sum_rr(A);
     extern __shared__ double ws[];
     const double* __restrict__ rn = A.r[par ^ 1];
     const double* __restrict__ t = A.t;
     auto body = [&](const Unit& W) {
         double v = 0.0;
-        if (W.inrow) {
+        if (W.live) {
             const double rv = rn[W.a];
             const double acc = ell_row(A.z, W.a - A.pitch, [&](int32_t g) { return __ldg(t + g); });
             A.s[W.a] = acc;
@@ -771,29 +777,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
         return v;
     };
     bool last;
-    if (A.x2) {
-        dynamic_units_x2(A, &A.sc->ticket[2], A.partial[2], [&](const Unit& W0, const Unit& W1, bool two, double& v0, double& v1) {
-            v0 = 0.0;
-            v1 = 0.0;
-            const bool in0 = W0.inrow, in1 = two && W1.inrow;
-            if (!in0 && !in1) return;
-            const int64_t e0 = in0 ? W0.a - A.pitch : 0, e1 = in1 ? W1.a - A.pitch : 0;
-            const double r0 = rn[e0 + A.pitch], r1 = rn[e1 + A.pitch];
-            double a0, a1;
-            ell_row_x2(A.z, e0, e1, in0, in1, [&](int32_t g) { return __ldg(t + g); }, a0, a1);
-            if (in0) {
-                A.s[W0.a] = a0;
-                v0 = __dmul_rn(a0, r0);
-            }
-            if (in1) {
-                A.s[W1.a] = a1;
-                v1 = __dmul_rn(a1, r1);
-            }
-        });
-        pdl_trigger();
-        TL(2, 2);
-        last = count_block(&A.sc->counter[2]);
-    } else if (A.dynamic) {
+    if (A.dynamic) {
         dynamic_units(A, &A.sc->ticket[2], A.partial[2], body);
         pdl_trigger();
         TL(2, 2);
@@ -805,16 +789,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
         last = finish_units<1>(A, ws, A.partial[2], nullptr, &A.sc->counter[2]);
     }
     if (last) {
-        FinPre pre{};
-        if (threadIdx.x == 0 && !A.multi && !init) pre = fin_prefetch(A);
-        const double tot = final_sum(A.partial[2], n_units(A));
-        if (threadIdx.x == 0) {
-            A.sc->counter[2] = 0;
-            A.sc->ticket[2] = 0;
-            if (A.multi) A.sc->loc[1] = tot;
-            else if (init) fin_init(A, tot, A.sc->red[2]);
-            else fin_iter(A, tot, pre);
-        }
+        k3_finish(A, init);
         TL(2, 3);
     }
 }
@@ -996,22 +971,13 @@ __global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k2_tma_kernel(const
         rn[a] = rnew;
         return __dmul_rn(rnew, rnew);
     });
-    if (count_block(&A.sc->counter[1])) {
-        const double tot = final_sum(A.partial[1], n_units(A));
-        if (threadIdx.x == 0) {
-            if (A.multi) A.sc->loc[2] = tot;
-            else A.sc->red[2] = tot;
-            A.sc->alpha = alpha;
-            A.sc->xpend = init ? 0 : 1;
-            A.sc->counter[1] = 0;
-            A.sc->ticket[1] = 0;
-        }
-    }
+    pdl_trigger();
 }
 
 __global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k3_tma_kernel(const KArgs A, const int par, const int init) {
     pdl_wait();
     if (!is_active(A)) return;
+    k3_sum_rr(A);
     extern __shared__ __align__(128) unsigned char smraw[];
     auto& S = *reinterpret_cast<TmaSmem<1>*>(smraw);
     const double* __restrict__ t = A.t;
@@ -1022,16 +988,7 @@ __global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k3_tma_kernel(const
         A.s[a] = acc;
         return __dmul_rn(acc, st.vec[0][tt]);
     });
-    if (count_block(&A.sc->counter[2])) {
-        const double tot = final_sum(A.partial[2], n_units(A));
-        if (threadIdx.x == 0) {
-            A.sc->counter[2] = 0;
-            A.sc->ticket[2] = 0;
-            if (A.multi) A.sc->loc[1] = tot;
-            else if (init) fin_init(A, tot, A.sc->red[2]);
-            else fin_iter(A, tot, A.sc->red[2]);
-        }
-    }
+    if (count_block(&A.sc->counter[2])) k3_finish(A, init);
 }
 
 // ---- the whole PCG loop as one cooperative persistent kernel (single rank) ---------------------
@@ -1461,6 +1418,11 @@ void configure_kernels(KArgs& A, int sms) {
     const int64_t U = (int64_t)A.nloc * A.nbx;
     const int64_t S = (int64_t)A.nbx * ((A.nloc + A.rpb - 1) / A.rpb);
     A.g_k1 = persistent_grid(k1_kernel<false>, S, sms, 4096);
+    // PCG_K1_EVEN: the same number of strips for every block (measured no faster at ORCA025)
+    if (!A.dynamic_k1 && getenv("PCG_K1_EVEN")) {
+        const int64_t per = (S + A.g_k1 - 1) / A.g_k1;
+        A.g_k1 = (int)((S + per - 1) / per);
+    }
     A.g_k2 = persistent_grid(k2_ainv_kernel, U, sms, 2048);
     A.g_k3 = persistent_grid(k3_ainv_kernel, U, sms, 2048);
     A.g_kd = persistent_grid(k2_diag_kernel, U, sms, 4096);
@@ -1469,8 +1431,8 @@ void configure_kernels(KArgs& A, int sms) {
     if (const char* e = getenv("PCG_K1FLAT")) A.k1flat = atoi(e) != 0;
     A.pdl = 1;
     if (const char* e = getenv("PCG_PDL")) A.pdl = atoi(e) != 0;
-    A.x2 = 0;
-    if (const char* e = getenv("PCG_X2")) A.x2 = atoi(e) != 0;
+    A.landskip = A.ocean != nullptr;
+    if (const char* e = getenv("PCG_LANDSKIP")) A.landskip = A.landskip && atoi(e) != 0;
     A.g_k1f = persistent_grid(k1_flat_kernel<false>, U, sms, 0);
     A.tma = 0;                                         // measured no faster than the LDG path (r01)
     if (const char* e = getenv("PCG_TMA")) A.tma = atoi(e) != 0;
@@ -1569,5 +1531,16 @@ void launch_set_cond(cudaGraphConditionalHandle h, cudaStream_t st) { set_cond_k
 // Diagnostic build only: copy the block timeline of the last K1/K2/K3 launches to the host.
 extern "C" int pcg_diag_timeline(unsigned long long* out) {
     return (int)cudaMemcpyFromSymbol(out, pcg::g_timeline, sizeof(pcg::g_timeline));
+}
+extern "C" int pcg_diag_tail(unsigned long long* out) {
+    return (int)cudaMemcpyFromSymbol(out, pcg::g_tail, sizeof(pcg::g_tail));
+}
+extern "C" int pcg_diag_units(unsigned* out, int reset) {
+    int e = (int)cudaMemcpyFromSymbol(out, pcg::g_units, sizeof(pcg::g_units));
+    if (reset) {
+        static unsigned z[2048] = {};
+        cudaMemcpyToSymbol(pcg::g_units, z, sizeof(z));
+    }
+    return e;
 }
 #endif

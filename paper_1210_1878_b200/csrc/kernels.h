@@ -39,7 +39,8 @@ struct KArgs {
     int32_t g_loop;                   // cooperative grid of the fused loop kernel
     int32_t k1flat, g_k1f;            // K1 in row-segment form (one element per thread)
     int32_t pdl;                      // programmatic dependent launch of the iteration kernels
-    int32_t x2;                       // K2/K3: two units per ticket, interleaved
+    int32_t landskip;                 // K2/K3 (dynamic): land / padding lanes issue no memory traffic
+    const uint32_t* ocean;            // [nloc][nbx][kWarps] ocean bit masks (bit l: column 32w + l)
     int32_t precond;                  // pcg_precond
     int64_t nel;                      // owned elements nloc * pitch
     const double *cE, *cN, *sigma, *diag, *piv;

@@ -32,6 +32,7 @@ struct pcg_ctx {
     std::vector<void*> allocs;
     int64_t dev_bytes = 0;
     double *cE = nullptr, *cN = nullptr, *sigma = nullptr, *diag = nullptr, *piv = nullptr;
+    uint32_t* ocean = nullptr;         // per (row, segment, warp) ocean bit masks
     double *x = nullptr, *b = nullptr, *q = nullptr, *t = nullptr, *s = nullptr, *r[2] = {}, *d[2] = {};
     double *partial[3] = {}, *gath = nullptr, *hist = nullptr;
     double *zt_val = nullptr, *z_val = nullptr, *zt_oval = nullptr, *z_oval = nullptr;
@@ -473,6 +474,14 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         A.rpb = 4;                                      // K1 strip height (measured best 4-6 at ORCA025)
         if (const char* e = getenv("PCG_ROWS_PER_BLOCK")) A.rpb = std::max(1, std::min(kMaxRowsK1, atoi(e)));
         A.rpb = std::min(A.rpb, P.nloc);
+        // ocean bit masks of every 32-column warp chunk (land flag = sign bit of cN; padding = 0)
+        std::vector<uint32_t> om((size_t)P.nloc * A.nbx * (kBlock / 32), 0u);
+        for (int32_t j = 0; j < P.nloc; ++j)
+            for (int32_t i = 0; i < P.ni; ++i)
+                if (!std::signbit(P.cN[(size_t)(j + 1) * P.pitch + i]))
+                    om[((size_t)j * A.nbx + i / kBlock) * (kBlock / 32) + (i % kBlock) / 32] |= 1u << (i % 32);
+        if (Status s = upload(c, c->ocean, om); !s) return s;
+        A.ocean = c->ocean;
         configure_kernels(A, sms);
     }
     A.periodic = P.periodic;

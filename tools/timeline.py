@@ -24,10 +24,14 @@ a = ap.parse_args()
 p = synth.config(a.config)
 S = pcg.Solver(p.cE, p.cN, p.mask, tau=0.1)
 b = S.apply_operator(torch.from_numpy(synth.xstar(p)).cuda())
-for _ in range(2):
-    S.solve(b, tol=0.0, maxit=a.maxit)
-torch.cuda.synchronize()
 lib = ctypes.CDLL(os.environ["PCG_LIB"])
+S.solve(b, tol=0.0, maxit=a.maxit)
+torch.cuda.synchronize()
+units = np.zeros(2048, dtype=np.uint32)
+lib.pcg_diag_units(units.ctypes.data_as(ctypes.c_void_p), 1)
+S.solve(b, tol=0.0, maxit=a.maxit)
+torch.cuda.synchronize()
+lib.pcg_diag_units(units.ctypes.data_as(ctypes.c_void_p), 0)
 buf = np.zeros((3, 2048, 4), dtype=np.uint64)
 assert lib.pcg_diag_timeline(buf.ctypes.data_as(ctypes.c_void_p)) == 0
 grid = [S._grid_sizes[i] if hasattr(S, "_grid_sizes") else None for i in range(3)]
@@ -44,3 +48,19 @@ for kk, name in enumerate(("K1", "K2", "K3")):
     print(f"{name} blocks={live.sum():4d} entry[{q(0)}] wait[{q(1)}] loopend[{q(2)}] last_done={fin.max() if len(fin) else float('nan'):7.2f}")
     busy = (rel[:, 2] - rel[:, 1])
     print(f"    block busy (loopend-wait): mean {busy.mean():6.2f} min {busy.min():6.2f} max {busy.max():6.2f}")
+    idx = np.nonzero(live)[0]
+    slow = np.argsort(-rel[:, 2])[:5]
+    print("    slowest blocks (id, wait, loopend):", [(int(idx[s]), round(float(rel[s, 1]), 2), round(float(rel[s, 2]), 2)) for s in slow])
+nz = units[units > 0] / (2 * a.maxit)
+print("units per block per K2+K3 launch (all dynamic kernels, summed / launches): mean %.2f min %.2f max %.2f" % (nz.mean(), nz.min(), nz.max()))
+print("blocks with most units:", [(int(i), round(float(units[i]) / (2 * a.maxit), 2)) for i in np.argsort(-units)[:5]])
+
+tail = np.zeros((3, 4), dtype=np.uint64)
+if hasattr(lib, "pcg_diag_tail"):
+    lib.pcg_diag_tail(tail.ctypes.data_as(ctypes.c_void_p))
+    for kk in range(3):
+        if tail[kk, 0]:
+            lb = int(np.argmax(buf[kk, :, 3]))
+            print("K%d last block %d: loopend->counted %.2f us, count->sums %.2f us, sums->end %.2f us; latest loopend of any block -> its loopend %.2f us" % (
+                  kk + 1, lb, (int(tail[kk, 0]) - int(buf[kk, lb, 2])) / 1e3, (int(tail[kk, 1]) - int(tail[kk, 0])) / 1e3,
+                  (int(buf[kk, :, 3].max()) - int(tail[kk, 1])) / 1e3, (int(buf[kk, lb, 2]) - int(buf[kk, :, 2].max())) / 1e3))
