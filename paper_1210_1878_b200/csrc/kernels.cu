@@ -83,17 +83,19 @@ __device__ __forceinline__ bool count_block(uint32_t* counter) {
 }
 
 // In the last block: thread t sums partials t, t+B, ... left to right, then the block tree.
-// All of a thread's loads (up to 32, i.e. G <= 8192) are issued before the first add, so the
-// walk costs one L2 round trip; longer walks continue in rounds of 32.
+// NB loads per thread are issued before their adds (NB = 32: G <= 8192 in one L2 round trip);
+// kernels with a tight register budget use a smaller NB so the walk does not force spills into
+// their main loop.
+template <int NB = 32>
 __device__ __forceinline__ double final_sum(const double* partial, int64_t G) {
     double acc = 0.0;
     int64_t m = threadIdx.x < kBlock ? (int64_t)threadIdx.x : G;
-    for (; m < G; m += 32 * kBlock) {
-        double p[32];
+    for (; m < G; m += NB * kBlock) {
+        double p[NB];
 #pragma unroll
-        for (int u = 0; u < 32; ++u) p[u] = m + u * kBlock < G ? __ldcg(partial + m + u * kBlock) : 0.0;
+        for (int u = 0; u < NB; ++u) p[u] = m + u * kBlock < G ? __ldcg(partial + m + u * kBlock) : 0.0;
 #pragma unroll
-        for (int u = 0; u < 32; ++u)
+        for (int u = 0; u < NB; ++u)
             if (m + u * kBlock < G) acc = __dadd_rn(acc, p[u]);
     }
     return block_tree(acc);
@@ -672,6 +674,9 @@ __device__ __forceinline__ double ell_row(const EllDev& E, int64_t e, Gather gat
 #endif
 
 
+#ifndef PCG_FINAL_NB_K3
+#define PCG_FINAL_NB_K3 32
+#endif
 // K2 has no last block: its (r, r) is first needed by the convergence test at the end of K3.
 // K3's block 0 forms that final sum as soon as K2 has completed (K2's partials are still in L2),
 // while the other blocks stream; k3_finish (K3's last block) then forms K3's own (s, r), does
@@ -680,7 +685,7 @@ __device__ __forceinline__ double ell_row(const EllDev& E, int64_t e, Gather gat
 // (which acquires there) reads it.
 __device__ __forceinline__ void k3_sum_rr(const KArgs& A) {
     if (blockIdx.x != 0) return;
-    const double rr = final_sum(A.partial[1], n_units(A));
+    const double rr = final_sum<PCG_FINAL_NB_K3>(A.partial[1], n_units(A));
     if (threadIdx.x == 0) {
         if (A.multi) A.sc->loc[2] = rr;
         else A.sc->red[2] = rr;
@@ -691,7 +696,7 @@ __device__ __forceinline__ void k3_finish(const KArgs& A, int init) {
     TT(2, 0);
     FinPre pre{};
     if (threadIdx.x == 0 && !A.multi && !init) pre = fin_prefetch(A);
-    const double rs = final_sum(A.partial[2], n_units(A));
+    const double rs = final_sum<PCG_FINAL_NB_K3>(A.partial[2], n_units(A));
     TT(2, 1);
     if (threadIdx.x == 0) {
         DevScalars* sc = A.sc;

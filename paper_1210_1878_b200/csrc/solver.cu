@@ -95,7 +95,9 @@ Status upload(pcg_ctx* c, T*& p, const std::vector<T>& h) {
 bool use_fused(const pcg_ctx* c) {
     if (c->multi || (c->plan.flags & PCG_FLAG_HOST_LOOP)) return false;
     if (const char* e = getenv("PCG_FUSED")) return atoi(e) != 0;
-    return (int64_t)c->A.nloc * c->A.nbx <= 2048;
+    // measured: fused wins at <= 149 units (cfg1-2: 16 vs 19, 20 vs 21 us/it), the graph at
+    // 584 units (cfg3: 27.6 vs 34.6 us/it) -- grid barriers get dearer with the grid
+    return (int64_t)c->A.nloc * c->A.nbx <= 256;
 }
 bool use_graph(const pcg_ctx* c) { return !c->multi && !(c->plan.flags & PCG_FLAG_HOST_LOOP) && !use_fused(c); }
 
