@@ -134,7 +134,7 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // Diagnostic build only (-DPCG_TIMELINE): per-block globaltimer stamps of the last launch of K1/K2/K3
 // (slot 0 entry, 1 after griddepcontrol.wait, 2 before the block count, 3 last block done).
 #ifdef PCG_TIMELINE
-__device__ unsigned long long g_timeline[3][2048][4];
+__device__ unsigned long long g_timeline[3][2048][8];
 __device__ unsigned g_units[2048];
 __device__ unsigned long long g_tail[3][4];
 #define TT(kk, slot) \
@@ -292,13 +292,44 @@ __device__ __forceinline__ bool finish_units(const KArgs& A, const double* ws, d
     return count_block(counter);
 }
 
-// Dynamic variant: units are handed out by an atomic ticket, so blocks that get slower memory do
-// fewer units; each unit's partial is completed and stored right away (block tree over its 8 warp
-// sums).  Same partials, same canonical order.  Tickets are drawn two units ahead: the atomic for
-// unit n+2 is issued when unit n starts and only consumed when it ends, so no warp waits on it.
-// With A.landskip each warp also loads the ocean bit mask of its 32 columns of the NEXT unit
-// while computing this one; lanes on land or padding then issue no memory traffic at all (their
-// vector entries are zero and stay zero, so the partials are bitwise unchanged).
+// Scheduled static variant (A.sched2/3): units [0, sched_u0) -- the northern rows, with the long
+// pole rows -- are assigned at setup by longest-processing-time on a cost model (overflow rounds
+// of the unit's slowest warp), heaviest first; block b walks sched[soff[b] .. soff[b+1]) with no
+// ticket and no barrier per unit (each warp leaves its warp sum in shared memory and moves on; the
+// block trees run once at the end, finish_sched).  The remaining units [sched_u0, U) are then
+// taken from the dynamic ticket, which absorbs the cost model's error.
+template <class Body>
+__device__ __forceinline__ int sched_units(const KArgs& A, const int32_t* sched, const int32_t* soff, double* ws, Body body) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int32_t k0 = soff[blockIdx.x], k1 = soff[blockIdx.x + 1];
+#ifdef PCG_TIMELINE
+    if (threadIdx.x == 0 && blockIdx.x < 2048) g_timeline[sched == A.sched2 ? 1 : 2][blockIdx.x][7] = (unsigned long long)(k1 - k0);
+#endif
+    for (int32_t k = k0; k < k1; ++k) {
+        Unit W = unit_of(A, sched[k]);
+        if (A.landskip) W.live = W.inrow && ((__ldg(A.ocean + ((int64_t)W.j * A.nbx + W.bx) * kWarps + warp) >> lane) & 1u);
+        double v = warp_tree(body(W));
+        if (lane == 0) ws[(k - k0) * kWarps + warp] = v;
+    }
+    return k1 - k0;
+}
+
+__device__ __forceinline__ void finish_sched(const KArgs& A, const int32_t* sched, const int32_t* soff, const double* ws,
+                                             double* partial) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        const int32_t k0 = soff[blockIdx.x], k1 = soff[blockIdx.x + 1];
+        for (int32_t k = k0; k < k1; ++k) {
+            const int64_t u = sched[k];
+            const int64_t m = (int64_t)(A.nloc - 1 - (int32_t)(u / A.nbx)) * A.nbx + (u % A.nbx);
+            double w = lane < kWarps ? ws[(k - k0) * kWarps + lane] : 0.0;
+            w = warp_tree(w);
+            if (lane == 0) partial[m] = w;
+        }
+    }
+}
+
 // Dynamic variant: units are handed out by an atomic ticket, so blocks that get slower memory do
 // fewer units; each unit's partial is completed and stored right away (block tree over its 8 warp
 // sums).  Same partials, same canonical order.  The ticket for the next unit is drawn when a unit
@@ -309,18 +340,22 @@ __device__ __forceinline__ bool finish_units(const KArgs& A, const double* ws, d
 // land or padding then issue no memory traffic (their vector entries are zero and stay zero, so
 // the partials are bitwise unchanged).
 template <class Body>
-__device__ __forceinline__ void dynamic_units(const KArgs& A, unsigned long long* ticket, double* partial, Body body) {
+__device__ __forceinline__ void dynamic_units(const KArgs& A, unsigned long long* ticket, double* partial, Body body,
+                                              int64_t u0 = 0) {
     __shared__ long long s_next;
     __shared__ double wsd[kWarps];
     const int64_t U = n_units(A);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) s_next = (long long)atomicAdd(ticket, 1ull);
+    if (threadIdx.x == 0) s_next = (long long)atomicAdd(ticket, 1ull) + u0;
     __syncthreads();
     int64_t u = s_next;
+#ifdef PCG_TIMELINE
+    unsigned long long dyn_count = 0;
+#endif
     while (u < U) {
         __syncthreads();                                   // everyone has read s_next
         unsigned long long tk = 0;
-        if (threadIdx.x == 0) tk = atomicAdd(ticket, 1ull);
+        if (threadIdx.x == 0) tk = atomicAdd(ticket, 1ull) + (unsigned long long)u0;
         Unit W = unit_of(A, u);
         if (A.landskip) W.live = W.inrow && ((__ldg(A.ocean + ((int64_t)W.j * A.nbx + W.bx) * kWarps + warp) >> lane) & 1u);
         double v = body(W);
@@ -335,9 +370,12 @@ __device__ __forceinline__ void dynamic_units(const KArgs& A, unsigned long long
         }
         u = s_next;
 #ifdef PCG_TIMELINE
-        if (threadIdx.x == 0 && blockIdx.x < 2048) g_units[blockIdx.x] += 1;
+        if (threadIdx.x == 0 && blockIdx.x < 2048) { g_units[blockIdx.x] += 1; dyn_count += 1; }
 #endif
     }
+#ifdef PCG_TIMELINE
+    if (threadIdx.x == 0 && blockIdx.x < 2048) g_timeline[ticket == &A.sc->ticket[1] ? 1 : (ticket == &A.sc->ticket[2] ? 2 : 0)][blockIdx.x][6] = dyn_count;
+#endif
 }
 
 // ---- K1: d = s + beta d_old ; x += alpha_prev d_old ; q = A d ; (d, q) --------------------
@@ -748,7 +786,15 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
         }
         return v;
     };
-    if (A.dynamic) {
+    if (A.sched2) {
+        sched_units(A, A.sched2, A.soff2, ws, body);
+        TL(1, 4);
+        finish_sched(A, A.sched2, A.soff2, ws, A.partial[1]);
+        TL(1, 5);
+        dynamic_units(A, &A.sc->ticket[1], A.partial[1], body, A.sched_u0);
+        pdl_trigger();
+        TL(1, 2);
+    } else if (A.dynamic) {
         dynamic_units(A, &A.sc->ticket[1], A.partial[1], body);
         pdl_trigger();
         TL(1, 2);
@@ -782,7 +828,16 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
         return v;
     };
     bool last;
-    if (A.dynamic) {
+    if (A.sched3) {
+        sched_units(A, A.sched3, A.soff3, ws, body);
+        TL(2, 4);
+        finish_sched(A, A.sched3, A.soff3, ws, A.partial[2]);
+        TL(2, 5);
+        dynamic_units(A, &A.sc->ticket[2], A.partial[2], body, A.sched_u0);
+        pdl_trigger();
+        TL(2, 2);
+        last = count_block(&A.sc->counter[2]);
+    } else if (A.dynamic) {
         dynamic_units(A, &A.sc->ticket[2], A.partial[2], body);
         pdl_trigger();
         TL(2, 2);
@@ -1384,7 +1439,7 @@ __global__ void set_cond_kernel(cudaGraphConditionalHandle h) { cudaGraphSetCond
 // shared memory of a persistent row kernel: NV warp-sum slots per unit it may process
 size_t row_smem(const KArgs& A, int grid, int NV) {
     const int64_t U = (int64_t)A.nloc * A.nbx;
-    const int64_t per = (U + grid - 1) / grid;
+    const int64_t per = std::max<int64_t>((U + grid - 1) / grid, A.sched_max);
     return (size_t)std::max<int64_t>(per, 1) * NV * kWarps * sizeof(double);
 }
 

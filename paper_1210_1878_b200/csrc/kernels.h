@@ -39,6 +39,12 @@ struct KArgs {
     int32_t g_loop;                   // cooperative grid of the fused loop kernel
     int32_t k1flat, g_k1f;            // K1 in row-segment form (one element per thread)
     int32_t pdl;                      // programmatic dependent launch of the iteration kernels
+    const int32_t* sched2;            // K2 scheduled static walk: unit list (NULL = dynamic tickets)
+    const int32_t* soff2;             // [g_k2 + 1] offsets of each block's list
+    const int32_t* sched3;            // same for K3
+    const int32_t* soff3;
+    int32_t sched_max;                // longest list (shared memory per block)
+    int64_t sched_u0;                 // units [sched_u0, U) come from the dynamic ticket
     int32_t landskip;                 // K2/K3 (dynamic): land / padding lanes issue no memory traffic
     const uint32_t* ocean;            // [nloc][nbx][kWarps] ocean bit masks (bit l: column 32w + l)
     int32_t precond;                  // pcg_precond

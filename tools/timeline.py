@@ -32,7 +32,7 @@ lib.pcg_diag_units(units.ctypes.data_as(ctypes.c_void_p), 1)
 S.solve(b, tol=0.0, maxit=a.maxit)
 torch.cuda.synchronize()
 lib.pcg_diag_units(units.ctypes.data_as(ctypes.c_void_p), 0)
-buf = np.zeros((3, 2048, 4), dtype=np.uint64)
+buf = np.zeros((3, 2048, 8), dtype=np.uint64)
 assert lib.pcg_diag_timeline(buf.ctypes.data_as(ctypes.c_void_p)) == 0
 grid = [S._grid_sizes[i] if hasattr(S, "_grid_sizes") else None for i in range(3)]
 t0 = min(int(v) for v in buf[0, :, 0] if v > 0)
@@ -64,3 +64,16 @@ if hasattr(lib, "pcg_diag_tail"):
             print("K%d last block %d: loopend->counted %.2f us, count->sums %.2f us, sums->end %.2f us; latest loopend of any block -> its loopend %.2f us" % (
                   kk + 1, lb, (int(tail[kk, 0]) - int(buf[kk, lb, 2])) / 1e3, (int(tail[kk, 1]) - int(tail[kk, 0])) / 1e3,
                   (int(buf[kk, :, 3].max()) - int(tail[kk, 1])) / 1e3, (int(buf[kk, lb, 2]) - int(buf[kk, :, 2].max())) / 1e3))
+
+for kk in (1, 2):
+    T = buf[kk].astype(np.int64)
+    live = T[:, 0] > 0
+    if not (T[live, 4] > 0).any():
+        continue
+    ids = np.nonzero(live)[0]
+    rel = (T[live] - t0) / 1e3
+    stat = rel[:, 4] - rel[:, 1]
+    order = np.argsort(-rel[:, 2])[:8]
+    print("K%d static phase: mean %.2f min %.2f max %.2f us; dynamic units/block mean %.2f" % (kk + 1, stat.mean(), stat.min(), stat.max(), T[live, 6].mean()))
+    for o in order:
+        print("   block %4d static %.2f us (%d units) + dyn %d units -> loopend %.2f" % (ids[o], stat[o], T[live][o, 7], T[live][o, 6], rel[o, 2]))
