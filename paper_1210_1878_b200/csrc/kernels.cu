@@ -184,7 +184,7 @@ __device__ void fin_init(const KArgs& A, double rho0, double rr0) {
 // Scalars fin_iter reads, loaded by the last block's thread 0 before its final sum so the loads
 // overlap the partial walk instead of following it.
 struct FinPre {
-    double rr, rho, nb, tol;
+    double rr, rho, nb, tol, h;
     int32_t k, maxit;
 };
 
@@ -192,6 +192,7 @@ __device__ __forceinline__ FinPre fin_prefetch(const KArgs& A) {
     const DevScalars* sc = A.sc;
     FinPre f;
     f.rr = sc->red[2];
+    f.h = sc->hpre;
     f.rho = sc->rho;
     f.nb = sc->nb;
     f.tol = sc->tol;
@@ -211,16 +212,19 @@ __device__ void fin_iter(const KArgs& A, double rho_new, const FinPre& f) {
     }
     sc->beta = __ddiv_rn(rho_new, f.rho);
     sc->rho = rho_new;
-    const double h = __ddiv_rn(__dsqrt_rn(f.rr), f.nb);
+    const double h = f.h;
     if (k < A.hist_cap) A.hist[k] = h;
     const int act = (h > f.tol) && (k < f.maxit);
     sc->active = act;
+    TT(2, 2);
     set_cond(A, act);
+    TT(2, 3);
 }
 
 __device__ void fin_iter(const KArgs& A, double rho_new, double rr) {
     FinPre f = fin_prefetch(A);
     f.rr = rr;
+    f.h = __ddiv_rn(__dsqrt_rn(rr), f.nb);
     fin_iter(A, rho_new, f);
 }
 
@@ -721,27 +725,32 @@ __device__ __forceinline__ double ell_row(const EllDev& E, int64_t e, Gather gat
 // K2's bookkeeping (alpha for the pending x update, ticket / counter reset) and fin_init /
 // fin_iter.  Block 0's store of (r, r) precedes its release in count_block, so the last block
 // (which acquires there) reads it.
-__device__ __forceinline__ void k3_sum_rr(const KArgs& A) {
+__device__ __forceinline__ void k3_sum_rr(const KArgs& A, int init) {
     if (blockIdx.x != 0) return;
     const double rr = final_sum<PCG_FINAL_NB_K3>(A.partial[1], n_units(A));
     if (threadIdx.x == 0) {
-        if (A.multi) A.sc->loc[2] = rr;
-        else A.sc->red[2] = rr;
+        DevScalars* sc = A.sc;
+        if (A.multi) {
+            sc->loc[2] = rr;
+        } else {
+            // everything of fin that does not depend on K3's own sum, off the last block's path:
+            // the history value h and K2's alpha (same IEEE operations as in fin_iter / get_alpha)
+            sc->red[2] = rr;
+            sc->hpre = __ddiv_rn(__dsqrt_rn(rr), sc->nb);
+        }
+        sc->alpha = init ? 0.0 : __ddiv_rn(sc->rho, sc->red[0]);   // K2 checked gamma > 0
+        sc->xpend = init ? 0 : 1;
     }
 }
 
 __device__ __forceinline__ void k3_finish(const KArgs& A, int init) {
     TT(2, 0);
     FinPre pre{};
-    if (threadIdx.x == 0 && !A.multi && !init) pre = fin_prefetch(A);
+    if (threadIdx.x == 0) pre = fin_prefetch(A);       // independent of the walk: overlaps it
     const double rs = final_sum<PCG_FINAL_NB_K3>(A.partial[2], n_units(A));
     TT(2, 1);
     if (threadIdx.x == 0) {
         DevScalars* sc = A.sc;
-        double alpha = 0.0;
-        get_alpha(A, init, alpha);                       // K2 ran, so gamma passed this check there
-        sc->alpha = alpha;
-        sc->xpend = init ? 0 : 1;
         sc->counter[1] = 0;
         sc->ticket[1] = 0;
         sc->counter[2] = 0;
@@ -749,7 +758,7 @@ __device__ __forceinline__ void k3_finish(const KArgs& A, int init) {
         if (A.multi) {
             sc->loc[1] = rs;
         } else if (init) {
-            fin_init(A, rs, sc->red[2]);
+            fin_init(A, rs, pre.rr);
         } else {
             fin_iter(A, rs, pre);
         }
@@ -813,7 +822,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
     pdl_wait();
     TL(2, 1);
     if (!is_active(A)) return;
-    k3_sum_rr(A);
+    k3_sum_rr(A, init);
     extern __shared__ double ws[];
     const double* __restrict__ rn = A.r[par ^ 1];
     const double* __restrict__ t = A.t;
@@ -1037,7 +1046,7 @@ __global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k2_tma_kernel(const
 __global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k3_tma_kernel(const KArgs A, const int par, const int init) {
     pdl_wait();
     if (!is_active(A)) return;
-    k3_sum_rr(A);
+    k3_sum_rr(A, init);
     extern __shared__ __align__(128) unsigned char smraw[];
     auto& S = *reinterpret_cast<TmaSmem<1>*>(smraw);
     const double* __restrict__ t = A.t;

@@ -61,6 +61,10 @@ if hasattr(lib, "pcg_diag_tail"):
     for kk in range(3):
         if tail[kk, 0]:
             lb = int(np.argmax(buf[kk, :, 3]))
+            if tail[kk, 2] and tail[kk, 3]:
+                print("K%d fin: sums->before set_cond %.2f us, set_cond %.2f us, after set_cond -> block end %.2f us" % (
+                      kk + 1, (int(tail[kk, 2]) - int(tail[kk, 1])) / 1e3, (int(tail[kk, 3]) - int(tail[kk, 2])) / 1e3,
+                      (int(buf[kk, :, 3].max()) - int(tail[kk, 3])) / 1e3))
             print("K%d last block %d: loopend->counted %.2f us, count->sums %.2f us, sums->end %.2f us; latest loopend of any block -> its loopend %.2f us" % (
                   kk + 1, lb, (int(tail[kk, 0]) - int(buf[kk, lb, 2])) / 1e3, (int(tail[kk, 1]) - int(tail[kk, 0])) / 1e3,
                   (int(buf[kk, :, 3].max()) - int(tail[kk, 1])) / 1e3, (int(buf[kk, lb, 2]) - int(buf[kk, :, 2].max())) / 1e3))
