@@ -60,6 +60,7 @@ struct Ell {
 struct Plan {
     int32_t ni = 0, nj = 0, periodic = 1, jb = 0, je = 0, rank = 0, nranks = 1;
     int32_t nloc = 0, pitch = 0;
+    int32_t halo = 1;              // halo grid rows on each side of the owned rows
     pcg_precond precond = PCG_PRECOND_AINV;
     double tau = 0.1;
     int32_t flags = 0;
@@ -72,7 +73,8 @@ struct Plan {
     std::vector<int64_t> zcolptr, zrow;
     std::vector<double> zhat, pivots, scale;
     double setup_s = 0.0;
-    int64_t elements() const { return (int64_t)(nloc + 2) * pitch; }
+    int64_t elements() const { return (int64_t)(nloc + 2 * halo) * pitch; }
+    int64_t hoff() const { return (int64_t)halo * pitch; }   // array index of owned element 0
     int64_t owned_elements() const { return (int64_t)nloc * pitch; }
 };
 

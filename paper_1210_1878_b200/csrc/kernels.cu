@@ -258,7 +258,7 @@ __device__ __forceinline__ Unit unit_of(const KArgs& A, int64_t u) {
     W.valid = W.i < A.ni;
     W.inrow = W.i < A.pitch;
     W.live = W.inrow;
-    W.a = (int64_t)(W.j + 1) * A.pitch + W.i;
+    W.a = (int64_t)(W.j + A.halo) * A.pitch + W.i;
     return W;
 }
 
@@ -404,7 +404,7 @@ __device__ __forceinline__ void k1_strip(const KArgs& A, int par, int64_t st, do
     const int32_t iw = i == 0 ? ni - 1 : i - 1, ie = i == ni - 1 ? 0 : i + 1;
     const bool ldw = valid && (lane == 0 || i == 0);
     const bool lde = valid && (lane == 31 || i == ni - 1);
-    int64_t a = (int64_t)(j0 + 1) * P + i;
+    int64_t a = (int64_t)(j0 + A.halo) * P + i;
     double dS = 0.0, dC = 0.0, doC = 0.0, cNs = 0.0;
     double pdo = 0.0, ps = 0.0, pcE = 0.0, pcN = 0.0, px = 0.0;   // next row's loads
     if (valid) {
@@ -787,7 +787,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
         if (W.live) {
             const double rnew = __fma_rn(-alpha, q[W.a], ro[W.a]);
             const double pv = A.piv[W.a];
-            const double acc = ell_row(A.zt, W.a - A.pitch,
+            const double acc = ell_row(A.zt, W.a - A.hoff,
                                        [&](int32_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); });
             A.t[W.a] = __ddiv_rn(acc, pv);
             rn[W.a] = rnew;
@@ -830,7 +830,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
         double v = 0.0;
         if (W.live) {
             const double rv = rn[W.a];
-            const double acc = ell_row(A.z, W.a - A.pitch, [&](int32_t g) { return __ldg(t + g); });
+            const double acc = ell_row(A.z, W.a - A.hoff, [&](int32_t g) { return __ldg(t + g); });
             A.s[W.a] = acc;
             v = __dmul_rn(acc, rv);
         }
@@ -933,7 +933,7 @@ __device__ __forceinline__ void tma_fill(TmaSmem<NVEC>& S, int s, const KArgs& A
     bulk_g2s(S.st[s].col, E.col + e0 * kEll, (unsigned)nel * 16u, &S.full[s]);
     bulk_g2s(S.st[s].val, E.val + e0 * kEll, (unsigned)nel * 32u, &S.full[s]);
 #pragma unroll
-    for (int v = 0; v < NVEC; ++v) bulk_g2s(S.st[s].vec[v], vecs[v] + e0 + A.pitch, (unsigned)nel * 8u, &S.full[s]);
+    for (int v = 0; v < NVEC; ++v) bulk_g2s(S.st[s].vec[v], vecs[v] + e0 + A.hoff, (unsigned)nel * 8u, &S.full[s]);
 }
 
 // Complete unit u's partial from the 8 warp sums left in stage s (producer warp, all lanes).
@@ -1032,9 +1032,9 @@ __global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k2_tma_kernel(const
     const double* __restrict__ q = A.q;
     const double* const vecs[3] = {A.q, ro, A.piv};
     tma_pipeline<3>(S, A, A.zt, vecs, &A.sc->ticket[1], A.partial[1], [&](const TmaStage<3>& st, int t, int32_t i, int32_t j) {
-        const int64_t a = (int64_t)(j + 1) * A.pitch + i;
+        const int64_t a = (int64_t)(j + A.halo) * A.pitch + i;
         const double rnew = __fma_rn(-alpha, st.vec[0][t], st.vec[1][t]);
-        const double acc = ell_row_smem(A.zt, st.col[t], st.val[t], a - A.pitch,
+        const double acc = ell_row_smem(A.zt, st.col[t], st.val[t], a - A.hoff,
                                         [&](int32_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); });
         A.t[a] = __ddiv_rn(acc, st.vec[2][t]);
         rn[a] = rnew;
@@ -1052,8 +1052,8 @@ __global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k3_tma_kernel(const
     const double* __restrict__ t = A.t;
     const double* const vecs[1] = {A.r[par ^ 1]};
     tma_pipeline<1>(S, A, A.z, vecs, &A.sc->ticket[2], A.partial[2], [&](const TmaStage<1>& st, int tt, int32_t i, int32_t j) {
-        const int64_t a = (int64_t)(j + 1) * A.pitch + i;
-        const double acc = ell_row_smem(A.z, st.col[tt], st.val[tt], a - A.pitch, [&](int32_t g) { return __ldg(t + g); });
+        const int64_t a = (int64_t)(j + A.halo) * A.pitch + i;
+        const double acc = ell_row_smem(A.z, st.col[tt], st.val[tt], a - A.hoff, [&](int32_t g) { return __ldg(t + g); });
         A.s[a] = acc;
         return __dmul_rn(acc, st.vec[0][tt]);
     });
@@ -1163,7 +1163,7 @@ __device__ __forceinline__ double k2_unit(const KArgs& A, const Unit& W, int par
     const double* __restrict__ q = A.q;
     const double rnew = __fma_rn(-alpha, q[W.a], ro[W.a]);
     const double pv = A.piv[W.a];
-    const double acc = ell_row(A.zt, W.a - A.pitch, [&](int32_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); });
+    const double acc = ell_row(A.zt, W.a - A.hoff, [&](int32_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); });
     A.t[W.a] = __ddiv_rn(acc, pv);
     A.r[par ^ 1][W.a] = rnew;
     return __dmul_rn(rnew, rnew);
@@ -1173,7 +1173,7 @@ __device__ __forceinline__ double k3_unit(const KArgs& A, const Unit& W, int par
     if (!W.inrow) return 0.0;
     const double* __restrict__ t = A.t;
     const double rv = A.r[par ^ 1][W.a];
-    const double acc = ell_row(A.z, W.a - A.pitch, [&](int32_t g) { return __ldg(t + g); });
+    const double acc = ell_row(A.z, W.a - A.hoff, [&](int32_t g) { return __ldg(t + g); });
     A.s[W.a] = acc;
     return __dmul_rn(acc, rv);
 }
@@ -1347,11 +1347,11 @@ __device__ __forceinline__ double stencil(const KArgs& A, const double* __restri
 
 // prep: zero land entries of x and b (land is not an unknown, reading R20), zero d[0] everywhere
 __global__ void __launch_bounds__(kBlock) prep_kernel(const KArgs A) {
-    const int64_t n = (int64_t)(A.nloc + 2) * A.pitch;
+    const int64_t n = (int64_t)(A.nloc + 2 * A.halo) * A.pitch;
     for (int64_t a = (int64_t)blockIdx.x * kBlock + threadIdx.x; a < n; a += (int64_t)gridDim.x * kBlock) {
         A.d[0][a] = 0.0;
         const int64_t row = a / A.pitch;
-        if (row >= 1 && row <= A.nloc) {
+        if (row >= A.halo && row < A.halo + A.nloc) {
             if (signbit(A.cN[a])) { A.x[a] = 0.0; A.b[a] = 0.0; }
         }
     }
@@ -1572,7 +1572,7 @@ void launch_k2_diag(const KArgs& A, int par, int init, int none, cudaStream_t st
     launch_pdl(A, k2_diag_kernel, A.g_kd, kBlock, row_smem(A, A.g_kd, 2), st, A, par, init, none);
 }
 void launch_prep(const KArgs& A, cudaStream_t st) {
-    const int64_t n = (int64_t)(A.nloc + 2) * A.pitch;
+    const int64_t n = (int64_t)(A.nloc + 2 * A.halo) * A.pitch;
     const int64_t G = std::min<int64_t>((n + kBlock - 1) / kBlock, 148 * 16);
     prep_kernel<<<(unsigned)G, kBlock, 0, st>>>(A);
 }

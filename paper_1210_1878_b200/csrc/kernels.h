@@ -33,6 +33,8 @@ struct EllDev {
 
 struct KArgs {
     int32_t ni, pitch, nloc, nranks;
+    int32_t halo;                     // halo grid rows on each side (owned row j at array row j + halo)
+    int64_t hoff;                     // halo * pitch: array index of owned element 0
     int32_t nbx, rpb;                 // column segments of kBlock per row; rows per K1 strip
     int32_t g_k1, g_k2, g_k3, g_kd, g_row;   // persistent grid sizes (configure_kernels)
     int32_t dynamic, dynamic_k1;      // units from an atomic ticket instead of a block stride

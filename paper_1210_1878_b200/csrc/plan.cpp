@@ -1,6 +1,7 @@
 // plan.cpp -- host half of pcg_setup: validation, row partition, anchor check, device-layout
 // coefficient arrays, AINV per block, SELL-32 packing of Z and Z^T.
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -89,11 +90,11 @@ int64_t global_unknown(const uint8_t* mask, int32_t ni, int64_t g) {
 // ascending column order) into SELL-32 with relative (di, dj) column offsets.
 void pack_sell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols,
                const std::vector<double>& vals, int64_t nel, int32_t pitch, int32_t ni, int32_t periodic, Sell& S,
-               bool absolute = false) {
+               bool absolute, int32_t halo) {
     S.dimin = S.dimax = S.djmin = S.djmax = 0;
     auto rel = [&](int64_t e, int32_t ac) -> int32_t {
         const int32_t jr = (int32_t)(e / pitch), ir = (int32_t)(e % pitch);
-        const int32_t jc = ac / pitch - 1, ic = ac % pitch;
+        const int32_t jc = ac / pitch - halo, ic = ac % pitch;
         int32_t di = ic - ir;
         const int32_t dj = jc - jr;
         if (periodic) {
@@ -129,7 +130,7 @@ void pack_sell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& c
                     S.col[slot] = absolute ? cols[rowptr[e] + m] : r;
                 } else {
                     S.val[slot] = 0.0;
-                    S.col[slot] = absolute ? (int32_t)(e + pitch) : 0;
+                    S.col[slot] = absolute ? (int32_t)(e + (int64_t)halo * pitch) : 0;
                 }
             }
         }
@@ -138,15 +139,17 @@ void pack_sell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& c
 
 // Split rows into ELL(kEll) + SELL overflow (same packed offsets, same ascending order).
 void pack_ell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols,
-              const std::vector<double>& vals, int64_t nel, int32_t pitch, int32_t ni, int32_t periodic, Ell& E) {
+              const std::vector<double>& vals, int64_t nel, int32_t pitch, int32_t ni, int32_t periodic, int32_t halo,
+              Ell& E) {
     Sell full;
-    pack_sell(rowptr, cols, vals, nel, pitch, ni, periodic, full, true);   // absolute columns + extents
+    pack_sell(rowptr, cols, vals, nel, pitch, ni, periodic, full, true, halo);   // absolute columns + extents
+    const int64_t hoff = (int64_t)halo * pitch;        // array index of owned element 0
     E.n = nel;
     E.dimin = full.dimin; E.dimax = full.dimax; E.djmin = full.djmin; E.djmax = full.djmax;
     E.val.assign((size_t)kEll * nel, 0.0);
     E.col.assign((size_t)kEll * nel, 0);
     for (int64_t e = 0; e < nel; ++e)                    // padding: value 0 at the row's own point
-        for (int m = 0; m < kEll; ++m) E.col[e * kEll + m] = (int32_t)(e + pitch);
+        for (int m = 0; m < kEll; ++m) E.col[e * kEll + m] = (int32_t)(e + hoff);
     std::vector<int64_t> orp(nel + 1, 0);
     std::vector<int32_t> ocol;
     std::vector<double> oval;
@@ -175,7 +178,7 @@ void pack_ell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& co
     E.ovf.col.assign(E.ovf.off[nsl], 0);
     for (int64_t s = 0; s < nsl; ++s)
         for (int64_t slot = E.ovf.off[s]; slot < E.ovf.off[s + 1]; ++slot)
-            E.ovf.col[slot] = (int32_t)(s * kSlice + (slot - E.ovf.off[s]) % kSlice + pitch);
+            E.ovf.col[slot] = (int32_t)(s * kSlice + (slot - E.ovf.off[s]) % kSlice + hoff);
     for (int64_t s = 0; s < nsl; ++s)
         for (int l = 0; l < kSlice; ++l) {
             const int64_t e = s * kSlice + l;
@@ -227,6 +230,8 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     P.jb = g->j_begin; P.je = g->j_end; P.rank = g->rank; P.nranks = g->nranks;
     P.nloc = P.je - P.jb;
     P.pitch = (ni + kSlice - 1) / kSlice * kSlice;
+    P.halo = 1;
+    if (const char* e = getenv("PCG_HALO_ROWS")) P.halo = std::max(1, atoi(e));   // layout test hook
     P.precond = o->precond;
     P.tau = o->drop_tol;
     P.flags = o->flags;
@@ -261,13 +266,14 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     P.cE.assign(nel, 0.0); P.cN.assign(nel, 0.0);
     P.diag.assign(nel, 1.0); P.piv.assign(nel, 1.0);
     if (P.has_sigma) P.sigma.assign(nel, 0.0);
-    for (int32_t lr = 0; lr < nloc + 2; ++lr) {
-        const int32_t j = P.jb + lr - 1;
+    const int32_t H = P.halo;
+    for (int32_t lr = 0; lr < nloc + 2 * H; ++lr) {
+        const int32_t j = P.jb + lr - H;
         if (j < 0 || j >= nj) continue;
         const int64_t row = (int64_t)j * ni;
         for (int32_t i = 0; i < ni; ++i) {
             const int64_t a = (int64_t)lr * pitch + i;
-            const bool owned = lr >= 1 && lr <= nloc;
+            const bool owned = lr >= H && lr < H + nloc;
             double ce = ((i + 1 < ni) || P.periodic) ? c->cE[row + i] : 0.0;
             double cn = (j + 1 < nj) ? c->cN[row + i] : 0.0;
             if (owned) {
@@ -276,7 +282,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
                 if (std::fabs(cn) == 0.0 && !c->mask[row + i]) P.cN[a] = -0.0;
                 if (P.has_sigma) P.sigma[a] = c->mask[row + i] ? c->sigma[row + i] : 0.0;
                 if (c->mask[row + i]) P.diag[a] = diag_of(row + i);
-            } else if (lr == 0) {
+            } else if (lr == H - 1) {
                 P.cN[a] = cn;                   // southern halo: S face of row j_begin
             }
         }
@@ -334,7 +340,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     // ---- owned columns in natural order: export + Z values z_kj = fl(s_k * zhat_kj)
     auto arr_of = [&](int64_t gi) -> int64_t {        // grid index -> array index (owned / halo rows)
         int32_t i = (int32_t)(gi % ni), j = (int32_t)(gi / ni);
-        return (int64_t)(j - P.jb + 1) * pitch + i;
+        return (int64_t)(j - P.jb + P.halo) * pitch + i;
     };
     P.zcolptr.assign(1, 0);
     std::vector<int64_t> colarr;                 // array index of each owned column
@@ -371,42 +377,43 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         }
     }
     if ((int64_t)colarr.size() != P.n_owned) return Status::err(PCG_ERR_ARG, "internal: owned column count mismatch");
+    const int64_t hoff = (int64_t)P.halo * pitch;        // array index of owned element 0
     for (int64_t r : ent_row_arr)
-        if (r < pitch) return Status::err(PCG_ERR_ARG, "internal: Z entry outside the owned rows");
+        if (r < hoff) return Status::err(PCG_ERR_ARG, "internal: Z entry outside the owned rows");
 
     // ---- SELL of Z^T rows: row (column j of Z) = entries k ascending
     const int64_t nown = P.owned_elements();
     {
         std::vector<int64_t> rp(nown + 1, 0);
-        for (size_t q = 0; q < colarr.size(); ++q) rp[colarr[q] - pitch + 1] = P.zcolptr[q + 1] - P.zcolptr[q];
+        for (size_t q = 0; q < colarr.size(); ++q) rp[colarr[q] - hoff + 1] = P.zcolptr[q + 1] - P.zcolptr[q];
         for (int64_t e = 0; e < nown; ++e) rp[e + 1] += rp[e];
         std::vector<int32_t> cols(rp[nown]);
         std::vector<double> vals(rp[nown]);
         for (size_t q = 0; q < colarr.size(); ++q) {
-            int64_t dst = rp[colarr[q] - pitch];
+            int64_t dst = rp[colarr[q] - hoff];
             for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e, ++dst) {
                 cols[dst] = (int32_t)ent_row_arr[e];
                 vals[dst] = ent_z[e];
             }
         }
-        pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.ZT);
+        pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.halo, P.ZT);
     }
     // ---- SELL of Z rows: row i = entries z_ij over columns j ascending
     {
         std::vector<int64_t> rp(nown + 1, 0);
-        for (int64_t r : ent_row_arr) rp[r - pitch + 1]++;
+        for (int64_t r : ent_row_arr) rp[r - hoff + 1]++;
         for (int64_t e = 0; e < nown; ++e) rp[e + 1] += rp[e];
         std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
         std::vector<int32_t> cols(rp[nown]);
         std::vector<double> vals(rp[nown]);
         for (size_t q = 0; q < colarr.size(); ++q)        // columns visited in ascending order
             for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e) {
-                int64_t r = ent_row_arr[e] - pitch;
+                int64_t r = ent_row_arr[e] - hoff;
                 cols[fill[r]] = (int32_t)colarr[q];
                 vals[fill[r]] = ent_z[e];
                 fill[r]++;
             }
-        pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.Z);
+        pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.halo, P.Z);
     }
     P.setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return Status::ok();

@@ -113,14 +113,16 @@ Status halo(pcg_ctx* c, double* arr, bool with_allgather) {
     NC(ncclGroupStart());
     if (with_allgather) NC(ncclAllGather((const void*)c->sc->loc, (void*)c->gath, 4, ncclDouble, c->comm, c->st));
     if (P.nranks > 1) {
-        const size_t n = (size_t)P.pitch;
+        // one row each way: first owned row <-> southern halo row H-1 of rank-1, last owned row
+        // <-> northern halo row H+nloc of rank+1
+        const size_t n = (size_t)P.pitch, H = (size_t)P.halo;
         if (P.rank > 0) {
-            NC(ncclSend(arr + (size_t)1 * P.pitch, n, ncclDouble, P.rank - 1, c->comm, c->st));
-            NC(ncclRecv(arr, n, ncclDouble, P.rank - 1, c->comm, c->st));
+            NC(ncclSend(arr + H * P.pitch, n, ncclDouble, P.rank - 1, c->comm, c->st));
+            NC(ncclRecv(arr + (H - 1) * P.pitch, n, ncclDouble, P.rank - 1, c->comm, c->st));
         }
         if (P.rank < P.nranks - 1) {
-            NC(ncclSend(arr + (size_t)P.nloc * P.pitch, n, ncclDouble, P.rank + 1, c->comm, c->st));
-            NC(ncclRecv(arr + (size_t)(P.nloc + 1) * P.pitch, n, ncclDouble, P.rank + 1, c->comm, c->st));
+            NC(ncclSend(arr + (H + P.nloc - 1) * P.pitch, n, ncclDouble, P.rank + 1, c->comm, c->st));
+            NC(ncclRecv(arr + (H + P.nloc) * P.pitch, n, ncclDouble, P.rank + 1, c->comm, c->st));
         }
     }
     NC(ncclGroupEnd());
@@ -216,8 +218,9 @@ Status local_exchange(const std::vector<pcg_ctx*>& cs, Ex ex, cudaStream_t st) {
             double* alo = ex == Ex::HaloX ? lo->x : lo->s;
             double* aup = ex == Ex::HaloX ? up->x : up->s;
             const size_t pitch = (size_t)lo->plan.pitch, bytes = pitch * sizeof(double);
-            CU(cudaMemcpyAsync(aup, alo + (size_t)lo->plan.nloc * pitch, bytes, cudaMemcpyDeviceToDevice, st));
-            CU(cudaMemcpyAsync(alo + (size_t)(lo->plan.nloc + 1) * pitch, aup + pitch, bytes, cudaMemcpyDeviceToDevice, st));
+            const size_t Hl = (size_t)lo->plan.halo, Hu = (size_t)up->plan.halo;
+            CU(cudaMemcpyAsync(aup + (Hu - 1) * pitch, alo + (Hl + lo->plan.nloc - 1) * pitch, bytes, cudaMemcpyDeviceToDevice, st));
+            CU(cudaMemcpyAsync(alo + (Hl + lo->plan.nloc) * pitch, aup + Hu * pitch, bytes, cudaMemcpyDeviceToDevice, st));
         }
     }
     return Status::ok();
@@ -354,9 +357,9 @@ Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, doubl
     const cudaMemcpyKind kin = host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     const cudaMemcpyKind kout = host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
     const size_t dp = (size_t)P.pitch * sizeof(double), sp = (size_t)P.ni * sizeof(double);
-    CU(cudaMemcpy2DAsync(c->b + P.pitch, dp, b, sp, sp, (size_t)P.nloc, kin, c->st));
-    if (x0) CU(cudaMemcpy2DAsync(c->x + P.pitch, dp, x0, sp, sp, (size_t)P.nloc, kin, c->st));
-    else CU(cudaMemsetAsync(c->x + P.pitch, 0, (size_t)P.nloc * dp, c->st));
+    CU(cudaMemcpy2DAsync(c->b + P.hoff(), dp, b, sp, sp, (size_t)P.nloc, kin, c->st));
+    if (x0) CU(cudaMemcpy2DAsync(c->x + P.hoff(), dp, x0, sp, sp, (size_t)P.nloc, kin, c->st));
+    else CU(cudaMemsetAsync(c->x + P.hoff(), 0, (size_t)P.nloc * dp, c->st));
     if (use_fused(c)) {
         if (Status s = launch_prologue(c); !s) return s;
         CU(launch_loop(c->A, c->st));
@@ -393,7 +396,7 @@ Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, doubl
         if (!ls) return ls;
         if (Status s = launch_epilogue(c); !s) return s;
     }
-    CU(cudaMemcpy2DAsync(x, sp, c->x + P.pitch, dp, sp, (size_t)P.nloc, kout, c->st));
+    CU(cudaMemcpy2DAsync(x, sp, c->x + P.hoff(), dp, sp, (size_t)P.nloc, kout, c->st));
     CU(cudaEventRecord(c->ev1, c->st));
     CU(cudaMemcpyAsync(c->h_sc, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost, c->st));
     CU(cudaStreamSynchronize(c->st));
@@ -468,6 +471,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     }
     CU(cudaMallocHost(&c->h_sc, sizeof(DevScalars)));
     A.ni = P.ni; A.pitch = P.pitch; A.nloc = P.nloc; A.nranks = P.nranks; A.nel = P.owned_elements();
+    A.halo = P.halo; A.hoff = P.hoff();
     // launch geometry: row segments of kBlock columns; K1 marches strips of rpb
     // rows.  PCG_ROWS_PER_BLOCK overrides (tuning).  The reduction order does not depend on it.
     A.nbx = (P.pitch + kBlock - 1) / kBlock;
@@ -481,7 +485,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         std::vector<uint32_t> om((size_t)P.nloc * A.nbx * (kBlock / 32), 0u);
         for (int32_t j = 0; j < P.nloc; ++j)
             for (int32_t i = 0; i < P.ni; ++i)
-                if (!std::signbit(P.cN[(size_t)(j + 1) * P.pitch + i]))
+                if (!std::signbit(P.cN[(size_t)(j + P.halo) * P.pitch + i]))
                     om[((size_t)j * A.nbx + i / kBlock) * (kBlock / 32) + (i % kBlock) / 32] |= 1u << (i % 32);
         if (Status s = upload(c, c->ocean, om); !s) return s;
         A.ocean = c->ocean;
@@ -663,12 +667,12 @@ pcg_status pcg_apply_operator(pcg_ctx* c, const double* x, double* y) {
         CU(cudaStreamWaitEvent(c->st, c->ev_in, 0));
         const size_t dp = (size_t)P.pitch * sizeof(double), sp = (size_t)P.ni * sizeof(double);
         // stage x in t (zero rows/padding first so halos and padding read 0), result in q
-        CU(cudaMemsetAsync(c->t, 0, (size_t)(P.nloc + 2) * dp, c->st));
-        CU(cudaMemcpy2DAsync(c->t + P.pitch, dp, x, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
+        CU(cudaMemsetAsync(c->t, 0, (size_t)P.elements() / (size_t)P.pitch * dp, c->st));
+        CU(cudaMemcpy2DAsync(c->t + P.hoff(), dp, x, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
         if (c->multi) if (Status s = halo(c, c->t, false); !s) return s;
         launch_apply(c->A, c->t, c->q, c->st);
         CU(cudaGetLastError());
-        CU(cudaMemcpy2DAsync(y, sp, c->q + P.pitch, dp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
+        CU(cudaMemcpy2DAsync(y, sp, c->q + P.hoff(), dp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
         CU(cudaStreamSynchronize(c->st));
         return Status::ok();
     };
@@ -689,15 +693,15 @@ pcg_status pcg_apply_preconditioner(pcg_ctx* c, const double* r, double* sout) {
         std::memset(c->h_sc, 0, sizeof(DevScalars));
         c->h_sc->active = 1; c->h_sc->nb = 1.0; c->h_sc->maxit = 0;
         CU(cudaMemcpyAsync(c->sc, c->h_sc, sizeof(DevScalars), cudaMemcpyHostToDevice, c->st));
-        CU(cudaMemsetAsync(c->q, 0, (size_t)(P.nloc + 2) * dp, c->st));
-        CU(cudaMemsetAsync(c->r[1], 0, (size_t)(P.nloc + 2) * dp, c->st));
-        CU(cudaMemcpy2DAsync(c->r[1] + P.pitch, dp, r, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
+        CU(cudaMemsetAsync(c->q, 0, (size_t)P.elements() / (size_t)P.pitch * dp, c->st));
+        CU(cudaMemsetAsync(c->r[1], 0, (size_t)P.elements() / (size_t)P.pitch * dp, c->st));
+        CU(cudaMemcpy2DAsync(c->r[1] + P.hoff(), dp, r, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
         KArgs A = c->A;
         A.use_cond = 0;
         if (P.precond == PCG_PRECOND_AINV) { launch_k2_ainv(A, 1, 1, c->st); launch_k3_ainv(A, 1, 1, c->st); }
         else launch_k2_diag(A, 1, 1, P.precond == PCG_PRECOND_NONE, c->st);
         CU(cudaGetLastError());
-        CU(cudaMemcpy2DAsync(sout, sp, c->s + P.pitch, dp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
+        CU(cudaMemcpy2DAsync(sout, sp, c->s + P.hoff(), dp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
         CU(cudaStreamSynchronize(c->st));
         c->solved_once = false;
         return Status::ok();
@@ -736,9 +740,9 @@ pcg_status pcg_solve_local_ranks(pcg_ctx* const* ctxs, int32_t n, const double* 
                 CU(cudaMemcpyAsync(c->sc, c->h_sc, sizeof(DevScalars), cudaMemcpyHostToDevice, st));
                 const size_t dp = (size_t)P.pitch * sizeof(double), sp = (size_t)P.ni * sizeof(double);
                 const size_t off = (size_t)P.jb * P.ni;
-                CU(cudaMemcpy2DAsync(c->b + P.pitch, dp, b + off, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, st));
-                if (x0) CU(cudaMemcpy2DAsync(c->x + P.pitch, dp, x0 + off, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, st));
-                else CU(cudaMemsetAsync(c->x + P.pitch, 0, (size_t)P.nloc * dp, st));
+                CU(cudaMemcpy2DAsync(c->b + P.hoff(), dp, b + off, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, st));
+                if (x0) CU(cudaMemcpy2DAsync(c->x + P.hoff(), dp, x0 + off, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, st));
+                else CU(cudaMemsetAsync(c->x + P.hoff(), 0, (size_t)P.nloc * dp, st));
                 CU(cudaStreamSynchronize(st));           // h_sc is reused per context
             }
             if (!(out = run_steps_local(cs, prologue_steps(cs[0]), st))) break;
@@ -757,7 +761,7 @@ pcg_status pcg_solve_local_ranks(pcg_ctx* const* ctxs, int32_t n, const double* 
             for (pcg_ctx* c : cs) {
                 const Plan& P = c->plan;
                 const size_t dp = (size_t)P.pitch * sizeof(double), sp = (size_t)P.ni * sizeof(double);
-                CU(cudaMemcpy2DAsync(x + (size_t)P.jb * P.ni, sp, c->x + P.pitch, dp, sp, (size_t)P.nloc,
+                CU(cudaMemcpy2DAsync(x + (size_t)P.jb * P.ni, sp, c->x + P.hoff(), dp, sp, (size_t)P.nloc,
                                      cudaMemcpyDeviceToDevice, st));
             }
             CU(cudaEventRecord(cs[0]->ev1, st));
