@@ -101,7 +101,11 @@ typedef struct {
     int32_t ainv_parts;    /* 0/1: AINV over this rank's rows; P > 1 (one GPU only): build the
                               preconditioner as P row blocks, exactly as P ranks would */
     int32_t ainv_halo;     /* halo-AINV width w (grid rows south of each block); 0 = block-local.
-                              Only with ainv_parts > 1 (reading R15) */
+                              With ainv_parts > 1 (one GPU) or nranks > 1: each block starts w
+                              rows below its first row, giving one global triangular Z (SURVEY
+                              §8e, R15 and §6).  Across ranks every rank but the last
+                              needs >= 16 owned rows (else PCG_ERR_ARG); the solve then exchanges
+                              w rows of q and r after K1 and the needed rows of t after K2. */
     int32_t setup_threads; /* host threads for the AINV build (0 = automatic) */
 } pcg_opts;
 

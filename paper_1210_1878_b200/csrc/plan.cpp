@@ -210,9 +210,6 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     if (o->ainv_parts < 0 || o->ainv_halo < 0) return Status::err(PCG_ERR_ARG, "pcg_setup: ainv_parts/ainv_halo < 0");
     if (o->ainv_parts > 1 && g->nranks > 1)
         return Status::err(PCG_ERR_ARG, "pcg_setup: ainv_parts emulates ranks on one GPU; use nranks instead");
-    if (g->nranks > 1 && o->ainv_halo > 0)
-        return Status::err(PCG_ERR_ARG, "pcg_setup: halo-AINV (ainv_halo > 0) across ranks is not implemented yet; "
-                                        "emulate it on one GPU with ainv_parts");
     const int32_t ni = g->ni, nj = g->nj;
     const int64_t ng = (int64_t)ni * nj;
     for (int64_t k = 0; k < ng; ++k) {
@@ -237,7 +234,6 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     P.flags = o->flags;
     P.has_sigma = c->sigma != nullptr;
     const int32_t pitch = P.pitch, nloc = P.nloc;
-    const int64_t nel = P.elements();
 
     // diagonal of every ocean point must be positive, then the structural anchor check
     auto diag_of = [&](int64_t gi) {
@@ -263,6 +259,8 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
 
     // device-layout coefficient arrays: absent faces -> 0, land flagged by the
     // sign bit of cN (cN >= 0 always, so -0.0 / -c mark a land cell).
+    auto build_coeff_arrays = [&]() {
+    const int64_t nel = P.elements();
     P.cE.assign(nel, 0.0); P.cN.assign(nel, 0.0);
     P.diag.assign(nel, 1.0); P.piv.assign(nel, 1.0);
     if (P.has_sigma) P.sigma.assign(nel, 0.0);
@@ -287,6 +285,8 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             }
         }
     }
+    };
+
     // owned ocean unknowns, first global index
     P.first_global = 0;
     for (int64_t k = 0; k < (int64_t)P.jb * ni; ++k) P.first_global += c->mask[k] ? 1 : 0;
@@ -294,6 +294,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     for (int64_t k = (int64_t)P.jb * ni; k < (int64_t)P.je * ni; ++k) P.n_owned += c->mask[k] ? 1 : 0;
 
     if (P.precond != PCG_PRECOND_AINV) {
+        build_coeff_arrays();
         P.setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         P.zcolptr.assign(P.n_owned + 1, 0);
         return Status::ok();
@@ -301,9 +302,25 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
 
     // ---- AINV per block (reading R15)
     std::vector<AinvBlock> blocks;
+    // halo-AINV across ranks (w > 0): this rank's block covers its owned rows plus w
+    // southern halo rows (its columns' entries there are applied through K2's gathers of the
+    // received q / r halo rows), and the columns of the northern neighbour whose entries fall in
+    // this rank's top rows are recomputed here -- the neighbour's block starts w rows below its
+    // first row and AINV is left-looking, so its first kNorthRows rows of columns depend on rows
+    // [je - w, je + kNorthRows) only -- and appended to this rank's Z rows (K3 then gathers t on
+    // the northern halo rows it receives from the neighbour).
+    constexpr int32_t kNorthRows = 16;
+    const bool halo_x = P.nranks > 1 && o->ainv_halo > 0;
+    const int32_t w = o->ainv_halo;
+    if (halo_x && P.rank < P.nranks - 1 && P.nloc < kNorthRows)
+        return Status::err(PCG_ERR_ARG, "pcg_setup: halo-AINV across ranks needs >= 16 rows per rank");
     if (P.nranks > 1) {
-        AinvBlock b; b.row_lo = std::max(0, P.jb - o->ainv_halo); b.row_own = P.jb; b.row_hi = P.je;
+        AinvBlock b; b.row_lo = std::max(0, P.jb - w); b.row_own = P.jb; b.row_hi = P.je;
         blocks.push_back(b);
+        if (halo_x && P.rank < P.nranks - 1) {
+            AinvBlock nb; nb.row_lo = std::max(0, P.je - w); nb.row_own = P.je; nb.row_hi = std::min(nj, P.je + kNorthRows);
+            blocks.push_back(nb);                        // blocks[1]: the neighbour's first columns
+        }
     } else {
         int32_t parts = std::max(1, o->ainv_parts);
         if (parts > nj) return Status::err(PCG_ERR_ARG, "pcg_setup: ainv_parts > nj");
@@ -336,6 +353,36 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
                      "A is not SPD to working precision", (int)(b.fail_grid % ni), (int)(b.fail_grid / ni));
             return Status::err(PCG_ERR_NOT_SPD, buf, global_unknown(c->mask, ni, b.fail_grid));
         }
+
+    AinvBlock north;
+    int32_t reach = 0;                                   // t rows needed north of je
+    if (blocks.size() == 2) {
+        north = std::move(blocks[1]);
+        blocks.pop_back();
+        for (size_t q = 0; q < north.col_g.size(); ++q) {
+            const int32_t jc = (int32_t)(north.col_g[q] / ni);
+            for (int64_t e = north.colptr[q]; e < north.colptr[q + 1]; ++e)
+                if (north.row_g[e] < (int64_t)P.je * ni) {
+                    if (jc >= P.je + kNorthRows - 1)
+                        return Status::err(PCG_ERR_ARG, "pcg_setup: Z reaches more than 15 rows (halo-AINV across ranks)");
+                    reach = std::max(reach, jc - P.je + 1);
+                }
+        }
+    }
+    // rows of this rank's t the southern neighbour gathers: the reach of this rank's own columns
+    // into its southern halo rows (the neighbour computed the same columns as its north block)
+    int32_t reach_s = 0;
+    if (halo_x && P.rank > 0)
+        for (size_t q = 0; q < blocks[0].col_g.size(); ++q) {
+            const int32_t jc = (int32_t)(blocks[0].col_g[q] / ni);
+            for (int64_t e = blocks[0].colptr[q]; e < blocks[0].colptr[q + 1]; ++e)
+                if (blocks[0].row_g[e] < (int64_t)P.jb * ni) reach_s = std::max(reach_s, jc - P.jb + 1);
+        }
+    if (halo_x) P.halo = std::max({P.halo, w, reach});
+    P.halo_w = halo_x ? w : 0;
+    P.halo_t = reach;
+    P.halo_t_send = reach_s;
+    build_coeff_arrays();
 
     // ---- owned columns in natural order: export + Z values z_kj = fl(s_k * zhat_kj)
     auto arr_of = [&](int64_t gi) -> int64_t {        // grid index -> array index (owned / halo rows)
@@ -378,8 +425,8 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     }
     if ((int64_t)colarr.size() != P.n_owned) return Status::err(PCG_ERR_ARG, "internal: owned column count mismatch");
     const int64_t hoff = (int64_t)P.halo * pitch;        // array index of owned element 0
-    for (int64_t r : ent_row_arr)
-        if (r < hoff) return Status::err(PCG_ERR_ARG, "internal: Z entry outside the owned rows");
+    for (int64_t r : ent_row_arr)        // entries in the southern halo rows only with halo-AINV across ranks
+        if (r < hoff - (int64_t)P.halo_w * pitch) return Status::err(PCG_ERR_ARG, "internal: Z entry outside the owned rows");
 
     // ---- SELL of Z^T rows: row (column j of Z) = entries k ascending
     const int64_t nown = P.owned_elements();
@@ -398,21 +445,42 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         }
         pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.halo, P.ZT);
     }
-    // ---- SELL of Z rows: row i = entries z_ij over columns j ascending
+    // ---- SELL of Z rows: row i = entries z_ij over columns j ascending (owned rows only; with
+    // halo-AINV across ranks the northern neighbour's columns follow this rank's, ascending)
     {
+        std::vector<int64_t> ncol_arr, nrow_arr;           // north entries in owned rows
+        std::vector<double> nz;
+        for (size_t q = 0; q < north.col_g.size(); ++q)
+            for (int64_t e = north.colptr[q]; e < north.colptr[q + 1]; ++e)
+                if (north.row_g[e] < (int64_t)P.je * ni) {
+                    const int64_t gr = north.row_g[e];
+                    ncol_arr.push_back(arr_of(north.col_g[q]));
+                    nrow_arr.push_back(arr_of(gr));
+                    nz.push_back((1.0 / std::sqrt(diag_of(gr))) * north.zhat[e]);
+                }
+        for (int64_t r : nrow_arr)
+            if (r < hoff) return Status::err(PCG_ERR_ARG, "internal: northern Z entry below the owned rows");
         std::vector<int64_t> rp(nown + 1, 0);
-        for (int64_t r : ent_row_arr) rp[r - hoff + 1]++;
+        for (int64_t r : ent_row_arr) if (r >= hoff) rp[r - hoff + 1]++;
+        for (int64_t r : nrow_arr) rp[r - hoff + 1]++;
         for (int64_t e = 0; e < nown; ++e) rp[e + 1] += rp[e];
         std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
         std::vector<int32_t> cols(rp[nown]);
         std::vector<double> vals(rp[nown]);
         for (size_t q = 0; q < colarr.size(); ++q)        // columns visited in ascending order
             for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e) {
+                if (ent_row_arr[e] < hoff) continue;       // a southern halo row: rank-1's Z row
                 int64_t r = ent_row_arr[e] - hoff;
                 cols[fill[r]] = (int32_t)colarr[q];
                 vals[fill[r]] = ent_z[e];
                 fill[r]++;
             }
+        for (size_t m = 0; m < nrow_arr.size(); ++m) {     // north columns, ascending
+            int64_t r = nrow_arr[m] - hoff;
+            cols[fill[r]] = (int32_t)ncol_arr[m];
+            vals[fill[r]] = nz[m];
+            fill[r]++;
+        }
         pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.halo, P.Z);
     }
     P.setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

@@ -129,16 +129,44 @@ Status halo(pcg_ctx* c, double* arr, bool with_allgather) {
     return Status::ok();
 }
 
+// Halo-AINV exchanges (contiguous row ranges, one message per array and direction).
+//   QR: rows [H+nloc-w, H+nloc) of q and r[par] -> rank+1's rows [H-w, H)
+//   T : rows [H, H+halo_t_send) of t -> rank-1's rows [H+nloc, H+nloc+halo_t)
+Status exch_halo_ainv(pcg_ctx* c, bool qr, bool t, bool with_allgather, int par) {
+    const Plan& P = c->plan;
+    const size_t pt = (size_t)P.pitch, H = (size_t)P.halo, w = (size_t)P.halo_w;
+    NC(ncclGroupStart());
+    if (with_allgather) NC(ncclAllGather((const void*)c->sc->loc, (void*)c->gath, 4, ncclDouble, c->comm, c->st));
+    if (qr && w > 0)
+        for (double* arr : {c->q, c->r[par]}) {
+            if (P.rank < P.nranks - 1)
+                NC(ncclSend(arr + (H + P.nloc - w) * pt, w * pt, ncclDouble, P.rank + 1, c->comm, c->st));
+            if (P.rank > 0) NC(ncclRecv(arr + (H - w) * pt, w * pt, ncclDouble, P.rank - 1, c->comm, c->st));
+        }
+    if (t) {
+        if (P.rank > 0 && P.halo_t_send > 0)
+            NC(ncclSend(c->t + H * pt, (size_t)P.halo_t_send * pt, ncclDouble, P.rank - 1, c->comm, c->st));
+        if (P.rank < P.nranks - 1 && P.halo_t > 0)
+            NC(ncclRecv(c->t + (H + P.nloc) * pt, (size_t)P.halo_t * pt, ncclDouble, P.rank + 1, c->comm, c->st));
+    }
+    NC(ncclGroupEnd());
+    return Status::ok();
+}
+
 // ---------------------------------------------------------------- one iteration / phases
 // Each phase is a list of steps: kernel launches on one rank, or an exchange between ranks
 // (allgather of the rank sums; halo rows of x or s).  run_steps() executes them for one context
 // (exchanges through NCCL); run_steps_local() executes them for several contexts of one process
 // on one GPU (exchanges as device copies) -- the multi-rank device code path emulated rank by
 // rank, phase by phase, with no kernel waiting on another.
-enum class Ex { None, Allgather, HaloX, HaloSAllgather };
+// Halo-AINV across ranks adds QR (w rows of q and r[par] from the southern neighbour, for K2's
+// gathers below the first owned row; fused with the allgather after K1) and T (the northern
+// neighbour's first rows of t, for K3's gathers above the last owned row).
+enum class Ex { None, Allgather, HaloX, HaloSAllgather, AllgatherQR, QR, HaloT };
 struct Step {
     Ex ex;
     std::function<void(pcg_ctx*)> run;   // kernels of one rank (ex == None)
+    int par = 0;                         // QR exchanges: which r buffer K2 reads
 };
 
 std::vector<Step> prologue_steps(const pcg_ctx* c) {
@@ -152,8 +180,15 @@ std::vector<Step> prologue_steps(const pcg_ctx* c) {
         s.push_back({Ex::Allgather, nullptr});
         s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsBB, x->st); }});
     }
-    if (ainv) s.push_back({Ex::None, [](pcg_ctx* x) { launch_k2_ainv(x->A, 1, 1, x->st); launch_k3_ainv(x->A, 1, 1, x->st); }});
-    else s.push_back({Ex::None, [none](pcg_ctx* x) { launch_k2_diag(x->A, 1, 1, none, x->st); }});
+    const bool hx = multi && c->plan.halo_w > 0;
+    if (ainv) {
+        if (hx) s.push_back({Ex::QR, nullptr, 1});
+        s.push_back({Ex::None, [](pcg_ctx* x) { launch_k2_ainv(x->A, 1, 1, x->st); }});
+        if (hx) s.push_back({Ex::HaloT, nullptr});
+        s.push_back({Ex::None, [](pcg_ctx* x) { launch_k3_ainv(x->A, 1, 1, x->st); }});
+    } else {
+        s.push_back({Ex::None, [none](pcg_ctx* x) { launch_k2_diag(x->A, 1, 1, none, x->st); }});
+    }
     if (multi) {
         s.push_back({Ex::HaloSAllgather, nullptr});
         s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsInit, x->st); }});
@@ -165,13 +200,19 @@ std::vector<Step> iteration_steps(const pcg_ctx* c, int par) {
     std::vector<Step> s;
     const bool multi = c->multi, ainv = c->plan.precond == PCG_PRECOND_AINV;
     const bool none = c->plan.precond == PCG_PRECOND_NONE;
+    const bool hx = multi && ainv && c->plan.halo_w > 0;
     s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k1(x->A, par, x->st); }});
     if (multi) {
-        s.push_back({Ex::Allgather, nullptr});
+        s.push_back({hx ? Ex::AllgatherQR : Ex::Allgather, nullptr, par});
         s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsGamma, x->st); }});
     }
-    if (ainv) s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k2_ainv(x->A, par, 0, x->st); launch_k3_ainv(x->A, par, 0, x->st); }});
-    else s.push_back({Ex::None, [par, none](pcg_ctx* x) { launch_k2_diag(x->A, par, 0, none, x->st); }});
+    if (ainv) {
+        s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k2_ainv(x->A, par, 0, x->st); }});
+        if (hx) s.push_back({Ex::HaloT, nullptr});
+        s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k3_ainv(x->A, par, 0, x->st); }});
+    } else {
+        s.push_back({Ex::None, [par, none](pcg_ctx* x) { launch_k2_diag(x->A, par, 0, none, x->st); }});
+    }
     if (multi) {
         s.push_back({Ex::HaloSAllgather, nullptr});
         s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsIter, x->st); }});
@@ -198,6 +239,9 @@ Status run_steps(pcg_ctx* c, const std::vector<Step>& steps) {
             case Ex::Allgather: if (Status r = allgather_loc(c); !r) return r; break;
             case Ex::HaloX: if (Status r = halo(c, c->x, false); !r) return r; break;
             case Ex::HaloSAllgather: if (Status r = halo(c, c->s, true); !r) return r; break;
+            case Ex::AllgatherQR: if (Status r = exch_halo_ainv(c, true, false, true, s.par); !r) return r; break;
+            case Ex::QR: if (Status r = exch_halo_ainv(c, true, false, false, s.par); !r) return r; break;
+            case Ex::HaloT: if (Status r = exch_halo_ainv(c, false, true, false, 0); !r) return r; break;
         }
     }
     CU(cudaGetLastError());
@@ -205,9 +249,30 @@ Status run_steps(pcg_ctx* c, const std::vector<Step>& steps) {
 }
 
 // exchanges between the contexts of one process (same device, one stream)
-Status local_exchange(const std::vector<pcg_ctx*>& cs, Ex ex, cudaStream_t st) {
+Status local_exchange(const std::vector<pcg_ctx*>& cs, Ex ex, cudaStream_t st, int par) {
     const size_t P = cs.size();
-    if (ex == Ex::Allgather || ex == Ex::HaloSAllgather)
+    if (ex == Ex::AllgatherQR || ex == Ex::QR || ex == Ex::HaloT) {
+        for (size_t r = 1; r < P; ++r) {
+            pcg_ctx* lo = cs[r - 1];
+            pcg_ctx* up = cs[r];
+            const size_t pt = (size_t)lo->plan.pitch, Hl = (size_t)lo->plan.halo, Hu = (size_t)up->plan.halo;
+            const size_t nl = (size_t)lo->plan.nloc;
+            if (ex != Ex::HaloT) {
+                const size_t w = (size_t)up->plan.halo_w;
+                if (w > 0) {
+                    CU(cudaMemcpyAsync(up->q + (Hu - w) * pt, lo->q + (Hl + nl - w) * pt, w * pt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+                    CU(cudaMemcpyAsync(up->r[par] + (Hu - w) * pt, lo->r[par] + (Hl + nl - w) * pt, w * pt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+                }
+            } else {
+                if (up->plan.halo_t_send != lo->plan.halo_t)
+                    return Status::err(PCG_ERR_ARG, "internal: t halo rows sent != rows expected");
+                const size_t n = (size_t)lo->plan.halo_t;
+                if (n > 0) CU(cudaMemcpyAsync(lo->t + (Hl + nl) * pt, up->t + Hu * pt, n * pt * sizeof(double), cudaMemcpyDeviceToDevice, st));
+            }
+        }
+        if (ex != Ex::AllgatherQR) return Status::ok();
+    }
+    if (ex == Ex::Allgather || ex == Ex::HaloSAllgather || ex == Ex::AllgatherQR)
         for (size_t r = 0; r < P; ++r)
             for (size_t q = 0; q < P; ++q)
                 CU(cudaMemcpyAsync(cs[r]->gath + 4 * q, cs[q]->sc->loc, 4 * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -230,7 +295,7 @@ Status run_steps_local(const std::vector<pcg_ctx*>& cs, const std::vector<Step>&
     for (const Step& s : steps) {
         if (s.ex == Ex::None) {
             for (pcg_ctx* c : cs) s.run(c);
-        } else if (Status r = local_exchange(cs, s.ex, st); !r) {
+        } else if (Status r = local_exchange(cs, s.ex, st, s.par); !r) {
             return r;
         }
     }

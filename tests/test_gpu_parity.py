@@ -254,6 +254,26 @@ def test_local_ranks_bitwise_vs_oracle_partitioned(name, P, precond):
     R.close()
 
 
+@pytest.mark.parametrize("name,P,w", [("cfg2", 2, 2), ("cfg2", 4, 3), ("cfg3", 3, 2), ("cfg3", 8, 3)])
+def test_local_ranks_halo_ainv_bitwise(name, P, w):
+    """Halo-AINV across ranks (w > 0): per-rank blocks start w rows below the owned
+    rows, the northern neighbour's first columns are recomputed locally, and each iteration
+    exchanges w rows of q and r (after K1) and the needed rows of t (after K2).  Equal bit for
+    bit to the oracle's partitioned canonical PCG with the same global Z (parts = P, halo = w)."""
+    p = synth.config(name)
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, TAU, parts=P, halo=w)
+    b = rhs(A, p)
+    R = pcg.LocalRanks(p.cE, p.cN, p.mask, P, tau=TAU, ainv_halo=w)
+    ref = oracle.pcg(A, b, "ainv", M, 1e-10, maxit=A.n, mode="canonical", pitch=R.pitch, block=R.block, parts=P)
+    xg, k, hist, rep = R.solve(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
+    assert k == ref.iterations
+    assert np.array_equal(hist, ref.hist)
+    assert np.array_equal(host(xg), A.to_grid(ref.x))
+    assert rep["true_rel_residual"] == ref.true_rel_residual
+    R.close()
+
+
 def test_local_ranks_one_rank_equals_single():
     p = synth.config("cfg2")
     A, M, S = setup_pair(p)

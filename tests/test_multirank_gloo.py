@@ -22,7 +22,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, name, q):
+def _worker(rank, world, port, name, halo, q):
     import sys
     sys.path.insert(0, ROOT)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -36,7 +36,7 @@ def _worker(rank, world, port, name, q):
         allrb = [None] * world
         dist.all_gather_object(allrb, rb.tolist())
         pl = pcg.Plan(p.cE, p.cN, p.mask, tau=0.1 + 1e-9, j_begin=int(rb[rank]), j_end=int(rb[rank + 1]),
-                      rank=rank, nranks=world)
+                      rank=rank, nranks=world, ainv_halo=halo)
         mine = dict(rank=rank, rows=(int(rb[rank]), int(rb[rank + 1])), n=pl.n_owned, first=pl.first_global,
                     zh=[a.tolist() for a in pl.export_zhat()])
         allp = [None] * world
@@ -50,15 +50,17 @@ def _worker(rank, world, port, name, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
-def test_two_rank_setup_matches_oracle_partitioned(name):
+@pytest.mark.parametrize("name,halo", [("cfg1", 0), ("cfg2", 0), ("cfg2", 2), ("cfg2", 3)])
+def test_two_rank_setup_matches_oracle_partitioned(name, halo):
+    """halo = 0: block-local AINV per rank; halo = w > 0: each rank's block starts w rows below its
+    first row (halo-AINV across ranks), so its owned columns carry entries in those rows."""
     import oracle
     from paper_1210_1878_b200 import synth
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, name, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, name, halo, q)) for r in range(world)]
     for pr in procs:
         pr.start()
     res = q.get(timeout=300)
@@ -70,7 +72,7 @@ def test_two_rank_setup_matches_oracle_partitioned(name):
     rb = oracle.partition(p.nj, p.ni, p.mask, world)
     assert res["rb"][0] == res["rb"][1] == rb.tolist()
     assert res["blob_ok"]
-    ref = oracle.ainv(A, 0.1 + 1e-9, parts=world, halo=0)
+    ref = oracle.ainv(A, 0.1 + 1e-9, parts=world, halo=halo)
     parts = sorted(res["parts"], key=lambda d: d["rank"])
     assert sum(d["n"] for d in parts) == A.n
     assert parts[0]["first"] == 0 and parts[1]["first"] == parts[0]["n"]
@@ -86,10 +88,13 @@ def test_two_rank_setup_matches_oracle_partitioned(name):
     assert np.array_equal(np.asarray(zh), ref.zhat)
     assert np.array_equal(np.asarray(piv), ref.pivots)
     assert np.array_equal(np.asarray(sc), ref.scale)
-    # block-local: no entry of a rank's columns lies in the other rank's rows
     cols = np.repeat(np.arange(A.n), np.diff(ref.colptr))
     owner = np.searchsorted(np.cumsum([d["n"] for d in parts]), np.arange(A.n), side="right")
-    assert np.all(owner[ref.row] == owner[cols])
+    if halo == 0:       # block-local: no entry of a rank's columns lies in the other rank's rows
+        assert np.all(owner[ref.row] == owner[cols])
+    else:               # halo-AINV: rank 1's columns reach into rank 0's top rows, never the reverse
+        cross = owner[ref.row] != owner[cols]
+        assert cross.any() and np.all(owner[cols[cross]] == 1) and np.all(owner[ref.row[cross]] == 0)
 
 
 def test_multirank_canonical_sum_is_rank_tree():
