@@ -314,10 +314,12 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     const int32_t w = o->ainv_halo;
     if (halo_x && P.rank < P.nranks - 1 && P.nloc < kNorthRows)
         return Status::err(PCG_ERR_ARG, "pcg_setup: halo-AINV across ranks needs >= 16 rows per rank");
+    bool have_north = false;
     if (P.nranks > 1) {
         AinvBlock b; b.row_lo = std::max(0, P.jb - w); b.row_own = P.jb; b.row_hi = P.je;
         blocks.push_back(b);
         if (halo_x && P.rank < P.nranks - 1) {
+            have_north = true;
             AinvBlock nb; nb.row_lo = std::max(0, P.je - w); nb.row_own = P.je; nb.row_hi = std::min(nj, P.je + kNorthRows);
             blocks.push_back(nb);                        // blocks[1]: the neighbour's first columns
         }
@@ -356,7 +358,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
 
     AinvBlock north;
     int32_t reach = 0;                                   // t rows needed north of je
-    if (blocks.size() == 2) {
+    if (have_north) {
         north = std::move(blocks[1]);
         blocks.pop_back();
         for (size_t q = 0; q < north.col_g.size(); ++q) {
