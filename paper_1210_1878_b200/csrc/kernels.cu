@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
 }
 
 #ifndef PCG_MINB_K1F
-#define PCG_MINB_K1F 6
+#define PCG_MINB_K1F 4           // 64 registers: no spills (6 blocks/SM spilled and ran slower)
 #endif
 // ---- K1, row-segment form: one element per thread, units from the dynamic ticket ----------------
 // Same arithmetic as k1_strip (bitwise): d at the point and at its S/N neighbours recomputed from
@@ -616,9 +616,22 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1F) k1_flat_kernel(const KAr
         }
     }
     const double beta = A.sc->beta, alpha = A.sc->alpha;
-    dynamic_units(A, &A.sc->ticket[0], A.partial[0], [&](const Unit& W) { return k1_point<SIGMA>(A, W, par, beta, alpha); });
-    pdl_trigger();
-    if (count_block(&A.sc->counter[0])) {
+    bool last;
+    if (A.k1flat == 2) {
+        // static block stride, no barrier per unit: warp sums in shared memory, trees at the end
+        extern __shared__ double ws[];
+        const int64_t U = n_units(A);
+        int k = 0;
+        for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k)
+            put_warp_sum(ws, k, k1_point<SIGMA>(A, unit_of(A, u), par, beta, alpha));
+        pdl_trigger();
+        last = finish_units<1>(A, ws, A.partial[0], nullptr, &A.sc->counter[0]);
+    } else {
+        dynamic_units(A, &A.sc->ticket[0], A.partial[0], [&](const Unit& W) { return k1_point<SIGMA>(A, W, par, beta, alpha); });
+        pdl_trigger();
+        last = count_block(&A.sc->counter[0]);
+    }
+    if (last) {
         const double tot = final_sum(A.partial[0], n_units(A));
         if (threadIdx.x == 0) {
             if (A.multi) A.sc->loc[0] = tot;
@@ -1496,8 +1509,10 @@ void configure_kernels(KArgs& A, int sms) {
     A.g_k3 = persistent_grid(k3_ainv_kernel, U, sms, 2048);
     A.g_kd = persistent_grid(k2_diag_kernel, U, sms, 4096);
     A.g_row = persistent_grid(init_residual_kernel, U, sms, 2048);
-    A.k1flat = 0;
-    if (const char* e = getenv("PCG_K1FLAT")) A.k1flat = atoi(e) != 0;
+    // K1 form: 2 = row-segment units, static block stride, no barrier per unit (default: 94.7 ->
+    // 91.9 us/iteration at ORCA025 against the 4-row strips, 0); 1 = same units, dynamic tickets
+    A.k1flat = 2;
+    if (const char* e = getenv("PCG_K1FLAT")) A.k1flat = atoi(e);
     A.pdl = 1;
     if (const char* e = getenv("PCG_PDL")) A.pdl = atoi(e) != 0;
     A.landskip = A.ocean != nullptr;
@@ -1553,8 +1568,9 @@ static void launch_pdl(const KArgs& A, void (*kern)(P...), int grid, int block, 
 
 void launch_k1(const KArgs& A, int par, cudaStream_t st) {
     if (A.k1flat) {
-        if (A.sigma) launch_pdl(A, k1_flat_kernel<true>, A.g_k1f, kBlock, 0, st, A, par);
-        else launch_pdl(A, k1_flat_kernel<false>, A.g_k1f, kBlock, 0, st, A, par);
+        const size_t sm = A.k1flat == 2 ? row_smem(A, A.g_k1f, 1) : 0;
+        if (A.sigma) launch_pdl(A, k1_flat_kernel<true>, A.g_k1f, kBlock, sm, st, A, par);
+        else launch_pdl(A, k1_flat_kernel<false>, A.g_k1f, kBlock, sm, st, A, par);
     } else {
         if (A.sigma) launch_pdl(A, k1_kernel<true>, A.g_k1, kBlock, k1_smem(A, A.g_k1), st, A, par);
         else launch_pdl(A, k1_kernel<false>, A.g_k1, kBlock, k1_smem(A, A.g_k1), st, A, par);
