@@ -10,6 +10,7 @@ Functions (all fp64; unknown vectors are ocean points in natural order, PAPER.md
   Assembled.apply(x)              -> A x
   Assembled.anchor_check()        -> -1 or the first unanchored unknown
   ainv(asm, tau, ...)             -> Ainv  (Zhat, pivots, scale; PAPER.md:459)
+  fsai(asm, q)                    -> Ainv  (the paper's banded FSAI of T)
   pcg(asm, b, ...)                -> PcgResult (Alg. 1, d = s + beta d)
   partition(nj, ni, mask, parts)  -> row bounds
 """
@@ -24,7 +25,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
-_SOURCES = ["assemble.c", "ainv.c", "pcg.c"]
+_SOURCES = ["assemble.c", "ainv.c", "fsai.c", "pcg.c"]
 
 ERR = {0: "OK", 1: "ARG", 2: "NOT_SPD", 3: "BREAKDOWN", 6: "NOMEM"}
 PRECOND = {"ainv": 0, "jacobi": 1, "none": 2}
@@ -68,6 +69,8 @@ def lib():
         L.orc_partition.argtypes = [I32, I32, vp, I32, vp]
         L.orc_ainv_build.argtypes = [P, D, I32, I32, I32, C.POINTER(P), C.POINTER(I64)]
         L.orc_ainv_build.restype = C.c_int
+        L.orc_fsai_build.argtypes = [P, I32, C.POINTER(P), C.POINTER(I64)]
+        L.orc_fsai_build.restype = C.c_int
         L.orc_ainv_free.argtypes = [P]
         L.orc_ainv_nnz.argtypes = [P]; L.orc_ainv_nnz.restype = I64
         L.orc_ainv_export.argtypes = [P, vp, vp, vp, vp, vp, vp]
@@ -245,6 +248,29 @@ def ainv(A: Assembled, tau: float, method: str = "sparse", parts: int = 1, halo:
                     C.byref(h), C.byref(fail))
     if rc != 0:
         e = OracleError(rc, f"ainv failed at column {fail.value}")
+        e.index = fail.value
+        raise e
+    nnz = int(L.orc_ainv_nnz(h))
+    n = A.n
+    cp = np.empty(n + 1, dtype=np.int64)
+    row = np.empty(nnz, dtype=np.int64)
+    zh = np.empty(nnz)
+    z = np.empty(nnz)
+    pv = np.empty(n)
+    sc = np.empty(n)
+    L.orc_ainv_export(h, _ptr(cp), _ptr(row), _ptr(zh), _ptr(z), _ptr(pv), _ptr(sc))
+    return Ainv(cp, row, zh, z, pv, sc, _AinvHandle(h))
+
+
+def fsai(A: Assembled, q: int) -> Ainv:
+    """The paper's banded FSAI of T = band(A, 1) (Eq. 19), bandwidth q, as an
+    AINV-form factor: unit-diagonal zhat, pivots u_kk^2, scale 1 (P = Zhat D^-1 Zhat^t)."""
+    L = lib()
+    h = C.c_void_p()
+    fail = C.c_int64(-1)
+    rc = L.orc_fsai_build(A._h, int(q), C.byref(h), C.byref(fail))
+    if rc != 0:
+        e = OracleError(rc, f"fsai failed at unknown {fail.value}")
         e.index = fail.value
         raise e
     nnz = int(L.orc_ainv_nnz(h))

@@ -14,6 +14,8 @@
  *     "Bridson P_B1", in two independent
  *     formulations (sparse left-looking and dense right-looking);
  *   - the partitioned ("per partition, halo w") AINV (reading R15);
+ *   - the paper's own preconditioner, the banded FSAI of T = band(A, 1) (PAPER.md:226-309,
+ *     Eq. 19; NEXT-1, reading R25), as an AINV-form factor;
  *   - PCG, Alg. 1 with the line-8 fix d = s + beta d (reading R6),
  *     in "plain" order (sequential sums) and in "canonical" order (the GPU's documented
  *     arithmetic order, re-implemented here from DESIGN.md §5, not from GPU code).
@@ -68,6 +70,12 @@ void orc_ainv_export(const orc_ainv*, int64_t* colptr, int64_t* row, double* zha
                      double* pivots, double* scale);
 /* s = Z D^-1 Z^T r, plain order: t_j = (sum_k z_kj r_k)/p_j, s_i = sum_j z_ij t_j. */
 void orc_ainv_apply(const orc_ainv*, const double* r, double* s);
+
+/* ---- the paper's banded FSAI of T (NEXT-1; Eq. 19) ---- */
+/* T = band(A, 1) in the unknown numbering; T = U^t U; zhat_{k-i,k} = prod_{r=1..i} rho_{k-r},
+ * rho_m = -u_{m,m+1}/u_mm, truncated at bandwidth q (and where the chain breaks); pivots
+ * p_k = u_kk^2; scale 1.  Returned as an orc_ainv: every apply / PCG routine takes it. */
+int  orc_fsai_build(const orc_problem*, int32_t q, orc_ainv** out, int64_t* failed_col);
 
 /* ---- PCG (Alg. 1, with d = s + beta d) ---- */
 typedef struct {
