@@ -2,7 +2,7 @@
 """bench.py -- PCG iterations/s and time-to-solution (fp64, ORCA025-like grid) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config cfg4] [--precond ainv|jacobi] [--tol 1e-10]
+                    [--config cfg4] [--precond ainv|jacobi|fsai] [--fsai-q 4] [--tol 1e-10]
 
 A step is one full solve (pcg_solve: init a3, the PCG loop a4-a8 until ||r||/||b|| <= tol,
 finish a9) of BASELINE.json's headline workload, configs[3]: the ORCA025-like 1442x1021
@@ -149,7 +149,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="cfg4")
-    ap.add_argument("--precond", default="ainv", choices=["ainv", "jacobi"])
+    ap.add_argument("--precond", default="ainv", choices=["ainv", "jacobi", "fsai"])
+    ap.add_argument("--fsai-q", type=int, default=4)
     ap.add_argument("--tau", type=float, default=0.1)
     ap.add_argument("--tol", type=float, default=1e-10)
     ap.add_argument("--ref-iters", type=int, default=40)
@@ -176,7 +177,8 @@ def main():
         group = dist.group.WORLD
     p = synth.config(args.config)
     t0 = time.perf_counter()
-    S = pcg.Solver(p.cE, p.cN, p.mask, tau=args.tau, precond=args.precond, group=group, device=local)
+    S = pcg.Solver(p.cE, p.cN, p.mask, tau=args.tau, precond=args.precond, group=group, device=local,
+                   fsai_q=args.fsai_q)
     setup_wall = time.perf_counter() - t0
     rows = slice(S.j_begin, S.j_end)
     xs = torch.from_numpy(np.ascontiguousarray(synth.xstar(p)[rows])).cuda()
@@ -262,8 +264,8 @@ def main():
                          f"oracle's own assembly+AINV ({r['setup_s']:.2f} s, excluded)"}
 
     # launches per solve: prologue 4 (prep, init, K2, K3) + WHILE body of 2 iterations x 3 + epilogue 2
-    per_iter = 3 if args.precond == "ainv" else 2
-    pro = 4 if args.precond == "ainv" else 3
+    per_iter = 3 if args.precond in ("ainv", "fsai") else 2
+    pro = 4 if args.precond in ("ainv", "fsai") else 3
     if world == 1:
         launches = sum(pro + per_iter * 2 * math.ceil(k / 2) + 2 for k in iters)
     else:
@@ -275,6 +277,7 @@ def main():
                 "data": "synthetic (SURVEY A.1 generator, seed 2; b = A x*, x* ~ N(0,1) seed 0)",
                 "config": {"workload": WORKLOAD, "grid": [p.ni, p.nj], "n_ocean": p.n_ocean,
                            "precond": args.precond, "tau": args.tau, "tol": args.tol,
+                           **({"fsai_q": args.fsai_q} if args.precond == "fsai" else {}),
                            "iterations_per_solve": iters, "time_to_solution_ms": dev_ms / args.steps,
                            "library_solve_ms": 1e3 * lib_s / args.steps,
                            "setup_s": rep["setup_s"], "setup_wall_s": setup_wall,

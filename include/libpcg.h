@@ -63,7 +63,10 @@ typedef enum {
 typedef enum {
     PCG_PRECOND_AINV = 0,   /* s = Z D^-1 Z^T r  (north star) */
     PCG_PRECOND_JACOBI = 1, /* s = r / A_pp: NEMO's diagonal preconditioner (Eq. 15) */
-    PCG_PRECOND_NONE = 2    /* s = r: plain CG */
+    PCG_PRECOND_NONE = 2,   /* s = r: plain CG */
+    PCG_PRECOND_FSAI = 3    /* the paper's own P = Z~ Z~^t: banded FSAI of T = band(A, 1), bandwidth
+                               fsai_q (Eq. 19; R25).
+                               One rank only (nranks > 1 -> PCG_ERR_ARG). */
 } pcg_precond;
 
 /* flags */
@@ -107,6 +110,8 @@ typedef struct {
                               needs >= 16 owned rows (else PCG_ERR_ARG); the solve then exchanges
                               w rows of q and r after K1 and the needed rows of t after K2. */
     int32_t setup_threads; /* host threads for the AINV build (0 = automatic) */
+    int32_t fsai_q;        /* PCG_PRECOND_FSAI: upper bandwidth q >= 0 of Z~ (entries z_ij with
+                              j > i + q dropped); ignored otherwise */
 } pcg_opts;
 
 typedef struct {

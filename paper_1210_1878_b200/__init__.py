@@ -25,7 +25,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PCG_LIB") or os.path.join(_HERE, "libpcg.so")   # PCG_LIB: tuning variants
 
 STATUS = {0: "OK", 1: "ERR_ARG", 2: "ERR_NOT_SPD", 3: "ERR_BREAKDOWN", 4: "ERR_CUDA", 5: "ERR_COMM", 6: "ERR_NOMEM"}
-PRECOND = {"ainv": 0, "jacobi": 1, "none": 2}
+PRECOND = {"ainv": 0, "jacobi": 1, "none": 2, "fsai": 3}
 FLAG_HOST_LOOP = 1
 FLAG_COMM_PATH = 2
 FLAG_LOCAL_RANKS = 4
@@ -49,7 +49,8 @@ class Coeffs(C.Structure):
 
 class Opts(C.Structure):
     _fields_ = [("precond", C.c_int32), ("drop_tol", C.c_double), ("flags", C.c_int32),
-                ("ainv_parts", C.c_int32), ("ainv_halo", C.c_int32), ("setup_threads", C.c_int32)]
+                ("ainv_parts", C.c_int32), ("ainv_halo", C.c_int32), ("setup_threads", C.c_int32),
+                ("fsai_q", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -136,15 +137,16 @@ def _host_inputs(cE, cN, mask, sigma):
     return cE, cN, mask, sigma
 
 
-def _opts(precond, tau, flags, ainv_parts, ainv_halo, setup_threads):
-    return Opts(PRECOND[precond], float(tau), int(flags), int(ainv_parts), int(ainv_halo), int(setup_threads))
+def _opts(precond, tau, flags, ainv_parts, ainv_halo, setup_threads, fsai_q=4):
+    return Opts(PRECOND[precond], float(tau), int(flags), int(ainv_parts), int(ainv_halo), int(setup_threads),
+                int(fsai_q))
 
 
 class Plan:
     """Host-only half of pcg_setup (validation, partition, anchor check, AINV, SELL packing)."""
 
     def __init__(self, cE, cN, mask, *, periodic=True, tau=0.1, precond="ainv", sigma=None,
-                 j_begin=None, j_end=None, rank=0, nranks=1, ainv_parts=0, ainv_halo=0, setup_threads=0):
+                 j_begin=None, j_end=None, rank=0, nranks=1, ainv_parts=0, ainv_halo=0, setup_threads=0, fsai_q=4):
         L = lib()
         cE, cN, mask, sigma = _host_inputs(cE, cN, mask, sigma)
         nj, ni = mask.shape
@@ -152,7 +154,7 @@ class Plan:
         co = Coeffs(_ptr(cE), _ptr(cN), _ptr(sigma), _ptr(mask))
         g = Grid(ni, nj, 1 if periodic else 0, 0 if j_begin is None else j_begin, nj if j_end is None else j_end,
                  rank, nranks, None, 0, None)
-        o = _opts(precond, tau, 0, ainv_parts, ainv_halo, setup_threads)
+        o = _opts(precond, tau, 0, ainv_parts, ainv_halo, setup_threads, fsai_q)
         h = C.c_void_p()
         _check(L.pcg_plan_build(C.byref(co), C.byref(g), C.byref(o), C.byref(h)), None, "pcg_plan_build")
         self._h = h
@@ -187,7 +189,7 @@ class Solver:
 
     def __init__(self, cE, cN, mask, *, periodic=True, tau=0.1, precond="ainv", sigma=None,
                  group=None, device=None, stream=None, flags=0, ainv_parts=0, ainv_halo=0,
-                 setup_threads=0, comm_path=False):
+                 setup_threads=0, comm_path=False, fsai_q=4):
         import torch
         import torch.distributed as dist
         L = lib()
@@ -222,7 +224,7 @@ class Solver:
         co = Coeffs(_ptr(cE), _ptr(cN), _ptr(sigma), _ptr(mask))
         g = Grid(ni, nj, 1 if periodic else 0, self.j_begin, self.j_end, self.rank, self.nranks,
                  self._comm, self.device.index, self.stream.cuda_stream)
-        o = _opts(precond, tau, flags, ainv_parts, ainv_halo, setup_threads)
+        o = _opts(precond, tau, flags, ainv_parts, ainv_halo, setup_threads, fsai_q)
         h = C.c_void_p()
         _check(L.pcg_setup(C.byref(co), C.byref(g), C.byref(o), C.byref(h)), None, "pcg_setup")
         self._h = h

@@ -203,8 +203,10 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         return Status::err(PCG_ERR_ARG, "pcg_setup: need 0 <= j_begin < j_end <= nj");
     if (g->nranks == 1 && (g->j_begin != 0 || g->j_end != g->nj))
         return Status::err(PCG_ERR_ARG, "pcg_setup: a single rank must own rows [0, nj)");
-    if (o->precond < PCG_PRECOND_AINV || o->precond > PCG_PRECOND_NONE)
+    if (o->precond < PCG_PRECOND_AINV || o->precond > PCG_PRECOND_FSAI)
         return Status::err(PCG_ERR_ARG, "pcg_setup: unknown preconditioner");
+    if (o->precond == PCG_PRECOND_FSAI && (o->fsai_q < 0 || g->nranks > 1 || o->ainv_parts > 1))
+        return Status::err(PCG_ERR_ARG, "pcg_setup: FSAI needs fsai_q >= 0 and one rank (no ainv_parts)");
     if (o->precond == PCG_PRECOND_AINV && !(o->drop_tol >= 0.0))
         return Status::err(PCG_ERR_ARG, "pcg_setup: drop_tol must be >= 0 (inf allowed, NaN not)");
     if (o->ainv_parts < 0 || o->ainv_halo < 0) return Status::err(PCG_ERR_ARG, "pcg_setup: ainv_parts/ainv_halo < 0");
@@ -230,6 +232,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     P.halo = 1;
     if (const char* e = getenv("PCG_HALO_ROWS")) P.halo = std::max(1, atoi(e));   // layout test hook
     P.precond = o->precond;
+    P.fsai_q = o->fsai_q;
     P.tau = o->drop_tol;
     P.flags = o->flags;
     P.has_sigma = c->sigma != nullptr;
@@ -293,7 +296,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     P.n_owned = 0;
     for (int64_t k = (int64_t)P.jb * ni; k < (int64_t)P.je * ni; ++k) P.n_owned += c->mask[k] ? 1 : 0;
 
-    if (P.precond != PCG_PRECOND_AINV) {
+    if (!P.factored()) {
         build_coeff_arrays();
         P.setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         P.zcolptr.assign(P.n_owned + 1, 0);
@@ -335,7 +338,10 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             blocks.push_back(b);
         }
     }
-    {
+    if (P.precond == PCG_PRECOND_FSAI) {            // one block: the banded FSAI of T (NEXT-1)
+        blocks.assign(1, AinvBlock());
+        fsai_block(ni, nj, P.periodic, c->cE, c->cN, c->mask, P.fsai_q, diag_of, blocks[0]);
+    } else {
         int nthreads = o->setup_threads > 0 ? o->setup_threads : (int)std::max(1u, std::thread::hardware_concurrency());
         nthreads = std::min<int>(nthreads, (int)blocks.size());
         std::vector<std::thread> pool;
@@ -413,13 +419,13 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
                 int64_t gr = b.row_g[e];
                 P.zrow.push_back(unk[gr - (int64_t)rlo * ni]);
                 P.zhat.push_back(b.zhat[e]);
-                double s = 1.0 / std::sqrt(diag_of(gr));
+                double s = P.precond == PCG_PRECOND_FSAI ? 1.0 : 1.0 / std::sqrt(diag_of(gr));   // FSAI: no Jacobi scale
                 ent_z.push_back(s * b.zhat[e]);
                 ent_row_arr.push_back(arr_of(gr));
             }
             P.zcolptr.push_back((int64_t)P.zrow.size());
             P.pivots.push_back(b.piv[q]);
-            P.scale.push_back(1.0 / std::sqrt(diag_of(b.col_g[q])));
+            P.scale.push_back(P.precond == PCG_PRECOND_FSAI ? 1.0 : 1.0 / std::sqrt(diag_of(b.col_g[q])));
             colarr.push_back(arr_of(b.col_g[q]));
             P.piv[colarr.back()] = b.piv[q];
             P.nnz_off += (b.colptr[q + 1] - b.colptr[q]) - 1;

@@ -171,7 +171,7 @@ struct Step {
 
 std::vector<Step> prologue_steps(const pcg_ctx* c) {
     std::vector<Step> s;
-    const bool multi = c->multi, ainv = c->plan.precond == PCG_PRECOND_AINV;
+    const bool multi = c->multi, ainv = c->plan.factored();
     const bool none = c->plan.precond == PCG_PRECOND_NONE;
     s.push_back({Ex::None, [](pcg_ctx* x) { launch_prep(x->A, x->st); }});
     if (multi) s.push_back({Ex::HaloX, nullptr});
@@ -198,7 +198,7 @@ std::vector<Step> prologue_steps(const pcg_ctx* c) {
 
 std::vector<Step> iteration_steps(const pcg_ctx* c, int par) {
     std::vector<Step> s;
-    const bool multi = c->multi, ainv = c->plan.precond == PCG_PRECOND_AINV;
+    const bool multi = c->multi, ainv = c->plan.factored();
     const bool none = c->plan.precond == PCG_PRECOND_NONE;
     const bool hx = multi && ainv && c->plan.halo_w > 0;
     s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k1(x->A, par, x->st); }});
@@ -513,7 +513,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     if (Status s = upload(c, c->cN, P.cN); !s) return s;
     if (P.has_sigma) { if (Status s = upload(c, c->sigma, P.sigma); !s) return s; }
     if (P.precond == PCG_PRECOND_JACOBI) { if (Status s = upload(c, c->diag, P.diag); !s) return s; }
-    if (P.precond == PCG_PRECOND_AINV) {
+    if (P.factored()) {
         if (Status s = upload(c, c->piv, P.piv); !s) return s;
         if (Status s = upload(c, c->zt_val, P.ZT.val); !s) return s;
         if (Status s = upload(c, c->zt_col, P.ZT.col); !s) return s;
@@ -564,7 +564,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         // (default on for K2 and K3: 97.1 -> 95.8 us/iteration at ORCA025; PCG_SCHED=0 disables)
         const char* se = getenv("PCG_SCHED");
         const int smask = se ? atoi(se) : 3;
-        if (P.precond == PCG_PRECOND_AINV && smask != 0) {
+        if (P.factored() && smask != 0) {
             const int64_t Uall = (int64_t)P.nloc * A.nbx;
             double frac = 0.8;                              // share of units scheduled statically
             if (const char* fe = getenv("PCG_SCHED_FRAC")) frac = std::max(0.0, std::min(1.0, atof(fe)));
@@ -635,11 +635,11 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     A.gath = c->gath; A.sc = c->sc;
     A.multi = c->multi ? 1 : 0;
     A.use_cond = 0;
-    A.precond = (int32_t)P.precond;
+    A.precond = P.factored() ? 0 : (int32_t)P.precond;   // kernels: 0 = factored Z D^-1 Z^T (AINV, FSAI)
     // algorithmic bytes per launch: N_o ocean points, z off-diagonals per column
     const double No = (double)P.n_owned, z = No > 0 ? (double)P.nnz_off / No : 0.0;
     c->bytes_k[0] = 64.0 * No;
-    if (P.precond == PCG_PRECOND_AINV) { c->bytes_k[1] = (48.0 + 12.0 * z) * No; c->bytes_k[2] = (32.0 + 12.0 * z) * No; }
+    if (P.factored()) { c->bytes_k[1] = (48.0 + 12.0 * z) * No; c->bytes_k[2] = (32.0 + 12.0 * z) * No; }
     else { c->bytes_k[1] = 40.0 * No; c->bytes_k[2] = 0.0; }
     CU(cudaGetLastError());
     if (Status s = ensure_hist(c, 1023); !s) return s;
@@ -763,7 +763,7 @@ pcg_status pcg_apply_preconditioner(pcg_ctx* c, const double* r, double* sout) {
         CU(cudaMemcpy2DAsync(c->r[1] + P.hoff(), dp, r, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
         KArgs A = c->A;
         A.use_cond = 0;
-        if (P.precond == PCG_PRECOND_AINV) { launch_k2_ainv(A, 1, 1, c->st); launch_k3_ainv(A, 1, 1, c->st); }
+        if (P.factored()) { launch_k2_ainv(A, 1, 1, c->st); launch_k3_ainv(A, 1, 1, c->st); }
         else launch_k2_diag(A, 1, 1, P.precond == PCG_PRECOND_NONE, c->st);
         CU(cudaGetLastError());
         CU(cudaMemcpy2DAsync(sout, sp, c->s + P.hoff(), dp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
@@ -892,7 +892,7 @@ pcg_status pcg_kernel_times(pcg_ctx* c, int32_t n_iter, double* ms_out, double* 
         }
         std::vector<cudaEvent_t> ev(4 * n_iter);
         for (auto& e : ev) CU(cudaEventCreate(&e));
-        const bool ainv = c->plan.precond == PCG_PRECOND_AINV;
+        const bool ainv = c->plan.factored();
         for (int m = 0; m < n_iter; ++m) {
             const int par = m & 1;
             cudaEventRecord(ev[4 * m + 0], c->st);

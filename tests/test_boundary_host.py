@@ -108,3 +108,61 @@ def test_sell_padding_is_small():
     pl = pcg.Plan(p.cE, p.cN, p.mask, tau=0.1 + 1e-9)
     nnz = pl.nnz
     assert 1.0 < pl.sell_z / nnz < 1.35 and 1.0 < pl.sell_zt / nnz < 1.35
+
+
+# ---------------------------------------------------------------- NEXT-1: the paper's FSAI
+def _fsai_equal(p, q):
+    A = oracle.assemble(p)
+    M = oracle.fsai(A, q)
+    pl = pcg.Plan(p.cE, p.cN, p.mask, periodic=p.periodic, sigma=p.sigma, precond="fsai", fsai_q=q)
+    cp, r, z, pv, sc = pl.export_zhat()
+    assert np.array_equal(cp, M.colptr) and np.array_equal(r, M.row)
+    assert np.array_equal(z, M.zhat) and np.array_equal(pv, M.pivots) and np.array_equal(sc, M.scale)
+    return A, M
+
+
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3"])
+@pytest.mark.parametrize("q", [0, 1, 4, 16])
+def test_host_fsai_bitwise_equals_oracle_configs(name, q):
+    """The library's banded FSAI of T (csrc/fsai.cpp) equals the oracle's (oracle/fsai.c) bit
+    for bit: factor, pivots u_kk^2, unit scale (reading R25)."""
+    _fsai_equal(synth.config(name), q)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("periodic", [True, False])
+def test_host_fsai_bitwise_literal_band(seed, periodic):
+    """Land-heavy random grids: consecutive unknowns are also periodic-wrap or N-S neighbours
+    here (T = band(A, 1) taken literally), and sigma > 0 enters the diagonal."""
+    p = synth.random_grid(7, 9, seed, land_frac=0.6, periodic=periodic, sigma=True)
+    A, M = _fsai_equal(p, 6)
+    gi = A.grid_index
+    D = A.dense()
+    # the factor's couplings are exactly A's entries between consecutive unknowns
+    sup = np.array([D[k, k + 1] for k in range(A.n - 1)])
+    linked = np.array([(M.row[M.colptr[k + 1]:M.colptr[k + 2]] == k).any() for k in range(A.n - 1)])
+    assert np.array_equal(linked, sup != 0)
+
+
+def test_fsai_setup_errors():
+    p = synth.config("cfg1")
+    with pytest.raises(pcg.PcgError):
+        pcg.Plan(p.cE, p.cN, p.mask, precond="fsai", fsai_q=-1)
+    with pytest.raises(pcg.PcgError):
+        pcg.Plan(p.cE, p.cN, p.mask, precond="fsai", fsai_q=4, j_begin=0, j_end=16, rank=0, nranks=2)
+
+
+def test_host_fsai_wrap_coupling():
+    """A row whose only ocean points are i = 0 and i = ni-1 on a periodic grid: the two
+    consecutive unknowns are coupled through the wrap face, which T = band(A, 1) keeps."""
+    ni, nj = 6, 4
+    rng = np.random.default_rng(7)
+    mask = np.zeros((nj, ni), dtype=np.uint8)
+    mask[1, 0] = mask[1, ni - 1] = 1
+    mask[2, 1:4] = 1
+    cE = rng.uniform(0.5, 2.0, (nj, ni)); cN = rng.uniform(0.5, 2.0, (nj, ni)); cN[nj - 1] = 0.0
+    p = synth.Problem("wrap", ni, nj, cE, cN, mask, True, None)
+    A, M = _fsai_equal(p, 3)
+    D = A.dense()
+    assert D[0, 1] == -cE[1, ni - 1]                       # unknowns 0, 1 = (0,1), (5,1)
+    assert M.row[M.colptr[1]] == 0 and M.zhat[M.colptr[1]] != 0.0

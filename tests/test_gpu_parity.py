@@ -284,3 +284,51 @@ def test_local_ranks_one_rank_equals_single():
     x1, k1, h1, _ = R.solve(b, tol=1e-10, maxit=A.n)
     assert k1 == k0 and np.array_equal(h1, h0) and torch.equal(x1, x0)
     R.close()
+
+
+# ------------------------------------------------ NEXT-1: the paper's banded FSAI of T (R25)
+def _fsai_pair(p, q):
+    A = oracle.assemble(p)
+    M = oracle.fsai(A, q)
+    S = pcg.Solver(p.cE, p.cN, p.mask, periodic=p.periodic, precond="fsai", fsai_q=q, sigma=p.sigma)
+    return A, M, S
+
+
+@pytest.mark.parametrize("q", [1, 4, 16])
+def test_fsai_preconditioner_bitwise(q):
+    p = synth.config("cfg2")
+    A, M, S = _fsai_pair(p, q)
+    r = A.from_grid(synth.xstar(p, 7))
+    s = host(S.apply_preconditioner(dev(A.to_grid(r))))
+    assert np.array_equal(s, A.to_grid(M.apply_canonical(r)))
+    S.close()
+
+
+@pytest.mark.parametrize("name,q", [("cfg1", 4), ("cfg2", 4), ("cfg2", 16), ("cfg3", 4)])
+def test_fsai_solve_bitwise_canonical(name, q):
+    """The paper's preconditioner through the factored device path: residual history,
+    iteration count, x and the true residual bitwise equal to the oracle's canonical PCG."""
+    p = synth.config(name)
+    A, M, S = _fsai_pair(p, q)
+    b = rhs(A, p)
+    ref = oracle.pcg(A, b, "ainv", M, 1e-10, maxit=A.n, mode="canonical", pitch=S.pitch, block=S.block)
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
+    assert k == ref.iterations
+    assert np.array_equal(hist, ref.hist)
+    assert np.array_equal(host(xg), A.to_grid(ref.x))
+    assert rep["true_rel_residual"] == ref.true_rel_residual
+    S.close()
+
+
+def test_fsai_solve_vs_plain_oracle():
+    """Plain-order bar at tol 1e-12: iterations within max(2, 1 %), x within 1e-9."""
+    p = synth.config("cfg2")
+    A, M, S = _fsai_pair(p, 4)
+    b = rhs(A, p)
+    ref = oracle.pcg(A, b, "ainv", M, 1e-12, maxit=A.n)
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-12, maxit=A.n)
+    x = A.from_grid(host(xg))
+    assert abs(k - ref.iterations) <= max(2, 0.01 * ref.iterations)
+    assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) <= 1e-9
+    assert rep["true_rel_residual"] <= 1e-12 * 1.5
+    S.close()
