@@ -76,6 +76,11 @@ struct Plan {
     // per-element arrays, (nloc + 2) * pitch
     std::vector<double> cE, cN, sigma, diag, piv;
     Ell Z, ZT;                     // rows of Z (for s = Z t) and of Z^T (for t = Z^T r)
+    // FSAI (NEXT-1) DIA form when every chain link is an E-W neighbour pair: dia[m-1][e] =
+    // zhat between owned element e - m and e (the column k = e's entry at row k - m), m = 1..dia_q;
+    // 0 where the chain is shorter.  dia_q = 0: no DIA form (the ELL path applies the factor).
+    int32_t dia_q = 0;
+    std::vector<double> dia;
     // export (owned columns of Zhat, global unknown numbering)
     std::vector<int64_t> zcolptr, zrow;
     std::vector<double> zhat, pivots, scale;

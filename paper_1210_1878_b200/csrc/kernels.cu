@@ -721,6 +721,45 @@ __device__ __forceinline__ double ell_row(const EllDev& E, int64_t e, Gather gat
     return overflow_sum(E, e, acc, gat);
 }
 
+// ---- FSAI in DIA form (NEXT-1, A.dia_q > 0): the factor's entries are chains
+// along grid rows, dia[m-1][e] = zhat between owned elements e - m and e.  Same entries, same
+// ascending-column fma order as the ELL row (zero slots are skipped, exactly like absent
+// entries).  Q >= dia_q is the compile-time width: all coefficient loads, then all gathers,
+// then the fma chain, so a row costs one load latency and one gather latency.
+// Z^T row of element e (for K2): columns e-M .. e-1, then the unit diagonal.
+template <int Q, class Gather>
+__device__ __forceinline__ double dia_zt_row(const KArgs& A, const Unit& W, double xself, Gather gat) {
+    const int64_t e = W.a - A.hoff;
+    double z[Q], x[Q];
+#pragma unroll
+    for (int m = 0; m < Q; ++m)
+        z[m] = (m < A.dia_q && W.i > m) ? __ldg(A.dia + (int64_t)m * A.nel + e) : 0.0;
+#pragma unroll
+    for (int m = 0; m < Q; ++m) x[m] = z[m] != 0.0 ? gat(W.a - (m + 1)) : 0.0;
+    double acc = 0.0;
+#pragma unroll
+    for (int m = Q - 1; m >= 0; --m)
+        if (z[m] != 0.0) acc = __fma_rn(z[m], x[m], acc);
+    return __fma_rn(1.0, xself, acc);
+}
+// Z row of element e (for K3): the unit diagonal, then columns e+1 .. e+M (chain order).
+template <int Q>
+__device__ __forceinline__ double dia_z_row(const KArgs& A, const Unit& W, const double* __restrict__ t) {
+    const int64_t e = W.a - A.hoff;
+    double z[Q], x[Q];
+#pragma unroll
+    for (int m = 0; m < Q; ++m)
+        z[m] = (m < A.dia_q && W.i + m + 1 < A.ni) ? __ldg(A.dia + (int64_t)m * A.nel + e + m + 1) : 0.0;
+    const double xs = __ldg(t + W.a);
+#pragma unroll
+    for (int m = 0; m < Q; ++m) x[m] = z[m] != 0.0 ? __ldg(t + W.a + m + 1) : 0.0;
+    double acc = __fma_rn(1.0, xs, 0.0);
+#pragma unroll
+    for (int m = 0; m < Q; ++m)
+        if (z[m] != 0.0) acc = __fma_rn(z[m], x[m], acc);
+    return acc;
+}
+
 #ifndef PCG_MINB_K2
 #define PCG_MINB_K2 4            // register budgets: resident 256-thread blocks per SM ptxas targets
 #endif
@@ -781,6 +820,7 @@ __device__ __forceinline__ void k3_finish(const KArgs& A, int init) {
 // ---- K2 (AINV): r -= alpha q ; t = Dhat^-1 Z^T r ; (r, r) --------------------------------
 // r_new at a gathered point c is recomputed as fma(-alpha, q_c, r_old_c) (bitwise the value
 // its own thread stores), so no grid-wide barrier is needed between the update and the gather.
+template <int DQ>
 __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArgs A, const int par, const int init) {
     TL(1, 0);
     pdl_wait();
@@ -800,8 +840,10 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
         if (W.live) {
             const double rnew = __fma_rn(-alpha, q[W.a], ro[W.a]);
             const double pv = A.piv[W.a];
-            const double acc = ell_row(A.zt, W.a - A.hoff,
-                                       [&](int32_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); });
+            auto gat = [&](int64_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); };
+            double acc;
+            if constexpr (DQ > 0) acc = dia_zt_row<DQ>(A, W, rnew, gat);
+            else acc = ell_row(A.zt, W.a - A.hoff, gat);
             A.t[W.a] = __ddiv_rn(acc, pv);
             rn[W.a] = rnew;
             v = __dmul_rn(rnew, rnew);
@@ -830,6 +872,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
 }
 
 // ---- K3 (AINV): s = Z t ; (s, r) ; beta / history / flag -----------------------------------
+template <int DQ>
 __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArgs A, const int par, const int init) {
     TL(2, 0);
     pdl_wait();
@@ -843,7 +886,9 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
         double v = 0.0;
         if (W.live) {
             const double rv = rn[W.a];
-            const double acc = ell_row(A.z, W.a - A.hoff, [&](int32_t g) { return __ldg(t + g); });
+            double acc;
+            if constexpr (DQ > 0) acc = dia_z_row<DQ>(A, W, t);
+            else acc = ell_row(A.z, W.a - A.hoff, [&](int32_t g) { return __ldg(t + g); });
             A.s[W.a] = acc;
             v = __dmul_rn(acc, rv);
         }
@@ -1176,7 +1221,9 @@ __device__ __forceinline__ double k2_unit(const KArgs& A, const Unit& W, int par
     const double* __restrict__ q = A.q;
     const double rnew = __fma_rn(-alpha, q[W.a], ro[W.a]);
     const double pv = A.piv[W.a];
-    const double acc = ell_row(A.zt, W.a - A.hoff, [&](int32_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); });
+    auto gat = [&](int64_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); };
+    const double acc = A.dia_q > 8 ? dia_zt_row<16>(A, W, rnew, gat) : A.dia_q > 0 ? dia_zt_row<8>(A, W, rnew, gat)
+                                                                                   : ell_row(A.zt, W.a - A.hoff, gat);
     A.t[W.a] = __ddiv_rn(acc, pv);
     A.r[par ^ 1][W.a] = rnew;
     return __dmul_rn(rnew, rnew);
@@ -1186,7 +1233,8 @@ __device__ __forceinline__ double k3_unit(const KArgs& A, const Unit& W, int par
     if (!W.inrow) return 0.0;
     const double* __restrict__ t = A.t;
     const double rv = A.r[par ^ 1][W.a];
-    const double acc = ell_row(A.z, W.a - A.hoff, [&](int32_t g) { return __ldg(t + g); });
+    const double acc = A.dia_q > 8 ? dia_z_row<16>(A, W, t) : A.dia_q > 0 ? dia_z_row<8>(A, W, t)
+                                   : ell_row(A.z, W.a - A.hoff, [&](int32_t g) { return __ldg(t + g); });
     A.s[W.a] = acc;
     return __dmul_rn(acc, rv);
 }
@@ -1505,8 +1553,8 @@ void configure_kernels(KArgs& A, int sms) {
         const int64_t per = (S + A.g_k1 - 1) / A.g_k1;
         A.g_k1 = (int)((S + per - 1) / per);
     }
-    A.g_k2 = persistent_grid(k2_ainv_kernel, U, sms, 2048);
-    A.g_k3 = persistent_grid(k3_ainv_kernel, U, sms, 2048);
+    A.g_k2 = persistent_grid(k2_ainv_kernel<0>, U, sms, 2048);
+    A.g_k3 = persistent_grid(k3_ainv_kernel<0>, U, sms, 2048);
     A.g_kd = persistent_grid(k2_diag_kernel, U, sms, 4096);
     A.g_row = persistent_grid(init_residual_kernel, U, sms, 2048);
     // K1 form: 2 = row-segment units, static block stride, no barrier per unit (default: 94.7 ->
@@ -1540,8 +1588,14 @@ void configure_kernels(KArgs& A, int sms) {
     }
     allow_smem(k1_kernel<false>, k1_smem(A, A.g_k1));
     allow_smem(k1_kernel<true>, k1_smem(A, A.g_k1));
-    allow_smem(k2_ainv_kernel, row_smem(A, A.g_k2, 1));
-    allow_smem(k3_ainv_kernel, row_smem(A, A.g_k3, 1));
+    allow_smem(k2_ainv_kernel<0>, row_smem(A, A.g_k2, 1));
+    allow_smem(k3_ainv_kernel<0>, row_smem(A, A.g_k3, 1));
+    allow_smem(k2_ainv_kernel<4>, row_smem(A, A.g_k2, 1));
+    allow_smem(k3_ainv_kernel<4>, row_smem(A, A.g_k3, 1));
+    allow_smem(k2_ainv_kernel<8>, row_smem(A, A.g_k2, 1));
+    allow_smem(k3_ainv_kernel<8>, row_smem(A, A.g_k3, 1));
+    allow_smem(k2_ainv_kernel<16>, row_smem(A, A.g_k2, 1));
+    allow_smem(k3_ainv_kernel<16>, row_smem(A, A.g_k3, 1));
     allow_smem(k2_diag_kernel, row_smem(A, A.g_kd, 2));
     allow_smem(init_residual_kernel, row_smem(A, A.g_row, 1));
     allow_smem(true_residual_kernel, row_smem(A, A.g_row, 1));
@@ -1578,11 +1632,17 @@ void launch_k1(const KArgs& A, int par, cudaStream_t st) {
 }
 void launch_k2_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
     if (A.tma) launch_pdl(A, k2_tma_kernel, A.g_t2, kBlock + 32, tma_smem_bytes<3>(), st, A, par, init);
-    else launch_pdl(A, k2_ainv_kernel, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
+    else if (A.dia_q > 8) launch_pdl(A, k2_ainv_kernel<16>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
+    else if (A.dia_q > 4) launch_pdl(A, k2_ainv_kernel<8>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
+    else if (A.dia_q > 0) launch_pdl(A, k2_ainv_kernel<4>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
+    else launch_pdl(A, k2_ainv_kernel<0>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
 }
 void launch_k3_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
     if (A.tma) launch_pdl(A, k3_tma_kernel, A.g_t3, kBlock + 32, tma_smem_bytes<1>(), st, A, par, init);
-    else launch_pdl(A, k3_ainv_kernel, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
+    else if (A.dia_q > 8) launch_pdl(A, k3_ainv_kernel<16>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
+    else if (A.dia_q > 4) launch_pdl(A, k3_ainv_kernel<8>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
+    else if (A.dia_q > 0) launch_pdl(A, k3_ainv_kernel<4>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
+    else launch_pdl(A, k3_ainv_kernel<0>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
 }
 void launch_k2_diag(const KArgs& A, int par, int init, int none, cudaStream_t st) {
     launch_pdl(A, k2_diag_kernel, A.g_kd, kBlock, row_smem(A, A.g_kd, 2), st, A, par, init, none);

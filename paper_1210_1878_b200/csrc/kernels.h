@@ -48,7 +48,9 @@ struct KArgs {
     const int32_t* soff3;
     int32_t sched_max;                // longest list (shared memory per block)
     int64_t sched_u0;                 // units [sched_u0, U) come from the dynamic ticket
-    int32_t landskip;                 // K2/K3 (dynamic): land / padding lanes issue no memory traffic
+    int32_t landskip;
+    int32_t dia_q;                    // FSAI DIA form: diagonals per factor (0 = ELL path)
+    const double* dia;                // [dia_q][nel] chain coefficients (see internal.h Plan::dia)                 // K2/K3 (dynamic): land / padding lanes issue no memory traffic
     const uint32_t* ocean;            // [nloc][nbx][kWarps] ocean bit masks (bit l: column 32w + l)
     int32_t precond;                  // pcg_precond
     int64_t nel;                      // owned elements nloc * pitch

@@ -491,6 +491,26 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         }
         pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.halo, P.Z);
     }
+    // ---- FSAI DIA form: each owned column's entries at consecutive columns of the
+    // same grid row i-1, i-2, ... (no land, wrap or N-S link inside the chain) -> diagonals
+    if (P.precond == PCG_PRECOND_FSAI && P.fsai_q > 0) {
+        const int32_t q = P.fsai_q;
+        bool plain = true;
+        std::vector<double> dia((size_t)q * nown, 0.0);
+        for (size_t c0 = 0; c0 < colarr.size() && plain; ++c0) {
+            const int64_t ec = colarr[c0] - hoff;                        // owned element of column
+            const int64_t ne = P.zcolptr[c0 + 1] - P.zcolptr[c0] - 1;  // entries above the diagonal
+            for (int64_t m = 1; m <= ne; ++m) {
+                const int64_t e = P.zcolptr[c0 + 1] - 1 - m;             // entry at row k - m
+                if (ent_row_arr[e] != colarr[c0] - m || (colarr[c0] % pitch) < m) { plain = false; break; }
+                dia[(size_t)(m - 1) * nown + ec] = ent_z[e];
+            }
+        }
+        if (plain) {
+            P.dia_q = q;
+            P.dia = std::move(dia);
+        }
+    }
     P.setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return Status::ok();
 }

@@ -33,6 +33,7 @@ struct pcg_ctx {
     int64_t dev_bytes = 0;
     double *cE = nullptr, *cN = nullptr, *sigma = nullptr, *diag = nullptr, *piv = nullptr;
     uint32_t* ocean = nullptr;         // per (row, segment, warp) ocean bit masks
+    double* dia = nullptr;             // FSAI DIA diagonals
     int32_t *sched2 = nullptr, *soff2 = nullptr, *sched3 = nullptr, *soff3 = nullptr;   // static schedules
     double *x = nullptr, *b = nullptr, *q = nullptr, *t = nullptr, *s = nullptr, *r[2] = {}, *d[2] = {};
     double *partial[3] = {}, *gath = nullptr, *hist = nullptr;
@@ -515,6 +516,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     if (P.precond == PCG_PRECOND_JACOBI) { if (Status s = upload(c, c->diag, P.diag); !s) return s; }
     if (P.factored()) {
         if (Status s = upload(c, c->piv, P.piv); !s) return s;
+        if (P.dia_q > 0) { if (Status s = upload(c, c->dia, P.dia); !s) return s; }
         if (Status s = upload(c, c->zt_val, P.ZT.val); !s) return s;
         if (Status s = upload(c, c->zt_col, P.ZT.col); !s) return s;
         if (Status s = upload(c, c->zt_ooff, P.ZT.ovf.off); !s) return s;
@@ -635,7 +637,13 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     A.gath = c->gath; A.sc = c->sc;
     A.multi = c->multi ? 1 : 0;
     A.use_cond = 0;
-    A.precond = P.factored() ? 0 : (int32_t)P.precond;   // kernels: 0 = factored Z D^-1 Z^T (AINV, FSAI)
+    A.precond = P.factored() ? 0 : (int32_t)P.precond;
+    A.dia_q = 0;
+    A.dia = c->dia;
+    if (P.dia_q > 0) {                                  // PCG_FSAI_DIA=0 keeps the ELL path (tests)
+        const char* e = getenv("PCG_FSAI_DIA");
+        if (!(e && atoi(e) == 0) && P.dia_q <= 16) A.dia_q = P.dia_q;   // wider bands: ELL path
+    }   // kernels: 0 = factored Z D^-1 Z^T (AINV, FSAI)
     // algorithmic bytes per launch: N_o ocean points, z off-diagonals per column
     const double No = (double)P.n_owned, z = No > 0 ? (double)P.nnz_off / No : 0.0;
     c->bytes_k[0] = 64.0 * No;
@@ -648,6 +656,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     P.cE.clear(); P.cE.shrink_to_fit(); P.cN.clear(); P.cN.shrink_to_fit();
     P.sigma.clear(); P.sigma.shrink_to_fit(); P.diag.clear(); P.diag.shrink_to_fit();
     P.piv.clear(); P.piv.shrink_to_fit();
+    P.dia.clear(); P.dia.shrink_to_fit();
     P.Z = Ell(); P.ZT = Ell();
     P.zrow.clear(); P.zrow.shrink_to_fit(); P.zhat.clear(); P.zhat.shrink_to_fit();
     if (use_graph(c)) {
