@@ -647,7 +647,12 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     // algorithmic bytes per launch: N_o ocean points, z off-diagonals per column
     const double No = (double)P.n_owned, z = No > 0 ? (double)P.nnz_off / No : 0.0;
     c->bytes_k[0] = 64.0 * No;
-    if (P.factored()) { c->bytes_k[1] = (48.0 + 12.0 * z) * No; c->bytes_k[2] = (32.0 + 12.0 * z) * No; }
+    if (A.dia_q > 0) {                                  // FSAI DIA: q diagonals, no indices
+        c->bytes_k[1] = (8.0 * A.dia_q + 40.0) * No;
+        c->bytes_k[2] = (8.0 * A.dia_q + 16.0) * No;
+    } else if (P.factored()) {
+        c->bytes_k[1] = (48.0 + 12.0 * z) * No; c->bytes_k[2] = (32.0 + 12.0 * z) * No;
+    }
     else { c->bytes_k[1] = 40.0 * No; c->bytes_k[2] = 0.0; }
     CU(cudaGetLastError());
     if (Status s = ensure_hist(c, 1023); !s) return s;
