@@ -174,6 +174,7 @@ __device__ void fin_init(const KArgs& A, double rho0, double rr0) {
     }
     sc->rho = rho0;
     sc->beta = 0.0;
+    sc->rho_prev = INFINITY;                 // beta of the first iteration = rho / inf = +0 (d_old = 0)
     const double h = __ddiv_rn(__dsqrt_rn(rr0), sc->nb);
     A.hist[0] = h;
     const int act = (h > sc->tol) && (sc->maxit > 0);
@@ -210,7 +211,7 @@ __device__ void fin_iter(const KArgs& A, double rho_new, const FinPre& f) {
         stop(A, kStBreakdown);
         return;
     }
-    sc->beta = __ddiv_rn(rho_new, f.rho);
+    sc->rho_prev = f.rho;                    // beta = rho_new / rho is formed by K1 (same IEEE division)
     sc->rho = rho_new;
     const double h = f.h;
     if (k < A.hist_cap) A.hist[k] = h;
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
     extern __shared__ double ws[];
     __shared__ double wrow[kMaxRowsK1][kWarps];
     __shared__ long long s_next;
-    const double beta = A.sc->beta, alpha = A.sc->alpha;
+    const double beta = __ddiv_rn(A.sc->rho, A.sc->rho_prev), alpha = A.sc->alpha;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int32_t nby = (A.nloc + A.rpb - 1) / A.rpb;
     const int64_t S = (int64_t)nby * A.nbx;
@@ -615,7 +616,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1F) k1_flat_kernel(const KAr
             set_cond(A, 0);
         }
     }
-    const double beta = A.sc->beta, alpha = A.sc->alpha;
+    const double beta = __ddiv_rn(A.sc->rho, A.sc->rho_prev), alpha = A.sc->alpha;
     bool last;
     if (A.k1flat == 2) {
         // static block stride, no barrier per unit: warp sums in shared memory, trees at the end

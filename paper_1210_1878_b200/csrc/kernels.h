@@ -14,6 +14,7 @@ constexpr int kMaxRowsK1 = 16;     // rows per K1 block (register march), <= kMa
 struct DevScalars {
     double alpha, beta, rho, nb, tol, true_rel;
     double hpre;          // sqrt((r,r)) / nb of the current iteration, formed early by K3's block 0
+    double rho_prev;      // rho of the previous iteration: K1 forms beta = rho / rho_prev itself
     double red[4];        // global reductions: [0] (d,q)  [1] (s,r)  [2] (r,r)  [3] (b,b) / true (r,r)
     double loc[4];        // this rank's block-tree sums (multi-rank path)
     int32_t k, maxit, active, status, bzero, xpend, guard, pad_;
