@@ -112,6 +112,11 @@ typedef struct {
     int32_t setup_threads; /* host threads for the AINV build (0 = automatic) */
     int32_t fsai_q;        /* PCG_PRECOND_FSAI: upper bandwidth q >= 0 of Z~ (entries z_ij with
                               j > i + q dropped); ignored otherwise */
+    int32_t ainv_fill;     /* PCG_PRECOND_AINV: 0 = drop tolerance only (P_B1); m > 0 = also keep at
+                              most m entries per column of Zhat (the diagonal and the m-1 largest
+                              |z|, ties to the smaller row) after every update: the paper's P_B2
+                              (R26); use drop_tol = 0 for pure
+                              P_B2 */
 } pcg_opts;
 
 typedef struct {

@@ -69,6 +69,8 @@ def lib():
         L.orc_partition.argtypes = [I32, I32, vp, I32, vp]
         L.orc_ainv_build.argtypes = [P, D, I32, I32, I32, C.POINTER(P), C.POINTER(I64)]
         L.orc_ainv_build.restype = C.c_int
+        L.orc_ainv_build_fill.argtypes = [P, D, I32, I32, I32, I32, C.POINTER(P), C.POINTER(I64)]
+        L.orc_ainv_build_fill.restype = C.c_int
         L.orc_fsai_build.argtypes = [P, I32, C.POINTER(P), C.POINTER(I64)]
         L.orc_fsai_build.restype = C.c_int
         L.orc_ainv_free.argtypes = [P]
@@ -240,12 +242,14 @@ class _AinvHandle:
             self._h = None
 
 
-def ainv(A: Assembled, tau: float, method: str = "sparse", parts: int = 1, halo: int = 0) -> Ainv:
+def ainv(A: Assembled, tau: float, method: str = "sparse", parts: int = 1, halo: int = 0, fill: int = 0) -> Ainv:
+    """AINV(A, tau) (P_B1); fill = m > 0 adds P_B2's count rule (m entries per column incl. the
+    diagonal, reading R26)."""
     L = lib()
     h = C.c_void_p()
     fail = C.c_int64(-1)
-    rc = L.orc_ainv_build(A._h, float(tau), 1 if method == "dense" else 0, int(parts), int(halo),
-                    C.byref(h), C.byref(fail))
+    rc = L.orc_ainv_build_fill(A._h, float(tau), int(fill), 1 if method == "dense" else 0, int(parts), int(halo),
+                               C.byref(h), C.byref(fail))
     if rc != 0:
         e = OracleError(rc, f"ainv failed at column {fail.value}")
         e.index = fail.value

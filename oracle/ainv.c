@@ -93,7 +93,27 @@ static int cmp_i64(const void* a, const void* b) {
 
 /* Sparse left-looking AINV on a local matrix.  Output: CSC Zhat (rows ascending), pivots.
  * Returns -1 on success or the failing column. */
-static int64_t ainv_sparse(const lcsr* A, double tau, cstore* Z, double* p) {
+/* P_B2 count rule ("predetermined the number of non-zeros elements on each its
+ * row"; reading R26): after each update (and the tau drop), keep the
+ * diagonal and the fill-1 largest-magnitude off-diagonal entries of the column, ties to the
+ * smaller row index; fill = 0 means no limit (P_B1). */
+static const double* g_keep_w;
+static int cmp_keep(const void* x, const void* y) {
+    const int64_t a = *(const int64_t*)x, b = *(const int64_t*)y;
+    const double fa = fabs(g_keep_w[a]), fb = fabs(g_keep_w[b]);
+    if (fa > fb) return -1;
+    if (fa < fb) return 1;
+    return a < b ? -1 : (a > b);
+}
+/* cand[0..cnt) = present off-diagonal rows; returns how many to drop (they end the sorted list) */
+static int64_t keep_largest(int64_t* cand, int64_t cnt, const double* w, int32_t fill) {
+    if (fill <= 0 || cnt <= (int64_t)fill - 1) return 0;
+    g_keep_w = w;
+    qsort(cand, (size_t)cnt, sizeof(int64_t), cmp_keep);
+    return cnt - ((int64_t)fill - 1);
+}
+
+static int64_t ainv_sparse(const lcsr* A, double tau, int32_t fill, cstore* Z, double* p) {
     int64_t n = A->n;
     double* w = (double*)calloc(n ? n : 1, sizeof(double));
     char* inz = (char*)calloc(n ? n : 1, 1);
@@ -148,6 +168,14 @@ static int64_t ainv_sparse(const lcsr* A, double tau, cstore* Z, double* p) {
                 int64_t k = touched[t];
                 if (k != j && fabs(w[k]) < tau) { inz[k] = 0; w[k] = 0.0; }
             }
+            if (fill > 0) {
+                int64_t cnt = 0;
+                if (nz > tcap) { tcap = nz; touched = (int64_t*)realloc(touched, sizeof(int64_t) * tcap); }
+                for (int64_t t = 0; t < nz; ++t)
+                    if (zlist[t] != j && inz[zlist[t]]) touched[cnt++] = zlist[t];
+                const int64_t ndrop = keep_largest(touched, cnt, w, fill);
+                for (int64_t t = cnt - ndrop; t < cnt; ++t) { inz[touched[t]] = 0; w[touched[t]] = 0.0; }
+            }
         }
         double pj = 0.0;
         for (int64_t e = A->rowptr[j]; e < A->rowptr[j + 1]; ++e) {
@@ -170,7 +198,7 @@ static int64_t ainv_sparse(const lcsr* A, double tau, cstore* Z, double* p) {
 
 /* Dense right-looking AINV (cross-check; n small): for i = 0..n-1: p_i = a^_i^T z_i;
  * for j > i: pi = a^_i^T z_j; skip if 0; z_j -= (pi/p_i) z_i; drop touched entries. */
-static int64_t ainv_dense(const lcsr* A, double tau, cstore* Z, double* p) {
+static int64_t ainv_dense(const lcsr* A, double tau, int32_t fill, cstore* Z, double* p) {
     int64_t n = A->n;
     double* Zc = (double*)calloc((size_t)n * n, sizeof(double));     /* column-major */
     char* pres = (char*)calloc((size_t)n * n, 1);
@@ -208,6 +236,13 @@ static int64_t ainv_dense(const lcsr* A, double tau, cstore* Z, double* p) {
                 int64_t k = touched[t];
                 if (k != j && fabs(zj[k]) < tau) { pj_[k] = 0; zj[k] = 0.0; }
             }
+            if (fill > 0) {
+                int64_t cnt = 0;
+                for (int64_t k = 0; k < n; ++k)
+                    if (k != j && pj_[k]) touched[cnt++] = k;
+                const int64_t ndrop = keep_largest(touched, cnt, zj, fill);
+                for (int64_t t = cnt - ndrop; t < cnt; ++t) { pj_[touched[t]] = 0; zj[touched[t]] = 0.0; }
+            }
         }
     }
     cs_init(Z, n);
@@ -222,9 +257,14 @@ static int64_t ainv_dense(const lcsr* A, double tau, cstore* Z, double* p) {
 
 int orc_ainv_build(const orc_problem* P, double tau, int32_t method, int32_t parts, int32_t halo,
              orc_ainv** out, int64_t* failed_col) {
+    return orc_ainv_build_fill(P, tau, 0, method, parts, halo, out, failed_col);
+}
+
+int orc_ainv_build_fill(const orc_problem* P, double tau, int32_t keep, int32_t method, int32_t parts, int32_t halo,
+             orc_ainv** out, int64_t* failed_col) {
     *out = NULL;
     if (failed_col) *failed_col = -1;
-    if (!(tau >= 0.0) || parts < 1 || halo < 0 || parts > P->nj) return ORC_ERR_ARG;
+    if (!(tau >= 0.0) || parts < 1 || halo < 0 || parts > P->nj || keep < 0) return ORC_ERR_ARG;
     int64_t n = P->n;
     if (method == 1 && n > 4000) return ORC_ERR_ARG;
     for (int64_t q = 0; q < n; ++q)
@@ -278,7 +318,7 @@ int orc_ainv_build(const orc_problem* P, double tau, int32_t method, int32_t par
         lcsr L = {m, lrp, lc, la};
         cstore Zl;
         double* pl = (double*)malloc(sizeof(double) * (m ? m : 1));
-        int64_t f = method == 1 ? ainv_dense(&L, tau, &Zl, pl) : ainv_sparse(&L, tau, &Zl, pl);
+        int64_t f = method == 1 ? ainv_dense(&L, tau, keep, &Zl, pl) : ainv_sparse(&L, tau, keep, &Zl, pl);
         if (f >= 0) {
             rc = ORC_ERR_NOT_SPD;
             if (failed_col) *failed_col = f + lo;

@@ -62,6 +62,11 @@ void orc_partition(int32_t nj, int32_t ni, const uint8_t* mask, int32_t parts, i
  * parts >= 1 row blocks, halo w >= 0 southern rows (parts == 1: global AINV). */
 int  orc_ainv_build(const orc_problem*, double tau, int32_t method, int32_t parts, int32_t halo,
               orc_ainv** out, int64_t* failed_col);
+/* P_B2 (reading R26): as orc_ainv_build, and after every update keep
+ * only the diagonal plus the fill-1 largest-magnitude entries of the column (ties: smaller row);
+ * fill = 0 = no limit (orc_ainv_build).  Use tau = 0 for the pure fixed-fill preconditioner. */
+int  orc_ainv_build_fill(const orc_problem*, double tau, int32_t fill, int32_t method, int32_t parts,
+                         int32_t halo, orc_ainv** out, int64_t* failed_col);
 void orc_ainv_free(orc_ainv*);
 int64_t orc_ainv_nnz(const orc_ainv*);          /* nnz of Zhat incl. unit diagonal */
 /* Zhat as CSC (columns j, rows k ascending), pivots p (=Dhat), scale s = 1/sqrt(A_pp),

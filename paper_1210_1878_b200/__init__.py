@@ -50,7 +50,7 @@ class Coeffs(C.Structure):
 class Opts(C.Structure):
     _fields_ = [("precond", C.c_int32), ("drop_tol", C.c_double), ("flags", C.c_int32),
                 ("ainv_parts", C.c_int32), ("ainv_halo", C.c_int32), ("setup_threads", C.c_int32),
-                ("fsai_q", C.c_int32)]
+                ("fsai_q", C.c_int32), ("ainv_fill", C.c_int32)]
 
 
 class Report(C.Structure):
@@ -137,16 +137,17 @@ def _host_inputs(cE, cN, mask, sigma):
     return cE, cN, mask, sigma
 
 
-def _opts(precond, tau, flags, ainv_parts, ainv_halo, setup_threads, fsai_q=4):
+def _opts(precond, tau, flags, ainv_parts, ainv_halo, setup_threads, fsai_q=4, ainv_fill=0):
     return Opts(PRECOND[precond], float(tau), int(flags), int(ainv_parts), int(ainv_halo), int(setup_threads),
-                int(fsai_q))
+                int(fsai_q), int(ainv_fill))
 
 
 class Plan:
     """Host-only half of pcg_setup (validation, partition, anchor check, AINV, SELL packing)."""
 
     def __init__(self, cE, cN, mask, *, periodic=True, tau=0.1, precond="ainv", sigma=None,
-                 j_begin=None, j_end=None, rank=0, nranks=1, ainv_parts=0, ainv_halo=0, setup_threads=0, fsai_q=4):
+                 j_begin=None, j_end=None, rank=0, nranks=1, ainv_parts=0, ainv_halo=0, setup_threads=0, fsai_q=4,
+                 ainv_fill=0):
         L = lib()
         cE, cN, mask, sigma = _host_inputs(cE, cN, mask, sigma)
         nj, ni = mask.shape
@@ -154,7 +155,7 @@ class Plan:
         co = Coeffs(_ptr(cE), _ptr(cN), _ptr(sigma), _ptr(mask))
         g = Grid(ni, nj, 1 if periodic else 0, 0 if j_begin is None else j_begin, nj if j_end is None else j_end,
                  rank, nranks, None, 0, None)
-        o = _opts(precond, tau, 0, ainv_parts, ainv_halo, setup_threads, fsai_q)
+        o = _opts(precond, tau, 0, ainv_parts, ainv_halo, setup_threads, fsai_q, ainv_fill)
         h = C.c_void_p()
         _check(L.pcg_plan_build(C.byref(co), C.byref(g), C.byref(o), C.byref(h)), None, "pcg_plan_build")
         self._h = h
@@ -189,7 +190,7 @@ class Solver:
 
     def __init__(self, cE, cN, mask, *, periodic=True, tau=0.1, precond="ainv", sigma=None,
                  group=None, device=None, stream=None, flags=0, ainv_parts=0, ainv_halo=0,
-                 setup_threads=0, comm_path=False, fsai_q=4):
+                 setup_threads=0, comm_path=False, fsai_q=4, ainv_fill=0):
         import torch
         import torch.distributed as dist
         L = lib()
@@ -224,7 +225,7 @@ class Solver:
         co = Coeffs(_ptr(cE), _ptr(cN), _ptr(sigma), _ptr(mask))
         g = Grid(ni, nj, 1 if periodic else 0, self.j_begin, self.j_end, self.rank, self.nranks,
                  self._comm, self.device.index, self.stream.cuda_stream)
-        o = _opts(precond, tau, flags, ainv_parts, ainv_halo, setup_threads, fsai_q)
+        o = _opts(precond, tau, flags, ainv_parts, ainv_halo, setup_threads, fsai_q, ainv_fill)
         h = C.c_void_p()
         _check(L.pcg_setup(C.byref(co), C.byref(g), C.byref(o), C.byref(h)), None, "pcg_setup")
         self._h = h
@@ -315,7 +316,7 @@ class LocalRanks:
     multi-rank device code path (halo rows, rank sums, rank-ordered tree) without n GPUs."""
 
     def __init__(self, cE, cN, mask, nranks, *, periodic=True, tau=0.1, precond="ainv", sigma=None, device=None,
-                 setup_threads=0, ainv_halo=0):
+                 setup_threads=0, ainv_halo=0, ainv_fill=0):
         import torch
         L = lib()
         cE, cN, mask, sigma = _host_inputs(cE, cN, mask, sigma)
@@ -329,7 +330,7 @@ class LocalRanks:
         for r in range(self.n):
             g = Grid(ni, nj, 1 if periodic else 0, int(self.rb[r]), int(self.rb[r + 1]), r, self.n, None, dev,
                      stream.cuda_stream)
-            o = _opts(precond, tau, FLAG_LOCAL_RANKS, 0, int(ainv_halo), setup_threads)
+            o = _opts(precond, tau, FLAG_LOCAL_RANKS, 0, int(ainv_halo), setup_threads, 4, ainv_fill)
             h = C.c_void_p()
             rc = L.pcg_setup(C.byref(co), C.byref(g), C.byref(o), C.byref(h))
             if rc != 0:

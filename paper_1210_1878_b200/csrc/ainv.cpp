@@ -46,7 +46,7 @@ inline void faces(int32_t ni, int32_t nj, int32_t periodic, const double* cE, co
 }  // namespace
 
 void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, const double* cN,
-                const double* sigma, const uint8_t* mask, double tau, AinvBlock& blk) {
+                const double* sigma, const uint8_t* mask, double tau, int32_t fill, AinvBlock& blk) {
     const int32_t r0 = blk.row_lo, r1 = blk.row_hi;
     BlockMatrix M;
     // local numbering of the ocean points of rows [r0, r1), natural order
@@ -143,6 +143,20 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
             }
             for (int32_t k : touched)
                 if (k != j && std::fabs(w[k]) < tau) { live[k] = 0; w[k] = 0.0; }
+            if (fill > 0) {
+                // P_B2 (reading R26): keep the diagonal and the fill-1 largest |z|, ties to the
+                // smaller index
+                touched.clear();
+                for (int32_t k : members)
+                    if (k != j && live[k]) touched.push_back(k);
+                if ((int64_t)touched.size() > (int64_t)fill - 1) {
+                    std::sort(touched.begin(), touched.end(), [&](int32_t a, int32_t b) {
+                        const double fa = std::fabs(w[a]), fb = std::fabs(w[b]);
+                        return fa > fb || (fa == fb && a < b);
+                    });
+                    for (size_t t = (size_t)fill - 1; t < touched.size(); ++t) { live[touched[t]] = 0; w[touched[t]] = 0.0; }
+                }
+            }
         }
         double pj = 0.0;
         for (int32_t e = M.rp[j]; e < M.rp[j + 1]; ++e) {

@@ -67,6 +67,7 @@ struct Plan {
     int32_t halo_t_send = 0;       // ... t rows the southern neighbour needs from this rank
     pcg_precond precond = PCG_PRECOND_AINV;
     int32_t fsai_q = 4;
+    int32_t ainv_fill = 0;        // P_B2: entries kept per column of Zhat (0 = drop tolerance only)
     // AINV and FSAI share the factored form s = Z D^-1 Z^T r and every device path
     bool factored() const { return precond == PCG_PRECOND_AINV || precond == PCG_PRECOND_FSAI; }
     double tau = 0.1;
@@ -107,7 +108,7 @@ struct AinvBlock {
     int64_t fail_grid = -1;
 };
 void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, const double* cN,
-                const double* sigma, const uint8_t* mask, double tau, AinvBlock& blk);
+                const double* sigma, const uint8_t* mask, double tau, int32_t fill, AinvBlock& blk);
 // NEXT-1 banded FSAI of T = band(A, 1) over the whole grid, as one factored block (fsai.cpp)
 void fsai_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, const double* cN, const uint8_t* mask,
                 int32_t q, const std::function<double(int64_t)>& diag_of, AinvBlock& blk);

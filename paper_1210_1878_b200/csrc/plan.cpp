@@ -205,6 +205,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         return Status::err(PCG_ERR_ARG, "pcg_setup: a single rank must own rows [0, nj)");
     if (o->precond < PCG_PRECOND_AINV || o->precond > PCG_PRECOND_FSAI)
         return Status::err(PCG_ERR_ARG, "pcg_setup: unknown preconditioner");
+    if (o->ainv_fill < 0) return Status::err(PCG_ERR_ARG, "pcg_setup: ainv_fill < 0");
     if (o->precond == PCG_PRECOND_FSAI && (o->fsai_q < 0 || g->nranks > 1 || o->ainv_parts > 1))
         return Status::err(PCG_ERR_ARG, "pcg_setup: FSAI needs fsai_q >= 0 and one rank (no ainv_parts)");
     if (o->precond == PCG_PRECOND_AINV && !(o->drop_tol >= 0.0))
@@ -233,6 +234,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     if (const char* e = getenv("PCG_HALO_ROWS")) P.halo = std::max(1, atoi(e));   // layout test hook
     P.precond = o->precond;
     P.fsai_q = o->fsai_q;
+    P.ainv_fill = o->ainv_fill;
     P.tau = o->drop_tol;
     P.flags = o->flags;
     P.has_sigma = c->sigma != nullptr;
@@ -348,7 +350,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         std::atomic_size_t next{0};
         auto work = [&]() {
             for (size_t k; (k = next.fetch_add(1)) < blocks.size();)
-                ainv_block(ni, nj, P.periodic, c->cE, c->cN, c->sigma, c->mask, P.tau, blocks[k]);
+                ainv_block(ni, nj, P.periodic, c->cE, c->cN, c->sigma, c->mask, P.tau, P.ainv_fill, blocks[k]);
         };
         for (int t = 1; t < nthreads; ++t) pool.emplace_back(work);
         work();

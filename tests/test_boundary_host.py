@@ -166,3 +166,27 @@ def test_host_fsai_wrap_coupling():
     D = A.dense()
     assert D[0, 1] == -cE[1, ni - 1]                       # unknowns 0, 1 = (0,1), (5,1)
     assert M.row[M.colptr[1]] == 0 and M.zhat[M.colptr[1]] != 0.0
+
+
+# ---------------------------------------------------------------- NEXT-4: P_B2 (fixed fill)
+def _pb2_equal(p, tau, fill, **kw):
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, tau, fill=fill, parts=max(1, kw.get("ainv_parts", 0) or 1), halo=kw.get("ainv_halo", 0))
+    pl = pcg.Plan(p.cE, p.cN, p.mask, periodic=p.periodic, sigma=p.sigma, tau=tau, ainv_fill=fill, **kw)
+    cp, r, z, pv, sc = pl.export_zhat()
+    assert np.array_equal(cp, M.colptr) and np.array_equal(r, M.row)
+    assert np.array_equal(z, M.zhat) and np.array_equal(pv, M.pivots) and np.array_equal(sc, M.scale)
+
+
+@pytest.mark.parametrize("name,fill", [("cfg1", 2), ("cfg1", 4), ("cfg2", 3), ("cfg2", 6), ("cfg3", 5)])
+def test_host_pb2_bitwise_equals_oracle(name, fill):
+    """The library's fixed-fill AINV (csrc/ainv.cpp) equals the oracle's bit for bit, incl. the
+    tie rule on cfg1's constant couplings."""
+    _pb2_equal(synth.config(name), 0.0, fill)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_host_pb2_with_tau_and_partitions(seed):
+    p = synth.random_grid(17, 14, seed, sigma=True, periodic=seed != 2)
+    _pb2_equal(p, 0.02 + 1e-9, 4)
+    _pb2_equal(p, 0.0, 3, ainv_parts=3, ainv_halo=2)

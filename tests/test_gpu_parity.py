@@ -332,3 +332,19 @@ def test_fsai_solve_vs_plain_oracle():
     assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) <= 1e-9
     assert rep["true_rel_residual"] <= 1e-12 * 1.5
     S.close()
+
+
+# ------------------------------------------------------ NEXT-4: P_B2, fixed fill per column (R26)
+@pytest.mark.parametrize("name,fill", [("cfg2", 3), ("cfg2", 6), ("cfg3", 5)])
+def test_pb2_solve_bitwise_canonical(name, fill):
+    p = synth.config(name)
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, 0.0, fill=fill)
+    S = pcg.Solver(p.cE, p.cN, p.mask, periodic=p.periodic, tau=0.0, ainv_fill=fill)
+    b = rhs(A, p)
+    ref = oracle.pcg(A, b, "ainv", M, 1e-10, maxit=A.n, mode="canonical", pitch=S.pitch, block=S.block)
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
+    assert k == ref.iterations
+    assert np.array_equal(hist, ref.hist)
+    assert np.array_equal(host(xg), A.to_grid(ref.x))
+    S.close()

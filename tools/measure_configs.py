@@ -23,6 +23,7 @@ ap.add_argument("--configs", default="cfg1,cfg2,cfg3,cfg4")
 ap.add_argument("--taus", default="0.1")
 ap.add_argument("--jacobi", action="store_true")
 ap.add_argument("--fsai", default="", help="comma list of FSAI bandwidths q (the paper's preconditioner)")
+ap.add_argument("--fill", default="", help="comma list of P_B2 fills m (AINV with tau = 0, m entries per column)")
 ap.add_argument("--tol", type=float, default=None)
 ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
@@ -35,11 +36,12 @@ for name in a.configs.split(","):
     gen_s = time.perf_counter() - t0
     xs = torch.from_numpy(synth.xstar(p)).cuda()
     runs = [("ainv", float(t)) for t in a.taus.split(",") if t] + ([("jacobi", 0.0)] if a.jacobi else []) + \
-        [("fsai", float(q)) for q in a.fsai.split(",") if q]
+        [("fsai", float(q)) for q in a.fsai.split(",") if q] + [("pb2", float(f)) for f in a.fill.split(",") if f]
     for pc, tau in runs:
         t0 = time.perf_counter()
-        S = pcg.Solver(p.cE, p.cN, p.mask, tau=tau if pc != "fsai" else 0.1, precond=pc,
-                       fsai_q=int(tau) if pc == "fsai" else 4)
+        S = pcg.Solver(p.cE, p.cN, p.mask, tau=0.0 if pc == "pb2" else (tau if pc != "fsai" else 0.1),
+                       precond="ainv" if pc == "pb2" else pc, fsai_q=int(tau) if pc == "fsai" else 4,
+                       ainv_fill=int(tau) if pc == "pb2" else 0)
         setup_wall = time.perf_counter() - t0
         b = S.apply_operator(xs)
         tol = a.tol if a.tol is not None else TOL[name]
@@ -51,7 +53,7 @@ for name in a.configs.split(","):
         err = float(torch.linalg.norm(x - xs) / torch.linalg.norm(xs))
         bpi = rep["bytes_per_iter"]
         out = {"config": name, "grid": [p.ni, p.nj], "n_ocean": rep["n_ocean"], "precond": pc,
-               ("fsai_q" if pc == "fsai" else "tau"): (int(tau) if pc == "fsai" else tau), "tol": tol,
+               ({"fsai": "fsai_q", "pb2": "fill"}.get(pc, "tau")): (int(tau) if pc in ("fsai", "pb2") else tau), "tol": tol,
                "iterations": k, "converged": rep["converged"], "true_rel_residual": rep["true_rel_residual"],
                "err_vs_xstar": err, "time_to_solution_ms": best * 1e3, "iter_per_s": k / best,
                "us_per_iter": best / k * 1e6, "alg_bytes_per_iter_MB": bpi / 1e6,
