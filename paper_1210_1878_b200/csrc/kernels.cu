@@ -761,6 +761,26 @@ __device__ __forceinline__ double dia_z_row(const KArgs& A, const Unit& W, const
     return acc;
 }
 
+// ELL row with int16 slot offsets (DQ = -1 kernels): one 8-byte column load per element instead
+// of 16; the gathered array index is the element's own index plus the offset.  Same entries and
+// order as ell_row.
+template <class Gather>
+__device__ __forceinline__ double ell_row16(const EllDev& E, int64_t e, int64_t self, Gather gat) {
+    double z[kEll], x[kEll];
+    const uint2 cw = __ldg(reinterpret_cast<const uint2*>(E.col16) + e);
+    ld_nc_f64x4(E.val + e * kEll, z);
+    const int32_t s = (int32_t)self;
+    const int32_t c[kEll] = {s + (int32_t)(int16_t)(cw.x & 0xffffu), s + (int32_t)(int16_t)(cw.x >> 16),
+                             s + (int32_t)(int16_t)(cw.y & 0xffffu), s + (int32_t)(int16_t)(cw.y >> 16)};
+#pragma unroll
+    for (int m = 0; m < kEll; ++m) x[m] = gat(c[m]);
+    asm volatile("" : "+d"(x[0]), "+d"(x[1]), "+d"(x[2]), "+d"(x[3]));
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < kEll; ++m) acc = __fma_rn(z[m], x[m], acc);
+    return overflow_sum(E, e, acc, gat);
+}
+
 #ifndef PCG_MINB_K2
 #define PCG_MINB_K2 4            // register budgets: resident 256-thread blocks per SM ptxas targets
 #endif
@@ -844,6 +864,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
             auto gat = [&](int64_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); };
             double acc;
             if constexpr (DQ > 0) acc = dia_zt_row<DQ>(A, W, rnew, gat);
+            else if constexpr (DQ < 0) acc = ell_row16(A.zt, W.a - A.hoff, W.a, gat);
             else acc = ell_row(A.zt, W.a - A.hoff, gat);
             A.t[W.a] = __ddiv_rn(acc, pv);
             rn[W.a] = rnew;
@@ -889,6 +910,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
             const double rv = rn[W.a];
             double acc;
             if constexpr (DQ > 0) acc = dia_z_row<DQ>(A, W, t);
+            else if constexpr (DQ < 0) acc = ell_row16(A.z, W.a - A.hoff, W.a, [&](int32_t g) { return __ldg(t + g); });
             else acc = ell_row(A.z, W.a - A.hoff, [&](int32_t g) { return __ldg(t + g); });
             A.s[W.a] = acc;
             v = __dmul_rn(acc, rv);
@@ -1591,6 +1613,8 @@ void configure_kernels(KArgs& A, int sms) {
     allow_smem(k1_kernel<true>, k1_smem(A, A.g_k1));
     allow_smem(k2_ainv_kernel<0>, row_smem(A, A.g_k2, 1));
     allow_smem(k3_ainv_kernel<0>, row_smem(A, A.g_k3, 1));
+    allow_smem(k2_ainv_kernel<-1>, row_smem(A, A.g_k2, 1));
+    allow_smem(k3_ainv_kernel<-1>, row_smem(A, A.g_k3, 1));
     allow_smem(k2_ainv_kernel<4>, row_smem(A, A.g_k2, 1));
     allow_smem(k3_ainv_kernel<4>, row_smem(A, A.g_k3, 1));
     allow_smem(k2_ainv_kernel<8>, row_smem(A, A.g_k2, 1));
@@ -1636,6 +1660,7 @@ void launch_k2_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
     else if (A.dia_q > 8) launch_pdl(A, k2_ainv_kernel<16>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else if (A.dia_q > 4) launch_pdl(A, k2_ainv_kernel<8>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else if (A.dia_q > 0) launch_pdl(A, k2_ainv_kernel<4>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
+    else if (A.zt.col16) launch_pdl(A, k2_ainv_kernel<-1>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else launch_pdl(A, k2_ainv_kernel<0>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
 }
 void launch_k3_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
@@ -1643,6 +1668,7 @@ void launch_k3_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
     else if (A.dia_q > 8) launch_pdl(A, k3_ainv_kernel<16>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else if (A.dia_q > 4) launch_pdl(A, k3_ainv_kernel<8>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else if (A.dia_q > 0) launch_pdl(A, k3_ainv_kernel<4>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
+    else if (A.z.col16) launch_pdl(A, k3_ainv_kernel<-1>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else launch_pdl(A, k3_ainv_kernel<0>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
 }
 void launch_k2_diag(const KArgs& A, int par, int init, int none, cudaStream_t st) {

@@ -30,6 +30,7 @@ struct EllDev {
     const double* oval;
     const int32_t* ocol;
     int64_t n;
+    const int16_t* col16 = nullptr;   // kEll * n slot offsets from the element's own array index
 };
 
 struct KArgs {

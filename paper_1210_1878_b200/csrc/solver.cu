@@ -39,6 +39,7 @@ struct pcg_ctx {
     double *partial[3] = {}, *gath = nullptr, *hist = nullptr;
     double *zt_val = nullptr, *z_val = nullptr, *zt_oval = nullptr, *z_oval = nullptr;
     int32_t *zt_col = nullptr, *z_col = nullptr, *zt_ocol = nullptr, *z_ocol = nullptr;
+    int16_t *zt_c16 = nullptr, *z_c16 = nullptr;          // ELL slot offsets (when they all fit)
     int64_t *zt_ooff = nullptr, *z_ooff = nullptr;
     DevScalars* sc = nullptr;
     DevScalars* h_sc = nullptr;        // pinned
@@ -527,6 +528,22 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         if (Status s = upload(c, c->z_ooff, P.Z.ovf.off); !s) return s;
         if (Status s = upload(c, c->z_oval, P.Z.ovf.val); !s) return s;
         if (Status s = upload(c, c->z_ocol, P.Z.ovf.col); !s) return s;
+        // int16 slot offsets relative to the element's own array index (PCG_COL16=0 disables)
+        const char* ce = getenv("PCG_COL16");
+        if (!(ce && atoi(ce) == 0) && P.dia_q == 0) {
+            auto rel16 = [&](const Ell& E, int16_t*& dst) -> Status {
+                std::vector<int16_t> r(E.col.size());
+                const int64_t hoff = P.hoff();
+                for (size_t m = 0; m < E.col.size(); ++m) {
+                    const int64_t off = (int64_t)E.col[m] - ((int64_t)(m / kEll) + hoff);
+                    if (off < -32768 || off > 32767) return Status::ok();      // keep int32 columns
+                    r[m] = (int16_t)off;
+                }
+                return upload(c, dst, r);
+            };
+            if (Status st = rel16(P.ZT, c->zt_c16); !st) return st;
+            if (Status st = rel16(P.Z, c->z_c16); !st) return st;
+        }
     }
     double** vecs[] = {&c->x, &c->b, &c->q, &c->t, &c->s, &c->r[0], &c->r[1], &c->d[0], &c->d[1]};
     for (double** v : vecs) if (Status s = dalloc(c, *v, nel); !s) return s;
@@ -629,8 +646,8 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     const int64_t G = std::max<int64_t>((int64_t)A.nbx * P.nloc, kBlock);
     for (int k = 0; k < 3; ++k) if (Status s = dalloc(c, c->partial[k], G); !s) return s;
     A.cE = c->cE; A.cN = c->cN; A.sigma = c->sigma; A.diag = c->diag; A.piv = c->piv;
-    A.zt = EllDev{c->zt_val, c->zt_col, c->zt_ooff, c->zt_oval, c->zt_ocol, P.owned_elements()};
-    A.z = EllDev{c->z_val, c->z_col, c->z_ooff, c->z_oval, c->z_ocol, P.owned_elements()};
+    A.zt = EllDev{c->zt_val, c->zt_col, c->zt_ooff, c->zt_oval, c->zt_ocol, P.owned_elements(), c->zt_c16};
+    A.z = EllDev{c->z_val, c->z_col, c->z_ooff, c->z_oval, c->z_ocol, P.owned_elements(), c->z_c16};
     A.x = c->x; A.b = c->b; A.q = c->q; A.t = c->t; A.s = c->s;
     A.r[0] = c->r[0]; A.r[1] = c->r[1]; A.d[0] = c->d[0]; A.d[1] = c->d[1];
     for (int k = 0; k < 3; ++k) A.partial[k] = c->partial[k];
@@ -651,7 +668,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         c->bytes_k[1] = (8.0 * A.dia_q + 40.0) * No;
         c->bytes_k[2] = (8.0 * A.dia_q + 16.0) * No;
     } else if (P.factored()) {
-        c->bytes_k[1] = (48.0 + 12.0 * z) * No; c->bytes_k[2] = (32.0 + 12.0 * z) * No;
+        c->bytes_k[1] = (48.0 + 12.0 * z) * No; c->bytes_k[2] = (32.0 + 12.0 * z) * No;   // model (int32 columns)
     }
     else { c->bytes_k[1] = 40.0 * No; c->bytes_k[2] = 0.0; }
     CU(cudaGetLastError());
