@@ -40,6 +40,14 @@ UNIT = "iter/s"
 WORKLOAD = "cfg4: ORCA025-like 1442x1021 grid, E-W periodic, ~17% land, AINV(tau=0.1) PCG to ||r||/||b|| <= 1e-10"
 
 
+def workload_name(args):
+    """The default bench line is WORKLOAD; other preconditioners / configs are named as run."""
+    if args.config == "cfg4" and args.precond == "ainv" and args.tau == 0.1 and args.tol == 1e-10:
+        return WORKLOAD
+    pc = {"ainv": "AINV(tau=%g)" % args.tau, "jacobi": "Jacobi", "fsai": "FSAI(q=%d, the paper's P)" % args.fsai_q}[args.precond]
+    return "%s: %s PCG to ||r||/||b|| <= %g" % (args.config, pc, args.tol)
+
+
 def fallback_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -275,7 +283,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": dev_ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (SURVEY A.1 generator, seed 2; b = A x*, x* ~ N(0,1) seed 0)",
-                "config": {"workload": WORKLOAD, "grid": [p.ni, p.nj], "n_ocean": p.n_ocean,
+                "config": {"workload": workload_name(args), "grid": [p.ni, p.nj], "n_ocean": p.n_ocean,
                            "precond": args.precond, "tau": args.tau, "tol": args.tol,
                            **({"fsai_q": args.fsai_q} if args.precond == "fsai" else {}),
                            "iterations_per_solve": iters, "time_to_solution_ms": dev_ms / args.steps,

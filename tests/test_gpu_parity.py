@@ -348,3 +348,18 @@ def test_pb2_solve_bitwise_canonical(name, fill):
     assert np.array_equal(hist, ref.hist)
     assert np.array_equal(host(xg), A.to_grid(ref.x))
     S.close()
+
+
+def test_local_ranks_pb2_bitwise():
+    """P_B2 per rank block (block-local, w = 0) through the multi-rank device path on one GPU =
+    the oracle's partitioned canonical PCG with the same fixed-fill factor."""
+    p = synth.config("cfg2")
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, 0.0, parts=3, halo=0, fill=5)
+    b = rhs(A, p)
+    R = pcg.LocalRanks(p.cE, p.cN, p.mask, 3, tau=0.0, ainv_fill=5)
+    ref = oracle.pcg(A, b, "ainv", M, 1e-10, maxit=A.n, mode="canonical", pitch=R.pitch, block=R.block, parts=3)
+    xg, k, hist, rep = R.solve(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
+    assert k == ref.iterations and np.array_equal(hist, ref.hist)
+    assert np.array_equal(host(xg), A.to_grid(ref.x))
+    R.close()
