@@ -248,6 +248,8 @@ def main():
         S.solve(b, tol=args.tol, maxit=maxit)
         ms, by = S.kernel_times(args.profile_iters)
         names = ["K1_stencil", "K2_ZTr", "K3_Zt"]
+        if by[2] == 0 and args.precond in ("ainv", "fsai"):
+            names[1] = "K23_ZTr_Zt"                              # K2 and K3 fused into one kernel
         kk = int(np.argmax(ms[:3]))
         peak, peak_src = fallback_peak()
         ach = by[kk] / (ms[kk] * 1e-3) / 1e9
@@ -260,7 +262,7 @@ def main():
                 "frac": ach / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": by[kk], "ms_per_launch": ms[kk]}
         ktimes = {names[i]: {"ms": ms[i], "alg_GBps": by[i] / (ms[i] * 1e-3) / 1e9 if ms[i] > 0 else None}
-                  for i in range(3)}
+                  for i in range(3) if by[i] > 0}
         ktimes["iteration_ms"] = ms[3]
         ktimes["iteration_alg_GBps"] = float(by.sum() / (ms[3] * 1e-3) / 1e9)
 
@@ -272,8 +274,10 @@ def main():
                          f"oracle's own assembly+AINV ({r['setup_s']:.2f} s, excluded)"}
 
     # launches per solve: prologue 4 (prep, init, K2, K3) + WHILE body of 2 iterations x 3 + epilogue 2
-    per_iter = 3 if args.precond in ("ainv", "fsai") else 2
-    pro = 4 if args.precond in ("ainv", "fsai") else 3
+    # (K23: prologue 3, 2 per iteration)
+    fused = ktimes is not None and "K23_ZTr_Zt" in ktimes
+    per_iter = 3 if args.precond in ("ainv", "fsai") and not fused else 2
+    pro = 4 if args.precond in ("ainv", "fsai") and not fused else 3
     if world == 1:
         launches = sum(pro + per_iter * 2 * math.ceil(k / 2) + 2 for k in iters)
     else:

@@ -781,6 +781,82 @@ __device__ __forceinline__ double ell_row16(const EllDev& E, int64_t e, int64_t 
     return overflow_sum(E, e, acc, gat);
 }
 
+// ---- structured Z / Z^T rows (internal.h Sz; DQ = -2 kernels) ---------------------
+// Every column is the element's own index plus a fixed offset or a run position, so the fixed
+// slots' gathers issue together with the value loads (no index load in between); a run of k
+// entries costs one more stage: its values and gathers, four per round, the next round's loads
+// in flight before this round's fmas.  A warp flagged generic applies the ELL form.  Same entries,
+// same ascending-column fma order as the ELL row (zero slots are fma(0, x, acc) = acc).
+template <class Gather>
+__device__ __forceinline__ double run_sum(const double* run, int nr, int rounds, int64_t g0, double acc, Gather gat) {
+    double zn[4], xn[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const bool in = u < nr;
+        zn[u] = in ? __ldg(run + 32 * u) : 0.0;
+        xn[u] = in ? gat(g0 + u) : 0.0;
+    }
+    for (int m0 = 0; m0 < rounds; m0 += 4) {
+        double z[4], x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) { z[u] = zn[u]; x[u] = xn[u]; }
+        if (m0 + 4 < rounds) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = m0 + 4 + u;
+                const bool in = j < nr;
+                zn[u] = in ? __ldg(run + 32 * j) : 0.0;
+                xn[u] = in ? gat(g0 + j) : 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (m0 + u < nr) acc = __fma_rn(z[u], x[u], acc);
+    }
+    return acc;
+}
+
+// Z^T row of owned element e at array index a (K2): a-2P, a-P, run a-k .. a-2, a-1, a (= xself)
+template <class Gather>
+__device__ __forceinline__ double sz_zt_row(const KArgs& A, int64_t e, int64_t a, double xself, Gather gat) {
+    const SzDev& S = A.szt;
+    const int64_t P = A.pitch;
+    const uint2 w = __ldg(S.w + (e >> 5));
+    const int k = __ldg(S.k + e);
+    double v[4];
+    ld_nc_f64x4(S.val4 + 4 * e, v);
+    const double x0 = gat(a >= 2 * P ? a - 2 * P : a);
+    const double x1 = gat(a - P);
+    const double x2 = gat(a - 1);
+    if (w.x >> 31) return A.zt.col16 ? ell_row16(A.zt, e, a, gat) : ell_row(A.zt, e, gat);
+    double acc = __fma_rn(v[0], x0, 0.0);
+    acc = __fma_rn(v[1], x1, acc);
+    if (w.x) acc = run_sum(S.run + w.y + (e & 31), k - 1, (int)w.x, a - k, acc, gat);
+    acc = __fma_rn(v[2], x2, acc);
+    return __fma_rn(v[3], xself, acc);
+}
+
+// Z row of owned element e at array index a (K3): a, a+1, run a+2 .. a+k, a+P, a+2P
+template <class Gather>
+__device__ __forceinline__ double sz_z_row(const KArgs& A, int64_t e, int64_t a, Gather gat) {
+    const SzDev& S = A.sz;
+    const int64_t P = A.pitch;
+    const uint2 w = __ldg(S.w + (e >> 5));
+    const int k = __ldg(S.k + e);
+    double v[4];
+    ld_nc_f64x4(S.val4 + 4 * e, v);
+    const double x0 = gat(a);
+    const double x1 = gat(a + 1);
+    const double x2 = gat(a + P);
+    const double x3 = gat(a + 2 * P < A.nel_all ? a + 2 * P : a);
+    if (w.x >> 31) return A.z.col16 ? ell_row16(A.z, e, a, gat) : ell_row(A.z, e, gat);
+    double acc = __fma_rn(v[0], x0, 0.0);
+    acc = __fma_rn(v[1], x1, acc);
+    if (w.x) acc = run_sum(S.run + w.y + (e & 31), k - 1, (int)w.x, a + 2, acc, gat);
+    acc = __fma_rn(v[2], x2, acc);
+    return __fma_rn(v[3], x3, acc);
+}
+
 #ifndef PCG_MINB_K2
 #define PCG_MINB_K2 4            // register budgets: resident 256-thread blocks per SM ptxas targets
 #endif
@@ -864,6 +940,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
             auto gat = [&](int64_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); };
             double acc;
             if constexpr (DQ > 0) acc = dia_zt_row<DQ>(A, W, rnew, gat);
+            else if constexpr (DQ == -2) acc = sz_zt_row(A, W.a - A.hoff, W.a, rnew, gat);
             else if constexpr (DQ < 0) acc = ell_row16(A.zt, W.a - A.hoff, W.a, gat);
             else acc = ell_row(A.zt, W.a - A.hoff, gat);
             A.t[W.a] = __ddiv_rn(acc, pv);
@@ -910,6 +987,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
             const double rv = rn[W.a];
             double acc;
             if constexpr (DQ > 0) acc = dia_z_row<DQ>(A, W, t);
+            else if constexpr (DQ == -2) acc = sz_z_row(A, W.a - A.hoff, W.a, [&](int64_t g) { return __ldg(t + g); });
             else if constexpr (DQ < 0) acc = ell_row16(A.z, W.a - A.hoff, W.a, [&](int32_t g) { return __ldg(t + g); });
             else acc = ell_row(A.z, W.a - A.hoff, [&](int32_t g) { return __ldg(t + g); });
             A.s[W.a] = acc;
@@ -941,6 +1019,191 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
     if (last) {
         k3_finish(A, init);
         TL(2, 3);
+    }
+}
+
+// ---- K23: K2 and K3 in one persistent kernel -------------------------------
+// Step v of one ticket sequence v = 0 .. U+L-1 does the K2 work of unit v (v < U) and then the K3
+// work of unit v-L (v >= L), L = A.lag23 >= nbx.  Units run north to south and a Z row reaches
+// only north (rows j .. j + zreach), so K3's unit w needs t and r_new of K2 units with smaller
+// tickets: rowdone[j] counts the K2 units of row j completed in this launch (thread 0's release
+// add after the block barrier that follows the unit's stores).  Each warp issues relaxed loads of
+// its K3 rows' counters before its K2 half and checks them after it (spinning only if a row is
+// short, which a lag beyond the in-flight window makes rare).  Progress: a step waits only on
+// K2 units with smaller tickets than its own, and the smallest unfinished K2 unit never waits.
+// The K3 half reads t and r_new with L1-cached loads issued after the counters were observed
+// complete: no SM holds an older copy of those lines (L1 is invalidated at launch, rows are
+// pitched so no line spans two rows, and nothing reads a row of t or r_new before it is
+// complete).  Partials, trees and the final sums are those of K2 then K3, so the result is bitwise
+// the same; the second kernel boundary (drain + ramp) and K3's DRAM reads of t and r_new (now L2
+// hits, written ~L units earlier) are saved.
+#ifndef PCG_MINB_K23
+#define PCG_MINB_K23 3
+#endif
+
+__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// final_sum over two partial arrays in one walk (each sum in final_sum's order: bitwise the same)
+template <int NB>
+__device__ __forceinline__ void final_sum_pair(const double* pa, const double* pb, int64_t G, double& ra, double& rb) {
+    double aa = 0.0, ab = 0.0;
+    int64_t m = threadIdx.x < kBlock ? (int64_t)threadIdx.x : G;
+    for (; m < G; m += NB * kBlock) {
+        double p[NB], q[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const bool in = m + u * kBlock < G;
+            p[u] = in ? __ldcg(pa + m + u * kBlock) : 0.0;
+            q[u] = in ? __ldcg(pb + m + u * kBlock) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < NB; ++u)
+            if (m + u * kBlock < G) { aa = __dadd_rn(aa, p[u]); ab = __dadd_rn(ab, q[u]); }
+    }
+    ra = block_tree(aa);
+    rb = block_tree(ab);
+}
+
+template <int DQ>
+__global__ void __launch_bounds__(kBlock + 32, PCG_MINB_K23) k23_ainv_kernel(const KArgs A, const int par, const int init) {
+    static_assert(DQ <= 0, "K23 applies the ELL form only");
+    pdl_wait();
+    if (!is_active(A)) return;
+    double alpha;
+    if (!get_alpha(A, init, alpha)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
+        return;
+    }
+    const uint32_t target = (uint32_t)A.nbx * (__ldcg(&A.sc->epoch) + 1u);
+    const double* __restrict__ ro = A.r[par];
+    double* rn = A.r[par ^ 1];
+    const double* __restrict__ q = A.q;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    auto tbody = [&](const Unit& W) {                 // K2: r -= alpha q ; t = (Z^T r) / Dhat ; (r, r)
+        double v = 0.0;
+        if (W.live) {
+            const double rnew = __fma_rn(-alpha, q[W.a], ro[W.a]);
+            const double pv = A.piv[W.a];
+            auto gat = [&](int64_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); };
+            double acc;
+            if constexpr (DQ == -2) acc = sz_zt_row(A, W.a - A.hoff, W.a, rnew, gat);
+            else if constexpr (DQ < 0) acc = ell_row16(A.zt, W.a - A.hoff, W.a, gat);
+            else acc = ell_row(A.zt, W.a - A.hoff, gat);
+            A.t[W.a] = __ddiv_rn(acc, pv);
+            rn[W.a] = rnew;
+            v = __dmul_rn(rnew, rnew);
+        }
+        return v;
+    };
+    auto sbody = [&](const Unit& W) {                 // K3: s = Z t ; (s, r)
+        double v = 0.0;
+        if (W.live) {
+            const double rv = __ldca(rn + W.a);
+            auto gat = [&](int64_t g) { return __ldca(A.t + g); };
+            double acc;
+            if constexpr (DQ == -2) acc = sz_z_row(A, W.a - A.hoff, W.a, gat);
+            else if constexpr (DQ < 0) acc = ell_row16(A.z, W.a - A.hoff, W.a, gat);
+            else acc = ell_row(A.z, W.a - A.hoff, gat);
+            A.s[W.a] = acc;
+            v = __dmul_rn(acc, rv);
+        }
+        return v;
+    };
+    auto live_of = [&](Unit& W) {
+        if (A.landskip) W.live = W.inrow && ((__ldg(A.ocean + ((int64_t)W.j * A.nbx + W.bx) * kWarps + warp) >> lane) & 1u);
+    };
+    // Warps 0..7 compute; warp 8 keeps the books (tickets, the row-flag release -- a gpu-scope
+    // fence that waits for the step's stores -- and the unit partials), so no compute warp stalls
+    // on the fence: it has a whole step to complete before the next barrier.
+    __shared__ long long s_next[2];
+    __shared__ double wsd[2][2][kWarps];
+    const int64_t U = n_units(A), L = A.lag23, V = U + L;
+    const bool books = warp == kWarps;
+    if (books && lane == 0) s_next[0] = (long long)atomicAdd(&A.sc->ticket[1], 1ull);
+    __syncthreads();
+    int64_t v = s_next[0];
+    int cur = 1;
+    while (v < V) {
+        const bool has_t = v < U, has_s = v >= L;
+        if (books) {
+            if (lane == 0) s_next[cur] = (long long)atomicAdd(&A.sc->ticket[1], 1ull);
+            __syncthreads();
+            if (has_t && lane == 0) {
+                const Unit Wt = unit_of(A, v);
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(A.rowdone + Wt.j) : "memory");
+            }
+            if (has_t) {
+                const int64_t u = v;
+                const int64_t m = (int64_t)(A.nloc - 1 - (int32_t)(u / A.nbx)) * A.nbx + (u % A.nbx);
+                const double w = warp_tree(lane < kWarps ? wsd[cur][0][lane] : 0.0);
+                if (lane == 0) A.partial[1][m] = w;
+            }
+            if (has_s) {
+                const int64_t u = v - L;
+                const int64_t m = (int64_t)(A.nloc - 1 - (int32_t)(u / A.nbx)) * A.nbx + (u % A.nbx);
+                const double w = warp_tree(lane < kWarps ? wsd[cur][1][lane] : 0.0);
+                if (lane == 0) A.partial[2][m] = w;
+            }
+        } else {
+            Unit Ws{};
+            uint32_t pv = target;
+            if (has_s) {                               // this step's K3 rows: flag loads in flight
+                Ws = unit_of(A, v - L);
+                if (lane <= A.zreach && Ws.j + lane < A.nloc) pv = ld_relaxed_u32(A.rowdone + Ws.j + lane);
+            }
+            double vt = 0.0, vs = 0.0;
+            if (has_t) {
+                Unit Wt = unit_of(A, v);
+                live_of(Wt);
+                vt = tbody(Wt);
+            }
+            if (has_s) {
+                bool ok = (int32_t)(pv - target) >= 0;
+                while (!__all_sync(kFull, ok))
+                    if (!ok) { pv = ld_relaxed_u32(A.rowdone + Ws.j + lane); ok = (int32_t)(pv - target) >= 0; }
+                asm volatile("" ::: "memory");          // the K3 loads of t / r_new stay below the check
+                live_of(Ws);
+                vs = sbody(Ws);
+            }
+            vt = warp_tree(vt);
+            vs = warp_tree(vs);
+            if (lane == 0) { wsd[cur][0][warp] = vt; wsd[cur][1][warp] = vs; }
+            __syncthreads();
+        }
+        v = s_next[cur];
+        cur ^= 1;
+    }
+    pdl_trigger();
+    if (!count_block(&A.sc->counter[2])) return;
+    // last block: K2's and K3's final sums, then the scalars of k3_sum_rr / k3_finish
+    FinPre pre{};
+    if (threadIdx.x == 0) pre = fin_prefetch(A);
+    double rr, rs;
+    final_sum_pair<PCG_FINAL_NB_K3>(A.partial[1], A.partial[2], U, rr, rs);
+    if (threadIdx.x == 0) {
+        DevScalars* sc = A.sc;
+        sc->alpha = alpha;                             // = rho / (d, q) (0 in the init pass)
+        sc->xpend = init ? 0 : 1;
+        sc->counter[1] = 0;
+        sc->ticket[1] = 0;
+        sc->counter[2] = 0;
+        sc->ticket[2] = 0;
+        sc->epoch = sc->epoch + 1u;
+        if (A.multi) {
+            sc->loc[2] = rr;
+            sc->loc[1] = rs;
+        } else {
+            sc->red[2] = rr;
+            pre.rr = rr;
+            pre.h = __ddiv_rn(__dsqrt_rn(rr), pre.nb);
+            sc->hpre = pre.h;
+            if (init) fin_init(A, rs, rr);
+            else fin_iter(A, rs, pre);
+        }
     }
 }
 
@@ -1434,6 +1697,7 @@ __global__ void __launch_bounds__(kBlock) prep_kernel(const KArgs A) {
     const int64_t n = (int64_t)(A.nloc + 2 * A.halo) * A.pitch;
     for (int64_t a = (int64_t)blockIdx.x * kBlock + threadIdx.x; a < n; a += (int64_t)gridDim.x * kBlock) {
         A.d[0][a] = 0.0;
+        if (A.rowdone && a < A.nloc) A.rowdone[a] = 0u;     // K23 row flags (DevScalars::epoch = 0)
         const int64_t row = a / A.pitch;
         if (row >= A.halo && row < A.halo + A.nloc) {
             if (signbit(A.cN[a])) { A.x[a] = 0.0; A.b[a] = 0.0; }
@@ -1544,13 +1808,13 @@ size_t k1_smem(const KArgs& A, int grid) {
 
 // persistent grid: resident blocks per SM (occupancy API) x SMs, capped by the units
 template <class K>
-int persistent_grid(K kernel, int64_t units, int sms, size_t smem_guess) {
+int persistent_grid(K kernel, int64_t units, int sms, size_t smem_guess, int block = kBlock) {
     if (const char* e = getenv("PCG_PERSIST"))          // tuning: 0 = one unit per block
         if (atoi(e) == 0) return (int)units;
     if (const char* e = getenv("PCG_BLOCKS_PER_SM"))    // tuning: fixed resident blocks per SM
         return (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)atoi(e) * sms));
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem_guess);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, block, smem_guess);
     per_sm = std::max(per_sm, 1);
     return (int)std::max<int64_t>(1, std::min<int64_t>(units, (int64_t)per_sm * sms));
 }
@@ -1577,6 +1841,10 @@ void configure_kernels(KArgs& A, int sms) {
         A.g_k1 = (int)((S + per - 1) / per);
     }
     A.g_k2 = persistent_grid(k2_ainv_kernel<0>, U, sms, 2048);
+    A.g_k23 = persistent_grid(k23_ainv_kernel<-2>, U, sms, 0, kBlock + 32);
+    A.lag23 = A.g_k23 + 2 * A.nbx;                     // beyond the in-flight window: flag waits are rare
+    if (const char* e = getenv("PCG_LAG23")) A.lag23 = atoi(e);
+    A.lag23 = std::max(A.lag23, A.nbx);                // >= nbx: progress (see k23_ainv_kernel)
     A.g_k3 = persistent_grid(k3_ainv_kernel<0>, U, sms, 2048);
     A.g_kd = persistent_grid(k2_diag_kernel, U, sms, 4096);
     A.g_row = persistent_grid(init_residual_kernel, U, sms, 2048);
@@ -1614,6 +1882,8 @@ void configure_kernels(KArgs& A, int sms) {
     allow_smem(k2_ainv_kernel<0>, row_smem(A, A.g_k2, 1));
     allow_smem(k3_ainv_kernel<0>, row_smem(A, A.g_k3, 1));
     allow_smem(k2_ainv_kernel<-1>, row_smem(A, A.g_k2, 1));
+    allow_smem(k2_ainv_kernel<-2>, row_smem(A, A.g_k2, 1));
+    allow_smem(k3_ainv_kernel<-2>, row_smem(A, A.g_k3, 1));
     allow_smem(k3_ainv_kernel<-1>, row_smem(A, A.g_k3, 1));
     allow_smem(k2_ainv_kernel<4>, row_smem(A, A.g_k2, 1));
     allow_smem(k3_ainv_kernel<4>, row_smem(A, A.g_k3, 1));
@@ -1637,11 +1907,24 @@ static void launch_pdl(const KArgs& A, void (*kern)(P...), int grid, int block, 
     cfg.blockDim = dim3((unsigned)block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    unsigned n = 0;
+    if (A.pdl) {
+        at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    if (A.l2_bytes) {
+        at[n].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[n].val.accessPolicyWindow.base_ptr = A.l2_base;
+        at[n].val.accessPolicyWindow.num_bytes = A.l2_bytes;
+        at[n].val.accessPolicyWindow.hitRatio = A.l2_ratio;
+        at[n].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        at[n].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        ++n;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = A.pdl ? 1 : 0;
+    cfg.numAttrs = n;
     cudaLaunchKernelEx(&cfg, kern, args...);
 }
 
@@ -1656,18 +1939,27 @@ void launch_k1(const KArgs& A, int par, cudaStream_t st) {
     }
 }
 void launch_k2_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
+    if (A.fuse23 && A.dia_q == 0 && !A.tma) {
+        if (A.use_sz) launch_pdl(A, k23_ainv_kernel<-2>, A.g_k23, kBlock + 32, 0, st, A, par, init);
+        else if (A.zt.col16 && A.z.col16) launch_pdl(A, k23_ainv_kernel<-1>, A.g_k23, kBlock + 32, 0, st, A, par, init);
+        else launch_pdl(A, k23_ainv_kernel<0>, A.g_k23, kBlock + 32, 0, st, A, par, init);
+        return;
+    }
     if (A.tma) launch_pdl(A, k2_tma_kernel, A.g_t2, kBlock + 32, tma_smem_bytes<3>(), st, A, par, init);
     else if (A.dia_q > 8) launch_pdl(A, k2_ainv_kernel<16>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else if (A.dia_q > 4) launch_pdl(A, k2_ainv_kernel<8>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else if (A.dia_q > 0) launch_pdl(A, k2_ainv_kernel<4>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
+    else if (A.use_sz) launch_pdl(A, k2_ainv_kernel<-2>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else if (A.zt.col16) launch_pdl(A, k2_ainv_kernel<-1>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else launch_pdl(A, k2_ainv_kernel<0>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
 }
 void launch_k3_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
+    if (A.fuse23 && A.dia_q == 0 && !A.tma) return;    // done by K23
     if (A.tma) launch_pdl(A, k3_tma_kernel, A.g_t3, kBlock + 32, tma_smem_bytes<1>(), st, A, par, init);
     else if (A.dia_q > 8) launch_pdl(A, k3_ainv_kernel<16>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else if (A.dia_q > 4) launch_pdl(A, k3_ainv_kernel<8>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else if (A.dia_q > 0) launch_pdl(A, k3_ainv_kernel<4>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
+    else if (A.use_sz) launch_pdl(A, k3_ainv_kernel<-2>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else if (A.z.col16) launch_pdl(A, k3_ainv_kernel<-1>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else launch_pdl(A, k3_ainv_kernel<0>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
 }

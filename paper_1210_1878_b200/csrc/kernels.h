@@ -17,7 +17,8 @@ struct DevScalars {
     double rho_prev;      // rho of the previous iteration: K1 forms beta = rho / rho_prev itself
     double red[4];        // global reductions: [0] (d,q)  [1] (s,r)  [2] (r,r)  [3] (b,b) / true (r,r)
     double loc[4];        // this rank's block-tree sums (multi-rank path)
-    int32_t k, maxit, active, status, bzero, xpend, guard, pad_;
+    int32_t k, maxit, active, status, bzero, xpend, guard;
+    uint32_t epoch;       // K23 launches completed in this solve (row-flag target)
     uint32_t counter[4];  // last-block detection, reset by the last block
     unsigned long long ticket[4];   // dynamic unit assignment, reset by the last block
 };
@@ -31,6 +32,14 @@ struct EllDev {
     const int32_t* ocol;
     int64_t n;
     const int16_t* col16 = nullptr;   // kEll * n slot offsets from the element's own array index
+};
+
+// Device view of the structured form (internal.h Sz).
+struct SzDev {
+    const double* val4 = nullptr;     // 4 * n
+    const uint8_t* k = nullptr;       // n
+    const uint2* w = nullptr;         // per warp of 32 elements {rounds | generic << 31, run offset}
+    const double* run = nullptr;
 };
 
 struct KArgs {
@@ -58,6 +67,9 @@ struct KArgs {
     int64_t nel;                      // owned elements nloc * pitch
     const double *cE, *cN, *sigma, *diag, *piv;
     EllDev zt, z;                     // rows of Z^T (K2) and of Z (K3)
+    SzDev szt, sz;                    // structured form of the same rows (used when use_sz)
+    int32_t use_sz;
+    int64_t nel_all;                  // elements of every per-point array, halo rows included
     int32_t periodic;
     double *x, *b, *q, *t, *s;
     double *r[2], *d[2];
@@ -69,6 +81,15 @@ struct KArgs {
     int32_t multi;                    // 1: reductions end at rank sums (NCCL path)
     int32_t use_cond;
     cudaGraphConditionalHandle cond;
+    // K23: K2 and K3 fused into one persistent kernel (one rank, or Z without cross-rank columns)
+    int32_t fuse23;                   // 1: launch_k2_ainv launches k23_ainv_kernel, launch_k3_ainv nothing
+    int32_t zreach;                   // grid rows north of its own row a Z row reaches (>= 0)
+    int32_t lag23;                    // ticket lag of the K3 half behind the K2 half (>= nbx)
+    int32_t g_k23;
+    uint32_t* rowdone;                // [nloc] t rows completed (nbx per K23 launch), zeroed by prep
+    void* l2_base;                    // persisting L2 access-policy window of the iteration kernels
+    size_t l2_bytes;                  // (0: none)
+    float l2_ratio;
 };
 
 int64_t grid_blocks(const KArgs& A);

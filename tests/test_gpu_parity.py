@@ -363,3 +363,37 @@ def test_local_ranks_pb2_bitwise():
     assert k == ref.iterations and np.array_equal(hist, ref.hist)
     assert np.array_equal(host(xg), A.to_grid(ref.x))
     R.close()
+
+
+# ------------------------------------------------------ kernel-form variants (setup-time switches)
+VARIANTS = {"k23": {"PCG_FUSE23": "1"}, "k23_lag": {"PCG_FUSE23": "1", "PCG_LAG23": "7"},
+            "sz": {"PCG_SZ": "1"}, "sz_k23": {"PCG_SZ": "1", "PCG_FUSE23": "1"},
+            "no_l2_window": {"PCG_L2PERSIST": "0"}}
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_kernel_variants_bitwise_canonical(name, variant, monkeypatch):
+    """K2+K3 fused into one kernel (K23, incl. the minimum lag), the structured Z form and the
+    run without the L2 window: the same canonical arithmetic, so preconditioner and solve are
+    bitwise the oracle's."""
+    for k, v in VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    p = synth.config(name)
+    A, S, ref, x, k, hist, rep, _ = _canonical_pair(p, "ainv", 1e-10)
+    assert k == ref.iterations
+    assert np.array_equal(hist, ref.hist)
+    assert np.array_equal(x, A.to_grid(ref.x))
+    M = oracle.ainv(A, TAU)
+    r = A.from_grid(synth.xstar(p, 7))
+    s = host(S.apply_preconditioner(dev(A.to_grid(r))))
+    assert np.array_equal(s, A.to_grid(M.apply_canonical(r)))
+    S.close()
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_local_ranks_k23_bitwise(P, monkeypatch):
+    """K23 on block-local Z (w = 0) across P in-process ranks = the oracle's partitioned mode."""
+    monkeypatch.setenv("PCG_FUSE23", "1")
+    monkeypatch.setenv("PCG_SZ", "1")
+    test_local_ranks_bitwise_vs_oracle_partitioned("cfg3", P, "ainv")
