@@ -101,6 +101,19 @@ __device__ __forceinline__ double final_sum(const double* partial, int64_t G) {
     return block_tree(acc);
 }
 
+// final_sum in every thread of the block (redundant-sum mode: each block of the consumer kernel
+// forms the same canonical sum, bitwise)
+template <int NB>
+__device__ __forceinline__ double final_sum_all(const double* partial, int64_t G) {
+    __shared__ double bc;
+    const double v = final_sum<NB>(partial, G);
+    if (threadIdx.x == 0) bc = v;
+    __syncthreads();
+    const double r = bc;
+    __syncthreads();
+    return r;
+}
+
 // tree over the per-rank sums in rank order, zero padded to 32
 __device__ double rank_tree(const double* gath, int nranks, int slot) {
     double u[32];
@@ -616,9 +629,41 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1F) k1_flat_kernel(const KAr
             set_cond(A, 0);
         }
     }
-    const double beta = __ddiv_rn(A.sc->rho, A.sc->rho_prev), alpha = A.sc->alpha;
+    double beta;
+    const double alpha = A.sc->alpha;
+    if (A.redundant) {
+        // rho = (s, r) of K3's partials, formed by every block; beta = rho / rho of the last iteration
+        const double rho = final_sum_all<8>(A.partial[2], n_units(A));
+        if (!isfinite(rho)) {                            // fin_iter's breakdown on (s, r)
+            if (blockIdx.x == 0 && threadIdx.x == 0) {
+                const int k = A.sc->k;
+                if (k < A.hist_cap) A.hist[k] = NAN;
+                stop(A, kStBreakdown);
+            }
+            return;
+        }
+        beta = __ddiv_rn(rho, A.sc->rhop[par ^ 1]);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            A.sc->rhop[par] = rho;
+            A.sc->rho = rho;
+            A.sc->xpend = 0;                               // this kernel does x += alpha_prev d_old
+            A.sc->ticket[1] = 0;                           // K2's / K3's tickets (both finished)
+            A.sc->ticket[2] = 0;
+        }
+    } else {
+        beta = __ddiv_rn(A.sc->rho, A.sc->rho_prev);
+    }
     bool last;
-    if (A.k1flat == 2) {
+    if (A.redundant) {
+        extern __shared__ double ws[];
+        const int64_t U = n_units(A);
+        int k = 0;
+        for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k)
+            put_warp_sum(ws, k, k1_point<SIGMA>(A, unit_of(A, u), par, beta, alpha));
+        pdl_trigger();
+        finish_units<1>(A, ws, A.partial[0], nullptr, nullptr);
+        return;
+    } else if (A.k1flat == 2) {
         // static block stride, no barrier per unit: warp sums in shared memory, trees at the end
         extern __shared__ double ws[];
         const int64_t U = n_units(A);
@@ -877,6 +922,43 @@ __device__ __forceinline__ double sz_z_row(const KArgs& A, int64_t e, int64_t a,
 __device__ __forceinline__ void k3_sum_rr(const KArgs& A, int init) {
     if (blockIdx.x != 0) return;
     const double rr = final_sum<PCG_FINAL_NB_K3>(A.partial[1], n_units(A));
+    if (A.redundant) {
+        // redundant-sum mode: the history value and the stop test need only (r, r), so block 0
+        // does fin_init / fin_iter's bookkeeping here; the (s, r) breakdown test moves to K1
+        if (threadIdx.x == 0) {
+            DevScalars* sc = A.sc;
+            sc->red[2] = rr;
+            const double h = __ddiv_rn(__dsqrt_rn(rr), sc->nb);
+            sc->hpre = h;
+            if (init) {
+                sc->rhop[1] = INFINITY;                  // beta of the first iteration = rho / inf = +0
+                sc->rho_prev = INFINITY;
+                if (sc->bzero) {
+                    A.hist[0] = 0.0;
+                    sc->active = 0;
+                    set_cond(A, 0);
+                } else {
+                    A.hist[0] = h;
+                    const int act = (h > sc->tol) && (sc->maxit > 0);
+                    sc->active = act;
+                    set_cond(A, act);
+                }
+            } else {
+                const int k = sc->k + 1;
+                sc->k = k;
+                if (!isfinite(rr)) {
+                    if (k < A.hist_cap) A.hist[k] = NAN;
+                    stop(A, kStBreakdown);
+                } else {
+                    if (k < A.hist_cap) A.hist[k] = h;
+                    const int act = (h > sc->tol) && (k < sc->maxit);
+                    sc->active = act;
+                    set_cond(A, act);
+                }
+            }
+        }
+        return;
+    }
     if (threadIdx.x == 0) {
         DevScalars* sc = A.sc;
         if (A.multi) {
@@ -924,7 +1006,22 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
     TL(1, 1);
     if (!is_active(A)) return;
     double alpha;
-    if (!get_alpha(A, init, alpha)) {
+    if (A.redundant) {
+        // alpha = rho / (d, q), (d, q) from K1's partials formed by every block
+        alpha = 0.0;
+        if (!init) {
+            const double gamma = final_sum_all<8>(A.partial[0], n_units(A));
+            if (!(gamma > 0.0) || !isfinite(gamma)) {
+                if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
+                return;
+            }
+            alpha = __ddiv_rn(A.sc->rhop[par], gamma);
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            A.sc->alpha = alpha;                           // the pending x update of the next K1 / fin
+            A.sc->xpend = init ? 0 : 1;
+        }
+    } else if (!get_alpha(A, init, alpha)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
         return;
     }
@@ -1004,17 +1101,19 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
         dynamic_units(A, &A.sc->ticket[2], A.partial[2], body, A.sched_u0);
         pdl_trigger();
         TL(2, 2);
+        if (A.redundant) return;                         // (s, r) is summed by the next K1's blocks
         last = count_block(&A.sc->counter[2]);
     } else if (A.dynamic) {
         dynamic_units(A, &A.sc->ticket[2], A.partial[2], body);
         pdl_trigger();
         TL(2, 2);
+        if (A.redundant) return;
         last = count_block(&A.sc->counter[2]);
     } else {
         const int64_t U = n_units(A);
         int k = 0;
         for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k) put_warp_sum(ws, k, body(unit_of(A, u)));
-        last = finish_units<1>(A, ws, A.partial[2], nullptr, &A.sc->counter[2]);
+        last = finish_units<1>(A, ws, A.partial[2], nullptr, A.redundant ? nullptr : &A.sc->counter[2]);
     }
     if (last) {
         k3_finish(A, init);
@@ -1634,7 +1733,22 @@ __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const in
     pdl_wait();
     if (!is_active(A)) return;
     double alpha;
-    if (!get_alpha(A, init, alpha)) {
+    if (A.redundant) {
+        // alpha = rho / (d, q), (d, q) from K1's partials formed by every block
+        alpha = 0.0;
+        if (!init) {
+            const double gamma = final_sum_all<8>(A.partial[0], n_units(A));
+            if (!(gamma > 0.0) || !isfinite(gamma)) {
+                if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
+                return;
+            }
+            alpha = __ddiv_rn(A.sc->rhop[par], gamma);
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            A.sc->alpha = alpha;                           // the pending x update of the next K1 / fin
+            A.sc->xpend = init ? 0 : 1;
+        }
+    } else if (!get_alpha(A, init, alpha)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
         return;
     }

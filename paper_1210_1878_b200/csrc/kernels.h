@@ -19,6 +19,7 @@ struct DevScalars {
     double loc[4];        // this rank's block-tree sums (multi-rank path)
     int32_t k, maxit, active, status, bzero, xpend, guard;
     uint32_t epoch;       // K23 launches completed in this solve (row-flag target)
+    double rhop[2];       // redundant-sum mode: rho of the iterations of parity 0 / 1 (rhop[1] = inf before the first)
     uint32_t counter[4];  // last-block detection, reset by the last block
     unsigned long long ticket[4];   // dynamic unit assignment, reset by the last block
 };
@@ -87,6 +88,10 @@ struct KArgs {
     int32_t lag23;                    // ticket lag of the K3 half behind the K2 half (>= nbx)
     int32_t g_k23;
     uint32_t* rowdone;                // [nloc] t rows completed (nbx per K23 launch), zeroed by prep
+    // Redundant-sum mode (one rank, K1 / K2 / K3 launches): no last-block tails; every block of the
+    // consumer kernel forms the canonical final sum it needs (K1: (s, r) -> beta, K2: (d, q) ->
+    // alpha) and K3's block 0 does the history / stop test from K2's (r, r) at its start.
+    int32_t redundant;
     void* l2_base;                    // persisting L2 access-policy window of the iteration kernels
     size_t l2_bytes;                  // (0: none)
     float l2_ratio;

@@ -434,9 +434,12 @@ Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, doubl
     if (x0) CU(cudaMemcpy2DAsync(c->x + P.hoff(), dp, x0, sp, sp, (size_t)P.nloc, kin, c->st));
     else CU(cudaMemsetAsync(c->x + P.hoff(), 0, (size_t)P.nloc * dp, c->st));
     if (use_fused(c)) {
-        if (Status s = launch_prologue(c); !s) return s;
-        CU(launch_loop(c->A, c->st));
-        if (Status s = launch_epilogue(c); !s) return s;
+        const int32_t red = c->A.redundant;               // the loop kernel keeps its own scalars
+        c->A.redundant = 0;
+        Status s = launch_prologue(c);
+        if (s) { CU(launch_loop(c->A, c->st)); s = launch_epilogue(c); }
+        c->A.redundant = red;
+        if (!s) return s;
     } else if (use_graph(c)) {
         CU(cudaGraphLaunch(c->exec, c->st));
     } else {
@@ -738,6 +741,12 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         const char* e = getenv("PCG_FSAI_DIA");
         if (!(e && atoi(e) == 0) && P.dia_q <= 16) A.dia_q = P.dia_q;   // wider bands: ELL path
     }   // kernels: 0 = factored Z D^-1 Z^T (AINV, FSAI)
+    // redundant-sum mode (kernels.h): one rank, the K1 row-segment form, K2 / K3 as two launches
+    A.redundant = 0;
+    if (P.factored() && !c->multi && !A.fuse23 && A.k1flat == 2 && !A.tma) {
+        const char* re = getenv("PCG_REDUNDANT");
+        A.redundant = re ? atoi(re) != 0 : 1;
+    }
     // algorithmic bytes per launch: N_o ocean points, z off-diagonals per column
     const double No = (double)P.n_owned, z = No > 0 ? (double)P.nnz_off / No : 0.0;
     c->bytes_k[0] = 64.0 * No;
