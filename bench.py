@@ -273,13 +273,14 @@ def main():
                "sample": f"{args.config} full grid, {r['iters']} plain-order PCG iterations (tol=0) after the "
                          f"oracle's own assembly+AINV ({r['setup_s']:.2f} s, excluded)"}
 
-    # launches per solve: prologue 4 (prep, init, K2, K3) + WHILE body of 2 iterations x 3 + epilogue 2
-    # (K23: prologue 3, 2 per iteration)
+    # launches per solve: prologue 4 (prep, init, K2, K3) + WHILE bodies of PCG_BODY_ITERS (8)
+    # iterations x 3 + epilogue 2 (K23: prologue 3, 2 per iteration)
     fused = ktimes is not None and "K23_ZTr_Zt" in ktimes
     per_iter = 3 if args.precond in ("ainv", "fsai") and not fused else 2
     pro = 4 if args.precond in ("ainv", "fsai") and not fused else 3
     if world == 1:
-        launches = sum(pro + per_iter * 2 * math.ceil(k / 2) + 2 for k in iters)
+        body = max(2, int(os.environ.get("PCG_BODY_ITERS", "8")) & ~1)
+        launches = sum(pro + per_iter * body * math.ceil(k / body) + 2 for k in iters)
     else:
         launches = None
     if rank == 0:

@@ -101,6 +101,9 @@ __device__ __forceinline__ double final_sum(const double* partial, int64_t G) {
     return block_tree(acc);
 }
 
+#ifndef PCG_RED_NB
+#define PCG_RED_NB 8                 // partial loads in flight per thread in the redundant sums
+#endif
 // final_sum in every thread of the block (redundant-sum mode: each block of the consumer kernel
 // forms the same canonical sum, bitwise)
 template <int NB>
@@ -633,7 +636,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1F) k1_flat_kernel(const KAr
     const double alpha = A.sc->alpha;
     if (A.redundant) {
         // rho = (s, r) of K3's partials, formed by every block; beta = rho / rho of the last iteration
-        const double rho = final_sum_all<8>(A.partial[2], n_units(A));
+        const double rho = final_sum_all<PCG_RED_NB>(A.partial[2], n_units(A));
         if (!isfinite(rho)) {                            // fin_iter's breakdown on (s, r)
             if (blockIdx.x == 0 && threadIdx.x == 0) {
                 const int k = A.sc->k;
@@ -1010,7 +1013,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
         // alpha = rho / (d, q), (d, q) from K1's partials formed by every block
         alpha = 0.0;
         if (!init) {
-            const double gamma = final_sum_all<8>(A.partial[0], n_units(A));
+            const double gamma = final_sum_all<PCG_RED_NB>(A.partial[0], n_units(A));
             if (!(gamma > 0.0) || !isfinite(gamma)) {
                 if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
                 return;
@@ -1733,22 +1736,7 @@ __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const in
     pdl_wait();
     if (!is_active(A)) return;
     double alpha;
-    if (A.redundant) {
-        // alpha = rho / (d, q), (d, q) from K1's partials formed by every block
-        alpha = 0.0;
-        if (!init) {
-            const double gamma = final_sum_all<8>(A.partial[0], n_units(A));
-            if (!(gamma > 0.0) || !isfinite(gamma)) {
-                if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
-                return;
-            }
-            alpha = __ddiv_rn(A.sc->rhop[par], gamma);
-        }
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            A.sc->alpha = alpha;                           // the pending x update of the next K1 / fin
-            A.sc->xpend = init ? 0 : 1;
-        }
-    } else if (!get_alpha(A, init, alpha)) {
+    if (!get_alpha(A, init, alpha)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
         return;
     }
