@@ -108,7 +108,11 @@ typedef struct {
                               rows below its first row, giving one global triangular Z (SURVEY
                               §8e, R15 and §6).  Across ranks every rank but the last
                               needs >= 16 owned rows (else PCG_ERR_ARG); the solve then exchanges
-                              w rows of q and r after K1 and the needed rows of t after K2. */
+                              the rows of q and r the owned columns reach (<= w) after K1 and the
+                              needed rows of t after K2.  w >= nj: every block starts at row 0, so
+                              each rank holds its columns of the GLOBAL Z (the
+                              preconditioner is bitwise independent of the rank count; the setup
+                              of rank p costs the AINV of rows [0, j_end)). */
     int32_t setup_threads; /* host threads for the AINV build (0 = automatic) */
     int32_t fsai_q;        /* PCG_PRECOND_FSAI: upper bandwidth q >= 0 of Z~ (entries z_ij with
                               j > i + q dropped); ignored otherwise */

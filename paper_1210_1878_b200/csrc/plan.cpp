@@ -392,7 +392,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     // the northern halo rows it receives from the neighbour).
     constexpr int32_t kNorthRows = 16;
     const bool halo_x = P.nranks > 1 && o->ainv_halo > 0;
-    const int32_t w = o->ainv_halo;
+    const int32_t w = std::min(o->ainv_halo, nj);     // >= nj: the global Z (every block from row 0)
     if (halo_x && P.rank < P.nranks - 1 && P.nloc < kNorthRows)
         return Status::err(PCG_ERR_ARG, "pcg_setup: halo-AINV across ranks needs >= 16 rows per rank");
     bool have_north = false;
@@ -464,8 +464,18 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             for (int64_t e = blocks[0].colptr[q]; e < blocks[0].colptr[q + 1]; ++e)
                 if (blocks[0].row_g[e] < (int64_t)P.jb * ni) reach_s = std::max(reach_s, jc - P.jb + 1);
         }
-    if (halo_x) P.halo = std::max({P.halo, w, reach});
-    P.halo_w = halo_x ? w : 0;
+    // rows of q / r the solve exchanges: the actual southern extent of this rank's columns (<= w;
+    // with w >= jb every block starts at row 0 and the owned columns are the GLOBAL Z's -- the
+    // left-looking column j only involves rows and columns < j -- NEXT-3's P-invariant
+    // preconditioner, whose extent is still Z's pattern reach, 2-3 rows at tau = 0.1)
+    int32_t w_eff = 0;
+    if (halo_x)
+        for (size_t q = 0; q < blocks[0].col_g.size(); ++q)
+            for (int64_t e = blocks[0].colptr[q]; e < blocks[0].colptr[q + 1]; ++e)
+                if (blocks[0].row_g[e] < (int64_t)P.jb * ni)
+                    w_eff = std::max(w_eff, P.jb - (int32_t)(blocks[0].row_g[e] / ni));
+    if (halo_x) P.halo = std::max({P.halo, w_eff, reach});
+    P.halo_w = halo_x ? std::max(1, w_eff) : 0;
     P.halo_t = reach;
     P.halo_t_send = reach_s;
     build_coeff_arrays();

@@ -77,6 +77,24 @@ def test_host_ainv_bitwise_equals_oracle_configs(name):
     assert pl.pitch % 32 == 0 and pl.pitch >= synth.config(name).ni
 
 
+@pytest.mark.parametrize("parts", [2, 3, 8])
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+def test_global_z_is_rank_count_invariant(name, parts):
+    """NEXT-3: with every block starting at row 0 (halo >= nj) the partitioned AINV
+    is the one-block AINV bit for bit, in the oracle and in the library -- the left-looking column
+    j only involves rows and columns < j, so its owner's row range does not
+    matter.  A wrong halo clamp or a block that drops southern rows breaks the equality."""
+    p = synth.config(name)
+    A = oracle.assemble(p)
+    one = oracle.ainv(A, 0.1 + 1e-9)
+    glob = oracle.ainv(A, 0.1 + 1e-9, parts=parts, halo=p.nj)
+    for f in ("colptr", "row", "zhat", "pivots", "scale"):
+        assert np.array_equal(getattr(glob, f), getattr(one, f))
+    local = oracle.ainv(A, 0.1 + 1e-9, parts=parts, halo=0)   # block-local differs (sanity)
+    assert local.row.size != one.row.size or not np.array_equal(local.zhat, one.zhat)
+    _compare(p, 0.1 + 1e-9, parts, p.nj)
+
+
 @pytest.mark.parametrize("parts,halo", [(2, 0), (4, 0), (4, 3), (8, 1)])
 def test_host_partitioned_ainv_bitwise_equals_oracle(parts, halo):
     _compare(synth.config("cfg2"), 0.1 + 1e-9, parts, halo)

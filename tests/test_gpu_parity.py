@@ -397,3 +397,25 @@ def test_local_ranks_k23_bitwise(P, monkeypatch):
     monkeypatch.setenv("PCG_FUSE23", "1")
     monkeypatch.setenv("PCG_SZ", "1")
     test_local_ranks_bitwise_vs_oracle_partitioned("cfg3", P, "ainv")
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_local_ranks_global_z(P):
+    """NEXT-3: ainv_halo >= nj gives every rank its columns of the global Z, so the preconditioner
+    applied across P ranks is the one-rank preconditioner (bitwise the oracle's partitioned
+    canonical PCG with halo = nj, whose factor equals the one-block factor); the q / r exchange
+    covers only the rows Z's pattern reaches."""
+    p = synth.config("cfg3")
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, TAU, parts=P, halo=p.nj)
+    b = rhs(A, p)
+    R = pcg.LocalRanks(p.cE, p.cN, p.mask, P, tau=TAU, ainv_halo=p.nj)
+    ref = oracle.pcg(A, b, "ainv", M, 1e-10, maxit=A.n, mode="canonical", pitch=R.pitch, block=R.block, parts=P)
+    xg, k, hist, rep = R.solve(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
+    assert k == ref.iterations
+    assert np.array_equal(hist, ref.hist)
+    assert np.array_equal(host(xg), A.to_grid(ref.x))
+    one = oracle.pcg(A, b, "ainv", oracle.ainv(A, TAU), 1e-10, maxit=A.n, mode="canonical", pitch=R.pitch,
+                     block=R.block)
+    assert abs(k - one.iterations) <= 2             # only the rank-ordered dot products differ
+    R.close()
