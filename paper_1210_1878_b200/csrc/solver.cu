@@ -696,7 +696,11 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         int maxp = 0, maxw = 0;
         cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, c->device);
         cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, c->device);
-        if (!(le && atoi(le) == 0) && maxp > 0 && maxw > 0 && c->hot_bytes > 0) {
+        // only when at least four vectors fit the set-aside: at ORCA12 (106 MB per vector) a window
+        // over part of one vector measured 737 against 647 us/iteration without (the set-aside then
+        // only shrinks the L2 left to everything else); PCG_L2PERSIST=2 forces it
+        const bool fits = (size_t)maxp >= 4 * (c->hot_bytes / 8);
+        if (!(le && atoi(le) == 0) && (fits || (le && atoi(le) == 2)) && maxp > 0 && maxw > 0 && c->hot_bytes > 0) {
             size_t setaside = std::min<size_t>((size_t)maxp, c->hot_bytes);
             size_t cur = 0;
             cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
@@ -832,6 +836,7 @@ void pcg_free(pcg_ctx* c) {
     cudaSetDevice(c->device);
     if (c->st) cudaStreamSynchronize(c->st);
     if (c->exec) cudaGraphExecDestroy(c->exec);
+    if (c->A.l2_bytes) cudaCtxResetPersistingL2Cache();   // its window's lines become normal lines
     for (void* p : c->allocs) cudaFree(p);
     if (c->h_sc) cudaFreeHost(c->h_sc);
     if (c->h_hist) cudaFreeHost(c->h_hist);
