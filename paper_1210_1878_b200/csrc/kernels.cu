@@ -905,6 +905,100 @@ __device__ __forceinline__ double sz_z_row(const KArgs& A, int64_t e, int64_t a,
     return __fma_rn(v[3], x3, acc);
 }
 
+// ---- per-thread cp.async double buffer for the scheduled walks (DQ = -3: ELL(4) + int16 offsets) --
+// Each thread copies its own element's streamed operands of the NEXT unit into shared memory
+// (LDGSTS, no registers held) while it gathers and computes the current one, so the DRAM latency
+// of unit k+1 overlaps unit k's gathers, overflow rounds, fma chain and warp sum.  The thread
+// reads back only what it copied itself: cp.async.wait_group suffices, no block barrier.
+__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// streamed operands of one unit of K2 (per thread: 4 Z^T values, 4 int16 slot offsets, r_old, q, pivot)
+struct K2Stage {
+    double2 v01[kBlock], v23[kBlock];
+    uint2 col[kBlock];
+    double r[kBlock], q[kBlock], piv[kBlock];
+};
+
+// K2's scheduled static walk (sched_units) with the double buffer; same units, same per-warp
+// sums, same arithmetic as the body of k2_ainv_kernel<-1> (bitwise).
+__device__ __forceinline__ void k2_sched_staged(const KArgs& A, int par, double alpha, double* ws, K2Stage* st) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+    const int32_t* sched = A.sched2;
+    const int32_t k0 = A.soff2[blockIdx.x], k1 = A.soff2[blockIdx.x + 1];
+    const double* __restrict__ ro = A.r[par];
+    double* __restrict__ rn = A.r[par ^ 1];
+    const double* __restrict__ q = A.q;
+    auto unit_k = [&](int32_t k) {
+        Unit W = unit_of(A, sched[k]);
+        if (A.landskip) W.live = W.inrow && ((__ldg(A.ocean + ((int64_t)W.j * A.nbx + W.bx) * kWarps + warp) >> lane) & 1u);
+        return W;
+    };
+    auto issue = [&](const Unit& W, int buf) {
+        if (W.live) {
+            const int64_t e = W.a - A.hoff;
+            cp_async16(&st[buf].v01[tid], A.zt.val + e * kEll);
+            cp_async16(&st[buf].v23[tid], A.zt.val + e * kEll + 2);
+            cp_async8(&st[buf].col[tid], A.zt.col16 + e * kEll);
+            cp_async8(&st[buf].r[tid], ro + W.a);
+            cp_async8(&st[buf].q[tid], q + W.a);
+            cp_async8(&st[buf].piv[tid], A.piv + W.a);
+        }
+        cp_async_commit();
+    };
+    if (k0 >= k1) return;
+    Unit Wc = unit_k(k0);
+    issue(Wc, 0);
+    for (int32_t k = k0; k < k1; ++k) {
+        const int buf = (k - k0) & 1;
+        Unit Wn{};
+        if (k + 1 < k1) {
+            Wn = unit_k(k + 1);
+            issue(Wn, buf ^ 1);
+            cp_async_wait<1>();                          // unit k's group has landed
+        } else {
+            cp_async_wait<0>();
+        }
+        double v = 0.0;
+        if (Wc.live) {
+            const K2Stage& S = st[buf];
+            const double2 v01 = S.v01[tid], v23 = S.v23[tid];
+            const uint2 cw = S.col[tid];
+            const double rnew = __fma_rn(-alpha, S.q[tid], S.r[tid]);
+            const double pv = S.piv[tid];
+            auto gat = [&](int64_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); };
+            const int32_t sf = (int32_t)Wc.a;
+            const int32_t c[kEll] = {sf + (int32_t)(int16_t)(cw.x & 0xffffu), sf + (int32_t)(int16_t)(cw.x >> 16),
+                                     sf + (int32_t)(int16_t)(cw.y & 0xffffu), sf + (int32_t)(int16_t)(cw.y >> 16)};
+            double x[kEll];
+#pragma unroll
+            for (int m = 0; m < kEll; ++m) x[m] = gat(c[m]);
+            asm volatile("" : "+d"(x[0]), "+d"(x[1]), "+d"(x[2]), "+d"(x[3]));
+            double acc = 0.0;
+            acc = __fma_rn(v01.x, x[0], acc);
+            acc = __fma_rn(v01.y, x[1], acc);
+            acc = __fma_rn(v23.x, x[2], acc);
+            acc = __fma_rn(v23.y, x[3], acc);
+            acc = overflow_sum(A.zt, Wc.a - A.hoff, acc, gat);
+            A.t[Wc.a] = __ddiv_rn(acc, pv);
+            rn[Wc.a] = rnew;
+            v = __dmul_rn(rnew, rnew);
+        }
+        v = warp_tree(v);
+        if (lane == 0) ws[(k - k0) * kWarps + warp] = v;
+        Wc = Wn;
+    }
+}
+
 #ifndef PCG_MINB_K2
 #define PCG_MINB_K2 4            // register budgets: resident 256-thread blocks per SM ptxas targets
 #endif
@@ -1050,7 +1144,12 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
         return v;
     };
     if (A.sched2) {
-        sched_units(A, A.sched2, A.soff2, ws, body);
+        if constexpr (DQ == -3) {
+            __shared__ K2Stage st[2];
+            k2_sched_staged(A, par, alpha, ws, st);
+        } else {
+            sched_units(A, A.sched2, A.soff2, ws, body);
+        }
         TL(1, 4);
         finish_sched(A, A.sched2, A.soff2, ws, A.partial[1]);
         TL(1, 5);
@@ -1985,6 +2084,7 @@ void configure_kernels(KArgs& A, int sms) {
     allow_smem(k3_ainv_kernel<0>, row_smem(A, A.g_k3, 1));
     allow_smem(k2_ainv_kernel<-1>, row_smem(A, A.g_k2, 1));
     allow_smem(k2_ainv_kernel<-2>, row_smem(A, A.g_k2, 1));
+    allow_smem(k2_ainv_kernel<-3>, row_smem(A, A.g_k2, 1) + 2 * sizeof(K2Stage));
     allow_smem(k3_ainv_kernel<-2>, row_smem(A, A.g_k3, 1));
     allow_smem(k3_ainv_kernel<-1>, row_smem(A, A.g_k3, 1));
     allow_smem(k2_ainv_kernel<4>, row_smem(A, A.g_k2, 1));
@@ -2052,6 +2152,7 @@ void launch_k2_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
     else if (A.dia_q > 4) launch_pdl(A, k2_ainv_kernel<8>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else if (A.dia_q > 0) launch_pdl(A, k2_ainv_kernel<4>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else if (A.use_sz) launch_pdl(A, k2_ainv_kernel<-2>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
+    else if (A.zt.col16 && A.stage2 && A.sched2) launch_pdl(A, k2_ainv_kernel<-3>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else if (A.zt.col16) launch_pdl(A, k2_ainv_kernel<-1>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else launch_pdl(A, k2_ainv_kernel<0>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
 }

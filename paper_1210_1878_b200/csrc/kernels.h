@@ -92,6 +92,7 @@ struct KArgs {
     // consumer kernel forms the canonical final sum it needs (K1: (s, r) -> beta, K2: (d, q) ->
     // alpha) and K3's block 0 does the history / stop test from K2's (r, r) at its start.
     int32_t redundant;
+    int32_t stage2;                   // K2's scheduled walk through the per-thread cp.async double buffer
     void* l2_base;                    // persisting L2 access-policy window of the iteration kernels
     size_t l2_bytes;                  // (0: none)
     float l2_ratio;

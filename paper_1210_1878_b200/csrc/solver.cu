@@ -11,6 +11,7 @@
 #include <functional>
 #include <string>
 #include <vector>
+#include <type_traits>
 
 #include "internal.h"
 #include "kernels.h"
@@ -36,6 +37,8 @@ struct pcg_ctx {
     uint32_t* rowdone = nullptr;       // K23 row flags
     double* hot = nullptr;             // the eight per-iteration vectors, contiguous
     size_t hot_bytes = 0;
+    char* ovf_base = nullptr;          // Z / Z^T overflow arrays, directly in front of `hot`
+    size_t ovf_bytes = 0;
     double* dia = nullptr;             // FSAI DIA diagonals
     int32_t *sched2 = nullptr, *soff2 = nullptr, *sched3 = nullptr, *soff3 = nullptr;   // static schedules
     double *x = nullptr, *b = nullptr, *q = nullptr, *t = nullptr, *s = nullptr, *r[2] = {}, *d[2] = {};
@@ -535,13 +538,11 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         if (Status s = upload(c, c->zt_val, P.ZT.val); !s) return s;
         if (Status s = upload(c, c->zt_col, P.ZT.col); !s) return s;
         if (Status s = upload(c, c->zt_ooff, P.ZT.ovf.off); !s) return s;
-        if (Status s = upload(c, c->zt_oval, P.ZT.ovf.val); !s) return s;
-        if (Status s = upload(c, c->zt_ocol, P.ZT.ovf.col); !s) return s;
+
         if (Status s = upload(c, c->z_val, P.Z.val); !s) return s;
         if (Status s = upload(c, c->z_col, P.Z.col); !s) return s;
         if (Status s = upload(c, c->z_ooff, P.Z.ovf.off); !s) return s;
-        if (Status s = upload(c, c->z_oval, P.Z.ovf.val); !s) return s;
-        if (Status s = upload(c, c->z_ocol, P.Z.ovf.col); !s) return s;
+
         // int16 slot offsets relative to the element's own array index (PCG_COL16=0 disables)
         const char* ce = getenv("PCG_COL16");
         if (!(ce && atoi(ce) == 0) && P.dia_q == 0) {
@@ -575,13 +576,36 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     // The eight per-iteration vectors live in one block, in the order of their passes per
     // iteration (r: 3, q, t, s, d, x: 2), so one L2 access-policy window can keep them resident
     // (DESIGN.md §4): only the static arrays (Z, Z^T, pivots, cE, cN) then stream from HBM.
+    // The overflow rows of Z and Z^T (the pole rows' long E-W tails, read in dependent rounds
+    // on K2's / K3's critical path) go in front of the vectors, so the window can cover them too.
     {
-        double* hot = nullptr;
-        if (Status s = dalloc(c, hot, 8 * nel); !s) return s;
+        auto rup = [](size_t b) { return (b + 255) / 256 * 256; };
+        const size_t b_ztv = rup(P.ZT.ovf.val.size() * sizeof(double)), b_ztc = rup(P.ZT.ovf.col.size() * sizeof(int32_t));
+        const size_t b_zv = rup(P.Z.ovf.val.size() * sizeof(double)), b_zc = rup(P.Z.ovf.col.size() * sizeof(int32_t));
+        const size_t ovf = P.factored() ? b_ztv + b_ztc + b_zv + b_zc : 0;
+        const size_t vb = (size_t)nel * sizeof(double);
+        char* blk = nullptr;
+        if (Status s = dalloc(c, blk, (int64_t)(ovf + 8 * vb)); !s) return s;
+        if (P.factored()) {
+            char* at = blk;
+            auto put = [&](auto*& dst, const auto& h, size_t bytes) -> Status {
+                dst = reinterpret_cast<std::remove_reference_t<decltype(dst)>>(at);
+                if (!h.empty()) CU(cudaMemcpy(at, h.data(), h.size() * sizeof(h[0]), cudaMemcpyHostToDevice));
+                at += bytes;
+                return Status::ok();
+            };
+            if (Status s = put(c->zt_oval, P.ZT.ovf.val, b_ztv); !s) return s;
+            if (Status s = put(c->zt_ocol, P.ZT.ovf.col, b_ztc); !s) return s;
+            if (Status s = put(c->z_oval, P.Z.ovf.val, b_zv); !s) return s;
+            if (Status s = put(c->z_ocol, P.Z.ovf.col, b_zc); !s) return s;
+        }
+        double* hot = reinterpret_cast<double*>(blk + ovf);
         double** order[] = {&c->r[0], &c->r[1], &c->q, &c->t, &c->s, &c->d[0], &c->d[1], &c->x};
         for (int k = 0; k < 8; ++k) *order[k] = hot + (int64_t)k * nel;
         c->hot = hot;
-        c->hot_bytes = (size_t)8 * (size_t)nel * sizeof(double);
+        c->hot_bytes = 8 * vb;
+        c->ovf_base = blk;
+        c->ovf_bytes = ovf;
     }
     if (Status s = dalloc(c, c->b, nel); !s) return s;
     if (Status s = dalloc(c, c->gath, 4 * std::max(1, P.nranks)); !s) return s;
@@ -701,20 +725,26 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         // only shrinks the L2 left to everything else); PCG_L2PERSIST=2 forces it
         const bool fits = (size_t)maxp >= 4 * (c->hot_bytes / 8);
         if (!(le && atoi(le) == 0) && (fits || (le && atoi(le) == 2)) && maxp > 0 && maxw > 0 && c->hot_bytes > 0) {
-            size_t setaside = std::min<size_t>((size_t)maxp, c->hot_bytes);
+            size_t setaside = std::min<size_t>((size_t)maxp, c->hot_bytes + c->ovf_bytes);
             size_t cur = 0;
             cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
             if (cur < setaside) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside);
             cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
             cudaGetLastError();
             if (cur > 0) {
-                A.l2_base = c->hot;
-                // the first ceil(set-aside / vector) vectors (cfg4: 7 of 8, hit ratio 0.98; measured
-                // 84.5 us/iteration against 86.5 with all 8 at ratio 0.86 and 90.3 without a window)
+                // vectors: the first ceil(rest / vector) (cfg4 without the overflow arrays: 7 of 8,
+                // hit ratio 0.98; measured 84.5 us/iteration against 86.5 with all 8 at ratio 0.86
+                // and 90.3 without a window)
                 const size_t vb = c->hot_bytes / 8;
-                int nv = (int)std::min<size_t>(8, (cur + vb - 1) / vb);
+                // PCG_L2OVF=1: the overflow arrays first, then ceil(rest / vector) vectors (measured
+                // equal at cfg4: 80.4 against 80.3 us/iteration with 7 vectors and no overflow arrays)
+                const char* oe = getenv("PCG_L2OVF");
+                const size_t ov = (oe && atoi(oe) != 0) ? c->ovf_bytes : 0;
+                const size_t rest = cur > ov ? cur - ov : 0;
+                int nv = (int)std::min<size_t>(8, (rest + vb - 1) / vb);
                 if (const char* ve = getenv("PCG_L2VECS")) nv = std::max(1, std::min(8, atoi(ve)));
-                A.l2_bytes = std::min<size_t>((size_t)maxw, (size_t)nv * vb);
+                A.l2_base = ov ? (void*)(reinterpret_cast<char*>(c->hot) - ov) : (void*)c->hot;
+                A.l2_bytes = std::min<size_t>((size_t)maxw, ov + (size_t)nv * vb);
                 A.l2_ratio = (float)std::min(1.0, (double)cur / (double)A.l2_bytes);
                 if (const char* re = getenv("PCG_L2RATIO")) A.l2_ratio = (float)atof(re);
             }
@@ -756,6 +786,8 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         const char* re = getenv("PCG_REDUNDANT");
         A.redundant = re ? atoi(re) != 0 : 1;
     }
+    A.stage2 = 0;
+    if (const char* se = getenv("PCG_STAGE2")) A.stage2 = atoi(se) != 0;
     // algorithmic bytes per launch: N_o ocean points, z off-diagonals per column
     const double No = (double)P.n_owned, z = No > 0 ? (double)P.nnz_off / No : 0.0;
     c->bytes_k[0] = 64.0 * No;
