@@ -82,6 +82,7 @@ struct Plan {
     int32_t nloc = 0, pitch = 0;
     int32_t halo = 1;              // halo grid rows on each side of the owned rows
     int32_t halo_w = 0;            // halo-AINV across ranks: q / r rows received from the south
+    int32_t halo_w_send = 0;       // ... q / r rows sent to the northern neighbour (= its halo_w)
     int32_t halo_t = 0;            // halo-AINV across ranks: t rows received from the north
     int32_t halo_t_send = 0;       // ... t rows the southern neighbour needs from this rank
     pcg_precond precond = PCG_PRECOND_AINV;

@@ -474,8 +474,17 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             for (int64_t e = blocks[0].colptr[q]; e < blocks[0].colptr[q + 1]; ++e)
                 if (blocks[0].row_g[e] < (int64_t)P.jb * ni)
                     w_eff = std::max(w_eff, P.jb - (int32_t)(blocks[0].row_g[e] / ni));
+    // rows of q / r this rank SENDS north: the southern extent of the northern neighbour's first
+    // columns, which this rank recomputed bitwise in `north` (same index set as the neighbour's
+    // block), so sender and receiver agree on the message size without communicating
+    int32_t w_send = 0;
+    if (have_north)
+        for (size_t q = 0; q < north.col_g.size(); ++q)
+            for (int64_t e = north.colptr[q]; e < north.colptr[q + 1]; ++e)
+                if (north.row_g[e] < (int64_t)P.je * ni) w_send = std::max(w_send, P.je - (int32_t)(north.row_g[e] / ni));
     if (halo_x) P.halo = std::max({P.halo, w_eff, reach});
     P.halo_w = halo_x ? std::max(1, w_eff) : 0;
+    P.halo_w_send = halo_x ? std::max(1, w_send) : 0;
     P.halo_t = reach;
     P.halo_t_send = reach_s;
     build_coeff_arrays();

@@ -148,10 +148,11 @@ Status exch_halo_ainv(pcg_ctx* c, bool qr, bool t, bool with_allgather, int par)
     const size_t pt = (size_t)P.pitch, H = (size_t)P.halo, w = (size_t)P.halo_w;
     NC(ncclGroupStart());
     if (with_allgather) NC(ncclAllGather((const void*)c->sc->loc, (void*)c->gath, 4, ncclDouble, c->comm, c->st));
-    if (qr && w > 0)
+    const size_t ws = (size_t)P.halo_w_send;
+    if (qr && (w > 0 || ws > 0))
         for (double* arr : {c->q, c->r[par]}) {
-            if (P.rank < P.nranks - 1)
-                NC(ncclSend(arr + (H + P.nloc - w) * pt, w * pt, ncclDouble, P.rank + 1, c->comm, c->st));
+            if (P.rank < P.nranks - 1 && ws > 0)
+                NC(ncclSend(arr + (H + P.nloc - ws) * pt, ws * pt, ncclDouble, P.rank + 1, c->comm, c->st));
             if (P.rank > 0) NC(ncclRecv(arr + (H - w) * pt, w * pt, ncclDouble, P.rank - 1, c->comm, c->st));
         }
     if (t) {
@@ -270,6 +271,8 @@ Status local_exchange(const std::vector<pcg_ctx*>& cs, Ex ex, cudaStream_t st, i
             const size_t nl = (size_t)lo->plan.nloc;
             if (ex != Ex::HaloT) {
                 const size_t w = (size_t)up->plan.halo_w;
+                if (lo->plan.halo_w_send != up->plan.halo_w)     // the NCCL path sends halo_w_send rows
+                    return Status::err(PCG_ERR_ARG, "internal: q / r halo rows sent != rows expected");
                 if (w > 0) {
                     CU(cudaMemcpyAsync(up->q + (Hu - w) * pt, lo->q + (Hl + nl - w) * pt, w * pt * sizeof(double), cudaMemcpyDeviceToDevice, st));
                     CU(cudaMemcpyAsync(up->r[par] + (Hu - w) * pt, lo->r[par] + (Hl + nl - w) * pt, w * pt * sizeof(double), cudaMemcpyDeviceToDevice, st));
