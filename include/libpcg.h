@@ -195,6 +195,13 @@ pcg_status pcg_apply_operator(pcg_ctx* ctx, const double* x, double* y);
  * Single rank only (PCG_ERR_ARG otherwise). */
 pcg_status pcg_apply_preconditioner(pcg_ctx* ctx, const double* r, double* s);
 
+/* NEMO's first guess for the next time step's solve (Alg. 1 l.1 "x0 = 2D^{t-1}",
+ * read as the extrapolation 2 D^t - D^{t-1} of NEMO's solver, R27):
+ * x0[e] = 2 x_t[e] - x_tm1[e] (2 x_t is exact, one IEEE subtraction) on this rank's rows.
+ * x_t, x_tm1, x0: DEVICE [rows][ni]; x0 may alias either input.  Ordered after the context's
+ * user stream, returns when done.  Used by the time-stepping driver. */
+pcg_status pcg_extrapolate(pcg_ctx* ctx, const double* x_t, const double* x_tm1, double* x0);
+
 /* Documented row-block split: with cum[j] = ocean points in rows < j and
  * N = cum[nj], row_begin[p] = min{ j : cum[j]*parts >= p*N } (forced strictly increasing),
  * row_begin[0] = 0, row_begin[parts] = nj.  row_begin has parts+1 entries (host).

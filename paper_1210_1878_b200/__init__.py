@@ -64,7 +64,7 @@ class Report(C.Structure):
 
 
 EXPORTS = ["pcg_setup", "pcg_solve", "pcg_solve_host", "pcg_solve_local_ranks", "pcg_free", "pcg_last_error", "pcg_apply_operator",
-           "pcg_apply_preconditioner", "pcg_partition", "pcg_layout", "pcg_kernel_times", "pcg_device_bytes",
+           "pcg_apply_preconditioner", "pcg_extrapolate", "pcg_partition", "pcg_layout", "pcg_kernel_times", "pcg_device_bytes",
            "pcg_plan_build", "pcg_plan_free", "pcg_plan_counts", "pcg_plan_export_zhat",
            "pcg_comm_unique_id", "pcg_comm_init_rank", "pcg_comm_destroy"]
 
@@ -89,6 +89,7 @@ def lib():
     L.pcg_last_error.argtypes = [vp]; L.pcg_last_error.restype = C.c_char_p
     L.pcg_apply_operator.argtypes = [vp, vp, vp]
     L.pcg_apply_preconditioner.argtypes = [vp, vp, vp]
+    L.pcg_extrapolate.argtypes = [vp, vp, vp, vp]
     L.pcg_partition.argtypes = [i32, i32, vp, i32, vp]
     L.pcg_layout.argtypes = [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]
     L.pcg_kernel_times.argtypes = [vp, i32, vp, vp]
@@ -284,6 +285,13 @@ class Solver:
         s = torch.empty_like(r) if s is None else s
         _check(lib().pcg_apply_preconditioner(self._h, _ptr(r), _ptr(s)), self._h, "pcg_apply_preconditioner")
         return s
+
+    def extrapolate(self, x_t, x_tm1, x0=None):
+        """NEMO's first guess 2 x_t - x_tm1 (pcg_extrapolate; torch CUDA float64 [rows][ni])."""
+        import torch
+        x0 = torch.empty_like(x_t) if x0 is None else x0
+        _check(lib().pcg_extrapolate(self._h, _ptr(x_t), _ptr(x_tm1), _ptr(x0)), self._h, "pcg_extrapolate")
+        return x0
 
     def kernel_times(self, n_iter=50):
         ms = np.zeros(4)

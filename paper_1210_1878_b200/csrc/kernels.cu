@@ -1977,6 +1977,13 @@ __global__ void __launch_bounds__(kBlock) apply_kernel(const KArgs A, const doub
     y[W.a] = land ? 0.0 : ax;
 }
 
+// x0 = 2 x_t - x_tm1 on n contiguous elements (pcg_extrapolate; 2 x_t is exact)
+__global__ void __launch_bounds__(kBlock) extrapolate_kernel(const double* __restrict__ xt, const double* __restrict__ xm,
+                                                             double* __restrict__ x0, int64_t n) {
+    for (int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x; e < n; e += (int64_t)gridDim.x * kBlock)
+        x0[e] = __dadd_rn(__dmul_rn(2.0, xt[e]), -xm[e]);
+}
+
 __global__ void scalar_kernel(const KArgs A, const int step) {
     DevScalars* sc = A.sc;
     const int P = A.nranks;
@@ -2185,6 +2192,10 @@ void launch_apply(const KArgs& A, const double* x, double* y, cudaStream_t st) {
     apply_kernel<<<(unsigned)grid_blocks(A), kBlock, 0, st>>>(A, x, y);
 }
 void launch_scalar(const KArgs& A, int step, cudaStream_t st) { scalar_kernel<<<1, 1, 0, st>>>(A, step); }
+void launch_extrapolate(const double* xt, const double* xm, double* x0, int64_t n, cudaStream_t st) {
+    const int64_t G = std::max<int64_t>(1, std::min<int64_t>((n + kBlock - 1) / kBlock, 148 * 8));
+    extrapolate_kernel<<<(unsigned)G, kBlock, 0, st>>>(xt, xm, x0, n);
+}
 cudaError_t launch_loop(const KArgs& A, cudaStream_t st) {
     void* args[] = {(void*)&A};
     const void* fn = A.sigma ? (const void*)loop_kernel<true> : (const void*)loop_kernel<false>;

@@ -115,6 +115,7 @@ void launch_apply(const KArgs& A, const double* x_arr, double* y_arr, cudaStream
 enum ScalarStep : int32_t { kSsBB = 0, kSsGamma = 1, kSsInit = 2, kSsIter = 3, kSsTrue = 4 };
 void launch_scalar(const KArgs& A, int step, cudaStream_t st);
 void launch_set_cond(cudaGraphConditionalHandle h, cudaStream_t st);
+void launch_extrapolate(const double* xt, const double* xm, double* x0, int64_t n, cudaStream_t st);
 void configure_kernels(KArgs& A, int sms);
 cudaError_t launch_loop(const KArgs& A, cudaStream_t st);   // whole PCG loop, cooperative (1 rank)
 

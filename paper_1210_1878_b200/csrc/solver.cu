@@ -907,6 +907,22 @@ pcg_status pcg_apply_operator(pcg_ctx* c, const double* x, double* y) {
     return s ? PCG_OK : fail(c, s);
 }
 
+pcg_status pcg_extrapolate(pcg_ctx* c, const double* xt, const double* xm, double* x0) {
+    if (!c || !xt || !xm || !x0) { set_thread_error("pcg_extrapolate: NULL argument"); return PCG_ERR_ARG; }
+    auto body = [&]() -> Status {
+        const Plan& P = c->plan;
+        CU(cudaSetDevice(c->device));
+        CU(cudaEventRecord(c->ev_in, c->user_stream));
+        CU(cudaStreamWaitEvent(c->st, c->ev_in, 0));
+        launch_extrapolate(xt, xm, x0, (int64_t)P.nloc * P.ni, c->st);
+        CU(cudaGetLastError());
+        CU(cudaStreamSynchronize(c->st));
+        return Status::ok();
+    };
+    Status s = body();
+    return s ? PCG_OK : fail(c, s);
+}
+
 pcg_status pcg_apply_preconditioner(pcg_ctx* c, const double* r, double* sout) {
     if (!c || !r || !sout) { set_thread_error("pcg_apply_preconditioner: NULL argument"); return PCG_ERR_ARG; }
     auto body = [&]() -> Status {

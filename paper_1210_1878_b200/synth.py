@@ -186,3 +186,22 @@ def xstar(p: Problem, seed: int = 0) -> np.ndarray:
 def random_rhs(p: Problem, seed: int = 0) -> np.ndarray:
     """b ~ N(0,1) on ocean points (grid layout, 0 on land)."""
     return xstar(p, seed)
+
+
+def forcing_series(p: Problem, nsteps: int, seed: int = 5, period: float = 40.0) -> list:
+    """Time series of target fields D*(t_n), n = 0..nsteps-1, for the time-stepping driver
+    (SURVEY §8f NEXT-4): D*(t) = cos(2 pi t / period) X1 + sin(2 pi t / period) X2 with X1, X2
+    smooth fields (SURVEY A.1 `smooth`, centred), zero on land -- a smoothly evolving
+    sea-surface trend, as D^n evolves between NEMO time steps.  Inputs only: the driver forms
+    b^n = A D*(t_n) through the library."""
+    rng = np.random.default_rng(seed)
+    X1 = smooth(p.ni, p.nj, rng) - 0.5
+    X2 = smooth(p.ni, p.nj, rng) - 0.5
+    land = p.mask == 0
+    out = []
+    for n in range(nsteps):
+        w = 2.0 * math.pi * n / period
+        f = math.cos(w) * X1 + math.sin(w) * X2
+        f[land] = 0.0
+        out.append(np.ascontiguousarray(f))
+    return out

@@ -419,3 +419,42 @@ def test_local_ranks_global_z(P):
                      block=R.block)
     assert abs(k - one.iterations) <= 2             # only the rank-ordered dot products differ
     R.close()
+
+
+# ------------------------------------------------------------ time-stepping driver (NEXT-4)
+def test_extrapolate_kernel():
+    p = synth.config("cfg2")
+    S = pcg.Solver(p.cE, p.cN, p.mask, tau=TAU)
+    rng = np.random.default_rng(3)
+    a, b = rng.standard_normal((p.nj, p.ni)), rng.standard_normal((p.nj, p.ni))
+    x0 = host(S.extrapolate(dev(a), dev(b)))
+    assert np.array_equal(x0, 2.0 * a - b)
+    S.close()
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_timestep_driver_bitwise(name):
+    """One setup, five time steps, NEMO's first guess 2 D^n - D^{n-1} formed on the device: every
+    step's D^{n+1} is bitwise the oracle's canonical PCG from the same first guess (computed on
+    the host from the oracle's own previous solutions), and warm starts need fewer iterations
+    than cold solves of the same right-hand sides."""
+    from paper_1210_1878_b200 import timestep
+    p = synth.config(name)
+    A, M, S = setup_pair(p)
+    st = timestep.Stepper(S, "extrapolate")
+    prev = cur = None
+    warm_its, cold_its = [], []
+    for n, f in enumerate(synth.forcing_series(p, 5)):
+        b = A.apply(A.from_grid(f))
+        x0 = None if cur is None else (cur if prev is None else 2.0 * cur - prev)
+        ref = oracle.pcg(A, b, "ainv", M, 1e-10, maxit=A.n, x0=x0, mode="canonical", pitch=S.pitch, block=S.block)
+        xg, k, rep = st.step(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
+        assert k == ref.iterations
+        assert np.array_equal(host(xg), A.to_grid(ref.x))
+        assert rep["converged"] == 1
+        prev, cur = cur, ref.x
+        warm_its.append(k)
+        cold_its.append(oracle.pcg(A, b, "ainv", M, 1e-10, maxit=A.n, mode="canonical", pitch=S.pitch,
+                                   block=S.block).iterations)
+    assert sum(warm_its[2:]) < sum(cold_its[2:])
+    S.close()
