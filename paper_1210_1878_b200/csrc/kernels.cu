@@ -479,6 +479,33 @@ __device__ __forceinline__ void k1_strip(const KArgs& A, int par, int64_t st, do
     if (valid && j1 == A.nloc) dnew[a] = dC;       // northern halo row (multi-rank)
 }
 
+// beta of K1 (both K1 forms).  Redundant-sum mode: rho = (s, r) of K3's partials formed by every
+// block, beta = rho / rho of the last iteration, block 0 keeps the books; false = breakdown (stop).
+__device__ __forceinline__ bool k1_beta(const KArgs& A, int par, double& beta) {
+    if (!A.redundant) {
+        beta = __ddiv_rn(A.sc->rho, A.sc->rho_prev);
+        return true;
+    }
+    const double rho = final_sum_all<PCG_RED_NB>(A.partial[2], n_units(A));
+    if (!isfinite(rho)) {                                // fin_iter's breakdown on (s, r)
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            const int k = A.sc->k;
+            if (k < A.hist_cap) A.hist[k] = NAN;
+            stop(A, kStBreakdown);
+        }
+        return false;
+    }
+    beta = __ddiv_rn(rho, A.sc->rhop[par ^ 1]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        A.sc->rhop[par] = rho;
+        A.sc->rho = rho;
+        A.sc->xpend = 0;                                   // this kernel does x += alpha_prev d_old
+        A.sc->ticket[1] = 0;                               // K2's / K3's tickets (both finished)
+        A.sc->ticket[2] = 0;
+    }
+    return true;
+}
+
 #ifndef PCG_MINB_K1
 #define PCG_MINB_K1 4
 #endif
@@ -499,7 +526,9 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
     extern __shared__ double ws[];
     __shared__ double wrow[kMaxRowsK1][kWarps];
     __shared__ long long s_next;
-    const double beta = __ddiv_rn(A.sc->rho, A.sc->rho_prev), alpha = A.sc->alpha;
+    double beta;
+    if (!k1_beta(A, par, beta)) return;
+    const double alpha = A.sc->alpha;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int32_t nby = (A.nloc + A.rpb - 1) / A.rpb;
     const int64_t S = (int64_t)nby * A.nbx;
@@ -553,6 +582,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
     }
     pdl_trigger();
     TL(0, 2);
+    if (A.redundant) return;                           // (d, q) is summed by K2's blocks
     if (count_block(&A.sc->counter[0])) {
         const double tot = final_sum(A.partial[0], n_units(A));
         if (threadIdx.x == 0) {
@@ -634,28 +664,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1F) k1_flat_kernel(const KAr
     }
     double beta;
     const double alpha = A.sc->alpha;
-    if (A.redundant) {
-        // rho = (s, r) of K3's partials, formed by every block; beta = rho / rho of the last iteration
-        const double rho = final_sum_all<PCG_RED_NB>(A.partial[2], n_units(A));
-        if (!isfinite(rho)) {                            // fin_iter's breakdown on (s, r)
-            if (blockIdx.x == 0 && threadIdx.x == 0) {
-                const int k = A.sc->k;
-                if (k < A.hist_cap) A.hist[k] = NAN;
-                stop(A, kStBreakdown);
-            }
-            return;
-        }
-        beta = __ddiv_rn(rho, A.sc->rhop[par ^ 1]);
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            A.sc->rhop[par] = rho;
-            A.sc->rho = rho;
-            A.sc->xpend = 0;                               // this kernel does x += alpha_prev d_old
-            A.sc->ticket[1] = 0;                           // K2's / K3's tickets (both finished)
-            A.sc->ticket[2] = 0;
-        }
-    } else {
-        beta = __ddiv_rn(A.sc->rho, A.sc->rho_prev);
-    }
+    if (!k1_beta(A, par, beta)) return;
     bool last;
     if (A.redundant) {
         extern __shared__ double ws[];
