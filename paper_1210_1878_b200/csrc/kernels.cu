@@ -602,8 +602,26 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
 // ---- K1, row-segment form: one element per thread, units from the dynamic ticket ----------------
 // Same arithmetic as k1_strip (bitwise): d at the point and at its S/N neighbours recomputed from
 // s and d_old, E/W neighbours by shuffle (warp-edge lanes and the periodic seam load them).
+// loads of one K1 point (row-segment form), issued before any of its arithmetic
+struct K1Ld {
+    double doC, sC, dSo, sS, dNo, sN, cEp, cNr, cNs, xv;
+};
+__device__ __forceinline__ void k1_load(const KArgs& A, const Unit& W, int par, K1Ld& L) {
+    const double* __restrict__ dold = A.d[par];
+    const double* __restrict__ s = A.s;
+    const int64_t a = W.a, P = A.pitch;
+    if (W.valid) {
+        L.doC = dold[a]; L.sC = s[a];
+        L.dSo = dold[a - P]; L.sS = s[a - P]; L.dNo = dold[a + P]; L.sN = s[a + P];
+        L.cEp = A.cE[a]; L.cNr = A.cN[a]; L.cNs = A.cN[a - P]; L.xv = A.x[a];
+    } else {
+        L.doC = L.sC = L.dSo = L.sS = L.dNo = L.sN = L.cEp = L.cNr = L.cNs = L.xv = 0.0;
+    }
+}
+
+// arithmetic and stores of one K1 point from its loads
 template <bool SIGMA>
-__device__ __forceinline__ double k1_point(const KArgs& A, const Unit& W, int par, double beta, double alpha) {
+__device__ __forceinline__ double k1_compute(const KArgs& A, const Unit& W, int par, double beta, double alpha, const K1Ld& L) {
     const double* __restrict__ dold = A.d[par];
     double* __restrict__ dnew = A.d[par ^ 1];
     const double* __restrict__ s = A.s;
@@ -613,12 +631,11 @@ __device__ __forceinline__ double k1_point(const KArgs& A, const Unit& W, int pa
     const int64_t a = W.a;
     double dC = 0.0, dS = 0.0, dN = 0.0, doC = 0.0, cEp = 0.0, cNr = 0.0, cNs = 0.0, xv = 0.0;
     if (valid) {
-        doC = dold[a];
-        const double sC = s[a], dSo = dold[a - P], sS = s[a - P], dNo = dold[a + P], sN = s[a + P];
-        cEp = A.cE[a]; cNr = A.cN[a]; cNs = fabs(A.cN[a - P]); xv = A.x[a];
-        dC = __fma_rn(beta, doC, sC);
-        dS = __fma_rn(beta, dSo, sS);
-        dN = __fma_rn(beta, dNo, sN);
+        doC = L.doC;
+        cEp = L.cEp; cNr = L.cNr; cNs = fabs(L.cNs); xv = L.xv;
+        dC = __fma_rn(beta, doC, L.sC);
+        dS = __fma_rn(beta, L.dSo, L.sS);
+        dN = __fma_rn(beta, L.dNo, L.sN);
     }
     double dW = __shfl_up_sync(kFull, dC, 1);
     double dE = __shfl_down_sync(kFull, dC, 1);
@@ -649,6 +666,53 @@ __device__ __forceinline__ double k1_point(const KArgs& A, const Unit& W, int pa
     if (W.j == 0) dnew[a - P] = dS;                     // halo rows (multi-rank)
     if (W.j == A.nloc - 1) dnew[a + P] = dN;
     return __dmul_rn(dC, qv);
+}
+
+// K1, row-segment form: one element per thread, units from the dynamic ticket or a block stride.
+// Same arithmetic as k1_strip (bitwise): d at the point and at its S/N neighbours recomputed from
+// s and d_old, E/W neighbours by shuffle (warp-edge lanes and the periodic seam load them).
+template <bool SIGMA>
+__device__ __forceinline__ double k1_point(const KArgs& A, const Unit& W, int par, double beta, double alpha) {
+    K1Ld L;
+    k1_load(A, W, par, L);
+    return k1_compute<SIGMA>(A, W, par, beta, alpha, L);
+}
+
+#ifndef PCG_MINB_K1P
+#define PCG_MINB_K1P 3
+#endif
+// K1, row-segment form with two units per thread in flight (units u and u + G of the block
+// stride: both points' loads issued before either computes).  Redundant-sum mode only; same
+// units, slots and arithmetic as k1_flat_kernel's static walk (bitwise).
+template <bool SIGMA>
+__global__ void __launch_bounds__(kBlock, PCG_MINB_K1P) k1_pair_kernel(const KArgs A, const int par) {
+    pdl_wait();
+    if (!is_active(A)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (++A.sc->guard > A.sc->maxit + 2) {          // safety net for the WHILE node
+            A.sc->active = 0;
+            A.sc->status = kStBreakdown;
+            set_cond(A, 0);
+        }
+    }
+    double beta;
+    if (!k1_beta(A, par, beta)) return;
+    const double alpha = A.sc->alpha;
+    extern __shared__ double ws[];
+    const int64_t U = n_units(A), G = gridDim.x;
+    int k = 0;
+    for (int64_t u = blockIdx.x; u < U; u += 2 * G, k += 2) {
+        const Unit W0 = unit_of(A, u);
+        const bool two = u + G < U;
+        const Unit W1 = unit_of(A, two ? u + G : u);
+        K1Ld L0, L1;
+        k1_load(A, W0, par, L0);
+        if (two) k1_load(A, W1, par, L1);
+        put_warp_sum(ws, k, k1_compute<SIGMA>(A, W0, par, beta, alpha, L0));
+        if (two) put_warp_sum(ws, k + 1, k1_compute<SIGMA>(A, W1, par, beta, alpha, L1));
+    }
+    pdl_trigger();
+    finish_units<1>(A, ws, A.partial[0], nullptr, nullptr);
 }
 
 template <bool SIGMA>
@@ -2074,6 +2138,7 @@ void configure_kernels(KArgs& A, int sms) {
     A.landskip = A.ocean != nullptr;
     if (const char* e = getenv("PCG_LANDSKIP")) A.landskip = A.landskip && atoi(e) != 0;
     A.g_k1f = persistent_grid(k1_flat_kernel<false>, U, sms, 0);
+    A.g_k1p = persistent_grid(k1_pair_kernel<false>, U, sms, 0);
     A.tma = 0;                                         // measured no faster than the LDG path (r01)
     if (const char* e = getenv("PCG_TMA")) A.tma = atoi(e) != 0;
     {
@@ -2110,6 +2175,8 @@ void configure_kernels(KArgs& A, int sms) {
     allow_smem(k2_ainv_kernel<16>, row_smem(A, A.g_k2, 1));
     allow_smem(k3_ainv_kernel<16>, row_smem(A, A.g_k3, 1));
     allow_smem(k2_diag_kernel, row_smem(A, A.g_kd, 2));
+    allow_smem(k1_pair_kernel<false>, row_smem(A, A.g_k1p, 1));
+    allow_smem(k1_pair_kernel<true>, row_smem(A, A.g_k1p, 1));
     allow_smem(init_residual_kernel, row_smem(A, A.g_row, 1));
     allow_smem(true_residual_kernel, row_smem(A, A.g_row, 1));
 }
@@ -2147,6 +2214,12 @@ static void launch_pdl(const KArgs& A, void (*kern)(P...), int grid, int block, 
 }
 
 void launch_k1(const KArgs& A, int par, cudaStream_t st) {
+    if (A.k1flat == 3 && A.redundant) {
+        const size_t sm = row_smem(A, A.g_k1p, 1);
+        if (A.sigma) launch_pdl(A, k1_pair_kernel<true>, A.g_k1p, kBlock, sm, st, A, par);
+        else launch_pdl(A, k1_pair_kernel<false>, A.g_k1p, kBlock, sm, st, A, par);
+        return;
+    }
     if (A.k1flat) {
         const size_t sm = A.k1flat == 2 ? row_smem(A, A.g_k1f, 1) : 0;
         if (A.sigma) launch_pdl(A, k1_flat_kernel<true>, A.g_k1f, kBlock, sm, st, A, par);

@@ -53,6 +53,7 @@ struct KArgs {
     int32_t tma, g_t2, g_t3;          // K2/K3 through the TMA bulk-copy pipeline; its grid sizes
     int32_t g_loop;                   // cooperative grid of the fused loop kernel
     int32_t k1flat, g_k1f;            // K1 in row-segment form (one element per thread)
+    int32_t g_k1p;                    // grid of the two-units-per-thread K1 (k1flat == 3)
     int32_t pdl;                      // programmatic dependent launch of the iteration kernels
     const int32_t* sched2;            // K2 scheduled static walk: unit list (NULL = dynamic tickets)
     const int32_t* soff2;             // [g_k2 + 1] offsets of each block's list

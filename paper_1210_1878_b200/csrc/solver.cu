@@ -785,7 +785,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     }   // kernels: 0 = factored Z D^-1 Z^T (AINV, FSAI)
     // redundant-sum mode (kernels.h): one rank, the K1 row-segment form, K2 / K3 as two launches
     A.redundant = 0;
-    if (P.factored() && !c->multi && !A.fuse23 && (A.k1flat == 2 || (A.k1flat == 0 && !A.dynamic_k1)) && !A.tma) {
+    if (P.factored() && !c->multi && !A.fuse23 && (A.k1flat == 2 || A.k1flat == 3 || (A.k1flat == 0 && !A.dynamic_k1)) && !A.tma) {
         const char* re = getenv("PCG_REDUNDANT");
         A.redundant = re ? atoi(re) != 0 : 1;
     }

@@ -369,7 +369,7 @@ def test_local_ranks_pb2_bitwise():
 VARIANTS = {"k23": {"PCG_FUSE23": "1"}, "k23_lag": {"PCG_FUSE23": "1", "PCG_LAG23": "7"},
             "sz": {"PCG_SZ": "1"}, "sz_k23": {"PCG_SZ": "1", "PCG_FUSE23": "1"},
             "no_l2_window": {"PCG_L2PERSIST": "0"}, "stage2": {"PCG_STAGE2": "1"},
-            "k1_strips": {"PCG_K1FLAT": "0"}, "no_redundant": {"PCG_REDUNDANT": "0"}}
+            "k1_strips": {"PCG_K1FLAT": "0"}, "k1_pairs": {"PCG_K1FLAT": "3"}, "no_redundant": {"PCG_REDUNDANT": "0"}}
 
 
 @pytest.mark.parametrize("variant", sorted(VARIANTS))
