@@ -1902,6 +1902,180 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_LOOP) loop_kernel(const KArgs
     }
 }
 
+// ---- the whole PCG loop in ONE CTA with the vectors in shared memory (tiny grids) -------------
+// For grids whose eight vectors fit in shared memory (cfg1: 34 x 32 elements, 70 KB) the solve is
+// latency-bound: three grid barriers per iteration of the cooperative loop kernel cost more than
+// the arithmetic.  One block of 1024 threads holds x, r0, r1, d0, d1, q, t, s in shared memory,
+// its 32 warps walk the (unit, warp) items of each phase (a unit is a row segment of 256 columns:
+// the canonical partials), and the phases are separated by __syncthreads.  Same per-point arithmetic (k1_load/k1_compute,
+// the ELL rows), same unit partials, same canonical final sums as the other drivers -> bitwise.
+// Z, Z^T, pivots and coefficients stay in global memory (read-only, L1-resident at this size).
+constexpr int kTinyThreads = 1024;
+
+__device__ __forceinline__ Unit tiny_unit(const KArgs& A, int64_t u, int t256) {
+    Unit W;
+    W.bx = (int32_t)(u % A.nbx);
+    W.j = A.nloc - 1 - (int32_t)(u / A.nbx);
+    W.i = W.bx * kBlock + t256;
+    W.valid = W.i < A.ni;
+    W.inrow = W.i < A.pitch;
+    W.live = W.inrow;
+    W.a = (int64_t)(W.j + A.halo) * A.pitch + W.i;
+    return W;
+}
+
+// canonical final sum of G partials held in shared memory (thread t < 256 sums t, t+256, ...
+// left to right, then the block tree of final_sum), broadcast to every thread
+__device__ __forceinline__ double tiny_final(const double* p, int64_t G, double* bc) {
+    double acc = 0.0;
+    if (threadIdx.x < kBlock)
+        for (int64_t m = threadIdx.x; m < G; m += kBlock) acc = __dadd_rn(acc, p[m]);
+    const double v = block_tree(acc);
+    if (threadIdx.x == 0) *bc = v;
+    __syncthreads();
+    const double r = *bc;
+    __syncthreads();
+    return r;
+}
+
+// per-unit warp sums (ws[u][8]) -> unit partials p[m(u)] (second level of the unit's block tree)
+__device__ __forceinline__ void tiny_partials(const KArgs& A, const double* ws, double* p) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t U = n_units(A);
+    for (int64_t u = warp; u < U; u += kTinyThreads / 32) {
+        double w = lane < kWarps ? ws[u * kWarps + lane] : 0.0;
+        w = warp_tree(w);
+        if (lane == 0) p[(int64_t)(A.nloc - 1 - (int32_t)(u / A.nbx)) * A.nbx + (u % A.nbx)] = w;
+    }
+}
+
+template <bool SIGMA>
+__global__ void __launch_bounds__(kTinyThreads, 1) tiny_kernel(const KArgs G) {
+    extern __shared__ double smv[];
+    __shared__ KArgs A;                        // the kernel arguments with the vectors re-pointed
+    const int64_t NE = G.nel_all, U = n_units(G);
+    if (threadIdx.x == 0) {
+        A = G;
+        A.x = smv; A.r[0] = smv + NE; A.r[1] = smv + 2 * NE; A.d[0] = smv + 3 * NE; A.d[1] = smv + 4 * NE;
+        A.q = smv + 5 * NE; A.t = smv + 6 * NE; A.s = smv + 7 * NE;
+    }
+    double* part = smv + 8 * NE;               // 3 x U canonical partials
+    double* ws = part + 3 * U;                 // U x 8 warp sums of the current phase
+    double* bc = ws + U * kWarps;              // broadcast slot
+    auto gvec = [&](int v) -> double* {
+        switch (v) {
+            case 0: return G.x; case 1: return G.r[0]; case 2: return G.r[1]; case 3: return G.d[0];
+            case 4: return G.d[1]; case 5: return G.q; case 6: return G.t; default: return G.s;
+        }
+    };
+    for (int v = 0; v < 8; ++v) {
+        const double* src = gvec(v);
+        for (int64_t e = threadIdx.x; e < NE; e += kTinyThreads) smv[v * NE + e] = src[e];
+    }
+    __syncthreads();
+    DevScalars* sc = G.sc;
+    const bool lead = threadIdx.x == 0;
+    double rho = sc->rho, beta = sc->beta, alpha = sc->alpha;
+    const double nb = sc->nb, tol = sc->tol;
+    int k = sc->k, status = sc->status, xpend = 0;
+    const int maxit = sc->maxit;
+    bool active = sc->active != 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // work items: (unit, warp of the unit); the 32 warps of the block take them round-robin, so a
+    // narrow grid (pitch <= 256: one live warp per unit) does a whole phase in one round.  A warp
+    // of a unit with no column inside the row contributes the exact zero the 256-thread unit's
+    // idle warps would.
+    const int64_t NW = U * kWarps;
+    auto items = [&](auto&& body) {
+        for (int64_t it = warp; it < NW; it += kTinyThreads / 32) {
+            const int64_t u = it / kWarps;
+            const int w = (int)(it % kWarps);
+            double v = 0.0;
+            if ((int64_t)(u % A.nbx) * kBlock + 32 * w < A.pitch) v = warp_tree(body(tiny_unit(A, u, 32 * w + lane)));
+            if (lane == 0) ws[it] = v;
+        }
+    };
+    int par = 0;
+    while (active) {
+        // K1: d = s + beta d_old ; x += alpha_prev d_old ; q = A d ; (d, q)
+        items([&](const Unit& W) {
+            K1Ld L;
+            k1_load(A, W, par, L);
+            return k1_compute<SIGMA>(A, W, par, beta, alpha, L);
+        });
+        xpend = 0;
+        __syncthreads();
+        tiny_partials(A, ws, part);
+        __syncthreads();
+        const double gamma = tiny_final(part, U, bc);
+        if (!(gamma > 0.0) || !isfinite(gamma)) { status = kStBreakdown; break; }
+        alpha = __ddiv_rn(rho, gamma);
+        // K2: r -= alpha q ; t = (Z^T r) / Dhat ; (r, r)
+        {
+            const double* ro = A.r[par];
+            double* rn = A.r[par ^ 1];
+            const double* q = A.q;
+            auto gat = [&](int64_t g) { return __fma_rn(-alpha, q[g], ro[g]); };
+            items([&](const Unit& W) {
+                double v = 0.0;
+                if (W.inrow) {
+                    const double rnew = __fma_rn(-alpha, q[W.a], ro[W.a]);
+                    const double acc = A.zt.col16 ? ell_row16(A.zt, W.a - A.hoff, W.a, gat) : ell_row(A.zt, W.a - A.hoff, gat);
+                    A.t[W.a] = __ddiv_rn(acc, A.piv[W.a]);
+                    rn[W.a] = rnew;
+                    v = __dmul_rn(rnew, rnew);
+                }
+                return v;
+            });
+        }
+        __syncthreads();
+        tiny_partials(A, ws, part + U);
+        __syncthreads();
+        // K3: s = Z t ; (s, r)
+        {
+            const double* rn = A.r[par ^ 1];
+            const double* t = A.t;
+            auto gat = [&](int64_t g) { return t[g]; };
+            items([&](const Unit& W) {
+                double v = 0.0;
+                if (W.inrow) {
+                    const double acc = A.z.col16 ? ell_row16(A.z, W.a - A.hoff, W.a, gat) : ell_row(A.z, W.a - A.hoff, gat);
+                    A.s[W.a] = acc;
+                    v = __dmul_rn(acc, rn[W.a]);
+                }
+                return v;
+            });
+        }
+        __syncthreads();
+        tiny_partials(A, ws, part + 2 * U);
+        __syncthreads();
+        const double rr = tiny_final(part + U, U, bc);
+        const double rho_new = tiny_final(part + 2 * U, U, bc);
+        k += 1;
+        xpend = 1;
+        if (!isfinite(rho_new) || !isfinite(rr)) {
+            if (lead && k < G.hist_cap) G.hist[k] = NAN;
+            status = kStBreakdown;
+            break;
+        }
+        beta = __ddiv_rn(rho_new, rho);
+        rho = rho_new;
+        const double h = __ddiv_rn(__dsqrt_rn(rr), nb);
+        if (lead && k < G.hist_cap) G.hist[k] = h;
+        active = (h > tol) && (k < maxit);
+        par ^= 1;
+    }
+    __syncthreads();
+    for (int v = 0; v < 8; ++v) {
+        double* dst = gvec(v);
+        for (int64_t e = threadIdx.x; e < NE; e += kTinyThreads) dst[e] = smv[v * NE + e];
+    }
+    if (lead) {
+        sc->k = k; sc->alpha = alpha; sc->beta = beta; sc->rho = rho;
+        sc->xpend = xpend; sc->status = status; sc->active = 0;
+    }
+}
+
 // ---- K2 (Jacobi / none): r -= alpha q ; s = r / A_pp (or r) ; (r, r), (s, r) ---------------
 __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const int par, const int init,
                                                          const int none) {
@@ -2278,7 +2452,27 @@ void launch_extrapolate(const double* xt, const double* xm, double* x0, int64_t 
     const int64_t G = std::max<int64_t>(1, std::min<int64_t>((n + kBlock - 1) / kBlock, 148 * 8));
     extrapolate_kernel<<<(unsigned)G, kBlock, 0, st>>>(xt, xm, x0, n);
 }
+size_t tiny_smem_bytes(const KArgs& A) {
+    const int64_t U = (int64_t)A.nloc * A.nbx;
+    return (size_t)(8 * A.nel_all + 3 * U + U * kWarps + 1) * sizeof(double);
+}
+bool tiny_eligible(const KArgs& A) {
+    if (A.precond != 0 || A.dia_q != 0 || A.nranks != 1 || A.multi) return false;
+    // opt-in (PCG_TINY=1): measured 31.4 against 16.9 us/iteration for the cooperative loop at cfg1
+    // -- one SM issues the whole iteration (82 k warp instructions, 5.6 M per solve), where the
+    // loop kernel spreads it over 148 SMs and pays three grid barriers instead
+    const char* e = getenv("PCG_TINY");
+    if (!(e && atoi(e) != 0)) return false;
+    return tiny_smem_bytes(A) <= 200 * 1024;
+}
 cudaError_t launch_loop(const KArgs& A, cudaStream_t st) {
+    if (tiny_eligible(A)) {
+        const size_t sm = tiny_smem_bytes(A);
+        auto fn = A.sigma ? tiny_kernel<true> : tiny_kernel<false>;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        fn<<<1, kTinyThreads, sm, st>>>(A);
+        return cudaGetLastError();
+    }
     void* args[] = {(void*)&A};
     const void* fn = A.sigma ? (const void*)loop_kernel<true> : (const void*)loop_kernel<false>;
     return cudaLaunchCooperativeKernel(fn, dim3(A.g_loop), dim3(kBlock), args, 0, st);

@@ -459,3 +459,23 @@ def test_timestep_driver_bitwise(name):
                                    block=S.block).iterations)
     assert sum(warm_its[2:]) < sum(cold_its[2:])
     S.close()
+
+
+@pytest.mark.parametrize("kind", ["cfg1", "sigma", "nonperiodic", "ragged"])
+def test_tiny_cta_driver_bitwise(kind, monkeypatch):
+    """Grids whose vectors fit in shared memory can run the whole loop in one CTA (tiny_kernel,
+    PCG_TINY=1, opt-in): bitwise the oracle's canonical PCG and the cooperative loop kernel."""
+    monkeypatch.setenv("PCG_TINY", "1")
+    if kind == "cfg1":
+        p = synth.config("cfg1")
+    else:
+        p = synth.random_grid(45 if kind == "ragged" else 30, 13, 3, periodic=kind != "nonperiodic",
+                              sigma=kind == "sigma")
+    A, S, ref, x, k, hist, rep, _ = _canonical_pair(p, "ainv", 1e-10)
+    assert k == ref.iterations and np.array_equal(hist, ref.hist)
+    assert np.array_equal(x, A.to_grid(ref.x))
+    b = dev(A.to_grid(rhs(A, p)))
+    monkeypatch.setenv("PCG_TINY", "0")
+    x2, k2, h2, _ = S.solve(b, tol=1e-10, maxit=A.n)
+    assert k2 == k and np.array_equal(h2, hist) and np.array_equal(host(x2), x)
+    S.close()
