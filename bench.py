@@ -61,8 +61,9 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index = index
-        self.samples = []
+        self.samples = []              # (host time, fields)
         self.proc = None
+        self.window = None             # (t0, t1) host times of the timed region
 
     def __enter__(self):
         q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
@@ -82,7 +83,7 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) >= 7:
-                self.samples.append(parts)
+                self.samples.append((time.perf_counter(), parts))
 
     def __exit__(self, *a):
         if self.proc is not None:
@@ -93,14 +94,20 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.samples:
+        """Clocks over the samples taken inside the timed region (the sampler runs from before the
+        warm-up, so nvidia-smi's start-up latency does not eat the window)."""
+        inside = [f for t, f in self.samples if self.window and self.window[0] <= t <= self.window[1]]
+        which = "timed region"
+        if not inside:
+            inside, which = [f for _, f in self.samples], "whole run (no sample inside the timed region)"
+        if not inside:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in inside if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in inside if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4) if s[3 + k].lower() == "active"})
+        reasons = sorted({names[k] for s in inside for k in range(4) if s[3 + k].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(inside), "sampled_over": which}
 
 
 def cpu_oracle_sample(p, tau, n_iter):
@@ -199,14 +206,14 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(args.warmup):
-        x, k, hist, rep = S.solve(b, tol=args.tol, maxit=maxit)
-    barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     iters = []
     lib_s = 0.0
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            x, k, hist, rep = S.solve(b, tol=args.tol, maxit=maxit)
         barrier()
+        w0 = time.perf_counter()
         e0.record(stream)
         for _ in range(args.steps):
             x, k, hist, rep = S.solve(b, tol=args.tol, maxit=maxit)
@@ -214,6 +221,7 @@ def main():
             lib_s += rep["solve_s"]
         e1.record(stream)
         barrier()
+        clk.window = (w0, time.perf_counter())
     dev_ms = e0.elapsed_time(e1)
     t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
     if world > 1:
