@@ -233,6 +233,30 @@ def test_cfg4_full_size_sampled():
     S.close()
 
 
+def test_cfg5_full_size_sampled():
+    """BASELINE's largest config (ORCA12-like 4322x3059, 10.9 M unknowns, tol 1e-12) on one GPU in
+    the bench's launch configuration: operator and preconditioner bitwise on the full grid, the
+    first 3 iterations bitwise, then the full solve's properties (converged with the recurrence
+    and the true residual <= tol-level, error vs x*, iterations near SURVEY §8(d)'s estimate)."""
+    p = synth.config("cfg5")
+    A, M, S = setup_pair(p)
+    xs = A.from_grid(synth.xstar(p))
+    b = A.apply(xs)
+    y = host(S.apply_operator(dev(A.to_grid(xs))))
+    assert np.array_equal(y, A.to_grid(A.apply_canonical(xs)))
+    s = host(S.apply_preconditioner(dev(A.to_grid(b))))
+    assert np.array_equal(s, A.to_grid(M.apply_canonical(b)))
+    ref = oracle.pcg(A, b, "ainv", M, 0.0, maxit=3, mode="canonical", pitch=S.pitch, block=S.block, rows=S.tile_rows)
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=0.0, maxit=3)
+    assert k == 3 and np.array_equal(hist, ref.hist) and np.array_equal(host(xg), A.to_grid(ref.x))
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-12, maxit=A.n)
+    assert rep["converged"] == 1 and rep["true_rel_residual"] < 5e-12
+    assert 4400 <= k <= 5000                                             # SURVEY §8(d): ~4800 +-15 %
+    x = A.from_grid(host(xg))
+    assert np.linalg.norm(x - xs) / np.linalg.norm(xs) < 1e-6
+    S.close()
+
+
 # --------------------------------------------------------- multi-rank path, emulated on one GPU
 @pytest.mark.parametrize("name,P,precond", [("cfg2", 2, "ainv"), ("cfg2", 3, "ainv"), ("cfg2", 8, "ainv"),
                                             ("cfg3", 4, "ainv"), ("cfg2", 4, "jacobi")])
