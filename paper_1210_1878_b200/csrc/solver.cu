@@ -58,6 +58,7 @@ struct pcg_ctx {
     // graph
     cudaGraphExec_t exec = nullptr;
     bool graph_built = false;
+    bool graph_failed = false;         // NCCL path: capture not possible here -> host loop
     cudaEvent_t ev_in = nullptr, ev0 = nullptr, ev1 = nullptr;
     std::string err;
     double bytes_k[3] = {0, 0, 0};
@@ -111,7 +112,20 @@ bool use_fused(const pcg_ctx* c) {
     // 584 units (cfg3: 27.6 vs 34.6 us/it) -- grid barriers get dearer with the grid
     return (int64_t)c->A.nloc * c->A.nbx <= 256;
 }
-bool use_graph(const pcg_ctx* c) { return !c->multi && !(c->plan.flags & PCG_FLAG_HOST_LOOP) && !use_fused(c); }
+// The NCCL path (several ranks, or one rank through PCG_FLAG_COMM_PATH) runs as the same
+// WHILE-node graph with its allgathers / halo send-recv captured in the body; the scalar kernels
+// after each allgather set the condition (one rank through NCCL at cfg4: 92.8 us/iteration
+// against 124.6 for the host loop; bitwise equal).  PCG_MULTI_GRAPH=0, or a capture that fails,
+// selects the host loop.
+bool multi_graph(const pcg_ctx* c) {
+    if (!c->multi || c->graph_failed || (c->plan.flags & (PCG_FLAG_HOST_LOOP | PCG_FLAG_LOCAL_RANKS))) return false;
+    const char* e = getenv("PCG_MULTI_GRAPH");
+    return !(e && atoi(e) == 0);
+}
+bool use_graph(const pcg_ctx* c) {
+    if (c->multi) return multi_graph(c);
+    return !(c->plan.flags & PCG_FLAG_HOST_LOOP) && !use_fused(c);
+}
 
 // ---------------------------------------------------------------- NCCL steps (multi path)
 Status allgather_loc(pcg_ctx* c) {
@@ -426,7 +440,11 @@ Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, doubl
     CU(cudaSetDevice(c->device));
     if (Status s = ensure_hist(c, maxit); !s) return s;
     if (use_graph(c) && !c->graph_built) {
-        if (Status s = build_graph(c); !s) return s;
+        if (Status s = build_graph(c); !s) {
+            if (!c->multi) return s;
+            c->graph_failed = true;                      // NCCL path: fall back to the host loop
+            cudaGetLastError();
+        }
     }
     // order after the caller's stream
     CU(cudaEventRecord(c->ev_in, c->user_stream));
@@ -813,9 +831,14 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     P.zrow.clear(); P.zrow.shrink_to_fit(); P.zhat.clear(); P.zhat.shrink_to_fit();
     if (use_graph(c)) {
         if (Status s = build_graph(c); !s) {
-            if (!c->A.pdl) return s;
-            c->A.pdl = 0;                                 // PDL edges not capturable here: plain launches
-            if (Status s2 = build_graph(c); !s2) return s2;
+            if (c->multi) {
+                c->graph_failed = true;                   // NCCL path: host loop
+                cudaGetLastError();
+            } else {
+                if (!c->A.pdl) return s;
+                c->A.pdl = 0;                             // PDL edges not capturable here: plain launches
+                if (Status s2 = build_graph(c); !s2) return s2;
+            }
         }
     }
     return Status::ok();

@@ -503,3 +503,23 @@ def test_tiny_cta_driver_bitwise(kind, monkeypatch):
     x2, k2, h2, _ = S.solve(b, tol=1e-10, maxit=A.n)
     assert k2 == k and np.array_equal(h2, hist) and np.array_equal(host(x2), x)
     S.close()
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_comm_path_graph_matches(name, monkeypatch):
+    """The NCCL path (one rank through PCG_FLAG_COMM_PATH) captured as the WHILE-node graph
+    (PCG_MULTI_GRAPH=1, allgathers and halo exchanges inside the body) equals the host-loop NCCL
+    path and the single-rank solve bit for bit."""
+    p = synth.config(name)
+    A, M, S = setup_pair(p)
+    b = dev(A.to_grid(rhs(A, p)))
+    x0, k0, h0, _ = S.solve(b, tol=1e-10, maxit=A.n)
+    S.close()
+    res = []
+    for mg in ("0", "1"):
+        monkeypatch.setenv("PCG_MULTI_GRAPH", mg)
+        S2 = pcg.Solver(p.cE, p.cN, p.mask, tau=TAU, comm_path=True)
+        for _ in range(2):                                   # the graph is replayed
+            x1, k1, h1, _ = S2.solve(b, tol=1e-10, maxit=A.n)
+            assert k1 == k0 and np.array_equal(h1, h0) and torch.equal(x1, x0)
+        S2.close()
