@@ -156,9 +156,10 @@ pcg_status pcg_setup(const pcg_coeffs* coeffs, const pcg_grid* grid, const pcg_o
  *   maxit    : iteration cap (reading R7); < 0 -> PCG_ERR_ARG.
  *   iterations (host out, may be NULL); res_hist (host out, may be NULL): res_hist[k] =
  *   ||r_k||/||b|| for k = 0..min(iterations, hist_cap-1); report (host out, may be NULL).
- * b = 0 gives x = 0 and 0 iterations.  Breakdown ((d,q) <= 0 or non-finite)
- * returns PCG_ERR_BREAKDOWN with the iterations done so far and x from the last valid
- * iterate.  Synchronises the context's stream before returning. */
+ * b = 0 gives x = 0 and 0 iterations.  Breakdown ((d,q) <= 0 or non-finite, or
+ * a non-finite ||b|| or ||r_0|| -- NaN / Inf in b or x0) returns PCG_ERR_BREAKDOWN with the
+ * iterations done so far and x from the last valid iterate.  Synchronises the context's stream
+ * before returning. */
 pcg_status pcg_solve(pcg_ctx* ctx, const double* b, const double* x0, double tol, int32_t maxit,
                      double* x, int32_t* iterations, double* res_hist, int32_t hist_cap,
                      pcg_report* report);

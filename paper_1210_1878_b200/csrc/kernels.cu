@@ -193,6 +193,10 @@ __device__ void fin_init(const KArgs& A, double rho0, double rr0) {
     sc->rho_prev = INFINITY;                 // beta of the first iteration = rho / inf = +0 (d_old = 0)
     const double h = __ddiv_rn(__dsqrt_rn(rr0), sc->nb);
     A.hist[0] = h;
+    if (!isfinite(h)) {                      // NaN / Inf in b or x0: breakdown before the first iteration
+        stop(A, kStBreakdown);
+        return;
+    }
     const int act = (h > sc->tol) && (sc->maxit > 0);
     sc->active = act;
     set_cond(A, act);
@@ -1107,6 +1111,9 @@ __device__ __forceinline__ void k3_sum_rr(const KArgs& A, int init) {
                     A.hist[0] = 0.0;
                     sc->active = 0;
                     set_cond(A, 0);
+                } else if (!isfinite(h)) {                 // NaN / Inf in b or x0
+                    A.hist[0] = h;
+                    stop(A, kStBreakdown);
                 } else {
                     A.hist[0] = h;
                     const int act = (h > sc->tol) && (sc->maxit > 0);

@@ -523,3 +523,34 @@ def test_comm_path_graph_matches(name, monkeypatch):
             x1, k1, h1, _ = S2.solve(b, tol=1e-10, maxit=A.n)
             assert k1 == k0 and np.array_equal(h1, h0) and torch.equal(x1, x0)
         S2.close()
+
+
+@pytest.mark.parametrize("name,env", [("cfg3", {}), ("cfg3", {"PCG_REDUNDANT": "0"}), ("cfg2", {}),
+                                      ("cfg3", {"PCG_FLAG": "host_loop"}), ("cfg3", {"PCG_MULTI": "comm"})])
+def test_breakdown_reported(name, env, monkeypatch):
+    """A non-finite right-hand side on an ocean point makes (d, q) non-finite in the first
+    iteration: every driver (graph with redundant sums or last-block sums, cooperative loop, host
+    loop, NCCL path) stops with PCG_ERR_BREAKDOWN instead of iterating on NaN, and the
+    context still solves a finite system afterwards."""
+    for k, v in env.items():
+        if k.startswith("PCG_") and k not in ("PCG_FLAG", "PCG_MULTI"):
+            monkeypatch.setenv(k, v)
+    p = synth.config(name)
+    A, M, S0 = setup_pair(p)
+    S0.close()
+    kw = {}
+    if env.get("PCG_FLAG") == "host_loop":
+        kw["flags"] = pcg.FLAG_HOST_LOOP
+    if env.get("PCG_MULTI") == "comm":
+        kw["comm_path"] = True
+    S = pcg.Solver(p.cE, p.cN, p.mask, tau=TAU, **kw)
+    b = A.to_grid(rhs(A, p))
+    bad = b.copy()
+    j, i = np.argwhere(p.mask == 1)[len(np.argwhere(p.mask == 1)) // 2]
+    bad[j, i] = np.nan
+    with pytest.raises(pcg.PcgError) as e:
+        S.solve(dev(bad), tol=1e-10, maxit=A.n)
+    assert e.value.code == "ERR_BREAKDOWN"
+    x, k, hist, rep = S.solve(dev(b), tol=1e-10, maxit=A.n)
+    assert rep["converged"] == 1
+    S.close()
