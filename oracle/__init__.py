@@ -83,6 +83,8 @@ def lib():
         L.orc_dot_canonical.restype = D
         L.orc_pcg.argtypes = [P, P, vp, vp, vp, D, I32, vp, vp, vp]
         L.orc_pcg.restype = C.c_int
+        L.orc_pcg_cg.argtypes = [P, P, vp, vp, vp, D, I32, vp, vp, vp]
+        L.orc_pcg_cg.restype = C.c_int
         _lib = L
     return _lib
 
@@ -302,8 +304,9 @@ class PcgResult:
 
 def pcg(A: Assembled, b, precond: str = "ainv", M: Ainv | None = None, tol: float = 1e-10,
         maxit: int | None = None, x0=None, mode: str = "plain", pitch: int | None = None,
-        block: int = 256, parts: int = 1, rows: int = 1) -> PcgResult:
-    """Alg. 1 with d = s + beta d.  Unknown-indexed vectors."""
+        block: int = 256, parts: int = 1, rows: int = 1, method: str = "pcg") -> PcgResult:
+    """Alg. 1 with d = s + beta d.  Unknown-indexed vectors.
+    method = "cg1": Chronopoulos-Gear single-reduction form (NEXT-2, orc_pcg_cg)."""
     L = lib()
     if maxit is None:
         maxit = A.n
@@ -313,8 +316,9 @@ def pcg(A: Assembled, b, precond: str = "ainv", M: Ainv | None = None, tol: floa
     hist = np.empty(maxit + 1)
     o = _PcgOpts(PRECOND[precond], MODE[mode], int(pitch if pitch else A.ni), int(block), int(parts), int(rows))
     rep = _PcgReport()
-    rc = L.orc_pcg(A._h, None if M is None else M.handle._h, C.byref(o), _ptr(b), _ptr(x0a),
-                   float(tol), int(maxit), _ptr(x), _ptr(hist), C.byref(rep))
+    fn = L.orc_pcg_cg if method == "cg1" else L.orc_pcg
+    rc = fn(A._h, None if M is None else M.handle._h, C.byref(o), _ptr(b), _ptr(x0a),
+            float(tol), int(maxit), _ptr(x), _ptr(hist), C.byref(rep))
     if rc == 1:
         raise OracleError(rc, "pcg")
     k = rep.iterations

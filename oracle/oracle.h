@@ -110,6 +110,15 @@ int orc_pcg(const orc_problem*, const orc_ainv* /*nullable unless AINV*/, const 
             const double* b, const double* x0, double tol, int32_t maxit,
             double* x, double* hist, orc_pcg_report* rep);
 
+/* Chronopoulos-Gear PCG: Alg. 1's iterates with ONE reduction point per
+ * iteration -- (r, u), (w, u) and (r, r) are formed together after w = A u -- using the
+ * recurrences p = u + beta p, s = w + beta s (s = A p), x += alpha p, r -= alpha s, u = P r,
+ * w = A u, beta = gamma'/gamma, alpha = gamma' / (delta - beta gamma'/alpha).  Same interface
+ * and modes as orc_pcg (canonical = the GPU's documented order). */
+int orc_pcg_cg(const orc_problem*, const orc_ainv* /*nullable unless AINV*/, const orc_pcg_opts*,
+               const double* b, const double* x0, double tol, int32_t maxit,
+               double* x, double* hist, orc_pcg_report* rep);
+
 #ifdef __cplusplus
 }
 #endif

@@ -252,3 +252,116 @@ done:
 #undef APPLY_A
 #undef PRECOND
 }
+
+/* Chronopoulos-Gear PCG (Alg. 1 of PAPER.md:318-334 rearranged so that its two
+ * inner products share one reduction point).  With s_k = A p_k, w_k = A u_k and u_k = P r_k:
+ *   p_k = u_k + beta_k p_{k-1};  s_k = w_k + beta_k s_{k-1};  x += alpha_k p_k;  r -= alpha_k s_k;
+ *   u = P r;  gamma' = (u, r);  rr = (r, r);  w = A u;  delta = (w, u);
+ *   beta' = gamma'/gamma;  alpha' = gamma' / (delta - beta' gamma' / alpha)
+ * (alpha_0 = gamma_0/delta_0, beta_0 = 0).  In exact arithmetic the iterates are Alg. 1's. */
+int orc_pcg_cg(const orc_problem* P, const orc_ainv* R, const orc_pcg_opts* o, const double* b,
+               const double* x0, double tol, int32_t maxit, double* x, double* hist, orc_pcg_report* rep) {
+    memset(rep, 0, sizeof *rep);
+    rep->failed_index = -1;
+    int64_t n = P->n;
+    if (!(tol >= 0.0) || maxit < 0) return rep->status = ORC_ERR_ARG;
+    if (o->precond == ORC_PRECOND_AINV && !R) return rep->status = ORC_ERR_ARG;
+    int canonical = o->mode == ORC_MODE_CANONICAL;
+    canon C = {0};
+    if (canonical) {
+        if (o->pitch < P->ni || o->block < 32 || o->block > 1024 || (o->block & (o->block - 1)) || o->parts != 1)
+            return rep->status = ORC_ERR_ARG;
+        C.P = P; C.pitch = o->pitch; C.B = o->block; C.parts = 1;
+        C.rb = (int32_t*)malloc(sizeof(int32_t) * 2);
+        C.rb[0] = 0; C.rb[1] = P->nj;
+        C.vals = (double*)malloc(sizeof(double) * o->block);
+        C.partial = (double*)malloc(sizeof(double) * (((int64_t)P->nj + 1) * (o->pitch / o->block + 2)));
+    }
+#define DOT(a, b) (canonical ? canon_dot(&C, (a), (b)) : plain_dot(n, (a), (b)))
+#define APPLY_A(in, out) (canonical ? canon_apply(P, (in), (out)) : orc_apply(P, (in), (out)))
+    size_t sz = sizeof(double) * (n ? n : 1);
+    double *r = malloc(sz), *u = malloc(sz), *w = malloc(sz), *p = malloc(sz), *sv = malloc(sz), *t = malloc(sz);
+#define PRECOND(rin, sout)                                                        \
+    do {                                                                          \
+        if (o->precond == ORC_PRECOND_AINV) {                                     \
+            if (canonical) canon_ainv_apply(R, (rin), (sout), t);                 \
+            else orc_ainv_apply(R, (rin), (sout));                                \
+        } else if (o->precond == ORC_PRECOND_JACOBI) {                            \
+            for (int64_t k_ = 0; k_ < n; ++k_) (sout)[k_] = (rin)[k_] / P->diag[k_]; \
+        } else {                                                                  \
+            memcpy((sout), (rin), sz);                                            \
+        }                                                                         \
+    } while (0)
+    for (int64_t k = 0; k < n; ++k) x[k] = x0 ? x0[k] : 0.0;
+    double nb = sqrt(DOT(b, b));
+    if (nb == 0.0) {
+        for (int64_t k = 0; k < n; ++k) x[k] = 0.0;
+        hist[0] = 0.0;
+        rep->iterations = 0; rep->converged = 1;
+        rep->status = ORC_OK;
+        goto done;
+    }
+    APPLY_A(x, w);
+    for (int64_t k = 0; k < n; ++k) r[k] = b[k] - w[k];
+    PRECOND(r, u);
+    double gamma = DOT(u, r);
+    double h = sqrt(DOT(r, r)) / nb;
+    hist[0] = h;
+    int32_t it = 0;
+    rep->status = ORC_OK;
+    if (!isfinite(h)) { rep->status = ORC_ERR_BREAKDOWN; goto fin; }
+    double alpha = 0.0, beta = 0.0;
+    if (h > tol && maxit > 0) {
+        APPLY_A(u, w);
+        double delta = DOT(w, u);
+        if (!(delta > 0.0) || !isfinite(delta)) { rep->status = ORC_ERR_BREAKDOWN; goto fin; }
+        alpha = gamma / delta;
+    }
+    for (int64_t k = 0; k < n; ++k) { p[k] = 0.0; sv[k] = 0.0; }
+    while (h > tol && it < maxit) {
+        if (canonical) {
+            for (int64_t k = 0; k < n; ++k) {
+                p[k] = fma(beta, p[k], u[k]);
+                sv[k] = fma(beta, sv[k], w[k]);
+                x[k] = fma(alpha, p[k], x[k]);
+                r[k] = fma(-alpha, sv[k], r[k]);
+            }
+        } else {
+            for (int64_t k = 0; k < n; ++k) {
+                p[k] = u[k] + beta * p[k];
+                sv[k] = w[k] + beta * sv[k];
+                x[k] = x[k] + alpha * p[k];
+                r[k] = r[k] - alpha * sv[k];
+            }
+        }
+        PRECOND(r, u);
+        double rr = DOT(r, r);
+        double gamma_new = DOT(u, r);
+        it++;
+        if (!isfinite(gamma_new) || !isfinite(rr)) { rep->status = ORC_ERR_BREAKDOWN; hist[it] = NAN; break; }
+        h = sqrt(rr) / nb;
+        hist[it] = h;
+        if (!(h > tol && it < maxit)) break;
+        APPLY_A(u, w);
+        double delta = DOT(w, u);
+        beta = gamma_new / gamma;
+        double den = delta - (beta * gamma_new) / alpha;
+        if (!(den > 0.0) || !isfinite(den)) { rep->status = ORC_ERR_BREAKDOWN; break; }
+        alpha = gamma_new / den;
+        gamma = gamma_new;
+    }
+fin:
+    rep->iterations = it;
+    rep->rel_residual = hist[it];
+    rep->converged = rep->status == ORC_OK && hist[it] <= tol;
+    APPLY_A(x, w);
+    for (int64_t k = 0; k < n; ++k) r[k] = b[k] - w[k];
+    rep->true_rel_residual = sqrt(DOT(r, r)) / nb;
+done:
+    free(r); free(u); free(w); free(p); free(sv); free(t);
+    if (canonical) { free(C.rb); free(C.vals); free(C.partial); }
+    return rep->status;
+#undef DOT
+#undef APPLY_A
+#undef PRECOND
+}

@@ -522,3 +522,43 @@ def test_generator_matches_survey_counts():
     assert (A.n, A.nnz) == (22288, 110528)
     p = synth.config("cfg1")
     assert oracle.assemble(p).n == 948
+
+
+# ----------------------------------------------- Chronopoulos-Gear single-reduction PCG (NEXT-2)
+@pytest.mark.parametrize("name", ["cfg1", "cfg2"])
+@pytest.mark.parametrize("precond", ["ainv", "jacobi"])
+def test_cg1_matches_alg1(name, precond):
+    """The single-reduction recurrences produce Alg. 1's iterates in exact arithmetic, so against
+    the (separately pinned) Alg. 1 oracle: iterations within max(2, 1 %), x within 1e-9 at tol
+    1e-12, both residuals converged.  A wrong sign or index in the alpha/beta recurrence, or a
+    missing beta term, diverges or needs many more iterations."""
+    p = synth.config(name)
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, 0.1 + 1e-9) if precond == "ainv" else None
+    b = A.apply(A.from_grid(synth.xstar(p)))
+    r1 = oracle.pcg(A, b, precond, M, 1e-12)
+    r2 = oracle.pcg(A, b, precond, M, 1e-12, method="cg1")
+    assert r2.converged and r2.true_rel_residual < 2e-12
+    assert abs(r2.iterations - r1.iterations) <= max(2, r1.iterations // 100)
+    assert np.linalg.norm(r2.x - r1.x) / np.linalg.norm(r1.x) < 1e-9
+
+
+def test_cg1_special_cases():
+    """tau = 0 (exact inverse): one iteration; dense solve on a tiny random grid; cfg1 (d = 4, a
+    power of two): Jacobi and no preconditioner are bitwise identical in this form too; b = 0."""
+    p = synth.config("cfg1")
+    A = oracle.assemble(p)
+    b = A.apply(A.from_grid(synth.xstar(p)))
+    r0 = oracle.pcg(A, b, "ainv", oracle.ainv(A, 0.0), 1e-10, method="cg1")
+    assert r0.iterations == 1 and r0.converged
+    rj = oracle.pcg(A, b, "jacobi", None, 1e-10, method="cg1")
+    rn = oracle.pcg(A, b, "none", None, 1e-10, method="cg1")
+    assert rj.iterations == rn.iterations and np.array_equal(rj.x, rn.x) and np.array_equal(rj.hist, rn.hist)
+    q = synth.random_grid(11, 9, 4)
+    Q = oracle.assemble(q)
+    bq = Q.apply(Q.from_grid(synth.xstar(q, 3)))
+    rq = oracle.pcg(Q, bq, "ainv", oracle.ainv(Q, 0.1 + 1e-9), 1e-13, method="cg1")
+    xd = np.linalg.solve(Q.dense(), bq)
+    assert np.linalg.norm(rq.x - xd) / np.linalg.norm(xd) < 1e-10
+    rz = oracle.pcg(A, np.zeros(A.n), "ainv", oracle.ainv(A, 0.1 + 1e-9), 1e-10, method="cg1")
+    assert rz.iterations == 0 and np.all(rz.x == 0.0)
