@@ -75,6 +75,10 @@ typedef enum {
 #define PCG_FLAG_COMM_PATH   2  /* use the multi-rank code path (NCCL) even when nranks == 1 */
 #define PCG_FLAG_LOCAL_RANKS 4  /* this context is one rank of an in-process, one-GPU emulation of a
                                    multi-rank run (no NCCL); solve with pcg_solve_local_ranks */
+#define PCG_FLAG_SINGLE_REDUCTION 8  /* Chronopoulos-Gear PCG: the iteration's
+                                        two inner products share one reduction point (kernels KA,
+                                        K3, KC).  One rank, factored preconditioners (AINV, P_B2,
+                                        FSAI through the ELL form); otherwise PCG_ERR_ARG. */
 
 /* "grid": geometry of this rank's part of the problem. */
 typedef struct {

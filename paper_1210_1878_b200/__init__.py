@@ -29,6 +29,7 @@ PRECOND = {"ainv": 0, "jacobi": 1, "none": 2, "fsai": 3}
 FLAG_HOST_LOOP = 1
 FLAG_COMM_PATH = 2
 FLAG_LOCAL_RANKS = 4
+FLAG_SINGLE_REDUCTION = 8
 
 
 class PcgError(RuntimeError):

@@ -1146,8 +1146,10 @@ __device__ __forceinline__ void k3_sum_rr(const KArgs& A, int init) {
             sc->red[2] = rr;
             sc->hpre = __ddiv_rn(__dsqrt_rn(rr), sc->nb);
         }
-        sc->alpha = init ? 0.0 : __ddiv_rn(sc->rho, sc->red[0]);   // K2 checked gamma > 0
-        sc->xpend = init ? 0 : 1;
+        if (!A.cgcg) {                                   // CG-CG: alpha / beta come from KC, x is updated in KA
+            sc->alpha = init ? 0.0 : __ddiv_rn(sc->rho, sc->red[0]);   // K2 checked gamma > 0
+            sc->xpend = init ? 0 : 1;
+        }
     }
 }
 
@@ -1247,6 +1249,49 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
         finish_units<1>(A, ws, A.partial[1], nullptr, nullptr);
         pdl_trigger();
     }
+}
+
+// ---- KA (Chronopoulos-Gear, NEXT-2): p = u + beta p ; s = w + beta s ; x += alpha p ;
+// r -= alpha s ; t = Dhat^-1 Z^T r ; (r, r).  u lives in A.s, w in A.q, s = A p in d[par] (old) /
+// d[par^1] (new).  r_new at a gathered point is recomputed as fma(-alpha, fma(beta, s_old, w),
+// r_old) -- bitwise what its own thread stores -- so no barrier separates the update and the
+// gather.  alpha, beta are KC's.  Same units, walks and partials as K2.
+__global__ void __launch_bounds__(kBlock, PCG_MINB_K2) ka_cg_kernel(const KArgs A, const int par) {
+    pdl_wait();
+    if (!is_active(A)) return;
+    const double alpha = A.sc->alpha, beta = A.sc->beta;
+    extern __shared__ double ws[];
+    const double* __restrict__ ro = A.r[par];
+    double* __restrict__ rn = A.r[par ^ 1];
+    const double* __restrict__ so = A.d[par];
+    double* __restrict__ sn = A.d[par ^ 1];
+    const double* __restrict__ w = A.q;
+    auto body = [&](const Unit& W) {
+        double v = 0.0;
+        if (W.live) {
+            const int64_t a = W.a;
+            const double pn = __fma_rn(beta, A.p[a], A.s[a]);
+            const double svn = __fma_rn(beta, so[a], w[a]);
+            A.x[a] = __fma_rn(alpha, pn, A.x[a]);
+            const double rnew = __fma_rn(-alpha, svn, ro[a]);
+            A.p[a] = pn;
+            sn[a] = svn;
+            auto gat = [&](int64_t g) { return __fma_rn(-alpha, __fma_rn(beta, __ldg(so + g), __ldg(w + g)), __ldg(ro + g)); };
+            const double acc = A.zt.col16 ? ell_row16(A.zt, a - A.hoff, a, gat) : ell_row(A.zt, a - A.hoff, gat);
+            A.t[a] = __ddiv_rn(acc, A.piv[a]);
+            rn[a] = rnew;
+            v = __dmul_rn(rnew, rnew);
+        }
+        return v;
+    };
+    if (A.sched2) {
+        sched_units(A, A.sched2, A.soff2, ws, body);
+        finish_sched(A, A.sched2, A.soff2, ws, A.partial[1]);
+        dynamic_units(A, &A.sc->ticket[1], A.partial[1], body, A.sched_u0);
+    } else {
+        dynamic_units(A, &A.sc->ticket[1], A.partial[1], body);
+    }
+    pdl_trigger();
 }
 
 // ---- K3 (AINV): s = Z t ; (s, r) ; beta / history / flag -----------------------------------
@@ -2147,11 +2192,61 @@ __device__ __forceinline__ double stencil(const KArgs& A, const double* __restri
     return acc;
 }
 
+// ---- KC (Chronopoulos-Gear, NEXT-2): w = A u ; (w, u) ; then alpha, beta -------------------
+// The one reduction point of the iteration: K3 has formed gamma' = (u, r) (as rho, fin_iter)
+// and (r, r); the last block here forms delta = (w, u) and beta = gamma'/gamma,
+// alpha = gamma' / (delta - beta gamma' / alpha) (init: alpha = gamma/delta, beta = 0), with the
+// breakdown test on the denominator.  Stencil in the canonical order of §5.3.
+__global__ void __launch_bounds__(kBlock) kc_cg_kernel(const KArgs A, const int init) {
+    pdl_wait();
+    if (!is_active(A)) return;
+    extern __shared__ double ws[];
+    const int64_t U = n_units(A);
+    int k = 0;
+    for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k) {
+        const Unit W = unit_of(A, u);
+        double v = 0.0;
+        if (W.valid) {
+            bool land;
+            const double ax = stencil(A, A.s, W.a, W.i, land);
+            const double wv = land ? 0.0 : ax;
+            A.q[W.a] = wv;
+            v = __dmul_rn(wv, A.s[W.a]);
+        }
+        put_warp_sum(ws, k, v);
+    }
+    pdl_trigger();
+    if (!finish_units<1>(A, ws, A.partial[0], nullptr, &A.sc->counter[0])) return;
+    const double delta = final_sum(A.partial[0], U);
+    if (threadIdx.x == 0) {
+        DevScalars* sc = A.sc;
+        sc->counter[0] = 0;
+        sc->red[0] = delta;
+        const double gamma = sc->rho;
+        double alpha, beta, den;
+        if (init) {
+            beta = 0.0;
+            den = delta;
+        } else {
+            beta = __ddiv_rn(gamma, sc->rho_prev);
+            den = __dadd_rn(delta, -__ddiv_rn(__dmul_rn(beta, gamma), sc->alpha));
+        }
+        if (!(den > 0.0) || !isfinite(den)) {
+            stop(A, kStBreakdown);
+        } else {
+            alpha = __ddiv_rn(gamma, den);
+            sc->alpha = alpha;
+            sc->beta = beta;
+        }
+    }
+}
+
 // prep: zero land entries of x and b (land is not an unknown, reading R20), zero d[0] everywhere
 __global__ void __launch_bounds__(kBlock) prep_kernel(const KArgs A) {
     const int64_t n = (int64_t)(A.nloc + 2 * A.halo) * A.pitch;
     for (int64_t a = (int64_t)blockIdx.x * kBlock + threadIdx.x; a < n; a += (int64_t)gridDim.x * kBlock) {
         A.d[0][a] = 0.0;
+        if (A.p) A.p[a] = 0.0;                               // CG-CG search direction
         if (A.rowdone && a < A.nloc) A.rowdone[a] = 0u;     // K23 row flags (DevScalars::epoch = 0)
         const int64_t row = a / A.pitch;
         if (row >= A.halo && row < A.halo + A.nloc) {
@@ -2356,6 +2451,8 @@ void configure_kernels(KArgs& A, int sms) {
     allow_smem(k2_ainv_kernel<16>, row_smem(A, A.g_k2, 1));
     allow_smem(k3_ainv_kernel<16>, row_smem(A, A.g_k3, 1));
     allow_smem(k2_diag_kernel, row_smem(A, A.g_kd, 2));
+    allow_smem(ka_cg_kernel, row_smem(A, A.g_k2, 1));
+    allow_smem(kc_cg_kernel, row_smem(A, A.g_row, 1));
     allow_smem(k1_pair_kernel<false>, row_smem(A, A.g_k1p, 1));
     allow_smem(k1_pair_kernel<true>, row_smem(A, A.g_k1p, 1));
     allow_smem(init_residual_kernel, row_smem(A, A.g_row, 1));
@@ -2410,7 +2507,15 @@ void launch_k1(const KArgs& A, int par, cudaStream_t st) {
         else launch_pdl(A, k1_kernel<false>, A.g_k1, kBlock, k1_smem(A, A.g_k1), st, A, par);
     }
 }
+void launch_kc(const KArgs& A, int par, int init, cudaStream_t st) {
+    (void)par;
+    launch_pdl(A, kc_cg_kernel, A.g_row, kBlock, row_smem(A, A.g_row, 1), st, A, init);
+}
 void launch_k2_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
+    if (A.cgcg && !init) {
+        launch_pdl(A, ka_cg_kernel, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par);
+        return;
+    }
     if (A.fuse23 && A.dia_q == 0 && !A.tma) {
         if (A.use_sz) launch_pdl(A, k23_ainv_kernel<-2>, A.g_k23, kBlock + 32, 0, st, A, par, init);
         else if (A.zt.col16 && A.z.col16) launch_pdl(A, k23_ainv_kernel<-1>, A.g_k23, kBlock + 32, 0, st, A, par, init);

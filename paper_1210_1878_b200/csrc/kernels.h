@@ -93,6 +93,8 @@ struct KArgs {
     // consumer kernel forms the canonical final sum it needs (K1: (s, r) -> beta, K2: (d, q) ->
     // alpha) and K3's block 0 does the history / stop test from K2's (r, r) at its start.
     int32_t redundant;
+    int32_t cgcg;                     // Chronopoulos-Gear single-reduction PCG (NEXT-2; KA, K3, KC)
+    double* p;                        // its search direction p (s = A p lives in d[0] / d[1], w in q, u in s)
     int32_t stage2;                   // K2's scheduled walk through the per-thread cp.async double buffer
     void* l2_base;                    // persisting L2 access-policy window of the iteration kernels
     size_t l2_bytes;                  // (0: none)
@@ -106,6 +108,7 @@ void launch_k1(const KArgs& A, int par, cudaStream_t st);
 void launch_k2_ainv(const KArgs& A, int par, int init, cudaStream_t st);
 void launch_k3_ainv(const KArgs& A, int par, int init, cudaStream_t st);
 void launch_k2_diag(const KArgs& A, int par, int init, int none, cudaStream_t st);
+void launch_kc(const KArgs& A, int par, int init, cudaStream_t st);   // CG-CG: w = A u, (w, u), alpha / beta
 // solve prologue / epilogue
 void launch_prep(const KArgs& A, cudaStream_t st);
 void launch_init_residual(const KArgs& A, cudaStream_t st);       // r0 = b - A x0 -> r[1], (b,b)

@@ -554,3 +554,41 @@ def test_breakdown_reported(name, env, monkeypatch):
     x, k, hist, rep = S.solve(dev(b), tol=1e-10, maxit=A.n)
     assert rep["converged"] == 1
     S.close()
+
+
+# -------------------------------------- Chronopoulos-Gear single-reduction PCG (NEXT-2) on the GPU
+@pytest.mark.parametrize("name,host_loop", [("cfg1", False), ("cfg2", False), ("cfg3", False), ("cfg3", True)])
+def test_cg1_bitwise_canonical(name, host_loop):
+    """PCG_FLAG_SINGLE_REDUCTION (kernels KA, K3, KC, one reduction point per iteration) equals
+    the oracle's Chronopoulos-Gear PCG in canonical order bit for bit, graph and host loop."""
+    p = synth.config(name)
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, TAU)
+    b = rhs(A, p)
+    flags = pcg.FLAG_SINGLE_REDUCTION | (pcg.FLAG_HOST_LOOP if host_loop else 0)
+    S = pcg.Solver(p.cE, p.cN, p.mask, tau=TAU, flags=flags)
+    ref = oracle.pcg(A, b, "ainv", M, 1e-10, maxit=A.n, mode="canonical", pitch=S.pitch, block=S.block, method="cg1")
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
+    assert k == ref.iterations
+    assert np.array_equal(hist, ref.hist)
+    assert np.array_equal(host(xg), A.to_grid(ref.x))
+    assert rep["converged"] == 1 and rep["true_rel_residual"] == ref.true_rel_residual
+    S.close()
+
+
+def test_cg1_vs_alg1_plain():
+    """Against the plain-order Alg. 1 oracle at tol 1e-12 (the north-star bar)."""
+    p = synth.config("cfg3")
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, TAU)
+    b = rhs(A, p)
+    ref = oracle.pcg(A, b, "ainv", M, 1e-12, maxit=A.n)
+    S = pcg.Solver(p.cE, p.cN, p.mask, tau=TAU, flags=pcg.FLAG_SINGLE_REDUCTION)
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-12, maxit=A.n)
+    assert abs(k - ref.iterations) <= max(2, ref.iterations // 100)
+    x = A.from_grid(host(xg))
+    assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) <= 1e-9
+    assert rep["true_rel_residual"] <= 2e-12
+    S.close()
+    with pytest.raises(pcg.PcgError):
+        pcg.Solver(p.cE, p.cN, p.mask, precond="jacobi", flags=pcg.FLAG_SINGLE_REDUCTION)
