@@ -268,14 +268,18 @@ int orc_pcg_cg(const orc_problem* P, const orc_ainv* R, const orc_pcg_opts* o, c
     if (o->precond == ORC_PRECOND_AINV && !R) return rep->status = ORC_ERR_ARG;
     int canonical = o->mode == ORC_MODE_CANONICAL;
     canon C = {0};
-    if (canonical) {
-        if (o->pitch < P->ni || o->block < 32 || o->block > 1024 || (o->block & (o->block - 1)) || o->parts != 1)
+    if (canonical) {                 /* as orc_pcg: parts > 1 = the rank-ordered tree over row blocks */
+        if (o->pitch < P->ni || o->block < 32 || o->block > 1024 || (o->block & (o->block - 1)) ||
+            o->parts < 1 || o->parts > 32 || o->parts > P->nj)
             return rep->status = ORC_ERR_ARG;
-        C.P = P; C.pitch = o->pitch; C.B = o->block; C.parts = 1;
-        C.rb = (int32_t*)malloc(sizeof(int32_t) * 2);
-        C.rb[0] = 0; C.rb[1] = P->nj;
+        C.P = P; C.pitch = o->pitch; C.B = o->block; C.parts = o->parts;
+        C.rb = (int32_t*)malloc(sizeof(int32_t) * (o->parts + 1));
+        if (o->parts == 1) { C.rb[0] = 0; C.rb[1] = P->nj; }
+        else orc_partition(P->nj, P->ni, P->mask, o->parts, C.rb);
         C.vals = (double*)malloc(sizeof(double) * o->block);
-        C.partial = (double*)malloc(sizeof(double) * (((int64_t)P->nj + 1) * (o->pitch / o->block + 2)));
+        int64_t maxrows = 0;
+        for (int r = 0; r < o->parts; ++r) if (C.rb[r + 1] - C.rb[r] > maxrows) maxrows = C.rb[r + 1] - C.rb[r];
+        C.partial = (double*)malloc(sizeof(double) * ((maxrows + 1) * (o->pitch / o->block + 2)));
     }
 #define DOT(a, b) (canonical ? canon_dot(&C, (a), (b)) : plain_dot(n, (a), (b)))
 #define APPLY_A(in, out) (canonical ? canon_apply(P, (in), (out)) : orc_apply(P, (in), (out)))

@@ -325,7 +325,7 @@ class LocalRanks:
     multi-rank device code path (halo rows, rank sums, rank-ordered tree) without n GPUs."""
 
     def __init__(self, cE, cN, mask, nranks, *, periodic=True, tau=0.1, precond="ainv", sigma=None, device=None,
-                 setup_threads=0, ainv_halo=0, ainv_fill=0):
+                 setup_threads=0, ainv_halo=0, ainv_fill=0, flags=0):
         import torch
         L = lib()
         cE, cN, mask, sigma = _host_inputs(cE, cN, mask, sigma)
@@ -339,7 +339,7 @@ class LocalRanks:
         for r in range(self.n):
             g = Grid(ni, nj, 1 if periodic else 0, int(self.rb[r]), int(self.rb[r + 1]), r, self.n, None, dev,
                      stream.cuda_stream)
-            o = _opts(precond, tau, FLAG_LOCAL_RANKS, 0, int(ainv_halo), setup_threads, 4, ainv_fill)
+            o = _opts(precond, tau, FLAG_LOCAL_RANKS | int(flags), 0, int(ainv_halo), setup_threads, 4, ainv_fill)
             h = C.c_void_p()
             rc = L.pcg_setup(C.byref(co), C.byref(g), C.byref(o), C.byref(h))
             if rc != 0:

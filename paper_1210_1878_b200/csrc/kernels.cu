@@ -2192,6 +2192,28 @@ __device__ __forceinline__ double stencil(const KArgs& A, const double* __restri
     return acc;
 }
 
+// alpha, beta of Chronopoulos-Gear from delta = (w, u) and gamma' = rho (one thread; fin_init /
+// fin_iter has set rho, rho_prev and decided the stop test)
+__device__ void cg_alpha_beta(const KArgs& A, double delta, int init) {
+    DevScalars* sc = A.sc;
+    sc->red[0] = delta;
+    const double gamma = sc->rho;
+    double beta, den;
+    if (init) {
+        beta = 0.0;
+        den = delta;
+    } else {
+        beta = __ddiv_rn(gamma, sc->rho_prev);
+        den = __dadd_rn(delta, -__ddiv_rn(__dmul_rn(beta, gamma), sc->alpha));
+    }
+    if (!(den > 0.0) || !isfinite(den)) {
+        stop(A, kStBreakdown);
+        return;
+    }
+    sc->alpha = __ddiv_rn(gamma, den);
+    sc->beta = beta;
+}
+
 // ---- KC (Chronopoulos-Gear, NEXT-2): w = A u ; (w, u) ; then alpha, beta -------------------
 // The one reduction point of the iteration: K3 has formed gamma' = (u, r) (as rho, fin_iter)
 // and (r, r); the last block here forms delta = (w, u) and beta = gamma'/gamma,
@@ -2219,25 +2241,9 @@ __global__ void __launch_bounds__(kBlock) kc_cg_kernel(const KArgs A, const int 
     if (!finish_units<1>(A, ws, A.partial[0], nullptr, &A.sc->counter[0])) return;
     const double delta = final_sum(A.partial[0], U);
     if (threadIdx.x == 0) {
-        DevScalars* sc = A.sc;
-        sc->counter[0] = 0;
-        sc->red[0] = delta;
-        const double gamma = sc->rho;
-        double alpha, beta, den;
-        if (init) {
-            beta = 0.0;
-            den = delta;
-        } else {
-            beta = __ddiv_rn(gamma, sc->rho_prev);
-            den = __dadd_rn(delta, -__ddiv_rn(__dmul_rn(beta, gamma), sc->alpha));
-        }
-        if (!(den > 0.0) || !isfinite(den)) {
-            stop(A, kStBreakdown);
-        } else {
-            alpha = __ddiv_rn(gamma, den);
-            sc->alpha = alpha;
-            sc->beta = beta;
-        }
+        A.sc->counter[0] = 0;
+        if (A.multi) A.sc->loc[0] = delta;               // rank sum: the allgather + kSsCg* follow
+        else cg_alpha_beta(A, delta, init);
     }
 }
 
@@ -2341,6 +2347,18 @@ __global__ void scalar_kernel(const KArgs A, const int step) {
         case kSsGamma: sc->red[0] = rank_tree(A.gath, P, 0); break;
         case kSsInit: if (sc->active) fin_init(A, rank_tree(A.gath, P, 1), rank_tree(A.gath, P, 2)); break;
         case kSsIter: if (sc->active) fin_iter(A, rank_tree(A.gath, P, 1), rank_tree(A.gath, P, 2)); break;
+        case kSsCgInit:
+            if (sc->active) {
+                fin_init(A, rank_tree(A.gath, P, 1), rank_tree(A.gath, P, 2));
+                if (sc->active) cg_alpha_beta(A, rank_tree(A.gath, P, 0), 1);
+            }
+            break;
+        case kSsCgIter:
+            if (sc->active) {
+                fin_iter(A, rank_tree(A.gath, P, 1), rank_tree(A.gath, P, 2));
+                if (sc->active) cg_alpha_beta(A, rank_tree(A.gath, P, 0), 0);
+            }
+            break;
         case kSsTrue: {
             const double tot = rank_tree(A.gath, P, 3);
             sc->true_rel = sc->bzero ? 0.0 : __ddiv_rn(__dsqrt_rn(tot), sc->nb);

@@ -116,7 +116,8 @@ void launch_fin(const KArgs& A, cudaStream_t st);                 // pending x u
 void launch_true_residual(const KArgs& A, cudaStream_t st);       // ||b - A x|| / ||b||
 void launch_apply(const KArgs& A, const double* x_arr, double* y_arr, cudaStream_t st);   // y = A x
 // multi-rank scalar steps (one thread) after an allgather of DevScalars::loc
-enum ScalarStep : int32_t { kSsBB = 0, kSsGamma = 1, kSsInit = 2, kSsIter = 3, kSsTrue = 4 };
+enum ScalarStep : int32_t { kSsBB = 0, kSsGamma = 1, kSsInit = 2, kSsIter = 3, kSsTrue = 4,
+                            kSsCgInit = 5, kSsCgIter = 6 };   // Chronopoulos-Gear: (delta, gamma, rr) at once
 void launch_scalar(const KArgs& A, int step, cudaStream_t st);
 void launch_set_cond(cudaGraphConditionalHandle h, cudaStream_t st);
 void launch_extrapolate(const double* xt, const double* xm, double* x0, int64_t n, cudaStream_t st);

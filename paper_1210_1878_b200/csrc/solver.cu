@@ -189,7 +189,7 @@ Status exch_halo_ainv(pcg_ctx* c, bool qr, bool t, bool with_allgather, int par)
 // Halo-AINV across ranks adds QR (w rows of q and r[par] from the southern neighbour, for K2's
 // gathers below the first owned row; fused with the allgather after K1) and T (the northern
 // neighbour's first rows of t, for K3's gathers above the last owned row).
-enum class Ex { None, Allgather, HaloX, HaloSAllgather, AllgatherQR, QR, HaloT };
+enum class Ex { None, Allgather, HaloX, HaloSAllgather, AllgatherQR, QR, HaloT, HaloS };
 struct Step {
     Ex ex;
     std::function<void(pcg_ctx*)> run;   // kernels of one rank (ex == None)
@@ -213,7 +213,15 @@ std::vector<Step> prologue_steps(const pcg_ctx* c) {
         s.push_back({Ex::None, [](pcg_ctx* x) { launch_k2_ainv(x->A, 1, 1, x->st); }});
         if (hx) s.push_back({Ex::HaloT, nullptr});
         s.push_back({Ex::None, [](pcg_ctx* x) { launch_k3_ainv(x->A, 1, 1, x->st); }});
-        if (c->A.cgcg) s.push_back({Ex::None, [](pcg_ctx* x) { launch_kc(x->A, 1, 1, x->st); }});   // w0, alpha0
+        if (c->A.cgcg) {                                 // w0 = A u0, delta0 -> alpha0 (NEXT-2)
+            if (multi) s.push_back({Ex::HaloS, nullptr});
+            s.push_back({Ex::None, [](pcg_ctx* x) { launch_kc(x->A, 1, 1, x->st); }});
+            if (multi) {
+                s.push_back({Ex::Allgather, nullptr});
+                s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsCgInit, x->st); }});
+            }
+            return s;
+        }
     } else {
         s.push_back({Ex::None, [none](pcg_ctx* x) { launch_k2_diag(x->A, 1, 1, none, x->st); }});
     }
@@ -229,10 +237,15 @@ std::vector<Step> iteration_steps(const pcg_ctx* c, int par) {
     const bool multi = c->multi, ainv = c->plan.factored();
     const bool none = c->plan.precond == PCG_PRECOND_NONE;
     const bool hx = multi && ainv && c->plan.halo_w > 0;
-    if (c->A.cgcg) {                     // Chronopoulos-Gear (one rank): KA, K3, KC
+    if (c->A.cgcg) {                     // Chronopoulos-Gear: KA, K3, (u halo), KC, ONE allgather
         s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k2_ainv(x->A, par, 0, x->st); }});
         s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k3_ainv(x->A, par, 0, x->st); }});
+        if (multi) s.push_back({Ex::HaloS, nullptr});
         s.push_back({Ex::None, [par](pcg_ctx* x) { launch_kc(x->A, par, 0, x->st); }});
+        if (multi) {
+            s.push_back({Ex::Allgather, nullptr});
+            s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsCgIter, x->st); }});
+        }
         return s;
     }
     s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k1(x->A, par, x->st); }});
@@ -272,6 +285,7 @@ Status run_steps(pcg_ctx* c, const std::vector<Step>& steps) {
             case Ex::None: s.run(c); break;
             case Ex::Allgather: if (Status r = allgather_loc(c); !r) return r; break;
             case Ex::HaloX: if (Status r = halo(c, c->x, false); !r) return r; break;
+            case Ex::HaloS: if (Status r = halo(c, c->s, false); !r) return r; break;
             case Ex::HaloSAllgather: if (Status r = halo(c, c->s, true); !r) return r; break;
             case Ex::AllgatherQR: if (Status r = exch_halo_ainv(c, true, false, true, s.par); !r) return r; break;
             case Ex::QR: if (Status r = exch_halo_ainv(c, true, false, false, s.par); !r) return r; break;
@@ -312,7 +326,7 @@ Status local_exchange(const std::vector<pcg_ctx*>& cs, Ex ex, cudaStream_t st, i
         for (size_t r = 0; r < P; ++r)
             for (size_t q = 0; q < P; ++q)
                 CU(cudaMemcpyAsync(cs[r]->gath + 4 * q, cs[q]->sc->loc, 4 * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    if (ex == Ex::HaloX || ex == Ex::HaloSAllgather) {
+    if (ex == Ex::HaloX || ex == Ex::HaloSAllgather || ex == Ex::HaloS) {
         for (size_t r = 1; r < P; ++r) {
             pcg_ctx* lo = cs[r - 1];
             pcg_ctx* up = cs[r];
@@ -821,8 +835,9 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     A.cgcg = 0;
     A.p = nullptr;
     if (P.flags & PCG_FLAG_SINGLE_REDUCTION) {
-        if (c->multi || !P.factored())
-            return Status::err(PCG_ERR_ARG, "pcg_setup: PCG_FLAG_SINGLE_REDUCTION needs one rank and a factored preconditioner (AINV, P_B2, FSAI)");
+        if (!P.factored() || (c->multi && P.halo_w > 0))
+            return Status::err(PCG_ERR_ARG, "pcg_setup: PCG_FLAG_SINGLE_REDUCTION needs a factored preconditioner "
+                               "(AINV, P_B2, FSAI) and, across ranks, block-local AINV (ainv_halo = 0)");
         A.cgcg = 1;
         A.redundant = 0;
         A.fuse23 = 0;

@@ -592,3 +592,38 @@ def test_cg1_vs_alg1_plain():
     S.close()
     with pytest.raises(pcg.PcgError):
         pcg.Solver(p.cE, p.cN, p.mask, precond="jacobi", flags=pcg.FLAG_SINGLE_REDUCTION)
+
+
+@pytest.mark.parametrize("name,P", [("cfg2", 2), ("cfg2", 4), ("cfg3", 3)])
+def test_cg1_local_ranks_bitwise(name, P):
+    """Chronopoulos-Gear across P ranks (one allgather of (delta, gamma', rr) and one u halo per
+    iteration instead of PCG's two allgathers), emulated on one GPU, equals the oracle's
+    partitioned canonical Chronopoulos-Gear PCG (block-local AINV) bit for bit."""
+    p = synth.config(name)
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, TAU, parts=P, halo=0)
+    b = rhs(A, p)
+    R = pcg.LocalRanks(p.cE, p.cN, p.mask, P, tau=TAU, flags=pcg.FLAG_SINGLE_REDUCTION)
+    ref = oracle.pcg(A, b, "ainv", M, 1e-10, maxit=A.n, mode="canonical", pitch=R.pitch, block=R.block, parts=P,
+                     method="cg1")
+    xg, k, hist, rep = R.solve(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
+    assert k == ref.iterations
+    assert np.array_equal(hist, ref.hist)
+    assert np.array_equal(host(xg), A.to_grid(ref.x))
+    assert rep["true_rel_residual"] == ref.true_rel_residual
+    R.close()
+
+
+def test_cg1_comm_path_matches_single_rank():
+    """One rank through the NCCL path (allgather + scalar step, captured in the graph) equals the
+    single-rank Chronopoulos-Gear solve bit for bit."""
+    p = synth.config("cfg3")
+    A = oracle.assemble(p)
+    b = dev(A.to_grid(rhs(A, p)))
+    S1 = pcg.Solver(p.cE, p.cN, p.mask, tau=TAU, flags=pcg.FLAG_SINGLE_REDUCTION)
+    x1, k1, h1, _ = S1.solve(b, tol=1e-10, maxit=A.n)
+    S1.close()
+    S2 = pcg.Solver(p.cE, p.cN, p.mask, tau=TAU, flags=pcg.FLAG_SINGLE_REDUCTION, comm_path=True)
+    x2, k2, h2, _ = S2.solve(b, tol=1e-10, maxit=A.n)
+    assert k2 == k1 and np.array_equal(h2, h1) and torch.equal(x2, x1)
+    S2.close()
