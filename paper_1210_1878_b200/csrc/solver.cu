@@ -109,9 +109,11 @@ Status upload(pcg_ctx* c, T*& p, const std::vector<T>& h) {
 bool use_fused(const pcg_ctx* c) {
     if (c->multi || c->A.cgcg || (c->plan.flags & PCG_FLAG_HOST_LOOP)) return false;
     if (const char* e = getenv("PCG_FUSED")) return atoi(e) != 0;
-    // measured: fused wins at <= 149 units (cfg1-2: 16 vs 19, 20 vs 21 us/it), the graph at
-    // 584 units (cfg3: 27.6 vs 34.6 us/it) -- grid barriers get dearer with the grid
-    return (int64_t)c->A.nloc * c->A.nbx <= 256;
+    // measured with the current graph (redundant sums, 8-iteration body): factored preconditioners
+    // -- cfg1 (32 units) 14.5 vs 14.6 us/it, cfg2 (149 units) 20.5-20.7 fused vs 16.9-18.4 graph,
+    // cfg3 35.7 vs 21.1; Jacobi / none -- cfg1 11.7 vs 12.9, cfg2 13.4 vs 13.8, cfg3 24.1 vs 14.9
+    const int64_t units = (int64_t)c->A.nloc * c->A.nbx;
+    return units <= (c->plan.factored() ? 64 : 256);
 }
 // The NCCL path (several ranks, or one rank through PCG_FLAG_COMM_PATH) runs as the same
 // WHILE-node graph with its allgathers / halo send-recv captured in the body; the scalar kernels
