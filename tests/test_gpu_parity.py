@@ -627,3 +627,19 @@ def test_cg1_comm_path_matches_single_rank():
     x2, k2, h2, _ = S2.solve(b, tol=1e-10, maxit=A.n)
     assert k2 == k1 and np.array_equal(h2, h1) and torch.equal(x2, x1)
     S2.close()
+
+
+@pytest.mark.parametrize("kind", ["nonperiodic_sigma", "ragged_wide"])
+def test_graph_path_edge_grids_bitwise(kind):
+    """Grids past the cooperative-loop threshold (> 64 units) with the features the ORCA configs
+    lack -- no E-W wrap with a diagonal shift, and a row length far from a multiple of 256 -- run
+    through the WHILE graph with redundant sums and the L2 window, bitwise the oracle's."""
+    if kind == "nonperiodic_sigma":
+        p = synth.random_grid(100, 90, 11, periodic=False, sigma=True)
+    else:
+        p = synth.random_grid(300, 40, 12)
+    A, S, ref, x, k, hist, rep, _ = _canonical_pair(p, "ainv", 1e-10)
+    assert k == ref.iterations and np.array_equal(hist, ref.hist)
+    assert np.array_equal(x, A.to_grid(ref.x))
+    assert rep["true_rel_residual"] == ref.true_rel_residual
+    S.close()
