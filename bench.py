@@ -262,17 +262,21 @@ def main():
         peak, peak_src = fallback_peak()
         ach = by[kk] / (ms[kk] * 1e-3) / 1e9
         traffic = None
+        traffic_src = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
             tj = json.load(open(tp))
             traffic = tj.get(args.config, {}).get(names[kk])
+            if traffic is not None:
+                traffic_src = ("profiles/ncu_traffic.json: dram__bytes_read+write per launch, one-pass ncu of the "
+                               "host-loop driver without the L2 window (ncu does not honour it)")
         # the same kernel inside the solve graph: its share of the event-timed iteration applied to
         # the graph's iteration time (the events include each launch's gap; the graph has none)
         it_graph_ms = dev_ms / max(1, sum(iters))
         share = ms[kk] / max(1e-12, float(ms[:3].sum()))
         ach_graph = by[kk] / (share * it_graph_ms * 1e-3) / 1e9
         roof = {"bound": "hbm", "kernel": names[kk], "achieved": ach, "peak": peak, "unit": "GB/s",
-                "frac": ach / peak, "traffic": traffic, "peak_source": peak_src,
+                "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                 "algorithmic_bytes_per_launch": by[kk], "ms_per_launch": ms[kk],
                 "in_graph": {"ms_per_launch_est": share * it_graph_ms, "achieved": ach_graph, "frac": ach_graph / peak,
                              "iteration_alg_GBps": float(by.sum()) / (it_graph_ms * 1e-3) / 1e9,
