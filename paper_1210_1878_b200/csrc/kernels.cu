@@ -733,8 +733,10 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1F) k1_flat_kernel(const KAr
     double beta;
     const double alpha = A.sc->alpha;
     if (!k1_beta(A, par, beta)) return;
+    if (A.red_gamma && !A.redundant && blockIdx.x == 0 && threadIdx.x == 0)
+        A.sc->xpend = 0;                                   // this kernel does x += alpha_prev d_old
     bool last;
-    if (A.redundant) {
+    if (A.redundant || A.red_gamma) {                      // (d, q) is formed by K2's blocks
         extern __shared__ double ws[];
         const int64_t U = n_units(A);
         int k = 0;
@@ -2134,7 +2136,16 @@ __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const in
     pdl_wait();
     if (!is_active(A)) return;
     double alpha;
-    if (!get_alpha(A, init, alpha)) {
+    if (A.red_gamma && !init) {
+        // (d, q) of K1's partials formed by every block (K1 has no last block); same IEEE alpha
+        const double gamma = final_sum_all<PCG_RED_NB>(A.partial[0], n_units(A));
+        if (!(gamma > 0.0) || !isfinite(gamma)) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
+            return;
+        }
+        alpha = __ddiv_rn(A.sc->rho, gamma);
+        if (blockIdx.x == 0 && threadIdx.x == 0) A.sc->red[0] = gamma;
+    } else if (!get_alpha(A, init, alpha)) {
         if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
         return;
     }
@@ -2159,8 +2170,8 @@ __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const in
     }
     pdl_trigger();
     if (finish_units<2>(A, ws, A.partial[1], A.partial[2], &A.sc->counter[1])) {
-        const double rr = final_sum(A.partial[1], n_units(A));
-        const double rs = final_sum(A.partial[2], n_units(A));
+        double rr, rs;                                     // both walks in one pass (same sums)
+        final_sum_pair<PCG_FINAL_NB_K3>(A.partial[1], A.partial[2], n_units(A), rr, rs);
         if (threadIdx.x == 0) {
             A.sc->counter[1] = 0;
             A.sc->alpha = alpha;

@@ -93,6 +93,7 @@ struct KArgs {
     // consumer kernel forms the canonical final sum it needs (K1: (s, r) -> beta, K2: (d, q) ->
     // alpha) and K3's block 0 does the history / stop test from K2's (r, r) at its start.
     int32_t redundant;
+    int32_t red_gamma;                // Jacobi / none (one rank): K1 without a last block, K2's blocks form (d, q)
     int32_t cgcg;                     // Chronopoulos-Gear single-reduction PCG (NEXT-2; KA, K3, KC)
     double* p;                        // its search direction p (s = A p lives in d[0] / d[1], w in q, u in s)
     int32_t stage2;                   // K2's scheduled walk through the per-thread cp.async double buffer

@@ -487,11 +487,13 @@ Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, doubl
     if (x0) CU(cudaMemcpy2DAsync(c->x + P.hoff(), dp, x0, sp, sp, (size_t)P.nloc, kin, c->st));
     else CU(cudaMemsetAsync(c->x + P.hoff(), 0, (size_t)P.nloc * dp, c->st));
     if (use_fused(c)) {
-        const int32_t red = c->A.redundant;               // the loop kernel keeps its own scalars
+        const int32_t red = c->A.redundant, redg = c->A.red_gamma;   // the loop kernel keeps its own scalars
         c->A.redundant = 0;
+        c->A.red_gamma = 0;
         Status s = launch_prologue(c);
         if (s) { CU(launch_loop(c->A, c->st)); s = launch_epilogue(c); }
         c->A.redundant = red;
+        c->A.red_gamma = redg;
         if (!s) return s;
     } else if (use_graph(c)) {
         CU(cudaGraphLaunch(c->exec, c->st));
@@ -830,6 +832,12 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     if (P.factored() && !c->multi && !A.fuse23 && (A.k1flat == 2 || A.k1flat == 3 || (A.k1flat == 0 && !A.dynamic_k1)) && !A.tma) {
         const char* re = getenv("PCG_REDUNDANT");
         A.redundant = re ? atoi(re) != 0 : 1;
+    }
+    // Jacobi / none: the (d, q) half of the redundant-sum mode (K2's blocks form it, K1 has no tail)
+    A.red_gamma = 0;
+    if (!P.factored() && !c->multi && A.k1flat == 2) {
+        const char* re = getenv("PCG_REDUNDANT");
+        A.red_gamma = re ? atoi(re) != 0 : 1;
     }
     A.stage2 = 0;
     if (const char* se = getenv("PCG_STAGE2")) A.stage2 = atoi(se) != 0;

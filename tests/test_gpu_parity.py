@@ -75,7 +75,8 @@ def _canonical_pair(p, precond, tol, maxit=None, x0=None, tau=TAU, **kw):
 
 
 @pytest.mark.parametrize("name,precond", [("cfg1", "ainv"), ("cfg1", "jacobi"), ("cfg1", "none"),
-                                          ("cfg2", "ainv"), ("cfg2", "jacobi"), ("cfg3", "ainv")])
+                                          ("cfg2", "ainv"), ("cfg2", "jacobi"), ("cfg3", "ainv"),
+                                          ("cfg3", "jacobi"), ("cfg3", "none")])
 def test_solve_bitwise_canonical(name, precond):
     p = synth.config(name)
     A, S, ref, x, k, hist, rep, _ = _canonical_pair(p, precond, 1e-10)
