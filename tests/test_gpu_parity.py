@@ -644,3 +644,16 @@ def test_graph_path_edge_grids_bitwise(kind):
     assert np.array_equal(x, A.to_grid(ref.x))
     assert rep["true_rel_residual"] == ref.true_rel_residual
     S.close()
+
+
+@pytest.mark.parametrize("tau", [0.01 + 1e-9, 0.05 + 1e-9, 0.2 + 1e-9])
+def test_cfg3_drop_tolerance_sweep_bitwise(tau):
+    """BASELINE config 3 is a drop-tolerance sweep: at tau = 0.01 Z has ~50 entries per column
+    (long overflow rows everywhere, not only at the pole), at 0.2 about 2 -- full solves bitwise
+    the oracle's canonical PCG across the sweep."""
+    p = synth.config("cfg3")
+    A, S, ref, x, k, hist, rep, _ = _canonical_pair(p, "ainv", 1e-10, tau=tau)
+    assert k == ref.iterations and np.array_equal(hist, ref.hist)
+    assert np.array_equal(x, A.to_grid(ref.x))
+    assert rep["true_rel_residual"] == ref.true_rel_residual
+    S.close()
