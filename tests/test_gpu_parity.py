@@ -657,3 +657,24 @@ def test_cfg3_drop_tolerance_sweep_bitwise(tau):
     assert np.array_equal(x, A.to_grid(ref.x))
     assert rep["true_rel_residual"] == ref.true_rel_residual
     S.close()
+
+
+@pytest.mark.parametrize("precond", ["jacobi", "fsai"])
+def test_cfg4_full_size_other_preconditioners(precond):
+    """ORCA025 size with the paper's two other preconditioners -- the diagonal P^-1 and its own
+    banded FSAI P (DIA kernels): the first 5 iterations bitwise, then a converged solve whose
+    iteration count matches BASELINE §5 (2618 / 3004)."""
+    p = synth.config("cfg4")
+    A = oracle.assemble(p)
+    M = oracle.fsai(A, 4) if precond == "fsai" else None
+    S = pcg.Solver(p.cE, p.cN, p.mask, tau=TAU, precond=precond, fsai_q=4)
+    xs = A.from_grid(synth.xstar(p))
+    b = A.apply(xs)
+    ref = oracle.pcg(A, b, "ainv" if precond == "fsai" else "jacobi", M, 0.0, maxit=5, mode="canonical",
+                     pitch=S.pitch, block=S.block, rows=S.tile_rows)
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=0.0, maxit=5)
+    assert k == 5 and np.array_equal(hist, ref.hist) and np.array_equal(host(xg), A.to_grid(ref.x))
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
+    assert rep["converged"] == 1 and rep["true_rel_residual"] < 2e-10
+    assert abs(k - (3004 if precond == "fsai" else 2618)) <= 30
+    S.close()
