@@ -221,8 +221,8 @@ pcg_status pcg_layout(const pcg_ctx* ctx, int32_t* pitch, int32_t* block, int32_
 
 /* Average device time (ms) of each per-iteration kernel over n_iter iterations run on the
  * context's stream with CUDA events around every launch, on the state left by the last
- * solve (a profiling aid for bench.py).  ms_out[0..3] = K1 (stencil), K2 (r update +
- * Z^T gather), K3 (Z gather), whole iteration; bytes_out[0..2] = algorithmic bytes per
+ * solve (a profiling aid for bench.py).  ms_out[0..3] = median per-launch time of K1
+ * (stencil), K2 (r update + Z^T gather), K3 (Z gather), and of the whole iteration; bytes_out[0..2] = algorithmic bytes per
  * launch of K1..K3.  Single rank only. */
 pcg_status pcg_kernel_times(pcg_ctx* ctx, int32_t n_iter, double* ms_out, double* bytes_out);
 

@@ -1174,16 +1174,24 @@ pcg_status pcg_kernel_times(pcg_ctx* c, int32_t n_iter, double* ms_out, double* 
         }
         CU(cudaGetLastError());
         CU(cudaStreamSynchronize(c->st));
-        double acc[4] = {0, 0, 0, 0};
+        // per-kernel MEDIAN over the iterations (robust to a stray slow launch, which would
+        // otherwise move the roofline to the wrong kernel)
+        std::vector<double> tk[4];
         for (int m = 0; m < n_iter; ++m) {
             float t01, t12, t23, t03;
             cudaEventElapsedTime(&t01, ev[4 * m + 0], ev[4 * m + 1]);
             cudaEventElapsedTime(&t12, ev[4 * m + 1], ev[4 * m + 2]);
             cudaEventElapsedTime(&t23, ev[4 * m + 2], ev[4 * m + 3]);
             cudaEventElapsedTime(&t03, ev[4 * m + 0], ev[4 * m + 3]);
-            acc[0] += t01; acc[1] += t12; acc[2] += t23; acc[3] += t03;
+            tk[0].push_back(t01); tk[1].push_back(t12); tk[2].push_back(t23); tk[3].push_back(t03);
         }
         for (auto& e : ev) cudaEventDestroy(e);
+        double acc[4];
+        for (int k = 0; k < 4; ++k) {
+            std::sort(tk[k].begin(), tk[k].end());
+            const size_t h = tk[k].size() / 2;
+            acc[k] = (tk[k].size() % 2 ? tk[k][h] : 0.5 * (tk[k][h - 1] + tk[k][h])) * n_iter;
+        }
         CU(cudaMemcpy(c->h_sc, c->sc, sizeof(DevScalars), cudaMemcpyDeviceToHost));
         if (c->h_sc->k < n_iter && !getenv("PCG_DIAG"))
             return Status::err(PCG_ERR_BREAKDOWN, "pcg_kernel_times: iteration stopped early");
