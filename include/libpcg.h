@@ -219,7 +219,7 @@ pcg_status pcg_partition(int32_t ni, int32_t nj, const uint8_t* mask, int32_t pa
  * tile.  Any output pointer may be NULL. */
 pcg_status pcg_layout(const pcg_ctx* ctx, int32_t* pitch, int32_t* block, int32_t* rows);
 
-/* Average device time (ms) of each per-iteration kernel over n_iter iterations run on the
+/* Device time (ms) of each per-iteration kernel over n_iter iterations run on the
  * context's stream with CUDA events around every launch, on the state left by the last
  * solve (a profiling aid for bench.py).  ms_out[0..3] = median per-launch time of K1
  * (stencil), K2 (r update + Z^T gather), K3 (Z gather), and of the whole iteration; bytes_out[0..2] = algorithmic bytes per
