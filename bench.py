@@ -317,7 +317,9 @@ def main():
                            "setup_s": rep["setup_s"], "setup_wall_s": setup_wall,
                            "bytes_per_iter_algorithmic": rep["bytes_per_iter"],
                            "device_bytes": S.device_bytes,
-                           "l2": "no flush: per-iteration working set (~280 MB) exceeds the 126 MB L2",
+                           "l2": ("no flush between steps: a step's data (~170 MB of static Z/Z^T/coefficient arrays + 94 MB "
+                                  "of vectors) exceeds the 126 MB L2; by design 7 of the 8 per-iteration vectors "
+                                  "stay in a persisting L2 window within a solve (DESIGN.md §4)"),
                            "parallelism": f"row blocks x{world}" if world > 1 else "1 GPU",
                            "kernels": ktimes},
                 "roofline": roof, "cpu_baseline": cpu,
