@@ -2132,6 +2132,9 @@ __global__ void __launch_bounds__(kTinyThreads, 1) tiny_kernel(const KArgs G) {
 }
 
 // ---- K2 (Jacobi / none): r -= alpha q ; s = r / A_pp (or r) ; (r, r), (s, r) ---------------
+#ifndef KD2_UNROLL
+#define KD2_UNROLL 2                 // measured at cfg4 (Jacobi): 1 / 2 / 4 / 8 -> 47.5 / 45.7 / 48.3 / 51.1 us/iteration
+#endif
 __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const int par, const int init,
                                                          const int none) {
     pdl_wait();
@@ -2153,21 +2156,38 @@ __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const in
     extern __shared__ double ws[];
     const double* __restrict__ ro = A.r[par];
     double* __restrict__ rn = A.r[par ^ 1];
-    const int64_t U = n_units(A);
+    const int64_t U = n_units(A), G = gridDim.x;
+    // KD2_UNROLL units of the block stride at once: every unit's three loads are issued before
+    // any unit computes (the body is too short to hide a memory latency per unit otherwise)
+    constexpr int NU = KD2_UNROLL;
     int k = 0;
-    for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k) {
-        const Unit W = unit_of(A, u);
-        double v1 = 0.0, v2 = 0.0;
-        if (W.inrow) {
-            const double rnew = __fma_rn(-alpha, A.q[W.a], ro[W.a]);
-            const double sv = none ? rnew : __ddiv_rn(rnew, A.diag[W.a]);
-            A.s[W.a] = sv;
-            rn[W.a] = rnew;
-            v1 = __dmul_rn(rnew, rnew);
-            v2 = __dmul_rn(sv, rnew);
+    for (int64_t u0 = blockIdx.x; u0 < U; u0 += NU * G, k += NU) {
+        Unit W[NU];
+        double qv[NU], rv[NU], dv[NU];
+#pragma unroll
+        for (int m = 0; m < NU; ++m) {
+            const int64_t u = u0 + m * G;
+            W[m] = unit_of(A, u < U ? u : u0);
+            const bool ld = u < U && W[m].inrow;
+            qv[m] = ld ? A.q[W[m].a] : 0.0;
+            rv[m] = ld ? ro[W[m].a] : 0.0;
+            dv[m] = (ld && !none) ? A.diag[W[m].a] : 1.0;
         }
-        put_warp_sum(ws, 2 * k, v1);
-        put_warp_sum(ws, 2 * k + 1, v2);
+#pragma unroll
+        for (int m = 0; m < NU; ++m) {
+            if (u0 + m * G >= U) break;
+            double v1 = 0.0, v2 = 0.0;
+            if (W[m].inrow) {
+                const double rnew = __fma_rn(-alpha, qv[m], rv[m]);
+                const double sv = none ? rnew : __ddiv_rn(rnew, dv[m]);
+                A.s[W[m].a] = sv;
+                rn[W[m].a] = rnew;
+                v1 = __dmul_rn(rnew, rnew);
+                v2 = __dmul_rn(sv, rnew);
+            }
+            put_warp_sum(ws, 2 * (k + m), v1);
+            put_warp_sum(ws, 2 * (k + m) + 1, v2);
+        }
     }
     pdl_trigger();
     if (finish_units<2>(A, ws, A.partial[1], A.partial[2], &A.sc->counter[1])) {
