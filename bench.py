@@ -42,10 +42,11 @@ WORKLOAD = "cfg4: ORCA025-like 1442x1021 grid, E-W periodic, ~17% land, AINV(tau
 
 def workload_name(args):
     """The default bench line is WORKLOAD; other preconditioners / configs are named as run."""
-    if args.config == "cfg4" and args.precond == "ainv" and args.tau == 0.1 and args.tol == 1e-10:
+    if args.config == "cfg4" and args.precond == "ainv" and args.tau == 0.1 and args.tol == 1e-10 and args.method == "pcg":
         return WORKLOAD
     pc = {"ainv": "AINV(tau=%g)" % args.tau, "jacobi": "Jacobi", "fsai": "FSAI(q=%d, the paper's P)" % args.fsai_q}[args.precond]
-    return "%s: %s PCG to ||r||/||b|| <= %g" % (args.config, pc, args.tol)
+    return "%s: %s %s to ||r||/||b|| <= %g" % (args.config, pc, "Chronopoulos-Gear PCG" if args.method == "cg1" else "PCG",
+                                               args.tol)
 
 
 def fallback_peak():
@@ -172,6 +173,8 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=150)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=60)
+    ap.add_argument("--method", default="pcg", choices=["pcg", "cg1"],
+                    help="cg1: Chronopoulos-Gear single-reduction PCG (one allgather per iteration across ranks)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -193,7 +196,7 @@ def main():
     p = synth.config(args.config)
     t0 = time.perf_counter()
     S = pcg.Solver(p.cE, p.cN, p.mask, tau=args.tau, precond=args.precond, group=group, device=local,
-                   fsai_q=args.fsai_q)
+                   fsai_q=args.fsai_q, flags=pcg.FLAG_SINGLE_REDUCTION if args.method == "cg1" else 0)
     setup_wall = time.perf_counter() - t0
     rows = slice(S.j_begin, S.j_end)
     xs = torch.from_numpy(np.ascontiguousarray(synth.xstar(p)[rows])).cuda()
@@ -252,7 +255,7 @@ def main():
     # roofline of the dominant kernel (single rank: per-kernel CUDA events on the launch stream)
     roof = None
     ktimes = None
-    if world == 1:
+    if world == 1 and args.method == "pcg":
         S.solve(b, tol=args.tol, maxit=maxit)
         ms, by = S.kernel_times(args.profile_iters)
         names = ["K1_stencil", "K2_ZTr", "K3_Zt"]
@@ -299,6 +302,8 @@ def main():
     fused = ktimes is not None and "K23_ZTr_Zt" in ktimes
     per_iter = 3 if args.precond in ("ainv", "fsai") and not fused else 2
     pro = 4 if args.precond in ("ainv", "fsai") and not fused else 3
+    if args.method == "cg1":
+        pro = 5                                                  # + KC's w0 = A u0 (alpha0)
     if world == 1:
         body = max(2, int(os.environ.get("PCG_BODY_ITERS", "8")) & ~1)
         launches = sum(pro + per_iter * body * math.ceil(k / body) + 2 for k in iters)
