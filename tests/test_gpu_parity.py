@@ -678,3 +678,30 @@ def test_cfg4_full_size_other_preconditioners(precond):
     assert rep["converged"] == 1 and rep["true_rel_residual"] < 2e-10
     assert abs(k - (3004 if precond == "fsai" else 2618)) <= 30
     S.close()
+
+
+def test_timestep_warm_modes_and_aliasing():
+    """pcg_extrapolate may write over either input; every warm mode of the driver converges, and
+    the first guesses order the iteration counts (zero >= previous >= extrapolate, summed)."""
+    from paper_1210_1878_b200 import timestep
+    p = synth.config("cfg2")
+    S = pcg.Solver(p.cE, p.cN, p.mask, tau=TAU)
+    rng = np.random.default_rng(4)
+    a, b = rng.standard_normal((p.nj, p.ni)), rng.standard_normal((p.nj, p.ni))
+    ta, tb = dev(a), dev(b)
+    S.extrapolate(ta, tb, ta)                                 # x0 aliases x_t
+    assert np.array_equal(host(ta), 2.0 * a - b)
+    tb2 = dev(b)
+    S.extrapolate(dev(a), tb2, tb2)                           # x0 aliases x_tm1
+    assert np.array_equal(host(tb2), 2.0 * a - b)
+    series = [S.apply_operator(dev(f)) for f in synth.forcing_series(p, 6)]
+    its = {}
+    for warm in timestep.WARM:
+        st = timestep.Stepper(S, warm)
+        its[warm] = 0
+        for bn in series:
+            x, k, rep = st.step(bn, tol=1e-10)
+            assert rep["converged"] == 1
+            its[warm] += k
+    assert its["zero"] >= its["previous"] >= its["extrapolate"]
+    S.close()
