@@ -111,6 +111,34 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(inside), "sampled_over": which}
 
 
+def nnz_operator(p):
+    """Entries of the assembled 5-point A (Eq. 9-10): one diagonal per ocean point and
+    two per coupled ocean pair (E-W across the periodic seam when periodic, N-S within the grid)."""
+    m = p.mask.astype(bool)
+    ew = m & np.roll(m, -1, axis=1) & (p.cE != 0)
+    if not p.periodic:
+        ew[:, -1] = False
+    ns = m[:-1] & m[1:] & (p.cN[:-1] != 0)
+    return int(m.sum() + 2 * (ew.sum() + ns.sum()))
+
+
+def flop_model(p, precond, nnz_off, iterations):
+    """SPEC S:387 (paper section 5, "we count ... the complexity of all linear algebra operations
+    involved"): per iteration 2 nnz(A) for the A-product, 2 nnz(Z) + 2 nnz(Z^T) for the factored
+    preconditioner (or n for the diagonal one), plus 10 n for the BLAS-1 work of Alg. 1.  The D^-1
+    scale of z = Z D^-1 Z^T r is counted as n more.  nnz_off = off-diagonal entries of Z."""
+    n = int(p.mask.astype(bool).sum())
+    pre = {"ainv": 4 * (n + nnz_off) + n, "fsai": 4 * (n + nnz_off) + n, "jacobi": n, "none": 0}[precond]
+    return iterations * (2 * nnz_operator(p) + pre + 10 * n)
+
+
+# The paper's one performance figure (BASELINE.md: P:488, P:515, P:534) -- context, not a target.
+PAPER_CONTEXT = {"paper_gflops_gpu": 87.0, "paper_gflops_cpu": 1.43,
+                 "paper_hw": "fp32; 1 GPU of a Tesla S2050 (Fermi) vs one Xeon E5620 core (serial C); "
+                             "banded-T FSAI P on the unmasked ORCA-025 band matrix (P:488, P:515, P:534)",
+                 "note": "context only: different matrix (no mask/wrap), precision and, for AINV, preconditioner"}
+
+
 def cpu_oracle_sample(p, tau, n_iter):
     """The oracle as it stands (plain C, single thread) on a bounded sample of the workload:
     assembly + AINV setup, then n_iter PCG iterations (tol = 0)."""
@@ -331,6 +359,11 @@ def main():
                 "e2e": {"value": e_iters / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                         "d2h_bytes_per_step": nbytes},
                 "gpu_launches": launches, "clocks": clk.summary()}
+        if world == 1:
+            fl = flop_model(p, args.precond, int(rep["nnz_z"]), 1)
+            line["paper_context"] = {"flops_per_iter": fl, "gflops": fl * value / 1e9,
+                                     "flop_model": "SPEC S:387: 2nnz(A) + 2nnz(Z) + 2nnz(Z^T) (+n D^-1) + 10n",
+                                     **PAPER_CONTEXT}
         print(json.dumps(line), flush=True)
     S.close()
     if world > 1:
