@@ -838,6 +838,11 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         const char* e = getenv("PCG_FSAI_DIA");
         if (!(e && atoi(e) == 0) && P.dia_q <= 16) A.dia_q = P.dia_q;   // wider bands: ELL path
     }   // kernels: 0 = factored Z D^-1 Z^T (AINV, FSAI)
+    // K1 form: without the L2 window (vectors streamed from HBM, cfg5) the 4-row strip form's
+    // register march re-uses the N/S rows and measured faster (632-635 against 639-658 us per
+    // iteration at cfg5); with the window the row-segment form wins (80.7 against 83.2 at cfg4).
+    // Both forms are bitwise equal.  PCG_K1FLAT overrides.
+    if (P.factored() && !c->multi && A.l2_bytes == 0 && A.k1flat == 2 && !getenv("PCG_K1FLAT")) A.k1flat = 0;
     // redundant-sum mode (kernels.h): one rank, the K1 row-segment form, K2 / K3 as two launches
     A.redundant = 0;
     if (P.factored() && !c->multi && !A.fuse23 && (A.k1flat == 2 || A.k1flat == 3 || (A.k1flat == 0 && !A.dynamic_k1)) && !A.tma) {
