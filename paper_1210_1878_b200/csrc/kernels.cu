@@ -588,6 +588,10 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
     pdl_trigger();
     TL(0, 2);
     if (A.redundant) return;                           // (d, q) is summed by K2's blocks
+    if (A.red_gamma) {                                 // Jacobi / none: k2_diag's blocks sum (d, q)
+        if (blockIdx.x == 0 && threadIdx.x == 0) A.sc->xpend = 0;   // x += alpha_prev d_old done
+        return;
+    }
     if (count_block(&A.sc->counter[0])) {
         const double tot = final_sum(A.partial[0], n_units(A));
         if (threadIdx.x == 0) {

@@ -841,8 +841,8 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     // K1 form: without the L2 window (vectors streamed from HBM, cfg5) the 4-row strip form's
     // register march re-uses the N/S rows and measured faster (632-635 against 639-658 us per
     // iteration at cfg5); with the window the row-segment form wins (80.7 against 83.2 at cfg4).
-    // Both forms are bitwise equal.  PCG_K1FLAT overrides.
-    if (P.factored() && !c->multi && A.l2_bytes == 0 && A.k1flat == 2 && !getenv("PCG_K1FLAT")) A.k1flat = 0;
+    // Both forms are bitwise equal (all preconditioners).  PCG_K1FLAT overrides.
+    if (!c->multi && A.l2_bytes == 0 && A.k1flat == 2 && !getenv("PCG_K1FLAT")) A.k1flat = 0;
     // redundant-sum mode (kernels.h): one rank, the K1 row-segment form, K2 / K3 as two launches
     A.redundant = 0;
     if (P.factored() && !c->multi && !A.fuse23 && (A.k1flat == 2 || A.k1flat == 3 || (A.k1flat == 0 && !A.dynamic_k1)) && !A.tma) {
@@ -851,7 +851,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     }
     // Jacobi / none: the (d, q) half of the redundant-sum mode (K2's blocks form it, K1 has no tail)
     A.red_gamma = 0;
-    if (!P.factored() && !c->multi && A.k1flat == 2) {
+    if (!P.factored() && !c->multi && (A.k1flat == 2 || (A.k1flat == 0 && !A.dynamic_k1))) {
         const char* re = getenv("PCG_REDUNDANT");
         A.red_gamma = re ? atoi(re) != 0 : 1;
     }

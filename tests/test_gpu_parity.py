@@ -464,6 +464,22 @@ def test_kernel_variants_bitwise_canonical(name, variant, monkeypatch):
     S.close()
 
 
+@pytest.mark.parametrize("env", [{"PCG_K1FLAT": "0"}, {"PCG_L2PERSIST": "0"}, {}])
+@pytest.mark.parametrize("precond", ["jacobi", "none"])
+def test_diag_k1_forms_bitwise_canonical(precond, env, monkeypatch):
+    """Jacobi / none on the graph path (cfg3) with either K1 form: the 4-row strips (forced, or
+    picked by the library when the L2 window is off) and the row segments feed k2_diag's (d, q)
+    sums the same partials, so the solve is bitwise the oracle's canonical PCG."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    p = synth.config("cfg3")
+    A, S, ref, x, k, hist, rep, _ = _canonical_pair(p, precond, 1e-10)
+    assert k == ref.iterations and np.array_equal(hist, ref.hist)
+    assert np.array_equal(x, A.to_grid(ref.x))
+    assert rep["true_rel_residual"] == ref.true_rel_residual
+    S.close()
+
+
 @pytest.mark.parametrize("P", [2, 3])
 def test_local_ranks_k23_bitwise(P, monkeypatch):
     """K23 on block-local Z (w = 0) across P in-process ranks = the oracle's partitioned mode."""
