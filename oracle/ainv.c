@@ -196,6 +196,27 @@ static int64_t ainv_sparse(const lcsr* A, double tau, int32_t fill, cstore* Z, d
     return fail;
 }
 
+/* The dense formulation's own P_B2 selection (independent of keep_largest's sort, so the two
+ * formulations cross-check the rule, not just the update sequence): fill-1 rounds, each picking
+ * the present off-diagonal entry of largest |z| by an ascending scan with a strict '>' (ties go
+ * to the smaller row index, R26); every present off-diagonal entry not picked is dropped. */
+static void dense_keep(char* pres, double* z, int64_t j, int64_t n, int32_t fill, int64_t* mark) {
+    int64_t cnt = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        mark[k] = 0;
+        if (k != j && pres[k]) ++cnt;
+    }
+    if (cnt <= (int64_t)fill - 1) return;
+    for (int32_t r = 0; r < fill - 1; ++r) {
+        int64_t best = -1;
+        for (int64_t k = 0; k < n; ++k)
+            if (k != j && pres[k] && !mark[k] && (best < 0 || fabs(z[k]) > fabs(z[best]))) best = k;
+        mark[best] = 1;
+    }
+    for (int64_t k = 0; k < n; ++k)
+        if (k != j && pres[k] && !mark[k]) { pres[k] = 0; z[k] = 0.0; }
+}
+
 /* Dense right-looking AINV (cross-check; n small): for i = 0..n-1: p_i = a^_i^T z_i;
  * for j > i: pi = a^_i^T z_j; skip if 0; z_j -= (pi/p_i) z_i; drop touched entries. */
 static int64_t ainv_dense(const lcsr* A, double tau, int32_t fill, cstore* Z, double* p) {
@@ -236,13 +257,7 @@ static int64_t ainv_dense(const lcsr* A, double tau, int32_t fill, cstore* Z, do
                 int64_t k = touched[t];
                 if (k != j && fabs(zj[k]) < tau) { pj_[k] = 0; zj[k] = 0.0; }
             }
-            if (fill > 0) {
-                int64_t cnt = 0;
-                for (int64_t k = 0; k < n; ++k)
-                    if (k != j && pj_[k]) touched[cnt++] = k;
-                const int64_t ndrop = keep_largest(touched, cnt, zj, fill);
-                for (int64_t t = cnt - ndrop; t < cnt; ++t) { pj_[touched[t]] = 0; zj[touched[t]] = 0.0; }
-            }
+            if (fill > 0) dense_keep(pj_, zj, j, n, fill, touched);
         }
     }
     cs_init(Z, n);

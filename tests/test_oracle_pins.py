@@ -411,6 +411,12 @@ def test_finite_termination():
     assert worst <= 2
 
 
+def eq11_bound(mu, m):
+    """Eq. 11 (P:145-150): 2 ((sqrt(mu) - 1) / (sqrt(mu) + 1))^(m-1)."""
+    q = (math.sqrt(mu) - 1) / (math.sqrt(mu) + 1)
+    return 2 * q ** (m - 1)
+
+
 def test_eq11_bound_and_monotone_anorm():
     """Eq. 11 (P:145-150): ||x - x_m||_A < 2((sqrt(mu)-1)/(sqrt(mu)+1))^(m-1) ||x - x_0||_A
     for plain CG; the A-norm error decreases monotonically."""
@@ -424,18 +430,17 @@ def test_eq11_bound_and_monotone_anorm():
     anorm = lambda e: math.sqrt(e @ D @ e)
     e0 = anorm(xs)
     prev = e0
-    q = (math.sqrt(mu) - 1) / (math.sqrt(mu) + 1)
     for m in range(1, A.n):
         r = oracle.pcg(A, b, "none", None, tol=0.0, maxit=m)
         em = anorm(xs - r.x)
         if em < 1e-12 * e0:
             break
-        assert em < 2 * q ** (m - 1) * e0
+        assert em < eq11_bound(mu, m) * e0
         assert em <= prev * (1 + 1e-12)
         prev = em
+    # the bound helper used above, at SPEC's printed example (printed to 3 digits)
     g = GOLD["convergence_bound_100_51"]
-    qq = (math.sqrt(g["mu2"]) - 1) / (math.sqrt(g["mu2"]) + 1)
-    assert abs(2 * qq ** (g["m"] - 1) - g["value"]) / g["value"] < g["rtol"]
+    assert abs(eq11_bound(g["mu2"], g["m"]) - g["value"]) <= g["atol"]
 
 
 def test_cfg1_cg_jacobi_ainvinf_bitwise():
@@ -487,16 +492,30 @@ def test_pcg_edge_cases():
         oracle.pcg(A, b, "ainv", M, -1.0)
 
 
-def test_canonical_dot_is_exact_on_integers():
-    """The canonical block-tree order sums integer-valued products exactly."""
+@pytest.mark.parametrize("parts,rows", [(1, 1), (3, 1), (1, 4)])
+def test_canonical_dot_pins(parts, rows):
+    """The canonical-order dot product (DESIGN.md §5.2/§5.5) against exact arithmetic:
+    integer-valued products whose partial sums stay below 2^53 must come out EXACTLY (Python
+    ints, any order); random fp64 data must lie within the worst-case bound
+    |fl(s) - s| <= (n-1) u sum|a_i b_i| of the exactly rounded sum (math.fsum)."""
     p = synth.config("cfg2")
     A = oracle.assemble(p)
     rng = np.random.default_rng(1)
-    # jacobi PCG with tol=0, maxit=0 exposes nothing; test through a 0-iteration run:
-    # hist[0] = sqrt((r,r))/sqrt((b,b)) with x0 = 0 -> r = b -> exactly 1.0 in any order
-    b = rng.integers(-1000, 1000, A.n).astype(float)
-    r = oracle.pcg(A, b, "none", None, 0.0, maxit=0, mode="canonical", pitch=192)
-    assert r.hist[0] == 1.0
+    a = rng.integers(-2 ** 20, 2 ** 20, A.n)
+    b = rng.integers(-2 ** 20, 2 ** 20, A.n)
+    exact = sum(int(x) * int(y) for x, y in zip(a, b))
+    got = A.dot_canonical(a.astype(float), b.astype(float), pitch=192, parts=parts, rows=rows)
+    assert got == float(exact)
+    x, y = rng.standard_normal(A.n), rng.standard_normal(A.n)
+    ref = math.fsum(float(u) * float(v) for u, v in zip(x, y))
+    got = A.dot_canonical(x, y, pitch=192, parts=parts, rows=rows)
+    bound = (A.n - 1) * 2.0 ** -53 * float(np.sum(np.abs(x * y))) + 2.0 ** -53 * abs(ref)
+    assert abs(got - ref) <= bound
+    # and the canonical order is not the sequential one (the bound is not vacuous)
+    seq = 0.0
+    for u, v in zip(x, y):
+        seq = seq + float(u) * float(v)
+    assert got != seq
 
 
 @pytest.mark.parametrize("name", ["cfg2"])
