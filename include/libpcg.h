@@ -229,6 +229,13 @@ pcg_status pcg_kernel_times(pcg_ctx* ctx, int32_t n_iter, double* ms_out, double
 /* Device bytes allocated by the context. */
 int64_t pcg_device_bytes(const pcg_ctx* ctx);
 
+/* Device time (ms, CUDA events on the context's stream) of the resident-strip loop kernel of the
+ * last pcg_solve -- one persistent cooperative launch that runs every PCG iteration (DESIGN.md
+ * §7.4) -- and the iterations it ran.  *ms = -1 when the last solve did not use that driver
+ * (several ranks, the host loop, the graph or cooperative-loop drivers).  Host pointers; iterations
+ * may be NULL.  PCG_ERR_ARG on a NULL ctx or ms. */
+pcg_status pcg_loop_time(const pcg_ctx* ctx, double* ms, int32_t* iterations);
+
 /* ---------------------------------------------------------------- host-only setup
  * The host half of pcg_setup (validation, partition, anchor check, AINV, SELL packing),
  * usable without a GPU; tests compare it bit for bit with the oracle. */

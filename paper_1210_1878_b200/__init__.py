@@ -65,7 +65,7 @@ class Report(C.Structure):
 
 
 EXPORTS = ["pcg_setup", "pcg_solve", "pcg_solve_host", "pcg_solve_local_ranks", "pcg_free", "pcg_last_error", "pcg_apply_operator",
-           "pcg_apply_preconditioner", "pcg_extrapolate", "pcg_partition", "pcg_layout", "pcg_kernel_times", "pcg_device_bytes",
+           "pcg_apply_preconditioner", "pcg_extrapolate", "pcg_partition", "pcg_layout", "pcg_kernel_times", "pcg_device_bytes", "pcg_loop_time",
            "pcg_plan_build", "pcg_plan_free", "pcg_plan_counts", "pcg_plan_export_zhat",
            "pcg_comm_unique_id", "pcg_comm_init_rank", "pcg_comm_destroy"]
 
@@ -95,6 +95,7 @@ def lib():
     L.pcg_layout.argtypes = [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]
     L.pcg_kernel_times.argtypes = [vp, i32, vp, vp]
     L.pcg_device_bytes.argtypes = [vp]; L.pcg_device_bytes.restype = i64
+    L.pcg_loop_time.argtypes = [vp, C.POINTER(d), C.POINTER(i32)]
     L.pcg_plan_build.argtypes = [C.POINTER(Coeffs), C.POINTER(Grid), C.POINTER(Opts), C.POINTER(vp)]
     L.pcg_plan_free.argtypes = [vp]; L.pcg_plan_free.restype = None
     L.pcg_plan_counts.argtypes = [vp, vp]
@@ -299,6 +300,13 @@ class Solver:
         by = np.zeros(3)
         _check(lib().pcg_kernel_times(self._h, int(n_iter), _ptr(ms), _ptr(by)), self._h, "pcg_kernel_times")
         return ms, by
+
+    def loop_time(self):
+        """(ms, iterations) of the resident-strip loop kernel in the last solve; ms = -1 when the
+        solve used another driver (pcg_loop_time)."""
+        ms, it = C.c_double(-1.0), C.c_int32(0)
+        _check(lib().pcg_loop_time(self._h, C.byref(ms), C.byref(it)), self._h, "pcg_loop_time")
+        return ms.value, it.value
 
     @property
     def device_bytes(self):

@@ -43,6 +43,33 @@ struct SzDev {
     const double* run = nullptr;
 };
 
+// Resident-strip driver (rs.cu): one persistent cooperative block of kRsThreads
+// per SM runs the whole PCG loop.  Block b owns a contiguous range of units (row segments, in
+// row-major order) per phase -- ub1 for the K1 phase (stencil), ub2 for the K2/K3 phase
+// (preconditioner) -- and keeps the vector that phase gathers from (d, r_new, t) for its range
+// plus the halo its stencil / Z rows reach in shared memory, so every gather is a shared-memory
+// load.  Two grid barriers per iteration (the two dot products of Alg. 1) and one neighbour flag
+// (t rows of the blocks to the north).
+#ifndef RS_THREADS
+#define RS_THREADS 512
+#endif
+constexpr int kRsThreads = RS_THREADS;
+struct RsDev {
+    int32_t on;                   // eligible and enabled
+    int32_t nblk;                 // blocks (= SMs, one resident block each)
+    int32_t cap;                  // shared-memory buffer (doubles)
+    int32_t maxu1, maxu2;         // most units of one block per phase
+    int32_t maxnx;                // most 32-element chunks any pass of one block touches
+    size_t smem;                  // dynamic shared memory per block (bytes)
+    const int32_t* ub1;     // [nblk + 1] K1-phase unit bounds
+    const int32_t* ub2;     // [nblk + 1] K2/K3-phase unit bounds
+    const int64_t* lo2;     // [nblk] first array index of the r_new buffer (Z^T reach)
+    const int64_t* hi2;     // [nblk] end of the t buffer (Z reach)
+    const int32_t* wait2;   // [nblk] last block whose t this block gathers
+    uint32_t* sync;         // [0] grid-barrier counter, [1 + b] t-ready stamp of block b
+    const int64_t* pf;      // [nblk][4] SELL overflow entry range of each block (Z^T first, count, Z first, count)
+};
+
 struct KArgs {
     int32_t ni, pitch, nloc, nranks;
     int32_t halo;                     // halo grid rows on each side (owned row j at array row j + halo)
@@ -100,6 +127,7 @@ struct KArgs {
     void* l2_base;                    // persisting L2 access-policy window of the iteration kernels
     size_t l2_bytes;                  // (0: none)
     float l2_ratio;
+    RsDev rs;                         // resident-strip driver (rs.on = 0: not used)
 };
 
 int64_t grid_blocks(const KArgs& A);
@@ -124,5 +152,9 @@ void launch_set_cond(cudaGraphConditionalHandle h, cudaStream_t st);
 void launch_extrapolate(const double* xt, const double* xm, double* x0, int64_t n, cudaStream_t st);
 void configure_kernels(KArgs& A, int sms);
 cudaError_t launch_loop(const KArgs& A, cudaStream_t st);   // whole PCG loop, cooperative (1 rank)
+cudaError_t launch_rs(const KArgs& A, cudaStream_t st);     // whole PCG loop, resident strips (rs.cu)
+const void* rs_kernel_fn(const KArgs& A);                  // the rs kernel a launch_rs call uses
+int rs_timeline(unsigned long long* out, int nblk);       // -DRS_TIMELINE builds: pass durations
+size_t rs_smem_bytes(int32_t cap, int32_t maxu1, int32_t maxu2, int32_t maxnx);   // dynamic smem of rs_loop_kernel
 
 }  // namespace pcg

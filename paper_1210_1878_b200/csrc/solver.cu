@@ -63,6 +63,9 @@ struct pcg_ctx {
     bool graph_built = false;
     bool graph_failed = false;         // NCCL path: capture not possible here -> host loop
     cudaEvent_t ev_in = nullptr, ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t ev_l0 = nullptr, ev_l1 = nullptr;   // around the resident-strip loop kernel
+    float loop_ms = -1.f;                           // its duration in the last solve (-1: not used)
+    int32_t loop_iters = 0;
     std::string err;
     double bytes_k[3] = {0, 0, 0};
     bool solved_once = false;
@@ -116,7 +119,16 @@ int l2_users(int device, int delta) {
     return users[device] += delta;
 }
 
+// One rank: the resident-strip loop kernel (rs.cu) when setup found it eligible (its shared-
+// memory ranges fit); PCG_RS=0 disables it.
+bool use_rs(const pcg_ctx* c) {
+    if (c->multi || c->A.cgcg || !c->A.rs.on || (c->plan.flags & PCG_FLAG_HOST_LOOP)) return false;
+    const char* e = getenv("PCG_RS");
+    return !(e && atoi(e) == 0);
+}
+
 bool use_fused(const pcg_ctx* c) {
+    if (use_rs(c)) return false;
     if (c->multi || c->A.cgcg || (c->plan.flags & PCG_FLAG_HOST_LOOP)) return false;
     if (const char* e = getenv("PCG_FUSED")) return atoi(e) != 0;
     // measured with the current graph (redundant sums, 8-iteration body): factored preconditioners
@@ -137,6 +149,7 @@ bool multi_graph(const pcg_ctx* c) {
 }
 bool use_graph(const pcg_ctx* c) {
     if (c->multi) return multi_graph(c);
+    if (use_rs(c)) return false;
     return !(c->plan.flags & PCG_FLAG_HOST_LOOP) && !use_fused(c);
 }
 
@@ -496,7 +509,23 @@ Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, doubl
     CU(cudaMemcpy2DAsync(c->b + P.hoff(), dp, b, sp, sp, (size_t)P.nloc, kin, c->st));
     if (x0) CU(cudaMemcpy2DAsync(c->x + P.hoff(), dp, x0, sp, sp, (size_t)P.nloc, kin, c->st));
     else CU(cudaMemsetAsync(c->x + P.hoff(), 0, (size_t)P.nloc * dp, c->st));
-    if (use_fused(c)) {
+    c->loop_ms = -1.f;
+    if (use_rs(c)) {
+        const int32_t red = c->A.redundant, redg = c->A.red_gamma;   // the rs kernel keeps its own scalars
+        c->A.redundant = 0;
+        c->A.red_gamma = 0;
+        Status s = launch_prologue(c);
+        if (s) {
+            CU(cudaMemsetAsync(c->A.rs.sync, 0, (size_t)(c->A.rs.nblk + 1) * sizeof(uint32_t), c->st));
+            CU(cudaEventRecord(c->ev_l0, c->st));
+            CU(launch_rs(c->A, c->st));
+            CU(cudaEventRecord(c->ev_l1, c->st));
+            s = launch_epilogue(c);
+        }
+        c->A.redundant = red;
+        c->A.red_gamma = redg;
+        if (!s) return s;
+    } else if (use_fused(c)) {
         const int32_t red = c->A.redundant, redg = c->A.red_gamma;   // the loop kernel keeps its own scalars
         c->A.redundant = 0;
         c->A.red_gamma = 0;
@@ -548,6 +577,10 @@ Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, doubl
     CU(cudaStreamSynchronize(c->st));
     float ms = 0.f;
     cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+    if (use_rs(c)) {
+        cudaEventElapsedTime(&c->loop_ms, c->ev_l0, c->ev_l1);
+        c->loop_iters = k;
+    }
     if (iterations) *iterations = k;
     if (res_hist) std::memcpy(res_hist, c->h_hist, (size_t)std::min(nh, hist_cap) * sizeof(double));
     pcg_report R{};
@@ -569,6 +602,179 @@ Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, doubl
     return Status::ok();
 }
 
+// Resident-strip driver (rs.cu): partition the units into one contiguous range
+// per block and phase, balanced by a cost model, and size the shared-memory buffer for the widest
+// range plus the halo its stencil (one row each way) or Z rows (the reach of Z^T / Z) need.  Not
+// eligible (A.rs.on = 0): several ranks, Chronopoulos-Gear, the FSAI DIA form, int32 ELL columns,
+// 2^31 or more elements, or a range that does not fit in shared memory (cfg5).
+Status setup_rs(pcg_ctx* c) {
+    KArgs& A = c->A;
+    const Plan& P = c->plan;
+    A.rs = RsDev{};
+    if (c->multi || A.cgcg || A.dia_q > 0) return Status::ok();
+    if (const char* e = getenv("PCG_RS")) if (atoi(e) == 0) return Status::ok();
+    const bool fac = P.factored();
+    if (fac && (!A.zt.col16 || !A.z.col16)) return Status::ok();
+    if (P.elements() >= ((int64_t)1 << 31) || P.pitch >= 65536) return Status::ok();
+    int sms = 148, optin = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device);
+    const int64_t U = (int64_t)P.nloc * A.nbx;
+    if (U < sms) return Status::ok();                   // fewer units than blocks: the loop kernel
+    const int nblk = sms;
+    const int W = kBlock / 32;
+    auto Lof = [](const Ell& E, int64_t sl) { return (E.ovf.off[(size_t)sl + 1] - E.ovf.off[(size_t)sl]) >> 5; };
+    // Cost model per unit, in units of one ocean chunk's passes: a chunk with ocean points costs 1
+    // per phase (its streams), an all-land chunk 0.3 (the mask test and loop overhead); K2/K3 add
+    // 0.15 per overflow entry per lane (Z^T and Z: 12 bytes each against ~80 bytes of an ELL
+    // element's streams -- the pole rows' long tails).
+    std::vector<double> c1((size_t)U), c2((size_t)U);
+    for (int64_t m = 0; m < U; ++m) {
+        const int64_t j = m / A.nbx, bx = m % A.nbx;
+        double k1 = 0.0, k2 = 0.0;
+        for (int w = 0; w < W; ++w) {
+            const int64_t i0 = bx * kBlock + 32 * w;
+            if (i0 >= P.pitch) break;
+            bool ocean = false;
+            for (int l = 0; l < 32 && !ocean; ++l) {
+                const int64_t i = i0 + l;
+                ocean = i < P.ni && !std::signbit(P.cN[(size_t)(j + P.halo) * P.pitch + i]);
+            }
+            k1 += ocean ? 1.0 : 0.3;
+            k2 += ocean ? (fac ? 2.0 : 1.0) : 0.3;
+            if (fac && ocean) {
+                const int64_t sl = (j * P.pitch + i0) >> 5;
+                k2 += 0.15 * (double)(Lof(P.ZT, sl) + Lof(P.Z, sl));
+            }
+        }
+        c1[(size_t)m] = k1;
+        c2[(size_t)m] = k2;
+    }
+    auto len = [&](int64_t m) { const int64_t bx = m % A.nbx; return (int64_t)std::min<int64_t>(kBlock, P.pitch - bx * kBlock); };
+    auto split = [&](const std::vector<double>& cost, double wlen, std::vector<int32_t>& ub) {
+        std::vector<double> pre((size_t)U + 1, 0.0);
+        for (int64_t m = 0; m < U; ++m) pre[(size_t)m + 1] = pre[(size_t)m] + cost[(size_t)m] + wlen * (double)len(m) / 32.0;
+        ub.assign((size_t)nblk + 1, 0);
+        for (int b = 1; b < nblk; ++b) {
+            const double tgt = pre[(size_t)U] * (double)b / (double)nblk;
+            int64_t m = std::lower_bound(pre.begin(), pre.end(), tgt) - pre.begin();
+            ub[(size_t)b] = (int32_t)std::max<int64_t>(ub[(size_t)b - 1], std::min<int64_t>(m, U));
+        }
+        ub[(size_t)nblk] = (int32_t)U;
+    };
+    auto a0 = [&](int64_t m) { return (m / A.nbx + P.halo) * (int64_t)P.pitch + (m % A.nbx) * kBlock; };
+    const size_t limit = (size_t)optin - 2048;
+    // phase 1: the stencil reaches one grid row each way
+    std::vector<int32_t> ub1, ub2;
+    int32_t maxu1 = 1, maxu2 = 1;
+    int64_t cap1 = 0;
+    for (double wl = 0.0;; wl = wl == 0.0 ? 0.25 : 2.0 * wl) {
+        split(c1, wl, ub1);
+        cap1 = 0; maxu1 = 1;
+        for (int b = 0; b < nblk; ++b) {
+            const int64_t e0 = a0(ub1[(size_t)b]), e1 = a0(ub1[(size_t)b + 1]);
+            maxu1 = std::max<int32_t>(maxu1, ub1[(size_t)b + 1] - ub1[(size_t)b]);
+            if (e1 > e0) cap1 = std::max<int64_t>(cap1, e1 - e0 + 2 * (int64_t)P.pitch);
+        }
+        if (rs_smem_bytes((int32_t)cap1, maxu1, maxu1, (int32_t)(cap1 / 32 + 2)) <= limit || wl > 1e6) break;
+    }
+    // phase 2: r_new from the lowest Z^T column of the range, t up to the highest Z column
+    std::vector<int64_t> lo2((size_t)nblk), hi2((size_t)nblk);
+    std::vector<int32_t> wait2((size_t)nblk);
+    int64_t cap = cap1, maxnx = 1;
+    for (double wl = 0.0;; wl = wl == 0.0 ? 0.25 : 2.0 * wl) {
+        split(c2, wl, ub2);
+        cap = cap1; maxu2 = 1;
+        for (int b = 0; b < nblk; ++b) {
+            const int64_t f0 = a0(ub2[(size_t)b]), f1 = a0(ub2[(size_t)b + 1]);
+            maxu2 = std::max<int32_t>(maxu2, ub2[(size_t)b + 1] - ub2[(size_t)b]);
+            int64_t lo = f0, hi = f1;
+            if (fac && f1 > f0) {
+                for (int64_t e = f0 - P.hoff(); e < f1 - P.hoff(); ++e)
+                    for (int m = 0; m < kEll; ++m) {
+                        lo = std::min<int64_t>(lo, P.ZT.col[(size_t)e * kEll + m]);
+                        hi = std::max<int64_t>(hi, (int64_t)P.Z.col[(size_t)e * kEll + m] + 1);
+                    }
+                for (int64_t sl = (f0 - P.hoff()) >> 5; sl < (f1 - P.hoff()) >> 5; ++sl) {
+                    for (int64_t o = P.ZT.ovf.off[(size_t)sl]; o < P.ZT.ovf.off[(size_t)sl + 1]; ++o)
+                        lo = std::min<int64_t>(lo, P.ZT.ovf.col[(size_t)o]);
+                    for (int64_t o = P.Z.ovf.off[(size_t)sl]; o < P.Z.ovf.off[(size_t)sl + 1]; ++o)
+                        hi = std::max<int64_t>(hi, (int64_t)P.Z.ovf.col[(size_t)o] + 1);
+                }
+                lo &= ~(int64_t)31;
+                const int64_t hr = (hi + 31) & ~(int64_t)31;    // the kernel copies t in whole chunks
+                cap = std::max<int64_t>(cap, std::max<int64_t>(f1 - lo, hr - f0));
+            }
+            lo2[(size_t)b] = lo;
+            hi2[(size_t)b] = hi;
+        }
+        // chunks (32 elements) whose mask and column a block keeps in shared memory (same rule as
+        // rs_loop_kernel): [K1 range - one row, K1 range + one row) u [lo2, hi2 rounded up)
+        maxnx = 1;
+        for (int b = 0; b < nblk; ++b) {
+            const int64_t e0 = a0(ub1[(size_t)b]), e1 = a0(ub1[(size_t)b + 1]);
+            const int64_t f0 = a0(ub2[(size_t)b]), f1 = a0(ub2[(size_t)b + 1]);
+            int64_t xlo = INT64_MAX, xhi = 0;
+            if (e1 > e0) { xlo = e0 - P.pitch; xhi = e1 + P.pitch; }
+            if (f1 > f0) { xlo = std::min(xlo, lo2[(size_t)b]); xhi = std::max(xhi, (hi2[(size_t)b] + 31) & ~(int64_t)31); }
+            if (xhi > xlo) maxnx = std::max<int64_t>(maxnx, (xhi - xlo) >> 5);
+        }
+        if (rs_smem_bytes((int32_t)cap, maxu1, maxu2, (int32_t)maxnx) <= limit || wl > 1e6) break;
+    }
+    for (int b = 0; b < nblk; ++b) {
+        int32_t w2 = b;
+        while (w2 + 1 < nblk && a0(ub2[(size_t)w2 + 1]) < hi2[(size_t)b]) ++w2;
+        wait2[(size_t)b] = w2;
+    }
+    const size_t smem = rs_smem_bytes((int32_t)cap, maxu1, maxu2, (int32_t)maxnx);
+    if (smem > limit) {
+        if (getenv("PCG_VERBOSE")) fprintf(stderr, "libpcg: resident strips need %zu B of shared memory (> %zu): off\n", smem, limit);
+        return Status::ok();
+    }
+    RsDev r{};
+    // each block's range of SELL overflow entries (bulk-prefetched into L2 at the start of phase 2)
+    std::vector<int64_t> pf((size_t)nblk * 4, 0);
+    if (fac) {
+        for (int b = 0; b < nblk; ++b) {
+            const int64_t s0 = (a0(ub2[(size_t)b]) - P.hoff()) >> 5, s1 = (a0(ub2[(size_t)b + 1]) - P.hoff()) >> 5;
+            if (s1 <= s0) continue;
+            int w = 0;
+            for (const Ell* E : {&P.ZT, &P.Z}) {
+                // entries [off[s0], off[s1]) -- a multiple of 32 entries (whole slices), so both the
+                // 8-byte values and the 4-byte columns span multiples of 16 bytes from 128-byte-aligned
+                // slice starts
+                pf[(size_t)b * 4 + 2 * w] = E->ovf.off[(size_t)s0];
+                pf[(size_t)b * 4 + 2 * w + 1] = E->ovf.off[(size_t)s1] - E->ovf.off[(size_t)s0];
+                ++w;
+            }
+        }
+    }
+    int32_t *d_ub1 = nullptr, *d_ub2 = nullptr, *d_w2 = nullptr;
+    int64_t *d_lo = nullptr, *d_hi = nullptr, *d_pf = nullptr;
+    uint32_t* d_sync = nullptr;
+    if (Status s = upload(c, d_ub1, ub1); !s) return s;
+    if (Status s = upload(c, d_ub2, ub2); !s) return s;
+    if (Status s = upload(c, d_lo, lo2); !s) return s;
+    if (Status s = upload(c, d_hi, hi2); !s) return s;
+    if (Status s = upload(c, d_w2, wait2); !s) return s;
+    if (Status s = upload(c, d_pf, pf); !s) return s;
+    if (Status s = dalloc(c, d_sync, (int64_t)nblk + 1); !s) return s;
+    r.nblk = nblk; r.cap = (int32_t)cap; r.maxu1 = maxu1; r.maxu2 = maxu2; r.maxnx = (int32_t)maxnx; r.smem = smem;
+    r.ub1 = d_ub1; r.ub2 = d_ub2; r.lo2 = d_lo; r.hi2 = d_hi; r.wait2 = d_w2; r.sync = d_sync; r.pf = d_pf;
+    // co-residency of one block per SM (cooperative launch)
+    A.rs = r;
+    const void* fn = rs_kernel_fn(A);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kRsThreads, smem);
+    cudaGetLastError();
+    A.rs.on = per_sm >= 1 ? 1 : 0;
+    if (getenv("PCG_VERBOSE"))
+        fprintf(stderr, "libpcg: resident strips %s: %d blocks x %d threads, buffer %lld doubles, smem %zu B, units/block <= %d / %d\n",
+                A.rs.on ? "on" : "off (occupancy)", nblk, kRsThreads, (long long)cap, smem, maxu1, maxu2);
+    return Status::ok();
+}
+
 Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_ctx* c) {
     if (Status s = build_plan(co, g, o, c->plan); !s) return s;
     Plan& P = c->plan;
@@ -583,6 +789,8 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     CU(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
     CU(cudaEventCreate(&c->ev0));
     CU(cudaEventCreate(&c->ev1));
+    CU(cudaEventCreate(&c->ev_l0));
+    CU(cudaEventCreate(&c->ev_l1));
     const int64_t nel = P.elements();
     KArgs& A = c->A;
     if (Status s = upload(c, c->cE, P.cE); !s) return s;
@@ -883,6 +1091,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     }
     else { c->bytes_k[1] = 40.0 * No; c->bytes_k[2] = 0.0; }
     CU(cudaGetLastError());
+    if (Status s = setup_rs(c); !s) return s;
     if (Status s = ensure_hist(c, 1023); !s) return s;
     CU(cudaStreamSynchronize(c->st));
     // release the bulky host copies
@@ -971,6 +1180,8 @@ void pcg_free(pcg_ctx* c) {
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->ev_l0) cudaEventDestroy(c->ev_l0);
+    if (c->ev_l1) cudaEventDestroy(c->ev_l1);
     if (c->st) cudaStreamDestroy(c->st);
     cudaGetLastError();
     delete c;
@@ -1141,6 +1352,18 @@ pcg_status pcg_layout(const pcg_ctx* c, int32_t* pitch, int32_t* block, int32_t*
 }
 
 int64_t pcg_device_bytes(const pcg_ctx* c) { return c ? c->dev_bytes : 0; }
+
+// diagnostic (not in libpcg.h): per-block pass durations of a -DRS_TIMELINE build, [nblk][12] ns
+int pcg_rs_timeline(const pcg_ctx* c, unsigned long long* out) {
+    return c ? rs_timeline(out, c->A.rs.nblk) : 0;
+}
+
+pcg_status pcg_loop_time(const pcg_ctx* c, double* ms, int32_t* iterations) {
+    if (!c || !ms) { set_thread_error("pcg_loop_time: NULL argument"); return PCG_ERR_ARG; }
+    *ms = (double)c->loop_ms;
+    if (iterations) *iterations = c->loop_iters;
+    return PCG_OK;
+}
 
 pcg_status pcg_kernel_times(pcg_ctx* c, int32_t n_iter, double* ms_out, double* bytes_out) {
     if (!c || n_iter < 1 || !ms_out) { set_thread_error("pcg_kernel_times: bad argument"); return PCG_ERR_ARG; }
