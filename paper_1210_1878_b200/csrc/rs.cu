@@ -52,9 +52,9 @@ constexpr int kRsWarps = kRsThreads / 32;
 #define RS_DEF_NB 8
 #define RS_DEF_NB2 4
 #else
-#define RS_DEF_VU 4
+#define RS_DEF_VU 8
 #define RS_DEF_K1C 4
-#define RS_DEF_ZC 4
+#define RS_DEF_ZC 2
 #define RS_DEF_NB 24
 #define RS_DEF_NB2 12
 #endif
@@ -207,7 +207,7 @@ __device__ __forceinline__ void rs_partials(int32_t ua, int32_t nu, const int32_
 }
 
 #ifndef RS_OVF
-#define RS_OVF 8                     // overflow entries per round (the next round's loads in flight)
+#define RS_OVF 8                     // overflow entries per round (two rounds in flight)
 #endif
 // One Z / Z^T row: the 4 preloaded ELL slots (z, cw: int16 offsets from the element's own array
 // index a; zero / own index on land lanes), then the row's entries in the SELL-32 overflow of its
@@ -227,30 +227,41 @@ __device__ __forceinline__ double rs_row(const double (&z)[kEll], uint2 cw, int6
     const int lane = threadIdx.x & 31;
     const double* vp = ov + o0 + lane;
     const int32_t* cp = oc + o0 + lane;
-    double zn[RS_OVF];
-    int32_t cn[RS_OVF];
+    // two rounds of RS_OVF entries in flight: round A is consumed while round B's loads are out,
+    // then A is refilled two rounds ahead (entries past L re-read the last entry, never used)
+    double za[RS_OVF], zb[RS_OVF];
+    int32_t ca[RS_OVF], cb[RS_OVF];
 #pragma unroll
     for (int u = 0; u < RS_OVF; ++u) {
-        const int m = min(u, L - 1) << 5;
-        zn[u] = __ldg(vp + m);
-        cn[u] = __ldg(cp + m);
+        const int m = min(u, L - 1) << 5, n = min(RS_OVF + u, L - 1) << 5;
+        za[u] = __ldg(vp + m);
+        ca[u] = __ldg(cp + m);
+        zb[u] = __ldg(vp + n);
+        cb[u] = __ldg(cp + n);
     }
-    for (int m0 = 0; m0 < L; m0 += RS_OVF) {
-        double zz[RS_OVF];
-        int32_t c[RS_OVF];
+    for (int m0 = 0; m0 < L; m0 += 2 * RS_OVF) {
 #pragma unroll
-        for (int u = 0; u < RS_OVF; ++u) { zz[u] = zn[u]; c[u] = cn[u]; }
-        if (m0 + RS_OVF < L) {
+        for (int u = 0; u < RS_OVF; ++u)
+            if (m0 + u < L) acc = __fma_rn(za[u], xb[ca[u]], acc);
+        if (m0 + 2 * RS_OVF < L) {
 #pragma unroll
             for (int u = 0; u < RS_OVF; ++u) {
-                const int m = min(m0 + RS_OVF + u, L - 1) << 5;
-                zn[u] = __ldg(vp + m);
-                cn[u] = __ldg(cp + m);
+                const int m = min(m0 + 2 * RS_OVF + u, L - 1) << 5;
+                za[u] = __ldg(vp + m);
+                ca[u] = __ldg(cp + m);
             }
         }
 #pragma unroll
         for (int u = 0; u < RS_OVF; ++u)
-            if (m0 + u < L) acc = __fma_rn(zz[u], xb[c[u]], acc);
+            if (m0 + RS_OVF + u < L) acc = __fma_rn(zb[u], xb[cb[u]], acc);
+        if (m0 + 3 * RS_OVF < L) {
+#pragma unroll
+            for (int u = 0; u < RS_OVF; ++u) {
+                const int m = min(m0 + 3 * RS_OVF + u, L - 1) << 5;
+                zb[u] = __ldg(vp + m);
+                cb[u] = __ldg(cp + m);
+            }
+        }
     }
     return acc;
 }
@@ -291,15 +302,13 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
     int32_t* uc1 = reinterpret_cast<int32_t*>(cm + maxnx);
     int32_t* uc2 = uc1 + maxu1 + 1;
     uint16_t* cc = reinterpret_cast<uint16_t*>(uc2 + maxu2 + 1);
-    // per-chunk tables over every element any pass of this block touches, [xlo, xhi): the ocean
-    // bit mask (cm; 0 outside the owned rows) and the grid column of the chunk's first element
-    // (cc), so the passes need no integer division
-    int32_t xlo = INT32_MAX, xhi = 0;
-    if (e1 > e0) { xlo = e0 - P; xhi = e1 + P; }
-    if (f1 > f0) { xlo = min(xlo, lo2); xhi = max(xhi, hi2); }
-    if (xhi <= xlo) xlo = xhi = 0;
-    for (int q = tid; q < (xhi - xlo) >> 5; q += kRsThreads) {
-        const int32_t e = xlo + 32 * q - (int32_t)A.hoff;
+    // per-chunk tables of the elements each phase touches -- K1: [e0 - P, e1 + P), K2/K3: [lo2,
+    // hi2) -- the ocean bit mask (cm; 0 outside the owned rows) and the grid column of the chunk's
+    // first element (cc), so the passes need no integer division
+    const int32_t nx1 = e1 > e0 ? (e1 - e0 + 2 * P) >> 5 : 0;
+    const int32_t nx2 = f1 > f0 ? (hi2 - lo2) >> 5 : 0;
+    for (int q = tid; q < nx1 + nx2; q += kRsThreads) {
+        const int32_t e = (q < nx1 ? e0 - P + 32 * q : lo2 + 32 * (q - nx1)) - (int32_t)A.hoff;
         uint32_t m = 0u;
         int32_t i = 0;
         if (e >= 0 && e < A.nloc * P) {
@@ -332,7 +341,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
             double* __restrict__ dnew = A.d[par ^ 1];
             const int32_t D0 = e0 - P;
             const int nD = (e1 - e0 + 2 * P) >> 5, own0 = P >> 5, own1 = own0 + ((e1 - e0) >> 5);
-            const int cmD = (D0 - xlo) >> 5;
+            const int cmD = 0;
             // 1a: d over [D0, D0 + 32 nD) -> buf (land chunks: 0, no loads); own chunks: d -> global,
             // x += alpha_prev d_old
             for (int c0 = warp; c0 < nD; c0 += RS_VU * NW) {
@@ -364,7 +373,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
             // 1b: q = A d on own ocean points, (d, q) warp sums; RS_K1C chunks per
             // warp with all their loads issued before any computes
             const double* bd = buf - D0;
-            const int nch = (e1 - e0) >> 5, cm1 = (e0 - xlo) >> 5;
+            const int nch = (e1 - e0) >> 5, cm1 = P >> 5;
             for (int c0 = warp; c0 < nch; c0 += RS_K1C * NW) {
                 double cEp[RS_K1C], cNr[RS_K1C], cNs[RS_K1C], cEw[RS_K1C], sg[RS_K1C];
                 uint32_t m[RS_K1C];
@@ -430,7 +439,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
             const double* __restrict__ ro = A.r[par];
             double* __restrict__ rn = A.r[par ^ 1];
             const int nch = (f1 - f0) >> 5;
-            const int cmF = (f0 - xlo) >> 5;
+            const int cmF = nx1 + ((f0 - lo2) >> 5);
             if (PC == 0) {
                 if (tid == 0 && nch > 0) {                      // this block's overflow rows -> L2
                     const int64_t* pf = A.rs.pf + 4 * (int64_t)b;
@@ -444,7 +453,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                     }
                 }
                 // 2A: r_new over [lo2, f1) -> buf; own chunks: r_new -> global, (r, r) warp sums
-                const int nR = (f1 - lo2) >> 5, own0 = (f0 - lo2) >> 5, cmR = (lo2 - xlo) >> 5;
+                const int nR = (f1 - lo2) >> 5, own0 = (f0 - lo2) >> 5, cmR = nx1;
                 for (int c0 = warp; c0 < nR; c0 += RS_VU * NW) {
                     double qv[RS_VU], rv[RS_VU];
                     uint32_t m[RS_VU];

@@ -624,66 +624,106 @@ Status setup_rs(pcg_ctx* c) {
     const int nblk = sms;
     const int W = kBlock / 32;
     auto Lof = [](const Ell& E, int64_t sl) { return (E.ovf.off[(size_t)sl + 1] - E.ovf.off[(size_t)sl]) >> 5; };
-    // Cost model per unit, in units of one ocean chunk's passes: a chunk with ocean points costs 1
-    // per phase (its streams), an all-land chunk 0.3 (the mask test and loop overhead); K2/K3 add
-    // 0.15 per overflow entry per lane (Z^T and Z: 12 bytes each against ~80 bytes of an ELL
-    // element's streams -- the pole rows' long tails).
-    std::vector<double> c1((size_t)U), c2((size_t)U);
+    auto a0 = [&](int64_t m) { return (m / A.nbx + P.halo) * (int64_t)P.pitch + (m % A.nbx) * kBlock; };
+    const size_t limit = (size_t)optin - 2048;
+    // Partition by a time model, not a byte count: the chunks of a block go round-robin to its
+    // warps and a warp processes its chunks one after another, so a block's time is its slowest
+    // warp's sum of chunk times (plus the vector copies every warp shares).  In the K2/K3 phase a
+    // chunk's overflow rows are a chain of dependent rounds (8 entries per round) -- at the pole
+    // (L up to 80 per slice) the longest warp chain, not the block's bytes, sets its time, so those
+    // blocks get few chunks.  Model (us per warp-chunk, measured at cfg4): K1 phase -- ocean chunk
+    // 0.45, land 0.05, plus 0.25 per chunk of the d copy (own + one halo row each way) over the
+    // warps; K2/K3 phase -- ocean chunk 0.85 + 0.65 per overflow round of 8 entries of Z^T and of
+    // Z (two rounds in flight), land 0.05, plus 0.43 per chunk of the r_new / t copies (own + halo).  Greedy contiguous blocks under a
+    // target time, bisection on the target for nblk blocks, at most maxch chunks per block (the
+    // shared-memory buffer).
+    const int NW = kRsThreads / 32;
+    // model constants (us): K1 ocean chunk, K1 shared per chunk, K2/K3 ocean chunk, per overflow
+    // round, K2/K3 shared per chunk; PCG_RS_MODEL="a,b,c,d,e" overrides (tuning)
+    double mk[5] = {0.45, 0.25, 0.85, 0.65, 0.43};
+    if (const char* e = getenv("PCG_RS_MODEL"))
+        sscanf(e, "%lf,%lf,%lf,%lf,%lf", &mk[0], &mk[1], &mk[2], &mk[3], &mk[4]);
+    const int64_t lim_dbl = (int64_t)((limit > 24576 ? limit - 24576 : 0) / 8);
+    auto chunk_is_ocean = [&](int64_t j, int64_t i0) {
+        for (int l = 0; l < 32; ++l) {
+            const int64_t i = i0 + l;
+            if (i < P.ni && !std::signbit(P.cN[(size_t)(j + P.halo) * P.pitch + i])) return true;
+        }
+        return false;
+    };
+    std::vector<std::vector<double>> wc1((size_t)U), wc2((size_t)U);
     for (int64_t m = 0; m < U; ++m) {
         const int64_t j = m / A.nbx, bx = m % A.nbx;
-        double k1 = 0.0, k2 = 0.0;
         for (int w = 0; w < W; ++w) {
             const int64_t i0 = bx * kBlock + 32 * w;
             if (i0 >= P.pitch) break;
-            bool ocean = false;
-            for (int l = 0; l < 32 && !ocean; ++l) {
-                const int64_t i = i0 + l;
-                ocean = i < P.ni && !std::signbit(P.cN[(size_t)(j + P.halo) * P.pitch + i]);
-            }
-            k1 += ocean ? 1.0 : 0.3;
-            k2 += ocean ? (fac ? 2.0 : 1.0) : 0.3;
-            if (fac && ocean) {
-                const int64_t sl = (j * P.pitch + i0) >> 5;
-                k2 += 0.15 * (double)(Lof(P.ZT, sl) + Lof(P.Z, sl));
-            }
+            const bool ocean = chunk_is_ocean(j, i0);
+            const int64_t sl = (j * P.pitch + i0) >> 5;
+            wc1[(size_t)m].push_back(ocean ? mk[0] : 0.05);
+            wc2[(size_t)m].push_back(!ocean ? 0.05 : fac ? mk[2] + mk[3] * (double)(((Lof(P.ZT, sl) + 7) / 8) + ((Lof(P.Z, sl) + 7) / 8)) : 0.6);
         }
-        c1[(size_t)m] = k1;
-        c2[(size_t)m] = k2;
     }
-    auto len = [&](int64_t m) { const int64_t bx = m % A.nbx; return (int64_t)std::min<int64_t>(kBlock, P.pitch - bx * kBlock); };
-    auto split = [&](const std::vector<double>& cost, double wlen, std::vector<int32_t>& ub) {
-        std::vector<double> pre((size_t)U + 1, 0.0);
-        for (int64_t m = 0; m < U; ++m) pre[(size_t)m + 1] = pre[(size_t)m] + cost[(size_t)m] + wlen * (double)len(m) / 32.0;
-        ub.assign((size_t)nblk + 1, 0);
-        for (int b = 1; b < nblk; ++b) {
-            const double tgt = pre[(size_t)U] * (double)b / (double)nblk;
-            int64_t m = std::lower_bound(pre.begin(), pre.end(), tgt) - pre.begin();
-            ub[(size_t)b] = (int32_t)std::max<int64_t>(ub[(size_t)b - 1], std::min<int64_t>(m, U));
+    auto greedy = [&](const std::vector<std::vector<double>>& wc, double shared, int64_t halo_ch, int64_t maxch, double T,
+                      std::vector<int32_t>* ub) -> int {
+        int nb = 0;
+        int64_t m = 0;
+        if (ub) ub->assign(1, 0);
+        std::vector<double> wt((size_t)NW), wt2((size_t)NW);
+        while (m < U) {
+            std::fill(wt.begin(), wt.end(), 0.0);
+            int64_t nch = 0;
+            double wmax = 0.0;
+            const int64_t m0 = m;
+            while (m < U) {
+                wt2 = wt;
+                double wm = wmax;
+                for (size_t q = 0; q < wc[(size_t)m].size(); ++q) {
+                    double& x = wt2[(size_t)((nch + (int64_t)q) % NW)];
+                    x += wc[(size_t)m][q];
+                    wm = std::max(wm, x);
+                }
+                const int64_t nch2 = nch + (int64_t)wc[(size_t)m].size();
+                const double t = wm + shared * (double)(nch2 + halo_ch) / NW;
+                if (m > m0 && (t > T || nch2 > maxch)) break;
+                wt.swap(wt2);
+                wmax = wm;
+                nch = nch2;
+                ++m;
+            }
+            ++nb;
+            if (ub) ub->push_back((int32_t)m);
         }
-        ub[(size_t)nblk] = (int32_t)U;
+        return nb;
     };
-    auto a0 = [&](int64_t m) { return (m / A.nbx + P.halo) * (int64_t)P.pitch + (m % A.nbx) * kBlock; };
-    const size_t limit = (size_t)optin - 2048;
-    // phase 1: the stencil reaches one grid row each way
+    auto model_split = [&](const std::vector<std::vector<double>>& wc, double shared, int64_t halo_ch, int64_t maxch,
+                           std::vector<int32_t>& ub) -> double {
+        double lo = 0.0, hi = 1e9;
+        for (int it = 0; it < 60; ++it) {
+            const double mid = 0.5 * (lo + hi);
+            if (greedy(wc, shared, halo_ch, maxch, mid, nullptr) <= nblk) hi = mid; else lo = mid;
+        }
+        greedy(wc, shared, halo_ch, maxch, hi, &ub);
+        while ((int)ub.size() < nblk + 1) ub.push_back((int32_t)U);        // idle blocks at the end
+        return hi;
+    };
     std::vector<int32_t> ub1, ub2;
+    const int64_t h1 = (2 * (int64_t)P.pitch) / 32, h2 = (4 * (int64_t)P.pitch) / 32;
+    const double t1 = model_split(wc1, mk[1], h1, std::max<int64_t>(8, lim_dbl / 32 - h1), ub1);
+    const double t2 = model_split(wc2, fac ? mk[4] : 0.2, fac ? h2 : 0, std::max<int64_t>(8, lim_dbl / 32 - 2 * h2), ub2);
+    if ((int)ub1.size() != nblk + 1 || (int)ub2.size() != nblk + 1) return Status::ok();
+    if (getenv("PCG_VERBOSE")) fprintf(stderr, "libpcg: resident strips model time K1 %.1f + K2/K3 %.1f us per iteration\n", t1, t2);
     int32_t maxu1 = 1, maxu2 = 1;
     int64_t cap1 = 0;
-    for (double wl = 0.0;; wl = wl == 0.0 ? 0.25 : 2.0 * wl) {
-        split(c1, wl, ub1);
-        cap1 = 0; maxu1 = 1;
-        for (int b = 0; b < nblk; ++b) {
-            const int64_t e0 = a0(ub1[(size_t)b]), e1 = a0(ub1[(size_t)b + 1]);
-            maxu1 = std::max<int32_t>(maxu1, ub1[(size_t)b + 1] - ub1[(size_t)b]);
-            if (e1 > e0) cap1 = std::max<int64_t>(cap1, e1 - e0 + 2 * (int64_t)P.pitch);
-        }
-        if (rs_smem_bytes((int32_t)cap1, maxu1, maxu1, (int32_t)(cap1 / 32 + 2)) <= limit || wl > 1e6) break;
+    for (int b = 0; b < nblk; ++b) {
+        const int64_t e0 = a0(ub1[(size_t)b]), e1 = a0(ub1[(size_t)b + 1]);
+        maxu1 = std::max<int32_t>(maxu1, ub1[(size_t)b + 1] - ub1[(size_t)b]);
+        if (e1 > e0) cap1 = std::max<int64_t>(cap1, e1 - e0 + 2 * (int64_t)P.pitch);
     }
     // phase 2: r_new from the lowest Z^T column of the range, t up to the highest Z column
     std::vector<int64_t> lo2((size_t)nblk), hi2((size_t)nblk);
     std::vector<int32_t> wait2((size_t)nblk);
     int64_t cap = cap1, maxnx = 1;
-    for (double wl = 0.0;; wl = wl == 0.0 ? 0.25 : 2.0 * wl) {
-        split(c2, wl, ub2);
+    {
         cap = cap1; maxu2 = 1;
         for (int b = 0; b < nblk; ++b) {
             const int64_t f0 = a0(ub2[(size_t)b]), f1 = a0(ub2[(size_t)b + 1]);
@@ -709,17 +749,15 @@ Status setup_rs(pcg_ctx* c) {
             hi2[(size_t)b] = hi;
         }
         // chunks (32 elements) whose mask and column a block keeps in shared memory (same rule as
-        // rs_loop_kernel): [K1 range - one row, K1 range + one row) u [lo2, hi2 rounded up)
+        // rs_loop_kernel): [K1 range - one row, K1 range + one row) and [lo2, hi2 rounded up)
         maxnx = 1;
         for (int b = 0; b < nblk; ++b) {
             const int64_t e0 = a0(ub1[(size_t)b]), e1 = a0(ub1[(size_t)b + 1]);
             const int64_t f0 = a0(ub2[(size_t)b]), f1 = a0(ub2[(size_t)b + 1]);
-            int64_t xlo = INT64_MAX, xhi = 0;
-            if (e1 > e0) { xlo = e0 - P.pitch; xhi = e1 + P.pitch; }
-            if (f1 > f0) { xlo = std::min(xlo, lo2[(size_t)b]); xhi = std::max(xhi, (hi2[(size_t)b] + 31) & ~(int64_t)31); }
-            if (xhi > xlo) maxnx = std::max<int64_t>(maxnx, (xhi - xlo) >> 5);
+            const int64_t nx1 = e1 > e0 ? (e1 - e0 + 2 * (int64_t)P.pitch) >> 5 : 0;
+            const int64_t nx2 = f1 > f0 ? (((hi2[(size_t)b] + 31) & ~(int64_t)31) - lo2[(size_t)b]) >> 5 : 0;
+            maxnx = std::max<int64_t>(maxnx, nx1 + nx2);
         }
-        if (rs_smem_bytes((int32_t)cap, maxu1, maxu2, (int32_t)maxnx) <= limit || wl > 1e6) break;
     }
     for (int b = 0; b < nblk; ++b) {
         int32_t w2 = b;
