@@ -246,10 +246,15 @@ def main():
         barrier()
         w0 = time.perf_counter()
         e0.record(stream)
+        loop_ms, loop_it = [], 0
         for _ in range(args.steps):
             x, k, hist, rep = S.solve(b, tol=args.tol, maxit=maxit)
             iters.append(k)
             lib_s += rep["solve_s"]
+            lm, li = S.loop_time()                       # resident-strip loop kernel (-1: other driver)
+            if lm > 0:
+                loop_ms.append(lm)
+                loop_it += li
         e1.record(stream)
         barrier()
         clk.window = (w0, time.perf_counter())
@@ -283,14 +288,35 @@ def main():
     # roofline of the dominant kernel (single rank: per-kernel CUDA events on the launch stream)
     roof = None
     ktimes = None
-    if world == 1 and args.method == "pcg":
+    rs_used = world == 1 and len(loop_ms) == args.steps
+    peak, peak_src = fallback_peak()
+    if rs_used:
+        # the resident-strip driver: one persistent kernel runs every iteration of a solve; its
+        # CUDA-event time (library events on the launch stream around the launch) per iteration
+        # against the algorithmic bytes of one iteration ((144 + 24 z) N_o)
+        it_ms = sum(loop_ms) / max(1, loop_it)
+        by_it = float(rep["bytes_per_iter"])
+        ach = by_it / (it_ms * 1e-3) / 1e9
+        traffic, traffic_src = None, None
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            tj = json.load(open(tp))
+            traffic = tj.get(args.config, {}).get("rs_loop_kernel_" + args.precond)
+            if traffic is not None:
+                traffic_src = ("profiles/ncu_traffic.json: dram__bytes_read+write of one rs_loop_kernel launch (ncu "
+                               "--set full, no L2 window under ncu) / its iterations")
+        roof = {"bound": "hbm", "kernel": "rs_loop_kernel (whole PCG iteration, resident strips)", "achieved": ach,
+                "peak": peak, "unit": "GB/s", "frac": ach / peak, "traffic": traffic, "traffic_source": traffic_src,
+                "peak_source": peak_src, "unit_of_work": "one PCG iteration of the persistent loop kernel",
+                "algorithmic_bytes_per_launch": by_it, "ms_per_launch": it_ms,
+                "launches_timed": loop_it, "loop_ms_per_solve": sum(loop_ms) / len(loop_ms)}
+    if world == 1 and args.method == "pcg" and not rs_used:
         S.solve(b, tol=args.tol, maxit=maxit)
         ms, by = S.kernel_times(args.profile_iters)
         names = ["K1_stencil", "K2_ZTr", "K3_Zt"]
         if by[2] == 0 and args.precond in ("ainv", "fsai"):
             names[1] = "K23_ZTr_Zt"                              # K2 and K3 fused into one kernel
         kk = int(np.argmax(ms[:3]))
-        peak, peak_src = fallback_peak()
         ach = by[kk] / (ms[kk] * 1e-3) / 1e9
         traffic = None
         traffic_src = None
@@ -332,7 +358,9 @@ def main():
     pro = 4 if args.precond in ("ainv", "fsai") and not fused else 3
     if args.method == "cg1":
         pro = 5                                                  # + KC's w0 = A u0 (alpha0)
-    if world == 1:
+    if rs_used:
+        launches = len(iters) * (pro + 1 + 2)                    # prologue, the loop kernel, epilogue
+    elif world == 1:
         body = max(2, int(os.environ.get("PCG_BODY_ITERS", "8")) & ~1)
         launches = sum(pro + per_iter * body * math.ceil(k / body) + 2 for k in iters)
     else:
@@ -354,6 +382,8 @@ def main():
                                   "of vectors) exceeds the 126 MB L2; by design 7 of the 8 per-iteration vectors "
                                   "stay in a persisting L2 window within a solve (DESIGN.md §4)"),
                            "parallelism": f"row blocks x{world}" if world > 1 else "1 GPU",
+                           "driver": "resident strips (one persistent cooperative kernel per solve)" if rs_used
+                                     else "WHILE-node graph of K1/K2/K3 launches" if world == 1 else "NCCL row blocks",
                            "kernels": ktimes},
                 "roofline": roof, "cpu_baseline": cpu,
                 "e2e": {"value": e_iters / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nbytes,
