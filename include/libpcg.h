@@ -138,7 +138,17 @@ typedef struct {
     int64_t n_ocean;           /* ocean unknowns owned by this rank */
     int64_t nnz_z;             /* off-diagonal nonzeros of this rank's Z columns */
     int64_t failed_index;      /* global unknown index for NOT_SPD, else -1 */
+    int32_t driver;            /* how the iterations ran (PCG_DRIVER_*): one rank -- the resident-strip
+                                  loop kernel, the WHILE-node graph, the cooperative loop kernel or the
+                                  host loop; several ranks -- the NCCL graph, or the NCCL host loop
+                                  when the graph could not be captured (PCG_DRIVER_NCCL_FALLBACK: the
+                                  capture failure is reported here, not hidden) */
+    int32_t reserved;
 } pcg_report;
+
+enum { PCG_DRIVER_GRAPH = 0, PCG_DRIVER_LOOP = 1, PCG_DRIVER_RESIDENT = 2, PCG_DRIVER_HOST_LOOP = 3,
+       PCG_DRIVER_NCCL_GRAPH = 4, PCG_DRIVER_NCCL_FALLBACK = 5, PCG_DRIVER_NCCL_HOST_LOOP = 6,
+       PCG_DRIVER_LOCAL_RANKS = 7 };
 
 /* ---------------------------------------------------------------- the three calls */
 

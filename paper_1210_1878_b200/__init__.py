@@ -58,10 +58,16 @@ class Report(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("rel_residual", C.c_double),
                 ("true_rel_residual", C.c_double), ("setup_s", C.c_double), ("solve_s", C.c_double),
                 ("bytes_per_iter", C.c_double), ("n_ocean", C.c_int64), ("nnz_z", C.c_int64),
-                ("failed_index", C.c_int64)]
+                ("failed_index", C.c_int64), ("driver", C.c_int32), ("reserved", C.c_int32)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        d["driver_name"] = DRIVERS.get(d["driver"], str(d["driver"]))
+        return d
+
+
+DRIVERS = {0: "graph", 1: "loop", 2: "resident", 3: "host_loop", 4: "nccl_graph", 5: "nccl_fallback_host_loop",
+           6: "nccl_host_loop", 7: "local_ranks"}
 
 
 EXPORTS = ["pcg_setup", "pcg_solve", "pcg_solve_host", "pcg_solve_local_ranks", "pcg_free", "pcg_last_error", "pcg_apply_operator",
@@ -200,6 +206,7 @@ class Solver:
         cE, cN, mask, sigma = _host_inputs(cE, cN, mask, sigma)
         nj, ni = mask.shape
         self.ni, self.nj = ni, nj
+        self.n_ocean = int(np.count_nonzero(mask))     # N_o: the default maxit (Alg. 1's k <= n)
         self.device = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
         torch.cuda.set_device(self.device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
@@ -243,10 +250,11 @@ class Solver:
         (x, iterations, hist (numpy), report dict)."""
         import torch
         if maxit is None:
-            maxit = 10 * self.ni * self.nj
+            maxit = self.n_ocean
         assert b.is_cuda and b.dtype == torch.float64 and b.is_contiguous() and tuple(b.shape) == (self.rows, self.ni)
         if x is None:
             x = torch.empty_like(b)
+        assert x.is_cuda and x.dtype == torch.float64 and x.is_contiguous() and x.shape == b.shape
         if x0 is not None:
             assert x0.is_cuda and x0.dtype == torch.float64 and x0.is_contiguous() and x0.shape == b.shape
         cap = int(hist_cap if hist_cap is not None else min(maxit + 1, 1 << 22))
@@ -263,9 +271,17 @@ class Solver:
         """Same with host numpy (or pinned torch CPU) buffers; the H2D/D2H copies happen inside
         pcg_solve_host."""
         if maxit is None:
-            maxit = 10 * self.ni * self.nj
+            maxit = self.n_ocean
+        shape = (self.rows, self.ni)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        assert b.shape == shape, f"b must be {shape}"
+        if x0 is not None:
+            x0 = np.ascontiguousarray(x0, dtype=np.float64)
+            assert x0.shape == shape, f"x0 must be {shape}"
         if out is None:
-            out = np.empty((self.rows, self.ni))
+            out = np.empty(shape)
+        assert isinstance(out, np.ndarray) and out.dtype == np.float64 and out.shape == shape and out.flags.c_contiguous, \
+            f"out must be a C-contiguous float64 {shape} array"
         cap = int(hist_cap if hist_cap is not None else min(maxit + 1, 1 << 22))
         hist = np.empty(max(cap, 1))
         it = C.c_int32()
@@ -339,6 +355,7 @@ class LocalRanks:
         cE, cN, mask, sigma = _host_inputs(cE, cN, mask, sigma)
         nj, ni = mask.shape
         self.ni, self.nj, self.n = ni, nj, int(nranks)
+        self.n_ocean = int(np.count_nonzero(mask))
         dev = torch.cuda.current_device() if device is None else int(device)
         stream = torch.cuda.current_stream(dev)
         self.rb = partition(ni, nj, mask, self.n)
@@ -361,7 +378,7 @@ class LocalRanks:
     def solve(self, b, x0=None, tol=1e-10, maxit=None, x=None, hist_cap=None):
         import torch
         if maxit is None:
-            maxit = 10 * self.ni * self.nj
+            maxit = self.n_ocean
         assert b.is_cuda and b.dtype == torch.float64 and b.is_contiguous() and tuple(b.shape) == (self.nj, self.ni)
         x = torch.empty_like(b) if x is None else x
         cap = int(hist_cap if hist_cap is not None else min(maxit + 1, 1 << 22))

@@ -140,7 +140,7 @@ __device__ void fin_bb(const KArgs& A, double bb) {
 __device__ void fin_init(const KArgs& A, double rho0, double rr0) {
     DevScalars* sc = A.sc;
     if (sc->bzero) {
-        A.hist[0] = 0.0;
+        put_hist(A, 0, 0.0);
         sc->active = 0;
         set_cond(A, 0);
         return;
@@ -149,7 +149,7 @@ __device__ void fin_init(const KArgs& A, double rho0, double rr0) {
     sc->beta = 0.0;
     sc->rho_prev = INFINITY;                 // beta of the first iteration = rho / inf = +0 (d_old = 0)
     const double h = __ddiv_rn(__dsqrt_rn(rr0), sc->nb);
-    A.hist[0] = h;
+    put_hist(A, 0, h);
     if (!isfinite(h)) {                      // NaN / Inf in b or x0: breakdown before the first iteration
         stop(A, kStBreakdown);
         return;
@@ -184,14 +184,14 @@ __device__ void fin_iter(const KArgs& A, double rho_new, const FinPre& f) {
     const int k = f.k + 1;
     sc->k = k;
     if (!isfinite(rho_new) || !isfinite(f.rr)) {
-        if (k < A.hist_cap) A.hist[k] = NAN;
+        put_hist(A, k, NAN);
         stop(A, kStBreakdown);
         return;
     }
     sc->rho_prev = f.rho;                    // beta = rho_new / rho is formed by K1 (same IEEE division)
     sc->rho = rho_new;
     const double h = f.h;
-    if (k < A.hist_cap) A.hist[k] = h;
+    put_hist(A, k, h);
     const int act = (h > f.tol) && (k < f.maxit);
     sc->active = act;
     TT(2, 2);
@@ -451,7 +451,7 @@ __device__ __forceinline__ bool k1_beta(const KArgs& A, int par, double& beta) {
     if (!isfinite(rho)) {                                // fin_iter's breakdown on (s, r)
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             const int k = A.sc->k;
-            if (k < A.hist_cap) A.hist[k] = NAN;
+            put_hist(A, k, NAN);
             stop(A, kStBreakdown);
         }
         return false;
@@ -1066,14 +1066,14 @@ __device__ __forceinline__ void k3_sum_rr(const KArgs& A, int init) {
                 sc->rhop[1] = INFINITY;                  // beta of the first iteration = rho / inf = +0
                 sc->rho_prev = INFINITY;
                 if (sc->bzero) {
-                    A.hist[0] = 0.0;
+                    put_hist(A, 0, 0.0);
                     sc->active = 0;
                     set_cond(A, 0);
                 } else if (!isfinite(h)) {                 // NaN / Inf in b or x0
-                    A.hist[0] = h;
+                    put_hist(A, 0, h);
                     stop(A, kStBreakdown);
                 } else {
-                    A.hist[0] = h;
+                    put_hist(A, 0, h);
                     const int act = (h > sc->tol) && (sc->maxit > 0);
                     sc->active = act;
                     set_cond(A, act);
@@ -1082,10 +1082,10 @@ __device__ __forceinline__ void k3_sum_rr(const KArgs& A, int init) {
                 const int k = sc->k + 1;
                 sc->k = k;
                 if (!isfinite(rr)) {
-                    if (k < A.hist_cap) A.hist[k] = NAN;
+                    put_hist(A, k, NAN);
                     stop(A, kStBreakdown);
                 } else {
-                    if (k < A.hist_cap) A.hist[k] = h;
+                    put_hist(A, k, h);
                     const int act = (h > sc->tol) && (k < sc->maxit);
                     sc->active = act;
                     set_cond(A, act);
@@ -1895,14 +1895,14 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_LOOP) loop_kernel(const KArgs
         k += 1;
         xpend = 1;
         if (!isfinite(rho_new) || !isfinite(rr)) {
-            if (lead && k < A.hist_cap) A.hist[k] = NAN;
+            if (lead) put_hist(A, k, NAN);
             status = kStBreakdown;
             break;
         }
         beta = __ddiv_rn(rho_new, rho);
         rho = rho_new;
         const double h = __ddiv_rn(__dsqrt_rn(rr), nb);
-        if (lead && k < A.hist_cap) A.hist[k] = h;
+        if (lead) put_hist(A, k, h);
         active = (h > tol) && (k < maxit);
         par ^= 1;
     }
@@ -2064,14 +2064,14 @@ __global__ void __launch_bounds__(kTinyThreads, 1) tiny_kernel(const KArgs G) {
         k += 1;
         xpend = 1;
         if (!isfinite(rho_new) || !isfinite(rr)) {
-            if (lead && k < G.hist_cap) G.hist[k] = NAN;
+            if (lead) put_hist(G, k, NAN);
             status = kStBreakdown;
             break;
         }
         beta = __ddiv_rn(rho_new, rho);
         rho = rho_new;
         const double h = __ddiv_rn(__dsqrt_rn(rr), nb);
-        if (lead && k < G.hist_cap) G.hist[k] = h;
+        if (lead) put_hist(G, k, h);
         active = (h > tol) && (k < maxit);
         par ^= 1;
     }

@@ -14,6 +14,7 @@ constexpr int kMaxRowsK1 = 16;     // rows per K1 block (register march), <= kMa
 struct DevScalars {
     double alpha, beta, rho, nb, tol, true_rel;
     double hpre;          // sqrt((r,r)) / nb of the current iteration, formed early by K3's block 0
+    double hlast;         // the last history value written (report.rel_residual; the history buffer may be shorter)
     double rho_prev;      // rho of the previous iteration: K1 forms beta = rho / rho_prev itself
     double red[4];        // global reductions: [0] (d,q)  [1] (s,r)  [2] (r,r)  [3] (b,b) / true (r,r)
     double loc[4];        // this rank's block-tree sums (multi-rank path)
@@ -131,6 +132,14 @@ struct KArgs {
 };
 
 int64_t grid_blocks(const KArgs& A);
+
+#ifdef __CUDACC__
+// history entry k (kept only while k < hist_cap) and the last value (always)
+__device__ __forceinline__ void put_hist(const KArgs& A, int k, double h) {
+    if (k < A.hist_cap) A.hist[k] = h;
+    A.sc->hlast = h;
+}
+#endif
 
 // per-iteration kernels (par = iteration parity; init = the a3 pass with alpha = 0)
 void launch_k1(const KArgs& A, int par, cudaStream_t st);

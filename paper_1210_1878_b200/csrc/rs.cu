@@ -623,14 +623,14 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
         k += 1;
         xpend = 1;
         if (!isfinite(rho_new) || !isfinite(rr)) {
-            if (lead && k < A.hist_cap) A.hist[k] = NAN;
+            if (lead) put_hist(A, k, NAN);
             status = kStBreakdown;
             break;
         }
         beta = __ddiv_rn(rho_new, rho);
         rho = rho_new;
         const double h = __ddiv_rn(__dsqrt_rn(rr), nb);
-        if (lead && k < A.hist_cap) A.hist[k] = h;
+        if (lead) put_hist(A, k, h);
         active = (h > tol) && (k < maxit);
         par ^= 1;
     }

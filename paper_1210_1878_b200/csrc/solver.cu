@@ -118,6 +118,16 @@ int l2_users(int device, int delta) {
     std::lock_guard<std::mutex> lock(mu);
     return users[device] += delta;
 }
+// the device's persisting-L2 set-aside as it was before libpcg first raised it (restored when the
+// last window user of the device is freed; -1: not recorded yet)
+size_t& l2_limit_before(int device) {
+    static std::map<int, size_t> before;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = before.find(device);
+    if (it == before.end()) it = before.emplace(device, (size_t)-1).first;
+    return it->second;
+}
 
 // One rank: the resident-strip loop kernel (rs.cu) when setup found it eligible (its shared-
 // memory ranges fit); PCG_RS=0 disables it.
@@ -153,54 +163,66 @@ bool use_graph(const pcg_ctx* c) {
     return !(c->plan.flags & PCG_FLAG_HOST_LOOP) && !use_fused(c);
 }
 
-// ---------------------------------------------------------------- NCCL steps (multi path)
-Status allgather_loc(pcg_ctx* c) {
-    NC(ncclAllGather((const void*)c->sc->loc, (void*)c->gath, 4, ncclDouble, c->comm, c->st));
-    return Status::ok();
-}
+// ---------------------------------------------------------------- exchanges between ranks
+// Every exchange of the multi-rank path is one list of contiguous row ranges per direction,
+// built by exchange_list() from the plan alone.  Both backends walk the same list: the NCCL path
+// (several processes: ncclSend / ncclRecv to rank -+ 1) and the local-ranks path (one process,
+// the ranks' contexts on one GPU: a device copy from the sender's entry to the receiver's), so
+// the offsets and counts the GPU tests check through the local path are the NCCL path's.
+//   halo of x / s (/ t in pcg_apply_operator): first owned row -> rank-1's row H+nloc,
+//     last owned row -> rank+1's row H-1 (one row each way)
+//   QR (halo-AINV, after K1): rows [H+nloc-ws, H+nloc) of q and r[par] -> rank+1's rows [H-w, H)
+//   T  (halo-AINV, after K2): rows [H, H+halo_t_send) of t -> rank-1's rows [H+nloc, H+nloc+halo_t)
+enum class Ex { None, Allgather, HaloX, HaloSAllgather, AllgatherQR, QR, HaloT, HaloS };
+struct Xfer {
+    double* arr;                     // this context's array
+    int64_t off, n;                  // elements
+};
+struct XferList {
+    std::vector<Xfer> send_south, send_north, recv_south, recv_north;   // in matching order
+    bool allgather = false;
+};
 
-Status halo(pcg_ctx* c, double* arr, bool with_allgather) {
+XferList exchange_list(pcg_ctx* c, Ex ex, int par, double* halo_arr = nullptr) {
     const Plan& P = c->plan;
-    NC(ncclGroupStart());
-    if (with_allgather) NC(ncclAllGather((const void*)c->sc->loc, (void*)c->gath, 4, ncclDouble, c->comm, c->st));
-    if (P.nranks > 1) {
-        // one row each way: first owned row <-> southern halo row H-1 of rank-1, last owned row
-        // <-> northern halo row H+nloc of rank+1
-        const size_t n = (size_t)P.pitch, H = (size_t)P.halo;
+    const int64_t pt = P.pitch, H = P.halo, nl = P.nloc;
+    XferList L;
+    L.allgather = ex == Ex::Allgather || ex == Ex::HaloSAllgather || ex == Ex::AllgatherQR;
+    double* row1 = halo_arr ? halo_arr : ex == Ex::HaloX ? c->x : (ex == Ex::HaloS || ex == Ex::HaloSAllgather) ? c->s : nullptr;
+    if (row1) {
         if (P.rank > 0) {
-            NC(ncclSend(arr + H * P.pitch, n, ncclDouble, P.rank - 1, c->comm, c->st));
-            NC(ncclRecv(arr + (H - 1) * P.pitch, n, ncclDouble, P.rank - 1, c->comm, c->st));
+            L.send_south.push_back({row1, H * pt, pt});
+            L.recv_south.push_back({row1, (H - 1) * pt, pt});
         }
         if (P.rank < P.nranks - 1) {
-            NC(ncclSend(arr + (H + P.nloc - 1) * P.pitch, n, ncclDouble, P.rank + 1, c->comm, c->st));
-            NC(ncclRecv(arr + (H + P.nloc) * P.pitch, n, ncclDouble, P.rank + 1, c->comm, c->st));
+            L.send_north.push_back({row1, (H + nl - 1) * pt, pt});
+            L.recv_north.push_back({row1, (H + nl) * pt, pt});
         }
     }
-    NC(ncclGroupEnd());
-    return Status::ok();
+    if (ex == Ex::AllgatherQR || ex == Ex::QR) {
+        const int64_t w = P.halo_w, ws = P.halo_w_send;
+        for (double* arr : {c->q, c->r[par]}) {
+            if (P.rank < P.nranks - 1 && ws > 0) L.send_north.push_back({arr, (H + nl - ws) * pt, ws * pt});
+            if (P.rank > 0 && w > 0) L.recv_south.push_back({arr, (H - w) * pt, w * pt});
+        }
+    }
+    if (ex == Ex::HaloT) {
+        if (P.rank > 0 && P.halo_t_send > 0) L.send_south.push_back({c->t, H * pt, (int64_t)P.halo_t_send * pt});
+        if (P.rank < P.nranks - 1 && P.halo_t > 0) L.recv_north.push_back({c->t, (H + nl) * pt, (int64_t)P.halo_t * pt});
+    }
+    return L;
 }
 
-// Halo-AINV exchanges (contiguous row ranges, one message per array and direction).
-//   QR: rows [H+nloc-w, H+nloc) of q and r[par] -> rank+1's rows [H-w, H)
-//   T : rows [H, H+halo_t_send) of t -> rank-1's rows [H+nloc, H+nloc+halo_t)
-Status exch_halo_ainv(pcg_ctx* c, bool qr, bool t, bool with_allgather, int par) {
+// NCCL backend: one group per exchange (the allgather of the rank sums rides in the same group)
+Status nccl_exchange(pcg_ctx* c, Ex ex, int par, double* halo_arr = nullptr) {
     const Plan& P = c->plan;
-    const size_t pt = (size_t)P.pitch, H = (size_t)P.halo, w = (size_t)P.halo_w;
+    const XferList L = exchange_list(c, ex, par, halo_arr);
     NC(ncclGroupStart());
-    if (with_allgather) NC(ncclAllGather((const void*)c->sc->loc, (void*)c->gath, 4, ncclDouble, c->comm, c->st));
-    const size_t ws = (size_t)P.halo_w_send;
-    if (qr && (w > 0 || ws > 0))
-        for (double* arr : {c->q, c->r[par]}) {
-            if (P.rank < P.nranks - 1 && ws > 0)
-                NC(ncclSend(arr + (H + P.nloc - ws) * pt, ws * pt, ncclDouble, P.rank + 1, c->comm, c->st));
-            if (P.rank > 0) NC(ncclRecv(arr + (H - w) * pt, w * pt, ncclDouble, P.rank - 1, c->comm, c->st));
-        }
-    if (t) {
-        if (P.rank > 0 && P.halo_t_send > 0)
-            NC(ncclSend(c->t + H * pt, (size_t)P.halo_t_send * pt, ncclDouble, P.rank - 1, c->comm, c->st));
-        if (P.rank < P.nranks - 1 && P.halo_t > 0)
-            NC(ncclRecv(c->t + (H + P.nloc) * pt, (size_t)P.halo_t * pt, ncclDouble, P.rank + 1, c->comm, c->st));
-    }
+    if (L.allgather) NC(ncclAllGather((const void*)c->sc->loc, (void*)c->gath, 4, ncclDouble, c->comm, c->st));
+    for (const Xfer& x : L.send_south) NC(ncclSend(x.arr + x.off, (size_t)x.n, ncclDouble, P.rank - 1, c->comm, c->st));
+    for (const Xfer& x : L.recv_south) NC(ncclRecv(x.arr + x.off, (size_t)x.n, ncclDouble, P.rank - 1, c->comm, c->st));
+    for (const Xfer& x : L.send_north) NC(ncclSend(x.arr + x.off, (size_t)x.n, ncclDouble, P.rank + 1, c->comm, c->st));
+    for (const Xfer& x : L.recv_north) NC(ncclRecv(x.arr + x.off, (size_t)x.n, ncclDouble, P.rank + 1, c->comm, c->st));
     NC(ncclGroupEnd());
     return Status::ok();
 }
@@ -214,7 +236,6 @@ Status exch_halo_ainv(pcg_ctx* c, bool qr, bool t, bool with_allgather, int par)
 // Halo-AINV across ranks adds QR (w rows of q and r[par] from the southern neighbour, for K2's
 // gathers below the first owned row; fused with the allgather after K1) and T (the northern
 // neighbour's first rows of t, for K3's gathers above the last owned row).
-enum class Ex { None, Allgather, HaloX, HaloSAllgather, AllgatherQR, QR, HaloT, HaloS };
 struct Step {
     Ex ex;
     std::function<void(pcg_ctx*)> run;   // kernels of one rank (ex == None)
@@ -308,61 +329,39 @@ Status run_steps(pcg_ctx* c, const std::vector<Step>& steps) {
     for (const Step& s : steps) {
         switch (s.ex) {
             case Ex::None: s.run(c); break;
-            case Ex::Allgather: if (Status r = allgather_loc(c); !r) return r; break;
-            case Ex::HaloX: if (Status r = halo(c, c->x, false); !r) return r; break;
-            case Ex::HaloS: if (Status r = halo(c, c->s, false); !r) return r; break;
-            case Ex::HaloSAllgather: if (Status r = halo(c, c->s, true); !r) return r; break;
-            case Ex::AllgatherQR: if (Status r = exch_halo_ainv(c, true, false, true, s.par); !r) return r; break;
-            case Ex::QR: if (Status r = exch_halo_ainv(c, true, false, false, s.par); !r) return r; break;
-            case Ex::HaloT: if (Status r = exch_halo_ainv(c, false, true, false, 0); !r) return r; break;
+            default: if (Status r = nccl_exchange(c, s.ex, s.par); !r) return r; break;
         }
     }
     CU(cudaGetLastError());
     return Status::ok();
 }
 
-// exchanges between the contexts of one process (same device, one stream)
+// local-ranks backend (the contexts of one process on one GPU, one stream): every pair of
+// neighbours' matching list entries becomes a device copy; a count that differs between sender
+// and receiver is a plan inconsistency (the NCCL path would deadlock or corrupt on it)
 Status local_exchange(const std::vector<pcg_ctx*>& cs, Ex ex, cudaStream_t st, int par) {
     const size_t P = cs.size();
-    if (ex == Ex::AllgatherQR || ex == Ex::QR || ex == Ex::HaloT) {
-        for (size_t r = 1; r < P; ++r) {
-            pcg_ctx* lo = cs[r - 1];
-            pcg_ctx* up = cs[r];
-            const size_t pt = (size_t)lo->plan.pitch, Hl = (size_t)lo->plan.halo, Hu = (size_t)up->plan.halo;
-            const size_t nl = (size_t)lo->plan.nloc;
-            if (ex != Ex::HaloT) {
-                const size_t w = (size_t)up->plan.halo_w;
-                if (lo->plan.halo_w_send != up->plan.halo_w)     // the NCCL path sends halo_w_send rows
-                    return Status::err(PCG_ERR_ARG, "internal: q / r halo rows sent != rows expected");
-                if (w > 0) {
-                    CU(cudaMemcpyAsync(up->q + (Hu - w) * pt, lo->q + (Hl + nl - w) * pt, w * pt * sizeof(double), cudaMemcpyDeviceToDevice, st));
-                    CU(cudaMemcpyAsync(up->r[par] + (Hu - w) * pt, lo->r[par] + (Hl + nl - w) * pt, w * pt * sizeof(double), cudaMemcpyDeviceToDevice, st));
-                }
-            } else {
-                if (up->plan.halo_t_send != lo->plan.halo_t)
-                    return Status::err(PCG_ERR_ARG, "internal: t halo rows sent != rows expected");
-                const size_t n = (size_t)lo->plan.halo_t;
-                if (n > 0) CU(cudaMemcpyAsync(lo->t + (Hl + nl) * pt, up->t + Hu * pt, n * pt * sizeof(double), cudaMemcpyDeviceToDevice, st));
-            }
+    std::vector<XferList> L;
+    for (pcg_ctx* c : cs) L.push_back(exchange_list(c, ex, par));
+    for (size_t r = 1; r < P; ++r) {
+        const XferList &lo = L[r - 1], &up = L[r];
+        if (lo.send_north.size() != up.recv_south.size() || up.send_south.size() != lo.recv_north.size())
+            return Status::err(PCG_ERR_ARG, "internal: halo messages sent != messages expected");
+        for (size_t k = 0; k < lo.send_north.size(); ++k) {
+            const Xfer &s = lo.send_north[k], &d = up.recv_south[k];
+            if (s.n != d.n) return Status::err(PCG_ERR_ARG, "internal: halo rows sent north != rows expected");
+            CU(cudaMemcpyAsync(d.arr + d.off, s.arr + s.off, (size_t)s.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
         }
-        if (ex != Ex::AllgatherQR) return Status::ok();
+        for (size_t k = 0; k < up.send_south.size(); ++k) {
+            const Xfer &s = up.send_south[k], &d = lo.recv_north[k];
+            if (s.n != d.n) return Status::err(PCG_ERR_ARG, "internal: halo rows sent south != rows expected");
+            CU(cudaMemcpyAsync(d.arr + d.off, s.arr + s.off, (size_t)s.n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        }
     }
-    if (ex == Ex::Allgather || ex == Ex::HaloSAllgather || ex == Ex::AllgatherQR)
+    if (L[0].allgather)
         for (size_t r = 0; r < P; ++r)
             for (size_t q = 0; q < P; ++q)
                 CU(cudaMemcpyAsync(cs[r]->gath + 4 * q, cs[q]->sc->loc, 4 * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    if (ex == Ex::HaloX || ex == Ex::HaloSAllgather || ex == Ex::HaloS) {
-        for (size_t r = 1; r < P; ++r) {
-            pcg_ctx* lo = cs[r - 1];
-            pcg_ctx* up = cs[r];
-            double* alo = ex == Ex::HaloX ? lo->x : lo->s;
-            double* aup = ex == Ex::HaloX ? up->x : up->s;
-            const size_t pitch = (size_t)lo->plan.pitch, bytes = pitch * sizeof(double);
-            const size_t Hl = (size_t)lo->plan.halo, Hu = (size_t)up->plan.halo;
-            CU(cudaMemcpyAsync(aup + (Hu - 1) * pitch, alo + (Hl + lo->plan.nloc - 1) * pitch, bytes, cudaMemcpyDeviceToDevice, st));
-            CU(cudaMemcpyAsync(alo + (Hl + lo->plan.nloc) * pitch, aup + Hu * pitch, bytes, cudaMemcpyDeviceToDevice, st));
-        }
-    }
     return Status::ok();
 }
 
@@ -459,10 +458,15 @@ Status build_graph(pcg_ctx* c) {
     return st;
 }
 
-Status ensure_hist(pcg_ctx* c, int32_t maxit) {
-    const int32_t need = maxit + 1;
+// Device residual history: only as many entries as the caller can receive, min(maxit + 1,
+// hist_cap) (at least 1024, computed in 64 bits), not maxit + 1 -- a large maxit (bench.py passes
+// 20 ni nj) must not allocate gigabytes; the last value is kept in DevScalars::hlast.
+Status ensure_hist(pcg_ctx* c, int32_t maxit, int32_t hist_cap) {
+    const int64_t want = std::min<int64_t>((int64_t)maxit + 1, std::max<int64_t>(hist_cap, 1));
+    const int64_t need = std::max<int64_t>(want, 1024);
     if (need <= c->hist_cap) return Status::ok();
-    int32_t cap = std::max(need, 1024);
+    if (need > INT32_MAX) return Status::err(PCG_ERR_ARG, "pcg_solve: history longer than 2^31 entries");
+    const int32_t cap = (int32_t)need;
     if (c->hist) { CU(cudaFree(c->hist)); c->allocs.erase(std::find(c->allocs.begin(), c->allocs.end(), (void*)c->hist)); c->dev_bytes -= (int64_t)c->hist_cap * 8; }
     if (c->h_hist) CU(cudaFreeHost(c->h_hist));
     c->hist = nullptr; c->h_hist = nullptr;
@@ -485,11 +489,12 @@ Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, doubl
     if (P.flags & PCG_FLAG_LOCAL_RANKS)
         return Status::err(PCG_ERR_ARG, "pcg_solve: a PCG_FLAG_LOCAL_RANKS context is solved with pcg_solve_local_ranks");
     CU(cudaSetDevice(c->device));
-    if (Status s = ensure_hist(c, maxit); !s) return s;
+    if (Status s = ensure_hist(c, maxit, res_hist ? hist_cap : 1); !s) return s;
     if (use_graph(c) && !c->graph_built) {
         if (Status s = build_graph(c); !s) {
             if (!c->multi) return s;
             c->graph_failed = true;                      // NCCL path: fall back to the host loop
+            if (getenv("PCG_VERBOSE")) fprintf(stderr, "libpcg: NCCL graph capture failed (%s): host loop\n", s.msg.c_str());
             cudaGetLastError();
         }
     }
@@ -585,7 +590,7 @@ Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, doubl
     if (res_hist) std::memcpy(res_hist, c->h_hist, (size_t)std::min(nh, hist_cap) * sizeof(double));
     pcg_report R{};
     R.iterations = k;
-    R.rel_residual = c->h_hist[std::min(k, c->hist_cap - 1)];
+    R.rel_residual = S.hlast;
     R.converged = S.status == kStOk && R.rel_residual <= tol;
     R.true_rel_residual = S.true_rel;
     R.setup_s = P.setup_s;
@@ -594,6 +599,10 @@ Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, doubl
     R.n_ocean = P.n_owned;
     R.nnz_z = P.nnz_off;
     R.failed_index = -1;
+    if (c->multi) R.driver = use_graph(c) ? PCG_DRIVER_NCCL_GRAPH : c->graph_failed ? PCG_DRIVER_NCCL_FALLBACK : PCG_DRIVER_NCCL_HOST_LOOP;
+    else if (use_rs(c)) R.driver = PCG_DRIVER_RESIDENT;
+    else if (use_fused(c)) R.driver = PCG_DRIVER_LOOP;
+    else R.driver = use_graph(c) ? PCG_DRIVER_GRAPH : PCG_DRIVER_HOST_LOOP;
     if (report) *report = R;
     c->solved_once = true;
     if (S.status == kStBreakdown)
@@ -1031,6 +1040,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
             size_t setaside = std::min<size_t>((size_t)maxp, c->hot_bytes + c->ovf_bytes);
             size_t cur = 0;
             cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+            if (l2_users(c->device, 0) == 0) l2_limit_before(c->device) = cur;   // the host application's own set-aside
             if (cur < setaside) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, setaside);
             cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
             cudaGetLastError();
@@ -1130,7 +1140,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     else { c->bytes_k[1] = 40.0 * No; c->bytes_k[2] = 0.0; }
     CU(cudaGetLastError());
     if (Status s = setup_rs(c); !s) return s;
-    if (Status s = ensure_hist(c, 1023); !s) return s;
+    if (Status s = ensure_hist(c, 1023, 1024); !s) return s;
     CU(cudaStreamSynchronize(c->st));
     // release the bulky host copies
     P.cE.clear(); P.cE.shrink_to_fit(); P.cN.clear(); P.cN.shrink_to_fit();
@@ -1142,7 +1152,8 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     if (use_graph(c)) {
         if (Status s = build_graph(c); !s) {
             if (c->multi) {
-                c->graph_failed = true;                   // NCCL path: host loop
+                c->graph_failed = true;                   // NCCL path: host loop (report.driver says so)
+                if (getenv("PCG_VERBOSE")) fprintf(stderr, "libpcg: NCCL graph capture failed (%s): host loop\n", s.msg.c_str());
                 cudaGetLastError();
             } else {
                 if (!c->A.pdl) return s;
@@ -1205,11 +1216,16 @@ void pcg_free(pcg_ctx* c) {
     if (c->st) cudaStreamSynchronize(c->st);
     if (c->exec) cudaGraphExecDestroy(c->exec);
     if (c->A.l2_bytes) {
-        cudaCtxResetPersistingL2Cache();                  // its window's lines become normal lines
-        // the last window user of the device gives the set-aside back: a set-aside left behind
-        // slows the next, window-less solve (cfg5 Jacobi after a cfg4 solve in one process: 634
-        // against 384 us/iteration)
-        if (l2_users(c->device, -1) == 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, 0);
+        // the last window user of the device turns the persisting lines back into normal lines
+        // (earlier, that would evict the lines of contexts still solving) and gives the set-aside
+        // back -- restoring the host application's own value: a set-aside left behind slows the
+        // next, window-less solve (cfg5 Jacobi after a cfg4 solve in one process: 634 against
+        // 384 us/iteration)
+        if (l2_users(c->device, -1) == 0) {
+            cudaCtxResetPersistingL2Cache();
+            const size_t before = l2_limit_before(c->device);
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, before == (size_t)-1 ? 0 : before);
+        }
         cudaGetLastError();
     }
     for (void* p : c->allocs) cudaFree(p);
@@ -1238,7 +1254,7 @@ pcg_status pcg_apply_operator(pcg_ctx* c, const double* x, double* y) {
         // stage x in t (zero rows/padding first so halos and padding read 0), result in q
         CU(cudaMemsetAsync(c->t, 0, (size_t)P.elements() / (size_t)P.pitch * dp, c->st));
         CU(cudaMemcpy2DAsync(c->t + P.hoff(), dp, x, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
-        if (c->multi) if (Status s = halo(c, c->t, false); !s) return s;
+        if (c->multi) if (Status s = nccl_exchange(c, Ex::None, 0, c->t); !s) return s;
         launch_apply(c->A, c->t, c->q, c->st);
         CU(cudaGetLastError());
         CU(cudaMemcpy2DAsync(y, sp, c->q + P.hoff(), dp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
@@ -1314,7 +1330,7 @@ pcg_status pcg_solve_local_ranks(pcg_ctx* const* ctxs, int32_t n, const double* 
         for (int32_t r = 0; r < n; ++r) { keep[r] = cs[r]->st; cs[r]->st = st; }   // one stream for all ranks
         Status out = Status::ok();
         do {
-            for (pcg_ctx* c : cs) if (!(out = ensure_hist(c, maxit))) break;
+            for (pcg_ctx* c : cs) if (!(out = ensure_hist(c, maxit, res_hist ? hist_cap : 1))) break;
             if (!out) break;
             CU(cudaEventRecord(cs[0]->ev_in, cs[0]->user_stream));
             CU(cudaStreamWaitEvent(st, cs[0]->ev_in, 0));
@@ -1364,12 +1380,13 @@ pcg_status pcg_solve_local_ranks(pcg_ctx* const* ctxs, int32_t n, const double* 
             if (report) {
                 pcg_report R{};
                 R.iterations = k;
-                R.rel_residual = c->h_hist[std::min(k, c->hist_cap - 1)];
+                R.rel_residual = S.hlast;
                 R.converged = S.status == kStOk && R.rel_residual <= tol;
                 R.true_rel_residual = S.true_rel;
                 R.solve_s = ms * 1e-3;
                 for (pcg_ctx* q : cs) { R.n_ocean += q->plan.n_owned; R.nnz_z += q->plan.nnz_off; R.setup_s = std::max(R.setup_s, q->plan.setup_s); }
                 R.failed_index = -1;
+                R.driver = PCG_DRIVER_LOCAL_RANKS;
                 *report = R;
             }
             if (S.status == kStBreakdown) out = Status::err(PCG_ERR_BREAKDOWN, "pcg_solve_local_ranks: breakdown");
@@ -1415,7 +1432,7 @@ pcg_status pcg_kernel_times(pcg_ctx* c, int32_t n_iter, double* ms_out, double* 
         c->h_sc->tol = 0.0; c->h_sc->maxit = n_iter + 2; c->h_sc->active = 1;
         CU(cudaMemcpyAsync(c->sc, c->h_sc, sizeof(DevScalars), cudaMemcpyHostToDevice, c->st));
         CU(cudaMemsetAsync(c->x, 0, (size_t)c->plan.elements() * sizeof(double), c->st));
-        if (Status s = ensure_hist(c, n_iter + 2); !s) return s;
+        if (Status s = ensure_hist(c, n_iter + 2, n_iter + 3); !s) return s;
         KArgs A = c->A;
         A.use_cond = 0;
         {

@@ -7,6 +7,8 @@ Bar (north star / SURVEY §8(c.4)):
   * plain order: iterations within +-max(2, 1 %), ||x_gpu - x_cpu||/||x_cpu|| <= 1e-9 at
     tol 1e-12, final relative residual <= tol (recurrence and true).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -99,7 +101,7 @@ def test_solve_vs_plain_oracle(name):
     x = A.from_grid(host(xg))
     assert abs(k - ref.iterations) <= max(2, 0.01 * ref.iterations)
     assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) <= 1e-9
-    assert rep["rel_residual"] <= 1e-12 and rep["true_rel_residual"] <= 1.5e-12
+    assert rep["rel_residual"] <= 1e-12 and rep["true_rel_residual"] <= 1e-12
     xs = A.from_grid(synth.xstar(p))
     assert np.linalg.norm(x - xs) / np.linalg.norm(xs) < 1e-7
     S.close()
@@ -227,7 +229,7 @@ def test_cfg4_full_size_sampled():
     xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=0.0, maxit=5)
     assert k == 5 and np.array_equal(hist, ref.hist) and np.array_equal(host(xg), A.to_grid(ref.x))
     xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
-    assert rep["converged"] == 1 and rep["true_rel_residual"] < 2e-10
+    assert rep["converged"] == 1 and rep["true_rel_residual"] <= 1e-10
     assert 1200 <= k <= 1420                                             # ~1300
     x = A.from_grid(host(xg))
     assert np.linalg.norm(x - xs) / np.linalg.norm(xs) < 5e-6
@@ -253,7 +255,7 @@ def test_cfg4_full_solve_vs_oracle():
     print(f"cfg4 plain order, tol 1e-12: GPU {k} iterations, oracle {ref.iterations}, "
           f"|x_gpu - x_cpu|/|x_cpu| = {np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x):.3e}")
     assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) <= 1e-9
-    assert rep["rel_residual"] <= 1e-12 and rep["true_rel_residual"] <= 1.5e-12
+    assert rep["rel_residual"] <= 1e-12 and rep["true_rel_residual"] <= 1e-12
     # DESIGN.md §9 band: the summation order alone moves the count near 1e-12 (measured 1773 vs 1776)
     assert abs(k - ref.iterations) <= max(2, 0.01 * ref.iterations)
     S.close()
@@ -262,7 +264,7 @@ def test_cfg4_full_solve_vs_oracle():
 def test_cfg5_full_size_sampled():
     """BASELINE's largest config (ORCA12-like 4322x3059, 10.9 M unknowns, tol 1e-12) on one GPU in
     the bench's launch configuration: operator and preconditioner bitwise on the full grid, the
-    first 3 iterations bitwise, then the full solve's properties (converged with the recurrence
+    first 17 iterations bitwise, then the full solve's properties (converged with the recurrence
     and the true residual <= tol-level, error vs x*, iterations near SURVEY §8(d)'s estimate)."""
     p = synth.config("cfg5")
     A, M, S = setup_pair(p)
@@ -272,11 +274,12 @@ def test_cfg5_full_size_sampled():
     assert np.array_equal(y, A.to_grid(A.apply_canonical(xs)))
     s = host(S.apply_preconditioner(dev(A.to_grid(b))))
     assert np.array_equal(s, A.to_grid(M.apply_canonical(b)))
-    ref = oracle.pcg(A, b, "ainv", M, 0.0, maxit=3, mode="canonical", pitch=S.pitch, block=S.block, rows=S.tile_rows)
-    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=0.0, maxit=3)
-    assert k == 3 and np.array_equal(hist, ref.hist) and np.array_equal(host(xg), A.to_grid(ref.x))
+    # 17 iterations: across two 8-iteration WHILE bodies of the graph driver
+    ref = oracle.pcg(A, b, "ainv", M, 0.0, maxit=17, mode="canonical", pitch=S.pitch, block=S.block, rows=S.tile_rows)
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=0.0, maxit=17)
+    assert k == 17 and np.array_equal(hist, ref.hist) and np.array_equal(host(xg), A.to_grid(ref.x))
     xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-12, maxit=A.n)
-    assert rep["converged"] == 1 and rep["true_rel_residual"] < 5e-12
+    assert rep["converged"] == 1 and rep["true_rel_residual"] <= 1e-12
     assert 4400 <= k <= 5000                                             # ~4800 +-15 %
     x = A.from_grid(host(xg))
     assert np.linalg.norm(x - xs) / np.linalg.norm(xs) < 1e-6
@@ -402,7 +405,7 @@ def test_fsai_solve_vs_plain_oracle():
     x = A.from_grid(host(xg))
     assert abs(k - ref.iterations) <= max(2, 0.01 * ref.iterations)
     assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) <= 1e-9
-    assert rep["true_rel_residual"] <= 1e-12 * 1.5
+    assert rep["true_rel_residual"] <= 1e-12
     S.close()
 
 
@@ -652,7 +655,7 @@ def test_cg1_vs_alg1_plain():
     assert abs(k - ref.iterations) <= max(2, ref.iterations // 100)
     x = A.from_grid(host(xg))
     assert np.linalg.norm(x - ref.x) / np.linalg.norm(ref.x) <= 1e-9
-    assert rep["true_rel_residual"] <= 2e-12
+    assert rep["true_rel_residual"] <= 1e-12
     S.close()
     with pytest.raises(pcg.PcgError):
         pcg.Solver(p.cE, p.cN, p.mask, precond="jacobi", flags=pcg.FLAG_SINGLE_REDUCTION)
@@ -738,7 +741,7 @@ def test_cfg4_full_size_other_preconditioners(precond):
     xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=0.0, maxit=5)
     assert k == 5 and np.array_equal(hist, ref.hist) and np.array_equal(host(xg), A.to_grid(ref.x))
     xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-10, maxit=A.n)
-    assert rep["converged"] == 1 and rep["true_rel_residual"] < 2e-10
+    assert rep["converged"] == 1 and rep["true_rel_residual"] <= 1e-10
     assert abs(k - (3004 if precond == "fsai" else 2618)) <= 30
     S.close()
 
@@ -767,4 +770,132 @@ def test_timestep_warm_modes_and_aliasing():
             assert rep["converged"] == 1
             its[warm] += k
     assert its["zero"] >= its["previous"] >= its["extrapolate"]
+    S.close()
+
+
+# ------------------------------------------ the NCCL path across real GPUs (skipped on 1 GPU)
+@pytest.mark.parametrize("w", [0, 3])
+def test_nccl_two_ranks_equals_local_ranks(w, tmp_path):
+    """Two processes, one GPU each, NCCL send/recv halos and allgathered rank sums (the code the
+    one-GPU tests reach only through the local-ranks backend): the solve equals the local-ranks
+    emulation and the oracle's partitioned canonical PCG bit for bit.  Needs >= 2 GPUs."""
+    import subprocess
+    import sys
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    p = synth.config("cfg3")
+    A = oracle.assemble(p)
+    b = A.to_grid(rhs(A, p))
+    out = str(tmp_path / "nccl2")
+    np.save(out + ".b.npy", b)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
+           "127.0.0.1", "--master-port", "29531", os.path.join(root, "tests", "nccl_worker.py"), out, "cfg3", str(w)]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    got = np.load(out + ".npz")
+    R = pcg.LocalRanks(p.cE, p.cN, p.mask, 2, tau=TAU, ainv_halo=w)
+    xg, k, hist, rep = R.solve(dev(b), tol=1e-10, maxit=A.n)
+    assert int(got["k"]) == k and np.array_equal(got["hist"], hist)
+    assert np.array_equal(got["x"], host(xg))
+    assert int(got["driver"]) in (4, 5)
+    M = oracle.ainv(A, TAU, parts=2, halo=w)
+    ref = oracle.pcg(A, A.from_grid(b), "ainv", M, 1e-10, maxit=A.n, mode="canonical", pitch=R.pitch, block=R.block,
+                     parts=2)
+    assert k == ref.iterations and np.array_equal(hist, ref.hist)
+    R.close()
+
+
+# ------------------------------------------- plain (sequential) order: the north-star bar itself
+def _plain_bar(x_gpu, x_ref, k_gpu, k_ref, rep, tol):
+    """||x_gpu - x_cpu|| / ||x_cpu|| <= 1e-9 at tol 1e-12, iterations within
+    +-max(2, 1 %) of the sequential-order oracle, recurrence and true residual <= tol."""
+    assert np.linalg.norm(x_gpu - x_ref) / np.linalg.norm(x_ref) <= 1e-9
+    assert abs(k_gpu - k_ref) <= max(2, 0.01 * k_ref)
+    assert rep["rel_residual"] <= tol
+    assert rep["true_rel_residual"] <= tol
+
+
+@pytest.mark.parametrize("name,P,w", [("cfg3", 2, 0), ("cfg3", 4, 3), ("cfg3", 8, "global"), ("cfg2", 4, 0),
+                                      ("cfg2", 8, 3), ("cfg2", 2, "global")])
+def test_local_ranks_vs_plain_oracle(name, P, w):
+    """The multi-rank device path (P ranks on one GPU) against the oracle's PLAIN sequential-order
+    PCG with the same partitioned preconditioner (parts = P, halo = w; "global" = the one-rank Z),
+    at tol 1e-12 -- not only the kernel-mirroring canonical mode."""
+    p = synth.config(name)
+    A = oracle.assemble(p)
+    halo = p.nj if w == "global" else w
+    M = oracle.ainv(A, TAU, parts=P, halo=halo)
+    b = rhs(A, p)
+    R = pcg.LocalRanks(p.cE, p.cN, p.mask, P, tau=TAU, ainv_halo=halo)
+    ref = oracle.pcg(A, b, "ainv", M, 1e-12, maxit=A.n)
+    xg, k, hist, rep = R.solve(dev(A.to_grid(b)), tol=1e-12, maxit=A.n)
+    _plain_bar(A.from_grid(host(xg)), ref.x, k, ref.iterations, rep, 1e-12)
+    R.close()
+
+
+@pytest.mark.parametrize("name,fill", [("cfg2", 3), ("cfg3", 5)])
+def test_pb2_vs_plain_oracle(name, fill):
+    """P_B2 (fixed fill per column, reading R26) against the sequential-order oracle at tol 1e-12."""
+    p = synth.config(name)
+    A = oracle.assemble(p)
+    M = oracle.ainv(A, 0.0, fill=fill)
+    S = pcg.Solver(p.cE, p.cN, p.mask, periodic=p.periodic, tau=0.0, ainv_fill=fill)
+    b = rhs(A, p)
+    ref = oracle.pcg(A, b, "ainv", M, 1e-12, maxit=A.n)
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-12, maxit=A.n)
+    _plain_bar(A.from_grid(host(xg)), ref.x, k, ref.iterations, rep, 1e-12)
+    S.close()
+
+
+def test_timestep_driver_vs_plain_oracle():
+    """Five time steps of the NEMO-style driver (warm start 2 D^n - D^{n-1}) against the plain
+    oracle run from ITS OWN previous solutions, each step at tol 1e-12."""
+    from paper_1210_1878_b200 import timestep
+    p = synth.config("cfg2")
+    A, M, S = setup_pair(p)
+    st = timestep.Stepper(S, "extrapolate")
+    prev = cur = None
+    for f in synth.forcing_series(p, 5):
+        b = A.apply(A.from_grid(f))
+        x0 = None if cur is None else (cur if prev is None else 2.0 * cur - prev)
+        ref = oracle.pcg(A, b, "ainv", M, 1e-12, maxit=A.n, x0=x0)
+        xg, k, rep = st.step(dev(A.to_grid(b)), tol=1e-12, maxit=A.n)
+        _plain_bar(A.from_grid(host(xg)), ref.x, k, ref.iterations, rep, 1e-12)
+        prev, cur = cur, ref.x
+    S.close()
+
+
+# ---------------------------------------------------- the resident-strip driver (rs.cu) itself
+@pytest.mark.parametrize("kind,precond", [("sigma_nonperiodic", "ainv"), ("ragged", "ainv"), ("ragged", "jacobi"),
+                                          ("sigma_nonperiodic", "none")])
+def test_resident_driver_edge_grids_bitwise(kind, precond, monkeypatch):
+    """Grids large enough for the resident-strip driver (>= 148 row segments) with sigma, no
+    E-W wrap and a ragged last segment: bitwise the oracle's canonical PCG and the graph driver."""
+    if kind == "sigma_nonperiodic":
+        p = synth.random_grid(300, 160, 21, periodic=False, sigma=True)
+    else:
+        p = synth.random_grid(333, 170, 22)
+    A, S, ref, x, k, hist, rep, _ = _canonical_pair(p, precond, 1e-12)
+    assert rep["driver_name"] == "resident"
+    assert k == ref.iterations and np.array_equal(hist, ref.hist)
+    assert np.array_equal(x, A.to_grid(ref.x))
+    assert rep["true_rel_residual"] == ref.true_rel_residual
+    S.close()
+    monkeypatch.setenv("PCG_RS", "0")
+    A2, S2, ref2, x2, k2, hist2, rep2, _ = _canonical_pair(p, precond, 1e-12)
+    assert rep2["driver_name"] != "resident"
+    assert k2 == k and np.array_equal(hist2, hist) and np.array_equal(x2, x)
+    S2.close()
+
+
+def test_resident_driver_cfg4_is_default():
+    """bench.py's workload runs on the resident-strip driver (report.driver), one launch per solve."""
+    p = synth.config("cfg4")
+    S = pcg.Solver(p.cE, p.cN, p.mask, tau=TAU)
+    b = S.apply_operator(dev(synth.xstar(p)))
+    x, k, hist, rep = S.solve(b, tol=1e-10)
+    assert rep["driver_name"] == "resident" and rep["converged"] == 1
+    ms, it = S.loop_time()
+    assert it == k and ms > 0
     S.close()
