@@ -314,8 +314,6 @@ def main():
         S.solve(b, tol=args.tol, maxit=maxit)
         ms, by = S.kernel_times(args.profile_iters)
         names = ["K1_stencil", "K2_ZTr", "K3_Zt"]
-        if by[2] == 0 and args.precond in ("ainv", "fsai"):
-            names[1] = "K23_ZTr_Zt"                              # K2 and K3 fused into one kernel
         kk = int(np.argmax(ms[:3]))
         ach = by[kk] / (ms[kk] * 1e-3) / 1e9
         traffic = None
@@ -352,10 +350,9 @@ def main():
                          f"oracle's own assembly+AINV ({r['setup_s']:.2f} s, excluded)"}
 
     # launches per solve: prologue 4 (prep, init, K2, K3) + WHILE bodies of PCG_BODY_ITERS (8)
-    # iterations x 3 + epilogue 2 (K23: prologue 3, 2 per iteration)
-    fused = ktimes is not None and "K23_ZTr_Zt" in ktimes
-    per_iter = 3 if args.precond in ("ainv", "fsai") and not fused else 2
-    pro = 4 if args.precond in ("ainv", "fsai") and not fused else 3
+    # iterations x 3 + epilogue 2; the resident-strip driver: prologue + 1 + epilogue
+    per_iter = 3 if args.precond in ("ainv", "fsai") else 2
+    pro = 4 if args.precond in ("ainv", "fsai") else 3
     if args.method == "cg1":
         pro = 5                                                  # + KC's w0 = A u0 (alpha0)
     if rs_used:

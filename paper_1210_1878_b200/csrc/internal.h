@@ -57,24 +57,6 @@ struct Ell {
     int64_t entries() const { return (int64_t)val.size() + ovf.entries(); }
 };
 
-// Structured form of Z / Z^T rows: at tau = 0.1 on ORCA-like grids 99.9 % of rows
-// are N-S entries at +-pitch, +-2 pitch plus one contiguous E-W run from the element itself, so
-// every column is known from the element's index and a run length k (no column indices, and no
-// gather waits on an index load).  Ascending column order, i.e. the fma order:
-//   Z^T row (dir -1): a-2P, a-P, run a-k .. a-2, a-1, a        slots 0, 1, run, 2, 3
-//   Z   row (dir +1): a, a+1, run a+2 .. a+k, a+P, a+2P        slots 0, 1, run, 2, 3
-// Absent entries are value 0 (fma(0, x, acc) leaves acc unchanged, as the ELL padding); run
-// values (columns a-k .. a-2 resp. a+2 .. a+k, zero where a column inside the run is absent) in a
-// SELL-32 per warp of 32 elements.  A warp with any row outside this form is flagged generic and
-// applies the ELL form instead.
-struct Sz {
-    bool ok = false;
-    std::vector<double> val4;      // 4 per owned element
-    std::vector<uint8_t> k;        // run length k per owned element (0: no E-W entry)
-    std::vector<uint32_t> w;       // per warp of 32 elements: {rounds | generic << 31, run offset}
-    std::vector<double> run;       // SELL-32 run values
-    int64_t fillers = 0, generic_warps = 0;
-};
 
 // Host product of setup: everything the device needs, in device layout.
 struct Plan {
@@ -97,7 +79,6 @@ struct Plan {
     // per-element arrays, (nloc + 2) * pitch
     std::vector<double> cE, cN, sigma, diag, piv;
     Ell Z, ZT;                     // rows of Z (for s = Z t) and of Z^T (for t = Z^T r)
-    Sz sZ, sZT;                    // the same rows in structured form (ok = false: not built / not used)
     // FSAI (NEXT-1) DIA form when every chain link is an E-W neighbour pair: dia[m-1][e] =
     // zhat between owned element e - m and e (the column k = e's entry at row k - m), m = 1..dia_q;
     // 0 where the chain is shorter.  dia_q = 0: no DIA form (the ELL path applies the factor).

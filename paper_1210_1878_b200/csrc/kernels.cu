@@ -643,43 +643,6 @@ __device__ __forceinline__ double k1_point(const KArgs& A, const Unit& W, int pa
     return k1_compute<SIGMA>(A, W, par, beta, alpha, L);
 }
 
-#ifndef PCG_MINB_K1P
-#define PCG_MINB_K1P 3
-#endif
-// K1, row-segment form with two units per thread in flight (units u and u + G of the block
-// stride: both points' loads issued before either computes).  Redundant-sum mode only; same
-// units, slots and arithmetic as k1_flat_kernel's static walk (bitwise).
-template <bool SIGMA>
-__global__ void __launch_bounds__(kBlock, PCG_MINB_K1P) k1_pair_kernel(const KArgs A, const int par) {
-    pdl_wait();
-    if (!is_active(A)) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        if (++A.sc->guard > A.sc->maxit + 2) {          // safety net for the WHILE node
-            A.sc->active = 0;
-            A.sc->status = kStBreakdown;
-            set_cond(A, 0);
-        }
-    }
-    double beta;
-    if (!k1_beta(A, par, beta)) return;
-    const double alpha = A.sc->alpha;
-    extern __shared__ double ws[];
-    const int64_t U = n_units(A), G = gridDim.x;
-    int k = 0;
-    for (int64_t u = blockIdx.x; u < U; u += 2 * G, k += 2) {
-        const Unit W0 = unit_of(A, u);
-        const bool two = u + G < U;
-        const Unit W1 = unit_of(A, two ? u + G : u);
-        K1Ld L0, L1;
-        k1_load(A, W0, par, L0);
-        if (two) k1_load(A, W1, par, L1);
-        put_warp_sum(ws, k, k1_compute<SIGMA>(A, W0, par, beta, alpha, L0));
-        if (two) put_warp_sum(ws, k + 1, k1_compute<SIGMA>(A, W1, par, beta, alpha, L1));
-    }
-    pdl_trigger();
-    finish_units<1>(A, ws, A.partial[0], nullptr, nullptr);
-}
-
 template <bool SIGMA>
 __global__ void __launch_bounds__(kBlock, PCG_MINB_K1F) k1_flat_kernel(const KArgs A, const int par) {
     pdl_wait();
@@ -864,183 +827,12 @@ __device__ __forceinline__ double ell_row16(const EllDev& E, int64_t e, int64_t 
     return overflow_sum(E, e, acc, gat);
 }
 
-// ---- structured Z / Z^T rows (internal.h Sz; DQ = -2 kernels) ---------------------
-// Every column is the element's own index plus a fixed offset or a run position, so the fixed
-// slots' gathers issue together with the value loads (no index load in between); a run of k
-// entries costs one more stage: its values and gathers, four per round, the next round's loads
-// in flight before this round's fmas.  A warp flagged generic applies the ELL form.  Same entries,
-// same ascending-column fma order as the ELL row (zero slots are fma(0, x, acc) = acc).
-template <class Gather>
-__device__ __forceinline__ double run_sum(const double* run, int nr, int rounds, int64_t g0, double acc, Gather gat) {
-    double zn[4], xn[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const bool in = u < nr;
-        zn[u] = in ? __ldg(run + 32 * u) : 0.0;
-        xn[u] = in ? gat(g0 + u) : 0.0;
-    }
-    for (int m0 = 0; m0 < rounds; m0 += 4) {
-        double z[4], x[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) { z[u] = zn[u]; x[u] = xn[u]; }
-        if (m0 + 4 < rounds) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int j = m0 + 4 + u;
-                const bool in = j < nr;
-                zn[u] = in ? __ldg(run + 32 * j) : 0.0;
-                xn[u] = in ? gat(g0 + j) : 0.0;
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (m0 + u < nr) acc = __fma_rn(z[u], x[u], acc);
-    }
-    return acc;
-}
-
-// Z^T row of owned element e at array index a (K2): a-2P, a-P, run a-k .. a-2, a-1, a (= xself)
-template <class Gather>
-__device__ __forceinline__ double sz_zt_row(const KArgs& A, int64_t e, int64_t a, double xself, Gather gat) {
-    const SzDev& S = A.szt;
-    const int64_t P = A.pitch;
-    const uint2 w = __ldg(S.w + (e >> 5));
-    const int k = __ldg(S.k + e);
-    double v[4];
-    ld_nc_f64x4(S.val4 + 4 * e, v);
-    const double x0 = gat(a >= 2 * P ? a - 2 * P : a);
-    const double x1 = gat(a - P);
-    const double x2 = gat(a - 1);
-    if (w.x >> 31) return A.zt.col16 ? ell_row16(A.zt, e, a, gat) : ell_row(A.zt, e, gat);
-    double acc = __fma_rn(v[0], x0, 0.0);
-    acc = __fma_rn(v[1], x1, acc);
-    if (w.x) acc = run_sum(S.run + w.y + (e & 31), k - 1, (int)w.x, a - k, acc, gat);
-    acc = __fma_rn(v[2], x2, acc);
-    return __fma_rn(v[3], xself, acc);
-}
-
-// Z row of owned element e at array index a (K3): a, a+1, run a+2 .. a+k, a+P, a+2P
-template <class Gather>
-__device__ __forceinline__ double sz_z_row(const KArgs& A, int64_t e, int64_t a, Gather gat) {
-    const SzDev& S = A.sz;
-    const int64_t P = A.pitch;
-    const uint2 w = __ldg(S.w + (e >> 5));
-    const int k = __ldg(S.k + e);
-    double v[4];
-    ld_nc_f64x4(S.val4 + 4 * e, v);
-    const double x0 = gat(a);
-    const double x1 = gat(a + 1);
-    const double x2 = gat(a + P);
-    const double x3 = gat(a + 2 * P < A.nel_all ? a + 2 * P : a);
-    if (w.x >> 31) return A.z.col16 ? ell_row16(A.z, e, a, gat) : ell_row(A.z, e, gat);
-    double acc = __fma_rn(v[0], x0, 0.0);
-    acc = __fma_rn(v[1], x1, acc);
-    if (w.x) acc = run_sum(S.run + w.y + (e & 31), k - 1, (int)w.x, a + 2, acc, gat);
-    acc = __fma_rn(v[2], x2, acc);
-    return __fma_rn(v[3], x3, acc);
-}
-
-// ---- per-thread cp.async double buffer for the scheduled walks (DQ = -3: ELL(4) + int16 offsets) --
-// Each thread copies its own element's streamed operands of the NEXT unit into shared memory
-// (LDGSTS, no registers held) while it gathers and computes the current one, so the DRAM latency
-// of unit k+1 overlaps unit k's gathers, overflow rounds, fma chain and warp sum.  The thread
-// reads back only what it copied itself: cp.async.wait_group suffices, no block barrier.
-__device__ __forceinline__ void cp_async8(void* smem, const void* g) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* g) {
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// streamed operands of one unit of K2 (per thread: 4 Z^T values, 4 int16 slot offsets, r_old, q, pivot)
-struct K2Stage {
-    double2 v01[kBlock], v23[kBlock];
-    uint2 col[kBlock];
-    double r[kBlock], q[kBlock], piv[kBlock];
-};
-
-// K2's scheduled static walk (sched_units) with the double buffer; same units, same per-warp
-// sums, same arithmetic as the body of k2_ainv_kernel<-1> (bitwise).
-__device__ __forceinline__ void k2_sched_staged(const KArgs& A, int par, double alpha, double* ws, K2Stage* st) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
-    const int32_t* sched = A.sched2;
-    const int32_t k0 = A.soff2[blockIdx.x], k1 = A.soff2[blockIdx.x + 1];
-    const double* __restrict__ ro = A.r[par];
-    double* __restrict__ rn = A.r[par ^ 1];
-    const double* __restrict__ q = A.q;
-    auto unit_k = [&](int32_t k) {
-        Unit W = unit_of(A, sched[k]);
-        if (A.landskip) W.live = W.inrow && ((__ldg(A.ocean + ((int64_t)W.j * A.nbx + W.bx) * kWarps + warp) >> lane) & 1u);
-        return W;
-    };
-    auto issue = [&](const Unit& W, int buf) {
-        if (W.live) {
-            const int64_t e = W.a - A.hoff;
-            cp_async16(&st[buf].v01[tid], A.zt.val + e * kEll);
-            cp_async16(&st[buf].v23[tid], A.zt.val + e * kEll + 2);
-            cp_async8(&st[buf].col[tid], A.zt.col16 + e * kEll);
-            cp_async8(&st[buf].r[tid], ro + W.a);
-            cp_async8(&st[buf].q[tid], q + W.a);
-            cp_async8(&st[buf].piv[tid], A.piv + W.a);
-        }
-        cp_async_commit();
-    };
-    if (k0 >= k1) return;
-    Unit Wc = unit_k(k0);
-    issue(Wc, 0);
-    for (int32_t k = k0; k < k1; ++k) {
-        const int buf = (k - k0) & 1;
-        Unit Wn{};
-        if (k + 1 < k1) {
-            Wn = unit_k(k + 1);
-            issue(Wn, buf ^ 1);
-            cp_async_wait<1>();                          // unit k's group has landed
-        } else {
-            cp_async_wait<0>();
-        }
-        double v = 0.0;
-        if (Wc.live) {
-            const K2Stage& S = st[buf];
-            const double2 v01 = S.v01[tid], v23 = S.v23[tid];
-            const uint2 cw = S.col[tid];
-            const double rnew = __fma_rn(-alpha, S.q[tid], S.r[tid]);
-            const double pv = S.piv[tid];
-            auto gat = [&](int64_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); };
-            const int32_t sf = (int32_t)Wc.a;
-            const int32_t c[kEll] = {sf + (int32_t)(int16_t)(cw.x & 0xffffu), sf + (int32_t)(int16_t)(cw.x >> 16),
-                                     sf + (int32_t)(int16_t)(cw.y & 0xffffu), sf + (int32_t)(int16_t)(cw.y >> 16)};
-            double x[kEll];
-#pragma unroll
-            for (int m = 0; m < kEll; ++m) x[m] = gat(c[m]);
-            asm volatile("" : "+d"(x[0]), "+d"(x[1]), "+d"(x[2]), "+d"(x[3]));
-            double acc = 0.0;
-            acc = __fma_rn(v01.x, x[0], acc);
-            acc = __fma_rn(v01.y, x[1], acc);
-            acc = __fma_rn(v23.x, x[2], acc);
-            acc = __fma_rn(v23.y, x[3], acc);
-            acc = overflow_sum(A.zt, Wc.a - A.hoff, acc, gat);
-            A.t[Wc.a] = __ddiv_rn(acc, pv);
-            rn[Wc.a] = rnew;
-            v = __dmul_rn(rnew, rnew);
-        }
-        v = warp_tree(v);
-        if (lane == 0) ws[(k - k0) * kWarps + warp] = v;
-        Wc = Wn;
-    }
-}
-
 #ifndef PCG_MINB_K2
 #define PCG_MINB_K2 4            // register budgets: resident 256-thread blocks per SM ptxas targets
 #endif
 #ifndef PCG_MINB_K3
 #define PCG_MINB_K3 5
 #endif
-
 
 #ifndef PCG_FINAL_NB_K3
 #define PCG_FINAL_NB_K3 8            // measured: 93.4 -> 92.0 us/iteration vs 32 (fewer spills in K3)
@@ -1174,7 +966,6 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
             auto gat = [&](int64_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); };
             double acc;
             if constexpr (DQ > 0) acc = dia_zt_row<DQ>(A, W, rnew, gat);
-            else if constexpr (DQ == -2) acc = sz_zt_row(A, W.a - A.hoff, W.a, rnew, gat);
             else if constexpr (DQ < 0) acc = ell_row16(A.zt, W.a - A.hoff, W.a, gat);
             else acc = ell_row(A.zt, W.a - A.hoff, gat);
             A.t[W.a] = __ddiv_rn(acc, pv);
@@ -1184,12 +975,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) k2_ainv_kernel(const KArg
         return v;
     };
     if (A.sched2) {
-        if constexpr (DQ == -3) {
-            __shared__ K2Stage st[2];
-            k2_sched_staged(A, par, alpha, ws, st);
-        } else {
-            sched_units(A, A.sched2, A.soff2, ws, body);
-        }
+        sched_units(A, A.sched2, A.soff2, ws, body);
         TL(1, 4);
         finish_sched(A, A.sched2, A.soff2, ws, A.partial[1]);
         TL(1, 5);
@@ -1269,7 +1055,6 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
             const double rv = rn[W.a];
             double acc;
             if constexpr (DQ > 0) acc = dia_z_row<DQ>(A, W, t);
-            else if constexpr (DQ == -2) acc = sz_z_row(A, W.a - A.hoff, W.a, [&](int64_t g) { return __ldg(t + g); });
             else if constexpr (DQ < 0) acc = ell_row16(A.z, W.a - A.hoff, W.a, [&](int32_t g) { return __ldg(t + g); });
             else acc = ell_row(A.z, W.a - A.hoff, [&](int32_t g) { return __ldg(t + g); });
             A.s[W.a] = acc;
@@ -1306,31 +1091,6 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
     }
 }
 
-// ---- K23: K2 and K3 in one persistent kernel -------------------------------
-// Step v of one ticket sequence v = 0 .. U+L-1 does the K2 work of unit v (v < U) and then the K3
-// work of unit v-L (v >= L), L = A.lag23 >= nbx.  Units run north to south and a Z row reaches
-// only north (rows j .. j + zreach), so K3's unit w needs t and r_new of K2 units with smaller
-// tickets: rowdone[j] counts the K2 units of row j completed in this launch (thread 0's release
-// add after the block barrier that follows the unit's stores).  Each warp issues relaxed loads of
-// its K3 rows' counters before its K2 half and checks them after it (spinning only if a row is
-// short, which a lag beyond the in-flight window makes rare).  Progress: a step waits only on
-// K2 units with smaller tickets than its own, and the smallest unfinished K2 unit never waits.
-// The K3 half reads t and r_new with L1-cached loads issued after the counters were observed
-// complete: no SM holds an older copy of those lines (L1 is invalidated at launch, rows are
-// pitched so no line spans two rows, and nothing reads a row of t or r_new before it is
-// complete).  Partials, trees and the final sums are those of K2 then K3, so the result is bitwise
-// the same; the second kernel boundary (drain + ramp) and K3's DRAM reads of t and r_new (now L2
-// hits, written ~L units earlier) are saved.
-#ifndef PCG_MINB_K23
-#define PCG_MINB_K23 3
-#endif
-
-__device__ __forceinline__ uint32_t ld_relaxed_u32(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-
 // final_sum over two partial arrays in one walk (each sum in final_sum's order: bitwise the same)
 template <int NB>
 __device__ __forceinline__ void final_sum_pair(const double* pa, const double* pb, int64_t G, double& ra, double& rb) {
@@ -1350,342 +1110,6 @@ __device__ __forceinline__ void final_sum_pair(const double* pa, const double* p
     }
     ra = block_tree(aa);
     rb = block_tree(ab);
-}
-
-template <int DQ>
-__global__ void __launch_bounds__(kBlock + 32, PCG_MINB_K23) k23_ainv_kernel(const KArgs A, const int par, const int init) {
-    static_assert(DQ <= 0, "K23 applies the ELL form only");
-    pdl_wait();
-    if (!is_active(A)) return;
-    double alpha;
-    if (!get_alpha(A, init, alpha)) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
-        return;
-    }
-    const uint32_t target = (uint32_t)A.nbx * (__ldcg(&A.sc->epoch) + 1u);
-    const double* __restrict__ ro = A.r[par];
-    double* rn = A.r[par ^ 1];
-    const double* __restrict__ q = A.q;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    auto tbody = [&](const Unit& W) {                 // K2: r -= alpha q ; t = (Z^T r) / Dhat ; (r, r)
-        double v = 0.0;
-        if (W.live) {
-            const double rnew = __fma_rn(-alpha, q[W.a], ro[W.a]);
-            const double pv = A.piv[W.a];
-            auto gat = [&](int64_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); };
-            double acc;
-            if constexpr (DQ == -2) acc = sz_zt_row(A, W.a - A.hoff, W.a, rnew, gat);
-            else if constexpr (DQ < 0) acc = ell_row16(A.zt, W.a - A.hoff, W.a, gat);
-            else acc = ell_row(A.zt, W.a - A.hoff, gat);
-            A.t[W.a] = __ddiv_rn(acc, pv);
-            rn[W.a] = rnew;
-            v = __dmul_rn(rnew, rnew);
-        }
-        return v;
-    };
-    auto sbody = [&](const Unit& W) {                 // K3: s = Z t ; (s, r)
-        double v = 0.0;
-        if (W.live) {
-            const double rv = __ldca(rn + W.a);
-            auto gat = [&](int64_t g) { return __ldca(A.t + g); };
-            double acc;
-            if constexpr (DQ == -2) acc = sz_z_row(A, W.a - A.hoff, W.a, gat);
-            else if constexpr (DQ < 0) acc = ell_row16(A.z, W.a - A.hoff, W.a, gat);
-            else acc = ell_row(A.z, W.a - A.hoff, gat);
-            A.s[W.a] = acc;
-            v = __dmul_rn(acc, rv);
-        }
-        return v;
-    };
-    auto live_of = [&](Unit& W) {
-        if (A.landskip) W.live = W.inrow && ((__ldg(A.ocean + ((int64_t)W.j * A.nbx + W.bx) * kWarps + warp) >> lane) & 1u);
-    };
-    // Warps 0..7 compute; warp 8 keeps the books (tickets, the row-flag release -- a gpu-scope
-    // fence that waits for the step's stores -- and the unit partials), so no compute warp stalls
-    // on the fence: it has a whole step to complete before the next barrier.
-    __shared__ long long s_next[2];
-    __shared__ double wsd[2][2][kWarps];
-    const int64_t U = n_units(A), L = A.lag23, V = U + L;
-    const bool books = warp == kWarps;
-    if (books && lane == 0) s_next[0] = (long long)atomicAdd(&A.sc->ticket[1], 1ull);
-    __syncthreads();
-    int64_t v = s_next[0];
-    int cur = 1;
-    while (v < V) {
-        const bool has_t = v < U, has_s = v >= L;
-        if (books) {
-            if (lane == 0) s_next[cur] = (long long)atomicAdd(&A.sc->ticket[1], 1ull);
-            __syncthreads();
-            if (has_t && lane == 0) {
-                const Unit Wt = unit_of(A, v);
-                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(A.rowdone + Wt.j) : "memory");
-            }
-            if (has_t) {
-                const int64_t u = v;
-                const int64_t m = (int64_t)(A.nloc - 1 - (int32_t)(u / A.nbx)) * A.nbx + (u % A.nbx);
-                const double w = warp_tree(lane < kWarps ? wsd[cur][0][lane] : 0.0);
-                if (lane == 0) A.partial[1][m] = w;
-            }
-            if (has_s) {
-                const int64_t u = v - L;
-                const int64_t m = (int64_t)(A.nloc - 1 - (int32_t)(u / A.nbx)) * A.nbx + (u % A.nbx);
-                const double w = warp_tree(lane < kWarps ? wsd[cur][1][lane] : 0.0);
-                if (lane == 0) A.partial[2][m] = w;
-            }
-        } else {
-            Unit Ws{};
-            uint32_t pv = target;
-            if (has_s) {                               // this step's K3 rows: flag loads in flight
-                Ws = unit_of(A, v - L);
-                if (lane <= A.zreach && Ws.j + lane < A.nloc) pv = ld_relaxed_u32(A.rowdone + Ws.j + lane);
-            }
-            double vt = 0.0, vs = 0.0;
-            if (has_t) {
-                Unit Wt = unit_of(A, v);
-                live_of(Wt);
-                vt = tbody(Wt);
-            }
-            if (has_s) {
-                bool ok = (int32_t)(pv - target) >= 0;
-                while (!__all_sync(kFull, ok))
-                    if (!ok) { pv = ld_relaxed_u32(A.rowdone + Ws.j + lane); ok = (int32_t)(pv - target) >= 0; }
-                asm volatile("" ::: "memory");          // the K3 loads of t / r_new stay below the check
-                live_of(Ws);
-                vs = sbody(Ws);
-            }
-            vt = warp_tree(vt);
-            vs = warp_tree(vs);
-            if (lane == 0) { wsd[cur][0][warp] = vt; wsd[cur][1][warp] = vs; }
-            __syncthreads();
-        }
-        v = s_next[cur];
-        cur ^= 1;
-    }
-    pdl_trigger();
-    if (!count_block(&A.sc->counter[2])) return;
-    // last block: K2's and K3's final sums, then the scalars of k3_sum_rr / k3_finish
-    FinPre pre{};
-    if (threadIdx.x == 0) pre = fin_prefetch(A);
-    double rr, rs;
-    final_sum_pair<PCG_FINAL_NB_K3>(A.partial[1], A.partial[2], U, rr, rs);
-    if (threadIdx.x == 0) {
-        DevScalars* sc = A.sc;
-        sc->alpha = alpha;                             // = rho / (d, q) (0 in the init pass)
-        sc->xpend = init ? 0 : 1;
-        sc->counter[1] = 0;
-        sc->ticket[1] = 0;
-        sc->counter[2] = 0;
-        sc->ticket[2] = 0;
-        sc->epoch = sc->epoch + 1u;
-        if (A.multi) {
-            sc->loc[2] = rr;
-            sc->loc[1] = rs;
-        } else {
-            sc->red[2] = rr;
-            pre.rr = rr;
-            pre.h = __ddiv_rn(__dsqrt_rn(rr), pre.nb);
-            sc->hpre = pre.h;
-            if (init) fin_init(A, rs, rr);
-            else fin_iter(A, rs, pre);
-        }
-    }
-}
-
-// ---- TMA bulk-copy pipeline for K2 / K3 ---------------------------------------
-// Block = 8 consumer warps (the 256 columns of a unit) + 1 producer warp.  The producer takes
-// units from the atomic ticket and streams each unit's contiguous arrays (ELL columns and values,
-// the unit's own vector entries) into a kStages ring of shared memory with cp.async.bulk, signalled
-// by mbarriers (SASS UBLKCP / SYNCS).  Consumers compute from shared memory (gathers of the
-// neighbouring points stay L1/L2 loads), leave their 8 warp sums in the stage and release it;
-// the producer, waiting for that stage anyway, completes the unit's partial (second level of the
-// block tree).  The main loop has no __syncthreads.
-#ifndef PCG_TMA_STAGES
-#define PCG_TMA_STAGES 4
-#endif
-#ifndef PCG_TMA_MINB
-#define PCG_TMA_MINB 2
-#endif
-constexpr int kStages = PCG_TMA_STAGES;
-constexpr uint32_t kSentinel = 0xffffffffu;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
-            smem_u32(b)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(b))
-                 : "memory");
-}
-
-template <int NVEC>
-struct TmaStage {
-    int4 col[kBlock];                 // ELL column slots (array indices)
-    double4 val[kBlock];              // ELL values
-    double vec[NVEC][kBlock];         // the unit's own entries of NVEC vectors
-};
-
-template <int NVEC>
-struct TmaSmem {
-    TmaStage<NVEC> st[kStages];
-    uint64_t full[kStages], empty[kStages];
-    uint32_t unit[kStages];
-    double wsum[kStages][kWarps];
-};
-
-template <int NVEC>
-size_t tma_smem_bytes() { return sizeof(TmaSmem<NVEC>); }
-
-// Producer side: stream unit u's arrays into stage s.
-template <int NVEC>
-__device__ __forceinline__ void tma_fill(TmaSmem<NVEC>& S, int s, const KArgs& A, const EllDev& E, int64_t u,
-                                         const double* const (&vecs)[NVEC]) {
-    const int32_t bx = (int32_t)(u % A.nbx), j = A.nloc - 1 - (int32_t)(u / A.nbx);
-    const int32_t nel = min(kBlock, A.pitch - bx * kBlock);
-    const int64_t e0 = (int64_t)j * A.pitch + (int64_t)bx * kBlock;
-    mbar_expect_tx(&S.full[s], (unsigned)nel * (16u + 32u + 8u * NVEC));
-    bulk_g2s(S.st[s].col, E.col + e0 * kEll, (unsigned)nel * 16u, &S.full[s]);
-    bulk_g2s(S.st[s].val, E.val + e0 * kEll, (unsigned)nel * 32u, &S.full[s]);
-#pragma unroll
-    for (int v = 0; v < NVEC; ++v) bulk_g2s(S.st[s].vec[v], vecs[v] + e0 + A.hoff, (unsigned)nel * 8u, &S.full[s]);
-}
-
-// Complete unit u's partial from the 8 warp sums left in stage s (producer warp, all lanes).
-template <int NVEC>
-__device__ __forceinline__ void tma_finalize(const TmaSmem<NVEC>& S, int s, const KArgs& A, double* partial) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t u = S.unit[s];
-    double w = lane < kWarps ? S.wsum[s][lane] : 0.0;
-    w = warp_tree(w);
-    if (lane == 0) {
-        const int32_t bx = (int32_t)(u % A.nbx), j = A.nloc - 1 - (int32_t)(u / A.nbx);
-        partial[(int64_t)j * A.nbx + bx] = w;
-    }
-}
-
-template <int NVEC, class Consume>
-__device__ __forceinline__ void tma_pipeline(TmaSmem<NVEC>& S, const KArgs& A, const EllDev& E,
-                                             const double* const (&vecs)[NVEC], unsigned long long* ticket,
-                                             double* partial, Consume consume) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t U = n_units(A);
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) { mbar_init(&S.full[s], 1); mbar_init(&S.empty[s], kWarps); }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (warp == kWarps) {                                  // ---- producer warp
-        int it = 0;
-        unsigned long long u_next = 0;                     // ticket prefetched one unit ahead
-        if (lane == 0) u_next = atomicAdd(ticket, 1ull);
-        for (;; ++it) {
-            const int s = it % kStages;
-            if (it >= kStages) {                           // stage reuse: wait for its consumers
-                mbar_wait(&S.empty[s], ((it / kStages) - 1) & 1);
-                tma_finalize(S, s, A, partial);
-            }
-            unsigned long long u = __shfl_sync(kFull, u_next, 0);
-            if (lane == 0 && (int64_t)u < U) u_next = atomicAdd(ticket, 1ull);
-            if (lane == 0) {
-                if ((int64_t)u >= U) {
-                    S.unit[s] = kSentinel;
-                    mbar_arrive(&S.full[s]);
-                } else {
-                    S.unit[s] = (uint32_t)u;
-                    tma_fill(S, s, A, E, (int64_t)u, vecs);
-                }
-            }
-            if ((int64_t)u >= U) break;
-        }
-        for (int k = max(0, it - kStages + 1); k < it; ++k) {   // drain: finalize units still in flight
-            const int s = k % kStages;
-            mbar_wait(&S.empty[s], (k / kStages) & 1);
-            tma_finalize(S, s, A, partial);
-        }
-    } else {                                               // ---- consumer warps
-        for (int it = 0;; ++it) {
-            const int s = it % kStages;
-            mbar_wait(&S.full[s], (it / kStages) & 1);
-            const uint32_t u = S.unit[s];
-            if (u == kSentinel) break;
-            const int32_t bx = (int32_t)(u % A.nbx), j = A.nloc - 1 - (int32_t)(u / A.nbx);
-            const int32_t i = bx * kBlock + (int32_t)threadIdx.x;
-            double v = 0.0;
-            if (i < A.pitch) v = consume(S.st[s], (int)threadIdx.x, i, j);
-            v = warp_tree(v);
-            if (lane == 0) S.wsum[s][warp] = v;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&S.empty[s]);
-        }
-    }
-}
-
-// row sum of the ELL slots staged in shared memory + overflow from global memory
-template <class Gather>
-__device__ __forceinline__ double ell_row_smem(const EllDev& E, int4 cv, double4 zv, int64_t e, Gather gat) {
-    double x0 = gat(cv.x), x1 = gat(cv.y), x2 = gat(cv.z), x3 = gat(cv.w);
-    double acc = __fma_rn(zv.x, x0, 0.0);
-    acc = __fma_rn(zv.y, x1, acc);
-    acc = __fma_rn(zv.z, x2, acc);
-    acc = __fma_rn(zv.w, x3, acc);
-    return overflow_sum(E, e, acc, gat);
-}
-
-__global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k2_tma_kernel(const KArgs A, const int par, const int init) {
-    pdl_wait();
-    if (!is_active(A)) return;
-    double alpha;
-    if (!get_alpha(A, init, alpha)) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) stop(A, kStBreakdown);
-        return;
-    }
-    extern __shared__ __align__(128) unsigned char smraw[];
-    auto& S = *reinterpret_cast<TmaSmem<3>*>(smraw);
-    const double* __restrict__ ro = A.r[par];
-    double* __restrict__ rn = A.r[par ^ 1];
-    const double* __restrict__ q = A.q;
-    const double* const vecs[3] = {A.q, ro, A.piv};
-    tma_pipeline<3>(S, A, A.zt, vecs, &A.sc->ticket[1], A.partial[1], [&](const TmaStage<3>& st, int t, int32_t i, int32_t j) {
-        const int64_t a = (int64_t)(j + A.halo) * A.pitch + i;
-        const double rnew = __fma_rn(-alpha, st.vec[0][t], st.vec[1][t]);
-        const double acc = ell_row_smem(A.zt, st.col[t], st.val[t], a - A.hoff,
-                                        [&](int32_t g) { return __fma_rn(-alpha, __ldg(q + g), __ldg(ro + g)); });
-        A.t[a] = __ddiv_rn(acc, st.vec[2][t]);
-        rn[a] = rnew;
-        return __dmul_rn(rnew, rnew);
-    });
-    pdl_trigger();
-}
-
-__global__ void __launch_bounds__(kBlock + 32, PCG_TMA_MINB) k3_tma_kernel(const KArgs A, const int par, const int init) {
-    pdl_wait();
-    if (!is_active(A)) return;
-    k3_sum_rr(A, init);
-    extern __shared__ __align__(128) unsigned char smraw[];
-    auto& S = *reinterpret_cast<TmaSmem<1>*>(smraw);
-    const double* __restrict__ t = A.t;
-    const double* const vecs[1] = {A.r[par ^ 1]};
-    tma_pipeline<1>(S, A, A.z, vecs, &A.sc->ticket[2], A.partial[2], [&](const TmaStage<1>& st, int tt, int32_t i, int32_t j) {
-        const int64_t a = (int64_t)(j + A.halo) * A.pitch + i;
-        const double acc = ell_row_smem(A.z, st.col[tt], st.val[tt], a - A.hoff, [&](int32_t g) { return __ldg(t + g); });
-        A.s[a] = acc;
-        return __dmul_rn(acc, st.vec[0][tt]);
-    });
-    if (count_block(&A.sc->counter[2])) k3_finish(A, init);
 }
 
 // ---- the whole PCG loop as one cooperative persistent kernel (single rank) ---------------------
@@ -1912,180 +1336,6 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_LOOP) loop_kernel(const KArgs
     }
 }
 
-// ---- the whole PCG loop in ONE CTA with the vectors in shared memory (tiny grids) -------------
-// For grids whose eight vectors fit in shared memory (cfg1: 34 x 32 elements, 70 KB) the solve is
-// latency-bound: three grid barriers per iteration of the cooperative loop kernel cost more than
-// the arithmetic.  One block of 1024 threads holds x, r0, r1, d0, d1, q, t, s in shared memory,
-// its 32 warps walk the (unit, warp) items of each phase (a unit is a row segment of 256 columns:
-// the canonical partials), and the phases are separated by __syncthreads.  Same per-point arithmetic (k1_load/k1_compute,
-// the ELL rows), same unit partials, same canonical final sums as the other drivers -> bitwise.
-// Z, Z^T, pivots and coefficients stay in global memory (read-only, L1-resident at this size).
-constexpr int kTinyThreads = 1024;
-
-__device__ __forceinline__ Unit tiny_unit(const KArgs& A, int64_t u, int t256) {
-    Unit W;
-    W.bx = (int32_t)(u % A.nbx);
-    W.j = A.nloc - 1 - (int32_t)(u / A.nbx);
-    W.i = W.bx * kBlock + t256;
-    W.valid = W.i < A.ni;
-    W.inrow = W.i < A.pitch;
-    W.live = W.inrow;
-    W.a = (int64_t)(W.j + A.halo) * A.pitch + W.i;
-    return W;
-}
-
-// canonical final sum of G partials held in shared memory (thread t < 256 sums t, t+256, ...
-// left to right, then the block tree of final_sum), broadcast to every thread
-__device__ __forceinline__ double tiny_final(const double* p, int64_t G, double* bc) {
-    double acc = 0.0;
-    if (threadIdx.x < kBlock)
-        for (int64_t m = threadIdx.x; m < G; m += kBlock) acc = __dadd_rn(acc, p[m]);
-    const double v = block_tree(acc);
-    if (threadIdx.x == 0) *bc = v;
-    __syncthreads();
-    const double r = *bc;
-    __syncthreads();
-    return r;
-}
-
-// per-unit warp sums (ws[u][8]) -> unit partials p[m(u)] (second level of the unit's block tree)
-__device__ __forceinline__ void tiny_partials(const KArgs& A, const double* ws, double* p) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t U = n_units(A);
-    for (int64_t u = warp; u < U; u += kTinyThreads / 32) {
-        double w = lane < kWarps ? ws[u * kWarps + lane] : 0.0;
-        w = warp_tree(w);
-        if (lane == 0) p[(int64_t)(A.nloc - 1 - (int32_t)(u / A.nbx)) * A.nbx + (u % A.nbx)] = w;
-    }
-}
-
-template <bool SIGMA>
-__global__ void __launch_bounds__(kTinyThreads, 1) tiny_kernel(const KArgs G) {
-    extern __shared__ double smv[];
-    __shared__ KArgs A;                        // the kernel arguments with the vectors re-pointed
-    const int64_t NE = G.nel_all, U = n_units(G);
-    if (threadIdx.x == 0) {
-        A = G;
-        A.x = smv; A.r[0] = smv + NE; A.r[1] = smv + 2 * NE; A.d[0] = smv + 3 * NE; A.d[1] = smv + 4 * NE;
-        A.q = smv + 5 * NE; A.t = smv + 6 * NE; A.s = smv + 7 * NE;
-    }
-    double* part = smv + 8 * NE;               // 3 x U canonical partials
-    double* ws = part + 3 * U;                 // U x 8 warp sums of the current phase
-    double* bc = ws + U * kWarps;              // broadcast slot
-    auto gvec = [&](int v) -> double* {
-        switch (v) {
-            case 0: return G.x; case 1: return G.r[0]; case 2: return G.r[1]; case 3: return G.d[0];
-            case 4: return G.d[1]; case 5: return G.q; case 6: return G.t; default: return G.s;
-        }
-    };
-    for (int v = 0; v < 8; ++v) {
-        const double* src = gvec(v);
-        for (int64_t e = threadIdx.x; e < NE; e += kTinyThreads) smv[v * NE + e] = src[e];
-    }
-    __syncthreads();
-    DevScalars* sc = G.sc;
-    const bool lead = threadIdx.x == 0;
-    double rho = sc->rho, beta = sc->beta, alpha = sc->alpha;
-    const double nb = sc->nb, tol = sc->tol;
-    int k = sc->k, status = sc->status, xpend = 0;
-    const int maxit = sc->maxit;
-    bool active = sc->active != 0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // work items: (unit, warp of the unit); the 32 warps of the block take them round-robin, so a
-    // narrow grid (pitch <= 256: one live warp per unit) does a whole phase in one round.  A warp
-    // of a unit with no column inside the row contributes the exact zero the 256-thread unit's
-    // idle warps would.
-    const int64_t NW = U * kWarps;
-    auto items = [&](auto&& body) {
-        for (int64_t it = warp; it < NW; it += kTinyThreads / 32) {
-            const int64_t u = it / kWarps;
-            const int w = (int)(it % kWarps);
-            double v = 0.0;
-            if ((int64_t)(u % A.nbx) * kBlock + 32 * w < A.pitch) v = warp_tree(body(tiny_unit(A, u, 32 * w + lane)));
-            if (lane == 0) ws[it] = v;
-        }
-    };
-    int par = 0;
-    while (active) {
-        // K1: d = s + beta d_old ; x += alpha_prev d_old ; q = A d ; (d, q)
-        items([&](const Unit& W) {
-            K1Ld L;
-            k1_load(A, W, par, L);
-            return k1_compute<SIGMA>(A, W, par, beta, alpha, L);
-        });
-        xpend = 0;
-        __syncthreads();
-        tiny_partials(A, ws, part);
-        __syncthreads();
-        const double gamma = tiny_final(part, U, bc);
-        if (!(gamma > 0.0) || !isfinite(gamma)) { status = kStBreakdown; break; }
-        alpha = __ddiv_rn(rho, gamma);
-        // K2: r -= alpha q ; t = (Z^T r) / Dhat ; (r, r)
-        {
-            const double* ro = A.r[par];
-            double* rn = A.r[par ^ 1];
-            const double* q = A.q;
-            auto gat = [&](int64_t g) { return __fma_rn(-alpha, q[g], ro[g]); };
-            items([&](const Unit& W) {
-                double v = 0.0;
-                if (W.inrow) {
-                    const double rnew = __fma_rn(-alpha, q[W.a], ro[W.a]);
-                    const double acc = A.zt.col16 ? ell_row16(A.zt, W.a - A.hoff, W.a, gat) : ell_row(A.zt, W.a - A.hoff, gat);
-                    A.t[W.a] = __ddiv_rn(acc, A.piv[W.a]);
-                    rn[W.a] = rnew;
-                    v = __dmul_rn(rnew, rnew);
-                }
-                return v;
-            });
-        }
-        __syncthreads();
-        tiny_partials(A, ws, part + U);
-        __syncthreads();
-        // K3: s = Z t ; (s, r)
-        {
-            const double* rn = A.r[par ^ 1];
-            const double* t = A.t;
-            auto gat = [&](int64_t g) { return t[g]; };
-            items([&](const Unit& W) {
-                double v = 0.0;
-                if (W.inrow) {
-                    const double acc = A.z.col16 ? ell_row16(A.z, W.a - A.hoff, W.a, gat) : ell_row(A.z, W.a - A.hoff, gat);
-                    A.s[W.a] = acc;
-                    v = __dmul_rn(acc, rn[W.a]);
-                }
-                return v;
-            });
-        }
-        __syncthreads();
-        tiny_partials(A, ws, part + 2 * U);
-        __syncthreads();
-        const double rr = tiny_final(part + U, U, bc);
-        const double rho_new = tiny_final(part + 2 * U, U, bc);
-        k += 1;
-        xpend = 1;
-        if (!isfinite(rho_new) || !isfinite(rr)) {
-            if (lead) put_hist(G, k, NAN);
-            status = kStBreakdown;
-            break;
-        }
-        beta = __ddiv_rn(rho_new, rho);
-        rho = rho_new;
-        const double h = __ddiv_rn(__dsqrt_rn(rr), nb);
-        if (lead) put_hist(G, k, h);
-        active = (h > tol) && (k < maxit);
-        par ^= 1;
-    }
-    __syncthreads();
-    for (int v = 0; v < 8; ++v) {
-        double* dst = gvec(v);
-        for (int64_t e = threadIdx.x; e < NE; e += kTinyThreads) dst[e] = smv[v * NE + e];
-    }
-    if (lead) {
-        sc->k = k; sc->alpha = alpha; sc->beta = beta; sc->rho = rho;
-        sc->xpend = xpend; sc->status = status; sc->active = 0;
-    }
-}
-
 // ---- K2 (Jacobi / none): r -= alpha q ; s = r / A_pp (or r) ; (r, r), (s, r) ---------------
 #ifndef KD2_UNROLL
 #define KD2_UNROLL 2                 // measured at cfg4 (Jacobi): 1 / 2 / 4 / 8 -> 47.5 / 45.7 / 48.3 / 51.1 us/iteration
@@ -2240,7 +1490,6 @@ __global__ void __launch_bounds__(kBlock) prep_kernel(const KArgs A) {
     for (int64_t a = (int64_t)blockIdx.x * kBlock + threadIdx.x; a < n; a += (int64_t)gridDim.x * kBlock) {
         A.d[0][a] = 0.0;
         if (A.p) A.p[a] = 0.0;                               // CG-CG search direction
-        if (A.rowdone && a < A.nloc) A.rowdone[a] = 0u;     // K23 row flags (DevScalars::epoch = 0)
         const int64_t row = a / A.pitch;
         if (row >= A.halo && row < A.halo + A.nloc) {
             if (signbit(A.cN[a])) { A.x[a] = 0.0; A.b[a] = 0.0; }
@@ -2403,10 +1652,6 @@ void configure_kernels(KArgs& A, int sms) {
         A.g_k1 = (int)((S + per - 1) / per);
     }
     A.g_k2 = persistent_grid(k2_ainv_kernel<0>, U, sms, 2048);
-    A.g_k23 = persistent_grid(k23_ainv_kernel<-2>, U, sms, 0, kBlock + 32);
-    A.lag23 = A.g_k23 + 2 * A.nbx;                     // beyond the in-flight window: flag waits are rare
-    if (const char* e = getenv("PCG_LAG23")) A.lag23 = atoi(e);
-    A.lag23 = std::max(A.lag23, A.nbx);                // >= nbx: progress (see k23_ainv_kernel)
     A.g_k3 = persistent_grid(k3_ainv_kernel<0>, U, sms, 2048);
     A.g_kd = persistent_grid(k2_diag_kernel, U, sms, 4096);
     A.g_row = persistent_grid(init_residual_kernel, U, sms, 2048);
@@ -2419,9 +1664,6 @@ void configure_kernels(KArgs& A, int sms) {
     A.landskip = A.ocean != nullptr;
     if (const char* e = getenv("PCG_LANDSKIP")) A.landskip = A.landskip && atoi(e) != 0;
     A.g_k1f = persistent_grid(k1_flat_kernel<false>, U, sms, 0);
-    A.g_k1p = persistent_grid(k1_pair_kernel<false>, U, sms, 0);
-    A.tma = 0;                                         // measured no faster than the LDG path (r01)
-    if (const char* e = getenv("PCG_TMA")) A.tma = atoi(e) != 0;
     {
         int bl = 1;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bl, A.sigma ? (const void*)loop_kernel<true> : (const void*)loop_kernel<false>,
@@ -2430,24 +1672,11 @@ void configure_kernels(KArgs& A, int sms) {
         const int64_t work = std::max<int64_t>(U, S);
         A.g_loop = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(bl, 1) * sms, work));
     }
-    {
-        const size_t s2 = tma_smem_bytes<3>(), s3 = tma_smem_bytes<1>();
-        cudaFuncSetAttribute(k2_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2);
-        cudaFuncSetAttribute(k3_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s3);
-        int b2 = 1, b3 = 1;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2_tma_kernel, kBlock + 32, s2);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b3, k3_tma_kernel, kBlock + 32, s3);
-        A.g_t2 = (int)std::max<int64_t>(1, std::min<int64_t>(U, (int64_t)std::max(b2, 1) * sms));
-        A.g_t3 = (int)std::max<int64_t>(1, std::min<int64_t>(U, (int64_t)std::max(b3, 1) * sms));
-    }
     allow_smem(k1_kernel<false>, k1_smem(A, A.g_k1));
     allow_smem(k1_kernel<true>, k1_smem(A, A.g_k1));
     allow_smem(k2_ainv_kernel<0>, row_smem(A, A.g_k2, 1));
     allow_smem(k3_ainv_kernel<0>, row_smem(A, A.g_k3, 1));
     allow_smem(k2_ainv_kernel<-1>, row_smem(A, A.g_k2, 1));
-    allow_smem(k2_ainv_kernel<-2>, row_smem(A, A.g_k2, 1));
-    allow_smem(k2_ainv_kernel<-3>, row_smem(A, A.g_k2, 1) + 2 * sizeof(K2Stage));
-    allow_smem(k3_ainv_kernel<-2>, row_smem(A, A.g_k3, 1));
     allow_smem(k3_ainv_kernel<-1>, row_smem(A, A.g_k3, 1));
     allow_smem(k2_ainv_kernel<4>, row_smem(A, A.g_k2, 1));
     allow_smem(k3_ainv_kernel<4>, row_smem(A, A.g_k3, 1));
@@ -2458,8 +1687,6 @@ void configure_kernels(KArgs& A, int sms) {
     allow_smem(k2_diag_kernel, row_smem(A, A.g_kd, 2));
     allow_smem(ka_cg_kernel, row_smem(A, A.g_k2, 1));
     allow_smem(kc_cg_kernel, row_smem(A, A.g_row, 1));
-    allow_smem(k1_pair_kernel<false>, row_smem(A, A.g_k1p, 1));
-    allow_smem(k1_pair_kernel<true>, row_smem(A, A.g_k1p, 1));
     allow_smem(init_residual_kernel, row_smem(A, A.g_row, 1));
     allow_smem(true_residual_kernel, row_smem(A, A.g_row, 1));
 }
@@ -2497,12 +1724,6 @@ static void launch_pdl(const KArgs& A, void (*kern)(P...), int grid, int block, 
 }
 
 void launch_k1(const KArgs& A, int par, cudaStream_t st) {
-    if (A.k1flat == 3 && A.redundant) {
-        const size_t sm = row_smem(A, A.g_k1p, 1);
-        if (A.sigma) launch_pdl(A, k1_pair_kernel<true>, A.g_k1p, kBlock, sm, st, A, par);
-        else launch_pdl(A, k1_pair_kernel<false>, A.g_k1p, kBlock, sm, st, A, par);
-        return;
-    }
     if (A.k1flat) {
         const size_t sm = A.k1flat == 2 ? row_smem(A, A.g_k1f, 1) : 0;
         if (A.sigma) launch_pdl(A, k1_flat_kernel<true>, A.g_k1f, kBlock, sm, st, A, par);
@@ -2521,28 +1742,16 @@ void launch_k2_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
         launch_pdl(A, ka_cg_kernel, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par);
         return;
     }
-    if (A.fuse23 && A.dia_q == 0 && !A.tma) {
-        if (A.use_sz) launch_pdl(A, k23_ainv_kernel<-2>, A.g_k23, kBlock + 32, 0, st, A, par, init);
-        else if (A.zt.col16 && A.z.col16) launch_pdl(A, k23_ainv_kernel<-1>, A.g_k23, kBlock + 32, 0, st, A, par, init);
-        else launch_pdl(A, k23_ainv_kernel<0>, A.g_k23, kBlock + 32, 0, st, A, par, init);
-        return;
-    }
-    if (A.tma) launch_pdl(A, k2_tma_kernel, A.g_t2, kBlock + 32, tma_smem_bytes<3>(), st, A, par, init);
-    else if (A.dia_q > 8) launch_pdl(A, k2_ainv_kernel<16>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
+    if (A.dia_q > 8) launch_pdl(A, k2_ainv_kernel<16>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else if (A.dia_q > 4) launch_pdl(A, k2_ainv_kernel<8>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else if (A.dia_q > 0) launch_pdl(A, k2_ainv_kernel<4>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
-    else if (A.use_sz) launch_pdl(A, k2_ainv_kernel<-2>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
-    else if (A.zt.col16 && A.stage2 && A.sched2) launch_pdl(A, k2_ainv_kernel<-3>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else if (A.zt.col16) launch_pdl(A, k2_ainv_kernel<-1>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
     else launch_pdl(A, k2_ainv_kernel<0>, A.g_k2, kBlock, row_smem(A, A.g_k2, 1), st, A, par, init);
 }
 void launch_k3_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
-    if (A.fuse23 && A.dia_q == 0 && !A.tma) return;    // done by K23
-    if (A.tma) launch_pdl(A, k3_tma_kernel, A.g_t3, kBlock + 32, tma_smem_bytes<1>(), st, A, par, init);
-    else if (A.dia_q > 8) launch_pdl(A, k3_ainv_kernel<16>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
+    if (A.dia_q > 8) launch_pdl(A, k3_ainv_kernel<16>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else if (A.dia_q > 4) launch_pdl(A, k3_ainv_kernel<8>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else if (A.dia_q > 0) launch_pdl(A, k3_ainv_kernel<4>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
-    else if (A.use_sz) launch_pdl(A, k3_ainv_kernel<-2>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else if (A.z.col16) launch_pdl(A, k3_ainv_kernel<-1>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else launch_pdl(A, k3_ainv_kernel<0>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
 }
@@ -2569,27 +1778,7 @@ void launch_extrapolate(const double* xt, const double* xm, double* x0, int64_t 
     const int64_t G = std::max<int64_t>(1, std::min<int64_t>((n + kBlock - 1) / kBlock, 148 * 8));
     extrapolate_kernel<<<(unsigned)G, kBlock, 0, st>>>(xt, xm, x0, n);
 }
-size_t tiny_smem_bytes(const KArgs& A) {
-    const int64_t U = (int64_t)A.nloc * A.nbx;
-    return (size_t)(8 * A.nel_all + 3 * U + U * kWarps + 1) * sizeof(double);
-}
-bool tiny_eligible(const KArgs& A) {
-    if (A.precond != 0 || A.dia_q != 0 || A.nranks != 1 || A.multi) return false;
-    // opt-in (PCG_TINY=1): measured 31.4 against 16.9 us/iteration for the cooperative loop at cfg1
-    // -- one SM issues the whole iteration (82 k warp instructions, 5.6 M per solve), where the
-    // loop kernel spreads it over 148 SMs and pays three grid barriers instead
-    const char* e = getenv("PCG_TINY");
-    if (!(e && atoi(e) != 0)) return false;
-    return tiny_smem_bytes(A) <= 200 * 1024;
-}
 cudaError_t launch_loop(const KArgs& A, cudaStream_t st) {
-    if (tiny_eligible(A)) {
-        const size_t sm = tiny_smem_bytes(A);
-        auto fn = A.sigma ? tiny_kernel<true> : tiny_kernel<false>;
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        fn<<<1, kTinyThreads, sm, st>>>(A);
-        return cudaGetLastError();
-    }
     void* args[] = {(void*)&A};
     const void* fn = A.sigma ? (const void*)loop_kernel<true> : (const void*)loop_kernel<false>;
     return cudaLaunchCooperativeKernel(fn, dim3(A.g_loop), dim3(kBlock), args, 0, st);

@@ -19,7 +19,6 @@ struct DevScalars {
     double red[4];        // global reductions: [0] (d,q)  [1] (s,r)  [2] (r,r)  [3] (b,b) / true (r,r)
     double loc[4];        // this rank's block-tree sums (multi-rank path)
     int32_t k, maxit, active, status, bzero, xpend, guard;
-    uint32_t epoch;       // K23 launches completed in this solve (row-flag target)
     double rhop[2];       // redundant-sum mode: rho of the iterations of parity 0 / 1 (rhop[1] = inf before the first)
     uint32_t counter[4];  // last-block detection, reset by the last block
     unsigned long long ticket[4];   // dynamic unit assignment, reset by the last block
@@ -36,13 +35,6 @@ struct EllDev {
     const int16_t* col16 = nullptr;   // kEll * n slot offsets from the element's own array index
 };
 
-// Device view of the structured form (internal.h Sz).
-struct SzDev {
-    const double* val4 = nullptr;     // 4 * n
-    const uint8_t* k = nullptr;       // n
-    const uint2* w = nullptr;         // per warp of 32 elements {rounds | generic << 31, run offset}
-    const double* run = nullptr;
-};
 
 // Resident-strip driver (rs.cu): one persistent cooperative block of kRsThreads
 // per SM runs the whole PCG loop.  Block b owns a contiguous range of units (row segments, in
@@ -78,10 +70,8 @@ struct KArgs {
     int32_t nbx, rpb;                 // column segments of kBlock per row; rows per K1 strip
     int32_t g_k1, g_k2, g_k3, g_kd, g_row;   // persistent grid sizes (configure_kernels)
     int32_t dynamic, dynamic_k1;      // units from an atomic ticket instead of a block stride
-    int32_t tma, g_t2, g_t3;          // K2/K3 through the TMA bulk-copy pipeline; its grid sizes
     int32_t g_loop;                   // cooperative grid of the fused loop kernel
     int32_t k1flat, g_k1f;            // K1 in row-segment form (one element per thread)
-    int32_t g_k1p;                    // grid of the two-units-per-thread K1 (k1flat == 3)
     int32_t pdl;                      // programmatic dependent launch of the iteration kernels
     const int32_t* sched2;            // K2 scheduled static walk: unit list (NULL = dynamic tickets)
     const int32_t* soff2;             // [g_k2 + 1] offsets of each block's list
@@ -97,8 +87,6 @@ struct KArgs {
     int64_t nel;                      // owned elements nloc * pitch
     const double *cE, *cN, *sigma, *diag, *piv;
     EllDev zt, z;                     // rows of Z^T (K2) and of Z (K3)
-    SzDev szt, sz;                    // structured form of the same rows (used when use_sz)
-    int32_t use_sz;
     int64_t nel_all;                  // elements of every per-point array, halo rows included
     int32_t periodic;
     double *x, *b, *q, *t, *s;
@@ -111,12 +99,6 @@ struct KArgs {
     int32_t multi;                    // 1: reductions end at rank sums (NCCL path)
     int32_t use_cond;
     cudaGraphConditionalHandle cond;
-    // K23: K2 and K3 fused into one persistent kernel (one rank, or Z without cross-rank columns)
-    int32_t fuse23;                   // 1: launch_k2_ainv launches k23_ainv_kernel, launch_k3_ainv nothing
-    int32_t zreach;                   // grid rows north of its own row a Z row reaches (>= 0)
-    int32_t lag23;                    // ticket lag of the K3 half behind the K2 half (>= nbx)
-    int32_t g_k23;
-    uint32_t* rowdone;                // [nloc] t rows completed (nbx per K23 launch), zeroed by prep
     // Redundant-sum mode (one rank, K1 / K2 / K3 launches): no last-block tails; every block of the
     // consumer kernel forms the canonical final sum it needs (K1: (s, r) -> beta, K2: (d, q) ->
     // alpha) and K3's block 0 does the history / stop test from K2's (r, r) at its start.
@@ -124,7 +106,6 @@ struct KArgs {
     int32_t red_gamma;                // Jacobi / none (one rank): K1 without a last block, K2's blocks form (d, q)
     int32_t cgcg;                     // Chronopoulos-Gear single-reduction PCG (NEXT-2; KA, K3, KC)
     double* p;                        // its search direction p (s = A p lives in d[0] / d[1], w in q, u in s)
-    int32_t stage2;                   // K2's scheduled walk through the per-thread cp.async double buffer
     void* l2_base;                    // persisting L2 access-policy window of the iteration kernels
     size_t l2_bytes;                  // (0: none)
     float l2_ratio;

@@ -137,81 +137,6 @@ void pack_sell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& c
     }
 }
 
-// Structured form (internal.h Sz).  A row fits when its entries are the diagonal, N-S entries at
-// exactly dir*P and dir*2P, and E-W entries in the element's own grid row on the dir side with
-// run length k <= 255 (fillers = absent columns inside the run).  Rows without entries (land,
-// padding) fit trivially.
-void pack_struct(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols, const std::vector<double>& vals,
-                 int64_t nel, int32_t pitch, int32_t halo, int dir, Sz& S) {
-    const int64_t hoff = (int64_t)halo * pitch;
-    const int64_t nw = nel / kSlice;
-    S.val4.assign((size_t)4 * nel, 0.0);
-    S.k.assign((size_t)nel, 0);
-    S.w.assign((size_t)2 * nw, 0u);
-    S.run.clear();
-    S.fillers = 0;
-    S.generic_warps = 0;
-    std::vector<int32_t> kk((size_t)nel, 0);
-    std::vector<char> fits((size_t)nel, 1);
-    for (int64_t e = 0; e < nel; ++e) {
-        const int64_t a = e + hoff, row0 = a - (e % pitch), row1 = row0 + pitch;   // own grid row [row0, row1)
-        int32_t k = 0, n_ew = 0;
-        for (int64_t m = rowptr[e]; m < rowptr[e + 1]; ++m) {
-            const int64_t c = cols[m];
-            const int64_t d = (c - a) * dir;                                       // >= 0 on the dir side
-            if (c == a || d == pitch || d == 2 * (int64_t)pitch) continue;
-            if (d > 0 && c >= row0 && c < row1) { k = std::max<int32_t>(k, (int32_t)d); ++n_ew; continue; }
-            fits[e] = 0;
-        }
-        if (k > 255) fits[e] = 0;
-        kk[e] = k;
-        if (fits[e]) S.fillers += k - n_ew;
-    }
-    for (int64_t wi = 0; wi < nw; ++wi) {
-        bool gen = false;
-        int32_t rounds = 0;
-        for (int l = 0; l < kSlice; ++l) {
-            const int64_t e = wi * kSlice + l;
-            gen = gen || !fits[e];
-            rounds = std::max(rounds, kk[e] - 1);
-        }
-        if (gen) {
-            S.w[2 * wi] = 1u << 31;
-            ++S.generic_warps;
-            continue;
-        }
-        S.w[2 * wi] = (uint32_t)rounds;
-        S.w[2 * wi + 1] = (uint32_t)S.run.size();
-        const size_t base = S.run.size();
-        S.run.resize(base + (size_t)rounds * kSlice, 0.0);
-        for (int l = 0; l < kSlice; ++l) {
-            const int64_t e = wi * kSlice + l, a = e + hoff;
-            const int32_t k = kk[e];
-            S.k[e] = (uint8_t)k;
-            for (int64_t m = rowptr[e]; m < rowptr[e + 1]; ++m) {
-                const int64_t c = cols[m];
-                const int64_t d = (c - a) * dir;
-                const double v = vals[m];
-                int slot = -1;
-                if (dir < 0) {
-                    if (d == 2 * (int64_t)pitch) slot = 0;
-                    else if (d == pitch) slot = 1;
-                    else if (d == 1) slot = 2;
-                    else if (d == 0) slot = 3;
-                    else S.run[base + (size_t)(k - d) * kSlice + l] = v;           // column a-d: round k-d
-                } else {
-                    if (d == 0) slot = 0;
-                    else if (d == 1) slot = 1;
-                    else if (d == pitch) slot = 2;
-                    else if (d == 2 * (int64_t)pitch) slot = 3;
-                    else S.run[base + (size_t)(d - 2) * kSlice + l] = v;           // column a+d: round d-2
-                }
-                if (slot >= 0) S.val4[(size_t)4 * e + slot] = v;
-            }
-        }
-    }
-    S.ok = true;
-}
 
 // Split rows into ELL(kEll) + SELL overflow (same packed offsets, same ascending order).
 void pack_ell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols,
@@ -549,7 +474,6 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             }
         }
         pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.halo, P.ZT);
-        if (P.precond != PCG_PRECOND_FSAI) pack_struct(rp, cols, vals, nown, pitch, P.halo, -1, P.sZT);
     }
     // ---- SELL of Z rows: row i = entries z_ij over columns j ascending (owned rows only; with
     // halo-AINV across ranks the northern neighbour's columns follow this rank's, ascending)
@@ -588,12 +512,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             fill[r]++;
         }
         pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.halo, P.Z);
-        if (P.precond != PCG_PRECOND_FSAI) pack_struct(rp, cols, vals, nown, pitch, P.halo, +1, P.sZ);
     }
-    if (getenv("PCG_VERBOSE") && P.sZ.ok && P.sZT.ok)
-        fprintf(stderr, "libpcg: structured Z: generic warps %lld / %lld (Z^T %lld), run fillers %lld (Z^T %lld), run values %zu (Z^T %zu)\n",
-                (long long)P.sZ.generic_warps, (long long)(nown / kSlice), (long long)P.sZT.generic_warps,
-                (long long)P.sZ.fillers, (long long)P.sZT.fillers, P.sZ.run.size(), P.sZT.run.size());
     // ---- FSAI DIA form: each owned column's entries at consecutive columns of the
     // same grid row i-1, i-2, ... (no land, wrap or N-S link inside the chain) -> diagonals
     if (P.precond == PCG_PRECOND_FSAI && P.fsai_q > 0) {

@@ -36,7 +36,6 @@ struct pcg_ctx {
     int64_t dev_bytes = 0;
     double *cE = nullptr, *cN = nullptr, *sigma = nullptr, *diag = nullptr, *piv = nullptr;
     uint32_t* ocean = nullptr;         // per (row, segment, warp) ocean bit masks
-    uint32_t* rowdone = nullptr;       // K23 row flags
     double* hot = nullptr;             // the eight per-iteration vectors, contiguous
     size_t hot_bytes = 0;
     char* ovf_base = nullptr;          // Z / Z^T overflow arrays, directly in front of `hot`
@@ -49,9 +48,6 @@ struct pcg_ctx {
     double *zt_val = nullptr, *z_val = nullptr, *zt_oval = nullptr, *z_oval = nullptr;
     int32_t *zt_col = nullptr, *z_col = nullptr, *zt_ocol = nullptr, *z_ocol = nullptr;
     int16_t *zt_c16 = nullptr, *z_c16 = nullptr;          // ELL slot offsets (when they all fit)
-    double *szt_val = nullptr, *szt_run = nullptr, *sz_val = nullptr, *sz_run = nullptr;   // structured form
-    uint8_t *szt_k = nullptr, *sz_k = nullptr;
-    uint32_t *szt_w = nullptr, *sz_w = nullptr;
     int64_t *zt_ooff = nullptr, *z_ooff = nullptr;
     DevScalars* sc = nullptr;
     DevScalars* h_sc = nullptr;        // pinned
@@ -872,19 +868,6 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
             if (Status st = rel16(P.Z, c->z_c16); !st) return st;
         }
     }
-    // structured Z / Z^T (internal.h Sz; PCG_SZ=0 keeps the ELL form)
-    bool use_sz = false;                          // measured 0.5-1.5 us/iteration slower than ELL(4) int16 at cfg4
-    if (const char* e = getenv("PCG_SZ")) use_sz = P.sZ.ok && P.sZT.ok && atoi(e) != 0;
-    if (use_sz) {
-        if (Status s = upload(c, c->szt_val, P.sZT.val4); !s) return s;
-        if (Status s = upload(c, c->szt_k, P.sZT.k); !s) return s;
-        if (Status s = upload(c, c->szt_w, P.sZT.w); !s) return s;
-        if (!P.sZT.run.empty()) if (Status s = upload(c, c->szt_run, P.sZT.run); !s) return s;
-        if (Status s = upload(c, c->sz_val, P.sZ.val4); !s) return s;
-        if (Status s = upload(c, c->sz_k, P.sZ.k); !s) return s;
-        if (Status s = upload(c, c->sz_w, P.sZ.w); !s) return s;
-        if (!P.sZ.run.empty()) if (Status s = upload(c, c->sz_run, P.sZ.run); !s) return s;
-    }
     // The eight per-iteration vectors live in one block, in the order of their passes per
     // iteration (r: 3, q, t, s, d, x: 2), so one L2 access-policy window can keep them resident
     // (DESIGN.md §4): only the static arrays (Z, Z^T, pivots, cE, cN) then stream from HBM.
@@ -1021,7 +1004,6 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     A.cE = c->cE; A.cN = c->cN; A.sigma = c->sigma; A.diag = c->diag; A.piv = c->piv;
     A.zt = EllDev{c->zt_val, c->zt_col, c->zt_ooff, c->zt_oval, c->zt_ocol, P.owned_elements(), c->zt_c16};
     A.z = EllDev{c->z_val, c->z_col, c->z_ooff, c->z_oval, c->z_ocol, P.owned_elements(), c->z_c16};
-    A.use_sz = use_sz ? 1 : 0;
     // L2 residency of the per-iteration vectors: a persisting access-policy window over the hot
     // block on every iteration kernel (launch attribute), with the persisting L2 set-aside sized
     // to it; the static arrays are left to stream.  PCG_L2PERSIST=0 disables (the set-aside is a
@@ -1067,8 +1049,6 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
                         "window %zu B, hit ratio %.3f\n", maxp, maxw, c->hot_bytes, cur, A.l2_bytes, A.l2_ratio);
         }
     }
-    A.szt = SzDev{c->szt_val, c->szt_k, reinterpret_cast<const uint2*>(c->szt_w), c->szt_run};
-    A.sz = SzDev{c->sz_val, c->sz_k, reinterpret_cast<const uint2*>(c->sz_w), c->sz_run};
     A.nel_all = P.elements();
     A.x = c->x; A.b = c->b; A.q = c->q; A.t = c->t; A.s = c->s;
     A.r[0] = c->r[0]; A.r[1] = c->r[1]; A.d[0] = c->d[0]; A.d[1] = c->d[1];
@@ -1079,17 +1059,6 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     A.precond = P.factored() ? 0 : (int32_t)P.precond;
     A.dia_q = 0;
     A.dia = c->dia;
-    // K23 (K2 + K3 in one kernel): not with halo-AINV across ranks (t rows arrive
-    // from the northern neighbour between K2 and K3) or the FSAI DIA form; PCG_FUSE23=0 disables
-    A.fuse23 = 0;
-    A.rowdone = nullptr;
-    A.zreach = std::max<int32_t>(0, P.Z.djmax);
-    if (P.factored() && !(c->multi && P.halo_w > 0)) {
-        const char* fe = getenv("PCG_FUSE23");
-        A.fuse23 = fe ? atoi(fe) != 0 : 0;
-        if (Status s = dalloc(c, c->rowdone, (int64_t)std::max(1, P.nloc)); !s) return s;
-        A.rowdone = c->rowdone;
-    }
     if (P.dia_q > 0) {                                  // PCG_FSAI_DIA=0 keeps the ELL path (tests)
         const char* e = getenv("PCG_FSAI_DIA");
         if (!(e && atoi(e) == 0) && P.dia_q <= 16) A.dia_q = P.dia_q;   // wider bands: ELL path
@@ -1101,7 +1070,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     if (!c->multi && A.l2_bytes == 0 && A.k1flat == 2 && !getenv("PCG_K1FLAT")) A.k1flat = 0;
     // redundant-sum mode (kernels.h): one rank, the K1 row-segment form, K2 / K3 as two launches
     A.redundant = 0;
-    if (P.factored() && !c->multi && !A.fuse23 && (A.k1flat == 2 || A.k1flat == 3 || (A.k1flat == 0 && !A.dynamic_k1)) && !A.tma) {
+    if (P.factored() && !c->multi && (A.k1flat == 2 || (A.k1flat == 0 && !A.dynamic_k1))) {
         const char* re = getenv("PCG_REDUNDANT");
         A.redundant = re ? atoi(re) != 0 : 1;
     }
@@ -1111,8 +1080,6 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         const char* re = getenv("PCG_REDUNDANT");
         A.red_gamma = re ? atoi(re) != 0 : 1;
     }
-    A.stage2 = 0;
-    if (const char* se = getenv("PCG_STAGE2")) A.stage2 = atoi(se) != 0;
     // Chronopoulos-Gear (NEXT-2): one rank, factored preconditioner through the ELL form
     A.cgcg = 0;
     A.p = nullptr;
@@ -1122,9 +1089,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
                                "(AINV, P_B2, FSAI) and, across ranks, block-local AINV (ainv_halo = 0)");
         A.cgcg = 1;
         A.redundant = 0;
-        A.fuse23 = 0;
         A.dia_q = 0;
-        A.tma = 0;
         if (Status st = dalloc(c, c->pvec, nel); !st) return st;
         A.p = c->pvec;
     }
@@ -1147,7 +1112,7 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     P.sigma.clear(); P.sigma.shrink_to_fit(); P.diag.clear(); P.diag.shrink_to_fit();
     P.piv.clear(); P.piv.shrink_to_fit();
     P.dia.clear(); P.dia.shrink_to_fit();
-    P.Z = Ell(); P.ZT = Ell(); P.sZ = Sz(); P.sZT = Sz();
+    P.Z = Ell(); P.ZT = Ell();
     P.zrow.clear(); P.zrow.shrink_to_fit(); P.zhat.clear(); P.zhat.shrink_to_fit();
     if (use_graph(c)) {
         if (Status s = build_graph(c); !s) {
@@ -1297,7 +1262,6 @@ pcg_status pcg_apply_preconditioner(pcg_ctx* c, const double* r, double* sout) {
         CU(cudaMemsetAsync(c->q, 0, (size_t)P.elements() / (size_t)P.pitch * dp, c->st));
         CU(cudaMemsetAsync(c->r[1], 0, (size_t)P.elements() / (size_t)P.pitch * dp, c->st));
         CU(cudaMemcpy2DAsync(c->r[1] + P.hoff(), dp, r, sp, sp, (size_t)P.nloc, cudaMemcpyDeviceToDevice, c->st));
-        if (c->rowdone) CU(cudaMemsetAsync(c->rowdone, 0, (size_t)P.nloc * sizeof(uint32_t), c->st));   // epoch = 0
         KArgs A = c->A;
         A.use_cond = 0;
         if (P.factored()) { launch_k2_ainv(A, 1, 1, c->st); launch_k3_ainv(A, 1, 1, c->st); }
@@ -1480,10 +1444,6 @@ pcg_status pcg_kernel_times(pcg_ctx* c, int32_t n_iter, double* ms_out, double* 
             return Status::err(PCG_ERR_BREAKDOWN, "pcg_kernel_times: iteration stopped early");
         for (int k = 0; k < 4; ++k) ms_out[k] = acc[k] / n_iter;
         if (bytes_out) for (int k = 0; k < 3; ++k) bytes_out[k] = c->bytes_k[k];
-        if (ainv && A.fuse23 && A.dia_q == 0 && !A.tma) {      // K23 in slot 1 (K2 + K3 bytes), slot 2 empty
-            ms_out[2] = 0.0;
-            if (bytes_out) { bytes_out[1] = c->bytes_k[1] + c->bytes_k[2]; bytes_out[2] = 0.0; }
-        }
         c->solved_once = false;            // x was overwritten
         return Status::ok();
     };

@@ -441,18 +441,16 @@ def test_local_ranks_pb2_bitwise():
 
 
 # ------------------------------------------------------ kernel-form variants (setup-time switches)
-VARIANTS = {"k23": {"PCG_FUSE23": "1"}, "k23_lag": {"PCG_FUSE23": "1", "PCG_LAG23": "7"},
-            "sz": {"PCG_SZ": "1"}, "sz_k23": {"PCG_SZ": "1", "PCG_FUSE23": "1"},
-            "no_l2_window": {"PCG_L2PERSIST": "0"}, "stage2": {"PCG_STAGE2": "1"},
-            "k1_strips": {"PCG_K1FLAT": "0"}, "k1_pairs": {"PCG_K1FLAT": "3"}, "no_redundant": {"PCG_REDUNDANT": "0"}}
+VARIANTS = {"no_l2_window": {"PCG_L2PERSIST": "0"}, "k1_strips": {"PCG_K1FLAT": "0"}, "no_redundant": {"PCG_REDUNDANT": "0"},
+            "graph_driver": {"PCG_RS": "0"}}
 
 
 @pytest.mark.parametrize("variant", sorted(VARIANTS))
 @pytest.mark.parametrize("name", ["cfg2", "cfg3"])
 def test_kernel_variants_bitwise_canonical(name, variant, monkeypatch):
-    """K2+K3 fused into one kernel (K23, incl. the minimum lag), the structured Z form and the
-    run without the L2 window: the same canonical arithmetic, so preconditioner and solve are
-    bitwise the oracle's."""
+    """The graph driver's kernel forms (K1 strips, last-block sums, no L2 window) and the graph
+    driver itself next to the default resident-strip driver: the same canonical arithmetic, so
+    preconditioner and solve are bitwise the oracle's."""
     for k, v in VARIANTS[variant].items():
         monkeypatch.setenv(k, v)
     p = synth.config(name)
@@ -481,14 +479,6 @@ def test_diag_k1_forms_bitwise_canonical(precond, env, monkeypatch):
     assert np.array_equal(x, A.to_grid(ref.x))
     assert rep["true_rel_residual"] == ref.true_rel_residual
     S.close()
-
-
-@pytest.mark.parametrize("P", [2, 3])
-def test_local_ranks_k23_bitwise(P, monkeypatch):
-    """K23 on block-local Z (w = 0) across P in-process ranks = the oracle's partitioned mode."""
-    monkeypatch.setenv("PCG_FUSE23", "1")
-    monkeypatch.setenv("PCG_SZ", "1")
-    test_local_ranks_bitwise_vs_oracle_partitioned("cfg3", P, "ainv")
 
 
 @pytest.mark.parametrize("P", [2, 4])
@@ -549,26 +539,6 @@ def test_timestep_driver_bitwise(name):
         cold_its.append(oracle.pcg(A, b, "ainv", M, 1e-10, maxit=A.n, mode="canonical", pitch=S.pitch,
                                    block=S.block).iterations)
     assert sum(warm_its[2:]) < sum(cold_its[2:])
-    S.close()
-
-
-@pytest.mark.parametrize("kind", ["cfg1", "sigma", "nonperiodic", "ragged"])
-def test_tiny_cta_driver_bitwise(kind, monkeypatch):
-    """Grids whose vectors fit in shared memory can run the whole loop in one CTA (tiny_kernel,
-    PCG_TINY=1, opt-in): bitwise the oracle's canonical PCG and the cooperative loop kernel."""
-    monkeypatch.setenv("PCG_TINY", "1")
-    if kind == "cfg1":
-        p = synth.config("cfg1")
-    else:
-        p = synth.random_grid(45 if kind == "ragged" else 30, 13, 3, periodic=kind != "nonperiodic",
-                              sigma=kind == "sigma")
-    A, S, ref, x, k, hist, rep, _ = _canonical_pair(p, "ainv", 1e-10)
-    assert k == ref.iterations and np.array_equal(hist, ref.hist)
-    assert np.array_equal(x, A.to_grid(ref.x))
-    b = dev(A.to_grid(rhs(A, p)))
-    monkeypatch.setenv("PCG_TINY", "0")
-    x2, k2, h2, _ = S.solve(b, tol=1e-10, maxit=A.n)
-    assert k2 == k and np.array_equal(h2, hist) and np.array_equal(host(x2), x)
     S.close()
 
 
