@@ -12,7 +12,11 @@
 // Block mode (reading R15): the index set is the ocean points of grid rows
 // [row_lo, row_hi); the principal submatrix of A on that set is orthogonalised and only
 // the columns of rows >= row_own are returned ("AINV computed per partition").
+#include <atomic>
 #include <cmath>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <cstring>
 #include <algorithm>
 #include <functional>
@@ -46,8 +50,18 @@ inline void faces(int32_t ni, int32_t nj, int32_t periodic, const double* cE, co
 }  // namespace
 
 void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, const double* cN,
-                const double* sigma, const uint8_t* mask, double tau, int32_t fill, AinvBlock& blk) {
+                const double* sigma, const uint8_t* mask, double tau, int32_t fill, AinvBlock& blk, int threads) {
+
     const int32_t r0 = blk.row_lo, r1 = blk.row_hi;
+    const int T0 = std::max(1, threads);
+    // parallel for over [0, n) in T0 contiguous ranges (element-wise independent work only)
+    auto pfor = [&](int64_t n_, const std::function<void(int64_t, int64_t)>& f) {
+        const int T = n_ < 50000 ? 1 : T0;
+        std::vector<std::thread> pool;
+        for (int t = 1; t < T; ++t) pool.emplace_back(f, n_ * t / T, n_ * (t + 1) / T);
+        f(0, n_ / T);
+        for (auto& th : pool) th.join();
+    };
     BlockMatrix M;
     // local numbering of the ocean points of rows [r0, r1), natural order
     std::vector<int32_t> loc((size_t)(r1 - r0) * ni, -1);
@@ -61,133 +75,228 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
     M.diag.resize(n);
     std::vector<double> sc(n);
     // diagonal A_pp = ((c_E + c_W) + c_N) + c_S (+ sigma) over all faces, then s = 1/sqrt(A_pp)
-    for (int32_t p = 0; p < n; ++p) {
-        int64_t g = M.grid[p];
-        int32_t i = (int32_t)(g % ni), j = (int32_t)(g / ni);
-        bool ex[4]; int64_t nb[4]; double c[4];
-        faces(ni, nj, periodic, cE, cN, i, j, ex, nb, c);
-        double d = ((c[0] + c[1]) + c[2]) + c[3];
-        if (sigma) d = d + sigma[g];
-        M.diag[p] = d;
-        sc[p] = 1.0 / std::sqrt(d);
-    }
-    // CSR of A^ restricted to the block: a^_pq = A_pq * (s_p * s_q)
-    M.ci.reserve((size_t)5 * n);
-    M.a.reserve((size_t)5 * n);
-    for (int32_t p = 0; p < n; ++p) {
-        int64_t g = M.grid[p];
-        int32_t i = (int32_t)(g % ni), j = (int32_t)(g / ni);
-        bool ex[4]; int64_t nb[4]; double c[4];
-        faces(ni, nj, periodic, cE, cN, i, j, ex, nb, c);
-        int32_t cols[5]; double vals[5]; int m = 0;
-        cols[m] = p; vals[m] = M.diag[p] * (sc[p] * sc[p]); ++m;
-        for (int f = 0; f < 4; ++f) {
-            if (!ex[f] || !(c[f] > 0.0) || !mask[nb[f]]) continue;
-            int32_t jn = (int32_t)(nb[f] / ni);
-            if (jn < r0 || jn >= r1) continue;          // outside the block's index set
-            int32_t q = loc[(size_t)(jn - r0) * ni + (int32_t)(nb[f] % ni)];
-            cols[m] = q; vals[m] = (-c[f]) * (sc[p] * sc[q]); ++m;
+    pfor(n, [&](int64_t lo, int64_t hi) {
+        for (int64_t p = lo; p < hi; ++p) {
+            int64_t g = M.grid[p];
+            int32_t i = (int32_t)(g % ni), j = (int32_t)(g / ni);
+            bool ex[4]; int64_t nb[4]; double c[4];
+            faces(ni, nj, periodic, cE, cN, i, j, ex, nb, c);
+            double d = ((c[0] + c[1]) + c[2]) + c[3];
+            if (sigma) d = d + sigma[g];
+            M.diag[p] = d;
+            sc[p] = 1.0 / std::sqrt(d);
         }
-        for (int x = 1; x < m; ++x)
-            for (int y = x; y > 0 && cols[y - 1] > cols[y]; --y) { std::swap(cols[y], cols[y - 1]); std::swap(vals[y], vals[y - 1]); }
-        for (int x = 0; x < m; ++x) { M.ci.push_back(cols[x]); M.a.push_back(vals[x]); }
-        M.rp[p + 1] = (int32_t)M.ci.size();
-    }
-
-    // Zhat columns (CSC), pivots
-    std::vector<int64_t> zp(1, 0);
-    zp.reserve(n + 1);
-    std::vector<int32_t> zr;
-    std::vector<double> zv;
-    zr.reserve((size_t)6 * n); zv.reserve((size_t)6 * n);
-    std::vector<double> piv(n);
-
-    std::vector<double> w(n, 0.0);
-    std::vector<uint8_t> live(n, 0);        // entry present in the current column
-    std::vector<int32_t> listed(n, -1);     // stamp: k recorded in `members` for column j
-    std::vector<int32_t> queued(n, -1);     // stamp: k queued as a candidate for column j
-    std::vector<int32_t> members, touched;
-    std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> cand;
-
-    int64_t fail = -1;
-    for (int32_t j = 0; j < n; ++j) {
-        members.clear();
-        members.push_back(j); listed[j] = j; live[j] = 1; w[j] = 1.0;
-        for (int32_t e = M.rp[j]; e < M.rp[j + 1]; ++e) {
-            int32_t i = M.ci[e];
-            if (i < j && queued[i] != j) { queued[i] = j; cand.push(i); }
-        }
-        while (!cand.empty()) {
-            const int32_t i = cand.top(); cand.pop();
-            // pi = a^_i . z over row i of A^ (ascending columns, present entries)
-            double pi = 0.0;
-            for (int32_t e = M.rp[i]; e < M.rp[i + 1]; ++e) {
-                int32_t k = M.ci[e];
-                if (live[k]) pi = pi + M.a[e] * w[k];
+    });
+    // CSR of A^ restricted to the block: a^_pq = A_pq * (s_p * s_q); rows built in parallel into
+    // 5 fixed slots per row, then compacted
+    std::vector<int32_t> c5((size_t)5 * n);
+    std::vector<double> a5((size_t)5 * n);
+    std::vector<uint8_t> m5(n);
+    pfor(n, [&](int64_t lo, int64_t hi) {
+        for (int64_t p = lo; p < hi; ++p) {
+            int64_t g = M.grid[p];
+            int32_t i = (int32_t)(g % ni), j = (int32_t)(g / ni);
+            bool ex[4]; int64_t nb[4]; double c[4];
+            faces(ni, nj, periodic, cE, cN, i, j, ex, nb, c);
+            int32_t* cols = &c5[(size_t)5 * p];
+            double* vals = &a5[(size_t)5 * p];
+            int m = 0;
+            cols[m] = (int32_t)p; vals[m] = M.diag[p] * (sc[p] * sc[p]); ++m;
+            for (int f = 0; f < 4; ++f) {
+                if (!ex[f] || !(c[f] > 0.0) || !mask[nb[f]]) continue;
+                int32_t jn = (int32_t)(nb[f] / ni);
+                if (jn < r0 || jn >= r1) continue;          // outside the block's index set
+                int32_t q = loc[(size_t)(jn - r0) * ni + (int32_t)(nb[f] % ni)];
+                cols[m] = q; vals[m] = (-c[f]) * (sc[p] * sc[q]); ++m;
             }
-            if (pi == 0.0) continue;
-            const double coef = pi / piv[i];
-            touched.clear();
-            for (int64_t e = zp[i]; e < zp[i + 1]; ++e) {
-                const int32_t k = zr[e];
-                if (!live[k]) {
-                    live[k] = 1; w[k] = 0.0;
-                    if (listed[k] != j) { listed[k] = j; members.push_back(k); }
-                    for (int32_t e2 = M.rp[k]; e2 < M.rp[k + 1]; ++e2) {
-                        int32_t i2 = M.ci[e2];
-                        if (i2 > i && i2 < j && queued[i2] != j) { queued[i2] = j; cand.push(i2); }
+            for (int x = 1; x < m; ++x)
+                for (int y = x; y > 0 && cols[y - 1] > cols[y]; --y) { std::swap(cols[y], cols[y - 1]); std::swap(vals[y], vals[y - 1]); }
+            m5[p] = (uint8_t)m;
+        }
+    });
+    for (int32_t p = 0; p < n; ++p) M.rp[p + 1] = M.rp[p] + m5[p];
+    M.ci.resize(M.rp[n]);
+    M.a.resize(M.rp[n]);
+    pfor(n, [&](int64_t lo, int64_t hi) {
+        for (int64_t p = lo; p < hi; ++p)
+            for (int x = 0; x < m5[p]; ++x) { M.ci[M.rp[p] + x] = c5[(size_t)5 * p + x]; M.a[M.rp[p] + x] = a5[(size_t)5 * p + x]; }
+    });
+
+    // Zhat columns and pivots.  Column j needs the finished columns i < j it meets as
+    // candidates (pivot p_i, entries of zhat_i), nothing else, so the columns can be built by
+    // several threads at once with bitwise the sequential result (every column runs the same
+    // operations in the same order; only the time it waits differs).  Thread t owns the grid
+    // columns [cb[t], cb[t+1]) of every row and builds its columns in increasing order -- a
+    // wavefront: the first column of its chunk in row r waits for the west neighbour, the last one
+    // of thread t-1's chunk in row r, so thread t runs about one row behind thread t-1.  A column
+    // whose candidate is not finished yet spins on its `done` flag (release / acquire).
+    // Progress: a thread only waits for smaller columns, and the smallest unfinished column's
+    // dependencies are all finished.  On an AINV failure (pivot <= 1e-12) columns beyond the
+    // smallest failing one are abandoned, so the reported column is the sequential one.
+    struct ColRef {
+        const int32_t* r = nullptr;
+        const double* v = nullptr;
+        int32_t len = 0;
+    };
+    std::vector<ColRef> cref(n);
+    std::vector<double> piv(n);
+    std::unique_ptr<std::atomic<uint8_t>[]> done(new std::atomic<uint8_t>[std::max(n, 1)]);
+    for (int32_t p = 0; p < n; ++p) done[p].store(0, std::memory_order_relaxed);
+    std::atomic<int32_t> limit(n);
+    int T = std::max(1, threads);
+    if (n < 20000) T = 1;
+    T = std::min(T, std::max(1, ni / 64));
+    std::vector<std::vector<int32_t>> mine((size_t)T);
+    for (int32_t p = 0; p < n; ++p) {
+        const int32_t i = (int32_t)(M.grid[p] % ni);
+        mine[(size_t)std::min<int64_t>(T - 1, (int64_t)i * T / ni)].push_back(p);
+    }
+    std::vector<std::vector<std::unique_ptr<int32_t[]>>> seg_r((size_t)T);
+    std::vector<std::vector<std::unique_ptr<double[]>>> seg_v((size_t)T);
+    auto worker = [&](int t) {
+        std::vector<double> w(n, 0.0);
+        std::vector<uint8_t> live(n, 0);        // entry present in the current column
+        std::vector<int32_t> listed(n, -1);     // stamp: k recorded in `members` for column j
+        std::vector<int32_t> queued(n, -1);     // stamp: k queued as a candidate for column j
+        std::vector<int32_t> members, touched;
+        std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> cand;
+        // column storage in fixed segments (a column's entries never move once published; the
+        // segments outlive every thread, which may read them until the last one finishes)
+        std::vector<std::unique_ptr<int32_t[]>>& segr = seg_r[(size_t)t];
+        std::vector<std::unique_ptr<double[]>>& segv = seg_v[(size_t)t];
+        size_t seg_cap = 0, seg_used = 0;
+        auto wait_for = [&](int32_t i, int32_t j) -> bool {
+            for (unsigned spin = 0; !done[i].load(std::memory_order_acquire); ++spin) {
+                if (j >= limit.load(std::memory_order_relaxed)) return false;
+                if (spin > 64) std::this_thread::yield();
+            }
+            return true;
+        };
+        for (int32_t j : mine[(size_t)t]) {
+            if (j >= limit.load(std::memory_order_relaxed)) return;
+            members.clear();
+            members.push_back(j); listed[j] = j; live[j] = 1; w[j] = 1.0;
+            for (int32_t e = M.rp[j]; e < M.rp[j + 1]; ++e) {
+                int32_t i = M.ci[e];
+                if (i < j && queued[i] != j) { queued[i] = j; cand.push(i); }
+            }
+            bool ok = true;
+            while (!cand.empty()) {
+                const int32_t i = cand.top(); cand.pop();
+                // pi = a^_i . z over row i of A^ (ascending columns, present entries)
+                double pi = 0.0;
+                for (int32_t e = M.rp[i]; e < M.rp[i + 1]; ++e) {
+                    int32_t k = M.ci[e];
+                    if (live[k]) pi = pi + M.a[e] * w[k];
+                }
+                if (pi == 0.0) continue;
+                if (!wait_for(i, j)) { ok = false; break; }
+                const double coef = pi / piv[i];
+                touched.clear();
+                const ColRef zi = cref[i];
+                for (int32_t q = 0; q < zi.len; ++q) {
+                    const int32_t k = zi.r[q];
+                    if (!live[k]) {
+                        live[k] = 1; w[k] = 0.0;
+                        if (listed[k] != j) { listed[k] = j; members.push_back(k); }
+                        for (int32_t e2 = M.rp[k]; e2 < M.rp[k + 1]; ++e2) {
+                            int32_t i2 = M.ci[e2];
+                            if (i2 > i && i2 < j && queued[i2] != j) { queued[i2] = j; cand.push(i2); }
+                        }
+                    }
+                    w[k] = w[k] - coef * zi.v[q];
+                    touched.push_back(k);
+                }
+                for (int32_t k : touched)
+                    if (k != j && std::fabs(w[k]) < tau) { live[k] = 0; w[k] = 0.0; }
+                if (fill > 0) {
+                    // P_B2 (reading R26): keep the diagonal and the fill-1 largest |z|, ties to the
+                    // smaller index
+                    touched.clear();
+                    for (int32_t k : members)
+                        if (k != j && live[k]) touched.push_back(k);
+                    if ((int64_t)touched.size() > (int64_t)fill - 1) {
+                        std::sort(touched.begin(), touched.end(), [&](int32_t a, int32_t b) {
+                            const double fa = std::fabs(w[a]), fb = std::fabs(w[b]);
+                            return fa > fb || (fa == fb && a < b);
+                        });
+                        for (size_t x = (size_t)fill - 1; x < touched.size(); ++x) { live[touched[x]] = 0; w[touched[x]] = 0.0; }
                     }
                 }
-                w[k] = w[k] - coef * zv[e];
-                touched.push_back(k);
             }
-            for (int32_t k : touched)
-                if (k != j && std::fabs(w[k]) < tau) { live[k] = 0; w[k] = 0.0; }
-            if (fill > 0) {
-                // P_B2 (reading R26): keep the diagonal and the fill-1 largest |z|, ties to the
-                // smaller index
-                touched.clear();
-                for (int32_t k : members)
-                    if (k != j && live[k]) touched.push_back(k);
-                if ((int64_t)touched.size() > (int64_t)fill - 1) {
-                    std::sort(touched.begin(), touched.end(), [&](int32_t a, int32_t b) {
-                        const double fa = std::fabs(w[a]), fb = std::fabs(w[b]);
-                        return fa > fb || (fa == fb && a < b);
-                    });
-                    for (size_t t = (size_t)fill - 1; t < touched.size(); ++t) { live[touched[t]] = 0; w[touched[t]] = 0.0; }
+            if (!ok) {                                    // abandoned: a smaller column failed
+                while (!cand.empty()) cand.pop();
+                for (int32_t k : members) { live[k] = 0; w[k] = 0.0; }
+                return;
+            }
+            double pj = 0.0;
+            for (int32_t e = M.rp[j]; e < M.rp[j + 1]; ++e) {
+                int32_t k = M.ci[e];
+                if (live[k]) pj = pj + M.a[e] * w[k];
+            }
+            std::sort(members.begin(), members.end());
+            int32_t len = 0;
+            for (int32_t k : members) len += live[k];
+            if (seg_used + (size_t)len > seg_cap) {
+                seg_cap = std::max<size_t>((size_t)len, 1 << 16);
+                segr.emplace_back(new int32_t[seg_cap]);
+                segv.emplace_back(new double[seg_cap]);
+                seg_used = 0;
+            }
+            int32_t* rr = segr.back().get() + seg_used;
+            double* vv = segv.back().get() + seg_used;
+            int32_t q = 0;
+            for (int32_t k : members) {
+                if (live[k]) { rr[q] = k; vv[q] = w[k]; ++q; }
+                live[k] = 0; w[k] = 0.0;
+            }
+            seg_used += (size_t)len;
+            cref[j] = ColRef{rr, vv, len};
+            piv[j] = pj;
+            if (!(pj > kPivotMin) || !std::isfinite(pj)) {
+                int32_t cur = limit.load();
+                while (j < cur && !limit.compare_exchange_weak(cur, j)) {
                 }
+                done[j].store(1, std::memory_order_release);
+                return;
             }
+            done[j].store(1, std::memory_order_release);
         }
-        double pj = 0.0;
-        for (int32_t e = M.rp[j]; e < M.rp[j + 1]; ++e) {
-            int32_t k = M.ci[e];
-            if (live[k]) pj = pj + M.a[e] * w[k];
-        }
-        piv[j] = pj;
-        if (!(pj > kPivotMin) || !std::isfinite(pj)) { fail = j; }
-        std::sort(members.begin(), members.end());
-        for (int32_t k : members) {
-            if (live[k]) { zr.push_back(k); zv.push_back(w[k]); }
-            live[k] = 0; w[k] = 0.0;
-        }
-        zp.push_back((int64_t)zr.size());
-        if (fail >= 0) break;
+    };
+    {
+        std::vector<std::thread> pool;
+        for (int t = 1; t < T; ++t) pool.emplace_back(worker, t);
+        worker(0);
+        for (auto& th : pool) th.join();
     }
+    const int64_t fail = limit.load() < n ? (int64_t)limit.load() : -1;
     blk.fail_grid = fail >= 0 ? M.grid[fail] : -1;
     if (fail >= 0) return;
 
-    // owned columns: local unknowns whose grid row >= row_own
+    // owned columns (local unknowns whose grid row >= row_own), straight from the column
+    // segments into the block's arrays (offsets by prefix sum, copies in parallel)
     int32_t first_owned = n;
     for (int32_t p = 0; p < n; ++p)
         if (M.grid[p] / ni >= blk.row_own) { first_owned = p; break; }
-    blk.colptr.assign(1, 0);
-    blk.row_g.clear(); blk.zhat.clear(); blk.piv.clear(); blk.col_g.clear();
-    for (int32_t j = first_owned; j < n; ++j) {
-        for (int64_t e = zp[j]; e < zp[j + 1]; ++e) { blk.row_g.push_back(M.grid[zr[e]]); blk.zhat.push_back(zv[e]); }
-        blk.colptr.push_back((int64_t)blk.row_g.size());
-        blk.piv.push_back(piv[j]);
-        blk.col_g.push_back(M.grid[j]);
-    }
+    const int32_t nown = n - first_owned;
+    blk.colptr.assign((size_t)nown + 1, 0);
+    for (int32_t q = 0; q < nown; ++q) blk.colptr[q + 1] = blk.colptr[q] + cref[first_owned + q].len;
+    blk.row_g.resize((size_t)blk.colptr[nown]);
+    blk.zhat.resize((size_t)blk.colptr[nown]);
+    blk.piv.resize(nown);
+    blk.col_g.resize(nown);
+    pfor(nown, [&](int64_t lo, int64_t hi) {
+        for (int64_t q = lo; q < hi; ++q) {
+            const int32_t j = first_owned + (int32_t)q;
+            const ColRef& z = cref[j];
+            for (int32_t x = 0; x < z.len; ++x) {
+                blk.row_g[(size_t)blk.colptr[q] + x] = M.grid[z.r[x]];
+                blk.zhat[(size_t)blk.colptr[q] + x] = z.v[x];
+            }
+            blk.piv[q] = piv[j];
+            blk.col_g[q] = M.grid[j];
+        }
+    });
 }
 
 }  // namespace pcg

@@ -36,8 +36,7 @@ struct Status {
 struct Sell {
     std::vector<int64_t> off;      // nslices + 1
     std::vector<double> val;
-    std::vector<int32_t> col;      // packed (di, dj)
-    int32_t dimin = 0, dimax = 0, djmin = 0, djmax = 0;   // extents over the real entries
+    std::vector<int32_t> col;      // array indices (padding: the row's own index)
     int64_t entries() const { return (int64_t)val.size(); }
 };
 
@@ -53,7 +52,6 @@ struct Ell {
     std::vector<double> val;       // n * kEll (element-major)
     std::vector<int32_t> col;      // n * kEll
     Sell ovf;
-    int32_t dimin = 0, dimax = 0, djmin = 0, djmax = 0;
     int64_t entries() const { return (int64_t)val.size() + ovf.entries(); }
 };
 
@@ -110,7 +108,7 @@ struct AinvBlock {
     int64_t fail_grid = -1;
 };
 void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, const double* cN,
-                const double* sigma, const uint8_t* mask, double tau, int32_t fill, AinvBlock& blk);
+                const double* sigma, const uint8_t* mask, double tau, int32_t fill, AinvBlock& blk, int threads = 1);
 // NEXT-1 banded FSAI of T = band(A, 1) over the whole grid, as one factored block (fsai.cpp)
 void fsai_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, const double* cN, const uint8_t* mask,
                 int32_t q, const std::function<double(int64_t)>& diag_of, AinvBlock& blk);

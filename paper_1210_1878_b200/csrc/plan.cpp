@@ -86,115 +86,74 @@ int64_t global_unknown(const uint8_t* mask, int32_t ni, int64_t g) {
     return c;
 }
 
-// Pack a set of sparse rows (one per owned element; entries (array column, value) already in
-// ascending column order) into SELL-32 with relative (di, dj) column offsets.
-void pack_sell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols,
-               const std::vector<double>& vals, int64_t nel, int32_t pitch, int32_t ni, int32_t periodic, Sell& S,
-               bool absolute, int32_t halo) {
-    S.dimin = S.dimax = S.djmin = S.djmax = 0;
-    auto rel = [&](int64_t e, int32_t ac) -> int32_t {
-        const int32_t jr = (int32_t)(e / pitch), ir = (int32_t)(e % pitch);
-        const int32_t jc = ac / pitch - halo, ic = ac % pitch;
-        int32_t di = ic - ir;
-        const int32_t dj = jc - jr;
-        if (periodic) {
-            if (di > ni / 2) di -= ni;
-            if (di < -((ni - 1) / 2)) di += ni;
-        }
-        S.dimin = std::min(S.dimin, di); S.dimax = std::max(S.dimax, di);
-        S.djmin = std::min(S.djmin, dj); S.djmax = std::max(S.djmax, dj);
-        return (int32_t)(((uint32_t)(uint16_t)(int16_t)dj << 16) | (uint32_t)(uint16_t)(int16_t)di);
-    };
-    const int64_t nsl = nel / kSlice;
-    S.off.assign(nsl + 1, 0);
-    for (int64_t s = 0; s < nsl; ++s) {
-        int64_t L = 0;
-        for (int l = 0; l < kSlice; ++l) {
-            int64_t e = s * kSlice + l;
-            L = std::max(L, rowptr[e + 1] - rowptr[e]);
-        }
-        S.off[s + 1] = S.off[s] + L * kSlice;
-    }
-    S.val.assign(S.off[nsl], 0.0);
-    S.col.assign(S.off[nsl], 0);
-    for (int64_t s = 0; s < nsl; ++s) {
-        const int64_t L = (S.off[s + 1] - S.off[s]) / kSlice;
-        for (int l = 0; l < kSlice; ++l) {
-            const int64_t e = s * kSlice + l;
-            const int64_t len = rowptr[e + 1] - rowptr[e];
-            for (int64_t m = 0; m < L; ++m) {
-                const int64_t slot = S.off[s] + m * kSlice + l;
-                if (m < len) {
-                    S.val[slot] = vals[rowptr[e] + m];
-                    const int32_t r = rel(e, cols[rowptr[e] + m]);
-                    S.col[slot] = absolute ? cols[rowptr[e] + m] : r;
-                } else {
-                    S.val[slot] = 0.0;
-                    S.col[slot] = absolute ? (int32_t)(e + (int64_t)halo * pitch) : 0;
-                }
-            }
-        }
-    }
+// parallel for over [0, n) in T contiguous ranges (independent iterations only)
+void pfor(int T, int64_t n, const std::function<void(int64_t, int64_t)>& f) {
+    if (n < 100000) T = 1;
+    T = std::max(1, T);
+    std::vector<std::thread> pool;
+    for (int t = 1; t < T; ++t) pool.emplace_back(f, n * t / T, n * (t + 1) / T);
+    f(0, n / T);
+    for (auto& th : pool) th.join();
 }
 
-
-// Split rows into ELL(kEll) + SELL overflow (same packed offsets, same ascending order).
+// Pack a set of sparse rows (one per owned element e; entries (absolute array column, value) in
+// ascending column order) as ELL(kEll) + SELL-32 overflow (internal.h Ell): the first kEll
+// entries of every row in its fixed slots (padding: value 0 at the row's own array index), the
+// rest of the slice's rows as SELL-32 (L = the slice's longest overflow; padding: value 0 at the
+// row's own index).  One pass over the rows, no intermediate full SELL.
 void pack_ell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols,
               const std::vector<double>& vals, int64_t nel, int32_t pitch, int32_t ni, int32_t periodic, int32_t halo,
-              Ell& E) {
-    Sell full;
-    pack_sell(rowptr, cols, vals, nel, pitch, ni, periodic, full, true, halo);   // absolute columns + extents
+              Ell& E, int T) {
+    (void)ni; (void)periodic;
     const int64_t hoff = (int64_t)halo * pitch;        // array index of owned element 0
     E.n = nel;
-    E.dimin = full.dimin; E.dimax = full.dimax; E.djmin = full.djmin; E.djmax = full.djmax;
     E.val.assign((size_t)kEll * nel, 0.0);
-    E.col.assign((size_t)kEll * nel, 0);
-    for (int64_t e = 0; e < nel; ++e)                    // padding: value 0 at the row's own point
-        for (int m = 0; m < kEll; ++m) E.col[e * kEll + m] = (int32_t)(e + hoff);
-    std::vector<int64_t> orp(nel + 1, 0);
-    std::vector<int32_t> ocol;
-    std::vector<double> oval;
+    E.col.resize((size_t)kEll * nel);
     const int64_t nsl = nel / kSlice;
-    for (int64_t s = 0; s < nsl; ++s) {
-        const int64_t L = (full.off[s + 1] - full.off[s]) / kSlice;
-        for (int l = 0; l < kSlice; ++l) {
-            const int64_t e = s * kSlice + l;
-            const int64_t len = rowptr[e + 1] - rowptr[e];
-            for (int64_t m = 0; m < L && m < len; ++m) {
-                const int64_t slot = full.off[s] + m * kSlice + l;
-                if (m < kEll) { E.val[e * kEll + m] = full.val[slot]; E.col[e * kEll + m] = full.col[slot]; }
-                else { ocol.push_back(full.col[slot]); oval.push_back(full.val[slot]); }
-            }
-            orp[e + 1] = orp[e] + std::max<int64_t>(0, len - kEll);
-        }
-    }
-    // overflow rows as SELL: reuse pack_sell on already-packed offsets (identity columns)
     E.ovf.off.assign(nsl + 1, 0);
     for (int64_t s = 0; s < nsl; ++s) {
         int64_t L = 0;
-        for (int l = 0; l < kSlice; ++l) L = std::max(L, orp[s * kSlice + l + 1] - orp[s * kSlice + l]);
+        for (int l = 0; l < kSlice; ++l) {
+            const int64_t e = s * kSlice + l;
+            L = std::max(L, rowptr[e + 1] - rowptr[e] - kEll);
+        }
         E.ovf.off[s + 1] = E.ovf.off[s] + L * kSlice;
     }
     E.ovf.val.assign(E.ovf.off[nsl], 0.0);
-    E.ovf.col.assign(E.ovf.off[nsl], 0);
-    for (int64_t s = 0; s < nsl; ++s)
-        for (int64_t slot = E.ovf.off[s]; slot < E.ovf.off[s + 1]; ++slot)
-            E.ovf.col[slot] = (int32_t)(s * kSlice + (slot - E.ovf.off[s]) % kSlice + hoff);
-    for (int64_t s = 0; s < nsl; ++s)
+    E.ovf.col.resize(E.ovf.off[nsl]);
+    pfor(T, nsl, [&](int64_t s0, int64_t s1) {
+    for (int64_t s = s0; s < s1; ++s) {
+        const int64_t L = (E.ovf.off[s + 1] - E.ovf.off[s]) / kSlice;
         for (int l = 0; l < kSlice; ++l) {
-            const int64_t e = s * kSlice + l;
-            for (int64_t m = 0; m < orp[e + 1] - orp[e]; ++m) {
+            const int64_t e = s * kSlice + l, r0 = rowptr[e], len = rowptr[e + 1] - r0;
+            const int32_t own = (int32_t)(e + hoff);
+            for (int m = 0; m < kEll; ++m) {
+                E.col[(size_t)e * kEll + m] = m < len ? cols[r0 + m] : own;
+                if (m < len) E.val[(size_t)e * kEll + m] = vals[r0 + m];
+            }
+            for (int64_t m = 0; m < L; ++m) {
                 const int64_t slot = E.ovf.off[s] + m * kSlice + l;
-                E.ovf.val[slot] = oval[orp[e] + m];
-                E.ovf.col[slot] = ocol[orp[e] + m];
+                const bool real = kEll + m < len;
+                E.ovf.col[slot] = real ? cols[r0 + kEll + m] : own;
+                if (real) E.ovf.val[slot] = vals[r0 + kEll + m];
             }
         }
+    }
+    });
 }
 
 }  // namespace
 
 Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Plan& P) {
     auto t0 = std::chrono::steady_clock::now();
+    const bool verbose = getenv("PCG_VERBOSE") != nullptr;
+    auto tprev = t0;
+    auto stage = [&](const char* what) {
+        if (!verbose) return;
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "libpcg: setup %-28s %.3f s\n", what, std::chrono::duration<double>(now - tprev).count());
+        tprev = now;
+    };
     if (!c || !g || !o) return Status::err(PCG_ERR_ARG, "pcg_setup: NULL coeffs/grid/opts");
     if (!c->cE || !c->cN || !c->mask) return Status::err(PCG_ERR_ARG, "pcg_setup: coeffs.cE, cN and mask are required");
     if (g->ni < 3 || g->nj < 3) return Status::err(PCG_ERR_ARG, "pcg_setup: need ni >= 3 and nj >= 3");
@@ -216,6 +175,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         return Status::err(PCG_ERR_ARG, "pcg_setup: ainv_parts emulates ranks on one GPU; use nranks instead");
     const int32_t ni = g->ni, nj = g->nj;
     const int64_t ng = (int64_t)ni * nj;
+    const int nthr = std::min(64, o->setup_threads > 0 ? o->setup_threads : (int)std::max(1u, std::thread::hardware_concurrency()));
     for (int64_t k = 0; k < ng; ++k) {
         if (!(c->cE[k] >= 0.0) || !std::isfinite(c->cE[k]) || !(c->cN[k] >= 0.0) || !std::isfinite(c->cN[k])) {
             char buf[160];
@@ -260,7 +220,9 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
                      (int)(k % ni), (int)(k / ni));
             return Status::err(PCG_ERR_NOT_SPD, buf, global_unknown(c->mask, ni, k));
         }
+    stage("validation + diagonal");
     if (Status s = anchor_check(ni, nj, P.periodic, c->cE, c->cN, c->sigma, c->mask); !s) return s;
+    stage("anchor check");
     if (ni > 65534) return Status::err(PCG_ERR_ARG, "pcg_setup: ni > 65534 not supported (int16 column offsets)");
 
     // device-layout coefficient arrays: absent faces -> 0, land flagged by the
@@ -346,16 +308,23 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         fsai_block(ni, nj, P.periodic, c->cE, c->cN, c->mask, P.fsai_q, diag_of, blocks[0]);
     } else {
         int nthreads = o->setup_threads > 0 ? o->setup_threads : (int)std::max(1u, std::thread::hardware_concurrency());
+        nthreads = std::min(nthreads, 64);
+        // threads across blocks first, the rest inside each block (ainv.cpp's column wavefront)
+        const int inner = std::max(1, nthreads / (int)blocks.size());
         nthreads = std::min<int>(nthreads, (int)blocks.size());
         std::vector<std::thread> pool;
         std::atomic_size_t next{0};
         auto work = [&]() {
             for (size_t k; (k = next.fetch_add(1)) < blocks.size();)
-                ainv_block(ni, nj, P.periodic, c->cE, c->cN, c->sigma, c->mask, P.tau, P.ainv_fill, blocks[k]);
+                ainv_block(ni, nj, P.periodic, c->cE, c->cN, c->sigma, c->mask, P.tau, P.ainv_fill, blocks[k], inner);
         };
+        const auto ta = std::chrono::steady_clock::now();
         for (int t = 1; t < nthreads; ++t) pool.emplace_back(work);
         work();
         for (auto& t : pool) t.join();
+        if (getenv("PCG_VERBOSE"))
+            fprintf(stderr, "libpcg: AINV %zu block(s) x %d thread(s): %.3f s\n", blocks.size(), inner,
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - ta).count());
     }
     for (auto& b : blocks)
         if (b.fail_grid >= 0) {
@@ -365,6 +334,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             return Status::err(PCG_ERR_NOT_SPD, buf, global_unknown(c->mask, ni, b.fail_grid));
         }
 
+    stage("AINV");
     AinvBlock north;
     int32_t reach = 0;                                   // t rows needed north of je
     if (have_north) {
@@ -413,6 +383,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     P.halo_t = reach;
     P.halo_t_send = reach_s;
     build_coeff_arrays();
+    stage("coefficient arrays");
 
     // ---- owned columns in natural order: export + Z values z_kj = fl(s_k * zhat_kj)
     auto arr_of = [&](int64_t gi) -> int64_t {        // grid index -> array index (owned / halo rows)
@@ -434,30 +405,55 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         for (int64_t k = (int64_t)rlo * ni; k < (int64_t)P.je * ni; ++k)
             if (c->mask[k]) unk[k - (int64_t)rlo * ni] = u++;
     }
-    P.nnz_off = 0;
-    for (auto& b : blocks) {
-        for (size_t q = 0; q < b.col_g.size(); ++q) {
-            for (int64_t e = b.colptr[q]; e < b.colptr[q + 1]; ++e) {
-                int64_t gr = b.row_g[e];
-                P.zrow.push_back(unk[gr - (int64_t)rlo * ni]);
-                P.zhat.push_back(b.zhat[e]);
-                double s = P.precond == PCG_PRECOND_FSAI ? 1.0 : 1.0 / std::sqrt(diag_of(gr));   // FSAI: no Jacobi scale
-                ent_z.push_back(s * b.zhat[e]);
-                ent_row_arr.push_back(arr_of(gr));
-            }
-            P.zcolptr.push_back((int64_t)P.zrow.size());
-            P.pivots.push_back(b.piv[q]);
-            P.scale.push_back(P.precond == PCG_PRECOND_FSAI ? 1.0 : 1.0 / std::sqrt(diag_of(b.col_g[q])));
-            colarr.push_back(arr_of(b.col_g[q]));
-            P.piv[colarr.back()] = b.piv[q];
-            P.nnz_off += (b.colptr[q + 1] - b.colptr[q]) - 1;
-        }
+    // Jacobi scale s_g = 1/sqrt(A_gg) once per grid point of the rows the entries touch (the same
+    // IEEE operations as per entry; FSAI: no scale)
+    const int32_t rhi = std::min(nj, P.je + kNorthRows);
+    std::vector<double> sgrid((size_t)(rhi - rlo) * ni, 1.0);
+    if (P.precond != PCG_PRECOND_FSAI)
+        for (int64_t g2 = (int64_t)rlo * ni; g2 < (int64_t)rhi * ni; ++g2)
+            if (c->mask[g2]) sgrid[(size_t)(g2 - (int64_t)rlo * ni)] = 1.0 / std::sqrt(diag_of(g2));
+    auto scale_of = [&](int64_t gr) { return sgrid[(size_t)(gr - (int64_t)rlo * ni)]; };
+    int64_t ntot = 0, ncols = 0;
+    for (auto& b : blocks) { ntot += b.colptr.back(); ncols += (int64_t)b.col_g.size(); }
+    // flat column index over the blocks, entry offsets by prefix sum, then a parallel fill
+    std::vector<std::pair<int32_t, int32_t>> colsrc;      // (block, column in block)
+    colsrc.reserve((size_t)ncols);
+    for (size_t bi = 0; bi < blocks.size(); ++bi)
+        for (size_t q = 0; q < blocks[bi].col_g.size(); ++q) colsrc.push_back({(int32_t)bi, (int32_t)q});
+    P.zcolptr.assign((size_t)ncols + 1, 0);
+    for (int64_t k = 0; k < ncols; ++k) {
+        const AinvBlock& b = blocks[(size_t)colsrc[(size_t)k].first];
+        const int32_t q = colsrc[(size_t)k].second;
+        P.zcolptr[(size_t)k + 1] = P.zcolptr[(size_t)k] + (b.colptr[q + 1] - b.colptr[q]);
     }
+    P.zrow.resize((size_t)ntot); P.zhat.resize((size_t)ntot);
+    ent_z.resize((size_t)ntot); ent_row_arr.resize((size_t)ntot);
+    P.pivots.resize((size_t)ncols); P.scale.resize((size_t)ncols); colarr.resize((size_t)ncols);
+    pfor(nthr, ncols, [&](int64_t k0, int64_t k1) {
+        for (int64_t k = k0; k < k1; ++k) {
+            const AinvBlock& b = blocks[(size_t)colsrc[(size_t)k].first];
+            const int32_t q = colsrc[(size_t)k].second;
+            int64_t dst = P.zcolptr[(size_t)k];
+            for (int64_t e = b.colptr[q]; e < b.colptr[q + 1]; ++e, ++dst) {
+                const int64_t gr = b.row_g[e];
+                P.zrow[(size_t)dst] = unk[gr - (int64_t)rlo * ni];
+                P.zhat[(size_t)dst] = b.zhat[e];
+                ent_z[(size_t)dst] = scale_of(gr) * b.zhat[e];
+                ent_row_arr[(size_t)dst] = arr_of(gr);
+            }
+            P.pivots[(size_t)k] = b.piv[q];
+            P.scale[(size_t)k] = scale_of(b.col_g[q]);
+            colarr[(size_t)k] = arr_of(b.col_g[q]);
+            P.piv[colarr[(size_t)k]] = b.piv[q];
+        }
+    });
+    P.nnz_off = ntot - ncols;
     if ((int64_t)colarr.size() != P.n_owned) return Status::err(PCG_ERR_ARG, "internal: owned column count mismatch");
     const int64_t hoff = (int64_t)P.halo * pitch;        // array index of owned element 0
     for (int64_t r : ent_row_arr)        // entries in the southern halo rows only with halo-AINV across ranks
         if (r < hoff - (int64_t)P.halo_w * pitch) return Status::err(PCG_ERR_ARG, "internal: Z entry outside the owned rows");
 
+    stage("export + Z values");
     // ---- SELL of Z^T rows: row (column j of Z) = entries k ascending
     const int64_t nown = P.owned_elements();
     {
@@ -466,15 +462,18 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         for (int64_t e = 0; e < nown; ++e) rp[e + 1] += rp[e];
         std::vector<int32_t> cols(rp[nown]);
         std::vector<double> vals(rp[nown]);
-        for (size_t q = 0; q < colarr.size(); ++q) {
-            int64_t dst = rp[colarr[q] - hoff];
-            for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e, ++dst) {
-                cols[dst] = (int32_t)ent_row_arr[e];
-                vals[dst] = ent_z[e];
+        pfor(nthr, (int64_t)colarr.size(), [&](int64_t q0, int64_t q1) {
+            for (int64_t q = q0; q < q1; ++q) {
+                int64_t dst = rp[colarr[q] - hoff];
+                for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e, ++dst) {
+                    cols[dst] = (int32_t)ent_row_arr[e];
+                    vals[dst] = ent_z[e];
+                }
             }
-        }
-        pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.halo, P.ZT);
+        });
+        pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.halo, P.ZT, nthr);
     }
+    stage("pack Z^T");
     // ---- SELL of Z rows: row i = entries z_ij over columns j ascending (owned rows only; with
     // halo-AINV across ranks the northern neighbour's columns follow this rank's, ascending)
     {
@@ -486,7 +485,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
                     const int64_t gr = north.row_g[e];
                     ncol_arr.push_back(arr_of(north.col_g[q]));
                     nrow_arr.push_back(arr_of(gr));
-                    nz.push_back((1.0 / std::sqrt(diag_of(gr))) * north.zhat[e]);
+                    nz.push_back(scale_of(gr) * north.zhat[e]);
                 }
         for (int64_t r : nrow_arr)
             if (r < hoff) return Status::err(PCG_ERR_ARG, "internal: northern Z entry below the owned rows");
@@ -497,22 +496,46 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
         std::vector<int32_t> cols(rp[nown]);
         std::vector<double> vals(rp[nown]);
-        for (size_t q = 0; q < colarr.size(); ++q)        // columns visited in ascending order
-            for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e) {
-                if (ent_row_arr[e] < hoff) continue;       // a southern halo row: rank-1's Z row
-                int64_t r = ent_row_arr[e] - hoff;
-                cols[fill[r]] = (int32_t)colarr[q];
-                vals[fill[r]] = ent_z[e];
-                fill[r]++;
-            }
+        // transpose with the ascending column order per row kept: thread t owns the rows
+        // [R_t, R_t+1) and visits, in ascending order, the columns that can hold entries of them
+        // (a column's entries are at rows <= the column, so columns from the first row >= R_t on)
+        {
+            const int64_t nc = (int64_t)colarr.size();
+            int64_t reach = 0;                             // largest column - row distance of an entry
+            for (int64_t q = 0; q < nc; ++q)
+                for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e) reach = std::max(reach, colarr[q] - ent_row_arr[e]);
+            int T = (nc < 100000) ? 1 : nthr;
+            std::vector<std::thread> pool;
+            auto part = [&](int t) {
+                const int64_t R0 = nown * t / T, R1 = nown * (t + 1) / T;
+                const int64_t q0 = std::lower_bound(colarr.begin(), colarr.end(), R0 + hoff) - colarr.begin();
+                for (int64_t q = q0; q < nc; ++q) {
+                    bool below = false;                    // some entry of this column lies below R1
+                    for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e) {
+                        if (ent_row_arr[e] < hoff) continue;   // a southern halo row: rank-1's Z row
+                        const int64_t r = ent_row_arr[e] - hoff;
+                        if (r < R1) below = true;
+                        if (r < R0 || r >= R1) continue;
+                        cols[fill[r]] = (int32_t)colarr[q];
+                        vals[fill[r]] = ent_z[e];
+                        fill[r]++;
+                    }
+                    if (!below && colarr[q] - hoff >= R1 + reach) break;   // past Z's reach
+                }
+            };
+            for (int t = 1; t < T; ++t) pool.emplace_back(part, t);
+            part(0);
+            for (auto& th : pool) th.join();
+        }
         for (size_t m = 0; m < nrow_arr.size(); ++m) {     // north columns, ascending
             int64_t r = nrow_arr[m] - hoff;
             cols[fill[r]] = (int32_t)ncol_arr[m];
             vals[fill[r]] = nz[m];
             fill[r]++;
         }
-        pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.halo, P.Z);
+        pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.halo, P.Z, nthr);
     }
+    stage("pack Z");
     // ---- FSAI DIA form: each owned column's entries at consecutive columns of the
     // same grid row i-1, i-2, ... (no land, wrap or N-S link inside the chain) -> diagonals
     if (P.precond == PCG_PRECOND_FSAI && P.fsai_q > 0) {
