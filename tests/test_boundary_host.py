@@ -208,3 +208,21 @@ def test_host_pb2_with_tau_and_partitions(seed):
     p = synth.random_grid(17, 14, seed, sigma=True, periodic=seed != 2)
     _pb2_equal(p, 0.02 + 1e-9, 4)
     _pb2_equal(p, 0.0, 3, ainv_parts=3, ainv_halo=2)
+
+
+@pytest.mark.parametrize("name,fill", [("cfg3", 0), ("cfg3", 5), ("cfg4", 0)])
+def test_threaded_ainv_equals_one_thread(name, fill):
+    """The column wavefront of ainv.cpp (several threads, each column waiting only on the finished
+    columns it reads) builds bitwise the single-thread factor, and at cfg3 the oracle's."""
+    p = synth.config(name)
+    tau = 0.0 if fill else 0.1 + 1e-9
+    one = pcg.Plan(p.cE, p.cN, p.mask, tau=tau, ainv_fill=fill, setup_threads=1).export_zhat()
+    for th in (3, 8):
+        many = pcg.Plan(p.cE, p.cN, p.mask, tau=tau, ainv_fill=fill, setup_threads=th).export_zhat()
+        assert all(np.array_equal(a, b) for a, b in zip(one, many))
+    if name == "cfg3":
+        A = oracle.assemble(p)
+        M = oracle.ainv(A, tau, fill=fill)
+        cp, row, zh, pv, sc = one
+        assert np.array_equal(cp, M.colptr) and np.array_equal(row, M.row) and np.array_equal(zh, M.zhat)
+        assert np.array_equal(pv, M.pivots)
