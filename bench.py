@@ -139,18 +139,38 @@ PAPER_CONTEXT = {"paper_gflops_gpu": 87.0, "paper_gflops_cpu": 1.43,
                  "note": "context only: different matrix (no mask/wrap), precision and, for AINV, preconditioner"}
 
 
-def cpu_oracle_sample(p, tau, n_iter):
-    """The oracle as it stands (plain C, single thread) on a bounded sample of the workload:
-    assembly + AINV setup, then n_iter PCG iterations (tol = 0)."""
+def cpu_info():
+    """Host cores (os.sched_getaffinity: the ones this process may use) and the CPU model name."""
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return cores, model
+
+
+def cpu_oracle_sample(p, tau, n_iter, mode="plain", threads=None):
+    """The oracle as it stands on a bounded sample of the workload: assembly + AINV setup, then
+    n_iter PCG iterations (tol = 0).  mode "plain": single thread (sequential sums); "chunked":
+    all host cores (OpenMP rows, fixed 4096-element chunk partials; thread-count independent)."""
     import oracle
     from paper_1210_1878_b200 import synth
+    if threads is not None:
+        os.environ["OMP_NUM_THREADS"] = str(threads)
     t0 = time.perf_counter()
     A = oracle.assemble(p)
     M = oracle.ainv(A, tau)
     t1 = time.perf_counter()
     b = A.apply(A.from_grid(synth.xstar(p)))
     t2 = time.perf_counter()
-    r = oracle.pcg(A, b, "ainv", M, 0.0, maxit=n_iter)
+    r = oracle.pcg(A, b, "ainv", M, 0.0, maxit=n_iter, mode=mode)
     t3 = time.perf_counter()
     return {"setup_s": t1 - t0, "iters": r.iterations, "solve_s": t3 - t2}
 
@@ -163,11 +183,12 @@ def run_reference(args):
     from paper_1210_1878_b200 import synth
     p = synth.config(args.config)
     n_iter = args.ref_iters
+    cores, model = cpu_info()
     for _ in range(args.warmup if args.warmup <= 1 else 1):
-        cpu_oracle_sample(p, args.tau, 2)
+        cpu_oracle_sample(p, args.tau, 2, mode="chunked")
     tot_it, tot_s, setup = 0, 0.0, []
     for _ in range(args.steps):
-        r = cpu_oracle_sample(p, args.tau, n_iter)
+        r = cpu_oracle_sample(p, args.tau, n_iter, mode="chunked")
         tot_it += r["iters"]
         tot_s += r["solve_s"]
         setup.append(r["setup_s"])
@@ -178,9 +199,10 @@ def run_reference(args):
             "data": "synthetic",
             "config": {"workload": WORKLOAD, "precond": "ainv", "tau": args.tau,
                        "sample": f"{n_iter} PCG iterations (tol=0) per step after the oracle's own setup"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{args.config}, {n_iter} plain-order PCG iterations per step, "
-                                       f"setup {np.mean(setup):.2f} s excluded"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "cpu_model": model, "kind": "oracle",
+                             "sample": f"{args.config}, {n_iter} PCG iterations per step on all {cores} host cores "
+                                       f"(CHUNKED mode: OpenMP rows, 4096-element chunk partials), setup "
+                                       f"{np.mean(setup):.2f} s excluded"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -344,10 +366,15 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        r = cpu_oracle_sample(p, args.tau, args.cpu_iters)
-        cpu = {"value": r["iters"] / r["solve_s"], "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"{args.config} full grid, {r['iters']} plain-order PCG iterations (tol=0) after the "
-                         f"oracle's own assembly+AINV ({r['setup_s']:.2f} s, excluded)"}
+        cores, model = cpu_info()
+        r = cpu_oracle_sample(p, args.tau, args.cpu_iters, mode="chunked")
+        r1 = cpu_oracle_sample(p, args.tau, max(10, args.cpu_iters // 5), mode="plain")
+        cpu = {"value": r["iters"] / r["solve_s"], "unit": UNIT, "cores": cores, "cpu_model": model, "kind": "oracle",
+               "sample": f"{args.config} full grid, {r['iters']} PCG iterations (tol=0) on all {cores} host cores "
+                         f"(CHUNKED mode: OpenMP rows, 4096-element chunk partials) after the oracle's own "
+                         f"assembly+AINV ({r['setup_s']:.2f} s, excluded)",
+               "single_core": {"value": r1["iters"] / r1["solve_s"], "unit": UNIT, "cores": 1,
+                               "sample": f"{r1['iters']} plain-order iterations, one thread"}}
 
     # launches per solve: prologue 4 (prep, init, K2, K3) + WHILE bodies of PCG_BODY_ITERS (8)
     # iterations x 3 + epilogue 2; the resident-strip driver: prologue + 1 + epilogue

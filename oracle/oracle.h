@@ -34,7 +34,12 @@ extern "C" {
 
 enum { ORC_OK = 0, ORC_ERR_ARG = 1, ORC_ERR_NOT_SPD = 2, ORC_ERR_BREAKDOWN = 3, ORC_ERR_NOMEM = 6 };
 enum { ORC_PRECOND_AINV = 0, ORC_PRECOND_JACOBI = 1, ORC_PRECOND_NONE = 2 };
-enum { ORC_MODE_PLAIN = 0, ORC_MODE_CANONICAL = 1 };
+enum { ORC_MODE_PLAIN = 0, ORC_MODE_CANONICAL = 1, ORC_MODE_CHUNKED = 2 };
+/* CHUNKED: PLAIN arithmetic for every row (A x, Z^T r, Z t, updates), dot products as
+ * partials of fixed 4096-element chunks of the natural order (each summed left to right), the
+ * partials then summed left to right in chunk order.  Rows and chunks run on all host cores
+ * (OpenMP); the result does not depend on the thread count.  Used for the all-cores CPU baseline
+ * (SURVEY §8(d)). */
 
 typedef struct orc_problem orc_problem;
 typedef struct orc_ainv orc_ainv;

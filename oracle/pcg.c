@@ -150,6 +150,47 @@ static double plain_dot(int64_t n, const double* a, const double* b) {
     return acc;
 }
 
+/* CHUNKED dot: chunk partials (4096 consecutive unknowns, left to right), then the partials
+ * left to right; independent of the thread count */
+#define ORC_CHUNK 4096
+static double chunked_dot(int64_t n, const double* a, const double* b, double* part) {
+    const int64_t nc = (n + ORC_CHUNK - 1) / ORC_CHUNK;
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < nc; ++c) {
+        const int64_t k1 = (c + 1) * ORC_CHUNK < n ? (c + 1) * ORC_CHUNK : n;
+        double acc = 0.0;
+        for (int64_t k = c * ORC_CHUNK; k < k1; ++k) acc = acc + a[k] * b[k];
+        part[c] = acc;
+    }
+    double acc = 0.0;
+    for (int64_t c = 0; c < nc; ++c) acc = acc + part[c];
+    return acc;
+}
+
+/* the PLAIN row operations on all cores (each row's arithmetic unchanged) */
+static void par_apply(const orc_problem* P, const double* x, double* y) {
+#pragma omp parallel for schedule(static)
+    for (int64_t p = 0; p < P->n; ++p) {
+        double acc = 0.0;
+        for (int64_t e = P->rowptr[p]; e < P->rowptr[p + 1]; ++e) acc = acc + P->val[e] * x[P->col[e]];
+        y[p] = acc;
+    }
+}
+static void par_ainv_apply(const orc_ainv* R, const double* r, double* s, double* t) {
+#pragma omp parallel for schedule(static)
+    for (int64_t j = 0; j < R->n; ++j) {
+        double acc = 0.0;
+        for (int64_t e = R->colptr[j]; e < R->colptr[j + 1]; ++e) acc = acc + R->z[e] * r[R->row[e]];
+        t[j] = acc / R->p[j];
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < R->n; ++i) {
+        double acc = 0.0;
+        for (int64_t e = R->rptr[i]; e < R->rptr[i + 1]; ++e) acc = acc + R->rval[e] * t[R->rcol[e]];
+        s[i] = acc;
+    }
+}
+
 int orc_pcg(const orc_problem* P, const orc_ainv* R, const orc_pcg_opts* o, const double* b,
             const double* x0, double tol, int32_t maxit, double* x, double* hist, orc_pcg_report* rep) {
     memset(rep, 0, sizeof *rep);
@@ -158,6 +199,8 @@ int orc_pcg(const orc_problem* P, const orc_ainv* R, const orc_pcg_opts* o, cons
     if (!(tol >= 0.0) || maxit < 0) return rep->status = ORC_ERR_ARG;
     if (o->precond == ORC_PRECOND_AINV && !R) return rep->status = ORC_ERR_ARG;
     int canonical = o->mode == ORC_MODE_CANONICAL;
+    const int chunked = o->mode == ORC_MODE_CHUNKED;
+    double* cpart = chunked ? (double*)malloc(sizeof(double) * ((n + ORC_CHUNK - 1) / ORC_CHUNK + 1)) : NULL;
     canon C = {0};
     if (canonical) {
         if (o->pitch < P->ni || o->block < 32 || o->block > 1024 || (o->block & (o->block - 1)) ||
@@ -172,8 +215,8 @@ int orc_pcg(const orc_problem* P, const orc_ainv* R, const orc_pcg_opts* o, cons
         for (int r = 0; r < o->parts; ++r) if (C.rb[r + 1] - C.rb[r] > maxrows) maxrows = C.rb[r + 1] - C.rb[r];
         C.partial = (double*)malloc(sizeof(double) * ((maxrows + 1) * (o->pitch / o->block + 2)));
     }
-#define DOT(a, b) (canonical ? canon_dot(&C, (a), (b)) : plain_dot(n, (a), (b)))
-#define APPLY_A(in, out) (canonical ? canon_apply(P, (in), (out)) : orc_apply(P, (in), (out)))
+#define DOT(a, b) (canonical ? canon_dot(&C, (a), (b)) : chunked ? chunked_dot(n, (a), (b), cpart) : plain_dot(n, (a), (b)))
+#define APPLY_A(in, out) (canonical ? canon_apply(P, (in), (out)) : chunked ? par_apply(P, (in), (out)) : orc_apply(P, (in), (out)))
     size_t sz = sizeof(double) * (n ? n : 1);
     double *r = malloc(sz), *s = malloc(sz), *d = malloc(sz), *q = malloc(sz), *t = malloc(sz);
 
@@ -182,6 +225,7 @@ int orc_pcg(const orc_problem* P, const orc_ainv* R, const orc_pcg_opts* o, cons
     do {                                                                          \
         if (o->precond == ORC_PRECOND_AINV) {                                     \
             if (canonical) canon_ainv_apply(R, (rin), (sout), t);                 \
+            else if (chunked) par_ainv_apply(R, (rin), (sout), t);                \
             else orc_ainv_apply(R, (rin), (sout));                                \
         } else if (o->precond == ORC_PRECOND_JACOBI) {                            \
             for (int64_t k_ = 0; k_ < n; ++k_) (sout)[k_] = (rin)[k_] / P->diag[k_]; \
@@ -220,7 +264,9 @@ int orc_pcg(const orc_problem* P, const orc_ainv* R, const orc_pcg_opts* o, cons
             for (int64_t k = 0; k < n; ++k) x[k] = fma(alpha, d[k], x[k]);
             for (int64_t k = 0; k < n; ++k) r[k] = fma(-alpha, q[k], r[k]);
         } else {
+#pragma omp parallel for schedule(static) if (chunked)
             for (int64_t k = 0; k < n; ++k) x[k] = x[k] + alpha * d[k];
+#pragma omp parallel for schedule(static) if (chunked)
             for (int64_t k = 0; k < n; ++k) r[k] = r[k] - alpha * q[k];
         }
         /* line 7 */
@@ -231,7 +277,10 @@ int orc_pcg(const orc_problem* P, const orc_ainv* R, const orc_pcg_opts* o, cons
         double beta = rho_new / rho;
         /* line 8 (with s, not r: reading R6) */
         if (canonical) for (int64_t k = 0; k < n; ++k) d[k] = fma(beta, d[k], s[k]);
-        else for (int64_t k = 0; k < n; ++k) d[k] = s[k] + beta * d[k];
+        else {
+#pragma omp parallel for schedule(static) if (chunked)
+            for (int64_t k = 0; k < n; ++k) d[k] = s[k] + beta * d[k];
+        }
         rho = rho_new;
         it++;
         h = sqrt(rr) / nb;
@@ -245,7 +294,7 @@ int orc_pcg(const orc_problem* P, const orc_ainv* R, const orc_pcg_opts* o, cons
     for (int64_t k = 0; k < n; ++k) r[k] = b[k] - q[k];
     rep->true_rel_residual = sqrt(DOT(r, r)) / nb;
 done:
-    free(r); free(s); free(d); free(q); free(t);
+    free(r); free(s); free(d); free(q); free(t); free(cpart);
     if (canonical) { free(C.rb); free(C.vals); free(C.partial); }
     return rep->status;
 #undef DOT

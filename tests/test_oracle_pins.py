@@ -581,3 +581,33 @@ def test_cg1_special_cases():
     assert np.linalg.norm(rq.x - xd) / np.linalg.norm(xd) < 1e-10
     rz = oracle.pcg(A, np.zeros(A.n), "ainv", oracle.ainv(A, 0.1 + 1e-9), 1e-10, method="cg1")
     assert rz.iterations == 0 and np.all(rz.x == 0.0)
+
+
+def test_chunked_mode_thread_invariant_and_within_plain_band():
+    """The all-cores CPU baseline (CHUNKED: plain row arithmetic, 4096-element chunk partials
+    summed in chunk order) gives bitwise the same solve with 1 and with 4 OpenMP threads, and
+    stays within the plain-order band of SURVEY §8(c.4) (x to 1e-9 at tol 1e-12)."""
+    import json
+    import subprocess
+    import sys
+    code = ("import sys, json, numpy as np; sys.path.insert(0, %r); import oracle; "
+            "from paper_1210_1878_b200 import synth; p = synth.config('cfg2'); A = oracle.assemble(p); "
+            "b = A.apply(A.from_grid(synth.xstar(p))); M = oracle.ainv(A, 0.1 + 1e-9); "
+            "r = oracle.pcg(A, b, 'ainv', M, 1e-12, mode='chunked'); "
+            "print(json.dumps({'k': r.iterations, 'x': r.x.tolist()[:4000:97], 'h': r.hist.tolist()}))"
+            % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    outs = []
+    for th in ("1", "4"):
+        env = dict(os.environ, OMP_NUM_THREADS=th)
+        out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, check=True)
+        outs.append(json.loads(out.stdout.strip().splitlines()[-1]))
+    assert outs[0] == outs[1]
+    p = synth.config("cfg2")
+    A = oracle.assemble(p)
+    b = A.apply(A.from_grid(synth.xstar(p)))
+    M = oracle.ainv(A, 0.1 + 1e-9)
+    ch = oracle.pcg(A, b, "ainv", M, 1e-12, mode="chunked")
+    pl = oracle.pcg(A, b, "ainv", M, 1e-12)
+    assert abs(ch.iterations - pl.iterations) <= max(2, 0.01 * pl.iterations)
+    assert np.linalg.norm(ch.x - pl.x) / np.linalg.norm(pl.x) <= 1e-9
+    assert ch.true_rel_residual <= 1e-12

@@ -61,6 +61,7 @@ for name in a.configs.split(","):
                "err_vs_xstar": err, "time_to_solution_ms": best * 1e3, "iter_per_s": k / best,
                "us_per_iter": best / k * 1e6, "alg_bytes_per_iter_MB": bpi / 1e6,
                "alg_GBps": bpi * k / best / 1e9, "frac_of_measured_hbm": bpi * k / best / 1e9 / peak,
+               "bytes_to_solution_GB": bpi * k / 1e9, "driver": rep.get("driver_name"),
                "z_per_col": rep["nnz_z"] / max(rep["n_ocean"], 1), "setup_s": rep["setup_s"],
                "setup_wall_s": setup_wall, "device_MB": S.device_bytes / 1e6, "gen_s": gen_s}
         print(json.dumps(out), flush=True)
