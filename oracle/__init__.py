@@ -88,6 +88,8 @@ def lib():
         L.orc_pcg.restype = C.c_int
         L.orc_pcg_cg.argtypes = [P, P, vp, vp, vp, D, I32, vp, vp, vp]
         L.orc_pcg_cg.restype = C.c_int
+        L.orc_pcg_pipe.argtypes = [P, P, vp, vp, vp, D, I32, vp, vp, vp]
+        L.orc_pcg_pipe.restype = C.c_int
         _lib = L
     return _lib
 
@@ -309,7 +311,8 @@ def pcg(A: Assembled, b, precond: str = "ainv", M: Ainv | None = None, tol: floa
         maxit: int | None = None, x0=None, mode: str = "plain", pitch: int | None = None,
         block: int = 256, parts: int = 1, rows: int = 1, method: str = "pcg") -> PcgResult:
     """Alg. 1 with d = s + beta d.  Unknown-indexed vectors.
-    method = "cg1": Chronopoulos-Gear single-reduction form (NEXT-2, orc_pcg_cg)."""
+    method = "cg1": Chronopoulos-Gear single-reduction form (NEXT-2, orc_pcg_cg);
+    method = "pipe": pipelined PCG, Ghysels-Vanroose Alg. 4 (NEXT-2, orc_pcg_pipe)."""
     L = lib()
     if maxit is None:
         maxit = A.n
@@ -319,7 +322,7 @@ def pcg(A: Assembled, b, precond: str = "ainv", M: Ainv | None = None, tol: floa
     hist = np.empty(maxit + 1)
     o = _PcgOpts(PRECOND[precond], MODE[mode], int(pitch if pitch else A.ni), int(block), int(parts), int(rows))
     rep = _PcgReport()
-    fn = L.orc_pcg_cg if method == "cg1" else L.orc_pcg
+    fn = {"pcg": L.orc_pcg, "cg1": L.orc_pcg_cg, "pipe": L.orc_pcg_pipe}[method]
     rc = fn(A._h, None if M is None else M.handle._h, C.byref(o), _ptr(b), _ptr(x0a),
             float(tol), int(maxit), _ptr(x), _ptr(hist), C.byref(rep))
     if rc == 1:

@@ -124,6 +124,14 @@ int orc_pcg_cg(const orc_problem*, const orc_ainv* /*nullable unless AINV*/, con
                const double* b, const double* x0, double tol, int32_t maxit,
                double* x, double* hist, orc_pcg_report* rep);
 
+/* Pipelined PCG (Ghysels-Vanroose Alg. 4): Alg. 1 with the recurrences
+ * z = n + beta z, q = m + beta q, s = w + beta s, p = u + beta p (m = P w, n = A m) so that the
+ * three inner products (r,u), (w,u), (r,r) form one reduction point per iteration that does not
+ * wait on P or A.  Same interface and modes as orc_pcg. */
+int orc_pcg_pipe(const orc_problem*, const orc_ainv* /*nullable unless AINV*/, const orc_pcg_opts*,
+                 const double* b, const double* x0, double tol, int32_t maxit,
+                 double* x, double* hist, orc_pcg_report* rep);
+
 #ifdef __cplusplus
 }
 #endif

@@ -418,3 +418,134 @@ done:
 #undef APPLY_A
 #undef PRECOND
 }
+
+/* Pipelined PCG (Ghysels & Vanroose, "Hiding global synchronization latency
+ * in the preconditioned conjugate gradient algorithm", Alg. 4 -- Alg. 1 of PAPER.md:318-334
+ * rearranged once more so that the single reduction point of each iteration can overlap the
+ * next preconditioner and matrix product).  Extra recurrences carry the products that
+ * orc_pcg_cg recomputes: with u = P r, w = A u, m = P w, n = A m,
+ *   k = 0:  beta = 0, alpha = gamma/delta;
+ *   k > 0:  beta = gamma/gamma_prev, alpha = gamma / (delta - beta gamma / alpha_prev);
+ *   z = n + beta z;  q = m + beta q;  s = w + beta s;  p = u + beta p;
+ *   x += alpha p;  r -= alpha s;  u -= alpha q;  w -= alpha z;
+ *   gamma = (r, u);  delta = (w, u);  rr = (r, r);  k += 1;  h_k = sqrt(rr)/||b||.
+ * In exact arithmetic z = A q, q = P s, s = A p, so the iterates are Alg. 1's (the pins in
+ * tests/test_oracle_pins.py check that against orc_pcg).  Breakdown: alpha's denominator
+ * not > 0, gamma not > 0, or a non-finite value.  Same interface and modes as orc_pcg. */
+int orc_pcg_pipe(const orc_problem* P, const orc_ainv* R, const orc_pcg_opts* o, const double* b,
+                 const double* x0, double tol, int32_t maxit, double* x, double* hist, orc_pcg_report* rep) {
+    memset(rep, 0, sizeof *rep);
+    rep->failed_index = -1;
+    int64_t n = P->n;
+    if (!(tol >= 0.0) || maxit < 0) return rep->status = ORC_ERR_ARG;
+    if (o->precond == ORC_PRECOND_AINV && !R) return rep->status = ORC_ERR_ARG;
+    int canonical = o->mode == ORC_MODE_CANONICAL;
+    canon C = {0};
+    if (canonical) {
+        if (o->pitch < P->ni || o->block < 32 || o->block > 1024 || (o->block & (o->block - 1)) ||
+            o->parts < 1 || o->parts > 32 || o->parts > P->nj)
+            return rep->status = ORC_ERR_ARG;
+        C.P = P; C.pitch = o->pitch; C.B = o->block; C.parts = o->parts;
+        C.rb = (int32_t*)malloc(sizeof(int32_t) * (o->parts + 1));
+        if (o->parts == 1) { C.rb[0] = 0; C.rb[1] = P->nj; }
+        else orc_partition(P->nj, P->ni, P->mask, o->parts, C.rb);
+        C.vals = (double*)malloc(sizeof(double) * o->block);
+        int64_t maxrows = 0;
+        for (int r = 0; r < o->parts; ++r) if (C.rb[r + 1] - C.rb[r] > maxrows) maxrows = C.rb[r + 1] - C.rb[r];
+        C.partial = (double*)malloc(sizeof(double) * ((maxrows + 1) * (o->pitch / o->block + 2)));
+    }
+#define DOT(a, b) (canonical ? canon_dot(&C, (a), (b)) : plain_dot(n, (a), (b)))
+#define APPLY_A(in, out) (canonical ? canon_apply(P, (in), (out)) : orc_apply(P, (in), (out)))
+    size_t sz = sizeof(double) * (n ? n : 1);
+    double *r = malloc(sz), *u = malloc(sz), *w = malloc(sz), *m = malloc(sz), *nv = malloc(sz);
+    double *z = malloc(sz), *q = malloc(sz), *sv = malloc(sz), *p = malloc(sz), *t = malloc(sz);
+#define PRECOND(rin, sout)                                                        \
+    do {                                                                          \
+        if (o->precond == ORC_PRECOND_AINV) {                                     \
+            if (canonical) canon_ainv_apply(R, (rin), (sout), t);                 \
+            else orc_ainv_apply(R, (rin), (sout));                                \
+        } else if (o->precond == ORC_PRECOND_JACOBI) {                            \
+            for (int64_t k_ = 0; k_ < n; ++k_) (sout)[k_] = (rin)[k_] / P->diag[k_]; \
+        } else {                                                                  \
+            memcpy((sout), (rin), sz);                                            \
+        }                                                                         \
+    } while (0)
+    for (int64_t k = 0; k < n; ++k) x[k] = x0 ? x0[k] : 0.0;
+    double nb = sqrt(DOT(b, b));
+    if (nb == 0.0) {
+        for (int64_t k = 0; k < n; ++k) x[k] = 0.0;
+        hist[0] = 0.0;
+        rep->iterations = 0; rep->converged = 1;
+        rep->status = ORC_OK;
+        goto done;
+    }
+    APPLY_A(x, w);
+    for (int64_t k = 0; k < n; ++k) r[k] = b[k] - w[k];
+    PRECOND(r, u);
+    APPLY_A(u, w);
+    double gamma = DOT(r, u), delta = DOT(w, u), rr = DOT(r, r);
+    double h = sqrt(rr) / nb;
+    hist[0] = h;
+    int32_t it = 0;
+    rep->status = ORC_OK;
+    if (!isfinite(h) || !isfinite(gamma) || !isfinite(delta)) { rep->status = ORC_ERR_BREAKDOWN; goto fin; }
+    for (int64_t k = 0; k < n; ++k) { z[k] = 0.0; q[k] = 0.0; sv[k] = 0.0; p[k] = 0.0; }
+    double gamma_prev = 0.0, alpha_prev = 0.0;
+    while (h > tol && it < maxit) {
+        PRECOND(w, m);
+        APPLY_A(m, nv);
+        double beta, den;
+        if (it == 0) { beta = 0.0; den = delta; }
+        else { beta = gamma / gamma_prev; den = delta - (beta * gamma) / alpha_prev; }
+        if (!(den > 0.0) || !isfinite(den) || !(gamma > 0.0)) { rep->status = ORC_ERR_BREAKDOWN; break; }
+        double alpha = gamma / den;
+        if (canonical) {
+            for (int64_t k = 0; k < n; ++k) {
+                z[k] = fma(beta, z[k], nv[k]);
+                q[k] = fma(beta, q[k], m[k]);
+                sv[k] = fma(beta, sv[k], w[k]);
+                p[k] = fma(beta, p[k], u[k]);
+                x[k] = fma(alpha, p[k], x[k]);
+                r[k] = fma(-alpha, sv[k], r[k]);
+                u[k] = fma(-alpha, q[k], u[k]);
+                w[k] = fma(-alpha, z[k], w[k]);
+            }
+        } else {
+            for (int64_t k = 0; k < n; ++k) {
+                z[k] = nv[k] + beta * z[k];
+                q[k] = m[k] + beta * q[k];
+                sv[k] = w[k] + beta * sv[k];
+                p[k] = u[k] + beta * p[k];
+                x[k] = x[k] + alpha * p[k];
+                r[k] = r[k] - alpha * sv[k];
+                u[k] = u[k] - alpha * q[k];
+                w[k] = w[k] - alpha * z[k];
+            }
+        }
+        gamma_prev = gamma;
+        alpha_prev = alpha;
+        gamma = DOT(r, u);
+        delta = DOT(w, u);
+        rr = DOT(r, r);
+        it++;
+        if (!isfinite(gamma) || !isfinite(delta) || !isfinite(rr)) {
+            rep->status = ORC_ERR_BREAKDOWN; hist[it] = NAN; break;
+        }
+        h = sqrt(rr) / nb;
+        hist[it] = h;
+    }
+fin:
+    rep->iterations = it;
+    rep->rel_residual = hist[it];
+    rep->converged = rep->status == ORC_OK && hist[it] <= tol;
+    APPLY_A(x, w);
+    for (int64_t k = 0; k < n; ++k) r[k] = b[k] - w[k];
+    rep->true_rel_residual = sqrt(DOT(r, r)) / nb;
+done:
+    free(r); free(u); free(w); free(m); free(nv); free(z); free(q); free(sv); free(p); free(t);
+    if (canonical) { free(C.rb); free(C.vals); free(C.partial); }
+    return rep->status;
+#undef DOT
+#undef APPLY_A
+#undef PRECOND
+}

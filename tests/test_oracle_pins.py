@@ -544,9 +544,10 @@ def test_generator_matches_survey_counts():
 
 
 # ----------------------------------------------- Chronopoulos-Gear single-reduction PCG (NEXT-2)
+@pytest.mark.parametrize("method", ["cg1", "pipe"])
 @pytest.mark.parametrize("name", ["cfg1", "cfg2"])
 @pytest.mark.parametrize("precond", ["ainv", "jacobi"])
-def test_cg1_matches_alg1(name, precond):
+def test_cg1_matches_alg1(name, precond, method):
     """The single-reduction recurrences produce Alg. 1's iterates in exact arithmetic, so against
     the (separately pinned) Alg. 1 oracle: iterations within max(2, 1 %), x within 1e-9 at tol
     1e-12, both residuals converged.  A wrong sign or index in the alpha/beta recurrence, or a
@@ -556,30 +557,38 @@ def test_cg1_matches_alg1(name, precond):
     M = oracle.ainv(A, 0.1 + 1e-9) if precond == "ainv" else None
     b = A.apply(A.from_grid(synth.xstar(p)))
     r1 = oracle.pcg(A, b, precond, M, 1e-12)
-    r2 = oracle.pcg(A, b, precond, M, 1e-12, method="cg1")
-    assert r2.converged and r2.true_rel_residual < 2e-12
+    r2 = oracle.pcg(A, b, precond, M, 1e-12, method=method)
+    # pipelined CG's extra recurrences (u, w updated instead of recomputed) let the recurrence
+    # residual drift from b - A x by a few ulps x kappa (the residual gap of Cools et al. 2018;
+    # DESIGN.md reading R29): the true residual is held to 10 tol there, 2 tol otherwise
+    assert r2.converged and r2.true_rel_residual < (1e-11 if method == "pipe" else 2e-12)
     assert abs(r2.iterations - r1.iterations) <= max(2, r1.iterations // 100)
     assert np.linalg.norm(r2.x - r1.x) / np.linalg.norm(r1.x) < 1e-9
+    # the first iterations, before rounding has had time to separate the recurrences, follow
+    # Alg. 1's residual history closely (a wrong sign in one update shows at k = 1 or 2)
+    k = min(8, r1.iterations)
+    assert np.allclose(r2.hist[:k + 1], r1.hist[:k + 1], rtol=1e-8, atol=0)
 
 
-def test_cg1_special_cases():
+@pytest.mark.parametrize("method", ["cg1", "pipe"])
+def test_cg1_special_cases(method):
     """tau = 0 (exact inverse): one iteration; dense solve on a tiny random grid; cfg1 (d = 4, a
     power of two): Jacobi and no preconditioner are bitwise identical in this form too; b = 0."""
     p = synth.config("cfg1")
     A = oracle.assemble(p)
     b = A.apply(A.from_grid(synth.xstar(p)))
-    r0 = oracle.pcg(A, b, "ainv", oracle.ainv(A, 0.0), 1e-10, method="cg1")
+    r0 = oracle.pcg(A, b, "ainv", oracle.ainv(A, 0.0), 1e-10, method=method)
     assert r0.iterations == 1 and r0.converged
-    rj = oracle.pcg(A, b, "jacobi", None, 1e-10, method="cg1")
-    rn = oracle.pcg(A, b, "none", None, 1e-10, method="cg1")
+    rj = oracle.pcg(A, b, "jacobi", None, 1e-10, method=method)
+    rn = oracle.pcg(A, b, "none", None, 1e-10, method=method)
     assert rj.iterations == rn.iterations and np.array_equal(rj.x, rn.x) and np.array_equal(rj.hist, rn.hist)
     q = synth.random_grid(11, 9, 4)
     Q = oracle.assemble(q)
     bq = Q.apply(Q.from_grid(synth.xstar(q, 3)))
-    rq = oracle.pcg(Q, bq, "ainv", oracle.ainv(Q, 0.1 + 1e-9), 1e-13, method="cg1")
+    rq = oracle.pcg(Q, bq, "ainv", oracle.ainv(Q, 0.1 + 1e-9), 1e-13, method=method)
     xd = np.linalg.solve(Q.dense(), bq)
     assert np.linalg.norm(rq.x - xd) / np.linalg.norm(xd) < 1e-10
-    rz = oracle.pcg(A, np.zeros(A.n), "ainv", oracle.ainv(A, 0.1 + 1e-9), 1e-10, method="cg1")
+    rz = oracle.pcg(A, np.zeros(A.n), "ainv", oracle.ainv(A, 0.1 + 1e-9), 1e-10, method=method)
     assert rz.iterations == 0 and np.all(rz.x == 0.0)
 
 
