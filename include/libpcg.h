@@ -79,6 +79,14 @@ typedef enum {
                                         two inner products share one reduction point (kernels KA,
                                         K3, KC).  One rank, factored preconditioners (AINV, P_B2,
                                         FSAI through the ELL form); otherwise PCG_ERR_ARG. */
+#define PCG_FLAG_PIPELINED 16  /* pipelined PCG (Ghysels & Vanroose Alg. 4, the
+                                  oracle's orc_pcg_pipe): the reduction of (r,u), (w,u), (r,r) is
+                                  consumed one phase later, so it overlaps the next application of
+                                  the preconditioner (kernels KPA, KPB, KPC); across ranks the rank
+                                  sums ride in the halo exchange of m = P w.  Factored
+                                  preconditioners only, block-local AINV across ranks, not with
+                                  PCG_FLAG_SINGLE_REDUCTION; otherwise PCG_ERR_ARG.  The stop test
+                                  and breakdown are Alg. 1's (reading R29). */
 
 /* "grid": geometry of this rank's part of the problem. */
 typedef struct {

@@ -30,6 +30,7 @@ FLAG_HOST_LOOP = 1
 FLAG_COMM_PATH = 2
 FLAG_LOCAL_RANKS = 4
 FLAG_SINGLE_REDUCTION = 8
+FLAG_PIPELINED = 16
 
 
 class PcgError(RuntimeError):

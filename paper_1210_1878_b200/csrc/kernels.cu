@@ -134,6 +134,7 @@ __device__ void fin_bb(const KArgs& A, double bb) {
     sc->nb = __dsqrt_rn(bb);
     sc->bzero = sc->nb == 0.0;
     sc->alpha = 0.0; sc->beta = 0.0; sc->k = 0; sc->status = kStOk; sc->xpend = 0;
+    sc->pstage = 0;
     sc->active = 1;                       // provisional: decided after s0 (fin_init)
 }
 
@@ -1484,12 +1485,206 @@ __global__ void __launch_bounds__(kBlock) kc_cg_kernel(const KArgs A, const int 
     }
 }
 
+// ---- pipelined PCG (NEXT-2; Ghysels-Vanroose Alg. 4, oracle orc_pcg_pipe) -------------------
+// Per iteration: KPA t = Dhat^-1 Z^T w, KPB m = Z t (m = P w), KPC n = A m and
+//   z = n + beta z, q = m + beta q, s = w + beta s, p = u + beta p,
+//   x += alpha p, r -= alpha s, u -= alpha q, w -= alpha z, (r,u) (w,u) (r,r).
+// The reduction KPC starts is not needed until the next KPC: one rank, KPA's block 0 forms the
+// three canonical final sums and the scalars (history, stop test, alpha, beta) while the other
+// blocks stream t; several ranks, the rank sums ride in the allgather fused with the m halo
+// exchange after KPB.  Scalars: rho = gamma of the previous iteration, alpha = alpha_prev.
+__device__ void pipe_fin(const KArgs& A, double gamma, double delta, double rr) {
+    DevScalars* sc = A.sc;
+    const bool init = sc->pstage == 0;
+    int k = 0;
+    if (!init) {
+        k = sc->k + 1;
+        sc->k = k;
+    }
+    if (!isfinite(gamma) || !isfinite(delta) || !isfinite(rr)) {
+        put_hist(A, k, init ? __ddiv_rn(__dsqrt_rn(rr), sc->nb) : NAN);
+        stop(A, kStBreakdown);
+        return;
+    }
+    const double h = __ddiv_rn(__dsqrt_rn(rr), sc->nb);
+    put_hist(A, k, h);
+    if (!((h > sc->tol) && (k < sc->maxit))) {
+        sc->active = 0;
+        set_cond(A, 0);
+        return;
+    }
+    double beta, den;
+    if (init) {
+        beta = 0.0;
+        den = delta;
+    } else {
+        beta = __ddiv_rn(gamma, sc->rho);
+        den = __dadd_rn(delta, -__ddiv_rn(__dmul_rn(beta, gamma), sc->alpha));
+    }
+    if (!(den > 0.0) || !isfinite(den) || !(gamma > 0.0)) {
+        stop(A, kStBreakdown);
+        return;
+    }
+    sc->alpha = __ddiv_rn(gamma, den);
+    sc->beta = beta;
+    sc->rho = gamma;
+    sc->pstage = 1;
+}
+
+// units from the dynamic ticket, no reduction (the ticket is reset by the next KPC)
+template <class Body>
+__device__ __forceinline__ void ticket_units(const KArgs& A, unsigned long long* ticket, Body body) {
+    __shared__ long long s_next;
+    const int64_t U = n_units(A);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) s_next = (long long)atomicAdd(ticket, 1ull);
+    __syncthreads();
+    int64_t u = s_next;
+    while (u < U) {
+        __syncthreads();                                   // everyone has read s_next
+        unsigned long long tk = 0;
+        if (threadIdx.x == 0) tk = atomicAdd(ticket, 1ull);
+        Unit W = unit_of(A, u);
+        if (A.landskip) W.live = W.inrow && ((__ldg(A.ocean + ((int64_t)W.j * A.nbx + W.bx) * kWarps + warp) >> lane) & 1u);
+        body(W);
+        if (threadIdx.x == 0) s_next = (long long)tk;
+        __syncthreads();
+        u = s_next;
+    }
+}
+
+__global__ void __launch_bounds__(kBlock, PCG_MINB_K2) kpa_kernel(const KArgs A) {
+    pdl_wait();
+    if (!is_active(A)) return;
+    if (!A.multi && blockIdx.x == 0) {
+        const int64_t U = n_units(A);
+        const double g = final_sum<PCG_FINAL_NB_K3>(A.partial[0], U);
+        const double dl = final_sum<PCG_FINAL_NB_K3>(A.partial[1], U);
+        const double rr = final_sum<PCG_FINAL_NB_K3>(A.partial[2], U);
+        if (threadIdx.x == 0) pipe_fin(A, g, dl, rr);
+        __syncthreads();
+    }
+    const double* __restrict__ w = A.q;
+    ticket_units(A, &A.sc->ticket[1], [&](const Unit& W) {
+        if (W.live) {
+            auto gat = [&](int32_t g) { return __ldg(w + g); };
+            const double acc = A.zt.col16 ? ell_row16(A.zt, W.a - A.hoff, W.a, gat) : ell_row(A.zt, W.a - A.hoff, gat);
+            A.t[W.a] = __ddiv_rn(acc, A.piv[W.a]);
+        }
+    });
+    pdl_trigger();
+}
+
+__global__ void __launch_bounds__(kBlock, PCG_MINB_K3) kpb_kernel(const KArgs A) {
+    pdl_wait();
+    if (!is_active(A)) return;
+    const double* __restrict__ t = A.t;
+    ticket_units(A, &A.sc->ticket[2], [&](const Unit& W) {
+        if (W.live) {
+            auto gat = [&](int32_t g) { return __ldg(t + g); };
+            A.pm[W.a] = A.z.col16 ? ell_row16(A.z, W.a - A.hoff, W.a, gat) : ell_row(A.z, W.a - A.hoff, gat);
+        }
+    });
+    pdl_trigger();
+}
+
+// init: w = A u and the three dots of the prologue; otherwise the iteration's updates
+__global__ void __launch_bounds__(kBlock) kpc_kernel(const KArgs A, const int init) {
+    pdl_wait();
+    if (!is_active(A)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {          // KPA / KPB have completed
+        A.sc->ticket[1] = 0;
+        A.sc->ticket[2] = 0;
+    }
+    extern __shared__ double ws[];
+    const double alpha = A.sc->alpha, beta = A.sc->beta;
+    double* __restrict__ r = A.r[0];
+    double* __restrict__ u = A.s;
+    double* __restrict__ w = A.q;
+    const int64_t U = n_units(A);
+    int k = 0;
+    for (int64_t un = blockIdx.x; un < U; un += gridDim.x, ++k) {
+        const Unit W = unit_of(A, un);
+        double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+        if (W.valid) {
+            const int64_t a = W.a;
+            bool land;
+            if (init) {
+                const double ax = stencil(A, u, a, W.i, land);
+                const double wv = land ? 0.0 : ax;
+                w[a] = wv;
+                const double rv = r[a], uv = u[a];
+                v0 = __dmul_rn(rv, uv);
+                v1 = __dmul_rn(wv, uv);
+                v2 = __dmul_rn(rv, rv);
+            } else {
+                const double nv = stencil(A, A.pm, a, W.i, land);
+                if (!land) {
+                    const double zn = __fma_rn(beta, A.pz[a], nv);
+                    const double qn = __fma_rn(beta, A.pq[a], A.pm[a]);
+                    const double sn = __fma_rn(beta, A.d[0][a], w[a]);
+                    const double pn = __fma_rn(beta, A.p[a], u[a]);
+                    A.x[a] = __fma_rn(alpha, pn, A.x[a]);
+                    const double rv = __fma_rn(-alpha, sn, r[a]);
+                    const double uv = __fma_rn(-alpha, qn, u[a]);
+                    const double wv = __fma_rn(-alpha, zn, w[a]);
+                    A.pz[a] = zn;
+                    A.pq[a] = qn;
+                    A.d[0][a] = sn;
+                    A.p[a] = pn;
+                    r[a] = rv;
+                    u[a] = uv;
+                    w[a] = wv;
+                    v0 = __dmul_rn(rv, uv);
+                    v1 = __dmul_rn(wv, uv);
+                    v2 = __dmul_rn(rv, rv);
+                }
+            }
+        }
+        v0 = warp_tree(v0);
+        v1 = warp_tree(v1);
+        v2 = warp_tree(v2);
+        if ((threadIdx.x & 31) == 0) {
+            ws[(k * 3 + 0) * kWarps + (threadIdx.x >> 5)] = v0;
+            ws[(k * 3 + 1) * kWarps + (threadIdx.x >> 5)] = v1;
+            ws[(k * 3 + 2) * kWarps + (threadIdx.x >> 5)] = v2;
+        }
+    }
+    pdl_trigger();
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        k = 0;
+        for (int64_t un = blockIdx.x; un < U; un += gridDim.x, ++k) {
+            const int64_t m = (int64_t)(A.nloc - 1 - (int32_t)(un / A.nbx)) * A.nbx + (un % A.nbx);
+#pragma unroll
+            for (int n = 0; n < 3; ++n) {
+                double v = lane < kWarps ? ws[(k * 3 + n) * kWarps + lane] : 0.0;
+                v = warp_tree(v);
+                if (lane == 0) A.partial[n][m] = v;
+            }
+        }
+    }
+    if (!A.multi) return;                                // one rank: the next KPA's block 0 sums
+    if (!count_block(&A.sc->counter[0])) return;
+    const double g = final_sum(A.partial[0], U);
+    const double dl = final_sum(A.partial[1], U);
+    const double rr = final_sum(A.partial[2], U);
+    if (threadIdx.x == 0) {
+        A.sc->counter[0] = 0;
+        A.sc->loc[0] = g;
+        A.sc->loc[1] = dl;
+        A.sc->loc[2] = rr;
+    }
+}
+
 // prep: zero land entries of x and b (land is not an unknown, reading R20), zero d[0] everywhere
 __global__ void __launch_bounds__(kBlock) prep_kernel(const KArgs A) {
     const int64_t n = (int64_t)(A.nloc + 2 * A.halo) * A.pitch;
     for (int64_t a = (int64_t)blockIdx.x * kBlock + threadIdx.x; a < n; a += (int64_t)gridDim.x * kBlock) {
         A.d[0][a] = 0.0;
-        if (A.p) A.p[a] = 0.0;                               // CG-CG search direction
+        if (A.p) A.p[a] = 0.0;                               // CG-CG / pipelined search direction
+        if (A.pipe) { A.pz[a] = 0.0; A.pq[a] = 0.0; A.pm[a] = 0.0; }
         const int64_t row = a / A.pitch;
         if (row >= A.halo && row < A.halo + A.nloc) {
             if (signbit(A.cN[a])) { A.x[a] = 0.0; A.b[a] = 0.0; }
@@ -1595,6 +1790,9 @@ __global__ void scalar_kernel(const KArgs A, const int step) {
                 if (sc->active) cg_alpha_beta(A, rank_tree(A.gath, P, 0), 0);
             }
             break;
+        case kSsPipe:
+            if (sc->active) pipe_fin(A, rank_tree(A.gath, P, 0), rank_tree(A.gath, P, 1), rank_tree(A.gath, P, 2));
+            break;
         case kSsTrue: {
             const double tot = rank_tree(A.gath, P, 3);
             sc->true_rel = sc->bzero ? 0.0 : __ddiv_rn(__dsqrt_rn(tot), sc->nb);
@@ -1687,6 +1885,7 @@ void configure_kernels(KArgs& A, int sms) {
     allow_smem(k2_diag_kernel, row_smem(A, A.g_kd, 2));
     allow_smem(ka_cg_kernel, row_smem(A, A.g_k2, 1));
     allow_smem(kc_cg_kernel, row_smem(A, A.g_row, 1));
+    allow_smem(kpc_kernel, row_smem(A, A.g_row, 3));
     allow_smem(init_residual_kernel, row_smem(A, A.g_row, 1));
     allow_smem(true_residual_kernel, row_smem(A, A.g_row, 1));
 }
@@ -1736,6 +1935,11 @@ void launch_k1(const KArgs& A, int par, cudaStream_t st) {
 void launch_kc(const KArgs& A, int par, int init, cudaStream_t st) {
     (void)par;
     launch_pdl(A, kc_cg_kernel, A.g_row, kBlock, row_smem(A, A.g_row, 1), st, A, init);
+}
+void launch_kpa(const KArgs& A, cudaStream_t st) { launch_pdl(A, kpa_kernel, A.g_k2, kBlock, 0, st, A); }
+void launch_kpb(const KArgs& A, cudaStream_t st) { launch_pdl(A, kpb_kernel, A.g_k3, kBlock, 0, st, A); }
+void launch_kpc(const KArgs& A, int init, cudaStream_t st) {
+    launch_pdl(A, kpc_kernel, A.g_row, kBlock, row_smem(A, A.g_row, 3), st, A, init);
 }
 void launch_k2_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
     if (A.cgcg && !init) {

@@ -19,6 +19,7 @@ struct DevScalars {
     double red[4];        // global reductions: [0] (d,q)  [1] (s,r)  [2] (r,r)  [3] (b,b) / true (r,r)
     double loc[4];        // this rank's block-tree sums (multi-rank path)
     int32_t k, maxit, active, status, bzero, xpend, guard;
+    int32_t pstage;       // pipelined PCG: 0 = the pending reduction is the prologue's, 1 = an iteration's
     double rhop[2];       // redundant-sum mode: rho of the iterations of parity 0 / 1 (rhop[1] = inf before the first)
     uint32_t counter[4];  // last-block detection, reset by the last block
     unsigned long long ticket[4];   // dynamic unit assignment, reset by the last block
@@ -106,6 +107,11 @@ struct KArgs {
     int32_t red_gamma;                // Jacobi / none (one rank): K1 without a last block, K2's blocks form (d, q)
     int32_t cgcg;                     // Chronopoulos-Gear single-reduction PCG (NEXT-2; KA, K3, KC)
     double* p;                        // its search direction p (s = A p lives in d[0] / d[1], w in q, u in s)
+    // Pipelined PCG (NEXT-2, Ghysels-Vanroose Alg. 4; KPA / KPB / KPC): u in s, w in q, r in r[0],
+    // p in p, s = A p in d[0]; z = A q, q = P s and m = P w in their own arrays (n = A m is formed
+    // in KPC's registers and never stored)
+    int32_t pipe;
+    double *pz, *pq, *pm;
     void* l2_base;                    // persisting L2 access-policy window of the iteration kernels
     size_t l2_bytes;                  // (0: none)
     float l2_ratio;
@@ -128,6 +134,11 @@ void launch_k2_ainv(const KArgs& A, int par, int init, cudaStream_t st);
 void launch_k3_ainv(const KArgs& A, int par, int init, cudaStream_t st);
 void launch_k2_diag(const KArgs& A, int par, int init, int none, cudaStream_t st);
 void launch_kc(const KArgs& A, int par, int init, cudaStream_t st);   // CG-CG: w = A u, (w, u), alpha / beta
+// pipelined PCG: KPA t = Dhat^-1 Z^T w (+ the pending reduction's scalars, one rank); KPB m = Z t;
+// KPC n = A m, the eight vector updates, (r,u) (w,u) (r,r)  (init: w = A u and the three dots)
+void launch_kpa(const KArgs& A, cudaStream_t st);
+void launch_kpb(const KArgs& A, cudaStream_t st);
+void launch_kpc(const KArgs& A, int init, cudaStream_t st);
 // solve prologue / epilogue
 void launch_prep(const KArgs& A, cudaStream_t st);
 void launch_init_residual(const KArgs& A, cudaStream_t st);       // r0 = b - A x0 -> r[1], (b,b)
@@ -136,7 +147,8 @@ void launch_true_residual(const KArgs& A, cudaStream_t st);       // ||b - A x||
 void launch_apply(const KArgs& A, const double* x_arr, double* y_arr, cudaStream_t st);   // y = A x
 // multi-rank scalar steps (one thread) after an allgather of DevScalars::loc
 enum ScalarStep : int32_t { kSsBB = 0, kSsGamma = 1, kSsInit = 2, kSsIter = 3, kSsTrue = 4,
-                            kSsCgInit = 5, kSsCgIter = 6 };   // Chronopoulos-Gear: (delta, gamma, rr) at once
+                            kSsCgInit = 5, kSsCgIter = 6,     // Chronopoulos-Gear: (delta, gamma, rr) at once
+                            kSsPipe = 7 };                    // pipelined: (gamma, delta, rr) -> alpha, beta
 void launch_scalar(const KArgs& A, int step, cudaStream_t st);
 void launch_set_cond(cudaGraphConditionalHandle h, cudaStream_t st);
 void launch_extrapolate(const double* xt, const double* xm, double* x0, int64_t n, cudaStream_t st);

@@ -39,7 +39,8 @@ struct pcg_ctx {
     double* hot = nullptr;             // the eight per-iteration vectors, contiguous
     size_t hot_bytes = 0;
     char* ovf_base = nullptr;          // Z / Z^T overflow arrays, directly in front of `hot`
-    double* pvec = nullptr;            // Chronopoulos-Gear search direction
+    double* pvec = nullptr;            // Chronopoulos-Gear / pipelined search direction
+    double *pz = nullptr, *pq = nullptr, *pm = nullptr;   // pipelined PCG: z, q, m
     size_t ovf_bytes = 0;
     double* dia = nullptr;             // FSAI DIA diagonals
     int32_t *sched2 = nullptr, *soff2 = nullptr, *sched3 = nullptr, *soff3 = nullptr;   // static schedules
@@ -128,14 +129,14 @@ size_t& l2_limit_before(int device) {
 // One rank: the resident-strip loop kernel (rs.cu) when setup found it eligible (its shared-
 // memory ranges fit); PCG_RS=0 disables it.
 bool use_rs(const pcg_ctx* c) {
-    if (c->multi || c->A.cgcg || !c->A.rs.on || (c->plan.flags & PCG_FLAG_HOST_LOOP)) return false;
+    if (c->multi || c->A.cgcg || c->A.pipe || !c->A.rs.on || (c->plan.flags & PCG_FLAG_HOST_LOOP)) return false;
     const char* e = getenv("PCG_RS");
     return !(e && atoi(e) == 0);
 }
 
 bool use_fused(const pcg_ctx* c) {
     if (use_rs(c)) return false;
-    if (c->multi || c->A.cgcg || (c->plan.flags & PCG_FLAG_HOST_LOOP)) return false;
+    if (c->multi || c->A.cgcg || c->A.pipe || (c->plan.flags & PCG_FLAG_HOST_LOOP)) return false;
     if (const char* e = getenv("PCG_FUSED")) return atoi(e) != 0;
     // measured with the current graph (redundant sums, 8-iteration body): factored preconditioners
     // -- cfg1 (32 units) 14.5 vs 14.6 us/it, cfg2 (149 units) 20.5-20.7 fused vs 16.9-18.4 graph,
@@ -169,7 +170,7 @@ bool use_graph(const pcg_ctx* c) {
 //     last owned row -> rank+1's row H-1 (one row each way)
 //   QR (halo-AINV, after K1): rows [H+nloc-ws, H+nloc) of q and r[par] -> rank+1's rows [H-w, H)
 //   T  (halo-AINV, after K2): rows [H, H+halo_t_send) of t -> rank-1's rows [H+nloc, H+nloc+halo_t)
-enum class Ex { None, Allgather, HaloX, HaloSAllgather, AllgatherQR, QR, HaloT, HaloS };
+enum class Ex { None, Allgather, HaloX, HaloSAllgather, AllgatherQR, QR, HaloT, HaloS, HaloMAllgather };
 struct Xfer {
     double* arr;                     // this context's array
     int64_t off, n;                  // elements
@@ -183,8 +184,9 @@ XferList exchange_list(pcg_ctx* c, Ex ex, int par, double* halo_arr = nullptr) {
     const Plan& P = c->plan;
     const int64_t pt = P.pitch, H = P.halo, nl = P.nloc;
     XferList L;
-    L.allgather = ex == Ex::Allgather || ex == Ex::HaloSAllgather || ex == Ex::AllgatherQR;
-    double* row1 = halo_arr ? halo_arr : ex == Ex::HaloX ? c->x : (ex == Ex::HaloS || ex == Ex::HaloSAllgather) ? c->s : nullptr;
+    L.allgather = ex == Ex::Allgather || ex == Ex::HaloSAllgather || ex == Ex::AllgatherQR || ex == Ex::HaloMAllgather;
+    double* row1 = halo_arr ? halo_arr : ex == Ex::HaloX ? c->x : (ex == Ex::HaloS || ex == Ex::HaloSAllgather) ? c->s
+                 : ex == Ex::HaloMAllgather ? c->pm : nullptr;
     if (row1) {
         if (P.rank > 0) {
             L.send_south.push_back({row1, H * pt, pt});
@@ -264,6 +266,14 @@ std::vector<Step> prologue_steps(const pcg_ctx* c) {
             }
             return s;
         }
+        if (c->A.pipe) {                                 // w0 = A u0 and (r,u) (w,u) (r,r) (pipelined)
+            if (multi) {
+                s.push_back({Ex::HaloSAllgather, nullptr});
+                s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsInit, x->st); }});
+            }
+            s.push_back({Ex::None, [](pcg_ctx* x) { launch_kpc(x->A, 1, x->st); }});
+            return s;                    // the first iteration's allgather carries the rank sums
+        }
     } else {
         s.push_back({Ex::None, [none](pcg_ctx* x) { launch_k2_diag(x->A, 1, 1, none, x->st); }});
     }
@@ -279,6 +289,16 @@ std::vector<Step> iteration_steps(const pcg_ctx* c, int par) {
     const bool multi = c->multi, ainv = c->plan.factored();
     const bool none = c->plan.precond == PCG_PRECOND_NONE;
     const bool hx = multi && ainv && c->plan.halo_w > 0;
+    if (c->A.pipe) {                     // pipelined: KPA, KPB, (m halo + allgather), KPC
+        s.push_back({Ex::None, [](pcg_ctx* x) { launch_kpa(x->A, x->st); }});
+        s.push_back({Ex::None, [](pcg_ctx* x) { launch_kpb(x->A, x->st); }});
+        if (multi) {
+            s.push_back({Ex::HaloMAllgather, nullptr});
+            s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsPipe, x->st); }});
+        }
+        s.push_back({Ex::None, [](pcg_ctx* x) { launch_kpc(x->A, 0, x->st); }});
+        return s;
+    }
     if (c->A.cgcg) {                     // Chronopoulos-Gear: KA, K3, (u halo), KC, ONE allgather
         s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k2_ainv(x->A, par, 0, x->st); }});
         s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k3_ainv(x->A, par, 0, x->st); }});
@@ -616,7 +636,7 @@ Status setup_rs(pcg_ctx* c) {
     KArgs& A = c->A;
     const Plan& P = c->plan;
     A.rs = RsDev{};
-    if (c->multi || A.cgcg || A.dia_q > 0) return Status::ok();
+    if (c->multi || A.cgcg || A.pipe || A.dia_q > 0) return Status::ok();
     if (const char* e = getenv("PCG_RS")) if (atoi(e) == 0) return Status::ok();
     const bool fac = P.factored();
     if (fac && (!A.zt.col16 || !A.z.col16)) return Status::ok();
@@ -1093,6 +1113,23 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         if (Status st = dalloc(c, c->pvec, nel); !st) return st;
         A.p = c->pvec;
     }
+    // pipelined PCG (NEXT-2): the same conditions
+    A.pipe = 0;
+    A.pz = A.pq = A.pm = nullptr;
+    if (P.flags & PCG_FLAG_PIPELINED) {
+        if (!P.factored() || (c->multi && P.halo_w > 0) || (P.flags & PCG_FLAG_SINGLE_REDUCTION))
+            return Status::err(PCG_ERR_ARG, "pcg_setup: PCG_FLAG_PIPELINED needs a factored preconditioner "
+                               "(AINV, P_B2, FSAI), across ranks block-local AINV (ainv_halo = 0), and excludes "
+                               "PCG_FLAG_SINGLE_REDUCTION");
+        A.pipe = 1;
+        A.redundant = 0;
+        A.dia_q = 0;
+        if (Status st = dalloc(c, c->pvec, nel); !st) return st;
+        if (Status st = dalloc(c, c->pz, nel); !st) return st;
+        if (Status st = dalloc(c, c->pq, nel); !st) return st;
+        if (Status st = dalloc(c, c->pm, nel); !st) return st;
+        A.p = c->pvec; A.pz = c->pz; A.pq = c->pq; A.pm = c->pm;
+    }
     // algorithmic bytes per launch: N_o ocean points, z off-diagonals per column
     const double No = (double)P.n_owned, z = No > 0 ? (double)P.nnz_off / No : 0.0;
     c->bytes_k[0] = 64.0 * No;
@@ -1389,7 +1426,8 @@ pcg_status pcg_kernel_times(pcg_ctx* c, int32_t n_iter, double* ms_out, double* 
     auto body = [&]() -> Status {
         if (c->multi) return Status::err(PCG_ERR_ARG, "pcg_kernel_times: single rank only");
         if (!c->solved_once) return Status::err(PCG_ERR_ARG, "pcg_kernel_times: call pcg_solve first (uses its b)");
-        if (c->A.cgcg) return Status::err(PCG_ERR_ARG, "pcg_kernel_times: not for PCG_FLAG_SINGLE_REDUCTION");
+        if (c->A.cgcg || c->A.pipe)
+            return Status::err(PCG_ERR_ARG, "pcg_kernel_times: not for PCG_FLAG_SINGLE_REDUCTION / PCG_FLAG_PIPELINED");
         CU(cudaSetDevice(c->device));
         // restart from x = 0 on the stored b with tol = 0, time n_iter iterations kernel by kernel
         std::memset(c->h_sc, 0, sizeof(DevScalars));
