@@ -45,8 +45,8 @@ def workload_name(args):
     if args.config == "cfg4" and args.precond == "ainv" and args.tau == 0.1 and args.tol == 1e-10 and args.method == "pcg":
         return WORKLOAD
     pc = {"ainv": "AINV(tau=%g)" % args.tau, "jacobi": "Jacobi", "fsai": "FSAI(q=%d, the paper's P)" % args.fsai_q}[args.precond]
-    return "%s: %s %s to ||r||/||b|| <= %g" % (args.config, pc, "Chronopoulos-Gear PCG" if args.method == "cg1" else "PCG",
-                                               args.tol)
+    form = {"cg1": "Chronopoulos-Gear PCG", "pipe": "pipelined PCG"}.get(args.method, "PCG")
+    return "%s: %s %s to ||r||/||b|| <= %g" % (args.config, pc, form, args.tol)
 
 
 def fallback_peak():
@@ -223,8 +223,9 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=150)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=60)
-    ap.add_argument("--method", default="pcg", choices=["pcg", "cg1"],
-                    help="cg1: Chronopoulos-Gear single-reduction PCG (one allgather per iteration across ranks)")
+    ap.add_argument("--method", default="pcg", choices=["pcg", "cg1", "pipe"],
+                    help="cg1: Chronopoulos-Gear single-reduction PCG (one allgather per iteration across ranks); "
+                         "pipe: pipelined PCG (the reduction overlaps the next preconditioner application)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -246,7 +247,7 @@ def main():
     p = synth.config(args.config)
     t0 = time.perf_counter()
     S = pcg.Solver(p.cE, p.cN, p.mask, tau=args.tau, precond=args.precond, group=group, device=local,
-                   fsai_q=args.fsai_q, flags=pcg.FLAG_SINGLE_REDUCTION if args.method == "cg1" else 0)
+                   fsai_q=args.fsai_q, flags={"cg1": pcg.FLAG_SINGLE_REDUCTION, "pipe": pcg.FLAG_PIPELINED}.get(args.method, 0))
     setup_wall = time.perf_counter() - t0
     rows = slice(S.j_begin, S.j_end)
     xs = torch.from_numpy(np.ascontiguousarray(synth.xstar(p)[rows])).cuda()
@@ -380,13 +381,16 @@ def main():
     # iterations x 3 + epilogue 2; the resident-strip driver: prologue + 1 + epilogue
     per_iter = 3 if args.precond in ("ainv", "fsai") else 2
     pro = 4 if args.precond in ("ainv", "fsai") else 3
-    if args.method == "cg1":
-        pro = 5                                                  # + KC's w0 = A u0 (alpha0)
+    extra = 0
+    if args.method in ("cg1", "pipe"):
+        pro = 5                                                  # + KC / KPC's w0 = A u0 and its dots
+    if args.method == "pipe":
+        extra = 1                                                # the KPA that takes the stop decision
     if rs_used:
         launches = len(iters) * (pro + 1 + 2)                    # prologue, the loop kernel, epilogue
     elif world == 1:
         body = max(2, int(os.environ.get("PCG_BODY_ITERS", "8")) & ~1)
-        launches = sum(pro + per_iter * body * math.ceil(k / body) + 2 for k in iters)
+        launches = sum(pro + per_iter * body * math.ceil((k + extra) / body) + 2 for k in iters)
     else:
         launches = None
     if rank == 0:

@@ -26,6 +26,7 @@ ap.add_argument("--fsai", default="", help="comma list of FSAI bandwidths q (the
 ap.add_argument("--fill", default="", help="comma list of P_B2 fills m (AINV with tau = 0, m entries per column)")
 ap.add_argument("--tol", type=float, default=None)
 ap.add_argument("--cg1", action="store_true", help="Chronopoulos-Gear single-reduction PCG (NEXT-2)")
+ap.add_argument("--pipe", action="store_true", help="pipelined PCG (NEXT-2)")
 ap.add_argument("--reps", type=int, default=3)
 a = ap.parse_args()
 TOL = {"cfg1": 1e-10, "cfg2": 1e-10, "cfg3": 1e-10, "cfg4": 1e-10, "cfg5": 1e-12}
@@ -43,7 +44,7 @@ for name in a.configs.split(","):
         S = pcg.Solver(p.cE, p.cN, p.mask, tau=0.0 if pc == "pb2" else (tau if pc != "fsai" else 0.1),
                        precond="ainv" if pc == "pb2" else pc, fsai_q=int(tau) if pc == "fsai" else 4,
                        ainv_fill=int(tau) if pc == "pb2" else 0,
-                       flags=pcg.FLAG_SINGLE_REDUCTION if a.cg1 else 0)
+                       flags=pcg.FLAG_SINGLE_REDUCTION if a.cg1 else pcg.FLAG_PIPELINED if a.pipe else 0)
         setup_wall = time.perf_counter() - t0
         b = S.apply_operator(xs)
         tol = a.tol if a.tol is not None else TOL[name]
@@ -55,7 +56,7 @@ for name in a.configs.split(","):
         err = float(torch.linalg.norm(x - xs) / torch.linalg.norm(xs))
         bpi = rep["bytes_per_iter"]
         out = {"config": name, "grid": [p.ni, p.nj], "n_ocean": rep["n_ocean"], "precond": pc,
-               "method": "cg1" if a.cg1 else "pcg",
+               "method": "cg1" if a.cg1 else "pipe" if a.pipe else "pcg",
                ({"fsai": "fsai_q", "pb2": "fill"}.get(pc, "tau")): (int(tau) if pc in ("fsai", "pb2") else tau), "tol": tol,
                "iterations": k, "converged": rep["converged"], "true_rel_residual": rep["true_rel_residual"],
                "err_vs_xstar": err, "time_to_solution_ms": best * 1e3, "iter_per_s": k / best,
