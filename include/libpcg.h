@@ -87,6 +87,17 @@ typedef enum {
                                   preconditioners only, block-local AINV across ranks, not with
                                   PCG_FLAG_SINGLE_REDUCTION; otherwise PCG_ERR_ARG.  The stop test
                                   and breakdown are Alg. 1's (reading R29). */
+#define PCG_FLAG_DEVICE_COMM 32  /* multi-rank NCCL path: every reduction's rank sums are gathered
+                                    inside the reducing kernel -- its last block stores them into
+                                    every rank's symmetric NCCL window over NVLink (ncclMemAlloc +
+                                    ncclCommWindowRegister, peer pointers from ncclGetPeerPointer)
+                                    and runs the scalar step (rank tree, alpha / beta, stop test)
+                                    inline -- instead of a host-enqueued ncclAllGather and a
+                                    scalar kernel (bitwise the same results).  Needs
+                                    nccl_comm with every rank load/store reachable (one NVLink
+                                    domain, else PCG_ERR_COMM); not with PCG_FLAG_LOCAL_RANKS
+                                    (PCG_ERR_ARG).  pcg_setup is then collective over the
+                                    communicator (window registration). */
 
 /* "grid": geometry of this rank's part of the problem. */
 typedef struct {
@@ -277,6 +288,15 @@ pcg_status pcg_comm_unique_id(char* out128);
 pcg_status pcg_comm_init_rank(const char* id128, int32_t nranks, int32_t rank, int32_t device,
                               void** comm);
 pcg_status pcg_comm_destroy(void* comm);
+
+/* Diagnostics: the device-comm protocol of PCG_FLAG_DEVICE_COMM (dc_publish / dc_collect, DESIGN.md
+ * §6.3) run by nranks virtual ranks -- the blocks of one cooperative launch on the current device,
+ * windows carved from one buffer -- for `rounds` reductions.  In round k rank r contributes the four
+ * values v(k, r, q) of a fixed hash of (seed, k, r, q) (odd rounds through the split publish /
+ * collect form); out[(k * nranks + r) * 4 + q] (host, rounds * nranks * 4 doubles) receives rank
+ * r's canonical rank tree of slot q.  Every rank must obtain the same sums, equal
+ * to the host's tree over the same values.  1 <= nranks <= 32, rounds >= 1, else PCG_ERR_ARG. */
+pcg_status pcg_devcomm_selftest(int32_t nranks, int32_t rounds, uint64_t seed, double* out);
 
 #ifdef __cplusplus
 }

@@ -31,6 +31,7 @@ FLAG_COMM_PATH = 2
 FLAG_LOCAL_RANKS = 4
 FLAG_SINGLE_REDUCTION = 8
 FLAG_PIPELINED = 16
+FLAG_DEVICE_COMM = 32
 
 
 class PcgError(RuntimeError):
@@ -74,7 +75,7 @@ DRIVERS = {0: "graph", 1: "loop", 2: "resident", 3: "host_loop", 4: "nccl_graph"
 EXPORTS = ["pcg_setup", "pcg_solve", "pcg_solve_host", "pcg_solve_local_ranks", "pcg_free", "pcg_last_error", "pcg_apply_operator",
            "pcg_apply_preconditioner", "pcg_extrapolate", "pcg_partition", "pcg_layout", "pcg_kernel_times", "pcg_device_bytes", "pcg_loop_time",
            "pcg_plan_build", "pcg_plan_free", "pcg_plan_counts", "pcg_plan_export_zhat",
-           "pcg_comm_unique_id", "pcg_comm_init_rank", "pcg_comm_destroy"]
+           "pcg_comm_unique_id", "pcg_comm_init_rank", "pcg_comm_destroy", "pcg_devcomm_selftest"]
 
 _lib = None
 
@@ -110,6 +111,7 @@ def lib():
     L.pcg_comm_unique_id.argtypes = [C.c_char_p]
     L.pcg_comm_init_rank.argtypes = [C.c_char_p, i32, i32, i32, C.POINTER(vp)]
     L.pcg_comm_destroy.argtypes = [vp]
+    L.pcg_devcomm_selftest.argtypes = [i32, i32, C.c_uint64, vp]
     for f in EXPORTS:
         if f not in ("pcg_free", "pcg_last_error", "pcg_device_bytes", "pcg_plan_free"):
             getattr(L, f).restype = C.c_int
@@ -129,6 +131,14 @@ def _ptr(a):
     if isinstance(a, np.ndarray):
         return a.ctypes.data
     return a.data_ptr()
+
+
+def devcomm_selftest(nranks: int, rounds: int, seed: int = 1) -> np.ndarray:
+    """pcg_devcomm_selftest: [rounds][nranks][4] rank trees of the device-comm protocol run by
+    nranks virtual ranks on the current device."""
+    out = np.empty((rounds, nranks, 4))
+    _check(lib().pcg_devcomm_selftest(int(nranks), int(rounds), int(seed), _ptr(out)), None, "pcg_devcomm_selftest")
+    return out
 
 
 def partition(ni: int, nj: int, mask, parts: int) -> np.ndarray:

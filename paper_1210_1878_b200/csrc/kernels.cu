@@ -37,6 +37,7 @@
 #include "internal.h"
 #include "kernels.h"
 #include "dev_common.cuh"
+#include "dev_comm.cuh"
 
 namespace pcg {
 
@@ -75,22 +76,31 @@ __device__ __forceinline__ double final_sum_all(const double* partial, int64_t G
 }
 
 // tree over the per-rank sums in rank order, zero padded to 32
-__device__ double rank_tree(const double* gath, int nranks, int slot) {
-    double u[32];
+// (u[l] += u[l + off] for off = 16, 8, 4, 2, 1, as warp_tree).  Evaluated depth first: leaf t of
+// the in-order walk is rank bitrev5(t), and after leaf t the stack merges (left + right) once per
+// trailing one bit of t -- the same additions with the same operands, in 6 live registers instead
+// of 32, so the reduction kernels that run it in their last block keep their register budget.
+__device__ __forceinline__ double rank_tree(const double* gath, int nranks, int slot) {
+    double st[6];
+    int sp = 0;
 #pragma unroll
-    for (int l = 0; l < 32; ++l) u[l] = l < nranks ? gath[l * 4 + slot] : 0.0;
+    for (int t = 0; t < 32; ++t) {
+        const int l = (int)(__brev((unsigned)t) >> 27);
+        double v = l < nranks ? gath[l * 4 + slot] : 0.0;
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1)
-#pragma unroll
-        for (int l = 0; l + off < 32; ++l) u[l] = __dadd_rn(u[l], u[l + off]);
-    return u[0];
+        for (int c = t; c & 1; c >>= 1) v = __dadd_rn(st[--sp], v);
+        st[sp++] = v;
+    }
+    return st[0];
 }
 
-__device__ __forceinline__ void set_cond(const KArgs& A, int v) {
+template <class KA>
+__device__ __forceinline__ void set_cond(const KA& A, int v) {
     if (A.use_cond) cudaGraphSetConditional(A.cond, (unsigned)v);
 }
 
-__device__ __forceinline__ void stop(const KArgs& A, int status) {
+template <class KA>
+__device__ __forceinline__ void stop(const KA& A, int status) {
     DevScalars* sc = A.sc;
     sc->status = status;
     sc->active = 0;
@@ -128,8 +138,38 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // other block has read it), so a cached read is exact.
 __device__ __forceinline__ bool is_active(const KArgs& A) { return __ldg(&A.sc->active) != 0; }
 
+// multi-rank scalar step after the rank sums are gathered (scalar_kernel; inline with device comm)
+template <class KA>
+__device__ void scalar_step(const KA& A, int step);
+// The fields of KArgs the scalar steps use.  The device-comm tails below run in the last block of
+// a reduction kernel; as out-of-line calls on this small view they cost the kernels' main loops
+// no registers (inlined, or called with the whole KArgs, they made K1 / K2 / K3 spill).
+struct SArgs {
+    DevScalars* sc;
+    double* gath;
+    double* hist;
+    char* const* dc_peer;
+    uint32_t* dc_seq;
+    int32_t hist_cap, nranks, rank, use_cond;
+    cudaGraphConditionalHandle cond;
+};
+__device__ __forceinline__ SArgs sargs(const KArgs& A) {
+    return SArgs{A.sc, A.gath, A.hist, A.dc_peer, A.dc_seq, A.hist_cap, A.nranks, A.rank, A.use_cond, A.cond};
+}
+// device comm: gather this rank's DevScalars::loc from every rank into gath, then the scalar step
+__device__ __noinline__ void dc_reduce(const SArgs S, int step) {
+    dc_allgather(S.dc_peer, S.nranks, S.rank, S.dc_seq, S.sc->loc, S.gath);
+    scalar_step(S, step);
+}
+__device__ __noinline__ void dc_publish_loc(const SArgs S) { dc_publish(S.dc_peer, S.nranks, S.rank, S.dc_seq, S.sc->loc); }
+__device__ __noinline__ void dc_collect_step(const SArgs S, int step) {
+    dc_collect(S.dc_peer, S.nranks, S.rank, S.dc_seq, S.gath);
+    scalar_step(S, step);
+}
+
 // ---- scalar updates (one thread) --------------------------------------------------------
-__device__ void fin_bb(const KArgs& A, double bb) {
+template <class KA>
+__device__ void fin_bb(const KA& A, double bb) {
     DevScalars* sc = A.sc;
     sc->nb = __dsqrt_rn(bb);
     sc->bzero = sc->nb == 0.0;
@@ -138,7 +178,8 @@ __device__ void fin_bb(const KArgs& A, double bb) {
     sc->active = 1;                       // provisional: decided after s0 (fin_init)
 }
 
-__device__ void fin_init(const KArgs& A, double rho0, double rr0) {
+template <class KA>
+__device__ void fin_init(const KA& A, double rho0, double rr0) {
     DevScalars* sc = A.sc;
     if (sc->bzero) {
         put_hist(A, 0, 0.0);
@@ -167,7 +208,8 @@ struct FinPre {
     int32_t k, maxit;
 };
 
-__device__ __forceinline__ FinPre fin_prefetch(const KArgs& A) {
+template <class KA>
+__device__ __forceinline__ FinPre fin_prefetch(const KA& A) {
     const DevScalars* sc = A.sc;
     FinPre f;
     f.rr = sc->red[2];
@@ -180,7 +222,8 @@ __device__ __forceinline__ FinPre fin_prefetch(const KArgs& A) {
     return f;
 }
 
-__device__ void fin_iter(const KArgs& A, double rho_new, const FinPre& f) {
+template <class KA>
+__device__ void fin_iter(const KA& A, double rho_new, const FinPre& f) {
     DevScalars* sc = A.sc;
     const int k = f.k + 1;
     sc->k = k;
@@ -200,7 +243,8 @@ __device__ void fin_iter(const KArgs& A, double rho_new, const FinPre& f) {
     TT(2, 3);
 }
 
-__device__ void fin_iter(const KArgs& A, double rho_new, double rr) {
+template <class KA>
+__device__ void fin_iter(const KA& A, double rho_new, double rr) {
     FinPre f = fin_prefetch(A);
     f.rr = rr;
     f.h = __ddiv_rn(__dsqrt_rn(rr), f.nb);
@@ -471,7 +515,9 @@ __device__ __forceinline__ bool k1_beta(const KArgs& A, int par, double& beta) {
 #ifndef PCG_MINB_K1
 #define PCG_MINB_K1 4
 #endif
-template <bool SIGMA>
+// DC (device comm, multi-rank only): the last block gathers the rank sums itself (dev_comm.cuh);
+// a separate instantiation, so the one-rank kernels carry none of its code or registers
+template <bool SIGMA, bool DC = false>
 __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, const int par) {
     TL(0, 0);
     pdl_wait();
@@ -552,8 +598,12 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
     if (count_block(&A.sc->counter[0])) {
         const double tot = final_sum(A.partial[0], n_units(A));
         if (threadIdx.x == 0) {
-            if (A.multi) A.sc->loc[0] = tot;
-            else A.sc->red[0] = tot;
+            if (A.multi) {
+                A.sc->loc[0] = tot;
+                if constexpr (DC) dc_reduce(sargs(A), kSsGamma);
+            } else {
+                A.sc->red[0] = tot;
+            }
             A.sc->xpend = 0;
             A.sc->counter[0] = 0;
             A.sc->ticket[0] = 0;
@@ -644,7 +694,7 @@ __device__ __forceinline__ double k1_point(const KArgs& A, const Unit& W, int pa
     return k1_compute<SIGMA>(A, W, par, beta, alpha, L);
 }
 
-template <bool SIGMA>
+template <bool SIGMA, bool DC = false>
 __global__ void __launch_bounds__(kBlock, PCG_MINB_K1F) k1_flat_kernel(const KArgs A, const int par) {
     pdl_wait();
     if (!is_active(A)) return;
@@ -687,8 +737,12 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1F) k1_flat_kernel(const KAr
     if (last) {
         const double tot = final_sum(A.partial[0], n_units(A));
         if (threadIdx.x == 0) {
-            if (A.multi) A.sc->loc[0] = tot;
-            else A.sc->red[0] = tot;
+            if (A.multi) {
+                A.sc->loc[0] = tot;
+                if constexpr (DC) dc_reduce(sargs(A), kSsGamma);
+            } else {
+                A.sc->red[0] = tot;
+            }
             A.sc->xpend = 0;
             A.sc->counter[0] = 0;
             A.sc->ticket[0] = 0;
@@ -904,6 +958,7 @@ __device__ __forceinline__ void k3_sum_rr(const KArgs& A, int init) {
     }
 }
 
+template <bool DC>
 __device__ __forceinline__ void k3_finish(const KArgs& A, int init) {
     TT(2, 0);
     FinPre pre{};
@@ -918,6 +973,9 @@ __device__ __forceinline__ void k3_finish(const KArgs& A, int init) {
         sc->ticket[2] = 0;
         if (A.multi) {
             sc->loc[1] = rs;
+            if constexpr (DC) {
+                if (!A.cgcg) dc_reduce(sargs(A), init ? kSsInit : kSsIter);   // CG-CG: gathered after KC
+            }
         } else if (init) {
             fin_init(A, rs, pre.rr);
         } else {
@@ -1040,7 +1098,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) ka_cg_kernel(const KArgs 
 }
 
 // ---- K3 (AINV): s = Z t ; (s, r) ; beta / history / flag -----------------------------------
-template <int DQ>
+template <int DQ, bool DC = false>
 __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArgs A, const int par, const int init) {
     TL(2, 0);
     pdl_wait();
@@ -1087,7 +1145,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
         last = finish_units<1>(A, ws, A.partial[2], nullptr, A.redundant ? nullptr : &A.sc->counter[2]);
     }
     if (last) {
-        k3_finish(A, init);
+        k3_finish<DC>(A, init);
         TL(2, 3);
     }
 }
@@ -1341,6 +1399,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_LOOP) loop_kernel(const KArgs
 #ifndef KD2_UNROLL
 #define KD2_UNROLL 2                 // measured at cfg4 (Jacobi): 1 / 2 / 4 / 8 -> 47.5 / 45.7 / 48.3 / 51.1 us/iteration
 #endif
+template <bool DC = false>
 __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const int par, const int init,
                                                          const int none) {
     pdl_wait();
@@ -1403,7 +1462,10 @@ __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const in
             A.sc->counter[1] = 0;
             A.sc->alpha = alpha;
             A.sc->xpend = init ? 0 : 1;
-            if (A.multi) { A.sc->loc[2] = rr; A.sc->loc[1] = rs; }
+            if (A.multi) {
+                A.sc->loc[2] = rr; A.sc->loc[1] = rs;
+                if constexpr (DC) dc_reduce(sargs(A), init ? kSsInit : kSsIter);
+            }
             else if (init) fin_init(A, rs, rr);
             else fin_iter(A, rs, rr);
         }
@@ -1432,7 +1494,8 @@ __device__ __forceinline__ double stencil(const KArgs& A, const double* __restri
 
 // alpha, beta of Chronopoulos-Gear from delta = (w, u) and gamma' = rho (one thread; fin_init /
 // fin_iter has set rho, rho_prev and decided the stop test)
-__device__ void cg_alpha_beta(const KArgs& A, double delta, int init) {
+template <class KA>
+__device__ void cg_alpha_beta(const KA& A, double delta, int init) {
     DevScalars* sc = A.sc;
     sc->red[0] = delta;
     const double gamma = sc->rho;
@@ -1480,8 +1543,12 @@ __global__ void __launch_bounds__(kBlock) kc_cg_kernel(const KArgs A, const int 
     const double delta = final_sum(A.partial[0], U);
     if (threadIdx.x == 0) {
         A.sc->counter[0] = 0;
-        if (A.multi) A.sc->loc[0] = delta;               // rank sum: the allgather + kSsCg* follow
-        else cg_alpha_beta(A, delta, init);
+        if (A.multi) {                                   // rank sum: the allgather + kSsCg* follow
+            A.sc->loc[0] = delta;
+            if (A.dc) dc_reduce(sargs(A), init ? kSsCgInit : kSsCgIter);
+        } else {
+            cg_alpha_beta(A, delta, init);
+        }
     }
 }
 
@@ -1493,7 +1560,8 @@ __global__ void __launch_bounds__(kBlock) kc_cg_kernel(const KArgs A, const int 
 // three canonical final sums and the scalars (history, stop test, alpha, beta) while the other
 // blocks stream t; several ranks, the rank sums ride in the allgather fused with the m halo
 // exchange after KPB.  Scalars: rho = gamma of the previous iteration, alpha = alpha_prev.
-__device__ void pipe_fin(const KArgs& A, double gamma, double delta, double rr) {
+template <class KA>
+__device__ void pipe_fin(const KA& A, double gamma, double delta, double rr) {
     DevScalars* sc = A.sc;
     const bool init = sc->pstage == 0;
     int k = 0;
@@ -1556,6 +1624,12 @@ __device__ __forceinline__ void ticket_units(const KArgs& A, unsigned long long*
 __global__ void __launch_bounds__(kBlock, PCG_MINB_K2) kpa_kernel(const KArgs A) {
     pdl_wait();
     if (!is_active(A)) return;
+    if (A.multi && A.dc && blockIdx.x == 0) {          // device comm: the previous KPC's rank sums
+        if (threadIdx.x == 0) {
+            dc_collect_step(sargs(A), kSsPipe);
+        }
+        __syncthreads();
+    }
     if (!A.multi && blockIdx.x == 0) {
         const int64_t U = n_units(A);
         const double g = final_sum<PCG_FINAL_NB_K3>(A.partial[0], U);
@@ -1675,6 +1749,7 @@ __global__ void __launch_bounds__(kBlock) kpc_kernel(const KArgs A, const int in
         A.sc->loc[0] = g;
         A.sc->loc[1] = dl;
         A.sc->loc[2] = rr;
+        if (A.dc) dc_publish_loc(sargs(A));             // collected by the next KPA
     }
 }
 
@@ -1713,8 +1788,12 @@ __global__ void __launch_bounds__(kBlock) init_residual_kernel(const KArgs A) {
         const double tot = final_sum(A.partial[0], n_units(A));
         if (threadIdx.x == 0) {
             A.sc->counter[3] = 0;
-            if (A.multi) A.sc->loc[3] = tot;
-            else fin_bb(A, tot);
+            if (A.multi) {
+                A.sc->loc[3] = tot;
+                if (A.dc) dc_reduce(sargs(A), kSsBB);
+            } else {
+                fin_bb(A, tot);
+            }
         }
     }
 }
@@ -1739,8 +1818,10 @@ __global__ void __launch_bounds__(kBlock) true_residual_kernel(const KArgs A) {
         const double tot = final_sum(A.partial[0], n_units(A));
         if (threadIdx.x == 0) {
             A.sc->counter[3] = 0;
-            if (A.multi) A.sc->loc[3] = tot;
-            else A.sc->true_rel = A.sc->bzero ? 0.0 : __ddiv_rn(__dsqrt_rn(tot), A.sc->nb);
+            if (A.multi) {
+                A.sc->loc[3] = tot;
+                if (A.dc) dc_reduce(sargs(A), kSsTrue);
+            } else A.sc->true_rel = A.sc->bzero ? 0.0 : __ddiv_rn(__dsqrt_rn(tot), A.sc->nb);
         }
     }
 }
@@ -1770,7 +1851,8 @@ __global__ void __launch_bounds__(kBlock) extrapolate_kernel(const double* __res
         x0[e] = __dadd_rn(__dmul_rn(2.0, xt[e]), -xm[e]);
 }
 
-__global__ void scalar_kernel(const KArgs A, const int step) {
+template <class KA>
+__device__ void scalar_step(const KA& A, int step) {
     DevScalars* sc = A.sc;
     const int P = A.nranks;
     switch (step) {
@@ -1799,6 +1881,8 @@ __global__ void scalar_kernel(const KArgs A, const int step) {
         } break;
     }
 }
+
+__global__ void scalar_kernel(const KArgs A, const int step) { scalar_step(A, step); }
 
 __global__ void set_cond_kernel(cudaGraphConditionalHandle h) { cudaGraphSetConditional(h, 1u); }
 
@@ -1851,7 +1935,7 @@ void configure_kernels(KArgs& A, int sms) {
     }
     A.g_k2 = persistent_grid(k2_ainv_kernel<0>, U, sms, 2048);
     A.g_k3 = persistent_grid(k3_ainv_kernel<0>, U, sms, 2048);
-    A.g_kd = persistent_grid(k2_diag_kernel, U, sms, 4096);
+    A.g_kd = persistent_grid(k2_diag_kernel<false>, U, sms, 4096);
     A.g_row = persistent_grid(init_residual_kernel, U, sms, 2048);
     // K1 form: 2 = row-segment units, static block stride, no barrier per unit (default: 94.7 ->
     // 91.9 us/iteration at ORCA025 against the 4-row strips, 0); 1 = same units, dynamic tickets
@@ -1882,7 +1966,12 @@ void configure_kernels(KArgs& A, int sms) {
     allow_smem(k3_ainv_kernel<8>, row_smem(A, A.g_k3, 1));
     allow_smem(k2_ainv_kernel<16>, row_smem(A, A.g_k2, 1));
     allow_smem(k3_ainv_kernel<16>, row_smem(A, A.g_k3, 1));
-    allow_smem(k2_diag_kernel, row_smem(A, A.g_kd, 2));
+    allow_smem(k2_diag_kernel<false>, row_smem(A, A.g_kd, 2));
+    allow_smem(k2_diag_kernel<true>, row_smem(A, A.g_kd, 2));
+    allow_smem(k1_kernel<false, true>, k1_smem(A, A.g_k1));
+    allow_smem(k1_kernel<true, true>, k1_smem(A, A.g_k1));
+    allow_smem(k3_ainv_kernel<0, true>, row_smem(A, A.g_k3, 1));
+    allow_smem(k3_ainv_kernel<-1, true>, row_smem(A, A.g_k3, 1));
     allow_smem(ka_cg_kernel, row_smem(A, A.g_k2, 1));
     allow_smem(kc_cg_kernel, row_smem(A, A.g_row, 1));
     allow_smem(kpc_kernel, row_smem(A, A.g_row, 3));
@@ -1925,10 +2014,16 @@ static void launch_pdl(const KArgs& A, void (*kern)(P...), int grid, int block, 
 void launch_k1(const KArgs& A, int par, cudaStream_t st) {
     if (A.k1flat) {
         const size_t sm = A.k1flat == 2 ? row_smem(A, A.g_k1f, 1) : 0;
-        if (A.sigma) launch_pdl(A, k1_flat_kernel<true>, A.g_k1f, kBlock, sm, st, A, par);
+        if (A.dc) {
+            if (A.sigma) launch_pdl(A, k1_flat_kernel<true, true>, A.g_k1f, kBlock, sm, st, A, par);
+            else launch_pdl(A, k1_flat_kernel<false, true>, A.g_k1f, kBlock, sm, st, A, par);
+        } else if (A.sigma) launch_pdl(A, k1_flat_kernel<true>, A.g_k1f, kBlock, sm, st, A, par);
         else launch_pdl(A, k1_flat_kernel<false>, A.g_k1f, kBlock, sm, st, A, par);
     } else {
-        if (A.sigma) launch_pdl(A, k1_kernel<true>, A.g_k1, kBlock, k1_smem(A, A.g_k1), st, A, par);
+        if (A.dc) {
+            if (A.sigma) launch_pdl(A, k1_kernel<true, true>, A.g_k1, kBlock, k1_smem(A, A.g_k1), st, A, par);
+            else launch_pdl(A, k1_kernel<false, true>, A.g_k1, kBlock, k1_smem(A, A.g_k1), st, A, par);
+        } else if (A.sigma) launch_pdl(A, k1_kernel<true>, A.g_k1, kBlock, k1_smem(A, A.g_k1), st, A, par);
         else launch_pdl(A, k1_kernel<false>, A.g_k1, kBlock, k1_smem(A, A.g_k1), st, A, par);
     }
 }
@@ -1956,11 +2051,14 @@ void launch_k3_ainv(const KArgs& A, int par, int init, cudaStream_t st) {
     if (A.dia_q > 8) launch_pdl(A, k3_ainv_kernel<16>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else if (A.dia_q > 4) launch_pdl(A, k3_ainv_kernel<8>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else if (A.dia_q > 0) launch_pdl(A, k3_ainv_kernel<4>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
+    else if (A.dc && A.z.col16) launch_pdl(A, k3_ainv_kernel<-1, true>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
+    else if (A.dc) launch_pdl(A, k3_ainv_kernel<0, true>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else if (A.z.col16) launch_pdl(A, k3_ainv_kernel<-1>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
     else launch_pdl(A, k3_ainv_kernel<0>, A.g_k3, kBlock, row_smem(A, A.g_k3, 1), st, A, par, init);
 }
 void launch_k2_diag(const KArgs& A, int par, int init, int none, cudaStream_t st) {
-    launch_pdl(A, k2_diag_kernel, A.g_kd, kBlock, row_smem(A, A.g_kd, 2), st, A, par, init, none);
+    if (A.dc) launch_pdl(A, k2_diag_kernel<true>, A.g_kd, kBlock, row_smem(A, A.g_kd, 2), st, A, par, init, none);
+    else launch_pdl(A, k2_diag_kernel<false>, A.g_kd, kBlock, row_smem(A, A.g_kd, 2), st, A, par, init, none);
 }
 void launch_prep(const KArgs& A, cudaStream_t st) {
     const int64_t n = (int64_t)(A.nloc + 2 * A.halo) * A.pitch;

@@ -116,13 +116,20 @@ struct KArgs {
     size_t l2_bytes;                  // (0: none)
     float l2_ratio;
     RsDev rs;                         // resident-strip driver (rs.on = 0: not used)
+    // device comm (PCG_FLAG_DEVICE_COMM, dev_comm.cuh): the last block of each reduction gathers
+    // the rank sums through the NCCL window itself and runs the scalar step inline
+    char* const* dc_peer;             // [nranks] window base of every rank (device pointers)
+    uint32_t* dc_seq;                 // this rank's reduction counter (persists across solves)
+    int32_t dc;
+    int32_t rank;                     // this rank (multi-rank path)
 };
 
 int64_t grid_blocks(const KArgs& A);
 
 #ifdef __CUDACC__
 // history entry k (kept only while k < hist_cap) and the last value (always)
-__device__ __forceinline__ void put_hist(const KArgs& A, int k, double h) {
+template <class KA>
+__device__ __forceinline__ void put_hist(const KA& A, int k, double h) {
     if (k < A.hist_cap) A.hist[k] = h;
     A.sc->hlast = h;
 }

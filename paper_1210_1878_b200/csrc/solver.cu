@@ -25,6 +25,12 @@ thread_local std::string g_last_error;
 void set_thread_error(const std::string& m) { g_last_error = m; }
 }  // namespace pcg
 
+namespace pcg {
+int dc_setup(ncclComm_t comm, int nranks, void** win_buf, void** win, char*** peers, uint32_t** seq, cudaStream_t st,
+             std::string& err);
+void dc_free(ncclComm_t comm, void* win_buf, void* win, char** peers, uint32_t* seq);
+}  // namespace pcg
+
 struct pcg_ctx {
     Plan plan;                         // host plan (SELL arrays are released after upload)
     int device = 0;
@@ -41,6 +47,9 @@ struct pcg_ctx {
     char* ovf_base = nullptr;          // Z / Z^T overflow arrays, directly in front of `hot`
     double* pvec = nullptr;            // Chronopoulos-Gear / pipelined search direction
     double *pz = nullptr, *pq = nullptr, *pm = nullptr;   // pipelined PCG: z, q, m
+    void *dc_buf = nullptr, *dc_win = nullptr;             // device comm: symmetric NCCL window
+    char** dc_peers = nullptr;                             // [nranks] window bases (device)
+    uint32_t* dc_seq = nullptr;                            // reduction counter (device)
     size_t ovf_bytes = 0;
     double* dia = nullptr;             // FSAI DIA diagonals
     int32_t *sched2 = nullptr, *soff2 = nullptr, *sched3 = nullptr, *soff3 = nullptr;   // static schedules
@@ -170,7 +179,7 @@ bool use_graph(const pcg_ctx* c) {
 //     last owned row -> rank+1's row H-1 (one row each way)
 //   QR (halo-AINV, after K1): rows [H+nloc-ws, H+nloc) of q and r[par] -> rank+1's rows [H-w, H)
 //   T  (halo-AINV, after K2): rows [H, H+halo_t_send) of t -> rank-1's rows [H+nloc, H+nloc+halo_t)
-enum class Ex { None, Allgather, HaloX, HaloSAllgather, AllgatherQR, QR, HaloT, HaloS, HaloMAllgather };
+enum class Ex { None, Allgather, HaloX, HaloSAllgather, AllgatherQR, QR, HaloT, HaloS, HaloMAllgather, HaloM };
 struct Xfer {
     double* arr;                     // this context's array
     int64_t off, n;                  // elements
@@ -186,7 +195,7 @@ XferList exchange_list(pcg_ctx* c, Ex ex, int par, double* halo_arr = nullptr) {
     XferList L;
     L.allgather = ex == Ex::Allgather || ex == Ex::HaloSAllgather || ex == Ex::AllgatherQR || ex == Ex::HaloMAllgather;
     double* row1 = halo_arr ? halo_arr : ex == Ex::HaloX ? c->x : (ex == Ex::HaloS || ex == Ex::HaloSAllgather) ? c->s
-                 : ex == Ex::HaloMAllgather ? c->pm : nullptr;
+                 : (ex == Ex::HaloMAllgather || ex == Ex::HaloM) ? c->pm : nullptr;
     if (row1) {
         if (P.rank > 0) {
             L.send_south.push_back({row1, H * pt, pt});
@@ -215,6 +224,8 @@ XferList exchange_list(pcg_ctx* c, Ex ex, int par, double* halo_arr = nullptr) {
 Status nccl_exchange(pcg_ctx* c, Ex ex, int par, double* halo_arr = nullptr) {
     const Plan& P = c->plan;
     const XferList L = exchange_list(c, ex, par, halo_arr);
+    if (!L.allgather && L.send_south.empty() && L.recv_south.empty() && L.send_north.empty() && L.recv_north.empty())
+        return Status::ok();                             // nothing to exchange (one rank, device comm)
     NC(ncclGroupStart());
     if (L.allgather) NC(ncclAllGather((const void*)c->sc->loc, (void*)c->gath, 4, ncclDouble, c->comm, c->st));
     for (const Xfer& x : L.send_south) NC(ncclSend(x.arr + x.off, (size_t)x.n, ncclDouble, P.rank - 1, c->comm, c->st));
@@ -240,6 +251,22 @@ struct Step {
     int par = 0;                         // QR exchanges: which r buffer K2 reads
 };
 
+// With device comm (A.dc) the rank sums are gathered inside the reduction kernels and the
+// scalar step runs there too: the allgather leaves every exchange and the scalar kernels go.
+void exch(std::vector<Step>& s, const pcg_ctx* c, Ex ex, int par = 0) {
+    if (c->A.dc) {
+        if (ex == Ex::Allgather) return;
+        if (ex == Ex::HaloSAllgather) ex = Ex::HaloS;
+        else if (ex == Ex::AllgatherQR) ex = Ex::QR;
+        else if (ex == Ex::HaloMAllgather) ex = Ex::HaloM;
+    }
+    s.push_back({ex, nullptr, par});
+}
+void scalar(std::vector<Step>& s, const pcg_ctx* c, int step) {
+    if (c->A.dc) return;
+    s.push_back({Ex::None, [step](pcg_ctx* x) { launch_scalar(x->A, step, x->st); }});
+}
+
 std::vector<Step> prologue_steps(const pcg_ctx* c) {
     std::vector<Step> s;
     const bool multi = c->multi, ainv = c->plan.factored();
@@ -248,8 +275,8 @@ std::vector<Step> prologue_steps(const pcg_ctx* c) {
     if (multi) s.push_back({Ex::HaloX, nullptr});
     s.push_back({Ex::None, [](pcg_ctx* x) { launch_init_residual(x->A, x->st); }});
     if (multi) {
-        s.push_back({Ex::Allgather, nullptr});
-        s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsBB, x->st); }});
+        exch(s, c, Ex::Allgather);
+        scalar(s, c, kSsBB);
     }
     const bool hx = multi && c->plan.halo_w > 0;
     if (ainv) {
@@ -261,15 +288,15 @@ std::vector<Step> prologue_steps(const pcg_ctx* c) {
             if (multi) s.push_back({Ex::HaloS, nullptr});
             s.push_back({Ex::None, [](pcg_ctx* x) { launch_kc(x->A, 1, 1, x->st); }});
             if (multi) {
-                s.push_back({Ex::Allgather, nullptr});
-                s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsCgInit, x->st); }});
+                exch(s, c, Ex::Allgather);
+                scalar(s, c, kSsCgInit);
             }
             return s;
         }
         if (c->A.pipe) {                                 // w0 = A u0 and (r,u) (w,u) (r,r) (pipelined)
             if (multi) {
-                s.push_back({Ex::HaloSAllgather, nullptr});
-                s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsInit, x->st); }});
+                exch(s, c, Ex::HaloSAllgather);
+                scalar(s, c, kSsInit);
             }
             s.push_back({Ex::None, [](pcg_ctx* x) { launch_kpc(x->A, 1, x->st); }});
             return s;                    // the first iteration's allgather carries the rank sums
@@ -278,8 +305,8 @@ std::vector<Step> prologue_steps(const pcg_ctx* c) {
         s.push_back({Ex::None, [none](pcg_ctx* x) { launch_k2_diag(x->A, 1, 1, none, x->st); }});
     }
     if (multi) {
-        s.push_back({Ex::HaloSAllgather, nullptr});
-        s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsInit, x->st); }});
+        exch(s, c, Ex::HaloSAllgather);
+        scalar(s, c, kSsInit);
     }
     return s;
 }
@@ -293,8 +320,8 @@ std::vector<Step> iteration_steps(const pcg_ctx* c, int par) {
         s.push_back({Ex::None, [](pcg_ctx* x) { launch_kpa(x->A, x->st); }});
         s.push_back({Ex::None, [](pcg_ctx* x) { launch_kpb(x->A, x->st); }});
         if (multi) {
-            s.push_back({Ex::HaloMAllgather, nullptr});
-            s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsPipe, x->st); }});
+            exch(s, c, Ex::HaloMAllgather);
+            scalar(s, c, kSsPipe);
         }
         s.push_back({Ex::None, [](pcg_ctx* x) { launch_kpc(x->A, 0, x->st); }});
         return s;
@@ -305,15 +332,15 @@ std::vector<Step> iteration_steps(const pcg_ctx* c, int par) {
         if (multi) s.push_back({Ex::HaloS, nullptr});
         s.push_back({Ex::None, [par](pcg_ctx* x) { launch_kc(x->A, par, 0, x->st); }});
         if (multi) {
-            s.push_back({Ex::Allgather, nullptr});
-            s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsCgIter, x->st); }});
+            exch(s, c, Ex::Allgather);
+            scalar(s, c, kSsCgIter);
         }
         return s;
     }
     s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k1(x->A, par, x->st); }});
     if (multi) {
-        s.push_back({hx ? Ex::AllgatherQR : Ex::Allgather, nullptr, par});
-        s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsGamma, x->st); }});
+        exch(s, c, hx ? Ex::AllgatherQR : Ex::Allgather, par);
+        scalar(s, c, kSsGamma);
     }
     if (ainv) {
         s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k2_ainv(x->A, par, 0, x->st); }});
@@ -323,8 +350,8 @@ std::vector<Step> iteration_steps(const pcg_ctx* c, int par) {
         s.push_back({Ex::None, [par, none](pcg_ctx* x) { launch_k2_diag(x->A, par, 0, none, x->st); }});
     }
     if (multi) {
-        s.push_back({Ex::HaloSAllgather, nullptr});
-        s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsIter, x->st); }});
+        exch(s, c, Ex::HaloSAllgather);
+        scalar(s, c, kSsIter);
     }
     return s;
 }
@@ -335,8 +362,8 @@ std::vector<Step> epilogue_steps(const pcg_ctx* c) {
     if (c->multi) s.push_back({Ex::HaloX, nullptr});
     s.push_back({Ex::None, [](pcg_ctx* x) { launch_true_residual(x->A, x->st); }});
     if (c->multi) {
-        s.push_back({Ex::Allgather, nullptr});
-        s.push_back({Ex::None, [](pcg_ctx* x) { launch_scalar(x->A, kSsTrue, x->st); }});
+        exch(s, c, Ex::Allgather);
+        scalar(s, c, kSsTrue);
     }
     return s;
 }
@@ -1075,6 +1102,23 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     for (int k = 0; k < 3; ++k) A.partial[k] = c->partial[k];
     A.gath = c->gath; A.sc = c->sc;
     A.multi = c->multi ? 1 : 0;
+    A.rank = P.rank;
+    A.dc = 0;
+    A.dc_peer = nullptr;
+    A.dc_seq = nullptr;
+    if (P.flags & PCG_FLAG_DEVICE_COMM) {
+        // device comm: the NCCL path only (the local-ranks emulation runs its
+        // ranks one after another, so no rank may wait on another inside a kernel)
+        if (!c->multi || (P.flags & PCG_FLAG_LOCAL_RANKS) || !c->comm)
+            return Status::err(PCG_ERR_ARG, "pcg_setup: PCG_FLAG_DEVICE_COMM needs the NCCL path (nccl_comm; "
+                                            "nranks > 1 or PCG_FLAG_COMM_PATH), not PCG_FLAG_LOCAL_RANKS");
+        std::string err;
+        const int rc = dc_setup(c->comm, P.nranks, &c->dc_buf, &c->dc_win, &c->dc_peers, &c->dc_seq, c->st, err);
+        if (rc != PCG_OK) return Status::err((pcg_status)rc, "pcg_setup: " + err);
+        A.dc = 1;
+        A.dc_peer = c->dc_peers;
+        A.dc_seq = c->dc_seq;
+    }
     A.use_cond = 0;
     A.precond = P.factored() ? 0 : (int32_t)P.precond;
     A.dia_q = 0;
@@ -1230,6 +1274,7 @@ void pcg_free(pcg_ctx* c) {
         }
         cudaGetLastError();
     }
+    if (c->dc_win || c->dc_buf) dc_free(c->comm, c->dc_buf, c->dc_win, c->dc_peers, c->dc_seq);
     for (void* p : c->allocs) cudaFree(p);
     if (c->h_sc) cudaFreeHost(c->h_sc);
     if (c->h_hist) cudaFreeHost(c->h_hist);

@@ -780,10 +780,12 @@ def test_timestep_warm_modes_and_aliasing():
 
 # ------------------------------------------ the NCCL path across real GPUs (skipped on 1 GPU)
 @pytest.mark.parametrize("w", [0, 3])
-def test_nccl_two_ranks_equals_local_ranks(w, tmp_path):
+@pytest.mark.parametrize("device_comm", [False, True])
+def test_nccl_two_ranks_equals_local_ranks(w, device_comm, tmp_path):
     """Two processes, one GPU each, NCCL send/recv halos and allgathered rank sums (the code the
-    one-GPU tests reach only through the local-ranks backend): the solve equals the local-ranks
-    emulation and the oracle's partitioned canonical PCG bit for bit.  Needs >= 2 GPUs."""
+    one-GPU tests reach only through the local-ranks backend) -- or, with PCG_FLAG_DEVICE_COMM, the
+    rank sums gathered inside the kernels over NVLink: the solve equals the local-ranks emulation
+    and the oracle's partitioned canonical PCG bit for bit.  Needs >= 2 GPUs."""
     import subprocess
     import sys
     if torch.cuda.device_count() < 2:
@@ -795,7 +797,8 @@ def test_nccl_two_ranks_equals_local_ranks(w, tmp_path):
     np.save(out + ".b.npy", b)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
-           "127.0.0.1", "--master-port", "29531", os.path.join(root, "tests", "nccl_worker.py"), out, "cfg3", str(w)]
+           "127.0.0.1", "--master-port", "29531", os.path.join(root, "tests", "nccl_worker.py"), out, "cfg3", str(w),
+           str(pcg.FLAG_DEVICE_COMM if device_comm else 0)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     got = np.load(out + ".npz")
@@ -904,3 +907,71 @@ def test_resident_driver_cfg4_is_default():
     ms, it = S.loop_time()
     assert it == k and ms > 0
     S.close()
+
+
+# ------------------------------------------------ device comm (PCG_FLAG_DEVICE_COMM)
+def _dc_value(seed, k, r, q):
+    """The self-test's value hash (csrc/devcomm.cu dc_test_value), in Python integers."""
+    M = (1 << 64) - 1
+    x = (seed ^ ((0x9e3779b97f4a7c15 * (k * 131 + r * 7 + q + 1)) & M)) & M
+    x ^= x >> 31
+    x = (x * 0xbf58476d1ce4e5b9) & M
+    x ^= x >> 29
+    x = (x * 0x94d049bb133111eb) & M
+    x ^= x >> 32
+    return float(x & 0xfffffffffffff) * 2.0 ** -40 - 2048.0
+
+
+def _rank_tree(vals):
+    """u[l] += u[l + off] for off = 16 .. 1 over the rank sums zero padded to 32."""
+    u = [float(v) for v in vals] + [0.0] * (32 - len(vals))
+    off = 16
+    while off >= 1:
+        for l in range(off):
+            u[l] = u[l] + u[l + off]
+        off //= 2
+    return u[0]
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 7, 8, 32])
+def test_devcomm_protocol_selftest(P):
+    """The device-comm exchange (stamps, two slots by reduction parity, peer stores) run by P virtual
+    ranks in one cooperative launch for 13 reductions (odd ones through the split publish / collect
+    form of the pipelined path): every rank forms bitwise the host's rank tree of every slot."""
+    rounds, seed = 13, 12345
+    out = pcg.devcomm_selftest(P, rounds, seed)
+    for k in range(rounds):
+        for q in range(4):
+            want = _rank_tree([_dc_value(seed, k, r, q) for r in range(P)])
+            assert np.all(out[k, :, q] == want), (k, q)
+
+
+@pytest.mark.parametrize("method,precond", [("pcg", "ainv"), ("pcg", "jacobi"), ("cg1", "ainv"), ("pipe", "ainv")])
+def test_device_comm_one_rank_bitwise(method, precond):
+    """One rank through the NCCL path with PCG_FLAG_DEVICE_COMM (symmetric window, in-kernel gather
+    of the rank sums, scalar steps inline) equals the same solve through the host-enqueued
+    allgather, and the single-rank driver, bit for bit."""
+    p = synth.config("cfg3")
+    A = oracle.assemble(p)
+    b = dev(A.to_grid(rhs(A, p)))
+    fl = {"pcg": 0, "cg1": pcg.FLAG_SINGLE_REDUCTION, "pipe": pcg.FLAG_PIPELINED}[method]
+    out = []
+    for flags, cp in ((fl, False), (fl, True), (fl | pcg.FLAG_DEVICE_COMM, True)):
+        S = pcg.Solver(p.cE, p.cN, p.mask, tau=TAU, precond=precond, flags=flags, comm_path=cp)
+        x, k, h, rep = S.solve(b, tol=1e-10, maxit=A.n)
+        x2, k2, h2, rep2 = S.solve(b, tol=1e-10, maxit=A.n)          # the window's stamps keep counting
+        assert k2 == k and np.array_equal(h2, h) and torch.equal(x2, x)
+        out.append((host(x), k, h, rep["true_rel_residual"]))
+        S.close()
+    for o in out[1:]:
+        assert o[1] == out[0][1] and np.array_equal(o[2], out[0][2]) and np.array_equal(o[0], out[0][0])
+        assert o[3] == out[0][3]
+
+
+def test_device_comm_argument_errors():
+    """PCG_FLAG_DEVICE_COMM without the NCCL path, or with the local-ranks emulation, is an argument error."""
+    p = synth.config("cfg2")
+    with pytest.raises(pcg.PcgError):
+        pcg.Solver(p.cE, p.cN, p.mask, tau=TAU, flags=pcg.FLAG_DEVICE_COMM)
+    with pytest.raises(pcg.PcgError):
+        pcg.LocalRanks(p.cE, p.cN, p.mask, 2, tau=TAU, flags=pcg.FLAG_DEVICE_COMM)
