@@ -223,6 +223,9 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=150)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-iters", type=int, default=60)
+    ap.add_argument("--comm", default="device", choices=["device", "host"],
+                    help="N > 1: rank sums gathered inside the kernels over a symmetric NCCL window "
+                         "(PCG_FLAG_DEVICE_COMM) or by a host-enqueued ncclAllGather per reduction")
     ap.add_argument("--method", default="pcg", choices=["pcg", "cg1", "pipe"],
                     help="cg1: Chronopoulos-Gear single-reduction PCG (one allgather per iteration across ranks); "
                          "pipe: pipelined PCG (the reduction overlaps the next preconditioner application)")
@@ -246,8 +249,23 @@ def main():
         group = dist.group.WORLD
     p = synth.config(args.config)
     t0 = time.perf_counter()
-    S = pcg.Solver(p.cE, p.cN, p.mask, tau=args.tau, precond=args.precond, group=group, device=local,
-                   fsai_q=args.fsai_q, flags={"cg1": pcg.FLAG_SINGLE_REDUCTION, "pipe": pcg.FLAG_PIPELINED}.get(args.method, 0))
+    flags = {"cg1": pcg.FLAG_SINGLE_REDUCTION, "pipe": pcg.FLAG_PIPELINED}.get(args.method, 0)
+    comm = "none"
+    if world > 1:
+        comm = args.comm
+        if comm == "device":
+            flags |= pcg.FLAG_DEVICE_COMM
+    try:
+        S = pcg.Solver(p.cE, p.cN, p.mask, tau=args.tau, precond=args.precond, group=group, device=local,
+                       fsai_q=args.fsai_q, flags=flags)
+    except pcg.PcgError as e:
+        if not flags & pcg.FLAG_DEVICE_COMM:
+            raise
+        # no symmetric NCCL window here (ranks outside one NVLink domain): host-enqueued allgathers
+        print("bench: device comm unavailable (%s); using the NCCL allgather path" % e, file=sys.stderr)
+        comm = "host"
+        S = pcg.Solver(p.cE, p.cN, p.mask, tau=args.tau, precond=args.precond, group=group, device=local,
+                       fsai_q=args.fsai_q, flags=flags & ~pcg.FLAG_DEVICE_COMM)
     setup_wall = time.perf_counter() - t0
     rows = slice(S.j_begin, S.j_end)
     xs = torch.from_numpy(np.ascontiguousarray(synth.xstar(p)[rows])).cuda()
@@ -409,7 +427,7 @@ def main():
                            "l2": ("no flush between steps: a step's data (~170 MB of static Z/Z^T/coefficient arrays + 94 MB "
                                   "of vectors) exceeds the 126 MB L2; by design 7 of the 8 per-iteration vectors "
                                   "stay in a persisting L2 window within a solve (DESIGN.md §4)"),
-                           "parallelism": f"row blocks x{world}" if world > 1 else "1 GPU",
+                           "parallelism": f"row blocks x{world}" if world > 1 else "1 GPU", "comm": comm,
                            "driver": "resident strips (one persistent cooperative kernel per solve)" if rs_used
                                      else "WHILE-node graph of K1/K2/K3 launches" if world == 1 else "NCCL row blocks",
                            "kernels": ktimes},
