@@ -512,6 +512,32 @@ __device__ __forceinline__ bool k1_beta(const KArgs& A, int par, double& beta) {
     return true;
 }
 
+// End of every K1 form, after its partials are stored: who sums (d, q).  Redundant-sum mode: K2's
+// blocks; Jacobi / none: k2_diag's blocks; otherwise the last block (rank sum on the NCCL path).
+template <bool DC>
+__device__ __forceinline__ void k1_tail(const KArgs& A) {
+    if (A.redundant) return;                           // (d, q) is summed by K2's blocks
+    if (A.red_gamma) {                                 // Jacobi / none: k2_diag's blocks sum (d, q)
+        if (blockIdx.x == 0 && threadIdx.x == 0) A.sc->xpend = 0;   // x += alpha_prev d_old done
+        return;
+    }
+    if (count_block(&A.sc->counter[0])) {
+        const double tot = final_sum(A.partial[0], n_units(A));
+        if (threadIdx.x == 0) {
+            if (A.multi) {
+                A.sc->loc[0] = tot;
+                if constexpr (DC) dc_reduce(sargs(A), kSsGamma);
+            } else {
+                A.sc->red[0] = tot;
+            }
+            A.sc->xpend = 0;
+            A.sc->counter[0] = 0;
+            A.sc->ticket[0] = 0;
+        }
+        TL(0, 3);
+    }
+}
+
 #ifndef PCG_MINB_K1
 #define PCG_MINB_K1 4
 #endif
@@ -590,26 +616,200 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1) k1_kernel(const KArgs A, 
     }
     pdl_trigger();
     TL(0, 2);
-    if (A.redundant) return;                           // (d, q) is summed by K2's blocks
-    if (A.red_gamma) {                                 // Jacobi / none: k2_diag's blocks sum (d, q)
-        if (blockIdx.x == 0 && threadIdx.x == 0) A.sc->xpend = 0;   // x += alpha_prev d_old done
-        return;
+    k1_tail<DC>(A);
+}
+
+// ---- K1, bulk-copy (TMA) form: the HBM-bound grids (cfg5) --------------------------------------
+// Each block owns one strip of kK1W columns of a chunk of rows and marches north through it.  One
+// thread issues 1-D bulk copies (cp.async.bulk, SASS UBLKCP) of the next rows' segments of s,
+// d_old, x, cE, cN (+ sigma) -- kK1W columns plus two halo columns each side, and for the strips
+// that hold the periodic seam the row's element at the other end -- into a ring of kK1S stages
+// signalled by mbarriers, so kK1S - 3 rows per block are in flight whatever the register budget.
+// Geometry measured at cfg5 (K1 us per launch): 256 columns x 4 stages x 4 blocks per SM 154;
+// 512 x 4 x 2 158; 512 x 5 x 2 158; 512 x 8 x 1 (256 threads) 229, (512 threads) 193; the
+// 4-row strip kernel 205.  Row j is computed from stages j-1, j, j+1 entirely out of shared memory: d at
+// the point and its four neighbours recomputed as fma(beta, d_old, s) (bitwise k1_strip's values),
+// the canonical stencil, x += alpha d_old, and d, q, x stored with coalesced
+// 256-byte warp stores.  The (row, 256-column segment) partials of (d, q) are the canonical block
+// trees, as in every K1 form.
+#ifndef PCG_K1T_W
+#define PCG_K1T_W 256
+#endif
+#ifndef PCG_K1T_STAGES
+#define PCG_K1T_STAGES 4
+#endif
+#ifndef PCG_K1T_THREADS
+#define PCG_K1T_THREADS 256
+#endif
+#ifndef PCG_K1T_MINB
+#define PCG_K1T_MINB 4
+#endif
+constexpr int kK1W = PCG_K1T_W;                    // strip width, a multiple of kBlock
+constexpr int kK1S = PCG_K1T_STAGES;               // ring stages (>= 4)
+constexpr int kK1T = PCG_K1T_THREADS;              // threads per block
+constexpr int kK1Row = kK1W + 4;                   // staged doubles per row segment: halo 2 + 2
+constexpr int kK1Seg = kK1W / kBlock;              // canonical segments per strip
+static_assert(kK1W % kBlock == 0 && kK1S >= 4 && kK1W % kK1T == 0 && kK1T % 32 == 0, "K1 bulk-copy geometry");
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned cnt) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+            smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(b))
+                 : "memory");
+}
+
+template <int NA>
+struct K1tSmem {
+    double row[kK1S][NA][kK1Row];                  // staged row segments (element col0 - 2 + o at o)
+    double seamW[kK1S][3][4];                      // west seam: s, d_old, cE of the 32-byte block holding ni-1
+    double seamE[kK1S][2][4];                      // east seam: s, d_old of elements 0..3
+    uint64_t full[kK1S];
+    double wsum[2][kK1Seg][kWarps];
+};
+template <bool SIGMA>
+size_t k1t_smem_bytes() { return sizeof(K1tSmem<SIGMA ? 6 : 5>); }
+
+// stage t of a block: grid row r (owned numbering; -1 and nloc are the halo rows) of its strip
+template <int NA>
+__device__ __forceinline__ void k1t_fill(K1tSmem<NA>& S, int slot, const KArgs& A, int par, int32_t r, int32_t col0,
+                                         int32_t lo, int32_t hi, int32_t seamW, int32_t seamE) {
+    const int64_t base = (int64_t)(r + A.halo) * A.pitch;
+    const unsigned nb = (unsigned)(hi - lo) * 8u;
+    const unsigned seam_bytes = (seamW >= 0 ? 3u * 32u : 0u) + (seamE >= 0 ? 2u * 32u : 0u);
+    mbar_expect_tx(&S.full[slot], (unsigned)NA * nb + seam_bytes);
+    const double* src[6] = {A.s, A.d[par], A.x, A.cE, A.cN, A.sigma};
+    const int off = lo - (col0 - 2);
+#pragma unroll
+    for (int v = 0; v < NA; ++v) bulk_g2s(&S.row[slot][v][off], src[v] + base + lo, nb, &S.full[slot]);
+    if (seamW >= 0) {                              // 4 doubles (32-byte aligned) holding element ni-1
+        bulk_g2s(S.seamW[slot][0], A.s + base + seamW, 32u, &S.full[slot]);
+        bulk_g2s(S.seamW[slot][1], A.d[par] + base + seamW, 32u, &S.full[slot]);
+        bulk_g2s(S.seamW[slot][2], A.cE + base + seamW, 32u, &S.full[slot]);
     }
-    if (count_block(&A.sc->counter[0])) {
-        const double tot = final_sum(A.partial[0], n_units(A));
-        if (threadIdx.x == 0) {
-            if (A.multi) {
-                A.sc->loc[0] = tot;
-                if constexpr (DC) dc_reduce(sargs(A), kSsGamma);
-            } else {
-                A.sc->red[0] = tot;
-            }
-            A.sc->xpend = 0;
-            A.sc->counter[0] = 0;
-            A.sc->ticket[0] = 0;
+    if (seamE >= 0) {                              // elements 0..3 (element 0 is the east neighbour of ni-1)
+        bulk_g2s(S.seamE[slot][0], A.s + base, 32u, &S.full[slot]);
+        bulk_g2s(S.seamE[slot][1], A.d[par] + base, 32u, &S.full[slot]);
+    }
+}
+
+template <bool SIGMA>
+__global__ void __launch_bounds__(kK1T, PCG_K1T_MINB) k1_tma_kernel(const KArgs A, const int par) {
+    constexpr int NA = SIGMA ? 6 : 5;
+    pdl_wait();
+    if (!is_active(A)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (++A.sc->guard > A.sc->maxit + 2) {             // the WHILE node's safety net (k1_kernel)
+            A.sc->active = 0;
+            A.sc->status = kStBreakdown;
+            set_cond(A, 0);
         }
-        TL(0, 3);
     }
+    extern __shared__ __align__(128) unsigned char k1t_raw[];
+    K1tSmem<NA>& S = *reinterpret_cast<K1tSmem<NA>*>(k1t_raw);
+    double beta;
+    if (!k1_beta(A, par, beta)) return;
+    const double alpha = A.sc->alpha;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int32_t P = A.pitch, ni = A.ni;
+    const int32_t c = blockIdx.x % A.k1t_strips, chunk = blockIdx.x / A.k1t_strips;
+    const int32_t j0 = chunk * A.k1t_rows, j1 = min(j0 + A.k1t_rows, A.nloc);
+    const int32_t col0 = c * kK1W, width = min(kK1W, P - col0);
+    const int32_t lo = c == 0 ? col0 : col0 - 2;                    // staged columns [lo, hi)
+    const int32_t hi = col0 + width == P ? P : col0 + width + 2;
+    const int32_t seamW = (c == 0) ? ((ni - 1) & ~3) : -1;          // 32-byte block holding ni - 1
+    const int32_t seamE = (ni - 1 >= col0 && ni - 1 < col0 + width) ? 0 : -1;
+    const int32_t R = j1 - j0 + 2;                                  // staged rows j0-1 .. j1
+    double* __restrict__ dnew = A.d[par ^ 1];
+    if (j0 < j1) {
+        if (tid == 0) {
+            for (int s = 0; s < kK1S; ++s) mbar_init(&S.full[s], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            for (int t = 0; t < min(kK1S, R); ++t) k1t_fill<NA>(S, t, A, par, j0 - 1 + t, col0, lo, hi, seamW, seamE);
+        }
+        __syncthreads();
+        mbar_wait(&S.full[0], 0);
+        mbar_wait(&S.full[1], 0);
+        for (int32_t j = j0; j < j1; ++j) {
+            const int t = j - j0;                                    // stages t (row j-1), t+1 (j), t+2 (j+1)
+            const int sS = t % kK1S, sC = (t + 1) % kK1S, sN = (t + 2) % kK1S;
+            mbar_wait(&S.full[sN], (unsigned)((t + 2) / kK1S) & 1u);
+            const int64_t arow = (int64_t)(j + A.halo) * P;
+#pragma unroll
+            for (int k = 0; k < kK1W / kK1T; ++k) {
+                const int32_t ic = k * kK1T + tid;                   // column within the strip
+                const int32_t i = col0 + ic;
+                double v = 0.0;
+                if (ic < width && i < ni) {
+                    const int o = ic + 2;
+                    const double doC = S.row[sC][1][o];
+                    const double dC = __fma_rn(beta, doC, S.row[sC][0][o]);
+                    const double dS = __fma_rn(beta, S.row[sS][1][o], S.row[sS][0][o]);
+                    const double dN = __fma_rn(beta, S.row[sN][1][o], S.row[sN][0][o]);
+                    double dW, dE, cEw;
+                    if (i == 0) {
+                        const int q = (ni - 1) & 3;
+                        dW = __fma_rn(beta, S.seamW[sC][1][q], S.seamW[sC][0][q]);
+                        cEw = S.seamW[sC][2][q];
+                    } else {
+                        dW = __fma_rn(beta, S.row[sC][1][o - 1], S.row[sC][0][o - 1]);
+                        cEw = S.row[sC][3][o - 1];
+                    }
+                    if (i == ni - 1) dE = __fma_rn(beta, S.seamE[sC][1][0], S.seamE[sC][0][0]);
+                    else dE = __fma_rn(beta, S.row[sC][1][o + 1], S.row[sC][0][o + 1]);
+                    const double cEp = S.row[sC][3][o];
+                    const double cNr = S.row[sC][4][o];
+                    const double cNs = fabs(S.row[sS][4][o]);
+                    const bool land = signbit(cNr);
+                    const double cNp = fabs(cNr);
+                    double app = __dadd_rn(__dadd_rn(__dadd_rn(cEp, cEw), cNp), cNs);
+                    if constexpr (SIGMA) app = __dadd_rn(app, S.row[sC][5][o]);
+                    double acc = __dmul_rn(app, dC);
+                    acc = __fma_rn(-cEw, dW, acc);
+                    acc = __fma_rn(-cEp, dE, acc);
+                    acc = __fma_rn(-cNs, dS, acc);
+                    acc = __fma_rn(-cNp, dN, acc);
+                    const double qv = land ? 0.0 : acc;
+                    const int64_t a = arow + i;
+                    dnew[a] = dC;
+                    A.q[a] = qv;
+                    A.x[a] = __fma_rn(alpha, doC, S.row[sC][2][o]);
+                    v = __dmul_rn(dC, qv);
+                }
+                v = warp_tree(v);
+                if (lane == 0) S.wsum[j & 1][ic >> 8][(ic & (kBlock - 1)) >> 5] = v;   // canonical (segment, warp)
+            }
+            __syncthreads();                                         // stage t is free; warp sums of row j
+            if (tid == 0 && t + kK1S < R) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                k1t_fill<NA>(S, sS, A, par, j0 - 1 + t + kK1S, col0, lo, hi, seamW, seamE);
+            }
+            if (warp == 0) {
+#pragma unroll
+                for (int k = 0; k < kK1Seg; ++k) {
+                    const int32_t seg = c * kK1Seg + k;
+                    double w = lane < kWarps ? S.wsum[j & 1][k][lane] : 0.0;
+                    w = warp_tree(w);
+                    if (lane == 0 && seg < A.nbx) A.partial[0][(int64_t)j * A.nbx + seg] = w;
+                }
+            }
+        }
+    }
+    pdl_trigger();
+    k1_tail<false>(A);                                     // one rank only (no halo-row stores)
 }
 
 #ifndef PCG_MINB_K1F
@@ -1966,6 +2166,15 @@ void configure_kernels(KArgs& A, int sms) {
     allow_smem(k3_ainv_kernel<8>, row_smem(A, A.g_k3, 1));
     allow_smem(k2_ainv_kernel<16>, row_smem(A, A.g_k2, 1));
     allow_smem(k3_ainv_kernel<16>, row_smem(A, A.g_k3, 1));
+    // K1 bulk-copy form: strips of kK1W columns x row chunks, one block per SM
+    A.k1t_strips = (A.pitch + kK1W - 1) / kK1W;
+    {
+        const int nch = std::max(1, sms * PCG_K1T_MINB / A.k1t_strips);
+        A.k1t_rows = (A.nloc + nch - 1) / nch;
+        A.g_k1t = A.k1t_strips * ((A.nloc + A.k1t_rows - 1) / A.k1t_rows);
+    }
+    allow_smem(k1_tma_kernel<false>, k1t_smem_bytes<false>());
+    allow_smem(k1_tma_kernel<true>, k1t_smem_bytes<true>());
     allow_smem(k2_diag_kernel<false>, row_smem(A, A.g_kd, 2));
     allow_smem(k2_diag_kernel<true>, row_smem(A, A.g_kd, 2));
     allow_smem(k1_kernel<false, true>, k1_smem(A, A.g_k1));
@@ -2012,6 +2221,11 @@ static void launch_pdl(const KArgs& A, void (*kern)(P...), int grid, int block, 
 }
 
 void launch_k1(const KArgs& A, int par, cudaStream_t st) {
+    if (A.k1tma) {
+        if (A.sigma) launch_pdl(A, k1_tma_kernel<true>, A.g_k1t, kK1T, k1t_smem_bytes<true>(), st, A, par);
+        else launch_pdl(A, k1_tma_kernel<false>, A.g_k1t, kK1T, k1t_smem_bytes<false>(), st, A, par);
+        return;
+    }
     if (A.k1flat) {
         const size_t sm = A.k1flat == 2 ? row_smem(A, A.g_k1f, 1) : 0;
         if (A.dc) {

@@ -122,6 +122,8 @@ struct KArgs {
     uint32_t* dc_seq;                 // this rank's reduction counter (persists across solves)
     int32_t dc;
     int32_t rank;                     // this rank (multi-rank path)
+    // K1 bulk-copy form (k1_tma_kernel; one rank): strips of kK1W columns x chunks of k1t_rows rows
+    int32_t k1tma, k1t_strips, k1t_rows, g_k1t;
 };
 
 int64_t grid_blocks(const KArgs& A);

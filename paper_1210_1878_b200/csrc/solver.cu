@@ -1132,6 +1132,9 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     // iteration at cfg5); with the window the row-segment form wins (80.7 against 83.2 at cfg4).
     // Both forms are bitwise equal (all preconditioners).  PCG_K1FLAT overrides.
     if (!c->multi && A.l2_bytes == 0 && A.k1flat == 2 && !getenv("PCG_K1FLAT")) A.k1flat = 0;
+    // K1 as the bulk-copy stencil where the strip form would run (one rank, no L2 window: cfg5)
+    A.k1tma = (!c->multi && A.k1flat == 0) ? 1 : 0;
+    if (const char* e = getenv("PCG_K1TMA")) A.k1tma = !c->multi && atoi(e) != 0;
     // redundant-sum mode (kernels.h): one rank, the K1 row-segment form, K2 / K3 as two launches
     A.redundant = 0;
     if (P.factored() && !c->multi && (A.k1flat == 2 || (A.k1flat == 0 && !A.dynamic_k1))) {

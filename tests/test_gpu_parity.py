@@ -441,8 +441,13 @@ def test_local_ranks_pb2_bitwise():
 
 
 # ------------------------------------------------------ kernel-form variants (setup-time switches)
-VARIANTS = {"no_l2_window": {"PCG_L2PERSIST": "0"}, "k1_strips": {"PCG_K1FLAT": "0"}, "no_redundant": {"PCG_REDUNDANT": "0"},
-            "graph_driver": {"PCG_RS": "0"}}
+# graph-driver kernel forms (PCG_RS=0: the resident-strip driver is the default on these grids)
+VARIANTS = {"graph_driver": {"PCG_RS": "0"},
+            "graph_no_l2_window": {"PCG_RS": "0", "PCG_L2PERSIST": "0"},          # picks the bulk-copy K1
+            "graph_k1_strips": {"PCG_RS": "0", "PCG_K1FLAT": "0", "PCG_K1TMA": "0"},
+            "graph_k1_tma": {"PCG_RS": "0", "PCG_K1TMA": "1"},
+            "graph_no_redundant": {"PCG_RS": "0", "PCG_REDUNDANT": "0"},
+            "graph_k1_tma_no_redundant": {"PCG_RS": "0", "PCG_K1TMA": "1", "PCG_REDUNDANT": "0"}}
 
 
 @pytest.mark.parametrize("variant", sorted(VARIANTS))
@@ -465,7 +470,8 @@ def test_kernel_variants_bitwise_canonical(name, variant, monkeypatch):
     S.close()
 
 
-@pytest.mark.parametrize("env", [{"PCG_K1FLAT": "0"}, {"PCG_L2PERSIST": "0"}, {}])
+@pytest.mark.parametrize("env", [{"PCG_RS": "0", "PCG_K1FLAT": "0", "PCG_K1TMA": "0"}, {"PCG_RS": "0", "PCG_L2PERSIST": "0"},
+                                 {"PCG_RS": "0", "PCG_K1TMA": "1"}, {"PCG_RS": "0"}, {}])
 @pytest.mark.parametrize("precond", ["jacobi", "none"])
 def test_diag_k1_forms_bitwise_canonical(precond, env, monkeypatch):
     """Jacobi / none on the graph path (cfg3) with either K1 form: the 4-row strips (forced, or
@@ -701,13 +707,23 @@ def test_cg1_comm_path_matches_single_rank(method):
     S2.close()
 
 
-@pytest.mark.parametrize("kind", ["nonperiodic_sigma", "ragged_wide"])
-def test_graph_path_edge_grids_bitwise(kind):
+@pytest.mark.parametrize("k1", ["default", "tma", "tma_no_window"])
+@pytest.mark.parametrize("kind", ["nonperiodic_sigma", "ragged_wide", "multistrip"])
+def test_graph_path_edge_grids_bitwise(kind, k1, monkeypatch):
     """Grids past the cooperative-loop threshold (> 64 units) with the features the ORCA configs
-    lack -- no E-W wrap with a diagonal shift, and a row length far from a multiple of 256 -- run
-    through the WHILE graph with redundant sums and the L2 window, bitwise the oracle's."""
+    lack -- no E-W wrap with a diagonal shift, a row length far from a multiple of 256, several
+    bulk-copy K1 strips with a narrow last one (ni = 1101: strips of 512, 512, 96 columns) -- run
+    through the WHILE graph (redundant sums, with and without the L2 window; row-segment or
+    bulk-copy K1), bitwise the oracle's."""
+    monkeypatch.setenv("PCG_RS", "0")
+    if k1 != "default":
+        monkeypatch.setenv("PCG_K1TMA", "1")
+    if k1 == "tma_no_window":
+        monkeypatch.setenv("PCG_L2PERSIST", "0")
     if kind == "nonperiodic_sigma":
         p = synth.random_grid(100, 90, 11, periodic=False, sigma=True)
+    elif kind == "multistrip":
+        p = synth.random_grid(1101, 50, 13)
     else:
         p = synth.random_grid(300, 40, 12)
     A, S, ref, x, k, hist, rep, _ = _canonical_pair(p, "ainv", 1e-10)
