@@ -22,6 +22,20 @@ namespace pcg {
 constexpr int kDcMaxRanks = 32;
 constexpr size_t kDcStampBytes = 2 * kDcMaxRanks * sizeof(uint32_t);
 constexpr size_t kDcWindowBytes = kDcStampBytes + 2 * kDcMaxRanks * 4 * sizeof(double);
+constexpr size_t kDcSOffset = 4096;                 // the s array in the window (halo stores)
+
+// host side of the window setup (devcomm.cu)
+struct DcHalo {
+    bool on;                                        // s in the window, halo rows stored by K3
+    int64_t nloc, nel, pitch, halo;                 // this rank's owned rows, s elements, pitch, halo rows
+};
+struct DcOut {
+    void *win_buf = nullptr, *win = nullptr;
+    char** peers = nullptr;                         // [nranks] window bases (device array)
+    uint32_t* seq = nullptr;
+    double* s = nullptr;                            // this rank's s array inside the window
+    double *south = nullptr, *north = nullptr;      // rank-1's northern / rank+1's southern halo row of s
+};
 
 #ifdef __CUDACC__
 __device__ __forceinline__ void dc_st_release_sys(uint32_t* p, uint32_t v) {

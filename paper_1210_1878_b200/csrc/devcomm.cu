@@ -9,8 +9,10 @@
 #include <nccl.h>
 #include <nccl_device.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "dev_comm.cuh"
 #include "../../include/libpcg.h"
@@ -20,8 +22,13 @@ void set_thread_error(const std::string& m);
 
 namespace {
 
-__global__ void dc_peer_kernel(ncclWindow_t win, int P, char** out) {
+__global__ void dc_peer_kernel(ncclWindow_t win, int P, char** out, int rank, int64_t south_off, int64_t north_off,
+                               double** halo) {
     for (int p = threadIdx.x; p < P; p += blockDim.x) out[p] = static_cast<char*>(ncclGetPeerPointer(win, 0, p));
+    if (threadIdx.x == 0) {
+        halo[0] = south_off >= 0 ? static_cast<double*>(ncclGetPeerPointer(win, (size_t)south_off, rank - 1)) : nullptr;
+        halo[1] = north_off >= 0 ? static_cast<double*>(ncclGetPeerPointer(win, (size_t)north_off, rank + 1)) : nullptr;
+    }
 }
 
 // P virtual ranks in one cooperative launch (block r = rank r, thread 0 does the protocol), over
@@ -62,9 +69,12 @@ __global__ void dc_selftest_kernel(char* base, int P, int rounds, uint64_t seed,
 
 }  // namespace
 
-// window + peer pointers of one context; called collectively by every rank of the communicator
-int dc_setup(ncclComm_t comm, int nranks, void** win_buf, void** win, char*** peers, uint32_t** seq, cudaStream_t st,
-             std::string& err) {
+// window + peer pointers of one context; called collectively by every rank of the communicator.
+// With halo stores (DcHalo::on) the window also holds this rank's s array (the vector K3 writes
+// and the next K1's stencil reads on the halo rows): region [kDcSOffset, kDcSOffset + 8 * max_r
+// nel_r) on every rank, and the pointers to the rows of the neighbours' s arrays this rank's first
+// and last owned rows are copied into (their northern / southern halo rows) are read here once.
+int dc_setup(ncclComm_t comm, int nranks, int rank, const DcHalo& h, DcOut& out, cudaStream_t st, std::string& err) {
     if (nranks > kDcMaxRanks) { err = "device comm: at most 32 ranks"; return PCG_ERR_ARG; }
     const ncclTeam_t lsa = ncclTeamLsa(comm);
     if (lsa.nRanks != nranks) {
@@ -72,16 +82,33 @@ int dc_setup(ncclComm_t comm, int nranks, void** win_buf, void** win, char*** pe
               std::to_string(lsa.nRanks) + " of " + std::to_string(nranks) + " ranks";
         return PCG_ERR_COMM;
     }
+    // every rank's (nloc, nel) -- the neighbours' halo rows and the largest s array
+    int64_t* dinfo = nullptr;
+    if (cudaMalloc(&dinfo, sizeof(int64_t) * 2 * nranks) != cudaSuccess) { err = "device comm: cudaMalloc failed"; return PCG_ERR_CUDA; }
+    const int64_t mine[2] = {h.nloc, h.nel};
+    cudaMemcpyAsync(dinfo + 2 * rank, mine, sizeof(mine), cudaMemcpyHostToDevice, st);
+    ncclResult_t r = ncclAllGather(dinfo + 2 * rank, dinfo, 2, ncclInt64, comm, st);
+    std::vector<int64_t> info((size_t)2 * nranks);
+    if (r != ncclSuccess || cudaMemcpyAsync(info.data(), dinfo, sizeof(int64_t) * 2 * nranks, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+        cudaStreamSynchronize(st) != cudaSuccess) {
+        cudaFree(dinfo);
+        err = std::string("device comm: setup allgather failed: ") + ncclGetErrorString(r);
+        return PCG_ERR_COMM;
+    }
+    cudaFree(dinfo);
+    int64_t max_nel = 0;
+    for (int q = 0; q < nranks; ++q) max_nel = std::max<int64_t>(max_nel, info[(size_t)2 * q + 1]);
+    const size_t bytes = h.on ? kDcSOffset + (size_t)max_nel * sizeof(double) : kDcWindowBytes;
     void* buf = nullptr;
-    ncclResult_t r = ncclMemAlloc(&buf, kDcWindowBytes);
+    r = ncclMemAlloc(&buf, bytes);
     if (r != ncclSuccess) { err = std::string("ncclMemAlloc: ") + ncclGetErrorString(r); return PCG_ERR_COMM; }
-    if (cudaMemsetAsync(buf, 0, kDcWindowBytes, st) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+    if (cudaMemsetAsync(buf, 0, bytes, st) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
         ncclMemFree(buf);
         err = "device comm: window memset failed";
         return PCG_ERR_CUDA;
     }
     ncclWindow_t w = nullptr;
-    r = ncclCommWindowRegister(comm, buf, kDcWindowBytes, &w, NCCL_WIN_COLL_SYMMETRIC);
+    r = ncclCommWindowRegister(comm, buf, bytes, &w, NCCL_WIN_COLL_SYMMETRIC);
     if (r != ncclSuccess) {
         ncclMemFree(buf);
         err = std::string("ncclCommWindowRegister: ") + ncclGetErrorString(r);
@@ -89,21 +116,35 @@ int dc_setup(ncclComm_t comm, int nranks, void** win_buf, void** win, char*** pe
     }
     char** pp = nullptr;
     uint32_t* sq = nullptr;
-    if (cudaMalloc(&pp, sizeof(char*) * nranks) != cudaSuccess || cudaMalloc(&sq, sizeof(uint32_t)) != cudaSuccess) {
+    double** hp = nullptr;
+    if (cudaMalloc(&pp, sizeof(char*) * nranks) != cudaSuccess || cudaMalloc(&sq, sizeof(uint32_t)) != cudaSuccess ||
+        cudaMalloc(&hp, 2 * sizeof(double*)) != cudaSuccess) {
         ncclCommWindowDeregister(comm, w);
         ncclMemFree(buf);
         err = "device comm: cudaMalloc failed";
         return PCG_ERR_CUDA;
     }
     cudaMemsetAsync(sq, 0, sizeof(uint32_t), st);
-    dc_peer_kernel<<<1, 32, 0, st>>>(w, nranks, pp);
-    // every rank's window is zero before any rank can publish into it
+    // neighbours' halo rows: rank-1's northern one (array row H + nloc_{r-1}), rank+1's southern
+    // one (array row H - 1); the pitch and H are the same on every rank
+    const int64_t south_off = rank > 0 ? (int64_t)kDcSOffset + (h.halo + info[(size_t)2 * (rank - 1)]) * h.pitch * 8 : -1;
+    const int64_t north_off = rank < nranks - 1 ? (int64_t)kDcSOffset + (int64_t)(h.halo - 1) * h.pitch * 8 : -1;
+    dc_peer_kernel<<<1, 32, 0, st>>>(w, nranks, pp, rank, h.on ? south_off : -1, h.on ? north_off : -1, hp);
+    double* hh[2] = {nullptr, nullptr};
+    if (cudaMemcpyAsync(hh, hp, sizeof(hh), cudaMemcpyDeviceToHost, st) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
+        err = "device comm: peer pointers";
+        return PCG_ERR_CUDA;
+    }
+    cudaFree(hp);
+    // every rank's window is zero before any rank can store into it
     r = ncclAllReduce(sq, sq, 1, ncclUint32, ncclSum, comm, st);   // sq = 0 on every rank: stays 0
     if (r != ncclSuccess || cudaStreamSynchronize(st) != cudaSuccess) {
         err = std::string("device comm: setup barrier failed: ") + ncclGetErrorString(r);
         return PCG_ERR_COMM;
     }
-    *win_buf = buf; *win = (void*)w; *peers = pp; *seq = sq;
+    out.win_buf = buf; out.win = (void*)w; out.peers = pp; out.seq = sq;
+    out.s = h.on ? reinterpret_cast<double*>(static_cast<char*>(buf) + kDcSOffset) : nullptr;
+    out.south = hh[0]; out.north = hh[1];
     return PCG_OK;
 }
 

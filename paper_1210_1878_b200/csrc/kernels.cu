@@ -167,6 +167,7 @@ __device__ __noinline__ void dc_collect_step(const SArgs S, int step) {
     scalar_step(S, step);
 }
 
+
 // ---- scalar updates (one thread) --------------------------------------------------------
 template <class KA>
 __device__ void fin_bb(const KA& A, double bb) {
@@ -283,6 +284,21 @@ __device__ __forceinline__ Unit unit_of(const KArgs& A, int64_t u) {
     W.live = W.inrow;
     W.a = (int64_t)(W.j + A.halo) * A.pitch + W.i;
     return W;
+}
+
+// device comm with halo stores: a point of the first / last owned row also goes to the
+// neighbour's halo row (NVLink store into its window); before the block's completion count, a
+// system-scope fence orders the block's stores before the count -> the last block's stamp ->
+// the neighbour's acquire of it, so the neighbour's next K1 reads them
+__device__ __forceinline__ void dc_halo_store(const KArgs& A, const Unit& W, double v) {
+    if (!A.dch) return;
+    if (W.j == 0 && A.dch_south) A.dch_south[W.i] = v;
+    if (W.j == A.nloc - 1 && A.dch_north) A.dch_north[W.i] = v;
+}
+__device__ __forceinline__ void dc_halo_fence(const KArgs& A) {
+    if (!A.dch) return;
+    __syncthreads();
+    if (threadIdx.x == 0) __threadfence_system();
 }
 
 // warp sum of v for local slot k (shared memory ws[k][warp])
@@ -1317,6 +1333,7 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
             else if constexpr (DQ < 0) acc = ell_row16(A.z, W.a - A.hoff, W.a, [&](int32_t g) { return __ldg(t + g); });
             else acc = ell_row(A.z, W.a - A.hoff, [&](int32_t g) { return __ldg(t + g); });
             A.s[W.a] = acc;
+            if constexpr (DC) dc_halo_store(A, W, acc);
             v = __dmul_rn(acc, rv);
         }
         return v;
@@ -1331,17 +1348,20 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
         pdl_trigger();
         TL(2, 2);
         if (A.redundant) return;                         // (s, r) is summed by the next K1's blocks
+        if constexpr (DC) dc_halo_fence(A);
         last = count_block(&A.sc->counter[2]);
     } else if (A.dynamic) {
         dynamic_units(A, &A.sc->ticket[2], A.partial[2], body);
         pdl_trigger();
         TL(2, 2);
         if (A.redundant) return;
+        if constexpr (DC) dc_halo_fence(A);
         last = count_block(&A.sc->counter[2]);
     } else {
         const int64_t U = n_units(A);
         int k = 0;
         for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k) put_warp_sum(ws, k, body(unit_of(A, u)));
+        if constexpr (DC) dc_halo_fence(A);
         last = finish_units<1>(A, ws, A.partial[2], nullptr, A.redundant ? nullptr : &A.sc->counter[2]);
     }
     if (last) {
@@ -1646,6 +1666,7 @@ __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const in
                 const double rnew = __fma_rn(-alpha, qv[m], rv[m]);
                 const double sv = none ? rnew : __ddiv_rn(rnew, dv[m]);
                 A.s[W[m].a] = sv;
+                if constexpr (DC) dc_halo_store(A, W[m], sv);
                 rn[W[m].a] = rnew;
                 v1 = __dmul_rn(rnew, rnew);
                 v2 = __dmul_rn(sv, rnew);
@@ -1655,6 +1676,7 @@ __global__ void __launch_bounds__(kBlock) k2_diag_kernel(const KArgs A, const in
         }
     }
     pdl_trigger();
+    if constexpr (DC) dc_halo_fence(A);
     if (finish_units<2>(A, ws, A.partial[1], A.partial[2], &A.sc->counter[1])) {
         double rr, rs;                                     // both walks in one pass (same sums)
         final_sum_pair<PCG_FINAL_NB_K3>(A.partial[1], A.partial[2], n_units(A), rr, rs);

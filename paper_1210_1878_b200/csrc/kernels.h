@@ -122,6 +122,9 @@ struct KArgs {
     uint32_t* dc_seq;                 // this rank's reduction counter (persists across solves)
     int32_t dc;
     int32_t rank;                     // this rank (multi-rank path)
+    int32_t dch;                      // device comm with halo stores: K3 / k2_diag write s's first / last
+    double* dch_south;                //   owned row into rank-1's northern / rank+1's southern halo row
+    double* dch_north;                //   (peer pointers into the window; null at the ends)
     // K1 bulk-copy form (k1_tma_kernel; one rank): strips of kK1W columns x chunks of k1t_rows rows
     int32_t k1tma, k1t_strips, k1t_rows, g_k1t;
 };

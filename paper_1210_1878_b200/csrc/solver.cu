@@ -17,6 +17,7 @@
 
 #include "internal.h"
 #include "kernels.h"
+#include "dev_comm.cuh"
 
 using namespace pcg;
 
@@ -26,8 +27,7 @@ void set_thread_error(const std::string& m) { g_last_error = m; }
 }  // namespace pcg
 
 namespace pcg {
-int dc_setup(ncclComm_t comm, int nranks, void** win_buf, void** win, char*** peers, uint32_t** seq, cudaStream_t st,
-             std::string& err);
+int dc_setup(ncclComm_t comm, int nranks, int rank, const DcHalo& h, DcOut& out, cudaStream_t st, std::string& err);
 void dc_free(ncclComm_t comm, void* win_buf, void* win, char** peers, uint32_t* seq);
 }  // namespace pcg
 
@@ -254,6 +254,7 @@ struct Step {
 // With device comm (A.dc) the rank sums are gathered inside the reduction kernels and the
 // scalar step runs there too: the allgather leaves every exchange and the scalar kernels go.
 void exch(std::vector<Step>& s, const pcg_ctx* c, Ex ex, int par = 0) {
+    if (c->A.dch && (ex == Ex::HaloSAllgather || ex == Ex::HaloS)) return;   // K3 stored s's halo rows itself
     if (c->A.dc) {
         if (ex == Ex::Allgather) return;
         if (ex == Ex::HaloSAllgather) ex = Ex::HaloS;
@@ -1106,6 +1107,8 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
     A.dc = 0;
     A.dc_peer = nullptr;
     A.dc_seq = nullptr;
+    A.dch = 0;
+    A.dch_south = A.dch_north = nullptr;
     if (P.flags & PCG_FLAG_DEVICE_COMM) {
         // device comm: the NCCL path only (the local-ranks emulation runs its
         // ranks one after another, so no rank may wait on another inside a kernel)
@@ -1113,11 +1116,26 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
             return Status::err(PCG_ERR_ARG, "pcg_setup: PCG_FLAG_DEVICE_COMM needs the NCCL path (nccl_comm; "
                                             "nranks > 1 or PCG_FLAG_COMM_PATH), not PCG_FLAG_LOCAL_RANKS");
         std::string err;
-        const int rc = dc_setup(c->comm, P.nranks, &c->dc_buf, &c->dc_win, &c->dc_peers, &c->dc_seq, c->st, err);
+        // halo stores (s rows written into the neighbours' halo rows by K3 / k2_diag): Alg. 1 with
+        // block-local or global Z (no halo-AINV exchanges), not the CG-CG / pipelined forms
+        DcHalo h{};
+        h.on = P.halo_w == 0 && !(P.flags & (PCG_FLAG_SINGLE_REDUCTION | PCG_FLAG_PIPELINED));
+        if (const char* e = getenv("PCG_DC_HALO")) h.on = h.on && atoi(e) != 0;
+        h.nloc = P.nloc; h.nel = P.elements(); h.pitch = P.pitch; h.halo = P.halo;
+        DcOut o;
+        const int rc = dc_setup(c->comm, P.nranks, P.rank, h, o, c->st, err);
         if (rc != PCG_OK) return Status::err((pcg_status)rc, "pcg_setup: " + err);
+        c->dc_buf = o.win_buf; c->dc_win = o.win; c->dc_peers = o.peers; c->dc_seq = o.seq;
         A.dc = 1;
         A.dc_peer = c->dc_peers;
         A.dc_seq = c->dc_seq;
+        if (h.on) {                    // s lives in the window from now on (zero, like the hot block's)
+            c->s = o.s;
+            A.s = c->s;
+            A.dch = 1;
+            A.dch_south = o.south;
+            A.dch_north = o.north;
+        }
     }
     A.use_cond = 0;
     A.precond = P.factored() ? 0 : (int32_t)P.precond;
