@@ -94,7 +94,7 @@ typedef enum {
                                     and runs the scalar step (rank tree, alpha / beta, stop test)
                                     inline -- instead of a host-enqueued ncclAllGather and a
                                     scalar kernel (bitwise the same results).  For
-                                    Alg. 1 with ainv_halo = 0 (or the global Z) the s array also
+                                    Alg. 1 with block-local AINV (ainv_halo = 0) the s array also
                                     lives in the window and K3 stores its first / last owned row
                                     into the neighbours' halo rows itself: no NCCL call per
                                     iteration (PCG_DC_HALO=0 keeps the NCCL halo).  Needs
