@@ -397,7 +397,7 @@ def main():
 
     # launches per solve: prologue 4 (prep, init, K2, K3) + WHILE bodies of PCG_BODY_ITERS (8)
     # iterations x 3 + epilogue 2; the resident-strip driver: prologue + 1 + epilogue
-    per_iter = 3 if args.precond in ("ainv", "fsai") else 2
+    per_iter = int(rep.get("kernels_per_iter", 0)) or (3 if args.precond in ("ainv", "fsai") else 2)
     pro = 4 if args.precond in ("ainv", "fsai") else 3
     extra = 0
     if args.method in ("cg1", "pipe"):

@@ -166,7 +166,9 @@ typedef struct {
                                   host loop; several ranks -- the NCCL graph, or the NCCL host loop
                                   when the graph could not be captured (PCG_DRIVER_NCCL_FALLBACK: the
                                   capture failure is reported here, not hidden) */
-    int32_t reserved;
+    int32_t kernels_per_iter;  /* this library's kernel launches per iteration of the driver used
+                                  (graph / host loop: the iteration's kernels incl. scalar steps;
+                                  resident strips and the cooperative loop: 0 -- one kernel per solve) */
 } pcg_report;
 
 enum { PCG_DRIVER_GRAPH = 0, PCG_DRIVER_LOOP = 1, PCG_DRIVER_RESIDENT = 2, PCG_DRIVER_HOST_LOOP = 3,
@@ -256,7 +258,9 @@ pcg_status pcg_layout(const pcg_ctx* ctx, int32_t* pitch, int32_t* block, int32_
  * context's stream with CUDA events around every launch, on the state left by the last
  * solve (a profiling aid for bench.py).  ms_out[0..3] = median per-launch time of K1
  * (stencil), K2 (r update + Z^T gather), K3 (Z gather), and of the whole iteration; bytes_out[0..2] = algorithmic bytes per
- * launch of K1..K3.  Single rank only. */
+ * launch of K1..K3.  With the kfin reduction kernels (large grids) K1's and
+ * K3's times include their kfin launch, as they otherwise include their last-block tails.
+ * Single rank only. */
 pcg_status pcg_kernel_times(pcg_ctx* ctx, int32_t n_iter, double* ms_out, double* bytes_out);
 
 /* Device bytes allocated by the context. */

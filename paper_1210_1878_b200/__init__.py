@@ -60,10 +60,10 @@ class Report(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("rel_residual", C.c_double),
                 ("true_rel_residual", C.c_double), ("setup_s", C.c_double), ("solve_s", C.c_double),
                 ("bytes_per_iter", C.c_double), ("n_ocean", C.c_int64), ("nnz_z", C.c_int64),
-                ("failed_index", C.c_int64), ("driver", C.c_int32), ("reserved", C.c_int32)]
+                ("failed_index", C.c_int64), ("driver", C.c_int32), ("kernels_per_iter", C.c_int32)]
 
     def as_dict(self):
-        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        d = {k: getattr(self, k) for k, _ in self._fields_}
         d["driver_name"] = DRIVERS.get(d["driver"], str(d["driver"]))
         return d
 

@@ -532,7 +532,7 @@ __device__ __forceinline__ bool k1_beta(const KArgs& A, int par, double& beta) {
 // blocks; Jacobi / none: k2_diag's blocks; otherwise the last block (rank sum on the NCCL path).
 template <bool DC>
 __device__ __forceinline__ void k1_tail(const KArgs& A) {
-    if (A.redundant) return;                           // (d, q) is summed by K2's blocks
+    if (A.redundant || A.kfin) return;                 // (d, q) is summed by K2's blocks / by kfin
     if (A.red_gamma) {                                 // Jacobi / none: k2_diag's blocks sum (d, q)
         if (blockIdx.x == 0 && threadIdx.x == 0) A.sc->xpend = 0;   // x += alpha_prev d_old done
         return;
@@ -944,11 +944,11 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K1F) k1_flat_kernel(const KAr
         for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k)
             put_warp_sum(ws, k, k1_point<SIGMA>(A, unit_of(A, u), par, beta, alpha));
         pdl_trigger();
-        last = finish_units<1>(A, ws, A.partial[0], nullptr, &A.sc->counter[0]);
+        last = finish_units<1>(A, ws, A.partial[0], nullptr, A.kfin ? nullptr : &A.sc->counter[0]);
     } else {
         dynamic_units(A, &A.sc->ticket[0], A.partial[0], [&](const Unit& W) { return k1_point<SIGMA>(A, W, par, beta, alpha); });
         pdl_trigger();
-        last = count_block(&A.sc->counter[0]);
+        last = A.kfin ? false : count_block(&A.sc->counter[0]);
     }
     if (last) {
         const double tot = final_sum(A.partial[0], n_units(A));
@@ -1347,14 +1347,14 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
         dynamic_units(A, &A.sc->ticket[2], A.partial[2], body, A.sched_u0);
         pdl_trigger();
         TL(2, 2);
-        if (A.redundant) return;                         // (s, r) is summed by the next K1's blocks
+        if (A.redundant || (A.kfin && !init)) return;    // (s, r) is summed by the next K1's blocks / kfin
         if constexpr (DC) dc_halo_fence(A);
         last = count_block(&A.sc->counter[2]);
     } else if (A.dynamic) {
         dynamic_units(A, &A.sc->ticket[2], A.partial[2], body);
         pdl_trigger();
         TL(2, 2);
-        if (A.redundant) return;
+        if (A.redundant || (A.kfin && !init)) return;
         if constexpr (DC) dc_halo_fence(A);
         last = count_block(&A.sc->counter[2]);
     } else {
@@ -1362,12 +1362,78 @@ __global__ void __launch_bounds__(kBlock, PCG_MINB_K3) k3_ainv_kernel(const KArg
         int k = 0;
         for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++k) put_warp_sum(ws, k, body(unit_of(A, u)));
         if constexpr (DC) dc_halo_fence(A);
-        last = finish_units<1>(A, ws, A.partial[2], nullptr, A.redundant ? nullptr : &A.sc->counter[2]);
+        last = finish_units<1>(A, ws, A.partial[2], nullptr, (A.redundant || (A.kfin && !init)) ? nullptr : &A.sc->counter[2]);
     }
     if (last) {
         k3_finish<DC>(A, init);
         TL(2, 3);
     }
+}
+
+// ---- kfin: the reduction tails of the large grids (cfg5, one rank, PCG_KFIN) ----------------------
+// At cfg5 a reduction has 52 k partials; the last block of K1 / K3 walks them with 256 threads
+// and few loads in flight (~15 us per reduction), and the redundant-sum mode makes every block of
+// the consumer read all of them (L2-bound).  kfin is one block of 1024 threads between the
+// kernels: all threads load a window of partials into shared memory (24 loads each in flight),
+// then threads t < 256 add their chains t, t + 256, ... from shared memory in order -- the
+// canonical final sum of DESIGN.md §5.2, bitwise -- and thread 0 does the last block's scalars.
+#ifndef PCG_KFIN_WIN
+#define PCG_KFIN_WIN 24576                           // doubles per window (192 KB), a multiple of 256
+#endif
+constexpr int kKfinT = 1024;
+constexpr int kKfinWin = PCG_KFIN_WIN;
+static_assert(kKfinWin % kBlock == 0 && kKfinWin % kKfinT == 0, "kfin window");
+
+__device__ __forceinline__ double kfin_sum(const double* partial, int64_t G, double* win) {
+    double acc = 0.0;
+    for (int64_t w0 = 0; w0 < G; w0 += kKfinWin) {
+        const int n = (int)((G - w0) < kKfinWin ? (G - w0) : kKfinWin);
+        double v[kKfinWin / kKfinT];
+#pragma unroll
+        for (int u = 0; u < kKfinWin / kKfinT; ++u) {
+            const int k = threadIdx.x + u * kKfinT;
+            v[u] = k < n ? __ldcg(partial + w0 + k) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kKfinWin / kKfinT; ++u) {
+            const int k = threadIdx.x + u * kKfinT;
+            if (k < n) win[k] = v[u];
+        }
+        __syncthreads();
+        if (threadIdx.x < kBlock)
+            for (int m = threadIdx.x; m < n; m += kBlock) acc = __dadd_rn(acc, win[m]);
+        __syncthreads();
+    }
+    return block_tree(acc);                                  // threads >= 256 add nothing
+}
+
+// which = 0: (d, q) after K1 -> red[0] (K2 forms alpha); which = 1: (s, r) after K3 -> fin_iter
+__global__ void __launch_bounds__(kKfinT, 1) kfin_kernel(const KArgs A, const int which) {
+    pdl_wait();
+    if (!is_active(A)) return;
+    extern __shared__ double kfin_win[];
+    DevScalars* sc = A.sc;
+    if (which == 0) {
+        const double tot = kfin_sum(A.partial[0], n_units(A), kfin_win);
+        if (threadIdx.x == 0) {
+            sc->red[0] = tot;
+            sc->xpend = 0;                                   // K1 did x += alpha_prev d_old
+            sc->counter[0] = 0;
+            sc->ticket[0] = 0;
+        }
+    } else {
+        FinPre pre{};
+        if (threadIdx.x == 0) pre = fin_prefetch(A);
+        const double rs = kfin_sum(A.partial[2], n_units(A), kfin_win);
+        if (threadIdx.x == 0) {
+            sc->counter[1] = 0;
+            sc->ticket[1] = 0;
+            sc->counter[2] = 0;
+            sc->ticket[2] = 0;
+            fin_iter(A, rs, pre);
+        }
+    }
+    pdl_trigger();
 }
 
 // final_sum over two partial arrays in one walk (each sum in final_sum's order: bitwise the same)
@@ -2206,6 +2272,7 @@ void configure_kernels(KArgs& A, int sms) {
     allow_smem(ka_cg_kernel, row_smem(A, A.g_k2, 1));
     allow_smem(kc_cg_kernel, row_smem(A, A.g_row, 1));
     allow_smem(kpc_kernel, row_smem(A, A.g_row, 3));
+    allow_smem(kfin_kernel, (size_t)kKfinWin * sizeof(double));
     allow_smem(init_residual_kernel, row_smem(A, A.g_row, 1));
     allow_smem(true_residual_kernel, row_smem(A, A.g_row, 1));
 }
@@ -2266,6 +2333,9 @@ void launch_k1(const KArgs& A, int par, cudaStream_t st) {
 void launch_kc(const KArgs& A, int par, int init, cudaStream_t st) {
     (void)par;
     launch_pdl(A, kc_cg_kernel, A.g_row, kBlock, row_smem(A, A.g_row, 1), st, A, init);
+}
+void launch_kfin(const KArgs& A, int which, cudaStream_t st) {
+    launch_pdl(A, kfin_kernel, 1, kKfinT, (size_t)kKfinWin * sizeof(double), st, A, which);
 }
 void launch_kpa(const KArgs& A, cudaStream_t st) { launch_pdl(A, kpa_kernel, A.g_k2, kBlock, 0, st, A); }
 void launch_kpb(const KArgs& A, cudaStream_t st) { launch_pdl(A, kpb_kernel, A.g_k3, kBlock, 0, st, A); }

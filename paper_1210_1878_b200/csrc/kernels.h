@@ -127,6 +127,7 @@ struct KArgs {
     double* dch_north;                //   (peer pointers into the window; null at the ends)
     // K1 bulk-copy form (k1_tma_kernel; one rank): strips of kK1W columns x chunks of k1t_rows rows
     int32_t k1tma, k1t_strips, k1t_rows, g_k1t;
+    int32_t kfin;                     // one rank, large grids: reduction tails in kfin_kernel (no last blocks)
 };
 
 int64_t grid_blocks(const KArgs& A);
@@ -149,6 +150,7 @@ void launch_kc(const KArgs& A, int par, int init, cudaStream_t st);   // CG-CG: 
 // pipelined PCG: KPA t = Dhat^-1 Z^T w (+ the pending reduction's scalars, one rank); KPB m = Z t;
 // KPC n = A m, the eight vector updates, (r,u) (w,u) (r,r)  (init: w = A u and the three dots)
 void launch_kpa(const KArgs& A, cudaStream_t st);
+void launch_kfin(const KArgs& A, int which, cudaStream_t st);   // 0: (d, q) -> red[0]; 1: (s, r) -> fin_iter
 void launch_kpb(const KArgs& A, cudaStream_t st);
 void launch_kpc(const KArgs& A, int init, cudaStream_t st);
 // solve prologue / epilogue

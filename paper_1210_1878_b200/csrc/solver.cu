@@ -339,6 +339,7 @@ std::vector<Step> iteration_steps(const pcg_ctx* c, int par) {
         return s;
     }
     s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k1(x->A, par, x->st); }});
+    if (c->A.kfin) s.push_back({Ex::None, [](pcg_ctx* x) { launch_kfin(x->A, 0, x->st); }});
     if (multi) {
         exch(s, c, hx ? Ex::AllgatherQR : Ex::Allgather, par);
         scalar(s, c, kSsGamma);
@@ -347,6 +348,7 @@ std::vector<Step> iteration_steps(const pcg_ctx* c, int par) {
         s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k2_ainv(x->A, par, 0, x->st); }});
         if (hx) s.push_back({Ex::HaloT, nullptr});
         s.push_back({Ex::None, [par](pcg_ctx* x) { launch_k3_ainv(x->A, par, 0, x->st); }});
+        if (c->A.kfin) s.push_back({Ex::None, [](pcg_ctx* x) { launch_kfin(x->A, 1, x->st); }});
     } else {
         s.push_back({Ex::None, [par, none](pcg_ctx* x) { launch_k2_diag(x->A, par, 0, none, x->st); }});
     }
@@ -647,6 +649,9 @@ Status run_solve(pcg_ctx* c, const double* b, const double* x0, bool host, doubl
     else if (use_rs(c)) R.driver = PCG_DRIVER_RESIDENT;
     else if (use_fused(c)) R.driver = PCG_DRIVER_LOOP;
     else R.driver = use_graph(c) ? PCG_DRIVER_GRAPH : PCG_DRIVER_HOST_LOOP;
+    R.kernels_per_iter = 0;
+    if (R.driver != PCG_DRIVER_RESIDENT && R.driver != PCG_DRIVER_LOOP)
+        for (const Step& st : iteration_steps(c, 0)) R.kernels_per_iter += st.ex == Ex::None ? 1 : 0;
     if (report) *report = R;
     c->solved_once = true;
     if (S.status == kStBreakdown)
@@ -1195,6 +1200,14 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         if (Status st = dalloc(c, c->pm, nel); !st) return st;
         A.p = c->pvec; A.pz = c->pz; A.pq = c->pq; A.pm = c->pm;
     }
+    // kfin (large grids, one rank, factored Alg. 1, not CG-CG / pipelined): the reduction tails in their own kernel
+    A.kfin = 0;
+    {
+        const int64_t U = (int64_t)P.nloc * A.nbx;
+        A.kfin = (!c->multi && P.factored() && !A.cgcg && !A.pipe && U >= 16384) ? 1 : 0;
+        if (const char* e = getenv("PCG_KFIN")) A.kfin = !c->multi && P.factored() && !A.cgcg && !A.pipe && atoi(e) != 0;
+        if (A.kfin) A.redundant = 0;
+    }
     // algorithmic bytes per launch: N_o ocean points, z off-diagonals per column
     const double No = (double)P.n_owned, z = No > 0 ? (double)P.nnz_off / No : 0.0;
     c->bytes_k[0] = 64.0 * No;
@@ -1516,11 +1529,13 @@ pcg_status pcg_kernel_times(pcg_ctx* c, int32_t n_iter, double* ms_out, double* 
             const int par = m & 1;
             cudaEventRecord(ev[4 * m + 0], c->st);
             launch_k1(A, par, c->st);
+            if (A.kfin) launch_kfin(A, 0, c->st);          // K1's reduction tail (kfin mode)
             cudaEventRecord(ev[4 * m + 1], c->st);
             if (ainv) launch_k2_ainv(A, par, 0, c->st);
             else launch_k2_diag(A, par, 0, c->plan.precond == PCG_PRECOND_NONE, c->st);
             cudaEventRecord(ev[4 * m + 2], c->st);
             if (ainv) launch_k3_ainv(A, par, 0, c->st);
+            if (ainv && A.kfin) launch_kfin(A, 1, c->st);  // K3's reduction tail
             cudaEventRecord(ev[4 * m + 3], c->st);
         }
         CU(cudaGetLastError());

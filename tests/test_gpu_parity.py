@@ -447,7 +447,9 @@ VARIANTS = {"graph_driver": {"PCG_RS": "0"},
             "graph_k1_strips": {"PCG_RS": "0", "PCG_K1FLAT": "0", "PCG_K1TMA": "0"},
             "graph_k1_tma": {"PCG_RS": "0", "PCG_K1TMA": "1"},
             "graph_no_redundant": {"PCG_RS": "0", "PCG_REDUNDANT": "0"},
-            "graph_k1_tma_no_redundant": {"PCG_RS": "0", "PCG_K1TMA": "1", "PCG_REDUNDANT": "0"}}
+            "graph_k1_tma_no_redundant": {"PCG_RS": "0", "PCG_K1TMA": "1", "PCG_REDUNDANT": "0"},
+            "graph_kfin": {"PCG_RS": "0", "PCG_KFIN": "1"},
+            "graph_kfin_k1_tma": {"PCG_RS": "0", "PCG_KFIN": "1", "PCG_K1TMA": "1"}}
 
 
 @pytest.mark.parametrize("variant", sorted(VARIANTS))
