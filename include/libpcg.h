@@ -93,11 +93,11 @@ typedef enum {
                                     ncclCommWindowRegister, peer pointers from ncclGetPeerPointer)
                                     and runs the scalar step (rank tree, alpha / beta, stop test)
                                     inline -- instead of a host-enqueued ncclAllGather and a
-                                    scalar kernel (bitwise the same results).  For
-                                    Alg. 1 with block-local AINV (ainv_halo = 0) the s array also
-                                    lives in the window and K3 stores its first / last owned row
-                                    into the neighbours' halo rows itself: no NCCL call per
-                                    iteration (PCG_DC_HALO=0 keeps the NCCL halo).  Needs
+                                    scalar kernel (bitwise the same results).  With
+                                    PCG_DC_HALO=1 (opt-in), for Alg. 1 with block-local AINV
+                                    (ainv_halo = 0), the s array also lives in the window and K3
+                                    stores its first / last owned row into the neighbours' halo
+                                    rows itself: no NCCL call per iteration.  Needs
                                     nccl_comm with every rank load/store reachable (one NVLink
                                     domain, else PCG_ERR_COMM); not with PCG_FLAG_LOCAL_RANKS
                                     (PCG_ERR_ARG).  pcg_setup is then collective over the

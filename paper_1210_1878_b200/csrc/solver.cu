@@ -1124,8 +1124,11 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         // halo stores (s rows written into the neighbours' halo rows by K3 / k2_diag): Alg. 1 with
         // block-local or global Z (no halo-AINV exchanges), not the CG-CG / pipelined forms
         DcHalo h{};
+        // opt-in (PCG_DC_HALO=1) until a run with real peers has exercised it: on one GPU both
+        // neighbour pointers are null, so no test reaches the stores themselves
         h.on = P.halo_w == 0 && !(P.flags & (PCG_FLAG_SINGLE_REDUCTION | PCG_FLAG_PIPELINED));
-        if (const char* e = getenv("PCG_DC_HALO")) h.on = h.on && atoi(e) != 0;
+        const char* he = getenv("PCG_DC_HALO");
+        h.on = h.on && he && atoi(he) != 0;
         h.nloc = P.nloc; h.nel = P.elements(); h.pitch = P.pitch; h.halo = P.halo;
         DcOut o;
         const int rc = dc_setup(c->comm, P.nranks, P.rank, h, o, c->st, err);
