@@ -270,7 +270,7 @@ def main():
     rows = slice(S.j_begin, S.j_end)
     xs = torch.from_numpy(np.ascontiguousarray(synth.xstar(p)[rows])).cuda()
     b = S.apply_operator(xs)                                     # b = A x* through the library
-    maxit = 20 * p.ni * p.nj
+    maxit = S.n_ocean                                            # Alg. 1: k <= n
     stream = torch.cuda.current_stream()
 
     def barrier():
