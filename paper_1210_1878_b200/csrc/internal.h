@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <string>
 #include <functional>
+#include <utility>
 #include <vector>
 
 #include "../../include/libpcg.h"
@@ -29,14 +30,28 @@ struct Status {
     explicit operator bool() const { return code == PCG_OK; }
 };
 
+// std::vector whose elements are left uninitialised by resize: the large setup arrays (hundreds
+// of MB at ORCA12 size) are written -- and their pages first touched -- by the parallel loops
+// that compute them, instead of being zero-filled by one thread first.
+template <class T>
+struct NoInitAlloc : std::allocator<T> {
+    NoInitAlloc() noexcept = default;
+    template <class U> NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
+    template <class U> struct rebind { using other = NoInitAlloc<U>; };
+    template <class U> void construct(U* p) noexcept { ::new ((void*)p) U; }
+    template <class U, class... A> void construct(U* p, A&&... a) { ::new ((void*)p) U(std::forward<A>(a)...); }
+};
+template <class T>
+using bigvec = std::vector<T, NoInitAlloc<T>>;
+
 // SELL-32 matrix over the owned elements: slice s covers owned elements [32 s, 32 s + 32)
 // of one grid row; entry m of lane l is at off[s] + 32 m + l.  A column is stored as the
 // packed grid offset (dj << 16) | (di & 0xffff) from the row's own point, di wrapped into
 // (-ni/2, ni/2] on a periodic grid.  Padding entries: value 0, offset (0, 0).
 struct Sell {
     std::vector<int64_t> off;      // nslices + 1
-    std::vector<double> val;
-    std::vector<int32_t> col;      // array indices (padding: the row's own index)
+    bigvec<double> val;
+    bigvec<int32_t> col;           // array indices (padding: the row's own index)
     int64_t entries() const { return (int64_t)val.size(); }
 };
 
@@ -49,8 +64,8 @@ struct Sell {
 constexpr int kEll = 4;
 struct Ell {
     int64_t n = 0;                 // owned elements
-    std::vector<double> val;       // n * kEll (element-major)
-    std::vector<int32_t> col;      // n * kEll
+    bigvec<double> val;            // n * kEll (element-major)
+    bigvec<int32_t> col;           // n * kEll
     Sell ovf;
     int64_t entries() const { return (int64_t)val.size() + ovf.entries(); }
 };
@@ -75,7 +90,7 @@ struct Plan {
     bool has_sigma = false;
     int64_t n_owned = 0, first_global = 0, nnz_off = 0;
     // per-element arrays, (nloc + 2) * pitch
-    std::vector<double> cE, cN, sigma, diag, piv;
+    bigvec<double> cE, cN, sigma, diag, piv;
     Ell Z, ZT;                     // rows of Z (for s = Z t) and of Z^T (for t = Z^T r)
     // FSAI (NEXT-1) DIA form when every chain link is an E-W neighbour pair: dia[m-1][e] =
     // zhat between owned element e - m and e (the column k = e's entry at row k - m), m = 1..dia_q;
@@ -83,8 +98,10 @@ struct Plan {
     int32_t dia_q = 0;
     std::vector<double> dia;
     // export (owned columns of Zhat, global unknown numbering)
-    std::vector<int64_t> zcolptr, zrow;
-    std::vector<double> zhat, pivots, scale;
+    std::vector<int64_t> zcolptr;
+    bigvec<int64_t> zrow;
+    bigvec<double> zhat;
+    std::vector<double> pivots, scale;
     double setup_s = 0.0;
     int64_t elements() const { return (int64_t)(nloc + 2 * halo) * pitch; }
     int64_t hoff() const { return (int64_t)halo * pitch; }   // array index of owned element 0

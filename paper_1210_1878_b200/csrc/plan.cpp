@@ -6,6 +6,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <thread>
 
 #include "internal.h"
@@ -87,8 +88,8 @@ int64_t global_unknown(const uint8_t* mask, int32_t ni, int64_t g) {
 }
 
 // parallel for over [0, n) in T contiguous ranges (independent iterations only)
-void pfor(int T, int64_t n, const std::function<void(int64_t, int64_t)>& f) {
-    if (n < 100000) T = 1;
+void pfor(int T, int64_t n, const std::function<void(int64_t, int64_t)>& f, int64_t serial_below = 100000) {
+    if (n < serial_below) T = 1;
     T = std::max(1, T);
     std::vector<std::thread> pool;
     for (int t = 1; t < T; ++t) pool.emplace_back(f, n * t / T, n * (t + 1) / T);
@@ -96,30 +97,116 @@ void pfor(int T, int64_t n, const std::function<void(int64_t, int64_t)>& f) {
     for (auto& th : pool) th.join();
 }
 
+// exclusive prefix sum out[0..n] of cnt(i), i in [0, n), in T contiguous ranges (two passes)
+template <class F>
+void pscan(int T, int64_t n, std::vector<int64_t>& out, F cnt) {
+    out.assign((size_t)n + 1, 0);
+    if (n < 100000) T = 1;
+    T = std::max(1, T);
+    std::vector<int64_t> part((size_t)T + 1, 0);
+    auto run = [&](auto&& body) {                        // body(t, [a, b)) on T threads
+        std::vector<std::thread> pool;
+        for (int t = 1; t < T; ++t) pool.emplace_back([&, t] { body(t, n * t / T, n * (t + 1) / T); });
+        body(0, 0, n / T);
+        for (auto& th : pool) th.join();
+    };
+    run([&](int t, int64_t a, int64_t b) {
+        int64_t sum = 0;
+        for (int64_t i = a; i < b; ++i) sum += cnt(i);
+        part[(size_t)t + 1] = sum;
+    });
+    for (int t = 0; t < T; ++t) part[(size_t)t + 1] += part[(size_t)t];
+    run([&](int t, int64_t a, int64_t b) {
+        int64_t acc = part[(size_t)t];
+        for (int64_t i = a; i < b; ++i) { out[(size_t)i] = acc; acc += cnt(i); }
+    });
+    out[(size_t)n] = part[(size_t)T];
+}
+
+// Ocean components each need an anchor (a positive face to land, or sigma > 0; R22):
+// the parallel check -- a lock-free union-find over the ocean-ocean faces with positive
+// coupling, linking the larger root to the smaller, so each root is its component's smallest
+// grid index (the component the sequential walk below would report first) -- then every cell
+// with an anchor marks its root.  true = every component anchored.
+bool anchors_ok_parallel(int T, int32_t ni, int32_t nj, int32_t periodic, const double* cE, const double* cN,
+                         const double* sigma, const uint8_t* mask) {
+    const int64_t ng = (int64_t)ni * nj;
+    std::unique_ptr<std::atomic<int64_t>[]> par(new std::atomic<int64_t>[(size_t)ng]);
+    pfor(T, ng, [&](int64_t a, int64_t b) { for (int64_t g = a; g < b; ++g) par[g].store(g, std::memory_order_relaxed); });
+    auto find = [&](int64_t x) {
+        for (;;) {
+            int64_t p = par[x].load(std::memory_order_relaxed);
+            if (p == x) return x;
+            const int64_t gp = par[p].load(std::memory_order_relaxed);
+            if (gp != p) par[x].compare_exchange_weak(p, gp, std::memory_order_relaxed);   // path halving
+            x = gp;
+        }
+    };
+    auto unite = [&](int64_t a, int64_t b) {
+        for (;;) {
+            a = find(a); b = find(b);
+            if (a == b) return;
+            if (a < b) std::swap(a, b);                  // link the larger root under the smaller
+            int64_t expect = a;
+            if (par[a].compare_exchange_strong(expect, b, std::memory_order_acq_rel)) return;
+        }
+    };
+    pfor(T, ng, [&](int64_t a, int64_t b) {
+        for (int64_t g = a; g < b; ++g) {
+            if (!mask[g]) continue;
+            const int32_t i = (int32_t)(g % ni), j = (int32_t)(g / ni);
+            const int64_t row = (int64_t)j * ni;
+            if (((i + 1 < ni) || periodic) && cE[row + i] > 0.0 && mask[row + (i + 1) % ni]) unite(g, row + (i + 1) % ni);
+            if (j + 1 < nj && cN[row + i] > 0.0 && mask[row + ni + i]) unite(g, row + ni + i);
+        }
+    });
+    std::unique_ptr<std::atomic<uint8_t>[]> anch(new std::atomic<uint8_t>[(size_t)ng]);
+    pfor(T, ng, [&](int64_t a, int64_t b) { for (int64_t g = a; g < b; ++g) anch[g].store(0, std::memory_order_relaxed); });
+    pfor(T, ng, [&](int64_t a, int64_t b) {
+        for (int64_t g = a; g < b; ++g) {
+            if (!mask[g]) continue;
+            const int32_t i = (int32_t)(g % ni), j = (int32_t)(g / ni);
+            const int64_t row = (int64_t)j * ni;
+            bool an = sigma && sigma[g] > 0.0;
+            const bool ex[4] = {(i + 1 < ni) || periodic != 0, (i >= 1) || periodic != 0, j + 1 < nj, j >= 1};
+            const int64_t nb[4] = {row + (i + 1) % ni, row + (i - 1 + ni) % ni, row + ni + i, row - ni + i};
+            const double cf[4] = {cE[row + i], cE[row + (i - 1 + ni) % ni], j + 1 < nj ? cN[row + i] : 0.0,
+                                  j >= 1 ? cN[row - ni + i] : 0.0};
+            for (int f = 0; f < 4 && !an; ++f) an = ex[f] && cf[f] > 0.0 && !mask[nb[f]];
+            if (an) anch[find(g)].store(1, std::memory_order_relaxed);
+        }
+    });
+    std::atomic<bool> ok(true);
+    pfor(T, ng, [&](int64_t a, int64_t b) {
+        for (int64_t g = a; g < b && ok.load(std::memory_order_relaxed); ++g)
+            if (mask[g] && par[g].load(std::memory_order_relaxed) == g && !anch[g].load(std::memory_order_relaxed)) ok = false;
+    });
+    return ok.load();
+}
+
 // Pack a set of sparse rows (one per owned element e; entries (absolute array column, value) in
 // ascending column order) as ELL(kEll) + SELL-32 overflow (internal.h Ell): the first kEll
 // entries of every row in its fixed slots (padding: value 0 at the row's own array index), the
 // rest of the slice's rows as SELL-32 (L = the slice's longest overflow; padding: value 0 at the
 // row's own index).  One pass over the rows, no intermediate full SELL.
-void pack_ell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& cols,
-              const std::vector<double>& vals, int64_t nel, int32_t pitch, int32_t ni, int32_t periodic, int32_t halo,
+void pack_ell(const std::vector<int64_t>& rowptr, const bigvec<int32_t>& cols,
+              const bigvec<double>& vals, int64_t nel, int32_t pitch, int32_t ni, int32_t periodic, int32_t halo,
               Ell& E, int T) {
     (void)ni; (void)periodic;
     const int64_t hoff = (int64_t)halo * pitch;        // array index of owned element 0
     E.n = nel;
-    E.val.assign((size_t)kEll * nel, 0.0);
+    E.val.resize((size_t)kEll * nel);           // every slot is written below (padding: 0)
     E.col.resize((size_t)kEll * nel);
     const int64_t nsl = nel / kSlice;
-    E.ovf.off.assign(nsl + 1, 0);
-    for (int64_t s = 0; s < nsl; ++s) {
+    pscan(T, nsl, E.ovf.off, [&](int64_t s) {
         int64_t L = 0;
         for (int l = 0; l < kSlice; ++l) {
             const int64_t e = s * kSlice + l;
             L = std::max(L, rowptr[e + 1] - rowptr[e] - kEll);
         }
-        E.ovf.off[s + 1] = E.ovf.off[s] + L * kSlice;
-    }
-    E.ovf.val.assign(E.ovf.off[nsl], 0.0);
+        return L * kSlice;
+    });
+    E.ovf.val.resize(E.ovf.off[nsl]);
     E.ovf.col.resize(E.ovf.off[nsl]);
     pfor(T, nsl, [&](int64_t s0, int64_t s1) {
     for (int64_t s = s0; s < s1; ++s) {
@@ -129,13 +216,13 @@ void pack_ell(const std::vector<int64_t>& rowptr, const std::vector<int32_t>& co
             const int32_t own = (int32_t)(e + hoff);
             for (int m = 0; m < kEll; ++m) {
                 E.col[(size_t)e * kEll + m] = m < len ? cols[r0 + m] : own;
-                if (m < len) E.val[(size_t)e * kEll + m] = vals[r0 + m];
+                E.val[(size_t)e * kEll + m] = m < len ? vals[r0 + m] : 0.0;
             }
             for (int64_t m = 0; m < L; ++m) {
                 const int64_t slot = E.ovf.off[s] + m * kSlice + l;
                 const bool real = kEll + m < len;
                 E.ovf.col[slot] = real ? cols[r0 + kEll + m] : own;
-                if (real) E.ovf.val[slot] = vals[r0 + kEll + m];
+                E.ovf.val[slot] = real ? vals[r0 + kEll + m] : 0.0;
             }
         }
     }
@@ -176,7 +263,16 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     const int32_t ni = g->ni, nj = g->nj;
     const int64_t ng = (int64_t)ni * nj;
     const int nthr = std::min(64, o->setup_threads > 0 ? o->setup_threads : (int)std::max(1u, std::thread::hardware_concurrency()));
-    for (int64_t k = 0; k < ng; ++k) {
+    std::atomic<bool> bad_input(false);
+    pfor(nthr, ng, [&](int64_t a, int64_t b) {
+        for (int64_t k = a; k < b; ++k)
+            if (!(c->cE[k] >= 0.0) || !std::isfinite(c->cE[k]) || !(c->cN[k] >= 0.0) || !std::isfinite(c->cN[k]) ||
+                (c->sigma && (!(c->sigma[k] >= 0.0) || !std::isfinite(c->sigma[k]))) || c->mask[k] > 1) {
+                bad_input = true;
+                return;
+            }
+    });
+    for (int64_t k = 0; k < (bad_input ? ng : 0); ++k) {     // the first offending point, in order
         if (!(c->cE[k] >= 0.0) || !std::isfinite(c->cE[k]) || !(c->cN[k] >= 0.0) || !std::isfinite(c->cN[k])) {
             char buf[160];
             snprintf(buf, sizeof buf, "pcg_setup: coefficient at (i=%d, j=%d) is negative or not finite",
@@ -213,7 +309,12 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         if (c->sigma) d = d + c->sigma[gi];
         return d;
     };
-    for (int64_t k = 0; k < ng; ++k)
+    std::atomic<bool> bad_diag(false);
+    pfor(nthr, ng, [&](int64_t a, int64_t b) {
+        for (int64_t k = a; k < b; ++k)
+            if (c->mask[k] && !(diag_of(k) > 0.0)) { bad_diag = true; return; }
+    });
+    for (int64_t k = 0; k < (bad_diag ? ng : 0); ++k)
         if (c->mask[k] && !(diag_of(k) > 0.0)) {
             char buf[160];
             snprintf(buf, sizeof buf, "pcg_setup: ocean point (i=%d, j=%d) has A_pp <= 0 (isolated, all faces 0)",
@@ -221,7 +322,9 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             return Status::err(PCG_ERR_NOT_SPD, buf, global_unknown(c->mask, ni, k));
         }
     stage("validation + diagonal");
-    if (Status s = anchor_check(ni, nj, P.periodic, c->cE, c->cN, c->sigma, c->mask); !s) return s;
+    // the parallel union-find decides; the sequential walk names the first unanchored basin
+    if (!anchors_ok_parallel(nthr, ni, nj, P.periodic, c->cE, c->cN, c->sigma, c->mask))
+        if (Status s = anchor_check(ni, nj, P.periodic, c->cE, c->cN, c->sigma, c->mask); !s) return s;
     stage("anchor check");
     if (ni > 65534) return Status::err(PCG_ERR_ARG, "pcg_setup: ni > 65534 not supported (int16 column offsets)");
 
@@ -229,11 +332,17 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     // sign bit of cN (cN >= 0 always, so -0.0 / -c mark a land cell).
     auto build_coeff_arrays = [&]() {
     const int64_t nel = P.elements();
-    P.cE.assign(nel, 0.0); P.cN.assign(nel, 0.0);
-    P.diag.assign(nel, 1.0); P.piv.assign(nel, 1.0);
-    if (P.has_sigma) P.sigma.assign(nel, 0.0);
+    P.cE.resize(nel); P.cN.resize(nel); P.diag.resize(nel); P.piv.resize(nel);
+    if (P.has_sigma) P.sigma.resize(nel);
+    pfor(nthr, nel, [&](int64_t a, int64_t b) {              // defaults, first touch in parallel
+        for (int64_t e = a; e < b; ++e) {
+            P.cE[e] = 0.0; P.cN[e] = 0.0; P.diag[e] = 1.0; P.piv[e] = 1.0;
+            if (P.has_sigma) P.sigma[e] = 0.0;
+        }
+    });
     const int32_t H = P.halo;
-    for (int32_t lr = 0; lr < nloc + 2 * H; ++lr) {
+    pfor(nthr, (int64_t)(nloc + 2 * H), [&](int64_t r0, int64_t r1) {
+    for (int32_t lr = (int32_t)r0; lr < (int32_t)r1; ++lr) {
         const int32_t j = P.jb + lr - H;
         if (j < 0 || j >= nj) continue;
         const int64_t row = (int64_t)j * ni;
@@ -253,13 +362,21 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             }
         }
     }
+    }, 64);
     };
 
     // owned ocean unknowns, first global index
-    P.first_global = 0;
-    for (int64_t k = 0; k < (int64_t)P.jb * ni; ++k) P.first_global += c->mask[k] ? 1 : 0;
-    P.n_owned = 0;
-    for (int64_t k = (int64_t)P.jb * ni; k < (int64_t)P.je * ni; ++k) P.n_owned += c->mask[k] ? 1 : 0;
+    {
+        std::atomic<int64_t> fg(0), no(0);
+        pfor(nthr, (int64_t)P.je * ni, [&](int64_t a, int64_t b) {
+            int64_t f = 0, o2 = 0;
+            for (int64_t k = a; k < b; ++k)
+                if (c->mask[k]) (k < (int64_t)P.jb * ni ? f : o2) += 1;
+            fg += f; no += o2;
+        });
+        P.first_global = fg.load();
+        P.n_owned = no.load();
+    }
 
     if (!P.factored()) {
         build_coeff_arrays();
@@ -392,40 +509,64 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     };
     P.zcolptr.assign(1, 0);
     std::vector<int64_t> colarr;                 // array index of each owned column
-    std::vector<int64_t> ent_row_arr;            // per entry: array index of its row
-    std::vector<double> ent_z;                   // per entry: z value
+    bigvec<int64_t> ent_row_arr;                 // per entry: array index of its row
+    bigvec<double> ent_z;                        // per entry: z value
     std::vector<int64_t> gunk_cache;
     // global unknown numbering of grid rows [min row_lo, je)
     int32_t rlo = P.je;
     for (auto& b : blocks) rlo = std::min(rlo, b.row_lo);
     std::vector<int64_t> unk((size_t)(P.je - rlo) * ni, -1);
     {
-        int64_t u = 0;
-        for (int64_t k = 0; k < (int64_t)rlo * ni; ++k) u += c->mask[k] ? 1 : 0;
-        for (int64_t k = (int64_t)rlo * ni; k < (int64_t)P.je * ni; ++k)
-            if (c->mask[k]) unk[k - (int64_t)rlo * ni] = u++;
+        std::atomic<int64_t> below(0);
+        pfor(nthr, (int64_t)rlo * ni, [&](int64_t a, int64_t b) {
+            int64_t u = 0;
+            for (int64_t k = a; k < b; ++k) u += c->mask[k] ? 1 : 0;
+            below += u;
+        });
+        std::vector<int64_t> rowstart;                   // ocean points before each row of [rlo, je)
+        pscan(nthr, (int64_t)(P.je - rlo), rowstart, [&](int64_t r) {
+            int64_t u = 0;
+            const uint8_t* m = c->mask + (int64_t)(rlo + r) * ni;
+            for (int32_t i = 0; i < ni; ++i) u += m[i] ? 1 : 0;
+            return u;
+        });
+        pfor(nthr, (int64_t)(P.je - rlo), [&](int64_t r0, int64_t r1) {
+            for (int64_t r = r0; r < r1; ++r) {
+                int64_t u = below.load() + rowstart[(size_t)r];
+                for (int32_t i = 0; i < ni; ++i)
+                    if (c->mask[(rlo + r) * ni + i]) unk[(size_t)(r * ni + i)] = u++;
+            }
+        }, 64);
     }
     // Jacobi scale s_g = 1/sqrt(A_gg) once per grid point of the rows the entries touch (the same
     // IEEE operations as per entry; FSAI: no scale)
     const int32_t rhi = std::min(nj, P.je + kNorthRows);
     std::vector<double> sgrid((size_t)(rhi - rlo) * ni, 1.0);
     if (P.precond != PCG_PRECOND_FSAI)
-        for (int64_t g2 = (int64_t)rlo * ni; g2 < (int64_t)rhi * ni; ++g2)
-            if (c->mask[g2]) sgrid[(size_t)(g2 - (int64_t)rlo * ni)] = 1.0 / std::sqrt(diag_of(g2));
+        pfor(nthr, (int64_t)(rhi - rlo) * ni, [&](int64_t a, int64_t b) {
+            for (int64_t g2 = (int64_t)rlo * ni + a; g2 < (int64_t)rlo * ni + b; ++g2)
+                if (c->mask[g2]) sgrid[(size_t)(g2 - (int64_t)rlo * ni)] = 1.0 / std::sqrt(diag_of(g2));
+        });
     auto scale_of = [&](int64_t gr) { return sgrid[(size_t)(gr - (int64_t)rlo * ni)]; };
     int64_t ntot = 0, ncols = 0;
     for (auto& b : blocks) { ntot += b.colptr.back(); ncols += (int64_t)b.col_g.size(); }
     // flat column index over the blocks, entry offsets by prefix sum, then a parallel fill
-    std::vector<std::pair<int32_t, int32_t>> colsrc;      // (block, column in block)
-    colsrc.reserve((size_t)ncols);
-    for (size_t bi = 0; bi < blocks.size(); ++bi)
-        for (size_t q = 0; q < blocks[bi].col_g.size(); ++q) colsrc.push_back({(int32_t)bi, (int32_t)q});
-    P.zcolptr.assign((size_t)ncols + 1, 0);
-    for (int64_t k = 0; k < ncols; ++k) {
+    bigvec<std::pair<int32_t, int32_t>> colsrc((size_t)ncols);      // (block, column in block)
+    {
+        int64_t k0 = 0;
+        for (size_t bi = 0; bi < blocks.size(); ++bi) {
+            const int64_t nb = (int64_t)blocks[bi].col_g.size();
+            pfor(nthr, nb, [&](int64_t a, int64_t b) {
+                for (int64_t q = a; q < b; ++q) colsrc[(size_t)(k0 + q)] = {(int32_t)bi, (int32_t)q};
+            });
+            k0 += nb;
+        }
+    }
+    pscan(nthr, ncols, P.zcolptr, [&](int64_t k) {
         const AinvBlock& b = blocks[(size_t)colsrc[(size_t)k].first];
         const int32_t q = colsrc[(size_t)k].second;
-        P.zcolptr[(size_t)k + 1] = P.zcolptr[(size_t)k] + (b.colptr[q + 1] - b.colptr[q]);
-    }
+        return b.colptr[q + 1] - b.colptr[q];
+    });
     P.zrow.resize((size_t)ntot); P.zhat.resize((size_t)ntot);
     ent_z.resize((size_t)ntot); ent_row_arr.resize((size_t)ntot);
     P.pivots.resize((size_t)ncols); P.scale.resize((size_t)ncols); colarr.resize((size_t)ncols);
@@ -450,18 +591,26 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     P.nnz_off = ntot - ncols;
     if ((int64_t)colarr.size() != P.n_owned) return Status::err(PCG_ERR_ARG, "internal: owned column count mismatch");
     const int64_t hoff = (int64_t)P.halo * pitch;        // array index of owned element 0
-    for (int64_t r : ent_row_arr)        // entries in the southern halo rows only with halo-AINV across ranks
-        if (r < hoff - (int64_t)P.halo_w * pitch) return Status::err(PCG_ERR_ARG, "internal: Z entry outside the owned rows");
+    {
+        std::atomic<bool> outside(false);        // entries in the southern halo rows only with halo-AINV across ranks
+        pfor(nthr, (int64_t)ent_row_arr.size(), [&](int64_t a, int64_t b) {
+            for (int64_t e = a; e < b; ++e)
+                if (ent_row_arr[(size_t)e] < hoff - (int64_t)P.halo_w * pitch) outside = true;
+        });
+        if (outside) return Status::err(PCG_ERR_ARG, "internal: Z entry outside the owned rows");
+    }
 
     stage("export + Z values");
     // ---- SELL of Z^T rows: row (column j of Z) = entries k ascending
     const int64_t nown = P.owned_elements();
     {
-        std::vector<int64_t> rp(nown + 1, 0);
-        for (size_t q = 0; q < colarr.size(); ++q) rp[colarr[q] - hoff + 1] = P.zcolptr[q + 1] - P.zcolptr[q];
-        for (int64_t e = 0; e < nown; ++e) rp[e + 1] += rp[e];
-        std::vector<int32_t> cols(rp[nown]);
-        std::vector<double> vals(rp[nown]);
+        std::vector<int64_t> len((size_t)nown, 0), rp;
+        pfor(nthr, (int64_t)colarr.size(), [&](int64_t a, int64_t b) {
+            for (int64_t q = a; q < b; ++q) len[(size_t)(colarr[(size_t)q] - hoff)] = P.zcolptr[(size_t)q + 1] - P.zcolptr[(size_t)q];
+        });
+        pscan(nthr, nown, rp, [&](int64_t e) { return len[(size_t)e]; });
+        bigvec<int32_t> cols(rp[nown]);
+        bigvec<double> vals(rp[nown]);
         pfor(nthr, (int64_t)colarr.size(), [&](int64_t q0, int64_t q1) {
             for (int64_t q = q0; q < q1; ++q) {
                 int64_t dst = rp[colarr[q] - hoff];
@@ -489,21 +638,33 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
                 }
         for (int64_t r : nrow_arr)
             if (r < hoff) return Status::err(PCG_ERR_ARG, "internal: northern Z entry below the owned rows");
-        std::vector<int64_t> rp(nown + 1, 0);
-        for (int64_t r : ent_row_arr) if (r >= hoff) rp[r - hoff + 1]++;
-        for (int64_t r : nrow_arr) rp[r - hoff + 1]++;
-        for (int64_t e = 0; e < nown; ++e) rp[e + 1] += rp[e];
+        std::vector<int64_t> cnt((size_t)nown, 0), rp;
+        pfor(nthr, (int64_t)ent_row_arr.size(), [&](int64_t a, int64_t b) {
+            for (int64_t e = a; e < b; ++e) {
+                const int64_t r = ent_row_arr[(size_t)e];
+                if (r >= hoff) __atomic_fetch_add(&cnt[(size_t)(r - hoff)], (int64_t)1, __ATOMIC_RELAXED);
+            }
+        });
+        for (int64_t r : nrow_arr) cnt[(size_t)(r - hoff)]++;
+        pscan(nthr, nown, rp, [&](int64_t e) { return cnt[(size_t)e]; });
         std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
-        std::vector<int32_t> cols(rp[nown]);
-        std::vector<double> vals(rp[nown]);
+        bigvec<int32_t> cols(rp[nown]);
+        bigvec<double> vals(rp[nown]);
         // transpose with the ascending column order per row kept: thread t owns the rows
         // [R_t, R_t+1) and visits, in ascending order, the columns that can hold entries of them
         // (a column's entries are at rows <= the column, so columns from the first row >= R_t on)
         {
             const int64_t nc = (int64_t)colarr.size();
-            int64_t reach = 0;                             // largest column - row distance of an entry
-            for (int64_t q = 0; q < nc; ++q)
-                for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e) reach = std::max(reach, colarr[q] - ent_row_arr[e]);
+            std::atomic<int64_t> reach_a(0);               // largest column - row distance of an entry
+            pfor(nthr, nc, [&](int64_t a, int64_t b) {
+                int64_t r = 0;
+                for (int64_t q = a; q < b; ++q)
+                    for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e) r = std::max(r, colarr[q] - ent_row_arr[e]);
+                int64_t cur = reach_a.load();
+                while (r > cur && !reach_a.compare_exchange_weak(cur, r)) {
+                }
+            });
+            const int64_t reach = reach_a.load();
             int T = (nc < 100000) ? 1 : nthr;
             std::vector<std::thread> pool;
             auto part = [&](int t) {

@@ -106,11 +106,19 @@ Status dalloc(pcg_ctx* c, T*& p, int64_t n) {
 }
 
 template <class T>
-Status upload(pcg_ctx* c, T*& p, const std::vector<T>& h) {
-    if (Status s = dalloc(c, p, (int64_t)h.size()); !s) return s;
-    if (!h.empty()) CU(cudaMemcpyAsync(p, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice, c->st));
+Status upload_n(pcg_ctx* c, T*& p, const T* data, int64_t n) {
+    if (Status s = dalloc(c, p, n); !s) return s;
+    if (n > 0) CU(cudaMemcpyAsync(p, data, (size_t)n * sizeof(T), cudaMemcpyHostToDevice, c->st));
     CU(cudaStreamSynchronize(c->st));   // host vectors may be released afterwards
     return Status::ok();
+}
+template <class T>
+Status upload(pcg_ctx* c, T*& p, const std::vector<T>& h) {
+    return upload_n(c, p, h.data(), (int64_t)h.size());
+}
+template <class T>
+Status upload(pcg_ctx* c, T*& p, const bigvec<T>& h) {
+    return upload_n(c, p, h.data(), (int64_t)h.size());
 }
 
 // One rank: the PCG loop is one cooperative kernel (default) or a WHILE-node graph
