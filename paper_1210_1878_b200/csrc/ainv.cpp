@@ -17,7 +17,9 @@
 #include <memory>
 #include <mutex>
 #include <thread>
+#include <cstdlib>
 #include <cstring>
+#include <new>
 #include <algorithm>
 #include <functional>
 #include <queue>
@@ -31,10 +33,24 @@ namespace {
 
 struct BlockMatrix {
     int32_t n = 0;
-    std::vector<int32_t> rp, ci;      // CSR of the scaled matrix A^, columns ascending
-    std::vector<double> a;
-    std::vector<int64_t> grid;        // local unknown -> grid index
-    std::vector<double> diag;         // A_pp
+    bigvec<int32_t> rp, ci;           // CSR of the scaled matrix A^, columns ascending
+    bigvec<double> a;
+    bigvec<int64_t> grid;             // local unknown -> grid index
+    bigvec<double> diag;              // A_pp
+};
+
+// zero-initialised array from calloc: the pages a thread never touches are never written (the
+// per-thread n-sized work arrays of the column workers touch only their columns' neighbourhood)
+template <class T>
+struct CallocArr {
+    T* p = nullptr;
+    explicit CallocArr(size_t n) : p(static_cast<T*>(std::calloc(std::max<size_t>(n, 1), sizeof(T)))) {
+        if (!p) throw std::bad_alloc();
+    }
+    ~CallocArr() { std::free(p); }
+    CallocArr(const CallocArr&) = delete;
+    CallocArr& operator=(const CallocArr&) = delete;
+    T& operator[](size_t i) { return p[i]; }
 };
 
 // Faces of (i,j): E, W, N, S with existence and coupling.
@@ -63,17 +79,38 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
         for (auto& th : pool) th.join();
     };
     BlockMatrix M;
-    // local numbering of the ocean points of rows [r0, r1), natural order
-    std::vector<int32_t> loc((size_t)(r1 - r0) * ni, -1);
-    for (int32_t j = r0; j < r1; ++j)
-        for (int32_t i = 0; i < ni; ++i) {
-            int64_t g = (int64_t)j * ni + i;
-            if (mask[g]) { loc[(size_t)(j - r0) * ni + i] = M.n++; M.grid.push_back(g); }
-        }
+    // local numbering of the ocean points of rows [r0, r1), natural order: ocean points per row,
+    // prefix over the rows, then every row numbered in parallel
+    const int32_t nr = r1 - r0;
+    std::vector<int32_t> rowstart((size_t)nr + 1, 0);
+    {
+        std::vector<int32_t> cnt((size_t)nr, 0);
+        pfor((int64_t)nr * 256, [&](int64_t a0, int64_t a1) {      // (x256: rows are few, each ni wide)
+            for (int64_t r = (a0 + 255) / 256; r < (a1 + 255) / 256; ++r) {
+                int32_t u = 0;
+                for (int32_t i = 0; i < ni; ++i) u += mask[(int64_t)(r0 + r) * ni + i] ? 1 : 0;
+                cnt[(size_t)r] = u;
+            }
+        });
+        for (int32_t r = 0; r < nr; ++r) rowstart[(size_t)r + 1] = rowstart[(size_t)r] + cnt[(size_t)r];
+    }
+    M.n = rowstart[(size_t)nr];
     const int32_t n = M.n;
+    bigvec<int32_t> loc((size_t)nr * ni);
+    M.grid.resize((size_t)n);
+    pfor((int64_t)nr * 256, [&](int64_t a0, int64_t a1) {
+        for (int64_t r = (a0 + 255) / 256; r < (a1 + 255) / 256; ++r) {
+            int32_t u = rowstart[(size_t)r];
+            for (int32_t i = 0; i < ni; ++i) {
+                const int64_t g = (int64_t)(r0 + r) * ni + i;
+                if (mask[g]) { loc[(size_t)r * ni + i] = u; M.grid[(size_t)u] = g; ++u; }
+                else loc[(size_t)r * ni + i] = -1;
+            }
+        }
+    });
     M.rp.assign(n + 1, 0);
     M.diag.resize(n);
-    std::vector<double> sc(n);
+    bigvec<double> sc(n);
     // diagonal A_pp = ((c_E + c_W) + c_N) + c_S (+ sigma) over all faces, then s = 1/sqrt(A_pp)
     pfor(n, [&](int64_t lo, int64_t hi) {
         for (int64_t p = lo; p < hi; ++p) {
@@ -89,9 +126,9 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
     });
     // CSR of A^ restricted to the block: a^_pq = A_pq * (s_p * s_q); rows built in parallel into
     // 5 fixed slots per row, then compacted
-    std::vector<int32_t> c5((size_t)5 * n);
-    std::vector<double> a5((size_t)5 * n);
-    std::vector<uint8_t> m5(n);
+    bigvec<int32_t> c5((size_t)5 * n);
+    bigvec<double> a5((size_t)5 * n);
+    bigvec<uint8_t> m5(n);
     pfor(n, [&](int64_t lo, int64_t hi) {
         for (int64_t p = lo; p < hi; ++p) {
             int64_t g = M.grid[p];
@@ -154,10 +191,10 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
     std::vector<std::vector<std::unique_ptr<int32_t[]>>> seg_r((size_t)T);
     std::vector<std::vector<std::unique_ptr<double[]>>> seg_v((size_t)T);
     auto worker = [&](int t) {
-        std::vector<double> w(n, 0.0);
-        std::vector<uint8_t> live(n, 0);        // entry present in the current column
-        std::vector<int32_t> listed(n, -1);     // stamp: k recorded in `members` for column j
-        std::vector<int32_t> queued(n, -1);     // stamp: k queued as a candidate for column j
+        CallocArr<double> w((size_t)n);
+        CallocArr<uint8_t> live((size_t)n);     // entry present in the current column
+        CallocArr<int32_t> listed((size_t)n);   // stamp j + 1: k recorded in `members` for column j
+        CallocArr<int32_t> queued((size_t)n);   // stamp j + 1: k queued as a candidate for column j
         std::vector<int32_t> members, touched;
         std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> cand;
         // column storage in fixed segments (a column's entries never move once published; the
@@ -175,10 +212,11 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
         for (int32_t j : mine[(size_t)t]) {
             if (j >= limit.load(std::memory_order_relaxed)) return;
             members.clear();
-            members.push_back(j); listed[j] = j; live[j] = 1; w[j] = 1.0;
+            const int32_t stamp = j + 1;
+            members.push_back(j); listed[j] = stamp; live[j] = 1; w[j] = 1.0;
             for (int32_t e = M.rp[j]; e < M.rp[j + 1]; ++e) {
                 int32_t i = M.ci[e];
-                if (i < j && queued[i] != j) { queued[i] = j; cand.push(i); }
+                if (i < j && queued[i] != stamp) { queued[i] = stamp; cand.push(i); }
             }
             bool ok = true;
             while (!cand.empty()) {
@@ -198,10 +236,10 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
                     const int32_t k = zi.r[q];
                     if (!live[k]) {
                         live[k] = 1; w[k] = 0.0;
-                        if (listed[k] != j) { listed[k] = j; members.push_back(k); }
+                        if (listed[k] != stamp) { listed[k] = stamp; members.push_back(k); }
                         for (int32_t e2 = M.rp[k]; e2 < M.rp[k + 1]; ++e2) {
                             int32_t i2 = M.ci[e2];
-                            if (i2 > i && i2 < j && queued[i2] != j) { queued[i2] = j; cand.push(i2); }
+                            if (i2 > i && i2 < j && queued[i2] != stamp) { queued[i2] = stamp; cand.push(i2); }
                         }
                     }
                     w[k] = w[k] - coef * zi.v[q];
@@ -279,7 +317,8 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
     for (int32_t p = 0; p < n; ++p)
         if (M.grid[p] / ni >= blk.row_own) { first_owned = p; break; }
     const int32_t nown = n - first_owned;
-    blk.colptr.assign((size_t)nown + 1, 0);
+    blk.colptr.resize((size_t)nown + 1);
+    blk.colptr[0] = 0;
     for (int32_t q = 0; q < nown; ++q) blk.colptr[q + 1] = blk.colptr[q] + cref[first_owned + q].len;
     blk.row_g.resize((size_t)blk.colptr[nown]);
     blk.zhat.resize((size_t)blk.colptr[nown]);

@@ -117,11 +117,11 @@ struct AinvBlock {
     int32_t row_lo = 0, row_own = 0, row_hi = 0;
     // output: owned columns, local unknown numbering of the block converted to GLOBAL grid
     // indices (j*ni + i) for rows, values zhat, pivots; failure column (global grid index)
-    std::vector<int64_t> colptr;   // owned columns + 1
-    std::vector<int64_t> row_g;    // grid index of each entry's row
-    std::vector<double> zhat;
-    std::vector<double> piv;       // per owned column
-    std::vector<int64_t> col_g;    // grid index of each owned column
+    bigvec<int64_t> colptr;        // owned columns + 1
+    bigvec<int64_t> row_g;         // grid index of each entry's row
+    bigvec<double> zhat;
+    bigvec<double> piv;            // per owned column
+    bigvec<int64_t> col_g;         // grid index of each owned column
     int64_t fail_grid = -1;
 };
 void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, const double* cN,
