@@ -156,6 +156,42 @@ def random_grid(ni: int, nj: int, seed: int, land_frac: float = 0.2,
     return Problem(f"rand{ni}x{nj}s{seed}", ni, nj, cE, cN, ocean.astype(np.uint8), periodic, sg)
 
 
+def nos6_like(n: int = 30) -> Problem:
+    """A synthetic stand-in for the paper's NOS6 test ("Finite difference
+    approximation to Poisson's equation in an L-shaped region, mixed boundary conditions", 675
+    unknowns, Matrix Market) -- the file itself needs network access, so this builds the
+    problem the description names on this library's operator: the 5-point Poisson stencil
+    (unit face couplings) on an L-shaped region of n x n cells minus its (n/2 x n/2) upper-right
+    quadrant (n = 30: 900 - 225 = 675 unknowns, NOS6's order), inside a one-cell land border;
+    Dirichlet faces (coupling 1 to the land border) on the west and south edges, Neumann faces
+    (coupling 0) everywhere else.  Not periodic.  Not NOS6's values -- its size, shape and
+    boundary mix."""
+    h = n // 2
+    ni = nj = n + 2
+    mask = np.zeros((nj, ni), dtype=np.uint8)
+    for j in range(1, n + 1):
+        for i in range(1, n + 1):
+            if not (i > h and j > h):
+                mask[j, i] = 1
+    cE = np.zeros((nj, ni))
+    cN = np.zeros((nj, ni))
+    for j in range(nj):
+        for i in range(ni - 1):
+            if mask[j, i] and mask[j, i + 1]:
+                cE[j, i] = 1.0
+    for j in range(nj - 1):
+        for i in range(ni):
+            if mask[j, i] and mask[j + 1, i]:
+                cN[j, i] = 1.0
+    for j in range(1, n + 1):                     # west edge: Dirichlet
+        if mask[j, 1]:
+            cE[j, 0] = 1.0
+    for i in range(1, n + 1):                     # south edge: Dirichlet
+        if mask[1, i]:
+            cN[0, i] = 1.0
+    return Problem(f"nos6like{n}", ni, nj, cE, cN, mask, False, None)
+
+
 def singular_channel(ni: int, nj: int, seed: int) -> Problem:
     """Unanchored basin: periodic channel bounded by land rows whose land
     faces carry c = 0, random interior couplings in [0.5, 2].  A is singular."""

@@ -993,3 +993,33 @@ def test_device_comm_argument_errors():
         pcg.Solver(p.cE, p.cN, p.mask, tau=TAU, flags=pcg.FLAG_DEVICE_COMM)
     with pytest.raises(pcg.PcgError):
         pcg.LocalRanks(p.cE, p.cN, p.mask, 2, tau=TAU, flags=pcg.FLAG_DEVICE_COMM)
+
+
+# ------------------------------------------------ NOS6-like L-shaped Poisson problem (NEXT-4)
+@pytest.mark.parametrize("precond", ["fsai", "jacobi", "ainv", "pb2"])
+def test_nos6_like_bitwise_canonical(precond):
+    """The paper's NOS6 experiment (P, P^-1, P_B1, P_B2 at eps = 1e-6, q = 4) on
+    its stand-in (synth.nos6_like: 5-point Poisson, L-shaped region, mixed Dirichlet / Neumann,
+    675 unknowns, non-periodic): every preconditioner's solve is bitwise the oracle's canonical PCG."""
+    p = synth.nos6_like()
+    A = oracle.assemble(p)
+    b = rhs(A, p)
+    if precond == "fsai":
+        M = oracle.fsai(A, 4)
+        S = pcg.Solver(p.cE, p.cN, p.mask, periodic=False, precond="fsai", fsai_q=4)
+    elif precond == "pb2":
+        M = oracle.ainv(A, 0.0, fill=4)
+        S = pcg.Solver(p.cE, p.cN, p.mask, periodic=False, tau=0.0, ainv_fill=4)
+    elif precond == "ainv":
+        M = oracle.ainv(A, TAU)
+        S = pcg.Solver(p.cE, p.cN, p.mask, periodic=False, tau=TAU)
+    else:
+        M = None
+        S = pcg.Solver(p.cE, p.cN, p.mask, periodic=False, precond="jacobi")
+    pc = "jacobi" if precond == "jacobi" else "ainv"
+    ref = oracle.pcg(A, b, pc, M, 1e-6, maxit=A.n, mode="canonical", pitch=S.pitch, block=S.block)
+    xg, k, hist, rep = S.solve(dev(A.to_grid(b)), tol=1e-6, maxit=A.n)
+    assert k == ref.iterations and np.array_equal(hist, ref.hist)
+    assert np.array_equal(host(xg), A.to_grid(ref.x))
+    assert rep["converged"] == 1
+    S.close()

@@ -620,3 +620,21 @@ def test_chunked_mode_thread_invariant_and_within_plain_band():
     assert abs(ch.iterations - pl.iterations) <= max(2, 0.01 * pl.iterations)
     assert np.linalg.norm(ch.x - pl.x) / np.linalg.norm(pl.x) <= 1e-9
     assert ch.true_rel_residual <= 1e-12
+
+
+# ------------------------------------------------ NOS6-like L-shaped Poisson problem (NEXT-4)
+def test_nos6_like_structure():
+    """The stand-in for the paper's NOS6 (5-point Poisson on an L-shaped region, mixed
+    boundary conditions, 675 unknowns): 675 unknowns; every interior and Neumann-edge row sums to
+    zero, the 59 rows of the Dirichlet west / south edges to 1 (the corner cell to 2); SPD; the
+    Dirichlet rows are exactly the cells with i = 1 or j = 1 of the region."""
+    p = synth.nos6_like()
+    A = oracle.assemble(p)
+    assert A.n == 675
+    D = A.dense()
+    assert np.array_equal(D, D.T) and np.linalg.eigvalsh(D).min() > 0
+    rs = D.sum(axis=1)
+    cells = np.argwhere(p.mask == 1)                   # (j, i) in the unknown (natural) order
+    dirichlet = (cells[:, 1] == 1).astype(int) + (cells[:, 0] == 1).astype(int)
+    assert np.array_equal(rs, dirichlet.astype(float))
+    assert int((dirichlet > 0).sum()) == 59 and int((dirichlet == 2).sum()) == 1
