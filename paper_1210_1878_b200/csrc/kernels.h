@@ -37,20 +37,18 @@ struct EllDev {
 };
 
 
-// Resident-strip driver (rs.cu): one persistent cooperative block of kRsThreads
+// Resident-strip driver (rs.cu): one persistent cooperative block of 512 or 768 threads
 // per SM runs the whole PCG loop.  Block b owns a contiguous range of units (row segments, in
 // row-major order) per phase -- ub1 for the K1 phase (stencil), ub2 for the K2/K3 phase
 // (preconditioner) -- and keeps the vector that phase gathers from (d, r_new, t) for its range
 // plus the halo its stencil / Z rows reach in shared memory, so every gather is a shared-memory
 // load.  Two grid barriers per iteration (the two dot products of Alg. 1) and one neighbour flag
 // (t rows of the blocks to the north).
-#ifndef RS_THREADS
-#define RS_THREADS 512
-#endif
-constexpr int kRsThreads = RS_THREADS;
+constexpr int kRsThreadsSmall = 512, kRsThreadsLarge = 768;   // the two rs_loop_kernel block sizes
 struct RsDev {
     int32_t on;                   // eligible and enabled
     int32_t nblk;                 // blocks (= SMs, one resident block each)
+    int32_t nt;                   // threads per block (kRsThreadsSmall or kRsThreadsLarge)
     int32_t cap;                  // shared-memory buffer (doubles)
     int32_t maxu1, maxu2;         // most units of one block per phase
     int32_t maxnx;                // most 32-element chunks any pass of one block touches

@@ -44,35 +44,22 @@
 namespace pcg {
 namespace {
 
-constexpr int kRsWarps = kRsThreads / 32;
-#if RS_THREADS >= 1024
-#define RS_DEF_VU 4
-#define RS_DEF_K1C 2
-#define RS_DEF_ZC 1
-#define RS_DEF_NB 8
-#define RS_DEF_NB2 4
-#else
-#define RS_DEF_VU 8
-#define RS_DEF_K1C 4
-#define RS_DEF_ZC 2
-#define RS_DEF_NB 24
-#define RS_DEF_NB2 12
-#endif
-#ifndef RS_VU
-#define RS_VU RS_DEF_VU              // chunks per warp in flight in the vector passes (1a, 2A, 2C, Jacobi)
-#endif
-#ifndef RS_K1C
-#define RS_K1C RS_DEF_K1C            // chunks per warp in flight in the stencil pass (1b)
-#endif
-#ifndef RS_ZC
-#define RS_ZC RS_DEF_ZC              // chunks per warp in flight in the Z / Z^T passes (2B, 2D)
-#endif
-#ifndef RS_FINAL_NB
-#define RS_FINAL_NB RS_DEF_NB        // partial loads in flight per thread in the final sum of (d, q)
-#endif
-#ifndef RS_FINAL_NB2
-#define RS_FINAL_NB2 RS_DEF_NB2      // ... per partial array in the final sums of (r, r) and (s, r)
-#endif
+// Per block size: chunks per warp in flight in the vector passes (1a, 2A, 2C, Jacobi: VU), the
+// stencil pass (1b: K1C) and the Z / Z^T passes (2B, 2D: ZC), overflow entries per round (OVF,
+// two rounds in flight), partial loads in flight per thread in the final sums (NB: (d, q); NB2:
+// per array for (r, r), (s, r)).  512 threads get 128 registers, 768 threads 80 (measured at
+// cfg4: 768 threads 75.7 vs 76.6 us per iteration for AINV(0.1), 34.2 vs 36.7 for Jacobi; at
+// cfg2 / cfg3 AINV 16.0 / 19.8 vs 14.9 / 17.9 -- setup_rs picks per problem).
+template <int NT>
+struct RsCfg;
+template <>
+struct RsCfg<512> {
+    static constexpr int VU = 8, K1C = 4, ZC = 2, OVF = 8, NB = 24, NB2 = 12;
+};
+template <>
+struct RsCfg<768> {
+    static constexpr int VU = 4, K1C = 2, ZC = 2, OVF = 4, NB = 12, NB2 = 6;
+};
 
 // Diagnostic build only (-DRS_TIMELINE): per-block globaltimer durations of each pass, summed over
 // the iterations (read back with pcg_rs_timeline).
@@ -196,9 +183,10 @@ __device__ __forceinline__ void rs_final2(const double* p1, const double* p2, in
 
 // unit partials of units [ua, ua + nu) from their chunk warp sums (second level of the block
 // tree); uc[u] = first chunk of unit ua + u relative to unit ua (uc[nu] = end)
+template <int NW>
 __device__ __forceinline__ void rs_partials(int32_t ua, int32_t nu, const int32_t* uc, const double* ws, double* partial) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int32_t u = warp; u < nu; u += kRsWarps) {
+    for (int32_t u = warp; u < nu; u += NW) {
         const int32_t c0 = uc[u], nc = uc[u + 1] - c0;
         double v = lane < nc ? ws[c0 + lane] : 0.0;
         v = warp_tree(v);
@@ -206,15 +194,13 @@ __device__ __forceinline__ void rs_partials(int32_t ua, int32_t nu, const int32_
     }
 }
 
-#ifndef RS_OVF
-#define RS_OVF 8                     // overflow entries per round (two rounds in flight)
-#endif
 // One Z / Z^T row: the 4 preloaded ELL slots (z, cw: int16 offsets from the element's own array
 // index a; zero / own index on land lanes), then the row's entries in the SELL-32 overflow of its
 // slice (o0 = first entry, L per lane; entry m of lane l at o0 + 32 m + l, coalesced per warp).
 // Gathers from shared memory: xb[c] is the gathered vector at array index c.  acc = 0, fma over
 // the entries in ascending column order, padding included (as kernels.cu's
 // overflow_sum).
+template <int RS_OVF>
 __device__ __forceinline__ double rs_row(const double (&z)[kEll], uint2 cw, int64_t o0, int L, int32_t a,
                                          const double* xb, const double* __restrict__ ov, const int32_t* __restrict__ oc) {
     const int32_t c0 = a + (int32_t)(int16_t)(cw.x & 0xffffu), c1 = a + (int32_t)(int16_t)(cw.x >> 16);
@@ -266,19 +252,18 @@ __device__ __forceinline__ double rs_row(const double (&z)[kEll], uint2 cw, int6
     return acc;
 }
 
-// Chunks of a pass handled by one warp: c = warp + NW q, q = 0 .. n-1.
-__device__ __forceinline__ int warp_chunks(int nch, int warp) { return nch > warp ? (nch - warp + kRsWarps - 1) / kRsWarps : 0; }
 
 // Every pass below walks the warp's chunks (c = warp + NW q) in batches of D: the loads of D
 // chunks are issued into register slots before any of them is consumed.  Every slot is assigned
 // on every batch (zeros for masked chunks), so no value is carried across batches.
 
 // PC: 0 = factored Z Dhat^-1 Z^T (AINV, P_B2, FSAI through the ELL form), 1 = Jacobi, 2 = none
-template <bool SIGMA, int PC>
-__global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
+template <bool SIGMA, int PC, int NT>
+__global__ void __launch_bounds__(NT, 1) rs_loop_kernel(const KArgs A) {
+    using C = RsCfg<NT>;
     extern __shared__ __align__(16) double sm[];
     __shared__ double bc[2];
-    constexpr int NW = kRsWarps;
+    constexpr int NW = NT / 32;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int b = blockIdx.x;
     const unsigned nblk = gridDim.x;
@@ -307,7 +292,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
     // first element (cc), so the passes need no integer division
     const int32_t nx1 = e1 > e0 ? (e1 - e0 + 2 * P) >> 5 : 0;
     const int32_t nx2 = f1 > f0 ? (hi2 - lo2) >> 5 : 0;
-    for (int q = tid; q < nx1 + nx2; q += kRsThreads) {
+    for (int q = tid; q < nx1 + nx2; q += NT) {
         const int32_t e = (q < nx1 ? e0 - P + 32 * q : lo2 + 32 * (q - nx1)) - (int32_t)A.hoff;
         uint32_t m = 0u;
         int32_t i = 0;
@@ -319,8 +304,8 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
         cm[q] = m;
         cc[q] = (uint16_t)i;
     }
-    for (int u = tid; u <= nu1; u += kRsThreads) uc1[u] = (unit_a0(A, ua1 + u) - e0) >> 5;
-    for (int u = tid; u <= nu2; u += kRsThreads) uc2[u] = (unit_a0(A, ua2 + u) - f0) >> 5;
+    for (int u = tid; u <= nu1; u += NT) uc1[u] = (unit_a0(A, ua1 + u) - e0) >> 5;
+    for (int u = tid; u <= nu2; u += NT) uc2[u] = (unit_a0(A, ua2 + u) - f0) >> 5;
     double rho = sc->rho, beta = sc->beta, alpha = sc->alpha;
     const double nb = sc->nb, tol = sc->tol;
     int k = sc->k, status = sc->status, xpend = 0;
@@ -344,11 +329,11 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
             const int cmD = 0;
             // 1a: d over [D0, D0 + 32 nD) -> buf (land chunks: 0, no loads); own chunks: d -> global,
             // x += alpha_prev d_old
-            for (int c0 = warp; c0 < nD; c0 += RS_VU * NW) {
-                double sv[RS_VU], dv[RS_VU], xv[RS_VU];
-                uint32_t m[RS_VU];
+            for (int c0 = warp; c0 < nD; c0 += C::VU * NW) {
+                double sv[C::VU], dv[C::VU], xv[C::VU];
+                uint32_t m[C::VU];
 #pragma unroll
-                for (int u = 0; u < RS_VU; ++u) {
+                for (int u = 0; u < C::VU; ++u) {
                     const int c = c0 + u * NW;
                     const int32_t a = D0 + 32 * c + lane;
                     m[u] = c < nD ? cm[cmD + c] : 0u;
@@ -357,7 +342,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                     xv[u] = (m[u] && c >= own0 && c < own1) ? __ldcg(A.x + a) : 0.0;
                 }
 #pragma unroll
-                for (int u = 0; u < RS_VU; ++u) {
+                for (int u = 0; u < C::VU; ++u) {
                     const int c = c0 + u * NW;
                     if (c >= nD) break;
                     const int32_t a = D0 + 32 * c + lane;
@@ -370,16 +355,16 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                 }
             }
             RS_TS(1);
-            // 1b: q = A d on own ocean points, (d, q) warp sums; RS_K1C chunks per
+            // 1b: q = A d on own ocean points, (d, q) warp sums; C::K1C chunks per
             // warp with all their loads issued before any computes
             const double* bd = buf - D0;
             const int nch = (e1 - e0) >> 5, cm1 = P >> 5;
-            for (int c0 = warp; c0 < nch; c0 += RS_K1C * NW) {
-                double cEp[RS_K1C], cNr[RS_K1C], cNs[RS_K1C], cEw[RS_K1C], sg[RS_K1C];
-                uint32_t m[RS_K1C];
-                int32_t ic[RS_K1C];
+            for (int c0 = warp; c0 < nch; c0 += C::K1C * NW) {
+                double cEp[C::K1C], cNr[C::K1C], cNs[C::K1C], cEw[C::K1C], sg[C::K1C];
+                uint32_t m[C::K1C];
+                int32_t ic[C::K1C];
 #pragma unroll
-                for (int u = 0; u < RS_K1C; ++u) {
+                for (int u = 0; u < C::K1C; ++u) {
                     const int c = c0 + u * NW;
                     const int32_t a = e0 + 32 * c + lane;
                     m[u] = c < nch ? cm[cm1 + c] : 0u;
@@ -392,7 +377,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                     sg[u] = (SIGMA && ld) ? __ldg(A.sigma + a) : 0.0;
                 }
 #pragma unroll
-                for (int u = 0; u < RS_K1C; ++u) {
+                for (int u = 0; u < C::K1C; ++u) {
                     const int c = c0 + u * NW;
                     if (c >= nch) break;
                     const int32_t a = e0 + 32 * c + lane, i = ic[u];
@@ -421,14 +406,14 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                 }
             }
             __syncthreads();
-            rs_partials(ua1, nu1, uc1, ws1, A.partial[0]);
+            rs_partials<NW>(ua1, nu1, uc1, ws1, A.partial[0]);
         }
         RS_T(2);
         xpend = 0;                                           // x += alpha_prev d_old done
         bar += nblk;
         rs_grid_sync(rs_sync, bar);
         RS_T(3);
-        const double gamma = rs_final<RS_FINAL_NB>(A.partial[0], U, bc);
+        const double gamma = rs_final<C::NB>(A.partial[0], U, bc);
         RS_T(4);
         if (!(gamma > 0.0) || !isfinite(gamma)) { status = kStBreakdown; break; }
         alpha = __ddiv_rn(rho, gamma);
@@ -454,11 +439,11 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                 }
                 // 2A: r_new over [lo2, f1) -> buf; own chunks: r_new -> global, (r, r) warp sums
                 const int nR = (f1 - lo2) >> 5, own0 = (f0 - lo2) >> 5, cmR = nx1;
-                for (int c0 = warp; c0 < nR; c0 += RS_VU * NW) {
-                    double qv[RS_VU], rv[RS_VU];
-                    uint32_t m[RS_VU];
+                for (int c0 = warp; c0 < nR; c0 += C::VU * NW) {
+                    double qv[C::VU], rv[C::VU];
+                    uint32_t m[C::VU];
 #pragma unroll
-                    for (int u = 0; u < RS_VU; ++u) {
+                    for (int u = 0; u < C::VU; ++u) {
                         const int c = c0 + u * NW;
                         const int32_t a = lo2 + 32 * c + lane;
                         m[u] = c < nR ? cm[cmR + c] : 0u;
@@ -466,7 +451,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                         rv[u] = m[u] ? __ldcg(ro + a) : 0.0;
                     }
 #pragma unroll
-                    for (int u = 0; u < RS_VU; ++u) {
+                    for (int u = 0; u < C::VU; ++u) {
                         const int c = c0 + u * NW;
                         if (c >= nR) break;
                         const int32_t a = lo2 + 32 * c + lane;
@@ -481,15 +466,15 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                     }
                 }
                 RS_TS(5);
-                // 2B: t = Dhat^-1 Z^T r_new on own ocean points, RS_ZC chunks per warp in flight
+                // 2B: t = Dhat^-1 Z^T r_new on own ocean points, C::ZC chunks per warp in flight
                 const double* rb = buf - lo2;
-                for (int c0 = warp; c0 < nch; c0 += RS_ZC * NW) {
-                    double z[RS_ZC][kEll], pv[RS_ZC];
-                    uint2 cw[RS_ZC];
-                    int32_t o0[RS_ZC], ol[RS_ZC];
-                    uint32_t m[RS_ZC];
+                for (int c0 = warp; c0 < nch; c0 += C::ZC * NW) {
+                    double z[C::ZC][kEll], pv[C::ZC];
+                    uint2 cw[C::ZC];
+                    int32_t o0[C::ZC], ol[C::ZC];
+                    uint32_t m[C::ZC];
 #pragma unroll
-                    for (int u = 0; u < RS_ZC; ++u) {
+                    for (int u = 0; u < C::ZC; ++u) {
                         const int c = c0 + u * NW;
                         const int32_t a = f0 + 32 * c + lane, e = a - (int32_t)A.hoff;
                         m[u] = c < nch ? cm[cmF + c] : 0u;
@@ -504,10 +489,10 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                         ol[u] = (int32_t)((ob - oa) >> 5);
                     }
 #pragma unroll
-                    for (int u = 0; u < RS_ZC; ++u) {
+                    for (int u = 0; u < C::ZC; ++u) {
                         if (!m[u]) continue;
                         const int32_t a = f0 + 32 * (c0 + u * NW) + lane;
-                        const double acc = rs_row(z[u], cw[u], o0[u], ol[u], a, rb, A.zt.oval, A.zt.ocol);
+                        const double acc = rs_row<C::OVF>(z[u], cw[u], o0[u], ol[u], a, rb, A.zt.oval, A.zt.ocol);
                         if ((m[u] >> lane) & 1u) A.t[a] = __ddiv_rn(acc, pv[u]);
                     }
                 }
@@ -522,29 +507,29 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                 RS_TS(7);
                 // 2C: t over [f0, hi2) -> buf (land chunks: 0)
                 const int nT = (hi2 - f0) >> 5;
-                for (int c0 = warp; c0 < nT; c0 += RS_VU * NW) {
-                    double tv[RS_VU];
+                for (int c0 = warp; c0 < nT; c0 += C::VU * NW) {
+                    double tv[C::VU];
 #pragma unroll
-                    for (int u = 0; u < RS_VU; ++u) {
+                    for (int u = 0; u < C::VU; ++u) {
                         const int c = c0 + u * NW;
                         tv[u] = (c < nT && cm[cmF + c]) ? __ldcg(A.t + f0 + 32 * c + lane) : 0.0;
                     }
 #pragma unroll
-                    for (int u = 0; u < RS_VU; ++u) {
+                    for (int u = 0; u < C::VU; ++u) {
                         const int c = c0 + u * NW;
                         if (c < nT) buf[32 * c + lane] = tv[u];
                     }
                 }
                 RS_TS(8);
-                // 2D: s = Z t on own ocean points, (s, r_new) warp sums, RS_ZC chunks per warp in flight
+                // 2D: s = Z t on own ocean points, (s, r_new) warp sums, C::ZC chunks per warp in flight
                 const double* tb = buf - f0;
-                for (int c0 = warp; c0 < nch; c0 += RS_ZC * NW) {
-                    double z[RS_ZC][kEll], rv[RS_ZC];
-                    uint2 cw[RS_ZC];
-                    int32_t o0[RS_ZC], ol[RS_ZC];
-                    uint32_t m[RS_ZC];
+                for (int c0 = warp; c0 < nch; c0 += C::ZC * NW) {
+                    double z[C::ZC][kEll], rv[C::ZC];
+                    uint2 cw[C::ZC];
+                    int32_t o0[C::ZC], ol[C::ZC];
+                    uint32_t m[C::ZC];
 #pragma unroll
-                    for (int u = 0; u < RS_ZC; ++u) {
+                    for (int u = 0; u < C::ZC; ++u) {
                         const int c = c0 + u * NW;
                         const int32_t a = f0 + 32 * c + lane, e = a - (int32_t)A.hoff;
                         m[u] = c < nch ? cm[cmF + c] : 0u;
@@ -559,13 +544,13 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                         ol[u] = (int32_t)((ob - oa) >> 5);
                     }
 #pragma unroll
-                    for (int u = 0; u < RS_ZC; ++u) {
+                    for (int u = 0; u < C::ZC; ++u) {
                         const int c = c0 + u * NW;
                         if (c >= nch) break;
                         const int32_t a = f0 + 32 * c + lane;
                         double v = 0.0;
                         if (m[u]) {
-                            const double acc = rs_row(z[u], cw[u], o0[u], ol[u], a, tb, A.z.oval, A.z.ocol);
+                            const double acc = rs_row<C::OVF>(z[u], cw[u], o0[u], ol[u], a, tb, A.z.oval, A.z.ocol);
                             if ((m[u] >> lane) & 1u) {
                                 A.s[a] = acc;
                                 v = __dmul_rn(acc, rv[u]);
@@ -577,11 +562,11 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                 }
             } else {
                 // Jacobi / none: r_new, s = r_new / A_pp (or r_new), (r, r), (s, r) in one pass
-                for (int c0 = warp; c0 < nch; c0 += RS_VU * NW) {
-                    double qv[RS_VU], rv[RS_VU], dv[RS_VU];
-                    uint32_t m[RS_VU];
+                for (int c0 = warp; c0 < nch; c0 += C::VU * NW) {
+                    double qv[C::VU], rv[C::VU], dv[C::VU];
+                    uint32_t m[C::VU];
 #pragma unroll
-                    for (int u = 0; u < RS_VU; ++u) {
+                    for (int u = 0; u < C::VU; ++u) {
                         const int c = c0 + u * NW;
                         const int32_t a = f0 + 32 * c + lane;
                         m[u] = c < nch ? cm[cmF + c] : 0u;
@@ -590,7 +575,7 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                         dv[u] = (PC == 1 && m[u]) ? __ldg(A.diag + a) : 1.0;
                     }
 #pragma unroll
-                    for (int u = 0; u < RS_VU; ++u) {
+                    for (int u = 0; u < C::VU; ++u) {
                         const int c = c0 + u * NW;
                         if (c >= nch) break;
                         const int32_t a = f0 + 32 * c + lane;
@@ -610,15 +595,15 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
                 }
             }
             __syncthreads();
-            rs_partials(ua2, nu2, uc2, ws2, A.partial[1]);
-            rs_partials(ua2, nu2, uc2, ws3, A.partial[2]);
+            rs_partials<NW>(ua2, nu2, uc2, ws2, A.partial[1]);
+            rs_partials<NW>(ua2, nu2, uc2, ws3, A.partial[2]);
         }
         RS_T(9);
         bar += nblk;
         rs_grid_sync(rs_sync, bar);
         RS_T(10);
         double rr, rho_new;
-        rs_final2<RS_FINAL_NB2>(A.partial[1], A.partial[2], U, bc, rr, rho_new);
+        rs_final2<C::NB2>(A.partial[1], A.partial[2], U, bc, rr, rho_new);
         RS_T(11);
         k += 1;
         xpend = 1;
@@ -640,11 +625,11 @@ __global__ void __launch_bounds__(kRsThreads, 1) rs_loop_kernel(const KArgs A) {
     }
 }
 
-template <bool SIGMA>
+template <bool SIGMA, int NT>
 const void* rs_fn(int pc) {
-    if (pc == 1) return (const void*)rs_loop_kernel<SIGMA, 1>;
-    if (pc == 2) return (const void*)rs_loop_kernel<SIGMA, 2>;
-    return (const void*)rs_loop_kernel<SIGMA, 0>;
+    if (pc == 1) return (const void*)rs_loop_kernel<SIGMA, 1, NT>;
+    if (pc == 2) return (const void*)rs_loop_kernel<SIGMA, 2, NT>;
+    return (const void*)rs_loop_kernel<SIGMA, 0, NT>;
 }
 
 }  // namespace
@@ -668,7 +653,10 @@ size_t rs_smem_bytes(int32_t cap, int32_t maxu1, int32_t maxu2, int32_t maxnx) {
            (size_t)(maxu1 + maxu2 + 2) * 4 + (size_t)maxnx * 2 + 16;
 }
 
-const void* rs_kernel_fn(const KArgs& A) { return A.sigma ? rs_fn<true>(A.precond) : rs_fn<false>(A.precond); }
+const void* rs_kernel_fn(const KArgs& A) {
+    if (A.rs.nt == 768) return A.sigma ? rs_fn<true, 768>(A.precond) : rs_fn<false, 768>(A.precond);
+    return A.sigma ? rs_fn<true, 512>(A.precond) : rs_fn<false, 512>(A.precond);
+}
 
 cudaError_t launch_rs(const KArgs& A, cudaStream_t st) {
     const void* fn = rs_kernel_fn(A);
@@ -676,7 +664,7 @@ cudaError_t launch_rs(const KArgs& A, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)A.rs.nblk);
-    cfg.blockDim = dim3((unsigned)kRsThreads);
+    cfg.blockDim = dim3((unsigned)A.rs.nt);
     cfg.dynamicSmemBytes = A.rs.smem;
     cfg.stream = st;
     cudaLaunchAttribute at[2];

@@ -703,7 +703,11 @@ Status setup_rs(pcg_ctx* c) {
     // Z (two rounds in flight), land 0.05, plus 0.43 per chunk of the r_new / t copies (own + halo).  Greedy contiguous blocks under a
     // target time, bisection on the target for nblk blocks, at most maxch chunks per block (the
     // shared-memory buffer).
-    const int NW = kRsThreads / 32;
+    // block size: 768 threads (80 registers) for the bandwidth-heavier passes -- every Jacobi / none
+    // size, factored from 4096 units (cfg4) -- 512 (128 registers) for the small factored grids
+    int nt = (!fac || U >= 4096) ? kRsThreadsLarge : kRsThreadsSmall;
+    if (const char* e = getenv("PCG_RS_THREADS")) nt = atoi(e) == kRsThreadsLarge ? kRsThreadsLarge : kRsThreadsSmall;
+    const int NW = nt / 32;
     // model constants (us): K1 ocean chunk, K1 shared per chunk, K2/K3 ocean chunk, per overflow
     // round, K2/K3 shared per chunk; PCG_RS_MODEL="a,b,c,d,e" overrides (tuning)
     double mk[5] = {0.45, 0.25, 0.85, 0.65, 0.43};
@@ -863,19 +867,19 @@ Status setup_rs(pcg_ctx* c) {
     if (Status s = upload(c, d_w2, wait2); !s) return s;
     if (Status s = upload(c, d_pf, pf); !s) return s;
     if (Status s = dalloc(c, d_sync, (int64_t)nblk + 1); !s) return s;
-    r.nblk = nblk; r.cap = (int32_t)cap; r.maxu1 = maxu1; r.maxu2 = maxu2; r.maxnx = (int32_t)maxnx; r.smem = smem;
+    r.nblk = nblk; r.nt = nt; r.cap = (int32_t)cap; r.maxu1 = maxu1; r.maxu2 = maxu2; r.maxnx = (int32_t)maxnx; r.smem = smem;
     r.ub1 = d_ub1; r.ub2 = d_ub2; r.lo2 = d_lo; r.hi2 = d_hi; r.wait2 = d_w2; r.sync = d_sync; r.pf = d_pf;
     // co-residency of one block per SM (cooperative launch)
     A.rs = r;
     const void* fn = rs_kernel_fn(A);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kRsThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, nt, smem);
     cudaGetLastError();
     A.rs.on = per_sm >= 1 ? 1 : 0;
     if (getenv("PCG_VERBOSE"))
         fprintf(stderr, "libpcg: resident strips %s: %d blocks x %d threads, buffer %lld doubles, smem %zu B, units/block <= %d / %d\n",
-                A.rs.on ? "on" : "off (occupancy)", nblk, kRsThreads, (long long)cap, smem, maxu1, maxu2);
+                A.rs.on ? "on" : "off (occupancy)", nblk, nt, (long long)cap, smem, maxu1, maxu2);
     return Status::ok();
 }
 

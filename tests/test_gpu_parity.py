@@ -449,7 +449,8 @@ VARIANTS = {"graph_driver": {"PCG_RS": "0"},
             "graph_no_redundant": {"PCG_RS": "0", "PCG_REDUNDANT": "0"},
             "graph_k1_tma_no_redundant": {"PCG_RS": "0", "PCG_K1TMA": "1", "PCG_REDUNDANT": "0"},
             "graph_kfin": {"PCG_RS": "0", "PCG_KFIN": "1"},
-            "graph_kfin_k1_tma": {"PCG_RS": "0", "PCG_KFIN": "1", "PCG_K1TMA": "1"}}
+            "graph_kfin_k1_tma": {"PCG_RS": "0", "PCG_KFIN": "1", "PCG_K1TMA": "1"},
+            "rs_768_threads": {"PCG_RS_THREADS": "768"}}
 
 
 @pytest.mark.parametrize("variant", sorted(VARIANTS))
@@ -473,7 +474,7 @@ def test_kernel_variants_bitwise_canonical(name, variant, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{"PCG_RS": "0", "PCG_K1FLAT": "0", "PCG_K1TMA": "0"}, {"PCG_RS": "0", "PCG_L2PERSIST": "0"},
-                                 {"PCG_RS": "0", "PCG_K1TMA": "1"}, {"PCG_RS": "0"}, {}])
+                                 {"PCG_RS": "0", "PCG_K1TMA": "1"}, {"PCG_RS": "0"}, {}, {"PCG_RS_THREADS": "512"}])
 @pytest.mark.parametrize("precond", ["jacobi", "none"])
 def test_diag_k1_forms_bitwise_canonical(precond, env, monkeypatch):
     """Jacobi / none on the graph path (cfg3) with either K1 form: the 4-row strips (forced, or
