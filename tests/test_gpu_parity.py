@@ -799,7 +799,7 @@ def test_timestep_warm_modes_and_aliasing():
 
 # ------------------------------------------ the NCCL path across real GPUs (skipped on 1 GPU)
 @pytest.mark.parametrize("w", [0, 3])
-@pytest.mark.parametrize("device_comm", [False, True])
+@pytest.mark.parametrize("device_comm", [False, True, "halo"])
 def test_nccl_two_ranks_equals_local_ranks(w, device_comm, tmp_path):
     """Two processes, one GPU each, NCCL send/recv halos and allgathered rank sums (the code the
     one-GPU tests reach only through the local-ranks backend) -- or, with PCG_FLAG_DEVICE_COMM, the
@@ -818,7 +818,12 @@ def test_nccl_two_ranks_equals_local_ranks(w, device_comm, tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2", "--master-addr",
            "127.0.0.1", "--master-port", "29531", os.path.join(root, "tests", "nccl_worker.py"), out, "cfg3", str(w),
            str(pcg.FLAG_DEVICE_COMM if device_comm else 0)]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ)
+    if device_comm == "halo":                            # the NVLink halo stores (opt-in, w = 0 only)
+        if w:
+            pytest.skip("halo stores need block-local AINV")
+        env["PCG_DC_HALO"] = "1"
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     got = np.load(out + ".npz")
     R = pcg.LocalRanks(p.cE, p.cN, p.mask, 2, tau=TAU, ainv_halo=w)
