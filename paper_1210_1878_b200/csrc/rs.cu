@@ -50,15 +50,48 @@ namespace {
 // per array for (r, r), (s, r)).  512 threads get 128 registers, 768 threads 80 (measured at
 // cfg4: 768 threads 75.7 vs 76.6 us per iteration for AINV(0.1), 34.2 vs 36.7 for Jacobi; at
 // cfg2 / cfg3 AINV 16.0 / 19.8 vs 14.9 / 17.9 -- setup_rs picks per problem).
-template <int NT>
+template <int NT, int PC>
 struct RsCfg;
-template <>
-struct RsCfg<512> {
+template <int PC>
+struct RsCfg<512, PC> {
     static constexpr int VU = 8, K1C = 4, ZC = 2, OVF = 8, NB = 24, NB2 = 12;
 };
-template <>
-struct RsCfg<768> {
-    static constexpr int VU = 4, K1C = 2, ZC = 2, OVF = 4, NB = 12, NB2 = 6;
+// 768 threads (tuning hooks RS768_* for the factored instantiation, RS768D_* for Jacobi / none)
+#ifndef RS768_VU
+#define RS768_VU 4
+#endif
+#ifndef RS768_K1C
+#define RS768_K1C 4
+#endif
+#ifndef RS768_ZC
+#define RS768_ZC 2
+#endif
+#ifndef RS768_OVF
+#define RS768_OVF 4
+#endif
+#ifndef RS768_NB
+#define RS768_NB 16
+#endif
+#ifndef RS768_NB2
+#define RS768_NB2 8
+#endif
+#ifndef RS768D_VU
+#define RS768D_VU 4
+#endif
+#ifndef RS768D_K1C
+#define RS768D_K1C 2
+#endif
+#ifndef RS768D_NB
+#define RS768D_NB 12
+#endif
+#ifndef RS768D_NB2
+#define RS768D_NB2 6
+#endif
+template <int PC>
+struct RsCfg<768, PC> {
+    static constexpr bool F = PC == 0;
+    static constexpr int VU = F ? RS768_VU : RS768D_VU, K1C = F ? RS768_K1C : RS768D_K1C, ZC = RS768_ZC,
+                         OVF = RS768_OVF, NB = F ? RS768_NB : RS768D_NB, NB2 = F ? RS768_NB2 : RS768D_NB2;
 };
 
 // Diagnostic build only (-DRS_TIMELINE): per-block globaltimer durations of each pass, summed over
@@ -260,7 +293,7 @@ __device__ __forceinline__ double rs_row(const double (&z)[kEll], uint2 cw, int6
 // PC: 0 = factored Z Dhat^-1 Z^T (AINV, P_B2, FSAI through the ELL form), 1 = Jacobi, 2 = none
 template <bool SIGMA, int PC, int NT>
 __global__ void __launch_bounds__(NT, 1) rs_loop_kernel(const KArgs A) {
-    using C = RsCfg<NT>;
+    using C = RsCfg<NT, PC>;
     extern __shared__ __align__(16) double sm[];
     __shared__ double bc[2];
     constexpr int NW = NT / 32;
