@@ -184,7 +184,7 @@ def run_reference(args):
     p = synth.config(args.config)
     n_iter = args.ref_iters
     cores, model = cpu_info()
-    for _ in range(args.warmup if args.warmup <= 1 else 1):
+    for _ in range(args.warmup):                         # W warm-up steps (short samples)
         cpu_oracle_sample(p, args.tau, 2, mode="chunked")
     tot_it, tot_s, setup = 0, 0.0, []
     for _ in range(args.steps):
