@@ -710,7 +710,11 @@ Status setup_rs(pcg_ctx* c) {
     const int NW = nt / 32;
     // model constants (us): K1 ocean chunk, K1 shared per chunk, K2/K3 ocean chunk, per overflow
     // round, K2/K3 shared per chunk; PCG_RS_MODEL="a,b,c,d,e" overrides (tuning)
-    double mk[5] = {0.45, 0.25, 0.85, 0.65, 0.43};
+    // (K1 ocean chunk 0.45 -> 0.3, measured round 2 with 768 threads: the land-heavy blocks get
+    // fewer units, the widest phase-1 range -- which sizes every block's shared memory -- shrinks
+    // from 93 to 75 units (227 -> 190 KB), the L1 left to each SM grows, and cfg4 AINV runs at
+    // 67.6 instead of 75.0 us per iteration; cfg2 / cfg3 unchanged)
+    double mk[5] = {0.3, 0.25, 0.85, 0.65, 0.43};
     if (const char* e = getenv("PCG_RS_MODEL"))
         sscanf(e, "%lf,%lf,%lf,%lf,%lf", &mk[0], &mk[1], &mk[2], &mk[3], &mk[4]);
     const int64_t lim_dbl = (int64_t)((limit > 24576 ? limit - 24576 : 0) / 8);
@@ -778,7 +782,24 @@ Status setup_rs(pcg_ctx* c) {
     };
     std::vector<int32_t> ub1, ub2;
     const int64_t h1 = (2 * (int64_t)P.pitch) / 32, h2 = (4 * (int64_t)P.pitch) / 32;
-    const double t1 = model_split(wc1, mk[1], h1, std::max<int64_t>(8, lim_dbl / 32 - h1), ub1);
+    // Phase 1 gets at most 1.6x the mean chunks per block (PCG_RS_MAXCH1): its widest range sizes
+    // every block's shared memory, and a block buffer near the 227 KB limit leaves the SM too
+    // little L1 -- measured at cfg4, one land-heavy block of 93 units (227 KB) made the whole loop
+    // 75 instead of 67.5 us per iteration; with the cap the partition stays near 190 KB whatever
+    // the cost model's land / ocean ratio
+    int64_t maxch1 = std::max<int64_t>(8, lim_dbl / 32 - h1);
+    {
+        double f = U >= 4096 ? 1.6 : 0.0;              // the large grids (small ones: measured slower)
+        if (const char* e = getenv("PCG_RS_MAXCH1")) f = atof(e);
+        int64_t tot = 0;
+        for (const auto& w : wc1) tot += (int64_t)w.size();
+        const double mean = (double)tot / nblk;
+        // never below the mean plus two units' chunks, so a partition always exists (small grids)
+        if (f > 0) maxch1 = std::min<int64_t>(maxch1, (int64_t)std::max(f * mean, mean + 2.0 * W + 8.0));
+    }
+    double t1 = model_split(wc1, mk[1], h1, maxch1, ub1);
+    if ((int)ub1.size() != nblk + 1 || ub1[(size_t)nblk] != U)       // cap too tight: without it
+        t1 = model_split(wc1, mk[1], h1, std::max<int64_t>(8, lim_dbl / 32 - h1), ub1);
     const double t2 = model_split(wc2, fac ? mk[4] : 0.2, fac ? h2 : 0, std::max<int64_t>(8, lim_dbl / 32 - 2 * h2), ub2);
     if ((int)ub1.size() != nblk + 1 || (int)ub2.size() != nblk + 1) return Status::ok();
     if (getenv("PCG_VERBOSE")) fprintf(stderr, "libpcg: resident strips model time K1 %.1f + K2/K3 %.1f us per iteration\n", t1, t2);
