@@ -12,7 +12,11 @@
 // Block mode (reading R15): the index set is the ocean points of grid rows
 // [row_lo, row_hi); the principal submatrix of A on that set is orthogonalised and only
 // the columns of rows >= row_own are returned ("AINV computed per partition").
+#include <sys/mman.h>
+
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <memory>
 #include <mutex>
@@ -39,17 +43,23 @@ struct BlockMatrix {
     bigvec<double> diag;              // A_pp
 };
 
-// zero-initialised array from calloc: the pages a thread never touches are never written (the
-// per-thread n-sized work arrays of the column workers touch only their columns' neighbourhood)
+// zero-initialised array from an anonymous mapping advised as transparent huge pages: the pages a
+// thread never touches are never written (the per-thread n-sized work arrays of the column
+// workers touch only their columns' neighbourhood), and the ones it touches fault in 2 MB at a
+// time (4 KB faults of 16 threads serialise in the kernel)
 template <class T>
-struct CallocArr {
+struct ZeroArr {
     T* p = nullptr;
-    explicit CallocArr(size_t n) : p(static_cast<T*>(std::calloc(std::max<size_t>(n, 1), sizeof(T)))) {
-        if (!p) throw std::bad_alloc();
+    size_t bytes = 0;
+    explicit ZeroArr(size_t n) : bytes((std::max<size_t>(n, 1) * sizeof(T) + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1)) {
+        void* m = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (m == MAP_FAILED) throw std::bad_alloc();
+        madvise(m, bytes, MADV_HUGEPAGE);
+        p = static_cast<T*>(m);
     }
-    ~CallocArr() { std::free(p); }
-    CallocArr(const CallocArr&) = delete;
-    CallocArr& operator=(const CallocArr&) = delete;
+    ~ZeroArr() { munmap(p, bytes); }
+    ZeroArr(const ZeroArr&) = delete;
+    ZeroArr& operator=(const ZeroArr&) = delete;
     T& operator[](size_t i) { return p[i]; }
 };
 
@@ -77,6 +87,36 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
         for (int t = 1; t < T; ++t) pool.emplace_back(f, n_ * t / T, n_ * (t + 1) / T);
         f(0, n_ / T);
         for (auto& th : pool) th.join();
+    };
+    const bool verbose = getenv("PCG_VERBOSE") != nullptr;
+    auto tprev = std::chrono::steady_clock::now();
+    auto stage = [&](const char* what) {
+        if (!verbose) return;
+        const auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "libpcg:   ainv %-24s %.3f s\n", what, std::chrono::duration<double>(now - tprev).count());
+        tprev = now;
+    };
+    // exclusive prefix sum out[0..n] of cnt(i) in T0 contiguous ranges (two passes)
+    auto prefix = [&](int64_t n_, auto&& cnt, auto* out) {
+        const int T = n_ < 50000 ? 1 : T0;
+        std::vector<int64_t> part((size_t)T + 1, 0);
+        auto run = [&](auto&& body) {
+            std::vector<std::thread> pool;
+            for (int t = 1; t < T; ++t) pool.emplace_back([&, t] { body(t, n_ * t / T, n_ * (t + 1) / T); });
+            body(0, 0, n_ / T);
+            for (auto& th : pool) th.join();
+        };
+        run([&](int t, int64_t a, int64_t b) {
+            int64_t sum = 0;
+            for (int64_t i = a; i < b; ++i) sum += cnt(i);
+            part[(size_t)t + 1] = sum;
+        });
+        for (int t = 0; t < T; ++t) part[(size_t)t + 1] += part[(size_t)t];
+        run([&](int t, int64_t a, int64_t b) {
+            int64_t acc = part[(size_t)t];
+            for (int64_t i = a; i < b; ++i) { out[i] = acc; acc += cnt(i); }
+        });
+        out[n_] = part[(size_t)T];
     };
     BlockMatrix M;
     // local numbering of the ocean points of rows [r0, r1), natural order: ocean points per row,
@@ -108,7 +148,8 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
             }
         }
     });
-    M.rp.assign(n + 1, 0);
+    stage("numbering");
+    M.rp.resize((size_t)n + 1);
     M.diag.resize(n);
     bigvec<double> sc(n);
     // diagonal A_pp = ((c_E + c_W) + c_N) + c_S (+ sigma) over all faces, then s = 1/sqrt(A_pp)
@@ -151,7 +192,8 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
             m5[p] = (uint8_t)m;
         }
     });
-    for (int32_t p = 0; p < n; ++p) M.rp[p + 1] = M.rp[p] + m5[p];
+    stage("diag + 5 slots");
+    prefix(n, [&](int64_t p) { return (int64_t)m5[p]; }, M.rp.data());
     M.ci.resize(M.rp[n]);
     M.a.resize(M.rp[n]);
     pfor(n, [&](int64_t lo, int64_t hi) {
@@ -159,6 +201,7 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
             for (int x = 0; x < m5[p]; ++x) { M.ci[M.rp[p] + x] = c5[(size_t)5 * p + x]; M.a[M.rp[p] + x] = a5[(size_t)5 * p + x]; }
     });
 
+    stage("CSR");
     // Zhat columns and pivots.  Column j needs the finished columns i < j it meets as
     // candidates (pivot p_i, entries of zhat_i), nothing else, so the columns can be built by
     // several threads at once with bitwise the sequential result (every column runs the same
@@ -175,26 +218,42 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
         const double* v = nullptr;
         int32_t len = 0;
     };
-    std::vector<ColRef> cref(n);
-    std::vector<double> piv(n);
+    bigvec<ColRef> cref(n);                      // written before done[j], read after it
+    bigvec<double> piv(n);
     std::unique_ptr<std::atomic<uint8_t>[]> done(new std::atomic<uint8_t>[std::max(n, 1)]);
-    for (int32_t p = 0; p < n; ++p) done[p].store(0, std::memory_order_relaxed);
+    pfor(n, [&](int64_t lo, int64_t hi) { for (int64_t p = lo; p < hi; ++p) done[p].store(0, std::memory_order_relaxed); });
     std::atomic<int32_t> limit(n);
     int T = std::max(1, threads);
     if (n < 20000) T = 1;
     T = std::min(T, std::max(1, ni / 64));
+    // thread t: grid columns [cb[t], cb[t+1]) of every row (i -> min(T-1, i T / ni)), its
+    // unknowns in increasing order, listed by the threads themselves from the local numbering
+    std::vector<int32_t> cb((size_t)T + 1, ni);
+    for (int32_t i = ni - 1; i >= 0; --i) cb[(size_t)std::min<int64_t>(T - 1, (int64_t)i * T / ni)] = i;
+    for (int t = T - 1; t >= 0; --t) cb[(size_t)t] = std::min(cb[(size_t)t], cb[(size_t)t + 1]);
     std::vector<std::vector<int32_t>> mine((size_t)T);
-    for (int32_t p = 0; p < n; ++p) {
-        const int32_t i = (int32_t)(M.grid[p] % ni);
-        mine[(size_t)std::min<int64_t>(T - 1, (int64_t)i * T / ni)].push_back(p);
+    {
+        std::vector<std::thread> pool;
+        auto list = [&](int t) {
+            std::vector<int32_t>& v = mine[(size_t)t];
+            v.reserve((size_t)n / T + (size_t)nr + 16);
+            for (int32_t r = 0; r < nr; ++r)
+                for (int32_t i = cb[(size_t)t]; i < cb[(size_t)t + 1]; ++i) {
+                    const int32_t p = loc[(size_t)r * ni + i];
+                    if (p >= 0) v.push_back(p);
+                }
+        };
+        for (int t = 1; t < T; ++t) pool.emplace_back(list, t);
+        list(0);
+        for (auto& th : pool) th.join();
     }
     std::vector<std::vector<std::unique_ptr<int32_t[]>>> seg_r((size_t)T);
     std::vector<std::vector<std::unique_ptr<double[]>>> seg_v((size_t)T);
     auto worker = [&](int t) {
-        CallocArr<double> w((size_t)n);
-        CallocArr<uint8_t> live((size_t)n);     // entry present in the current column
-        CallocArr<int32_t> listed((size_t)n);   // stamp j + 1: k recorded in `members` for column j
-        CallocArr<int32_t> queued((size_t)n);   // stamp j + 1: k queued as a candidate for column j
+        ZeroArr<double> w((size_t)n);
+        ZeroArr<uint8_t> live((size_t)n);     // entry present in the current column
+        ZeroArr<int32_t> listed((size_t)n);   // stamp j + 1: k recorded in `members` for column j
+        ZeroArr<int32_t> queued((size_t)n);   // stamp j + 1: k queued as a candidate for column j
         std::vector<int32_t> members, touched;
         std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> cand;
         // column storage in fixed segments (a column's entries never move once published; the
@@ -301,12 +360,14 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
             done[j].store(1, std::memory_order_release);
         }
     };
+    stage("numbering + scaled CSR");
     {
         std::vector<std::thread> pool;
         for (int t = 1; t < T; ++t) pool.emplace_back(worker, t);
         worker(0);
         for (auto& th : pool) th.join();
     }
+    stage("column wavefront");
     const int64_t fail = limit.load() < n ? (int64_t)limit.load() : -1;
     blk.fail_grid = fail >= 0 ? M.grid[fail] : -1;
     if (fail >= 0) return;
@@ -318,8 +379,7 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
         if (M.grid[p] / ni >= blk.row_own) { first_owned = p; break; }
     const int32_t nown = n - first_owned;
     blk.colptr.resize((size_t)nown + 1);
-    blk.colptr[0] = 0;
-    for (int32_t q = 0; q < nown; ++q) blk.colptr[q + 1] = blk.colptr[q] + cref[first_owned + q].len;
+    prefix(nown, [&](int64_t q) { return (int64_t)cref[first_owned + q].len; }, blk.colptr.data());
     blk.row_g.resize((size_t)blk.colptr[nown]);
     blk.zhat.resize((size_t)blk.colptr[nown]);
     blk.piv.resize(nown);
@@ -336,6 +396,7 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
             blk.col_g[q] = M.grid[j];
         }
     });
+    stage("owned columns");
 }
 
 }  // namespace pcg

@@ -7,7 +7,11 @@
 // i >= ni, land points and (on one GPU) the halo rows hold 0 in every vector.
 #pragma once
 
+#include <sys/mman.h>
+
 #include <cstdint>
+#include <cstdlib>
+#include <new>
 #include <string>
 #include <functional>
 #include <utility>
@@ -38,6 +42,31 @@ struct NoInitAlloc : std::allocator<T> {
     NoInitAlloc() noexcept = default;
     template <class U> NoInitAlloc(const NoInitAlloc<U>&) noexcept {}
     template <class U> struct rebind { using other = NoInitAlloc<U>; };
+    // arrays of 2 MB and more: 2 MB-aligned and advised as transparent huge pages, so the
+    // parallel first touch takes one fault per 2 MB instead of one per 4 KB page (page faults
+    // of one process serialise in the kernel)
+    static constexpr size_t kHuge = size_t(2) << 20;
+    T* allocate(size_t n) {
+        const size_t bytes = n * sizeof(T);
+#ifndef PCG_NO_THP
+        if (bytes < kHuge) return std::allocator<T>::allocate(n);
+#else
+        if (true) return std::allocator<T>::allocate(n);
+#endif
+        const size_t r = (bytes + kHuge - 1) / kHuge * kHuge;
+        void* p = std::aligned_alloc(kHuge, r);
+        if (!p) throw std::bad_alloc();
+        madvise(p, r, MADV_HUGEPAGE);
+        return static_cast<T*>(p);
+    }
+    void deallocate(T* p, size_t n) noexcept {
+#ifndef PCG_NO_THP
+        if (n * sizeof(T) < kHuge) std::allocator<T>::deallocate(p, n);
+#else
+        if (true) std::allocator<T>::deallocate(p, n);
+#endif
+        else std::free(p);
+    }
     template <class U> void construct(U* p) noexcept { ::new ((void*)p) U; }
     template <class U, class... A> void construct(U* p, A&&... a) { ::new ((void*)p) U(std::forward<A>(a)...); }
 };
@@ -66,6 +95,7 @@ struct Ell {
     int64_t n = 0;                 // owned elements
     bigvec<double> val;            // n * kEll (element-major)
     bigvec<int32_t> col;           // n * kEll
+    bigvec<int16_t> col16;         // n * kEll: col - (own array index), when every slot fits (else empty)
     Sell ovf;
     int64_t entries() const { return (int64_t)val.size() + ovf.entries(); }
 };
@@ -97,11 +127,13 @@ struct Plan {
     // 0 where the chain is shorter.  dia_q = 0: no DIA form (the ELL path applies the factor).
     int32_t dia_q = 0;
     std::vector<double> dia;
-    // export (owned columns of Zhat, global unknown numbering)
-    std::vector<int64_t> zcolptr;
+    // export (owned columns of Zhat, global unknown numbering); zrow / zhat are filled only with
+    // keep_export (pcg_plan_build), not for pcg_setup, which never reads them
+    bool keep_export = true;
+    bigvec<int64_t> zcolptr;
     bigvec<int64_t> zrow;
     bigvec<double> zhat;
-    std::vector<double> pivots, scale;
+    bigvec<double> pivots, scale;
     double setup_s = 0.0;
     int64_t elements() const { return (int64_t)(nloc + 2 * halo) * pitch; }
     int64_t hoff() const { return (int64_t)halo * pitch; }   // array index of owned element 0

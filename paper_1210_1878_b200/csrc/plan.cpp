@@ -98,9 +98,9 @@ void pfor(int T, int64_t n, const std::function<void(int64_t, int64_t)>& f, int6
 }
 
 // exclusive prefix sum out[0..n] of cnt(i), i in [0, n), in T contiguous ranges (two passes)
-template <class F>
-void pscan(int T, int64_t n, std::vector<int64_t>& out, F cnt) {
-    out.assign((size_t)n + 1, 0);
+template <class V, class F>
+void pscan(int T, int64_t n, V& out, F cnt) {
+    out.resize((size_t)n + 1);                           // every slot is written below
     if (n < 100000) T = 1;
     T = std::max(1, T);
     std::vector<int64_t> part((size_t)T + 1, 0);
@@ -184,49 +184,62 @@ bool anchors_ok_parallel(int T, int32_t ni, int32_t nj, int32_t periodic, const 
     return ok.load();
 }
 
-// Pack a set of sparse rows (one per owned element e; entries (absolute array column, value) in
-// ascending column order) as ELL(kEll) + SELL-32 overflow (internal.h Ell): the first kEll
-// entries of every row in its fixed slots (padding: value 0 at the row's own array index), the
-// rest of the slice's rows as SELL-32 (L = the slice's longest overflow; padding: value 0 at the
-// row's own index).  One pass over the rows, no intermediate full SELL.
-void pack_ell(const std::vector<int64_t>& rowptr, const bigvec<int32_t>& cols,
-              const bigvec<double>& vals, int64_t nel, int32_t pitch, int32_t ni, int32_t periodic, int32_t halo,
-              Ell& E, int T) {
-    (void)ni; (void)periodic;
-    const int64_t hoff = (int64_t)halo * pitch;        // array index of owned element 0
+// ELL(kEll) + SELL-32 overflow (internal.h Ell) over nel owned elements, filled in place: the
+// first kEll entries of every row in its fixed slots, the rest of the slice's rows as SELL-32 (L =
+// the slice's longest overflow).  ell_shape sizes the arrays from the row lengths and writes the
+// padding everywhere (value 0 at the row's own array index; also the pages' first touch, in
+// parallel); ell_slot then gives the slot of a row's k-th entry, so the rows are written straight
+// from the AINV's columns (Z^T) or from the transposition (Z), with no intermediate copy.
+template <class F>
+void ell_shape(Ell& E, int64_t nel, int64_t hoff, int T, F len) {
     E.n = nel;
-    E.val.resize((size_t)kEll * nel);           // every slot is written below (padding: 0)
+    E.val.resize((size_t)kEll * nel);
     E.col.resize((size_t)kEll * nel);
     const int64_t nsl = nel / kSlice;
     pscan(T, nsl, E.ovf.off, [&](int64_t s) {
         int64_t L = 0;
-        for (int l = 0; l < kSlice; ++l) {
-            const int64_t e = s * kSlice + l;
-            L = std::max(L, rowptr[e + 1] - rowptr[e] - kEll);
-        }
+        for (int l = 0; l < kSlice; ++l) L = std::max(L, len(s * kSlice + l) - kEll);
         return L * kSlice;
     });
     E.ovf.val.resize(E.ovf.off[nsl]);
     E.ovf.col.resize(E.ovf.off[nsl]);
     pfor(T, nsl, [&](int64_t s0, int64_t s1) {
-    for (int64_t s = s0; s < s1; ++s) {
-        const int64_t L = (E.ovf.off[s + 1] - E.ovf.off[s]) / kSlice;
-        for (int l = 0; l < kSlice; ++l) {
-            const int64_t e = s * kSlice + l, r0 = rowptr[e], len = rowptr[e + 1] - r0;
-            const int32_t own = (int32_t)(e + hoff);
-            for (int m = 0; m < kEll; ++m) {
-                E.col[(size_t)e * kEll + m] = m < len ? cols[r0 + m] : own;
-                E.val[(size_t)e * kEll + m] = m < len ? vals[r0 + m] : 0.0;
-            }
-            for (int64_t m = 0; m < L; ++m) {
-                const int64_t slot = E.ovf.off[s] + m * kSlice + l;
-                const bool real = kEll + m < len;
-                E.ovf.col[slot] = real ? cols[r0 + kEll + m] : own;
-                E.ovf.val[slot] = real ? vals[r0 + kEll + m] : 0.0;
+        for (int64_t s = s0; s < s1; ++s) {
+            for (int64_t e = s * kSlice; e < (s + 1) * kSlice; ++e)
+                for (int m = 0; m < kEll; ++m) {
+                    E.col[(size_t)e * kEll + m] = (int32_t)(e + hoff);
+                    E.val[(size_t)e * kEll + m] = 0.0;
+                }
+            for (int64_t o = E.ovf.off[s]; o < E.ovf.off[s + 1]; ++o) {
+                E.ovf.col[(size_t)o] = (int32_t)(s * kSlice + (o - E.ovf.off[s]) % kSlice + hoff);
+                E.ovf.val[(size_t)o] = 0.0;
             }
         }
-    }
     });
+}
+// int16 slot offsets relative to the element's own array index (the device form of the ELL
+// columns); left empty when one does not fit
+void ell_col16(Ell& E, int64_t hoff, int T) {
+    E.col16.resize(E.col.size());
+    std::atomic<bool> fits(true);
+    pfor(T, (int64_t)E.col.size(), [&](int64_t a, int64_t b) {
+        for (int64_t m = a; m < b; ++m) {
+            const int64_t off = (int64_t)E.col[(size_t)m] - (m / kEll + hoff);
+            if (off < -32768 || off > 32767) { fits = false; return; }
+            E.col16[(size_t)m] = (int16_t)off;
+        }
+    });
+    if (!fits) { E.col16.clear(); E.col16.shrink_to_fit(); }
+}
+inline void ell_put(Ell& E, int64_t e, int64_t k, int32_t col, double val) {
+    if (k < kEll) {
+        E.col[(size_t)(e * kEll + k)] = col;
+        E.val[(size_t)(e * kEll + k)] = val;
+    } else {
+        const int64_t s = e / kSlice, o = E.ovf.off[(size_t)s] + (k - kEll) * kSlice + (e - s * kSlice);
+        E.ovf.col[(size_t)o] = col;
+        E.ovf.val[(size_t)o] = val;
+    }
 }
 
 }  // namespace
@@ -508,15 +521,16 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         return (int64_t)(j - P.jb + P.halo) * pitch + i;
     };
     P.zcolptr.assign(1, 0);
-    std::vector<int64_t> colarr;                 // array index of each owned column
-    bigvec<int64_t> ent_row_arr;                 // per entry: array index of its row
+    bigvec<int64_t> colarr;                      // array index of each owned column
+    bigvec<int32_t> ent_row_arr;                 // per entry: array index of its row
     bigvec<double> ent_z;                        // per entry: z value
     std::vector<int64_t> gunk_cache;
     // global unknown numbering of grid rows [min row_lo, je)
     int32_t rlo = P.je;
     for (auto& b : blocks) rlo = std::min(rlo, b.row_lo);
-    std::vector<int64_t> unk((size_t)(P.je - rlo) * ni, -1);
-    {
+    const bool exp = P.keep_export;
+    std::vector<int64_t> unk(exp ? (size_t)(P.je - rlo) * ni : 0, -1);
+    if (exp) {
         std::atomic<int64_t> below(0);
         pfor(nthr, (int64_t)rlo * ni, [&](int64_t a, int64_t b) {
             int64_t u = 0;
@@ -541,12 +555,12 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     // Jacobi scale s_g = 1/sqrt(A_gg) once per grid point of the rows the entries touch (the same
     // IEEE operations as per entry; FSAI: no scale)
     const int32_t rhi = std::min(nj, P.je + kNorthRows);
-    std::vector<double> sgrid((size_t)(rhi - rlo) * ni, 1.0);
-    if (P.precond != PCG_PRECOND_FSAI)
-        pfor(nthr, (int64_t)(rhi - rlo) * ni, [&](int64_t a, int64_t b) {
-            for (int64_t g2 = (int64_t)rlo * ni + a; g2 < (int64_t)rlo * ni + b; ++g2)
-                if (c->mask[g2]) sgrid[(size_t)(g2 - (int64_t)rlo * ni)] = 1.0 / std::sqrt(diag_of(g2));
-        });
+    bigvec<double> sgrid((size_t)(rhi - rlo) * ni);
+    pfor(nthr, (int64_t)(rhi - rlo) * ni, [&](int64_t a, int64_t b) {
+        for (int64_t g2 = (int64_t)rlo * ni + a; g2 < (int64_t)rlo * ni + b; ++g2)
+            sgrid[(size_t)(g2 - (int64_t)rlo * ni)] =
+                (P.precond != PCG_PRECOND_FSAI && c->mask[g2]) ? 1.0 / std::sqrt(diag_of(g2)) : 1.0;
+    });
     auto scale_of = [&](int64_t gr) { return sgrid[(size_t)(gr - (int64_t)rlo * ni)]; };
     int64_t ntot = 0, ncols = 0;
     for (auto& b : blocks) { ntot += b.colptr.back(); ncols += (int64_t)b.col_g.size(); }
@@ -567,7 +581,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         const int32_t q = colsrc[(size_t)k].second;
         return b.colptr[q + 1] - b.colptr[q];
     });
-    P.zrow.resize((size_t)ntot); P.zhat.resize((size_t)ntot);
+    if (exp) { P.zrow.resize((size_t)ntot); P.zhat.resize((size_t)ntot); }
     ent_z.resize((size_t)ntot); ent_row_arr.resize((size_t)ntot);
     P.pivots.resize((size_t)ncols); P.scale.resize((size_t)ncols); colarr.resize((size_t)ncols);
     pfor(nthr, ncols, [&](int64_t k0, int64_t k1) {
@@ -577,10 +591,12 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             int64_t dst = P.zcolptr[(size_t)k];
             for (int64_t e = b.colptr[q]; e < b.colptr[q + 1]; ++e, ++dst) {
                 const int64_t gr = b.row_g[e];
-                P.zrow[(size_t)dst] = unk[gr - (int64_t)rlo * ni];
-                P.zhat[(size_t)dst] = b.zhat[e];
+                if (exp) {
+                    P.zrow[(size_t)dst] = unk[gr - (int64_t)rlo * ni];
+                    P.zhat[(size_t)dst] = b.zhat[e];
+                }
                 ent_z[(size_t)dst] = scale_of(gr) * b.zhat[e];
-                ent_row_arr[(size_t)dst] = arr_of(gr);
+                ent_row_arr[(size_t)dst] = (int32_t)arr_of(gr);
             }
             P.pivots[(size_t)k] = b.piv[q];
             P.scale[(size_t)k] = scale_of(b.col_g[q]);
@@ -604,23 +620,23 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     // ---- SELL of Z^T rows: row (column j of Z) = entries k ascending
     const int64_t nown = P.owned_elements();
     {
-        std::vector<int64_t> len((size_t)nown, 0), rp;
+        bigvec<int64_t> colq((size_t)nown);                 // element -> owned column (-1: none)
+        pfor(nthr, nown, [&](int64_t a, int64_t b) { for (int64_t e = a; e < b; ++e) colq[(size_t)e] = -1; });
         pfor(nthr, (int64_t)colarr.size(), [&](int64_t a, int64_t b) {
-            for (int64_t q = a; q < b; ++q) len[(size_t)(colarr[(size_t)q] - hoff)] = P.zcolptr[(size_t)q + 1] - P.zcolptr[(size_t)q];
+            for (int64_t q = a; q < b; ++q) colq[(size_t)(colarr[(size_t)q] - hoff)] = q;
         });
-        pscan(nthr, nown, rp, [&](int64_t e) { return len[(size_t)e]; });
-        bigvec<int32_t> cols(rp[nown]);
-        bigvec<double> vals(rp[nown]);
+        auto len = [&](int64_t e) {
+            const int64_t q = colq[(size_t)e];
+            return q < 0 ? (int64_t)0 : P.zcolptr[(size_t)q + 1] - P.zcolptr[(size_t)q];
+        };
+        ell_shape(P.ZT, nown, hoff, nthr, len);
         pfor(nthr, (int64_t)colarr.size(), [&](int64_t q0, int64_t q1) {
             for (int64_t q = q0; q < q1; ++q) {
-                int64_t dst = rp[colarr[q] - hoff];
-                for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e, ++dst) {
-                    cols[dst] = (int32_t)ent_row_arr[e];
-                    vals[dst] = ent_z[e];
-                }
+                const int64_t e = colarr[(size_t)q] - hoff, z0 = P.zcolptr[(size_t)q];
+                for (int64_t k = 0; k < P.zcolptr[(size_t)q + 1] - z0; ++k)
+                    ell_put(P.ZT, e, k, ent_row_arr[(size_t)(z0 + k)], ent_z[(size_t)(z0 + k)]);
             }
         });
-        pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.halo, P.ZT, nthr);
     }
     stage("pack Z^T");
     // ---- SELL of Z rows: row i = entries z_ij over columns j ascending (owned rows only; with
@@ -638,7 +654,8 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
                 }
         for (int64_t r : nrow_arr)
             if (r < hoff) return Status::err(PCG_ERR_ARG, "internal: northern Z entry below the owned rows");
-        std::vector<int64_t> cnt((size_t)nown, 0), rp;
+        bigvec<int64_t> cnt((size_t)nown);
+        pfor(nthr, nown, [&](int64_t a, int64_t b) { for (int64_t e = a; e < b; ++e) cnt[(size_t)e] = 0; });
         pfor(nthr, (int64_t)ent_row_arr.size(), [&](int64_t a, int64_t b) {
             for (int64_t e = a; e < b; ++e) {
                 const int64_t r = ent_row_arr[(size_t)e];
@@ -646,10 +663,9 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             }
         });
         for (int64_t r : nrow_arr) cnt[(size_t)(r - hoff)]++;
-        pscan(nthr, nown, rp, [&](int64_t e) { return cnt[(size_t)e]; });
-        std::vector<int64_t> fill(rp.begin(), rp.end() - 1);
-        bigvec<int32_t> cols(rp[nown]);
-        bigvec<double> vals(rp[nown]);
+        ell_shape(P.Z, nown, hoff, nthr, [&](int64_t e) { return cnt[(size_t)e]; });
+        bigvec<int64_t> fill((size_t)nown);                     // entries placed per row so far
+        pfor(nthr, nown, [&](int64_t a, int64_t b) { for (int64_t e = a; e < b; ++e) fill[(size_t)e] = 0; });
         // transpose with the ascending column order per row kept: thread t owns the rows
         // [R_t, R_t+1) and visits, in ascending order, the columns that can hold entries of them
         // (a column's entries are at rows <= the column, so columns from the first row >= R_t on)
@@ -677,9 +693,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
                         const int64_t r = ent_row_arr[e] - hoff;
                         if (r < R1) below = true;
                         if (r < R0 || r >= R1) continue;
-                        cols[fill[r]] = (int32_t)colarr[q];
-                        vals[fill[r]] = ent_z[e];
-                        fill[r]++;
+                        ell_put(P.Z, r, fill[(size_t)r]++, (int32_t)colarr[q], ent_z[e]);
                     }
                     if (!below && colarr[q] - hoff >= R1 + reach) break;   // past Z's reach
                 }
@@ -689,13 +703,12 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             for (auto& th : pool) th.join();
         }
         for (size_t m = 0; m < nrow_arr.size(); ++m) {     // north columns, ascending
-            int64_t r = nrow_arr[m] - hoff;
-            cols[fill[r]] = (int32_t)ncol_arr[m];
-            vals[fill[r]] = nz[m];
-            fill[r]++;
+            const int64_t r = nrow_arr[m] - hoff;
+            ell_put(P.Z, r, fill[(size_t)r]++, (int32_t)ncol_arr[m], nz[m]);
         }
-        pack_ell(rp, cols, vals, nown, pitch, ni, P.periodic, P.halo, P.Z, nthr);
     }
+    ell_col16(P.ZT, hoff, nthr);
+    ell_col16(P.Z, hoff, nthr);
     stage("pack Z");
     // ---- FSAI DIA form: each owned column's entries at consecutive columns of the
     // same grid row i-1, i-2, ... (no land, wrap or N-S link inside the chain) -> diagonals

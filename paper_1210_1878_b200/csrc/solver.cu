@@ -905,6 +905,7 @@ Status setup_rs(pcg_ctx* c) {
 }
 
 Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_ctx* c) {
+    c->plan.keep_export = false;
     if (Status s = build_plan(co, g, o, c->plan); !s) return s;
     Plan& P = c->plan;
     c->device = g->device;
@@ -940,18 +941,8 @@ Status do_setup(const pcg_coeffs* co, const pcg_grid* g, const pcg_opts* o, pcg_
         // int16 slot offsets relative to the element's own array index (PCG_COL16=0 disables)
         const char* ce = getenv("PCG_COL16");
         if (!(ce && atoi(ce) == 0) && P.dia_q == 0) {
-            auto rel16 = [&](const Ell& E, int16_t*& dst) -> Status {
-                std::vector<int16_t> r(E.col.size());
-                const int64_t hoff = P.hoff();
-                for (size_t m = 0; m < E.col.size(); ++m) {
-                    const int64_t off = (int64_t)E.col[m] - ((int64_t)(m / kEll) + hoff);
-                    if (off < -32768 || off > 32767) return Status::ok();      // keep int32 columns
-                    r[m] = (int16_t)off;
-                }
-                return upload(c, dst, r);
-            };
-            if (Status st = rel16(P.ZT, c->zt_c16); !st) return st;
-            if (Status st = rel16(P.Z, c->z_c16); !st) return st;
+            if (!P.ZT.col16.empty()) { if (Status st = upload(c, c->zt_c16, P.ZT.col16); !st) return st; }
+            if (!P.Z.col16.empty()) { if (Status st = upload(c, c->z_c16, P.Z.col16); !st) return st; }
         }
     }
     // The eight per-iteration vectors live in one block, in the order of their passes per
