@@ -65,12 +65,13 @@ struct ZeroArr {
 
 // Faces of (i,j): E, W, N, S with existence and coupling.
 inline void faces(int32_t ni, int32_t nj, int32_t periodic, const double* cE, const double* cN,
-                  int32_t i, int32_t j, bool ex[4], int64_t nb[4], double c[4]) {
+                  int32_t i, int32_t j, bool ex[4], int32_t in[4], int32_t jn[4], double c[4]) {
     const int64_t row = (int64_t)j * ni;
-    ex[0] = (i + 1 < ni) || periodic;  nb[0] = row + (i + 1) % ni;      c[0] = ex[0] ? cE[row + i] : 0.0;
-    ex[1] = (i >= 1) || periodic;      nb[1] = row + (i - 1 + ni) % ni; c[1] = ex[1] ? cE[row + (i - 1 + ni) % ni] : 0.0;
-    ex[2] = (j + 1 < nj);              nb[2] = row + ni + i;            c[2] = ex[2] ? cN[row + i] : 0.0;
-    ex[3] = (j >= 1);                  nb[3] = row - ni + i;            c[3] = ex[3] ? cN[row - ni + i] : 0.0;
+    const int32_t ie = i + 1 == ni ? 0 : i + 1, iw = i == 0 ? ni - 1 : i - 1;     // E-W wrap
+    ex[0] = (i + 1 < ni) || periodic;  in[0] = ie; jn[0] = j;     c[0] = ex[0] ? cE[row + i] : 0.0;
+    ex[1] = (i >= 1) || periodic;      in[1] = iw; jn[1] = j;     c[1] = ex[1] ? cE[row + iw] : 0.0;
+    ex[2] = (j + 1 < nj);              in[2] = i;  jn[2] = j + 1; c[2] = ex[2] ? cN[row + i] : 0.0;
+    ex[3] = (j >= 1);                  in[3] = i;  jn[3] = j - 1; c[3] = ex[3] ? cN[row - ni + i] : 0.0;
 }
 
 }  // namespace
@@ -152,53 +153,56 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
     M.rp.resize((size_t)n + 1);
     M.diag.resize(n);
     bigvec<double> sc(n);
+    bigvec<int32_t> gi(n), gj(n);                   // grid column / row of each unknown
+    pfor((int64_t)nr * 256, [&](int64_t a0, int64_t a1) {
+        for (int64_t r = (a0 + 255) / 256; r < (a1 + 255) / 256; ++r)
+            for (int32_t i = 0; i < ni; ++i) {
+                const int32_t p = loc[(size_t)r * ni + i];
+                if (p >= 0) { gi[(size_t)p] = i; gj[(size_t)p] = r0 + (int32_t)r; }
+            }
+    });
     // diagonal A_pp = ((c_E + c_W) + c_N) + c_S (+ sigma) over all faces, then s = 1/sqrt(A_pp)
     pfor(n, [&](int64_t lo, int64_t hi) {
         for (int64_t p = lo; p < hi; ++p) {
-            int64_t g = M.grid[p];
-            int32_t i = (int32_t)(g % ni), j = (int32_t)(g / ni);
-            bool ex[4]; int64_t nb[4]; double c[4];
-            faces(ni, nj, periodic, cE, cN, i, j, ex, nb, c);
+            const int64_t g = M.grid[p];
+            const int32_t i = gi[(size_t)p], j = gj[(size_t)p];
+            bool ex[4]; int32_t in[4], jn[4]; double c[4];
+            faces(ni, nj, periodic, cE, cN, i, j, ex, in, jn, c);
             double d = ((c[0] + c[1]) + c[2]) + c[3];
             if (sigma) d = d + sigma[g];
             M.diag[p] = d;
             sc[p] = 1.0 / std::sqrt(d);
         }
     });
-    // CSR of A^ restricted to the block: a^_pq = A_pq * (s_p * s_q); rows built in parallel into
-    // 5 fixed slots per row, then compacted
-    bigvec<int32_t> c5((size_t)5 * n);
-    bigvec<double> a5((size_t)5 * n);
-    bigvec<uint8_t> m5(n);
-    pfor(n, [&](int64_t lo, int64_t hi) {
-        for (int64_t p = lo; p < hi; ++p) {
-            int64_t g = M.grid[p];
-            int32_t i = (int32_t)(g % ni), j = (int32_t)(g / ni);
-            bool ex[4]; int64_t nb[4]; double c[4];
-            faces(ni, nj, periodic, cE, cN, i, j, ex, nb, c);
-            int32_t* cols = &c5[(size_t)5 * p];
-            double* vals = &a5[(size_t)5 * p];
-            int m = 0;
-            cols[m] = (int32_t)p; vals[m] = M.diag[p] * (sc[p] * sc[p]); ++m;
-            for (int f = 0; f < 4; ++f) {
-                if (!ex[f] || !(c[f] > 0.0) || !mask[nb[f]]) continue;
-                int32_t jn = (int32_t)(nb[f] / ni);
-                if (jn < r0 || jn >= r1) continue;          // outside the block's index set
-                int32_t q = loc[(size_t)(jn - r0) * ni + (int32_t)(nb[f] % ni)];
-                cols[m] = q; vals[m] = (-c[f]) * (sc[p] * sc[q]); ++m;
+    // CSR of A^ restricted to the block: a^_pq = A_pq * (s_p * s_q); row lengths, prefix sum, then
+    // every row written in place (at most 5 entries, sorted by column)
+    auto row_of = [&](int64_t p, int32_t* cols, double* vals) {
+        const int32_t i = gi[(size_t)p], j = gj[(size_t)p];
+        bool ex[4]; int32_t in[4], jn[4]; double c[4];
+        faces(ni, nj, periodic, cE, cN, i, j, ex, in, jn, c);
+        int m = 0;
+        if (cols) { cols[m] = (int32_t)p; vals[m] = M.diag[p] * (sc[p] * sc[p]); }
+        ++m;
+        for (int f = 0; f < 4; ++f) {
+            if (!ex[f] || !(c[f] > 0.0) || !mask[(int64_t)jn[f] * ni + in[f]]) continue;
+            if (jn[f] < r0 || jn[f] >= r1) continue;    // outside the block's index set
+            if (cols) {
+                const int32_t q = loc[(size_t)(jn[f] - r0) * ni + in[f]];
+                cols[m] = q; vals[m] = (-c[f]) * (sc[p] * sc[q]);
             }
+            ++m;
+        }
+        if (cols)
             for (int x = 1; x < m; ++x)
                 for (int y = x; y > 0 && cols[y - 1] > cols[y]; --y) { std::swap(cols[y], cols[y - 1]); std::swap(vals[y], vals[y - 1]); }
-            m5[p] = (uint8_t)m;
-        }
-    });
-    stage("diag + 5 slots");
-    prefix(n, [&](int64_t p) { return (int64_t)m5[p]; }, M.rp.data());
+        return m;
+    };
+    prefix(n, [&](int64_t p) { return (int64_t)row_of(p, nullptr, nullptr); }, M.rp.data());
+    stage("row lengths");
     M.ci.resize(M.rp[n]);
     M.a.resize(M.rp[n]);
     pfor(n, [&](int64_t lo, int64_t hi) {
-        for (int64_t p = lo; p < hi; ++p)
-            for (int x = 0; x < m5[p]; ++x) { M.ci[M.rp[p] + x] = c5[(size_t)5 * p + x]; M.a[M.rp[p] + x] = a5[(size_t)5 * p + x]; }
+        for (int64_t p = lo; p < hi; ++p) row_of(p, &M.ci[M.rp[p]], &M.a[M.rp[p]]);
     });
 
     stage("CSR");
@@ -360,7 +364,7 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
             done[j].store(1, std::memory_order_release);
         }
     };
-    stage("numbering + scaled CSR");
+    stage("column lists");
     {
         std::vector<std::thread> pool;
         for (int t = 1; t < T; ++t) pool.emplace_back(worker, t);

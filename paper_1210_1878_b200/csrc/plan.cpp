@@ -562,6 +562,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
                 (P.precond != PCG_PRECOND_FSAI && c->mask[g2]) ? 1.0 / std::sqrt(diag_of(g2)) : 1.0;
     });
     auto scale_of = [&](int64_t gr) { return sgrid[(size_t)(gr - (int64_t)rlo * ni)]; };
+    stage("  numbering + scales");
     int64_t ntot = 0, ncols = 0;
     for (auto& b : blocks) { ntot += b.colptr.back(); ncols += (int64_t)b.col_g.size(); }
     // flat column index over the blocks, entry offsets by prefix sum, then a parallel fill
@@ -581,6 +582,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
         const int32_t q = colsrc[(size_t)k].second;
         return b.colptr[q + 1] - b.colptr[q];
     });
+    stage("  column offsets");
     if (exp) { P.zrow.resize((size_t)ntot); P.zhat.resize((size_t)ntot); }
     ent_z.resize((size_t)ntot); ent_row_arr.resize((size_t)ntot);
     P.pivots.resize((size_t)ncols); P.scale.resize((size_t)ncols); colarr.resize((size_t)ncols);
