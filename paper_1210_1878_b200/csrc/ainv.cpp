@@ -254,10 +254,12 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
     std::vector<std::vector<std::unique_ptr<int32_t[]>>> seg_r((size_t)T);
     std::vector<std::vector<std::unique_ptr<double[]>>> seg_v((size_t)T);
     auto worker = [&](int t) {
-        ZeroArr<double> w((size_t)n);
-        ZeroArr<uint8_t> live((size_t)n);     // entry present in the current column
-        ZeroArr<int32_t> listed((size_t)n);   // stamp j + 1: k recorded in `members` for column j
-        ZeroArr<int32_t> queued((size_t)n);   // stamp j + 1: k queued as a candidate for column j
+        // per unknown k, one 16-byte slot: the working value w, the stamp of the last column that
+        // listed k (bit 31: k is live -- present -- in the current column; a live k is always
+        // listed by it), the stamp of the last column that queued k as a candidate
+        struct Slot { double w; uint32_t lst; int32_t queued; };
+        ZeroArr<Slot> sl((size_t)n);
+        constexpr uint32_t kLive = 0x80000000u;
         std::vector<int32_t> members, touched;
         std::priority_queue<int32_t, std::vector<int32_t>, std::greater<int32_t>> cand;
         // column storage in fixed segments (a column's entries never move once published; the
@@ -276,10 +278,10 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
             if (j >= limit.load(std::memory_order_relaxed)) return;
             members.clear();
             const int32_t stamp = j + 1;
-            members.push_back(j); listed[j] = stamp; live[j] = 1; w[j] = 1.0;
+            members.push_back(j); sl[j].lst = (uint32_t)stamp | kLive; sl[j].w = 1.0;
             for (int32_t e = M.rp[j]; e < M.rp[j + 1]; ++e) {
                 int32_t i = M.ci[e];
-                if (i < j && queued[i] != stamp) { queued[i] = stamp; cand.push(i); }
+                if (i < j && sl[i].queued != stamp) { sl[i].queued = stamp; cand.push(i); }
             }
             bool ok = true;
             while (!cand.empty()) {
@@ -288,7 +290,7 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
                 double pi = 0.0;
                 for (int32_t e = M.rp[i]; e < M.rp[i + 1]; ++e) {
                     int32_t k = M.ci[e];
-                    if (live[k]) pi = pi + M.a[e] * w[k];
+                    if (sl[k].lst == ((uint32_t)stamp | kLive)) pi = pi + M.a[e] * sl[k].w;
                 }
                 if (pi == 0.0) continue;
                 if (!wait_for(i, j)) { ok = false; break; }
@@ -297,47 +299,47 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
                 const ColRef zi = cref[i];
                 for (int32_t q = 0; q < zi.len; ++q) {
                     const int32_t k = zi.r[q];
-                    if (!live[k]) {
-                        live[k] = 1; w[k] = 0.0;
-                        if (listed[k] != stamp) { listed[k] = stamp; members.push_back(k); }
+                    if (sl[k].lst != ((uint32_t)stamp | kLive)) {
+                        if (sl[k].lst != (uint32_t)stamp) members.push_back(k);
+                        sl[k].lst = (uint32_t)stamp | kLive; sl[k].w = 0.0;
                         for (int32_t e2 = M.rp[k]; e2 < M.rp[k + 1]; ++e2) {
                             int32_t i2 = M.ci[e2];
-                            if (i2 > i && i2 < j && queued[i2] != stamp) { queued[i2] = stamp; cand.push(i2); }
+                            if (i2 > i && i2 < j && sl[i2].queued != stamp) { sl[i2].queued = stamp; cand.push(i2); }
                         }
                     }
-                    w[k] = w[k] - coef * zi.v[q];
+                    sl[k].w = sl[k].w - coef * zi.v[q];
                     touched.push_back(k);
                 }
                 for (int32_t k : touched)
-                    if (k != j && std::fabs(w[k]) < tau) { live[k] = 0; w[k] = 0.0; }
+                    if (k != j && std::fabs(sl[k].w) < tau) { sl[k].lst = (uint32_t)stamp; sl[k].w = 0.0; }
                 if (fill > 0) {
                     // P_B2 (reading R26): keep the diagonal and the fill-1 largest |z|, ties to the
                     // smaller index
                     touched.clear();
                     for (int32_t k : members)
-                        if (k != j && live[k]) touched.push_back(k);
+                        if (k != j && sl[k].lst == ((uint32_t)stamp | kLive)) touched.push_back(k);
                     if ((int64_t)touched.size() > (int64_t)fill - 1) {
                         std::sort(touched.begin(), touched.end(), [&](int32_t a, int32_t b) {
-                            const double fa = std::fabs(w[a]), fb = std::fabs(w[b]);
+                            const double fa = std::fabs(sl[a].w), fb = std::fabs(sl[b].w);
                             return fa > fb || (fa == fb && a < b);
                         });
-                        for (size_t x = (size_t)fill - 1; x < touched.size(); ++x) { live[touched[x]] = 0; w[touched[x]] = 0.0; }
+                        for (size_t x = (size_t)fill - 1; x < touched.size(); ++x) { sl[touched[x]].lst = (uint32_t)stamp; sl[touched[x]].w = 0.0; }
                     }
                 }
             }
             if (!ok) {                                    // abandoned: a smaller column failed
                 while (!cand.empty()) cand.pop();
-                for (int32_t k : members) { live[k] = 0; w[k] = 0.0; }
+                for (int32_t k : members) { sl[k].lst = (uint32_t)stamp; sl[k].w = 0.0; }
                 return;
             }
             double pj = 0.0;
             for (int32_t e = M.rp[j]; e < M.rp[j + 1]; ++e) {
                 int32_t k = M.ci[e];
-                if (live[k]) pj = pj + M.a[e] * w[k];
+                if (sl[k].lst == ((uint32_t)stamp | kLive)) pj = pj + M.a[e] * sl[k].w;
             }
             std::sort(members.begin(), members.end());
             int32_t len = 0;
-            for (int32_t k : members) len += live[k];
+            for (int32_t k : members) len += sl[k].lst == ((uint32_t)stamp | kLive);
             if (seg_used + (size_t)len > seg_cap) {
                 seg_cap = std::max<size_t>((size_t)len, 1 << 16);
                 segr.emplace_back(new int32_t[seg_cap]);
@@ -348,8 +350,8 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
             double* vv = segv.back().get() + seg_used;
             int32_t q = 0;
             for (int32_t k : members) {
-                if (live[k]) { rr[q] = k; vv[q] = w[k]; ++q; }
-                live[k] = 0; w[k] = 0.0;
+                if (sl[k].lst == ((uint32_t)stamp | kLive)) { rr[q] = k; vv[q] = sl[k].w; ++q; }
+                sl[k].lst = (uint32_t)stamp; sl[k].w = 0.0;
             }
             seg_used += (size_t)len;
             cref[j] = ColRef{rr, vv, len};
