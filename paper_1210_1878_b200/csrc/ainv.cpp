@@ -37,8 +37,11 @@ namespace {
 
 struct BlockMatrix {
     int32_t n = 0;
-    bigvec<int32_t> rp, ci;           // CSR of the scaled matrix A^, columns ascending
-    bigvec<double> a;
+    // the scaled matrix A^ as 5 fixed slots per row (value and column side by side, columns
+    // ascending): row p = e5[5p .. 5p + m5[p])
+    struct Ent { double a; int32_t c; int32_t pad; };
+    bigvec<Ent> e5;
+    bigvec<uint8_t> m5;
     bigvec<int64_t> grid;             // local unknown -> grid index
     bigvec<double> diag;              // A_pp
 };
@@ -150,7 +153,6 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
         }
     });
     stage("numbering");
-    M.rp.resize((size_t)n + 1);
     M.diag.resize(n);
     bigvec<double> sc(n);
     bigvec<int32_t> gi(n), gj(n);                   // grid column / row of each unknown
@@ -174,38 +176,32 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
             sc[p] = 1.0 / std::sqrt(d);
         }
     });
-    // CSR of A^ restricted to the block: a^_pq = A_pq * (s_p * s_q); row lengths, prefix sum, then
-    // every row written in place (at most 5 entries, sorted by column)
-    auto row_of = [&](int64_t p, int32_t* cols, double* vals) {
+    // A^ restricted to the block: a^_pq = A_pq * (s_p * s_q), every row in its 5 slots (sorted by
+    // column)
+    M.e5.resize((size_t)5 * n);
+    M.m5.resize((size_t)n);
+    auto row_of = [&](int64_t p, BlockMatrix::Ent* r) {
         const int32_t i = gi[(size_t)p], j = gj[(size_t)p];
         bool ex[4]; int32_t in[4], jn[4]; double c[4];
         faces(ni, nj, periodic, cE, cN, i, j, ex, in, jn, c);
         int m = 0;
-        if (cols) { cols[m] = (int32_t)p; vals[m] = M.diag[p] * (sc[p] * sc[p]); }
+        r[m].c = (int32_t)p; r[m].a = M.diag[p] * (sc[p] * sc[p]); r[m].pad = 0;
         ++m;
         for (int f = 0; f < 4; ++f) {
             if (!ex[f] || !(c[f] > 0.0) || !mask[(int64_t)jn[f] * ni + in[f]]) continue;
             if (jn[f] < r0 || jn[f] >= r1) continue;    // outside the block's index set
-            if (cols) {
-                const int32_t q = loc[(size_t)(jn[f] - r0) * ni + in[f]];
-                cols[m] = q; vals[m] = (-c[f]) * (sc[p] * sc[q]);
-            }
+            const int32_t q = loc[(size_t)(jn[f] - r0) * ni + in[f]];
+            r[m].c = q; r[m].a = (-c[f]) * (sc[p] * sc[q]); r[m].pad = 0;
             ++m;
         }
-        if (cols)
-            for (int x = 1; x < m; ++x)
-                for (int y = x; y > 0 && cols[y - 1] > cols[y]; --y) { std::swap(cols[y], cols[y - 1]); std::swap(vals[y], vals[y - 1]); }
+        for (int x = 1; x < m; ++x)
+            for (int y = x; y > 0 && r[y - 1].c > r[y].c; --y) std::swap(r[y], r[y - 1]);
         return m;
     };
-    prefix(n, [&](int64_t p) { return (int64_t)row_of(p, nullptr, nullptr); }, M.rp.data());
-    stage("row lengths");
-    M.ci.resize(M.rp[n]);
-    M.a.resize(M.rp[n]);
     pfor(n, [&](int64_t lo, int64_t hi) {
-        for (int64_t p = lo; p < hi; ++p) row_of(p, &M.ci[M.rp[p]], &M.a[M.rp[p]]);
+        for (int64_t p = lo; p < hi; ++p) M.m5[(size_t)p] = (uint8_t)row_of(p, &M.e5[(size_t)5 * p]);
     });
-
-    stage("CSR");
+    stage("scaled matrix");
     // Zhat columns and pivots.  Column j needs the finished columns i < j it meets as
     // candidates (pivot p_i, entries of zhat_i), nothing else, so the columns can be built by
     // several threads at once with bitwise the sequential result (every column runs the same
@@ -279,8 +275,8 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
             members.clear();
             const int32_t stamp = j + 1;
             members.push_back(j); sl[j].lst = (uint32_t)stamp | kLive; sl[j].w = 1.0;
-            for (int32_t e = M.rp[j]; e < M.rp[j + 1]; ++e) {
-                int32_t i = M.ci[e];
+            for (const BlockMatrix::Ent* e = &M.e5[(size_t)5 * j], *ee = e + M.m5[(size_t)j]; e < ee; ++e) {
+                const int32_t i = e->c;
                 if (i < j && sl[i].queued != stamp) { sl[i].queued = stamp; cand.push(i); }
             }
             bool ok = true;
@@ -288,9 +284,9 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
                 const int32_t i = cand.top(); cand.pop();
                 // pi = a^_i . z over row i of A^ (ascending columns, present entries)
                 double pi = 0.0;
-                for (int32_t e = M.rp[i]; e < M.rp[i + 1]; ++e) {
-                    int32_t k = M.ci[e];
-                    if (sl[k].lst == ((uint32_t)stamp | kLive)) pi = pi + M.a[e] * sl[k].w;
+                for (const BlockMatrix::Ent* e = &M.e5[(size_t)5 * i], *ee = e + M.m5[(size_t)i]; e < ee; ++e) {
+                    const int32_t k = e->c;
+                    if (sl[k].lst == ((uint32_t)stamp | kLive)) pi = pi + e->a * sl[k].w;
                 }
                 if (pi == 0.0) continue;
                 if (!wait_for(i, j)) { ok = false; break; }
@@ -302,8 +298,8 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
                     if (sl[k].lst != ((uint32_t)stamp | kLive)) {
                         if (sl[k].lst != (uint32_t)stamp) members.push_back(k);
                         sl[k].lst = (uint32_t)stamp | kLive; sl[k].w = 0.0;
-                        for (int32_t e2 = M.rp[k]; e2 < M.rp[k + 1]; ++e2) {
-                            int32_t i2 = M.ci[e2];
+                        for (const BlockMatrix::Ent* e2 = &M.e5[(size_t)5 * k], *ee2 = e2 + M.m5[(size_t)k]; e2 < ee2; ++e2) {
+                            const int32_t i2 = e2->c;
                             if (i2 > i && i2 < j && sl[i2].queued != stamp) { sl[i2].queued = stamp; cand.push(i2); }
                         }
                     }
@@ -333,9 +329,9 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
                 return;
             }
             double pj = 0.0;
-            for (int32_t e = M.rp[j]; e < M.rp[j + 1]; ++e) {
-                int32_t k = M.ci[e];
-                if (sl[k].lst == ((uint32_t)stamp | kLive)) pj = pj + M.a[e] * sl[k].w;
+            for (const BlockMatrix::Ent* e = &M.e5[(size_t)5 * j], *ee = e + M.m5[(size_t)j]; e < ee; ++e) {
+                const int32_t k = e->c;
+                if (sl[k].lst == ((uint32_t)stamp | kLive)) pj = pj + e->a * sl[k].w;
             }
             std::sort(members.begin(), members.end());
             int32_t len = 0;
