@@ -195,6 +195,7 @@ void ell_shape(Ell& E, int64_t nel, int64_t hoff, int T, F len) {
     E.n = nel;
     E.val.resize((size_t)kEll * nel);
     E.col.resize((size_t)kEll * nel);
+    E.col16.resize((size_t)kEll * nel);
     const int64_t nsl = nel / kSlice;
     pscan(T, nsl, E.ovf.off, [&](int64_t s) {
         int64_t L = 0;
@@ -209,6 +210,7 @@ void ell_shape(Ell& E, int64_t nel, int64_t hoff, int T, F len) {
                 for (int m = 0; m < kEll; ++m) {
                     E.col[(size_t)e * kEll + m] = (int32_t)(e + hoff);
                     E.val[(size_t)e * kEll + m] = 0.0;
+                    E.col16[(size_t)e * kEll + m] = 0;
                 }
             for (int64_t o = E.ovf.off[s]; o < E.ovf.off[s + 1]; ++o) {
                 E.ovf.col[(size_t)o] = (int32_t)(s * kSlice + (o - E.ovf.off[s]) % kSlice + hoff);
@@ -217,24 +219,15 @@ void ell_shape(Ell& E, int64_t nel, int64_t hoff, int T, F len) {
         }
     });
 }
-// int16 slot offsets relative to the element's own array index (the device form of the ELL
-// columns); left empty when one does not fit
-void ell_col16(Ell& E, int64_t hoff, int T) {
-    E.col16.resize(E.col.size());
-    std::atomic<bool> fits(true);
-    pfor(T, (int64_t)E.col.size(), [&](int64_t a, int64_t b) {
-        for (int64_t m = a; m < b; ++m) {
-            const int64_t off = (int64_t)E.col[(size_t)m] - (m / kEll + hoff);
-            if (off < -32768 || off > 32767) { fits = false; return; }
-            E.col16[(size_t)m] = (int16_t)off;
-        }
-    });
-    if (!fits) { E.col16.clear(); E.col16.shrink_to_fit(); }
-}
-inline void ell_put(Ell& E, int64_t e, int64_t k, int32_t col, double val) {
+// (col16: the ELL slot's column as an int16 offset from the element's own array index -- the
+// device form; when one does not fit, c16_fits is cleared and the int32 columns are used)
+inline void ell_put(Ell& E, int64_t e, int64_t k, int32_t col, double val, int64_t hoff, std::atomic<bool>& c16_fits) {
     if (k < kEll) {
         E.col[(size_t)(e * kEll + k)] = col;
         E.val[(size_t)(e * kEll + k)] = val;
+        const int64_t off = (int64_t)col - (e + hoff);
+        if (off < -32768 || off > 32767) c16_fits.store(false, std::memory_order_relaxed);
+        else E.col16[(size_t)(e * kEll + k)] = (int16_t)off;
     } else {
         const int64_t s = e / kSlice, o = E.ovf.off[(size_t)s] + (k - kEll) * kSlice + (e - s * kSlice);
         E.ovf.col[(size_t)o] = col;
@@ -621,6 +614,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     stage("export + Z values");
     // ---- SELL of Z^T rows: row (column j of Z) = entries k ascending
     const int64_t nown = P.owned_elements();
+    std::atomic<bool> fits_zt(true), fits_z(true);
     {
         bigvec<int64_t> colq((size_t)nown);                 // element -> owned column (-1: none)
         pfor(nthr, nown, [&](int64_t a, int64_t b) { for (int64_t e = a; e < b; ++e) colq[(size_t)e] = -1; });
@@ -636,7 +630,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             for (int64_t q = q0; q < q1; ++q) {
                 const int64_t e = colarr[(size_t)q] - hoff, z0 = P.zcolptr[(size_t)q];
                 for (int64_t k = 0; k < P.zcolptr[(size_t)q + 1] - z0; ++k)
-                    ell_put(P.ZT, e, k, ent_row_arr[(size_t)(z0 + k)], ent_z[(size_t)(z0 + k)]);
+                    ell_put(P.ZT, e, k, ent_row_arr[(size_t)(z0 + k)], ent_z[(size_t)(z0 + k)], hoff, fits_zt);
             }
         });
     }
@@ -656,34 +650,23 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
                 }
         for (int64_t r : nrow_arr)
             if (r < hoff) return Status::err(PCG_ERR_ARG, "internal: northern Z entry below the owned rows");
-        bigvec<int64_t> cnt((size_t)nown);
-        pfor(nthr, nown, [&](int64_t a, int64_t b) { for (int64_t e = a; e < b; ++e) cnt[(size_t)e] = 0; });
-        pfor(nthr, (int64_t)ent_row_arr.size(), [&](int64_t a, int64_t b) {
-            for (int64_t e = a; e < b; ++e) {
-                const int64_t r = ent_row_arr[(size_t)e];
-                if (r >= hoff) __atomic_fetch_add(&cnt[(size_t)(r - hoff)], (int64_t)1, __ATOMIC_RELAXED);
-            }
-        });
-        for (int64_t r : nrow_arr) cnt[(size_t)(r - hoff)]++;
-        ell_shape(P.Z, nown, hoff, nthr, [&](int64_t e) { return cnt[(size_t)e]; });
-        bigvec<int64_t> fill((size_t)nown);                     // entries placed per row so far
-        pfor(nthr, nown, [&](int64_t a, int64_t b) { for (int64_t e = a; e < b; ++e) fill[(size_t)e] = 0; });
         // transpose with the ascending column order per row kept: thread t owns the rows
         // [R_t, R_t+1) and visits, in ascending order, the columns that can hold entries of them
-        // (a column's entries are at rows <= the column, so columns from the first row >= R_t on)
-        {
-            const int64_t nc = (int64_t)colarr.size();
-            std::atomic<int64_t> reach_a(0);               // largest column - row distance of an entry
-            pfor(nthr, nc, [&](int64_t a, int64_t b) {
-                int64_t r = 0;
-                for (int64_t q = a; q < b; ++q)
-                    for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e) r = std::max(r, colarr[q] - ent_row_arr[e]);
-                int64_t cur = reach_a.load();
-                while (r > cur && !reach_a.compare_exchange_weak(cur, r)) {
-                }
-            });
-            const int64_t reach = reach_a.load();
-            int T = (nc < 100000) ? 1 : nthr;
+        // (a column's entries are at rows <= the column, so columns from the first row >= R_t on,
+        // until past Z's reach); one such walk counts the rows' entries, the second places them
+        const int64_t nc = (int64_t)colarr.size();
+        std::atomic<int64_t> reach_a(0);                   // largest column - row distance of an entry
+        pfor(nthr, nc, [&](int64_t a, int64_t b) {
+            int64_t r = 0;
+            for (int64_t q = a; q < b; ++q)
+                for (int64_t e = P.zcolptr[q]; e < P.zcolptr[q + 1]; ++e) r = std::max(r, colarr[q] - ent_row_arr[e]);
+            int64_t cur = reach_a.load();
+            while (r > cur && !reach_a.compare_exchange_weak(cur, r)) {
+            }
+        });
+        const int64_t reach = reach_a.load();
+        const int T = (nc < 100000) ? 1 : nthr;
+        auto walk = [&](auto&& visit) {                    // visit(row, column q, entry e) in order
             std::vector<std::thread> pool;
             auto part = [&](int t) {
                 const int64_t R0 = nown * t / T, R1 = nown * (t + 1) / T;
@@ -695,7 +678,7 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
                         const int64_t r = ent_row_arr[e] - hoff;
                         if (r < R1) below = true;
                         if (r < R0 || r >= R1) continue;
-                        ell_put(P.Z, r, fill[(size_t)r]++, (int32_t)colarr[q], ent_z[e]);
+                        visit(r, q, e);
                     }
                     if (!below && colarr[q] - hoff >= R1 + reach) break;   // past Z's reach
                 }
@@ -703,14 +686,24 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
             for (int t = 1; t < T; ++t) pool.emplace_back(part, t);
             part(0);
             for (auto& th : pool) th.join();
-        }
+        };
+        bigvec<int64_t> cnt((size_t)nown);                      // entries per row, then placed so far
+        pfor(nthr, nown, [&](int64_t a, int64_t b) { for (int64_t e = a; e < b; ++e) cnt[(size_t)e] = 0; });
+        walk([&](int64_t r, int64_t, int64_t) { cnt[(size_t)r]++; });
+        for (int64_t r : nrow_arr) cnt[(size_t)(r - hoff)]++;
+        ell_shape(P.Z, nown, hoff, nthr, [&](int64_t e) { return cnt[(size_t)e]; });
+        bigvec<int64_t>& fill = cnt;
+        pfor(nthr, nown, [&](int64_t a, int64_t b) { for (int64_t e = a; e < b; ++e) fill[(size_t)e] = 0; });
+        walk([&](int64_t r, int64_t q, int64_t e) {
+            ell_put(P.Z, r, fill[(size_t)r]++, (int32_t)colarr[q], ent_z[e], hoff, fits_z);
+        });
         for (size_t m = 0; m < nrow_arr.size(); ++m) {     // north columns, ascending
             const int64_t r = nrow_arr[m] - hoff;
-            ell_put(P.Z, r, fill[(size_t)r]++, (int32_t)ncol_arr[m], nz[m]);
+            ell_put(P.Z, r, fill[(size_t)r]++, (int32_t)ncol_arr[m], nz[m], hoff, fits_z);
         }
     }
-    ell_col16(P.ZT, hoff, nthr);
-    ell_col16(P.Z, hoff, nthr);
+    for (auto [E, f] : {std::pair<Ell*, bool>{&P.ZT, fits_zt.load()}, {&P.Z, fits_z.load()}})
+        if (!f) { E->col16.clear(); E->col16.shrink_to_fit(); }
     stage("pack Z");
     // ---- FSAI DIA form: each owned column's entries at consecutive columns of the
     // same grid row i-1, i-2, ... (no land, wrap or N-S link inside the chain) -> diagonals
