@@ -15,8 +15,9 @@
 //   --  grid barrier; every block forms the canonical (d, q) sum -> alpha               (reduce 1)
 //   2A  r_new = r - alpha q over [lo2, range end) -> smem; own: r_new -> global, (r, r)   l.7
 //   2B  t = Dhat^-1 Z^T r_new (ELL(4) slots + overflow) on own ocean points -> global t
-//   --  t-ready stamp of b; wait for the stamps of the blocks whose t this block's Z rows reach
-//   2C  t over [range start, hi2) -> smem
+//   --  t-ready stamp of b
+//   2C  own t -> smem; wait for the stamps of the blocks whose t this block's Z rows reach, then
+//       their t over [range end, hi2) -> smem
 //   2D  s = Z t (ELL(4) + overflow) on own ocean points -> global; (s, r_new) warp sums
 //   --  grid barrier; every block forms (r, r) and (s, r) -> beta, history, stop test    (reduce 2)
 // Jacobi / none: phase 2 is one pointwise pass (s = r_new / A_pp or r_new).
@@ -529,30 +530,36 @@ __global__ void __launch_bounds__(NT, 1) rs_loop_kernel(const KArgs A) {
                         if ((m[u] >> lane) & 1u) A.t[a] = __ddiv_rn(acc, pv[u]);
                     }
                 }
-                // publish this block's t, wait for the t of the blocks its Z rows reach
+                // publish this block's t; copy it to buf while the blocks its Z rows reach finish
+                // theirs, then wait for their stamps and copy their t
                 RS_TS(6);
                 const unsigned stamp = (unsigned)k + 1u;
                 if (tid == 0) {
                     __threadfence();
                     st_release_u32(rs_sync + 1 + b, stamp);
+                }
+                // 2C: t over [f0, hi2) -> buf (land chunks: 0); the own chunks [0, nOwn) first
+                const int nT = (hi2 - f0) >> 5, nOwn = (f1 - f0) >> 5;
+                auto copy_t = [&](int cbeg, int cend) {
+                    for (int c0 = cbeg + warp; c0 < cend; c0 += C::VU * NW) {
+                        double tv[C::VU];
+#pragma unroll
+                        for (int u = 0; u < C::VU; ++u) {
+                            const int c = c0 + u * NW;
+                            tv[u] = (c < cend && cm[cmF + c]) ? __ldcg(A.t + f0 + 32 * c + lane) : 0.0;
+                        }
+#pragma unroll
+                        for (int u = 0; u < C::VU; ++u) {
+                            const int c = c0 + u * NW;
+                            if (c < cend) buf[32 * c + lane] = tv[u];
+                        }
+                    }
+                };
+                copy_t(0, nOwn);
+                if (tid == 0)
                     for (int bb = b + 1; bb <= wait2; ++bb) rs_spin(rs_sync + 1 + bb, stamp, 1u + (unsigned)bb);
-                }
                 RS_TS(7);
-                // 2C: t over [f0, hi2) -> buf (land chunks: 0)
-                const int nT = (hi2 - f0) >> 5;
-                for (int c0 = warp; c0 < nT; c0 += C::VU * NW) {
-                    double tv[C::VU];
-#pragma unroll
-                    for (int u = 0; u < C::VU; ++u) {
-                        const int c = c0 + u * NW;
-                        tv[u] = (c < nT && cm[cmF + c]) ? __ldcg(A.t + f0 + 32 * c + lane) : 0.0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < C::VU; ++u) {
-                        const int c = c0 + u * NW;
-                        if (c < nT) buf[32 * c + lane] = tv[u];
-                    }
-                }
+                copy_t(nOwn, nT);
                 RS_TS(8);
                 // 2D: s = Z t on own ocean points, (s, r_new) warp sums, C::ZC chunks per warp in flight
                 const double* tb = buf - f0;
