@@ -713,8 +713,10 @@ Status setup_rs(pcg_ctx* c) {
     // (K1 ocean chunk 0.45 -> 0.3, measured round 2 with 768 threads: the land-heavy blocks get
     // fewer units, the widest phase-1 range -- which sizes every block's shared memory -- shrinks
     // from 93 to 75 units (227 -> 190 KB), the L1 left to each SM grows, and cfg4 AINV runs at
-    // 67.6 instead of 75.0 us per iteration; cfg2 / cfg3 unchanged)
-    double mk[5] = {0.3, 0.25, 0.85, 0.65, 0.43};
+    // 67.6 instead of 75.0 us per iteration; cfg2 / cfg3 unchanged).  K2/K3 shared per chunk
+    // 0.55 on the large grids since own t is staged during the t-ready wait (cfg4 66.97 -> 66.40
+    // us; cfg3 would lose 0.4 us with it, so the small grids keep 0.43)
+    double mk[5] = {0.3, 0.25, 0.85, 0.65, U >= 4096 ? 0.55 : 0.43};
     if (const char* e = getenv("PCG_RS_MODEL"))
         sscanf(e, "%lf,%lf,%lf,%lf,%lf", &mk[0], &mk[1], &mk[2], &mk[3], &mk[4]);
     const int64_t lim_dbl = (int64_t)((limit > 24576 ? limit - 24576 : 0) / 8);
