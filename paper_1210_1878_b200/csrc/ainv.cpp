@@ -243,9 +243,14 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
                     if (p >= 0) v.push_back(p);
                 }
         };
-        for (int t = 1; t < T; ++t) pool.emplace_back(list, t);
-        list(0);
+        std::atomic<bool> oom(false);
+        auto run = [&](int t) {
+            try { list(t); } catch (const std::bad_alloc&) { oom = true; }
+        };
+        for (int t = 1; t < T; ++t) pool.emplace_back(run, t);
+        run(0);
         for (auto& th : pool) th.join();
+        if (oom) throw std::bad_alloc();
     }
     std::vector<std::vector<std::unique_ptr<int32_t[]>>> seg_r((size_t)T);
     std::vector<std::vector<std::unique_ptr<double[]>>> seg_v((size_t)T);
@@ -364,10 +369,22 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
     };
     stage("column lists");
     {
+        // an allocation failure in a worker abandons every column (limit 0) and is rethrown here,
+        // in the calling thread (pcg_setup reports PCG_ERR_NOMEM), never out of a std::thread
+        std::atomic<bool> oom(false);
+        auto run = [&](int t) {
+            try {
+                worker(t);
+            } catch (const std::bad_alloc&) {
+                oom = true;
+                limit.store(0);
+            }
+        };
         std::vector<std::thread> pool;
-        for (int t = 1; t < T; ++t) pool.emplace_back(worker, t);
-        worker(0);
+        for (int t = 1; t < T; ++t) pool.emplace_back(run, t);
+        run(0);
         for (auto& th : pool) th.join();
+        if (oom) throw std::bad_alloc();
     }
     stage("column wavefront");
     const int64_t fail = limit.load() < n ? (int64_t)limit.load() : -1;
