@@ -450,7 +450,8 @@ VARIANTS = {"graph_driver": {"PCG_RS": "0"},
             "graph_k1_tma_no_redundant": {"PCG_RS": "0", "PCG_K1TMA": "1", "PCG_REDUNDANT": "0"},
             "graph_kfin": {"PCG_RS": "0", "PCG_KFIN": "1"},
             "graph_kfin_k1_tma": {"PCG_RS": "0", "PCG_KFIN": "1", "PCG_K1TMA": "1"},
-            "rs_768_threads": {"PCG_RS_THREADS": "768"}}
+            "rs_768_threads": {"PCG_RS_THREADS": "768"},
+            "graph_int32_columns": {"PCG_COL16": "0"}}                # no int16 offsets: graph, int32 ELL columns
 
 
 @pytest.mark.parametrize("variant", sorted(VARIANTS))
