@@ -1030,3 +1030,15 @@ def test_nos6_like_bitwise_canonical(precond):
     assert np.array_equal(host(xg), A.to_grid(ref.x))
     assert rep["converged"] == 1
     S.close()
+
+
+def test_wide_grid_int32_columns_bitwise_canonical():
+    """A grid so wide (pitch 17024) that Z's entries two rows south no longer fit the int16 slot
+    offsets (the largest ELL-slot offset here is 34049 array elements): setup falls
+    back to int32 ELL columns, and the solve is still bitwise the canonical oracle's."""
+    p = synth.random_grid(17000, 7, 21, land_frac=0.1)
+    A, S, ref, x, k, hist, rep, _ = _canonical_pair(p, "ainv", 1e-10)
+    assert k == ref.iterations
+    assert np.array_equal(hist, ref.hist)
+    assert np.array_equal(x, A.to_grid(ref.x))
+    S.close()
