@@ -540,7 +540,9 @@ __global__ void __launch_bounds__(NT, 1) rs_loop_kernel(const KArgs A) {
                 }
                 // 2C: t over [f0, hi2) -> buf (land chunks: 0); the own chunks [0, nOwn) first
                 const int nT = (hi2 - f0) >> 5, nOwn = (f1 - f0) >> 5;
-                auto copy_t = [&](int cbeg, int cend) {
+#pragma unroll 1
+                for (int pass = 0; pass < 2; ++pass) {              // own chunks, then the rest
+                    const int cbeg = pass ? nOwn : 0, cend = pass ? nT : nOwn;
                     for (int c0 = cbeg + warp; c0 < cend; c0 += C::VU * NW) {
                         double tv[C::VU];
 #pragma unroll
@@ -554,12 +556,12 @@ __global__ void __launch_bounds__(NT, 1) rs_loop_kernel(const KArgs A) {
                             if (c < cend) buf[32 * c + lane] = tv[u];
                         }
                     }
-                };
-                copy_t(0, nOwn);
-                if (tid == 0)
-                    for (int bb = b + 1; bb <= wait2; ++bb) rs_spin(rs_sync + 1 + bb, stamp, 1u + (unsigned)bb);
-                RS_TS(7);
-                copy_t(nOwn, nT);
+                    if (pass == 0) {
+                        if (tid == 0)
+                            for (int bb = b + 1; bb <= wait2; ++bb) rs_spin(rs_sync + 1 + bb, stamp, 1u + (unsigned)bb);
+                        RS_TS(7);
+                    }
+                }
                 RS_TS(8);
                 // 2D: s = Z t on own ocean points, (s, r_new) warp sums, C::ZC chunks per warp in flight
                 const double* tb = buf - f0;
