@@ -71,7 +71,7 @@ struct RsCfg<512, PC> {
 #define RS768_OVF 4
 #endif
 #ifndef RS768_NB
-#define RS768_NB 16
+#define RS768_NB 24
 #endif
 #ifndef RS768_NB2
 #define RS768_NB2 8
