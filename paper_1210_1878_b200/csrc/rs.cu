@@ -83,10 +83,10 @@ struct RsCfg<512, PC> {
 #define RS768D_K1C 2
 #endif
 #ifndef RS768D_NB
-#define RS768D_NB 12
+#define RS768D_NB 24
 #endif
 #ifndef RS768D_NB2
-#define RS768D_NB2 6
+#define RS768D_NB2 12
 #endif
 template <int PC>
 struct RsCfg<768, PC> {
