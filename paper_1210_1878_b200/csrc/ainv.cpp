@@ -213,10 +213,10 @@ void ainv_block(int32_t ni, int32_t nj, int32_t periodic, const double* cE, cons
     // Progress: a thread only waits for smaller columns, and the smallest unfinished column's
     // dependencies are all finished.  On an AINV failure (pivot <= 1e-12) columns beyond the
     // smallest failing one are abandoned, so the reported column is the sequential one.
-    struct ColRef {
-        const int32_t* r = nullptr;
-        const double* v = nullptr;
-        int32_t len = 0;
+    struct ColRef {                              // trivial: bigvec leaves it uninitialised
+        const int32_t* r;
+        const double* v;
+        int32_t len;
     };
     bigvec<ColRef> cref(n);                      // written before done[j], read after it
     bigvec<double> piv(n);
