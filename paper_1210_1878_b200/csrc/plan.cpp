@@ -559,7 +559,8 @@ Status build_plan(const pcg_coeffs* c, const pcg_grid* g, const pcg_opts* o, Pla
     int64_t ntot = 0, ncols = 0;
     for (auto& b : blocks) { ntot += b.colptr.back(); ncols += (int64_t)b.col_g.size(); }
     // flat column index over the blocks, entry offsets by prefix sum, then a parallel fill
-    bigvec<std::pair<int32_t, int32_t>> colsrc((size_t)ncols);      // (block, column in block)
+    struct ColSrc { int32_t first, second; };                        // trivial: no serial init
+    bigvec<ColSrc> colsrc((size_t)ncols);                            // (block, column in block)
     {
         int64_t k0 = 0;
         for (size_t bi = 0; bi < blocks.size(); ++bi) {
