@@ -50,7 +50,8 @@ namespace {
 // two rounds in flight), partial loads in flight per thread in the final sums (NB: (d, q); NB2:
 // per array for (r, r), (s, r)).  512 threads get 128 registers, 768 threads 80 (measured at
 // cfg4: 768 threads 75.7 vs 76.6 us per iteration for AINV(0.1), 34.2 vs 36.7 for Jacobi; at
-// cfg2 / cfg3 AINV 16.0 / 19.8 vs 14.9 / 17.9 -- setup_rs picks per problem).
+// cfg2 / cfg3 AINV 16.0 / 19.8 vs 14.9 / 17.9 -- setup_rs picks per problem).  NB = 24 puts a
+// cfg4-sized (d, q) sum (6126 partials, 24 per thread) in one round of loads.
 template <int NT, int PC>
 struct RsCfg;
 template <int PC>
